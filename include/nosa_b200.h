@@ -1,0 +1,225 @@
+/*
+ * nosa_b200.h — C ABI of the B200-native NOSA offloaded sparse-attention decode step.
+ *
+ * The reference (arXiv 2510.13602 testbench, /root/reference/pkg/src/nosa_sim) has no FFI:
+ * everything is in-process NumPy.  Each entry point below is the batched, device-resident
+ * replacement of one reference call site; the citation names the reference interface it
+ * stands behind (file:line under pkg/src/nosa_sim/).  A Python maintainer binds this header
+ * with ctypes; paper_2510_13602_b200/_lib.py is that binding.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Device pointers are CUDA device addresses; `stream`
+ *    arguments are cudaStream_t handles passed as void* (NULL = legacy default stream).
+ *  - Every call returns an int status (NOSA_OK or one NOSA_ERR_*); the message of the last
+ *    failure is nosa_last_error(ctx) (ctx may be NULL for creation failures).
+ *  - Single writer per context, one context per GPU.  All per-step calls are asynchronous
+ *    on the caller's stream; calls named nosa_read_* synchronise and copy to host memory.
+ *  - Errors raised inside kernels (CapacityExceeded, ...) are latched in a device flag word
+ *    and surfaced by nosa_check_errors() / the next synchronising call.
+ */
+#ifndef NOSA_B200_H
+#define NOSA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: the reference's exception types (kv_manager.py:31-56, config.py:38-65) ---- */
+#define NOSA_OK 0
+#define NOSA_ERR_VALUE 1         /* ValueError: shapes / config / argument range          */
+#define NOSA_ERR_CAPACITY 2      /* kv_manager.CapacityExceeded  (kv_manager.py:47-48)    */
+#define NOSA_ERR_UNKNOWN_KEY 3   /* kv_manager.UnknownKey        (kv_manager.py:43-44)    */
+#define NOSA_ERR_OUT_OF_BLOCKS 4 /* kv_manager.OutOfBlocks       (kv_manager.py:35-36)    */
+#define NOSA_ERR_CUDA 5          /* CUDA runtime failure (RuntimeError)                    */
+#define NOSA_ERR_STATE 6         /* call order misuse, e.g. step before prefill            */
+
+/* device error-flag bits (nosa_check_errors) */
+#define NOSA_FLAG_CAPACITY 1u
+#define NOSA_FLAG_EMPTY_SUPPORT 2u /* softmax over empty support (numerics.py:50-52)       */
+
+/* selectors (decode.py:28 SELECTORS) */
+#define NOSA_SELECTOR_NOSA 0     /* selection.nosa_select      (selection.py:130-160)     */
+#define NOSA_SELECTOR_INFLLMV2 1 /* selection.infllmv2_select  (selection.py:163-178)     */
+
+/* eviction-head variants (attention.py:26 VARIANTS; `retaining` needs hidden states and is
+ * out of scope on this path) */
+#define NOSA_VARIANT_ED_DMA 0 /* beta = s_e_c                (attention.py:160-161)       */
+#define NOSA_VARIANT_S_DMA 1  /* beta = 0                    (attention.py:164-165)       */
+#define NOSA_VARIANT_DMA 2    /* beta = log(mean exp-score)  (attention.py:162-164)       */
+
+#define NOSA_DTYPE_BF16 0
+#define NOSA_DTYPE_FP32 1
+
+#define NOSA_GATHER_UVA 0     /* zero-copy SM gather kernel over mapped pinned memory     */
+#define NOSA_GATHER_MEMCPY 1  /* copy-engine path: host-planned cudaMemcpyAsync per miss  */
+
+/* AttentionConfig (config.py:15-36) plus the engine extents of one GPU. */
+typedef struct NosaConfig {
+  int32_t n, d, n_head, n_kv_head, d_head, n_b, n_s, n_w, k, k_q, k_e;
+  int32_t accounting; /* 0 = "inclusive", 1 = "exclusive" (config.py:8-12)             */
+  int32_t batch;      /* sequences owned by this context                                */
+  int32_t layers;     /* attention layers (independent caches)                          */
+  int32_t max_tokens; /* per-sequence cache capacity in tokens (HeadState capacity)     */
+  int32_t fast_slots; /* HBM slots per (layer, sequence, kv head) = fast-tier num_blocks */
+  int32_t dtype;      /* NOSA_DTYPE_*: K/V/q storage type                               */
+  int32_t variant;    /* NOSA_VARIANT_*                                                 */
+} NosaConfig;
+
+/* ResidencyStats (kv_manager.py:101-122), summed over a (layer, sequence, head) range. */
+typedef struct NosaStats {
+  int64_t hits, misses, new_blocks, evictions, steps;
+  int64_t bytes_up, bytes_down; /* misses * bytes_per_block, evictions * bytes_per_block */
+} NosaStats;
+
+/* Per-step inputs/outputs of nosa_decode_step: one pointer per tensor, layer-major.
+ *   q     [layers][batch][n_head][d_head]     (dtype)
+ *   k_new [layers][batch][n_kv_head][d_head]  (dtype)
+ *   v_new [layers][batch][n_kv_head][d_head]  (dtype)
+ *   out   [layers][batch][n_head][d_head]     (float32)                                 */
+typedef struct NosaStepIO {
+  const void* q;
+  const void* k_new;
+  const void* v_new;
+  float* out;
+  int32_t selector;    /* NOSA_SELECTOR_* */
+  int32_t gather_mode; /* NOSA_GATHER_*   */
+} NosaStepIO;
+
+typedef struct NosaCtx NosaCtx;
+
+/* ---- configuration ---------------------------------------------------------------- */
+
+/* AttentionConfig.__post_init__ validation (config.py:38-65) plus engine-extent checks.
+ * Writes the ValueError text into msg. */
+int nosa_config_validate(const NosaConfig* cfg, char* msg, int msg_len);
+
+/* Derived budgets (config.py:72-94): blocks_q, blocks_e, blocks_topk. */
+int nosa_config_budgets(const NosaConfig* cfg, int32_t* blocks_q, int32_t* blocks_e,
+                        int32_t* blocks_topk);
+
+/* ---- context lifetime ------------------------------------------------------------- */
+
+/* Allocates the HBM slot pools (PhysicalLayout FAST, kv_manager.py:59-81), the block tables
+ * (TieredBlockManager.__init__, kv_manager.py:138-167) and the pinned, mapped host mirror
+ * (the SLOW tier).  Every logical block starts in the slow tier (offload_sim.py:262-266). */
+int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out);
+void nosa_ctx_destroy(NosaCtx* ctx);
+const char* nosa_last_error(const NosaCtx* ctx);
+/* bytes of device and pinned host memory held by the context */
+int nosa_ctx_memory(const NosaCtx* ctx, int64_t* device_bytes, int64_t* host_bytes);
+
+/* EvictionHead weights (attention.py:104-118): w1 (d_head x n_head) row-major, w2 (n_head),
+ * host float64.  Required before nosa_prefill for ed-dma / s-dma / dma. */
+int nosa_set_eviction_head(NosaCtx* ctx, const double* w1, const double* w2);
+
+/* ---- prefill / run start (DecodeEngine.prefill, start_run: decode.py:139-150) ------- */
+
+/* Caches t tokens for sequences [seq_begin, seq_begin+seq_count) of one layer and makes
+ * them slow-resident.  k, v: device [seq_count][n_kv_head][t][d_head] (dtype).  Computes the
+ * per-token importance scores (importance_scores, attention.py:121-146), the block means
+ * used for selection (compress_blocks, attention.py:42-59) and writes the host mirror.
+ * Resets the sequences' residency to all-slow.  Synchronous w.r.t. `stream` completion
+ * of its inputs only. */
+int nosa_prefill(NosaCtx* ctx, int layer, int seq_begin, int seq_count, const void* k,
+                 const void* v, int t, void* stream);
+
+/* BlockGeometry.for_run (selection.py:46-50) for every layer of the sequences: freezes
+ * recent_start at the current cache length and ranks the frozen pool by its query-agnostic
+ * score (the second phase of nosa_select, selection.py:151-156). */
+int nosa_start_run(NosaCtx* ctx, int seq_begin, int seq_count, void* stream);
+
+/* ---- the hot path, stage by stage (DecodeEngine.step decode.py:152-190 +
+ *      the residency loop of simulate_decode offload_sim.py:279-299) -------------------- */
+
+/* K1+K2 fused: GQA-summed scoring of the frozen pool (decode.py:171-172), top-k selection
+ * (nosa_select / infllmv2_select), required = fixed U topk (offload_sim.py:233-234), then
+ * plan_transfers + apply_transfers on the block tables (kv_manager.py:205-279).
+ * q: device [batch][n_head][d_head] (dtype).  Enqueues the layer's miss list. */
+int nosa_select_plan(NosaCtx* ctx, int layer, const void* q, int selector, void* stream);
+
+/* K1 only (no residency change): fills the selection buffers read by nosa_read_selection. */
+int nosa_select(NosaCtx* ctx, int layer, const void* q, int selector, void* stream);
+
+/* K2 only, with caller-provided required block sets (TieredBlockManager.plan_transfers +
+ * apply_transfers, kv_manager.py:205-279).  req: device int32 [batch][n_kv_head][fast_slots],
+ * n_req: device int32 [batch][n_kv_head]; each row sorted ascending, unique. */
+int nosa_cache_plan(NosaCtx* ctx, int layer, const int32_t* req, const int32_t* n_req,
+                    void* stream);
+
+/* K3: moves the layer's missed blocks from the host mirror into their HBM slots
+ * (the `mover` of apply_transfers, kv_manager.py:290, 300-305). */
+int nosa_gather(NosaCtx* ctx, int layer, int mode, void* stream);
+
+/* K4+K5: block-sparse biased attention over the required blocks (attend_biased over the
+ * token mask, attention.py:167-182, decode.py:179-185), then append of the new token with its
+ * importance score (decode.py:187-189).  out: device float32 [batch][n_head][d_head]. */
+int nosa_attend(NosaCtx* ctx, int layer, const void* q, const void* k_new, const void* v_new,
+                float* out, void* stream);
+
+/* All layers of one decode step, pipelined: select+plan on `stream`, gathers on the
+ * context's copy stream overlapped with scoring of the next layers, attention after each
+ * layer's gather.  Equivalent to per-layer nosa_select_plan, nosa_gather, nosa_attend. */
+int nosa_decode_step(NosaCtx* ctx, const NosaStepIO* io, void* stream);
+
+/* CUDA-graph form of nosa_decode_step for fixed io pointers: capture once, replay per step. */
+int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io);
+int nosa_step_graph_launch(NosaCtx* ctx, void* stream);
+
+/* ---- standalone selector (drop-in for nosa_select / infllmv2_select on given scores) --- */
+
+/* n_prob independent selections.  s_q, s_e: device float64 [n_prob][stride] block scores.
+ * pool_lo/pool_hi: device int32 [n_prob] (BlockGeometry.pool_blocks).  Outputs sorted
+ * ascending block ids: out_q [n_prob][m_q], out_e [n_prob][m_e], counts n_q/n_e [n_prob].
+ * selector NOSA_SELECTOR_INFLLMV2 ignores s_e and uses m_q as the total top-k budget. */
+int nosa_select_scores(int n_prob, const double* s_q, const double* s_e, int stride,
+                       const int32_t* pool_lo, const int32_t* pool_hi, int m_q, int m_e,
+                       int selector, int32_t* out_q, int32_t* n_q, int32_t* out_e,
+                       int32_t* n_e, void* stream);
+
+/* ---- readback / statistics (synchronising) ---------------------------------------- */
+
+/* Last selection of a layer, host buffers sized [batch][n_kv_head][cap]:
+ * blocks_q/e (sorted), required (sorted, = fixed U topk) and counts.
+ * s_q (optional, may be NULL): [batch][n_kv_head][max_blocks] float64 pool scores. */
+int nosa_read_selection(NosaCtx* ctx, int layer, int cap, int32_t* blocks_q, int32_t* n_q,
+                        int32_t* blocks_e, int32_t* n_e, int32_t* required, int32_t* n_req,
+                        double* s_q);
+
+/* Last TransferPlan of a layer (kv_manager.py:84-98), host [batch][n_kv_head][fast_slots]:
+ * fetch (block ids, plan order), evict (victims, LRR order), hit counts. */
+int nosa_read_plan(NosaCtx* ctx, int layer, int32_t* fetch, int32_t* n_fetch, int32_t* evict,
+                   int32_t* n_evict, int32_t* n_hit);
+
+/* Block table of one (layer, sequence, head): slot_of [max_blocks] (-1 = slow tier),
+ * block_of [fast_slots] (-1 = free).  TieredBlockManager.lookup / fast_resident. */
+int nosa_read_residency(NosaCtx* ctx, int layer, int seq, int head, int32_t* slot_of,
+                        int32_t* block_of);
+
+/* Selection scores of the frozen pool, host float64 [batch][n_kv_head][max_blocks]:
+ * s_e_c block means (compress_scores) as used by the selector. */
+int nosa_read_block_scores(NosaCtx* ctx, int layer, double* s_e_c);
+
+/* Cached K/V of one (layer, sequence, head), host [t][d_head] in dtype, from the host
+ * mirror (the slow tier always holds every block; HBM slots hold copies). */
+int nosa_read_kv(NosaCtx* ctx, int layer, int seq, int head, int t, void* k, void* v);
+/* Copy of one HBM slot, host [2][n_b][d_head] in dtype (un-swizzled). */
+int nosa_read_slot(NosaCtx* ctx, int layer, int seq, int head, int slot, void* kv);
+
+int nosa_read_stats(NosaCtx* ctx, int layer_begin, int layer_end, int seq_begin, int seq_end,
+                    NosaStats* out);
+int nosa_reset_stats(NosaCtx* ctx, void* stream);
+/* cache length per (layer, sequence) (HeadState.t, decode.py:70) */
+int nosa_read_lengths(NosaCtx* ctx, int32_t* t /* [layers][batch] */);
+/* synchronises; returns NOSA_ERR_CAPACITY etc. if a kernel latched an error, and clears it */
+int nosa_check_errors(NosaCtx* ctx, uint32_t* flags);
+
+/* kernel launches issued by this library since context creation (bench evidence) */
+int64_t nosa_launch_count(const NosaCtx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NOSA_B200_H */

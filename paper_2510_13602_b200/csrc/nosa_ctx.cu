@@ -1,0 +1,749 @@
+// nosa_ctx.cu — the C ABI (include/nosa_b200.h): context lifetime, the per-layer stages,
+// the pipelined multi-layer decode step (+ CUDA graph), readback and statistics.
+#include <sys/mman.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/nosa_b200.h"
+#include "nosa_device.cuh"
+
+namespace nosa {
+cudaError_t launch_select_plan(const Dev& dv, int layer, const void* q, int selector, int mode,
+                               const int* ext_req, const int* ext_nreq, cudaStream_t st);
+cudaError_t launch_start_run(const Dev& dv, int seq_begin, int seq_count, cudaStream_t st);
+cudaError_t launch_select_scores(int n_prob, const double* s_q, const double* s_e, int stride,
+                                 const int* lo, const int* hi, int m_q, int m_e, int selector,
+                                 int* out_q, int* n_q, int* out_e, int* n_e, cudaStream_t st);
+cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid);
+cudaError_t launch_prefill(const Dev& dv, int layer, int seq_begin, int S, const void* k,
+                           const void* v, int t, char* staging, cudaStream_t st);
+cudaError_t launch_unswizzle(const char* src, char* dst, int nblocks, int n_b, int D, int elem,
+                             cudaStream_t st);
+cudaError_t launch_attend(const Dev& dv, int layer, const void* q, const void* kn, const void* vn,
+                          float* out, cudaStream_t st, int num_sms);
+bool attend_supported(int n_b, int d_head, int dtype);
+}  // namespace nosa
+
+using nosa::Dev;
+
+struct NosaCtx {
+  NosaConfig cfg{};
+  Dev dv{};
+  int device = 0;
+  int num_sms = 148;
+  int gather_grid = 32;
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> ev_plan, ev_gather;
+  char* host_mirror = nullptr;
+  size_t host_bytes = 0;
+  bool host_registered = false;  // mmap + cudaHostRegister (else cudaHostAlloc)
+  std::vector<void*> dev_allocs;
+  size_t dev_bytes = 0;
+  char* staging = nullptr;
+  size_t staging_bytes = 0;
+  bool have_evhead = false;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaStream_t capture_stream = nullptr;
+  int graph_kernels = 0;
+  std::atomic<long long> launches{0};
+  std::string err;
+};
+
+static thread_local std::string g_create_error;
+
+static int fail(NosaCtx* ctx, int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf; else g_create_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                   \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess)                                                                   \
+      return fail(ctx, NOSA_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));       \
+  } while (0)
+
+static int budgets(const NosaConfig& c, int* bq, int* be, int* bt) {
+  const int k_e_topk = c.accounting == 0 ? c.k - c.n_s - c.n_w - c.k_q : c.k_e;  // config.py:72-77
+  *bq = c.k_q / c.n_b;
+  *be = k_e_topk / c.n_b;
+  *bt = *bq + *be;
+  return NOSA_OK;
+}
+
+extern "C" int nosa_config_validate(const NosaConfig* c, char* msg, int msg_len) {
+  auto bad = [&](const char* fmt, auto... args) {
+    if (msg && msg_len > 0) snprintf(msg, msg_len, fmt, args...);
+    return NOSA_ERR_VALUE;
+  };
+  if (!c) return bad("config is NULL");
+  // AttentionConfig.__post_init__ (config.py:38-65), same order and messages
+  if (c->n_b <= 0) return bad("n_b must be positive");
+  if (c->k != c->k_q + c->k_e) return bad("k must equal k_q + k_e (%d != %d + %d)", c->k, c->k_q, c->k_e);
+  const char* names[5] = {"n_s", "n_w", "k", "k_q", "k_e"};
+  const int vals[5] = {c->n_s, c->n_w, c->k, c->k_q, c->k_e};
+  for (int i = 0; i < 5; ++i) {
+    if (vals[i] < 0) return bad("%s must be non-negative", names[i]);
+    if (vals[i] % c->n_b != 0) return bad("%s=%d must be divisible by n_b=%d", names[i], vals[i], c->n_b);
+  }
+  if (!(c->n_s + c->n_w <= c->k && c->k <= c->n))
+    return bad("need n_s + n_w <= k <= n, got n_s+n_w=%d, k=%d, n=%d", c->n_s + c->n_w, c->k, c->n);
+  if (c->n_head <= 0 || c->n_kv_head <= 0 || c->n_head % c->n_kv_head != 0)
+    return bad("n_head=%d must be a positive multiple of n_kv_head=%d", c->n_head, c->n_kv_head);
+  if (c->d_head <= 0 || c->d <= 0) return bad("d and d_head must be positive");
+  if (c->accounting != 0 && c->accounting != 1) return bad("accounting must be one of ('inclusive', 'exclusive')");
+  if (c->accounting == 0 && c->k - c->n_s - c->n_w - c->k_q < 0)
+    return bad("inclusive accounting needs k_q <= k - n_s - n_w (k_q=%d, k - n_s - n_w = %d)", c->k_q,
+               c->k - c->n_s - c->n_w);
+  // engine extents (B200 build)
+  if (c->batch <= 0 || c->layers <= 0) return bad("batch and layers must be positive");
+  if (c->max_tokens <= 0) return bad("max_tokens must be positive");
+  if (c->fast_slots <= 0) return bad("fast_slots must be positive");
+  if (c->dtype != NOSA_DTYPE_BF16 && c->dtype != NOSA_DTYPE_FP32) return bad("dtype must be bf16 or fp32");
+  if (c->variant < 0 || c->variant > 2) return bad("variant must be ed-dma, s-dma or dma");
+  if (c->n_head / c->n_kv_head > 16) return bad("group size n_head/n_kv_head must be <= 16");
+  if (!nosa::attend_supported(c->n_b, c->d_head, c->dtype))
+    return bad("unsupported (n_b=%d, d_head=%d, dtype=%d): n_b in {16,32,64,128}, d_head in {64,128}",
+               c->n_b, c->d_head, c->dtype);
+  return NOSA_OK;
+}
+
+extern "C" int nosa_config_budgets(const NosaConfig* c, int32_t* bq, int32_t* be, int32_t* bt) {
+  int q, e, t;
+  budgets(*c, &q, &e, &t);
+  if (bq) *bq = q;
+  if (be) *be = e;
+  if (bt) *bt = t;
+  return NOSA_OK;
+}
+
+template <typename T>
+static int dalloc(NosaCtx* ctx, T** p, size_t count) {
+  const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+  if (e != cudaSuccess)
+    return fail(ctx, NOSA_ERR_CUDA, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+  cudaMemset(*p, 0, bytes);
+  ctx->dev_allocs.push_back(*p);
+  ctx->dev_bytes += bytes;
+  return NOSA_OK;
+}
+
+static void release(NosaCtx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+  if (ctx->graph) cudaGraphDestroy(ctx->graph);
+  if (ctx->capture_stream) cudaStreamDestroy(ctx->capture_stream);
+  for (auto e : ctx->ev_plan) cudaEventDestroy(e);
+  for (auto e : ctx->ev_gather) cudaEventDestroy(e);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  for (void* p : ctx->dev_allocs) cudaFree(p);
+  if (ctx->staging) cudaFree(ctx->staging);
+  if (ctx->host_mirror) {
+    if (ctx->host_registered) {
+      cudaHostUnregister(ctx->host_mirror);
+      munmap(ctx->host_mirror, ctx->host_bytes);
+    } else {
+      cudaFreeHost(ctx->host_mirror);
+    }
+  }
+  delete ctx;
+}
+
+extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out) {
+  char msg[512];
+  if (!out) return fail(nullptr, NOSA_ERR_VALUE, "out is NULL");
+  *out = nullptr;
+  if (nosa_config_validate(cfg, msg, sizeof(msg)) != NOSA_OK) return fail(nullptr, NOSA_ERR_VALUE, "%s", msg);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(nullptr, NOSA_ERR_CUDA, "no CUDA device visible (this path has no CPU fallback)");
+  if (device < 0 || device >= ndev) return fail(nullptr, NOSA_ERR_VALUE, "device %d out of range", device);
+  cudaSetDevice(device);
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major < 10)
+    return fail(nullptr, NOSA_ERR_CUDA, "device %d is sm_%d%d; this library is built for sm_100a", device,
+                prop.major, prop.minor);
+
+  NosaCtx* ctx = new NosaCtx();
+  ctx->cfg = *cfg;
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  if (const char* g = getenv("NOSA_GATHER_CTAS")) ctx->gather_grid = std::max(1, atoi(g));
+  const NosaConfig& c = *cfg;
+  Dev& dv = ctx->dv;
+  dv.B = c.batch;
+  dv.H = c.n_kv_head;
+  dv.Hq = c.n_head;
+  dv.G = c.n_head / c.n_kv_head;
+  dv.D = c.d_head;
+  dv.n_b = c.n_b;
+  dv.n_s = c.n_s;
+  dv.n_w = c.n_w;
+  dv.n_sink = c.n_s / c.n_b;
+  budgets(c, &dv.m_q, &dv.m_e, &dv.m_topk);
+  dv.MQ = std::max(dv.m_topk, 1);
+  dv.ME = std::max(dv.m_e, 1);
+  dv.L = c.layers;
+  dv.C = c.fast_slots;
+  dv.NB = (c.max_tokens + c.n_b - 1) / c.n_b;
+  dv.n_ev = c.n_head;
+  dv.dtype = c.dtype;
+  dv.variant = c.variant;
+  dv.elem = c.dtype == NOSA_DTYPE_BF16 ? 2 : 4;
+  dv.bpb = 2LL * c.n_b * c.d_head * dv.elem;
+  dv.max_chunks = (dv.C + nosa::kChunk - 1) / nosa::kChunk;
+  const size_t LBH = (size_t)dv.L * dv.B * dv.H;
+  const size_t BH = (size_t)dv.B * dv.H;
+
+  int rc = NOSA_OK;
+#define ALLOC(p, n)                                                   \
+  if ((rc = dalloc(ctx, &(p), (n))) != NOSA_OK) {                     \
+    g_create_error = ctx->err;                                        \
+    release(ctx);                                                     \
+    return rc;                                                        \
+  }
+  char* pool = nullptr;
+  ALLOC(pool, LBH * dv.C * (size_t)dv.bpb);
+  dv.pool = pool;
+  ALLOC(dv.kc, LBH * dv.NB * dv.D);
+  ALLOC(dv.se, LBH * dv.NB);
+  ALLOC(dv.tail_ksum, LBH * dv.D);
+  ALLOC(dv.tail_se, LBH);
+  ALLOC(dv.rank_e, LBH * dv.NB);
+  ALLOC(dv.slot_of, LBH * dv.NB);
+  ALLOC(dv.blk_of, LBH * dv.C);
+  ALLOC(dv.lastreq, LBH * dv.C);
+  ALLOC(dv.fstack, LBH * dv.C);
+  ALLOC(dv.ftop, LBH);
+  ALLOC(dv.clock, LBH);
+  ALLOC(dv.t, LBH);
+  ALLOC(dv.t0, LBH);
+  ALLOC(dv.stats, LBH * nosa::ST_N);
+  ALLOC(dv.req, LBH * dv.C);
+  ALLOC(dv.req_slot, LBH * dv.C);
+  ALLOC(dv.n_req, LBH);
+  ALLOC(dv.sel_q, LBH * dv.MQ);
+  ALLOC(dv.n_selq, LBH);
+  ALLOC(dv.sel_e, LBH * dv.ME);
+  ALLOC(dv.n_sele, LBH);
+  ALLOC(dv.s_q, LBH * dv.NB);
+  ALLOC(dv.plan_fetch, LBH * dv.C);
+  ALLOC(dv.plan_evict, LBH * dv.C);
+  ALLOC(dv.plan_n, LBH * 3);
+  ALLOC(dv.cnt, (size_t)dv.L * 2);
+  ALLOC(dv.miss_list, (size_t)dv.L * BH * dv.C);
+  ALLOC(dv.done, (size_t)dv.L * BH);
+  ALLOC(dv.part_o, BH * dv.max_chunks * dv.G * dv.D);
+  ALLOC(dv.part_ml, BH * dv.max_chunks * dv.G);
+  ALLOC(dv.w1, (size_t)dv.D * dv.n_ev);
+  ALLOC(dv.w2, (size_t)dv.n_ev);
+  ALLOC(dv.err, 1);
+#undef ALLOC
+  // every slot free, every block slow-resident (offload_sim.py:262-266)
+  {
+    std::vector<int> neg((size_t)std::max<size_t>(LBH * dv.NB, LBH * dv.C), -1);
+    cudaMemcpy(dv.slot_of, neg.data(), LBH * dv.NB * sizeof(int), cudaMemcpyHostToDevice);
+    cudaMemcpy(dv.blk_of, neg.data(), LBH * dv.C * sizeof(int), cudaMemcpyHostToDevice);
+    std::vector<int> stack(LBH * dv.C), top(LBH, dv.C);
+    for (size_t x = 0; x < LBH; ++x)
+      for (int i = 0; i < dv.C; ++i) stack[x * dv.C + i] = dv.C - 1 - i;
+    cudaMemcpy(dv.fstack, stack.data(), stack.size() * sizeof(int), cudaMemcpyHostToDevice);
+    cudaMemcpy(dv.ftop, top.data(), top.size() * sizeof(int), cudaMemcpyHostToDevice);
+  }
+
+  // slow tier: pinned + mapped host mirror
+  ctx->host_bytes = LBH * dv.NB * (size_t)dv.bpb;
+  const char* hmode = getenv("NOSA_HOST_ALLOC");
+  const bool use_register = !(hmode && strcmp(hmode, "hostalloc") == 0);
+  cudaError_t he = cudaErrorMemoryAllocation;
+  if (use_register) {
+    void* p = mmap(nullptr, ctx->host_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p != MAP_FAILED) {
+      madvise(p, ctx->host_bytes, MADV_HUGEPAGE);
+      he = cudaHostRegister(p, ctx->host_bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+      if (he == cudaSuccess) {
+        ctx->host_mirror = static_cast<char*>(p);
+        ctx->host_registered = true;
+      } else {
+        munmap(p, ctx->host_bytes);
+      }
+    }
+  }
+  if (!ctx->host_mirror) {
+    he = cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_mirror), std::max<size_t>(ctx->host_bytes, 16),
+                       cudaHostAllocMapped | cudaHostAllocPortable);
+    if (he != cudaSuccess) {
+      ctx->host_mirror = nullptr;
+      fail(ctx, NOSA_ERR_CUDA, "pinned host mirror of %zu bytes: %s", ctx->host_bytes, cudaGetErrorString(he));
+      g_create_error = ctx->err;
+      release(ctx);
+      return NOSA_ERR_CUDA;
+    }
+  }
+  void* hdev = nullptr;
+  cudaHostGetDevicePointer(&hdev, ctx->host_mirror, 0);
+  dv.host = static_cast<char*>(hdev);
+
+  cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking);
+  ctx->ev_plan.resize(dv.L);
+  ctx->ev_gather.resize(dv.L);
+  for (int l = 0; l < dv.L; ++l) {
+    cudaEventCreateWithFlags(&ctx->ev_plan[l], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->ev_gather[l], cudaEventDisableTiming);
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    fail(ctx, NOSA_ERR_CUDA, "context init: %s", cudaGetErrorString(e));
+    g_create_error = ctx->err;
+    release(ctx);
+    return NOSA_ERR_CUDA;
+  }
+  *out = ctx;
+  return NOSA_OK;
+}
+
+extern "C" void nosa_ctx_destroy(NosaCtx* ctx) { release(ctx); }
+
+extern "C" const char* nosa_last_error(const NosaCtx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+extern "C" int nosa_ctx_memory(const NosaCtx* ctx, int64_t* dev, int64_t* host) {
+  if (!ctx) return NOSA_ERR_VALUE;
+  if (dev) *dev = (int64_t)ctx->dev_bytes;
+  if (host) *host = (int64_t)ctx->host_bytes;
+  return NOSA_OK;
+}
+
+extern "C" int64_t nosa_launch_count(const NosaCtx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+extern "C" int nosa_set_eviction_head(NosaCtx* ctx, const double* w1, const double* w2) {
+  if (!ctx || !w1 || !w2) return fail(ctx, NOSA_ERR_VALUE, "eviction head weights are NULL");
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaMemcpy(ctx->dv.w1, w1, sizeof(double) * ctx->dv.D * ctx->dv.n_ev, cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpy(ctx->dv.w2, w2, sizeof(double) * ctx->dv.n_ev, cudaMemcpyHostToDevice));
+  ctx->have_evhead = true;
+  return NOSA_OK;
+}
+
+static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+static int check_layer(NosaCtx* ctx, int layer) {
+  if (!ctx) return NOSA_ERR_VALUE;
+  if (layer < 0 || layer >= ctx->dv.L) return fail(ctx, NOSA_ERR_VALUE, "layer %d out of range [0, %d)", layer, ctx->dv.L);
+  return NOSA_OK;
+}
+
+extern "C" int nosa_prefill(NosaCtx* ctx, int layer, int seq_begin, int seq_count, const void* k,
+                            const void* v, int t, void* stream) {
+  int rc = check_layer(ctx, layer);
+  if (rc) return rc;
+  const Dev& dv = ctx->dv;
+  if (!ctx->have_evhead) return fail(ctx, NOSA_ERR_STATE, "set the eviction head before prefill");
+  if (seq_begin < 0 || seq_count <= 0 || seq_begin + seq_count > dv.B)
+    return fail(ctx, NOSA_ERR_VALUE, "sequence range [%d, %d) outside batch %d", seq_begin, seq_begin + seq_count, dv.B);
+  if (t < 0 || t > ctx->cfg.max_tokens)
+    return fail(ctx, NOSA_ERR_VALUE, "head cache capacity exhausted: prefill of %d tokens > max_tokens %d", t,
+                ctx->cfg.max_tokens);
+  if (t > 0 && (!k || !v)) return fail(ctx, NOSA_ERR_VALUE, "k/v are NULL");
+  cudaSetDevice(ctx->device);
+  const size_t need = (size_t)seq_count * dv.H * dv.NB * (size_t)dv.bpb;
+  if (need > ctx->staging_bytes) {
+    cudaStreamSynchronize(S(stream));
+    if (ctx->staging) cudaFree(ctx->staging);
+    ctx->staging = nullptr;
+    CUDA_TRY(ctx, cudaMalloc(&ctx->staging, need));
+    ctx->staging_bytes = need;
+  }
+  CUDA_TRY(ctx, nosa::launch_prefill(dv, layer, seq_begin, seq_count, k, v, t, ctx->staging, S(stream)));
+  ctx->launches += 3;
+  const size_t lbh0 = ((size_t)layer * dv.B + seq_begin) * dv.H;
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_mirror + lbh0 * dv.NB * (size_t)dv.bpb, ctx->staging, need,
+                                cudaMemcpyDeviceToHost, S(stream)));
+  return NOSA_OK;
+}
+
+extern "C" int nosa_start_run(NosaCtx* ctx, int seq_begin, int seq_count, void* stream) {
+  if (!ctx) return NOSA_ERR_VALUE;
+  if (seq_begin < 0 || seq_count <= 0 || seq_begin + seq_count > ctx->dv.B)
+    return fail(ctx, NOSA_ERR_VALUE, "sequence range outside batch");
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, nosa::launch_start_run(ctx->dv, seq_begin, seq_count, S(stream)));
+  ctx->launches += 1;
+  return NOSA_OK;
+}
+
+extern "C" int nosa_select_plan(NosaCtx* ctx, int layer, const void* q, int selector, void* stream) {
+  int rc = check_layer(ctx, layer);
+  if (rc) return rc;
+  if (selector != 0 && selector != 1) return fail(ctx, NOSA_ERR_VALUE, "selector must be nosa or infllmv2");
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->dv.cnt + 2 * layer, 0, 2 * sizeof(int), S(stream)));
+  CUDA_TRY(ctx, nosa::launch_select_plan(ctx->dv, layer, q, selector, 1, nullptr, nullptr, S(stream)));
+  ctx->launches += 1;
+  return NOSA_OK;
+}
+
+extern "C" int nosa_select(NosaCtx* ctx, int layer, const void* q, int selector, void* stream) {
+  int rc = check_layer(ctx, layer);
+  if (rc) return rc;
+  if (selector != 0 && selector != 1) return fail(ctx, NOSA_ERR_VALUE, "selector must be nosa or infllmv2");
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, nosa::launch_select_plan(ctx->dv, layer, q, selector, 0, nullptr, nullptr, S(stream)));
+  ctx->launches += 1;
+  return NOSA_OK;
+}
+
+extern "C" int nosa_cache_plan(NosaCtx* ctx, int layer, const int32_t* req, const int32_t* n_req, void* stream) {
+  int rc = check_layer(ctx, layer);
+  if (rc) return rc;
+  if (!req || !n_req) return fail(ctx, NOSA_ERR_VALUE, "required sets are NULL");
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->dv.cnt + 2 * layer, 0, 2 * sizeof(int), S(stream)));
+  CUDA_TRY(ctx, nosa::launch_select_plan(ctx->dv, layer, nullptr, 0, 2, req, n_req, S(stream)));
+  ctx->launches += 1;
+  return NOSA_OK;
+}
+
+static int gather_memcpy(NosaCtx* ctx, int layer, cudaStream_t st) {
+  // copy-engine mover: the host learns the miss list (one sync) and batches the DMA copies
+  const Dev& dv = ctx->dv;
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  int n = 0;
+  CUDA_TRY(ctx, cudaMemcpy(&n, dv.cnt + 2 * layer, sizeof(int), cudaMemcpyDeviceToHost));
+  if (n == 0) return NOSA_OK;
+  std::vector<int4> list(n);
+  CUDA_TRY(ctx, cudaMemcpy(list.data(), dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C, n * sizeof(int4),
+                           cudaMemcpyDeviceToHost));
+  std::vector<void*> dsts(n), srcs(n);
+  std::vector<size_t> sizes(n, (size_t)dv.bpb);
+  for (int i = 0; i < n; ++i) {
+    srcs[i] = ctx->host_mirror + ((size_t)list[i].x * dv.NB + list[i].y) * dv.bpb;
+    dsts[i] = dv.pool + ((size_t)list[i].x * dv.C + list[i].z) * dv.bpb;
+  }
+  cudaMemcpyAttributes attr{};
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  attr.srcLocHint.type = cudaMemLocationTypeHost;
+  attr.dstLocHint.type = cudaMemLocationTypeDevice;
+  attr.dstLocHint.id = ctx->device;
+  size_t idx0 = 0, fail_idx = 0;
+  cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &idx0, 1, &fail_idx, st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    for (int i = 0; i < n; ++i) CUDA_TRY(ctx, cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyHostToDevice, st));
+  }
+  return NOSA_OK;
+}
+
+extern "C" int nosa_gather(NosaCtx* ctx, int layer, int mode, void* stream) {
+  int rc = check_layer(ctx, layer);
+  if (rc) return rc;
+  cudaSetDevice(ctx->device);
+  if (mode == NOSA_GATHER_MEMCPY) return gather_memcpy(ctx, layer, S(stream));
+  if (mode != NOSA_GATHER_UVA) return fail(ctx, NOSA_ERR_VALUE, "unknown gather mode %d", mode);
+  CUDA_TRY(ctx, nosa::launch_gather(ctx->dv, layer, S(stream), ctx->gather_grid));
+  ctx->launches += 1;
+  return NOSA_OK;
+}
+
+extern "C" int nosa_attend(NosaCtx* ctx, int layer, const void* q, const void* k_new, const void* v_new, float* out,
+                           void* stream) {
+  int rc = check_layer(ctx, layer);
+  if (rc) return rc;
+  if (!q || !k_new || !v_new || !out) return fail(ctx, NOSA_ERR_VALUE, "attend: NULL tensor");
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, nosa::launch_attend(ctx->dv, layer, q, k_new, v_new, out, S(stream), ctx->num_sms));
+  ctx->launches += 1;
+  return NOSA_OK;
+}
+
+static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, bool count) {
+  const Dev& dv = ctx->dv;
+  const size_t qstride = (size_t)dv.B * dv.Hq * dv.D * dv.elem;
+  const size_t kstride = (size_t)dv.B * dv.H * dv.D * dv.elem;
+  const size_t ostride = (size_t)dv.B * dv.Hq * dv.D;
+  const char* q = static_cast<const char*>(io->q);
+  const char* kn = static_cast<const char*>(io->k_new);
+  const char* vn = static_cast<const char*>(io->v_new);
+  CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt, 0, (size_t)dv.L * 2 * sizeof(int), st));
+  for (int l = 0; l < dv.L; ++l) {
+    CUDA_TRY(ctx, nosa::launch_select_plan(dv, l, q + l * qstride, io->selector, 1, nullptr, nullptr, st));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[l], st));
+  }
+  for (int l = 0; l < dv.L; ++l) {
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_plan[l], 0));
+    CUDA_TRY(ctx, nosa::launch_gather(dv, l, ctx->copy_stream, ctx->gather_grid));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[l], ctx->copy_stream));
+  }
+  for (int l = 0; l < dv.L; ++l) {
+    CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_gather[l], 0));
+    CUDA_TRY(ctx, nosa::launch_attend(dv, l, q + l * qstride, kn + l * kstride, vn + l * kstride,
+                                      io->out + l * ostride, st, ctx->num_sms));
+  }
+  if (count) ctx->launches += 3LL * dv.L;
+  return NOSA_OK;
+}
+
+extern "C" int nosa_decode_step(NosaCtx* ctx, const NosaStepIO* io, void* stream) {
+  if (!ctx || !io || !io->q || !io->k_new || !io->v_new || !io->out)
+    return fail(ctx, NOSA_ERR_VALUE, "decode_step: NULL io");
+  if (io->selector != 0 && io->selector != 1) return fail(ctx, NOSA_ERR_VALUE, "selector must be nosa or infllmv2");
+  cudaSetDevice(ctx->device);
+  if (io->gather_mode == NOSA_GATHER_MEMCPY) {
+    // host-planned copies: per layer, select+plan, sync, batched DMA, attend
+    const Dev& dv = ctx->dv;
+    const size_t qstride = (size_t)dv.B * dv.Hq * dv.D * dv.elem;
+    const size_t kstride = (size_t)dv.B * dv.H * dv.D * dv.elem;
+    const size_t ostride = (size_t)dv.B * dv.Hq * dv.D;
+    for (int l = 0; l < dv.L; ++l) {
+      int rc = nosa_select_plan(ctx, l, static_cast<const char*>(io->q) + l * qstride, io->selector, stream);
+      if (rc) return rc;
+      rc = gather_memcpy(ctx, l, S(stream));
+      if (rc) return rc;
+      rc = nosa_attend(ctx, l, static_cast<const char*>(io->q) + l * qstride,
+                       static_cast<const char*>(io->k_new) + l * kstride,
+                       static_cast<const char*>(io->v_new) + l * kstride, io->out + l * ostride, stream);
+      if (rc) return rc;
+    }
+    return NOSA_OK;
+  }
+  return enqueue_step(ctx, io, S(stream), true);
+}
+
+extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {
+  if (!ctx || !io) return NOSA_ERR_VALUE;
+  if (io->gather_mode != NOSA_GATHER_UVA) return fail(ctx, NOSA_ERR_VALUE, "graph capture needs the UVA gather");
+  cudaSetDevice(ctx->device);
+  if (ctx->graph_exec) { cudaGraphExecDestroy(ctx->graph_exec); ctx->graph_exec = nullptr; }
+  if (ctx->graph) { cudaGraphDestroy(ctx->graph); ctx->graph = nullptr; }
+  CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->capture_stream, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue_step(ctx, io, ctx->capture_stream, false);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(ctx->capture_stream, &g);
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail(ctx, NOSA_ERR_CUDA, "stream capture: %s", cudaGetErrorString(e));
+  ctx->graph = g;
+  CUDA_TRY(ctx, cudaGraphInstantiate(&ctx->graph_exec, g, 0));
+  ctx->graph_kernels = 3 * ctx->dv.L;
+  return NOSA_OK;
+}
+
+extern "C" int nosa_step_graph_launch(NosaCtx* ctx, void* stream) {
+  if (!ctx || !ctx->graph_exec) return fail(ctx, NOSA_ERR_STATE, "no captured step graph");
+  CUDA_TRY(ctx, cudaGraphLaunch(ctx->graph_exec, S(stream)));
+  ctx->launches += ctx->graph_kernels;
+  return NOSA_OK;
+}
+
+extern "C" int nosa_select_scores(int n_prob, const double* s_q, const double* s_e, int stride,
+                                  const int32_t* pool_lo, const int32_t* pool_hi, int m_q, int m_e, int selector,
+                                  int32_t* out_q, int32_t* n_q, int32_t* out_e, int32_t* n_e, void* stream) {
+  if (n_prob <= 0) return NOSA_OK;
+  if (!s_q || !pool_lo || !pool_hi || !out_q || !n_q || !out_e || !n_e || (selector == 0 && !s_e))
+    return fail(nullptr, NOSA_ERR_VALUE, "select_scores: NULL argument");
+  if (m_q < 0 || m_e < 0 || stride <= 0) return fail(nullptr, NOSA_ERR_VALUE, "select_scores: bad budgets");
+  cudaError_t e = nosa::launch_select_scores(n_prob, s_q, s_e, stride, pool_lo, pool_hi, m_q, m_e, selector, out_q,
+                                             n_q, out_e, n_e, S(stream));
+  if (e != cudaSuccess) return fail(nullptr, NOSA_ERR_CUDA, "select_scores: %s", cudaGetErrorString(e));
+  return NOSA_OK;
+}
+
+// ---------------------------------------------------------------- readback
+#define SYNC_OR_FAIL(ctx)                                                      \
+  do {                                                                         \
+    cudaSetDevice((ctx)->device);                                              \
+    cudaError_t _e = cudaDeviceSynchronize();                                  \
+    if (_e != cudaSuccess)                                                     \
+      return fail(ctx, NOSA_ERR_CUDA, "device error: %s", cudaGetErrorString(_e)); \
+  } while (0)
+
+extern "C" int nosa_read_selection(NosaCtx* ctx, int layer, int cap, int32_t* bq, int32_t* nq, int32_t* be,
+                                   int32_t* ne, int32_t* req, int32_t* nreq, double* s_q) {
+  int rc = check_layer(ctx, layer);
+  if (rc) return rc;
+  SYNC_OR_FAIL(ctx);
+  const Dev& dv = ctx->dv;
+  const size_t BH = (size_t)dv.B * dv.H, off = (size_t)layer * BH;
+  std::vector<int> tq(BH * dv.MQ), te(BH * dv.ME), tr(BH * dv.C), cq(BH), ce(BH), cr(BH);
+  CUDA_TRY(ctx, cudaMemcpy(tq.data(), dv.sel_q + off * dv.MQ, tq.size() * 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpy(te.data(), dv.sel_e + off * dv.ME, te.size() * 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpy(tr.data(), dv.req + off * dv.C, tr.size() * 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpy(cq.data(), dv.n_selq + off, BH * 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpy(ce.data(), dv.n_sele + off, BH * 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpy(cr.data(), dv.n_req + off, BH * 4, cudaMemcpyDeviceToHost));
+  for (size_t x = 0; x < BH; ++x) {
+    if (nq) nq[x] = cq[x];
+    if (ne) ne[x] = ce[x];
+    if (nreq) nreq[x] = cr[x];
+    for (int i = 0; i < cap; ++i) {
+      if (bq) bq[x * cap + i] = i < cq[x] && i < dv.MQ ? tq[x * dv.MQ + i] : -1;
+      if (be) be[x * cap + i] = i < ce[x] && i < dv.ME ? te[x * dv.ME + i] : -1;
+      if (req) req[x * cap + i] = i < cr[x] && i < dv.C ? tr[x * dv.C + i] : -1;
+    }
+  }
+  if (s_q) CUDA_TRY(ctx, cudaMemcpy(s_q, dv.s_q + off * dv.NB, BH * dv.NB * 8, cudaMemcpyDeviceToHost));
+  return NOSA_OK;
+}
+
+extern "C" int nosa_read_plan(NosaCtx* ctx, int layer, int32_t* fetch, int32_t* nf, int32_t* evict, int32_t* ne,
+                              int32_t* nh) {
+  int rc = check_layer(ctx, layer);
+  if (rc) return rc;
+  SYNC_OR_FAIL(ctx);
+  const Dev& dv = ctx->dv;
+  const size_t BH = (size_t)dv.B * dv.H, off = (size_t)layer * BH;
+  std::vector<int> n(BH * 3);
+  CUDA_TRY(ctx, cudaMemcpy(n.data(), dv.plan_n + off * 3, n.size() * 4, cudaMemcpyDeviceToHost));
+  if (fetch) CUDA_TRY(ctx, cudaMemcpy(fetch, dv.plan_fetch + off * dv.C, BH * dv.C * 4, cudaMemcpyDeviceToHost));
+  if (evict) CUDA_TRY(ctx, cudaMemcpy(evict, dv.plan_evict + off * dv.C, BH * dv.C * 4, cudaMemcpyDeviceToHost));
+  for (size_t x = 0; x < BH; ++x) {
+    if (nf) nf[x] = n[x * 3 + 0];
+    if (ne) ne[x] = n[x * 3 + 1];
+    if (nh) nh[x] = n[x * 3 + 2];
+  }
+  return NOSA_OK;
+}
+
+extern "C" int nosa_read_residency(NosaCtx* ctx, int layer, int seq, int head, int32_t* slot_of, int32_t* block_of) {
+  int rc = check_layer(ctx, layer);
+  if (rc) return rc;
+  const Dev& dv = ctx->dv;
+  if (seq < 0 || seq >= dv.B || head < 0 || head >= dv.H) return fail(ctx, NOSA_ERR_VALUE, "seq/head out of range");
+  SYNC_OR_FAIL(ctx);
+  const size_t lbh = ((size_t)layer * dv.B + seq) * dv.H + head;
+  if (slot_of) CUDA_TRY(ctx, cudaMemcpy(slot_of, dv.slot_of + lbh * dv.NB, dv.NB * 4, cudaMemcpyDeviceToHost));
+  if (block_of) CUDA_TRY(ctx, cudaMemcpy(block_of, dv.blk_of + lbh * dv.C, dv.C * 4, cudaMemcpyDeviceToHost));
+  return NOSA_OK;
+}
+
+extern "C" int nosa_read_block_scores(NosaCtx* ctx, int layer, double* s_e_c) {
+  int rc = check_layer(ctx, layer);
+  if (rc) return rc;
+  SYNC_OR_FAIL(ctx);
+  const Dev& dv = ctx->dv;
+  const size_t BH = (size_t)dv.B * dv.H;
+  CUDA_TRY(ctx, cudaMemcpy(s_e_c, dv.se + (size_t)layer * BH * dv.NB, BH * dv.NB * 8, cudaMemcpyDeviceToHost));
+  return NOSA_OK;
+}
+
+static int read_blocks(NosaCtx* ctx, const char* src_dev, int nblocks, std::vector<char>& out) {
+  const Dev& dv = ctx->dv;
+  char* tmp = nullptr;
+  const size_t bytes = (size_t)nblocks * dv.bpb;
+  CUDA_TRY(ctx, cudaMalloc(&tmp, std::max<size_t>(bytes, 16)));
+  nosa::launch_unswizzle(src_dev, tmp, nblocks, dv.n_b, dv.D, dv.elem, 0);
+  out.resize(bytes);
+  cudaError_t e = cudaMemcpy(out.data(), tmp, bytes, cudaMemcpyDeviceToHost);
+  cudaFree(tmp);
+  if (e != cudaSuccess) return fail(ctx, NOSA_ERR_CUDA, "read_blocks: %s", cudaGetErrorString(e));
+  return NOSA_OK;
+}
+
+extern "C" int nosa_read_kv(NosaCtx* ctx, int layer, int seq, int head, int t, void* k, void* v) {
+  int rc = check_layer(ctx, layer);
+  if (rc) return rc;
+  const Dev& dv = ctx->dv;
+  if (seq < 0 || seq >= dv.B || head < 0 || head >= dv.H) return fail(ctx, NOSA_ERR_VALUE, "seq/head out of range");
+  if (t < 0 || t > dv.NB * dv.n_b) return fail(ctx, NOSA_ERR_VALUE, "t out of range");
+  if (t == 0) return NOSA_OK;
+  SYNC_OR_FAIL(ctx);
+  const size_t lbh = ((size_t)layer * dv.B + seq) * dv.H + head;
+  const int nblk = (t + dv.n_b - 1) / dv.n_b;
+  std::vector<char> buf;
+  rc = read_blocks(ctx, dv.host + lbh * dv.NB * dv.bpb, nblk, buf);
+  if (rc) return rc;
+  const size_t row = (size_t)dv.D * dv.elem;
+  memcpy(k, buf.data(), (size_t)t * row);
+  memcpy(v, buf.data() + (size_t)nblk * dv.n_b * row, (size_t)t * row);
+  return NOSA_OK;
+}
+
+extern "C" int nosa_read_slot(NosaCtx* ctx, int layer, int seq, int head, int slot, void* kv) {
+  int rc = check_layer(ctx, layer);
+  if (rc) return rc;
+  const Dev& dv = ctx->dv;
+  if (seq < 0 || seq >= dv.B || head < 0 || head >= dv.H || slot < 0 || slot >= dv.C)
+    return fail(ctx, NOSA_ERR_VALUE, "seq/head/slot out of range");
+  SYNC_OR_FAIL(ctx);
+  const size_t lbh = ((size_t)layer * dv.B + seq) * dv.H + head;
+  std::vector<char> buf;
+  rc = read_blocks(ctx, dv.pool + (lbh * dv.C + slot) * dv.bpb, 1, buf);
+  if (rc) return rc;
+  memcpy(kv, buf.data(), buf.size());
+  return NOSA_OK;
+}
+
+extern "C" int nosa_read_stats(NosaCtx* ctx, int l0, int l1, int s0, int s1, NosaStats* out) {
+  if (!ctx || !out) return NOSA_ERR_VALUE;
+  const Dev& dv = ctx->dv;
+  if (l0 < 0 || l1 > dv.L || l0 > l1 || s0 < 0 || s1 > dv.B || s0 > s1) return fail(ctx, NOSA_ERR_VALUE, "stats range");
+  SYNC_OR_FAIL(ctx);
+  const size_t LBH = (size_t)dv.L * dv.B * dv.H;
+  std::vector<long long> st(LBH * nosa::ST_N);
+  CUDA_TRY(ctx, cudaMemcpy(st.data(), dv.stats, st.size() * 8, cudaMemcpyDeviceToHost));
+  memset(out, 0, sizeof(*out));
+  for (int l = l0; l < l1; ++l)
+    for (int s = s0; s < s1; ++s)
+      for (int h = 0; h < dv.H; ++h) {
+        const long long* p = &st[(((size_t)l * dv.B + s) * dv.H + h) * nosa::ST_N];
+        out->hits += p[nosa::ST_HITS];
+        out->misses += p[nosa::ST_MISSES];
+        out->new_blocks += p[nosa::ST_NEW];
+        out->evictions += p[nosa::ST_EVICT];
+        out->steps += p[nosa::ST_STEPS];
+      }
+  out->bytes_up = out->misses * dv.bpb;
+  out->bytes_down = out->evictions * dv.bpb;
+  return NOSA_OK;
+}
+
+extern "C" int nosa_reset_stats(NosaCtx* ctx, void* stream) {
+  if (!ctx) return NOSA_ERR_VALUE;
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->dv.stats, 0, (size_t)ctx->dv.L * ctx->dv.B * ctx->dv.H * nosa::ST_N * 8, S(stream)));
+  return NOSA_OK;
+}
+
+extern "C" int nosa_read_lengths(NosaCtx* ctx, int32_t* t) {
+  if (!ctx || !t) return NOSA_ERR_VALUE;
+  SYNC_OR_FAIL(ctx);
+  const Dev& dv = ctx->dv;
+  std::vector<int> all((size_t)dv.L * dv.B * dv.H);
+  CUDA_TRY(ctx, cudaMemcpy(all.data(), dv.t, all.size() * 4, cudaMemcpyDeviceToHost));
+  for (int l = 0; l < dv.L; ++l)
+    for (int b = 0; b < dv.B; ++b) t[l * dv.B + b] = all[((size_t)l * dv.B + b) * dv.H];
+  return NOSA_OK;
+}
+
+extern "C" int nosa_check_errors(NosaCtx* ctx, uint32_t* flags) {
+  if (!ctx) return NOSA_ERR_VALUE;
+  SYNC_OR_FAIL(ctx);
+  unsigned f = 0;
+  CUDA_TRY(ctx, cudaMemcpy(&f, ctx->dv.err, 4, cudaMemcpyDeviceToHost));
+  if (flags) *flags = f;
+  if (f) {
+    cudaMemset(ctx->dv.err, 0, 4);
+    if (f & NOSA_FLAG_CAPACITY)
+      return fail(ctx, NOSA_ERR_CAPACITY, "step requires more blocks than the fast tier holds per head (%d)", ctx->dv.C);
+    return fail(ctx, NOSA_ERR_VALUE, "device error flags 0x%x", f);
+  }
+  return NOSA_OK;
+}

@@ -1,0 +1,199 @@
+// nosa_gather.cu — K3 miss gather (slow -> fast mover) and the prefill / residency-reset
+// kernels that set up a run.
+//
+// K3 is the `mover` of TieredBlockManager.apply_transfers (kv_manager.py:290, 300-305) for the
+// whole layer at once: every (lbh, block, slot) entry the planner enqueued is copied from the
+// pinned, mapped host mirror into its HBM slot.  The SMs read host memory directly over PCIe
+// (zero-copy UVA), so the copy needs no host round trip to learn the miss list.
+#include "nosa_device.cuh"
+
+namespace nosa {
+
+// grid = a few dozen CTAs (latency-bound on PCIe, leaves SMs to the attention kernel)
+template <int UNROLL>
+__global__ void __launch_bounds__(256) gather_kernel(Dev dv, int layer) {
+  const int n = *reinterpret_cast<volatile int*>(dv.cnt + 2 * layer);
+  const int4* list = dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C;
+  const int vecs = (int)(dv.bpb / 16);
+  for (int e = blockIdx.x; e < n; e += gridDim.x) {
+    const int4 m = list[e];
+    const int4* src = reinterpret_cast<const int4*>(dv.host + ((size_t)m.x * dv.NB + m.y) * dv.bpb);
+    int4* dst = reinterpret_cast<int4*>(dv.pool + ((size_t)m.x * dv.C + m.z) * dv.bpb);
+    for (int base = threadIdx.x; base < vecs; base += blockDim.x * UNROLL) {
+      int4 v[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int i = base + u * blockDim.x;
+        if (i < vecs) v[u] = __ldcs(src + i);
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int i = base + u * blockDim.x;
+        if (i < vecs) dst[i] = v[u];
+      }
+    }
+  }
+}
+
+cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid) {
+  gather_kernel<8><<<grid, 256, 0, st>>>(dv, layer);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// Prefill, step 1: K/V rows [S][H][t][D] -> swizzled block format [S*H][NB][2][n_b][D] in a
+// device staging buffer (zero padded past t), later copied to the host mirror in one DMA.
+template <typename T>
+__global__ void prefill_layout_kernel(Dev dv, const T* __restrict__ k, const T* __restrict__ v,
+                                      int t, int S, char* __restrict__ staging) {
+  const int elem = sizeof(T);
+  const int D = dv.D, n_b = dv.n_b;
+  const int chunks_per_row = D * elem / 16;
+  const long long per_sh = (long long)dv.NB * 2 * n_b * chunks_per_row;  // 16-byte chunks
+  const long long total = (long long)S * dv.H * per_sh;
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+       x += (long long)gridDim.x * blockDim.x) {
+    const long long sh = x / per_sh;
+    long long rem = x - sh * per_sh;
+    const int blk = (int)(rem / (2 * n_b * chunks_per_row));
+    rem -= (long long)blk * 2 * n_b * chunks_per_row;
+    const int which = (int)(rem / (n_b * chunks_per_row));
+    rem -= (long long)which * n_b * chunks_per_row;
+    const int row = (int)(rem / chunks_per_row);
+    const int ch = (int)(rem - (long long)row * chunks_per_row);
+    const int tok = blk * n_b + row;
+    int4 val = make_int4(0, 0, 0, 0);
+    if (tok < t) {
+      const T* src = (which ? v : k) + ((size_t)sh * t + tok) * D;
+      val = reinterpret_cast<const int4*>(src)[ch];
+    }
+    char* dst = staging + ((size_t)sh * dv.NB + blk) * dv.bpb + (size_t)which * n_b * D * elem +
+                (size_t)row * D * elem + ((ch ^ (row & 7)) << 4);
+    *reinterpret_cast<int4*>(dst) = val;
+  }
+}
+
+// Prefill, step 2: per block of the prefix, the f64 block means of K (compress_blocks,
+// attention.py:42-59) and of the per-token importance scores (importance_scores +
+// compress_scores, attention.py:62-64, 121-146); partial tail block -> running sums.
+// One warp per (s, h, block).
+template <typename T>
+__global__ void prefill_stats_kernel(Dev dv, int layer, int seq_begin, const T* __restrict__ k,
+                                     const T* __restrict__ v, int t, int S) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nblk = (t + dv.n_b - 1) / dv.n_b;
+  const int total = S * dv.H * nblk;
+  if (gw >= total) return;
+  const int sh = gw / nblk, blk = gw - sh * nblk;
+  const int s = sh / dv.H, h = sh - s * dv.H;
+  const int lbh = (layer * dv.B + seq_begin + s) * dv.H + h;
+  const int D = dv.D, n_b = dv.n_b;
+  const int lo = blk * n_b, cnt = min(n_b, t - lo);
+  double se_sum = 0.0;
+  double ks[8];  // D <= 256
+#pragma unroll
+  for (int j = 0; j < 8; ++j) ks[j] = 0.0;
+  for (int r = 0; r < cnt; ++r) {
+    const T* krow = k + ((size_t)sh * t + lo + r) * D;
+    const T* vrow = v + ((size_t)sh * t + lo + r) * D;
+    se_sum += token_score_warp<T>(vrow, dv.w1, dv.w2, D, dv.n_ev, dv.variant);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int d = lane + 32 * j;
+      if (d < D) ks[j] += to_f64(krow[d]);
+    }
+  }
+  if (cnt == n_b) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int d = lane + 32 * j;
+      if (d < D) dv.kc[((size_t)lbh * dv.NB + blk) * D + d] = ks[j] / (double)n_b;
+    }
+    if (lane == 0) dv.se[(size_t)lbh * dv.NB + blk] = se_sum / (double)n_b;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int d = lane + 32 * j;
+      if (d < D) dv.tail_ksum[(size_t)lbh * D + d] = ks[j];
+    }
+    if (lane == 0) dv.tail_se[lbh] = se_sum;
+  }
+}
+
+// Reset the residency of [seq_begin, seq_begin+S) in one layer: every block slow-resident,
+// fresh LIFO free lists (kv_manager.py:147-150), cache length t.
+__global__ void reset_residency_kernel(Dev dv, int layer, int seq_begin, int S, int t) {
+  const int sh = blockIdx.x;
+  const int lbh = (layer * dv.B + seq_begin) * dv.H + sh;  // S*H consecutive lbh
+  for (int i = threadIdx.x; i < dv.NB; i += blockDim.x) dv.slot_of[(size_t)lbh * dv.NB + i] = -1;
+  for (int i = threadIdx.x; i < dv.C; i += blockDim.x) {
+    dv.blk_of[(size_t)lbh * dv.C + i] = -1;
+    dv.lastreq[(size_t)lbh * dv.C + i] = 0;
+    dv.fstack[(size_t)lbh * dv.C + i] = dv.C - 1 - i;
+  }
+  if (threadIdx.x == 0) {
+    dv.ftop[lbh] = dv.C;
+    dv.clock[lbh] = 0;
+    dv.t[lbh] = t;
+    dv.t0[lbh] = t;
+    dv.n_req[lbh] = 0;
+    if (t % dv.n_b == 0) {
+      dv.tail_se[lbh] = 0.0;
+    }
+  }
+  if (t % dv.n_b == 0)
+    for (int d = threadIdx.x; d < dv.D; d += blockDim.x) dv.tail_ksum[(size_t)lbh * dv.D + d] = 0.0;
+}
+
+cudaError_t launch_prefill(const Dev& dv, int layer, int seq_begin, int S, const void* k,
+                           const void* v, int t, char* staging, cudaStream_t st) {
+  const int nblk = (t + dv.n_b - 1) / dv.n_b;
+  reset_residency_kernel<<<S * dv.H, 256, 0, st>>>(dv, layer, seq_begin, S, t);
+  const int warps = S * dv.H * nblk;
+  const int blocks = (warps * 32 + 255) / 256;
+  if (dv.dtype == 0) {
+    prefill_layout_kernel<__nv_bfloat16><<<2048, 256, 0, st>>>(
+        dv, static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), t, S, staging);
+    if (warps > 0)
+      prefill_stats_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(
+          dv, layer, seq_begin, static_cast<const __nv_bfloat16*>(k),
+          static_cast<const __nv_bfloat16*>(v), t, S);
+  } else {
+    prefill_layout_kernel<float><<<2048, 256, 0, st>>>(dv, static_cast<const float*>(k),
+                                                       static_cast<const float*>(v), t, S, staging);
+    if (warps > 0)
+      prefill_stats_kernel<float><<<blocks, 256, 0, st>>>(dv, layer, seq_begin, static_cast<const float*>(k),
+                                                          static_cast<const float*>(v), t, S);
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// Readback helper: un-swizzle n blocks [n][2][n_b][D] (storage format) into [2][n][n_b][D]
+// row order (K rows then V rows), on the device.
+__global__ void unswizzle_kernel(const char* __restrict__ src, char* __restrict__ dst, int nblocks,
+                                 int n_b, int D, int elem) {
+  const int chunks_per_row = D * elem / 16;
+  const long long total = (long long)nblocks * 2 * n_b * chunks_per_row;
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+       x += (long long)gridDim.x * blockDim.x) {
+    const int ch = (int)(x % chunks_per_row);
+    const long long rr = x / chunks_per_row;  // (blk, which, row)
+    const int row = (int)(rr % n_b);
+    const long long bw = rr / n_b;
+    const int which = (int)(bw % 2);
+    const long long blk = bw / 2;
+    const int4 val = *reinterpret_cast<const int4*>(src + (size_t)rr * D * elem + ((ch ^ (row & 7)) << 4));
+    char* o = dst + (((size_t)which * nblocks + blk) * n_b + row) * D * elem + (size_t)ch * 16;
+    *reinterpret_cast<int4*>(o) = val;
+  }
+}
+
+cudaError_t launch_unswizzle(const char* src, char* dst, int nblocks, int n_b, int D, int elem,
+                             cudaStream_t st) {
+  unswizzle_kernel<<<256, 256, 0, st>>>(src, dst, nblocks, n_b, D, elem);
+  return cudaGetLastError();
+}
+
+}  // namespace nosa

@@ -1,0 +1,526 @@
+// nosa_select.cu — K1 (block selection) and K2 (GPU-resident block-cache planner).
+//
+// K1 restates, per (sequence, kv head), the selection half of DecodeEngine.step
+// (decode.py:169-176): GQA-summed query scoring of the frozen pool (decode.py:171-172),
+// then nosa_select (selection.py:130-160) or infllmv2_select (selection.py:163-178) with
+// argtopk's order (numerics.py:59-73: score desc, index asc).  Scores are computed in f64
+// from f64 block means so the chosen sets agree with the f64 oracle except on exact ties.
+// K2 restates TieredBlockManager.plan_transfers + apply_transfers (kv_manager.py:205-298)
+// for one manager per (sequence, kv head): hit test, least-recently-required victims
+// (kv_manager.py:125-127), LIFO free-slot reuse (kv_manager.py:147-150, 281-298).
+#include "nosa_device.cuh"
+
+namespace nosa {
+
+// Bitonic sort of Pp (power of two) (key, idx) pairs in shared memory, best first:
+// larger key wins, equal keys -> smaller idx wins.  Called by the whole block.
+__device__ void block_sort_best_first(unsigned long long* key, int* idx, int Pp) {
+  for (int k = 2; k <= Pp; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < Pp; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long ka = key[i], kb = key[ixj];
+          const int ia = idx[i], ib = idx[ixj];
+          const bool b_better = (kb > ka) || (kb == ka && ib < ia);
+          const bool a_better = (ka > kb) || (ka == kb && ia < ib);
+          const bool up = (i & k) == 0;
+          if (up ? b_better : a_better) {
+            key[i] = kb; key[ixj] = ka;
+            idx[i] = ib; idx[ixj] = ia;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __forceinline__ int next_pow2(int x) {
+  int p = 32;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// Writes the ascending list of set bits of bm (nwords words, bit p -> value base + p) to out.
+// One warp.  Returns the count.
+__device__ int warp_bits_to_sorted(const unsigned* bm, int nwords, int base, int* out) {
+  const int lane = threadIdx.x & 31;
+  int n = 0;
+  for (int w = 0; w < nwords; ++w) {
+    const unsigned word = bm[w];
+    if (word == 0u) continue;
+    const bool set = (word >> lane) & 1u;
+    if (set) out[n + __popc(word & ((1u << lane) - 1u))] = base + w * 32 + lane;
+    n += __popc(word);
+  }
+  return n;
+}
+
+struct SelSmem {
+  double* qsum;
+  unsigned long long* key;
+  int* idx;
+  unsigned* bm_q;
+  unsigned* bm_e;
+  int* req;
+  int* reqslot;
+  int* fetch;
+  int* fpos;
+  int* victims;
+  unsigned long long* ckey;
+  int* misc;  // [16]
+};
+
+__device__ SelSmem carve_sel_smem(char* base, int D, int Pp, int C) {
+  SelSmem s;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* p = base + off;
+    off += (bytes + 15) & ~size_t(15);
+    return p;
+  };
+  s.qsum = reinterpret_cast<double*>(take(sizeof(double) * D));
+  s.key = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * Pp));
+  s.idx = reinterpret_cast<int*>(take(sizeof(int) * Pp));
+  s.bm_q = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * (Pp / 32)));
+  s.bm_e = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * (Pp / 32)));
+  s.req = reinterpret_cast<int*>(take(sizeof(int) * C));
+  s.reqslot = reinterpret_cast<int*>(take(sizeof(int) * C));
+  s.fetch = reinterpret_cast<int*>(take(sizeof(int) * C));
+  s.fpos = reinterpret_cast<int*>(take(sizeof(int) * C));
+  s.victims = reinterpret_cast<int*>(take(sizeof(int) * C));
+  s.ckey = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * C));
+  s.misc = reinterpret_cast<int*>(take(sizeof(int) * 16));
+  return s;
+}
+
+size_t sel_smem_bytes(int D, int Pp, int C) {
+  auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
+  return r(8 * D) + r(8 * (size_t)Pp) + r(4 * (size_t)Pp) + 2 * r(4 * (size_t)(Pp / 32)) +
+         5 * r(4 * (size_t)C) + r(8 * (size_t)C) + r(64);
+}
+
+enum { M_NREQ = 0, M_NF, M_SHORT, M_NCAND, M_CLOCK, M_ERR, M_NQ, M_NE };
+
+// ------------------------------------------------------------------------------------------
+// Selection phase: fills sm.req[0..n_req) (sorted) and the selection buffers.
+template <typename T>
+__device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __restrict__ q,
+                             int selector, SelSmem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int lbh = (layer * dv.B + b) * dv.H + h;
+  const int D = dv.D, n_b = dv.n_b;
+  const int t = dv.t[lbh], t0 = dv.t0[lbh];
+  const int nblk = (t + n_b - 1) / n_b;                       // BlockGeometry.n_blocks
+  const int recent_start = max(0, t0 - dv.n_w + 1);           // selection.py:49
+  const int pool_lo = dv.n_sink;                              // selection.py:59
+  const int pool_hi = max(pool_lo, recent_start / n_b);       // selection.py:60-61
+  const int P = pool_hi - pool_lo;
+  const int recent_lo = min(recent_start / n_b, nblk);        // selection.py:68-70
+  const int a_end = min(dv.n_sink, nblk);                     // sink blocks < n_blocks(t)
+  const int r_begin = max(recent_lo, a_end);
+  const int Pp = next_pow2(P);
+
+  // (1) q_sum = sum of the group's query heads (decode.py:171-172), f64
+  for (int i = tid; i < D; i += blockDim.x) {
+    double acc = 0.0;
+    for (int g = 0; g < dv.G; ++g) acc += to_f64(q[((size_t)b * dv.Hq + h * dv.G + g) * D + i]);
+    sm.qsum[i] = acc;
+  }
+  __syncthreads();
+
+  // (2) s_q = K_c[pool] . q_sum, one warp per block row, 4 rows in flight per warp
+  const double* kc = dv.kc + (size_t)lbh * dv.NB * D;
+  double* s_q_out = dv.s_q + (size_t)lbh * dv.NB;
+  for (int p0 = warp * 4; p0 < P; p0 += nwarps * 4) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int p = p0 + u;
+      if (p < P) {
+        const double* row = kc + (size_t)(pool_lo + p) * D;
+        for (int i = lane; i < D; i += 32) acc[u] = fma(row[i], sm.qsum[i], acc[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+      const int p = p0 + u;
+      if (lane == 0 && p < P) {
+        sm.key[p] = order_key(acc[u]);
+        sm.idx[p] = p;
+        s_q_out[pool_lo + p] = acc[u];
+      }
+    }
+  }
+  for (int p = P + tid; p < Pp; p += blockDim.x) {
+    sm.key[p] = 0ull;
+    sm.idx[p] = 0x7fffffff;
+  }
+  for (int w = tid; w < Pp / 32; w += blockDim.x) {
+    sm.bm_q[w] = 0u;
+    sm.bm_e[w] = 0u;
+  }
+  __syncthreads();
+
+  // (3) query-aware top-k over the pool (argtopk order)
+  if (P > 0) block_sort_best_first(sm.key, sm.idx, Pp);
+  const int m_q_eff = min(selector == 0 ? dv.m_q : dv.m_topk, P);
+  for (int r = tid; r < m_q_eff; r += blockDim.x) {
+    const int p = sm.idx[r];
+    atomicOr(&sm.bm_q[p >> 5], 1u << (p & 31));
+  }
+  __syncthreads();
+
+  // (4) NOSA: query-agnostic picks = first m_e pool blocks of the frozen s_e rank order that
+  //     were not picked by the query (selection.py:151-156)
+  if (selector == 0 && warp == 0) {
+    const int m_e_eff = min(dv.m_e, P - m_q_eff);
+    const int* rank = dv.rank_e + (size_t)lbh * dv.NB;
+    int cnt = 0;
+    for (int base = 0; base < P && cnt < m_e_eff; base += 32) {
+      const int i = base + lane;
+      const int p = (i < P) ? rank[i] : 0;
+      const bool ok = (i < P) && !((sm.bm_q[p >> 5] >> (p & 31)) & 1u);
+      const unsigned bal = __ballot_sync(0xffffffffu, ok);
+      const int pos = cnt + __popc(bal & ((1u << lane) - 1u));
+      if (ok && pos < m_e_eff) atomicOr(&sm.bm_e[p >> 5], 1u << (p & 31));
+      cnt += __popc(bal);
+    }
+  }
+  __syncthreads();
+
+  // (5) sorted outputs: blocks_q, blocks_e, required = sink U picked U recent
+  if (warp == 0) {
+    const int nw = Pp / 32;
+    int* sel_q = dv.sel_q + (size_t)lbh * dv.MQ;
+    int* sel_e = dv.sel_e + (size_t)lbh * dv.ME;
+    const int nq = warp_bits_to_sorted(sm.bm_q, nw, pool_lo, sel_q);
+    const int ne = warp_bits_to_sorted(sm.bm_e, nw, pool_lo, sel_e);
+    // merged picked list, written after the sink part of req
+    int n_picked = 0;
+    const int cap = dv.C;
+    for (int w = 0; w < nw; ++w) {
+      const unsigned word = sm.bm_q[w] | sm.bm_e[w];
+      if (word == 0u) continue;
+      if ((word >> lane) & 1u) {
+        const int pos = a_end + n_picked + __popc(word & ((1u << lane) - 1u));
+        if (pos < cap) sm.req[pos] = pool_lo + w * 32 + lane;
+      }
+      n_picked += __popc(word);
+    }
+    const int n_req = a_end + n_picked + (nblk - r_begin);
+    if (lane == 0) {
+      sm.misc[M_NREQ] = n_req;
+      sm.misc[M_NQ] = nq;
+      sm.misc[M_NE] = ne;
+      dv.n_selq[lbh] = nq;
+      dv.n_sele[lbh] = ne;
+    }
+  }
+  __syncthreads();
+  const int n_req = sm.misc[M_NREQ];
+  const int n_picked = n_req - a_end - (nblk - r_begin);
+  if (n_req <= dv.C) {
+    for (int j = tid; j < a_end; j += blockDim.x) sm.req[j] = j;
+    for (int j = r_begin + tid; j < nblk; j += blockDim.x) sm.req[a_end + n_picked + (j - r_begin)] = j;
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------------------------------
+// Planning phase on sm.req[0..n_req): plan_transfers + apply_transfers for one manager.
+__device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lbh = (layer * dv.B + b) * dv.H + h;
+  const int C = dv.C, NB = dv.NB;
+  int* slot_of = dv.slot_of + (size_t)lbh * NB;
+  int* blk_of = dv.blk_of + (size_t)lbh * C;
+  int* lastreq = dv.lastreq + (size_t)lbh * C;
+  int* fstack = dv.fstack + (size_t)lbh * C;
+  const int n_req = sm.misc[M_NREQ];
+
+  if (n_req > C) {  // CapacityExceeded (kv_manager.py:215-219): no state change
+    if (tid == 0) {
+      atomicOr(dv.err, 1u);
+      dv.n_req[lbh] = 0;
+      dv.plan_n[lbh * 3 + 0] = 0;
+      dv.plan_n[lbh * 3 + 1] = 0;
+      dv.plan_n[lbh * 3 + 2] = 0;
+    }
+    return;
+  }
+
+  // (1) clock tick, hit test, fetch list in required order (kv_manager.py:212-229)
+  if (warp == 0) {
+    const int clock = dv.clock[lbh] + 1;
+    int nf = 0;
+    for (int base = 0; base < n_req; base += 32) {
+      const int i = base + lane;
+      const int blk = (i < n_req) ? sm.req[i] : 0;
+      const int s = (i < n_req) ? slot_of[blk] : 0;
+      const bool miss = (i < n_req) && s < 0;
+      if (i < n_req && s >= 0) {
+        lastreq[s] = clock;
+        sm.reqslot[i] = s;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, miss);
+      if (miss) {
+        const int pos = nf + __popc(bal & ((1u << lane) - 1u));
+        sm.fetch[pos] = blk;
+        sm.fpos[pos] = i;
+      }
+      nf += __popc(bal);
+    }
+    if (lane == 0) {
+      dv.clock[lbh] = clock;
+      sm.misc[M_CLOCK] = clock;
+      sm.misc[M_NF] = nf;
+      sm.misc[M_SHORT] = nf - dv.ftop[lbh];  // shortfall (kv_manager.py:232)
+      sm.misc[M_NCAND] = 0;
+    }
+  }
+  __syncthreads();
+  const int nf = sm.misc[M_NF];
+  const int shortfall = sm.misc[M_SHORT];
+  const int clock = sm.misc[M_CLOCK];
+
+  // (2) victims: least-recently-required resident blocks not required now (kv_manager.py:233-246)
+  if (shortfall > 0) {
+    for (int s = tid; s < C; s += blockDim.x) {
+      const int blk = blk_of[s];
+      const bool cand = blk >= 0 && lastreq[s] != clock;
+      sm.ckey[s] = cand ? ((unsigned long long)(unsigned)lastreq[s] << 32) | (unsigned)blk
+                        : ~0ull;
+      if (cand) atomicAdd(&sm.misc[M_NCAND], 1);
+    }
+    __syncthreads();
+    for (int s = tid; s < C; s += blockDim.x) {
+      const unsigned long long mine = sm.ckey[s];
+      if (mine == ~0ull) continue;
+      int rank = 0;
+      for (int u = 0; u < C; ++u) rank += sm.ckey[u] < mine;
+      if (rank < shortfall) sm.victims[rank] = s;
+    }
+    __syncthreads();
+    if (sm.misc[M_NCAND] < shortfall) {  // cannot happen when n_req <= C; kept for parity
+      if (tid == 0) atomicOr(dv.err, 1u);
+      return;
+    }
+  }
+
+  // (3) apply: evictions push their slots (LRR order), fetches pop (required order)
+  if (warp == 0) {
+    int top = dv.ftop[lbh];
+    int* pe = dv.plan_evict + (size_t)lbh * C;
+    int* pf = dv.plan_fetch + (size_t)lbh * C;
+    const int nev = shortfall > 0 ? shortfall : 0;
+    for (int r = lane; r < nev; r += 32) {
+      const int s = sm.victims[r];
+      const int blk = blk_of[s];
+      slot_of[blk] = -1;
+      blk_of[s] = -1;
+      fstack[top + r] = s;
+      pe[r] = blk;
+    }
+    __syncwarp();
+    top += nev;
+    const int t0 = dv.t0[lbh];
+    int n_new = 0;
+    for (int f = lane; f < nf; f += 32) {
+      const int s = fstack[top - 1 - f];
+      const int blk = sm.fetch[f];
+      slot_of[blk] = s;
+      blk_of[s] = blk;
+      lastreq[s] = clock;
+      sm.reqslot[sm.fpos[f]] = s;
+      pf[f] = blk;
+      n_new += (blk * dv.n_b >= t0);  // born during the run (offload_sim.py:286-289)
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) n_new += __shfl_xor_sync(0xffffffffu, n_new, o);
+    top -= nf;
+    // enqueue the misses for the gather (K3)
+    int base = 0;
+    if (lane == 0 && nf > 0) base = atomicAdd(dv.cnt + 2 * layer, nf);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    int4* ml = dv.miss_list + (size_t)layer * dv.B * dv.H * C;
+    for (int f = lane; f < nf; f += 32) ml[base + f] = make_int4(lbh, sm.fetch[f], sm.reqslot[sm.fpos[f]], 0);
+    if (lane == 0) {
+      dv.ftop[lbh] = top;
+      long long* st = dv.stats + (size_t)lbh * ST_N;
+      st[ST_HITS] += n_req - nf;
+      st[ST_MISSES] += nf;
+      st[ST_NEW] += n_new;
+      st[ST_EVICT] += nev;
+      st[ST_STEPS] += 1;
+      dv.plan_n[lbh * 3 + 0] = nf;
+      dv.plan_n[lbh * 3 + 1] = nev;
+      dv.plan_n[lbh * 3 + 2] = n_req - nf;
+      dv.n_req[lbh] = n_req;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < n_req; i += blockDim.x) {
+    dv.req[(size_t)lbh * C + i] = sm.req[i];
+    dv.req_slot[(size_t)lbh * C + i] = sm.reqslot[i];
+  }
+}
+
+// grid = B*H, block = 256.  mode: 0 = select only, 1 = select + plan, 2 = plan on ext_req.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    select_plan_kernel(Dev dv, int layer, const T* __restrict__ q, int selector, int mode,
+                       const int* __restrict__ ext_req, const int* __restrict__ ext_nreq) {
+  extern __shared__ __align__(16) char smem_raw[];
+  const int bh = blockIdx.x;
+  const int b = bh / dv.H, h = bh % dv.H;
+  const int lbh = (layer * dv.B + b) * dv.H + h;
+  const int Pp = next_pow2(dv.NB);
+  SelSmem sm = carve_sel_smem(smem_raw, dv.D, Pp, dv.C);
+  if (threadIdx.x == 0) dv.done[layer * dv.B * dv.H + bh] = 0;  // attention split-K counter
+
+  if (mode == 2) {
+    const int n = ext_nreq[bh];
+    if (n < 0) return;  // this manager is not part of the call: no clock tick, no stats
+    if (threadIdx.x == 0) sm.misc[M_NREQ] = n;
+    for (int i = threadIdx.x; i < min(n, dv.C); i += blockDim.x) sm.req[i] = ext_req[(size_t)bh * dv.C + i];
+    __syncthreads();
+  } else {
+    select_phase<T>(dv, layer, b, h, q, selector, sm);
+  }
+  if (mode == 0) {
+    if (threadIdx.x == 0) dv.n_req[lbh] = min(sm.misc[M_NREQ], dv.C);
+    for (int i = threadIdx.x; i < min(sm.misc[M_NREQ], dv.C); i += blockDim.x)
+      dv.req[(size_t)lbh * dv.C + i] = sm.req[i];
+    return;
+  }
+  plan_phase(dv, layer, b, h, sm);
+}
+
+// ------------------------------------------------------------------------------------------
+// start_run: freeze the geometry at the current length and rank the frozen pool by the
+// query-agnostic block score (score desc, index asc).  grid = (#lbh in range), block = 256.
+__global__ void __launch_bounds__(256) start_run_kernel(Dev dv, int seq_begin, int seq_count) {
+  extern __shared__ __align__(16) char smem_raw[];
+  const int i = blockIdx.x;  // over layers x seq_count x H
+  const int h = i % dv.H;
+  const int s = (i / dv.H) % seq_count;
+  const int l = i / (dv.H * seq_count);
+  const int lbh = (l * dv.B + seq_begin + s) * dv.H + h;
+  const int t = dv.t[lbh];
+  const int recent_start = max(0, t - dv.n_w + 1);
+  const int pool_lo = dv.n_sink;
+  const int pool_hi = max(pool_lo, recent_start / dv.n_b);
+  const int P = pool_hi - pool_lo;
+  const int Pp = next_pow2(P);
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(smem_raw);
+  int* idx = reinterpret_cast<int*>(key + Pp);
+  const double* se = dv.se + (size_t)lbh * dv.NB;
+  for (int p = threadIdx.x; p < Pp; p += blockDim.x) {
+    key[p] = p < P ? order_key(se[pool_lo + p]) : 0ull;
+    idx[p] = p < P ? p : 0x7fffffff;
+  }
+  __syncthreads();
+  if (P > 0) block_sort_best_first(key, idx, Pp);
+  int* rank = dv.rank_e + (size_t)lbh * dv.NB;
+  for (int p = threadIdx.x; p < P; p += blockDim.x) rank[p] = idx[p];
+  if (threadIdx.x == 0) dv.t0[lbh] = t;
+}
+
+// ------------------------------------------------------------------------------------------
+// Standalone selector on caller-provided block scores (nosa_select / infllmv2_select).
+__global__ void __launch_bounds__(256)
+    select_scores_kernel(const double* __restrict__ s_q, const double* __restrict__ s_e,
+                         int stride, const int* __restrict__ pool_lo_a,
+                         const int* __restrict__ pool_hi_a, int m_q, int m_e, int selector,
+                         int* out_q, int* n_q, int* out_e, int* n_e, int Pp) {
+  extern __shared__ __align__(16) char smem_raw[];
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(smem_raw);
+  int* idx = reinterpret_cast<int*>(key + Pp);
+  unsigned* bm_q = reinterpret_cast<unsigned*>(idx + Pp);
+  unsigned* bm_e = bm_q + Pp / 32;
+  const int prob = blockIdx.x;
+  const int lo = pool_lo_a[prob];
+  const int P = max(0, pool_hi_a[prob] - lo);
+  const int Ps = next_pow2(P);
+  const double* sq = s_q + (size_t)prob * stride;
+  for (int p = threadIdx.x; p < Ps; p += blockDim.x) {
+    key[p] = p < P ? order_key(sq[lo + p]) : 0ull;
+    idx[p] = p < P ? p : 0x7fffffff;
+  }
+  for (int w = threadIdx.x; w < Ps / 32; w += blockDim.x) bm_q[w] = bm_e[w] = 0u;
+  __syncthreads();
+  if (P > 0) block_sort_best_first(key, idx, Ps);
+  const int mq = min(m_q, P);
+  for (int r = threadIdx.x; r < mq; r += blockDim.x) atomicOr(&bm_q[idx[r] >> 5], 1u << (idx[r] & 31));
+  __syncthreads();
+  if (selector == 0) {
+    // second phase over the rest: picked_q keys sink below every real score
+    const double* se = s_e + (size_t)prob * stride;
+    for (int p = threadIdx.x; p < Ps; p += blockDim.x) {
+      const bool picked = p < P && ((bm_q[p >> 5] >> (p & 31)) & 1u);
+      key[p] = (p < P && !picked) ? order_key(se[lo + p]) : 0ull;
+      idx[p] = (p < P && !picked) ? p : 0x7fffffff;
+    }
+    __syncthreads();
+    if (P > 0) block_sort_best_first(key, idx, Ps);
+    const int me = min(m_e, P - mq);
+    for (int r = threadIdx.x; r < me; r += blockDim.x) atomicOr(&bm_e[idx[r] >> 5], 1u << (idx[r] & 31));
+    __syncthreads();
+  }
+  if ((threadIdx.x >> 5) == 0) {
+    const int cq = warp_bits_to_sorted(bm_q, Ps / 32, lo, out_q + (size_t)prob * max(m_q, 1));
+    const int ce = warp_bits_to_sorted(bm_e, Ps / 32, lo, out_e + (size_t)prob * max(m_e, 1));
+    if ((threadIdx.x & 31) == 0) {
+      n_q[prob] = cq;
+      n_e[prob] = ce;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// host-side launchers
+cudaError_t launch_select_plan(const Dev& dv, int layer, const void* q, int selector, int mode,
+                               const int* ext_req, const int* ext_nreq, cudaStream_t st) {
+  int Pp = 32;
+  while (Pp < dv.NB) Pp <<= 1;
+  const size_t smem = sel_smem_bytes(dv.D, Pp, dv.C);
+  if (dv.dtype == 0) {
+    auto k = select_plan_kernel<__nv_bfloat16>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<dv.B * dv.H, 256, smem, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(q), selector,
+                                      mode, ext_req, ext_nreq);
+  } else {
+    auto k = select_plan_kernel<float>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<dv.B * dv.H, 256, smem, st>>>(dv, layer, static_cast<const float*>(q), selector, mode,
+                                      ext_req, ext_nreq);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_start_run(const Dev& dv, int seq_begin, int seq_count, cudaStream_t st) {
+  int Pp = 32;
+  while (Pp < dv.NB) Pp <<= 1;
+  const size_t smem = (size_t)Pp * 12;
+  cudaFuncSetAttribute(start_run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  start_run_kernel<<<dv.L * seq_count * dv.H, 256, smem, st>>>(dv, seq_begin, seq_count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select_scores(int n_prob, const double* s_q, const double* s_e, int stride,
+                                 const int* lo, const int* hi, int m_q, int m_e, int selector,
+                                 int* out_q, int* n_q, int* out_e, int* n_e, cudaStream_t st) {
+  int Pp = 32;
+  while (Pp < stride) Pp <<= 1;
+  const size_t smem = (size_t)Pp * 12 + 2 * (size_t)(Pp / 32) * 4;
+  cudaFuncSetAttribute(select_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  select_scores_kernel<<<n_prob, 256, smem, st>>>(s_q, s_e, stride, lo, hi, m_q, m_e, selector,
+                                                  out_q, n_q, out_e, n_e, Pp);
+  return cudaGetLastError();
+}
+
+}  // namespace nosa

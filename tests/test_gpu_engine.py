@@ -1,0 +1,240 @@
+"""GPU decode step (select -> cache plan -> gather -> attend -> append) against the golden
+reference runs and the CPU oracle, through the C ABI.
+
+Tolerances (north star): selected blocks and hit/miss sets bit-exact (exact ties excepted and
+reported); outputs max|o - o_ref| / max|o_ref| <= 2e-2 in bf16 storage, <= 1e-5 in fp32."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import nosa_oracle as O
+from paper_2510_13602_b200 import AttentionConfig, CapacityExceeded, NosaEngine, workload
+
+from helpers import assert_same_selection, oracle_for, rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"bf16": 2e-2, "fp32": 1e-5}
+
+
+def _cfg(row):
+    n, d, n_head, n_kv, d_head, n_b, n_s, n_w, k, k_q, k_e, excl = (int(x) for x in row)
+    return AttentionConfig(n=n, d=d, n_head=n_head, n_kv_head=n_kv, d_head=d_head, n_b=n_b, n_s=n_s, n_w=n_w,
+                           k=k, k_q=k_q, k_e=k_e, accounting="exclusive" if excl else "inclusive")
+
+
+@pytest.mark.parametrize("name", ["engine_small", "engine_small_infllmv2", "engine_cfg1"])
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_engine_vs_reference_golden(golden, name, dtype):
+    g = golden(name)
+    cfg = _cfg(g["cfg"])
+    B, t0, steps, C, seed = (int(g[k]) for k in ("batch", "t0", "steps", "fast_slots", "seed"))
+    rho, selector = float(g["rho"]), str(g["selector"])
+    w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, seed)
+    K, V = workload.prefix_kv(seed, B, cfg.n_kv_head, t0, cfg.d_head)
+    stream = workload.QueryStream(seed, 1, B, cfg.n_head, cfg.n_kv_head, cfg.d_head, rho)
+    eng = NosaEngine(cfg, batch=B, max_tokens=t0 + steps + 1, fast_slots=C, w1=w1, w2=w2, dtype=dtype)
+    eng.prefill(torch.from_numpy(K), torch.from_numpy(V), layer=0)
+    eng.start_run()
+    lo, hi = (int(x) for x in g["pool"])
+    pool = list(range(lo, hi))
+    worst = 0.0
+    for s in range(steps):
+        q, kn, vn = stream.next()
+        out = eng.step(q, kn, vn, selector=selector).cpu().numpy()
+        sels = eng.selections(0)
+        plans = eng.plans(0)
+        _, _, _, _, _, _, s_q = eng.raw_selection(0)
+        for b in range(B):
+            for h in range(cfg.n_kv_head):
+                want_q = [x for x in g["sel_q"][s, b, h] if x >= 0]
+                want_e = [x for x in g["sel_e"][s, b, h] if x >= 0]
+                sq = np.zeros(hi)
+                sq[lo:hi] = g["s_q"][s, b, h]
+                assert_same_selection(sels[b][h].blocks_q, want_q, sq, pool, f"step {s} seq {b} head {h} blocks_q")
+                assert list(sels[b][h].blocks_e) == want_e, (s, b, h)
+                assert plans[b][h].fetch == [x for x in g["fetch"][s, b, h] if x >= 0], (s, b, h)
+                assert plans[b][h].evict == [x for x in g["evict"][s, b, h] if x >= 0], (s, b, h)
+                assert plans[b][h].hits == g["hits"][s, b, h]
+                # GPU pool scores agree with the f64 reference to f64 rounding
+                np.testing.assert_allclose(s_q[b, h, lo:hi], g["s_q"][s, b, h], rtol=1e-12, atol=1e-12)
+        err = rel_err(out[0], g["outputs"][s])
+        worst = max(worst, err)
+        assert err <= TOL[dtype], f"step {s}: relative error {err:.3e} > {TOL[dtype]}"
+    # the append path wrote every token through to the slow tier
+    for b in range(B):
+        k, v = eng.read_kv(0, b, 0)
+        assert k.shape[0] == t0 + steps
+        np.testing.assert_array_equal(k[:t0], K[b, 0])
+    eng.close()
+    print(f"{name} {dtype}: worst relative output error {worst:.3e}")
+
+
+def _run_pair(cfg, *, batch, t0s, steps, fast_slots, seed, rho, selector="nosa", dtype="bf16", layers=1,
+              variant="ed-dma", check_residency=True, gather="uva"):
+    """GPU engine and oracle on identical inputs; returns the worst relative output error."""
+    w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, seed)
+    if variant == "dma":
+        w2 = w2 * 0.2
+    tmax = max(t0s)
+    cap = tmax + steps + 1
+    eng = NosaEngine(cfg, batch=batch, layers=layers, max_tokens=cap, fast_slots=fast_slots, w1=w1, w2=w2,
+                     dtype=dtype, variant=variant)
+    orc = oracle_for(cfg, batch, layers, cap, fast_slots, w1, w2, variant)
+    K, V = workload.prefix_kv(seed, batch * layers, cfg.n_kv_head, tmax, cfg.d_head)
+    K = K.reshape(layers, batch, cfg.n_kv_head, tmax, cfg.d_head)
+    V = V.reshape(layers, batch, cfg.n_kv_head, tmax, cfg.d_head)
+    for l in range(layers):
+        for b in range(batch):
+            t = t0s[b]
+            eng.prefill(torch.from_numpy(np.ascontiguousarray(K[l, b:b + 1, :, :t])),
+                        torch.from_numpy(np.ascontiguousarray(V[l, b:b + 1, :, :t])), layer=l, seq_begin=b)
+            orc.prefill(l, b, K[l, b, :, :t], V[l, b, :, :t])
+    eng.start_run()
+    orc.start_run()
+    stream = workload.QueryStream(seed, layers, batch, cfg.n_head, cfg.n_kv_head, cfg.d_head, rho)
+    worst = 0.0
+    for s in range(steps):
+        q, kn, vn = stream.next()
+        out = eng.step(q, kn, vn, selector=selector, gather=gather).cpu().numpy()
+        ref, recs = orc.step(q, kn, vn, selector)
+        for l in range(layers):
+            sels, plans = eng.selections(l), eng.plans(l)
+            _, _, _, _, req, nreq, s_q = eng.raw_selection(l)
+            for b in range(batch):
+                geom = orc.geom[b]
+                lo, hi = geom.pool
+                pool = list(range(lo, hi))
+                for h in range(cfg.n_kv_head):
+                    r = recs[l][b][h]
+                    sq = np.zeros(max(hi, 1))
+                    sq[lo:hi] = r.s_q
+                    assert_same_selection(sels[b][h].blocks_q, r.blocks_q.tolist(), sq, pool, f"l{l} s{s} b{b} h{h} q")
+                    assert list(sels[b][h].blocks_e) == r.blocks_e.tolist(), (l, s, b, h)
+                    assert req[b, h, :nreq[b, h]].tolist() == r.required, (l, s, b, h)
+                    assert plans[b][h].fetch == r.fetch, (l, s, b, h)
+                    assert plans[b][h].evict == r.evict, (l, s, b, h)
+                    assert plans[b][h].hits == r.hits
+                    np.testing.assert_allclose(s_q[b, h, lo:hi], r.s_q, rtol=1e-12, atol=1e-12)
+                    if check_residency and s == steps - 1:
+                        slot_of, block_of = eng.residency(l, b, h)
+                        want = orc.managers[l][b].slot_of[h]
+                        got = {int(blk): int(sl) for blk, sl in enumerate(slot_of) if sl >= 0}
+                        assert got == want, (l, b, h)
+        worst = max(worst, rel_err(out, ref))
+        assert worst <= TOL[dtype], f"step {s}: relative error {worst:.3e}"
+    st = eng.residency_stats()
+    ost = orc.stats()
+    assert (st.hits, st.misses, st.evictions, st.steps) == (ost["hits"], ost["misses"], ost["evictions"], ost["steps"])
+    assert st.bytes_up == st.misses * eng.bytes_per_block
+    assert (eng.lengths() == np.array([[t + steps for t in t0s]] * layers)).all()
+    eng.close()
+    return worst
+
+
+SMALL = AttentionConfig(n=4096, d=512, n_head=4, n_kv_head=2, d_head=64, n_b=16, n_s=32, n_w=128, k=512, k_q=128,
+                        k_e=384)
+ONE_B_SMALL = AttentionConfig(n=8192, d=2048, n_head=16, n_kv_head=2, d_head=128, n_b=64, n_s=64, n_w=1024, k=4096,
+                              k_q=1024, k_e=3072)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_eviction_pressure_low_locality(dtype):
+    # rho = 0: adversarial stream, fast tier barely above the requirement -> evictions every step
+    _run_pair(SMALL, batch=3, t0s=[1000, 1000, 1000], steps=12, fast_slots=36, seed=3, rho=0.0, dtype=dtype)
+
+
+def test_ragged_batch_and_partial_tails():
+    # different cache lengths per sequence, partial tail blocks, one sequence with an empty pool
+    _run_pair(SMALL, batch=4, t0s=[1000, 517, 160, 2049], steps=20, fast_slots=48, seed=4, rho=0.5)
+
+
+def test_tiny_contexts_everything_fixed():
+    # t <= n_s + n_w: the pool is empty, every cached block is attended (test_decode.py:123-134)
+    _run_pair(SMALL, batch=2, t0s=[1, 100], steps=40, fast_slots=16, seed=5, rho=0.9)
+
+
+def test_short_pool_selects_everything():
+    # pool smaller than the top-k budget (test_selection.py:109-115)
+    _run_pair(SMALL, batch=2, t0s=[300, 250], steps=6, fast_slots=40, seed=6, rho=0.3)
+
+
+@pytest.mark.parametrize("selector", ["nosa", "infllmv2"])
+def test_one_b_shape_multi_layer(selector):
+    _run_pair(ONE_B_SMALL, batch=2, t0s=[6000, 4100], steps=4, fast_slots=80, seed=7, rho=0.95, layers=2,
+              selector=selector)
+
+
+@pytest.mark.parametrize("variant", ["s-dma", "dma"])
+def test_other_eviction_variants(variant):
+    _run_pair(SMALL, batch=2, t0s=[700, 900], steps=6, fast_slots=40, seed=8, rho=0.5, variant=variant)
+
+
+def test_exclusive_accounting():
+    cfg = AttentionConfig(n=4096, d=512, n_head=8, n_kv_head=2, d_head=64, n_b=32, n_s=32, n_w=256, k=768, k_q=256,
+                          k_e=512, accounting="exclusive")
+    _run_pair(cfg, batch=2, t0s=[1500, 1200], steps=6, fast_slots=40, seed=9, rho=0.5)
+
+
+@pytest.mark.parametrize("n_b", [16, 32, 128])
+def test_block_sizes(n_b):
+    cfg = AttentionConfig(n=8192, d=1024, n_head=4, n_kv_head=2, d_head=128, n_b=n_b, n_s=n_b, n_w=4 * n_b,
+                          k=16 * n_b, k_q=4 * n_b, k_e=12 * n_b)
+    _run_pair(cfg, batch=2, t0s=[40 * n_b + 3, 30 * n_b], steps=5, fast_slots=20, seed=10, rho=0.5)
+
+
+def test_memcpy_gather_matches_uva():
+    a = _run_pair(SMALL, batch=2, t0s=[900, 800], steps=5, fast_slots=36, seed=12, rho=0.0, gather="memcpy")
+    assert a <= TOL["bf16"]
+
+
+def test_capacity_exceeded_is_raised():
+    w1, w2 = workload.eviction_head(SMALL.n_head, SMALL.d_head, 0)
+    eng = NosaEngine(SMALL, batch=1, max_tokens=1100, fast_slots=10, w1=w1, w2=w2)
+    K, V = workload.prefix_kv(0, 1, SMALL.n_kv_head, 1000, SMALL.d_head)
+    eng.prefill(torch.from_numpy(K), torch.from_numpy(V), layer=0)
+    q, kn, vn = workload.QueryStream(0, 1, 1, SMALL.n_head, SMALL.n_kv_head, SMALL.d_head, 0.5).next()
+    with pytest.raises(CapacityExceeded):
+        eng.step(q, kn, vn)
+    eng.close()
+
+
+def test_empty_cache_rejected():
+    w1, w2 = workload.eviction_head(SMALL.n_head, SMALL.d_head, 0)
+    eng = NosaEngine(SMALL, batch=1, max_tokens=100, fast_slots=10, w1=w1, w2=w2)
+    q, kn, vn = workload.QueryStream(0, 1, 1, SMALL.n_head, SMALL.n_kv_head, SMALL.d_head, 0.5).next()
+    with pytest.raises(ValueError, match="empty support"):
+        eng.step(q, kn, vn)
+    eng.close()
+
+
+def test_graph_replay_matches_eager():
+    cfg = ONE_B_SMALL
+    w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, 1)
+    K, V = workload.prefix_kv(1, 2, cfg.n_kv_head, 5000, cfg.d_head)
+    outs = []
+    for use_graph in (False, True):
+        eng = NosaEngine(cfg, batch=2, layers=1, max_tokens=5100, fast_slots=70, w1=w1, w2=w2)
+        eng.prefill(torch.from_numpy(K), torch.from_numpy(V), layer=0)
+        eng.start_run()
+        stream = workload.QueryStream(1, 1, 2, cfg.n_head, cfg.n_kv_head, cfg.d_head, 0.9)
+        dev = eng.device
+        qb = torch.empty((1, 2, cfg.n_head, cfg.d_head), dtype=torch.bfloat16, device=dev)
+        kb = torch.empty((1, 2, cfg.n_kv_head, cfg.d_head), dtype=torch.bfloat16, device=dev)
+        vb = torch.empty_like(kb)
+        ob = torch.empty((1, 2, cfg.n_head, cfg.d_head), dtype=torch.float32, device=dev)
+        res = []
+        for s in range(6):
+            q, kn, vn = stream.next()
+            qb.copy_(torch.from_numpy(q)); kb.copy_(torch.from_numpy(kn)); vb.copy_(torch.from_numpy(vn))
+            if use_graph:
+                if s == 0:
+                    eng.capture(qb, kb, vb, ob)
+                eng.replay()
+            else:
+                eng.step(qb, kb, vb, out=ob)
+            res.append(ob.cpu().numpy().copy())
+        outs.append(np.stack(res))
+        eng.close()
+    np.testing.assert_array_equal(outs[0], outs[1])  # same kernels, same decomposition: bitwise equal

@@ -1,0 +1,82 @@
+"""The CPU oracle against the golden fixtures generated from the unmodified reference
+(tests/golden/make_golden.py).  This pins the oracle before any GPU result is compared with it."""
+
+import numpy as np
+import pytest
+
+from oracle import nosa_oracle as O
+
+
+def _cfg(row):
+    n, d, n_head, n_kv, d_head, n_b, n_s, n_w, k, k_q, k_e, excl = (int(x) for x in row)
+    return dict(n=n, d=d, n_head=n_head, n_kv_head=n_kv, d_head=d_head, n_b=n_b, n_s=n_s, n_w=n_w, k=k, k_q=k_q,
+                k_e=k_e, accounting="exclusive" if excl else "inclusive")
+
+
+def test_selection_kats_bit_exact(golden):
+    g = golden("selection_kats")
+    for i in range(len(g["t"])):
+        c = _cfg(g["cfg_rows"][g["cfg"][i]])
+        t, nblk = int(g["t"][i]), int(g["nblk"][i])
+        s_q, s_e = g["s_q"][i][:nblk], g["s_e"][i][:nblk]
+        geom = O.Geometry.for_run(c["n_b"], c["n_s"], c["n_w"], t)
+        m_q, m_e, m_topk = O.budgets(c["n_b"], c["n_s"], c["n_w"], c["k"], c["k_q"], c["k_e"], c["accounting"])
+        bq, be = O.select(s_q, s_e, geom, m_q, m_e, "nosa")
+        want = lambda key: [x for x in g[key][i] if x >= 0]
+        assert bq.tolist() == want("nosa_q"), i
+        assert be.tolist() == want("nosa_e"), i
+        assert geom.fixed(t) == want("fixed"), i
+        iq, _ = O.select(s_q, None, geom, m_topk, 0, "infllmv2")
+        assert iq.tolist() == want("inf_q"), i
+
+
+def test_manager_trace_bit_exact(golden):
+    g = golden("manager_trace")
+    C = int(g["capacity"])
+    steps, H, _ = g["req"].shape
+    mgr = O.SequenceManager(H, C)
+    for s in range(steps):
+        for h in range(H):
+            req = [x for x in g["req"][s, h] if x >= 0]
+            fetch, evict, hits = mgr.plan_apply(req, h)
+            assert fetch == [x for x in g["fetch"][s, h] if x >= 0], (s, h)
+            assert evict == [x for x in g["evict"][s, h] if x >= 0], (s, h)
+            assert hits == g["hits"][s, h]
+            assert [mgr.slot_of[h][b] for b in req] == [x for x in g["slots"][s, h] if x >= 0]
+    hits, misses, _, calls = g["stats"]
+    assert (mgr.hits, mgr.misses, mgr.steps) == (hits, misses, calls)
+
+
+@pytest.mark.parametrize("name", ["engine_small", "engine_small_infllmv2", "engine_cfg1"])
+def test_engine_matches_reference(golden, name):
+    from paper_2510_13602_b200 import workload
+    g = golden(name)
+    c = _cfg(g["cfg"])
+    B, t0, steps, C, seed = (int(g[k]) for k in ("batch", "t0", "steps", "fast_slots", "seed"))
+    rho, selector = float(g["rho"]), str(g["selector"])
+    oc = O.OracleConfig(c["n_head"], c["n_kv_head"], c["d_head"], c["n_b"], c["n_s"], c["n_w"], c["k"], c["k_q"],
+                        c["k_e"], c["accounting"])
+    w1, w2 = workload.eviction_head(c["n_head"], c["d_head"], seed)
+    K, V = workload.prefix_kv(seed, B, c["n_kv_head"], t0, c["d_head"])
+    stream = workload.QueryStream(seed, 1, B, c["n_head"], c["n_kv_head"], c["d_head"], rho)
+    eng = O.OracleEngine(oc, B, 1, t0 + steps + 1, C, w1, w2)
+    for b in range(B):
+        eng.prefill(0, b, K[b], V[b])
+    eng.start_run()
+    lo, hi = (int(x) for x in g["pool"])
+    for s in range(steps):
+        q, kn, vn = stream.next()
+        out, recs = eng.step(q, kn, vn, selector)
+        for b in range(B):
+            for h in range(c["n_kv_head"]):
+                r = recs[0][b][h]
+                assert r.blocks_q.tolist() == [x for x in g["sel_q"][s, b, h] if x >= 0], (s, b, h)
+                assert r.blocks_e.tolist() == [x for x in g["sel_e"][s, b, h] if x >= 0], (s, b, h)
+                assert r.fetch == [x for x in g["fetch"][s, b, h] if x >= 0], (s, b, h)
+                assert r.evict == [x for x in g["evict"][s, b, h] if x >= 0], (s, b, h)
+                assert r.hits == g["hits"][s, b, h]
+                np.testing.assert_allclose(r.s_q, g["s_q"][s, b, h], rtol=1e-12, atol=1e-12)
+                if s == 0:
+                    np.testing.assert_allclose(r.s_e_c, g["s_e_pool"][b, h], rtol=1e-12, atol=1e-14)
+        tol = 1e-6 if g["outputs"].dtype == np.float32 else 1e-10
+        np.testing.assert_allclose(out[0], g["outputs"][s], rtol=0, atol=tol)
