@@ -1,0 +1,475 @@
+#!/usr/bin/env python
+"""Batched NOSA offloaded sparse-attention decode throughput on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg3] [--impl native|reference]
+
+A step is one decode step of every sequence through every layer: per layer, selection + cache
+plan (K1+K2), miss gather pinned-host -> HBM (K3, side stream), block-sparse attention + append
+(K4+K5).  Default workload = BASELINE config 3: 1B-class attention shape (16 q / 2 kv heads,
+d_head 128, 28 layers), 32K context, batch 128 per GPU, HBM cache holding 25% of the KV blocks
+(128 slots per sequence and head), rest in pinned host memory, high-locality AR(1) query stream.
+
+Under torchrun each rank owns its own batch shard, host KV pool and PCIe link (no data-path
+collective; one barrier + max-over-ranks timing reduce).  `--impl reference` times the
+reference CPU algorithm (the oracle port, oracle/nosa_oracle.py) on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "batched decode tokens/s at 32K ctx w/ KV offload; H2D miss GB/s; % roofline"
+MODEL = "1B-class NOSA attention (16 q / 2 kv heads, d_head 128, block 64, k 4096, k_q 1024)"
+
+WORKLOADS = {
+    "cfg1": dict(desc="single NOSA sparse-attention decode layer, batch 4, 8q/2kv, d128, 8K ctx, block 64, top-k 16",
+                 shape="cfg1", layers=1, batch=4, context=8192, cache="resident", rho=0.95),
+    "cfg2": dict(desc="1B-class shape, 28 layers, batch 32, 16K ctx, all KV resident in HBM, high locality",
+                 shape="1b", layers=28, batch=32, context=16384, cache="resident", rho=0.95),
+    "cfg3": dict(desc="1B-class shape, 28 layers, 32K ctx, batch 128, HBM cache = 25% of KV blocks, rest pinned host",
+                 shape="1b", layers=28, batch=128, context=32768, cache=0.25, rho=0.95),
+    "cfg4": dict(desc="1B-class shape, 28 layers, 32K ctx, batch 128, 25% HBM cache, adversarial random queries (rho=0)",
+                 shape="1b", layers=28, batch=128, context=32768, cache=0.25, rho=0.0),
+    "cfg5": dict(desc="1B-class shape, 64K ctx, batch 512 total batch-sharded over GPUs, 25% HBM cache, per-GPU host pools",
+                 shape="1b", layers=28, batch=512, context=65536, cache=0.25, rho=0.95, strong=True),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["native", "reference"], default="native")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
+    ap.add_argument("--selector", choices=["nosa", "infllmv2"], default="nosa")
+    ap.add_argument("--layers", type=int, default=None, help="override (for quick local checks only)")
+    ap.add_argument("--batch", type=int, default=None, help="override (for quick local checks only)")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--gather", choices=["uva", "memcpy"], default="uva")
+    ap.add_argument("--cpu-pairs", type=int, default=8, help="(sequence, layer) pairs in the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def attention_config(shape):
+    from paper_2510_13602_b200 import cfg1_config, one_b_config
+    return cfg1_config() if shape == "cfg1" else one_b_config(65536)
+
+
+def workload_dims(args, world):
+    w = dict(WORKLOADS[args.workload])
+    if args.layers:
+        w["layers"] = args.layers
+    if args.batch:
+        w["batch"] = args.batch
+    w["batch_local"] = w["batch"] // world if w.get("strong") else w["batch"]
+    w["global_batch"] = w["batch"] if w.get("strong") else w["batch"] * world
+    return w
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------------ native arm
+def measure_link_gbs(torch, device):
+    x = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+    y = torch.empty(1 << 30, dtype=torch.uint8, device=device)
+    for _ in range(2):
+        y.copy_(x, non_blocking=True)
+    torch.cuda.synchronize(device)
+    best = 0.0
+    for _ in range(10):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); y.copy_(x, non_blocking=True); b.record(); b.synchronize()
+        best = max(best, (1 << 30) / (a.elapsed_time(b) * 1e-3) / 1e9)
+    del x, y
+    return best
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"], "measured"
+    return 6650.0, "fallback"
+
+
+def run_native(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_13602_b200 import NosaEngine, workload
+
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    w = workload_dims(args, world)
+    cfg = attention_config(w["shape"])
+    L, B, ctx_len = w["layers"], w["batch_local"], w["context"]
+    total_steps = args.warmup + args.steps * (1 if args.no_e2e else 2)
+    max_tokens = ctx_len + total_steps + 2
+    nblk = -(-max_tokens // cfg.n_b)
+    fast = nblk if w["cache"] == "resident" else int(w["cache"] * nblk)
+    dtype = torch.bfloat16
+    link_gbs = measure_link_gbs(torch, device)
+
+    w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, args.seed)
+    t_setup = time.time()
+    eng = NosaEngine(cfg, batch=B, layers=L, max_tokens=max_tokens, fast_slots=fast, w1=w1, w2=w2, dtype="bf16",
+                     device=local_rank)
+    t_alloc = time.time() - t_setup
+    seed_base = args.seed * 1000003 + rank * 7919
+    for l in range(L):
+        shape = (B, cfg.n_kv_head, ctx_len, cfg.d_head)
+        k = workload.torch_prefix_kv(seed_base + 2 * l, shape, device, dtype)
+        v = workload.torch_prefix_kv(seed_base + 2 * l + 1, shape, device, dtype)
+        eng.prefill(k, v, layer=l)
+        del k, v
+    eng.start_run()
+    torch.cuda.synchronize(device)
+    t_prefill = time.time() - t_setup - t_alloc
+
+    stream = workload.TorchQueryStream(seed_base + 99991, L, B, cfg.n_head, cfg.n_kv_head, cfg.d_head, w["rho"],
+                                       device, dtype)
+    inputs = [stream.next() for _ in range(total_steps)]
+    out = torch.empty((L, B, cfg.n_head, cfg.d_head), dtype=torch.float32, device=device)
+    warm_out = []
+    for i in range(args.warmup):
+        q, kn, vn = inputs[i]
+        eng.step(q, kn, vn, selector=args.selector, out=out, gather=args.gather)
+        warm_out.append(out.clone())
+    torch.cuda.synchronize(device)
+    eng.reset_stats()
+
+    # ---------------- timed region (value): inputs resident in HBM
+    eng.timing_enable(3 * L * args.steps + 8)
+    launches0 = eng.launch_count
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        ev0.record()
+        for i in range(args.warmup, args.warmup + args.steps):
+            q, kn, vn = inputs[i]
+            eng.step(q, kn, vn, selector=args.selector, out=out, gather=args.gather, check=False)
+        ev1.record()
+        torch.cuda.synchronize(device)
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = eng.launch_count - launches0
+    kern = eng.timing_read()
+    eng.check_errors()
+    st = eng.residency_stats()
+    ms_t = torch.tensor([ms], device=device)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    tokens = B * world * args.steps if not w.get("strong") else w["global_batch"] * args.steps
+
+    # ---------------- end to end: host inputs H2D + step + D2H of the outputs, every step
+    e2e = None
+    if not args.no_e2e:
+        host_in = [tuple(x.cpu().pin_memory() for x in inputs[i])
+                   for i in range(args.warmup + args.steps, args.warmup + 2 * args.steps)]
+        dq, dk, dv = (torch.empty_like(x) for x in inputs[0])
+        host_out = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for hq, hk, hv in host_in:
+            dq.copy_(hq, non_blocking=True); dk.copy_(hk, non_blocking=True); dv.copy_(hv, non_blocking=True)
+            eng.step(dq, dk, dv, selector=args.selector, out=out, gather=args.gather, check=False)
+            host_out.copy_(out, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize(device)
+        e_ms = torch.tensor([e0.elapsed_time(e1)], device=device)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        h2d = sum(x.numel() * x.element_size() for x in host_in[0])
+        e2e = {"value": round(tokens / (float(e_ms.item()) * 1e-3), 2), "unit": "tokens/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": host_out.numel() * 4,
+               "ms_per_step": round(float(e_ms.item()) / args.steps, 4),
+               "api": "NosaEngine.step (C ABI nosa_decode_step) on host-copied inputs"}
+        eng.check_errors()
+
+    # ---------------- roofline arithmetic (algorithmic bytes, SURVEY.md §8d / DESIGN.md)
+    hbm_peak, peak_kind = peaks()
+    bpb = eng.bytes_per_block
+    calls = L * args.steps  # launches per kernel kind in the timed region
+    R_total = st.hits + st.misses                     # attended blocks, summed
+    P = eng.geometry[0].pool_blocks.stop - eng.geometry[0].pool_blocks.start
+    per_launch = {
+        # K1+K2: f64 K_c pool scan + q read + tables (reads of required-list metadata are small)
+        "select_plan": (B * cfg.n_kv_head * P * cfg.d_head * 8 + B * cfg.n_head * cfg.d_head * 2),
+        # K3: each missed block crosses PCIe once and is written to HBM once
+        "gather": st.misses * bpb / calls,
+        # K4+K5: K|V of every attended block + its bias + q in + f32 out + append row
+        "attend": (R_total * (bpb + 4)) / calls + B * cfg.n_head * cfg.d_head * (2 + 4)
+                  + B * cfg.n_kv_head * 2 * cfg.d_head * 2,
+    }
+    for k_ in kern:
+        kern[k_]["bytes_per_launch"] = per_launch[k_]
+        kern[k_]["gbs"] = per_launch[k_] / (kern[k_]["avg_ms"] * 1e-3) / 1e9 if kern[k_]["avg_ms"] else None
+    traffic = None
+    tpath = ROOT / "profiles" / "traffic.json"
+    if tpath.exists():
+        traffic = json.loads(tpath.read_text()).get(f"{args.workload}:attend")
+    att = kern["attend"]
+    roofline = {"bound": "hbm", "kernel": "attend_bf16_kernel (K4+K5)", "achieved": round(att["gbs"], 1),
+                "peak": hbm_peak, "unit": "GB/s", "frac": round(att["gbs"] / hbm_peak, 4), "traffic": traffic,
+                "peak_kind": peak_kind, "bytes_per_launch": int(per_launch["attend"]),
+                "avg_launch_ms": round(att["avg_ms"], 5)}
+    hbm_step = (per_launch["select_plan"] + per_launch["attend"] + per_launch["gather"]) * L
+    h2d_step = st.misses * bpb / args.steps
+    t_roof = max(hbm_step / 8e12, h2d_step / (link_gbs * 1e9))
+    step_ms = ms_max / args.steps
+    g = kern["gather"]
+    link_roofline = {"bound": "pcie-h2d", "kernel": "gather_kernel (K3, UVA zero-copy)",
+                     "achieved": round(g["gbs"], 2) if g["gbs"] else 0.0, "peak": round(link_gbs, 2), "unit": "GB/s",
+                     "frac": round(g["gbs"] / link_gbs, 4) if g["gbs"] else 0.0,
+                     "peak_kind": "measured pinned 1 GiB H2D cudaMemcpyAsync, best of 10"}
+    step_roofline = {"definition": "t_roof = max(HBM bytes / 8 TB/s, H2D miss bytes / measured link GB/s)",
+                     "hbm_bytes_per_step": int(hbm_step), "h2d_bytes_per_step": int(h2d_step),
+                     "t_roof_ms": round(t_roof * 1e3, 4), "t_step_ms": round(step_ms, 4),
+                     "frac": round(t_roof * 1e3 / step_ms, 4),
+                     "bound": "h2d" if h2d_step / (link_gbs * 1e9) > hbm_step / 8e12 else "hbm",
+                     "frac_at_measured_hbm": round(max(hbm_step / (hbm_peak * 1e9), h2d_step / (link_gbs * 1e9))
+                                                   * 1e3 / step_ms, 4)}
+
+    # ---------------- CPU baseline: the oracle (reference algorithm) on a bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(args, eng, cfg, w, inputs, warm_out, seed_base, device, fast, max_tokens)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(tokens / (ms_max * 1e-3), 2), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
+            "higher_is_better": True, "scaling": "strong" if w.get("strong") else "weak", "vs_baseline": None,
+            "dtype": "bf16",
+            "data": f"synthetic: K/V ~ N(0,1) bf16, AR(1) queries rho={w['rho']} (torch Philox, seed {args.seed})",
+            "config": {"workload": f"{args.workload}: {w['desc']}", "model": MODEL, "global_batch": w["global_batch"],
+                       "seq_len": ctx_len, "layers": L, "selector": args.selector,
+                       "fast_slots_per_seq_head": fast, "blocks_per_seq_head": nblk,
+                       "parallelism": f"dp{world} (batch-sharded, no data-path collective)",
+                       "gather": args.gather,
+                       "l2": "no flush needed: attended KV per layer-step exceeds the 126 MB L2"},
+            "h2d_miss_gbs": round(h2d_step / (step_ms * 1e-3) / 1e9, 3),
+            "hit_rate": round(st.hit_rate, 4),
+            "misses_per_seq_head_step": round(st.misses / (B * cfg.n_kv_head * L * args.steps), 3),
+            "attended_blocks_per_seq_head": round(R_total / (B * cfg.n_kv_head * L * args.steps), 2),
+            "link_gbs_measured": round(link_gbs, 2),
+            "roofline": roofline, "link_roofline": link_roofline, "step_roofline": step_roofline,
+            "kernels": {k_: {"avg_ms": round(v["avg_ms"], 5), "launches": v["launches"],
+                             "gbs": round(v["gbs"], 2) if v["gbs"] else None} for k_, v in kern.items()},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "setup_s": {"alloc_and_pin": round(t_alloc, 1), "prefill": round(t_prefill, 1)},
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+
+
+def cpu_baseline_sample(args, eng, cfg, w, inputs, warm_out, seed_base, device, fast, max_tokens):
+    """Replay the warm-up steps of a few (sequence, layer) pairs through the oracle on one host
+    core, with the identical inputs, timing it and checking the GPU outputs on the way."""
+    import numpy as np
+    import torch
+
+    from oracle import nosa_oracle as O
+    from paper_2510_13602_b200 import workload
+
+    L, B = w["layers"], w["batch_local"]
+    rng = np.random.default_rng(5)
+    pairs = [(int(rng.integers(L)), int(rng.integers(B))) for _ in range(args.cpu_pairs)]
+    oc = O.OracleConfig.from_attention_config(cfg)
+    w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, args.seed)
+    steps = args.warmup
+    worst, sel_ok, prefill_s, step_s = 0.0, True, 0.0, 0.0
+    for (l, b) in pairs:
+        shape = (B, cfg.n_kv_head, w["context"], cfg.d_head)
+        k = workload.torch_prefix_kv(seed_base + 2 * l, shape, device, torch.bfloat16)[b].float().cpu().numpy()
+        v = workload.torch_prefix_kv(seed_base + 2 * l + 1, shape, device, torch.bfloat16)[b].float().cpu().numpy()
+        orc = O.OracleEngine(oc, 1, 1, max_tokens, fast, w1, w2, store_payload=True)
+        t0 = time.perf_counter()
+        orc.prefill(0, 0, k, v)
+        orc.start_run()
+        t1 = time.perf_counter()
+        for s in range(steps):
+            q, kn, vn = (x[l, b].float().cpu().numpy() for x in inputs[s])
+            ts = time.perf_counter()
+            ref, _ = orc.step_seq(0, 0, q, kn, vn, args.selector)
+            step_s += time.perf_counter() - ts
+            got = warm_out[s][l, b].cpu().numpy()
+            worst = max(worst, float(np.max(np.abs(got - ref)) / np.max(np.abs(ref))))
+        prefill_s += t1 - t0
+    per_pair_step = step_s / (len(pairs) * steps)
+    return {"value": round(1.0 / (L * per_pair_step), 4), "unit": "tokens/s", "cores": 1, "kind": "port",
+            "sample": f"{len(pairs)} random (sequence, layer) pairs x {steps} decode steps of the oracle "
+                      f"(DecodeEngine.step re-pooling K every step + per-sequence TieredBlockManager with 32 KiB "
+                      f"payload copies), one host core; tokens/s = 1 / (layers x seconds per pair-step)",
+            "seconds_per_pair_step": round(per_pair_step, 5), "prefill_seconds_per_pair": round(prefill_s / len(pairs), 3),
+            "gpu_vs_oracle_max_rel_err": worst}
+
+
+# ------------------------------------------------------------------------------ reference arm
+def _ref_worker(conn, cfg_d, layers, context, max_tokens, fast, rho, seed, selector):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    import numpy as np
+    from oracle import nosa_oracle as O
+    from paper_2510_13602_b200 import workload
+    oc = O.OracleConfig(**cfg_d)
+    w1, w2 = workload.eviction_head(oc.n_head, oc.d_head, 0)
+    K, V = workload.prefix_kv(seed, 1, oc.n_kv_head, context, oc.d_head)
+    orc = O.OracleEngine(oc, 1, 1, max_tokens, fast, w1, w2, store_payload=True)
+    orc.prefill(0, 0, K[0], V[0])
+    orc.start_run()
+    stream = workload.QueryStream(seed, 1, 1, oc.n_head, oc.n_kv_head, oc.d_head, rho)
+    conn.send("ready")
+    while True:
+        cmd = conn.recv()
+        if cmd == "stop":
+            break
+        q, kn, vn = stream.next()
+        orc.step_seq(0, 0, q[0, 0], kn[0, 0], vn[0, 0], selector)
+        conn.send("done")
+
+
+def run_reference(args, rank, world):
+    import multiprocessing as mp
+
+    from paper_2510_13602_b200 import workload  # noqa: F401  (same generator as the native arm)
+    if rank != 0:
+        return
+    w = workload_dims(args, world)
+    cfg = attention_config(w["shape"])
+    cores = len(os.sched_getaffinity(0))
+    max_tokens = w["context"] + args.warmup + args.steps + 2
+    nblk = -(-max_tokens // cfg.n_b)
+    fast = nblk if w["cache"] == "resident" else int(w["cache"] * nblk)
+    cfg_d = dict(n_head=cfg.n_head, n_kv_head=cfg.n_kv_head, d_head=cfg.d_head, n_b=cfg.n_b, n_s=cfg.n_s,
+                 n_w=cfg.n_w, k=cfg.k, k_q=cfg.k_q, k_e=cfg.k_e, accounting=cfg.accounting)
+    ctx = mp.get_context("spawn")
+    procs, conns = [], []
+    for i in range(cores):
+        a, b = ctx.Pipe()
+        p = ctx.Process(target=_ref_worker, args=(b, cfg_d, w["layers"], w["context"], max_tokens, fast, w["rho"],
+                                                  args.seed * 1000 + i, args.selector), daemon=True)
+        p.start()
+        procs.append(p)
+        conns.append(a)
+    for c in conns:
+        assert c.recv() == "ready"
+
+    def one_step():
+        for c in conns:
+            c.send("step")
+        for c in conns:
+            assert c.recv() == "done"
+
+    for _ in range(args.warmup):
+        one_step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one_step()
+    dt = time.perf_counter() - t0
+    for c in conns:
+        c.send("stop")
+    for p in procs:
+        p.join(timeout=10)
+    # each step advanced `cores` (sequence, layer) pairs of the B x L a full decode step needs
+    L, B = w["layers"], w["global_batch"]
+    step_s_full = dt / args.steps * (B * L) / cores
+    value = B / step_s_full
+    sample = (f"each step = {cores} (sequence, layer) pairs of the {B} x {L} workload, one per host core "
+              f"(multiprocessing, OPENBLAS_NUM_THREADS=1), extrapolated linearly to the full step")
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s_full * 1e3, 2),
+            "higher_is_better": True, "scaling": "strong" if w.get("strong") else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": f"synthetic: K/V ~ N(0,1) bf16-representable, AR(1) queries rho={w['rho']} (numpy PCG64)",
+            "config": {"workload": f"{args.workload}: {w['desc']}", "model": MODEL, "global_batch": B,
+                       "seq_len": w["context"], "layers": L, "selector": args.selector,
+                       "fast_slots_per_seq_head": fast, "parallelism": f"{cores} host processes"},
+            "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_native(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

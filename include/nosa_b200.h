@@ -216,6 +216,13 @@ int nosa_read_lengths(NosaCtx* ctx, int32_t* t /* [layers][batch] */);
 /* synchronises; returns NOSA_ERR_CAPACITY etc. if a kernel latched an error, and clears it */
 int nosa_check_errors(NosaCtx* ctx, uint32_t* flags);
 
+/* Device timing of every kernel of subsequent eager steps, bracketed by CUDA events on the
+ * stream each kernel runs on (bench evidence).  Kinds: 0 = select+plan (K1+K2), 1 = gather (K3),
+ * 2 = attend+append (K4+K5).  enable(0) turns it off; read synchronises and returns the summed
+ * milliseconds and launch counts per kind since enable. */
+int nosa_timing_enable(NosaCtx* ctx, int max_launches);
+int nosa_timing_read(NosaCtx* ctx, double* total_ms /* [3] */, int64_t* launches /* [3] */);
+
 /* kernel launches issued by this library since context creation (bench evidence) */
 int64_t nosa_launch_count(const NosaCtx* ctx);
 

@@ -82,6 +82,8 @@ SIGNATURES = {
     "nosa_read_lengths": (_I, [_P, _I32P]),
     "nosa_check_errors": (_I, [_P, ctypes.POINTER(ctypes.c_uint32)]),
     "nosa_launch_count": (ctypes.c_int64, [_P]),
+    "nosa_timing_enable": (_I, [_P, _I]),
+    "nosa_timing_read": (_I, [_P, _F64P, ctypes.POINTER(ctypes.c_int64)]),
 }
 
 

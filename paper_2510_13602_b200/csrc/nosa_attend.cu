@@ -573,8 +573,10 @@ __global__ void __launch_bounds__(32)
 template <int NBK, int DH>
 static cudaError_t launch_bf16(const Dev& dv, int layer, const void* q, const void* kn,
                                const void* vn, float* out, cudaStream_t st, int num_sms) {
-  constexpr int NW = 2, NS = 3;
   constexpr int BPB = 2 * NBK * DH * 2;
+  // ~192 KiB of stages per CTA (one CTA per SM): 3 stages per warp, as many warps as fit
+  constexpr int NS = 3;
+  constexpr int NW = BPB >= 65536 ? 1 : (BPB >= 32768 ? 2 : 4);
   const int BH = dv.B * dv.H;
   const size_t smem = (size_t)NW * NS * BPB + NW * NS * 8 + (BH + 1) * 4 + NW * (NS + 2) * 4 + NW * 32 * 4 + 64;
   auto k = attend_bf16_kernel<NBK, DH, NW, NS>;

@@ -53,6 +53,9 @@ struct NosaCtx {
   cudaGraphExec_t graph_exec = nullptr;
   cudaStream_t capture_stream = nullptr;
   int graph_kernels = 0;
+  struct Timed { cudaEvent_t a, b; int kind; };
+  std::vector<Timed> timing;       // pre-created event pairs
+  size_t timing_used = 0;
   std::atomic<long long> launches{0};
   std::string err;
 };
@@ -152,6 +155,10 @@ static void release(NosaCtx* ctx) {
   for (auto e : ctx->ev_plan) cudaEventDestroy(e);
   for (auto e : ctx->ev_gather) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  for (auto& t : ctx->timing) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
   for (void* p : ctx->dev_allocs) cudaFree(p);
   if (ctx->staging) cudaFree(ctx->staging);
   if (ctx->host_mirror) {
@@ -475,6 +482,59 @@ extern "C" int nosa_attend(NosaCtx* ctx, int layer, const void* q, const void* k
   return NOSA_OK;
 }
 
+// brackets one launch with timing events when timing is enabled (eager steps only)
+struct TimeScope {
+  NosaCtx* ctx;
+  cudaStream_t st;
+  NosaCtx::Timed* slot = nullptr;
+  TimeScope(NosaCtx* c, cudaStream_t s, int kind, bool on) : ctx(c), st(s) {
+    if (on && ctx->timing_used < ctx->timing.size()) {
+      slot = &ctx->timing[ctx->timing_used++];
+      slot->kind = kind;
+      cudaEventRecord(slot->a, st);
+    }
+  }
+  ~TimeScope() {
+    if (slot) cudaEventRecord(slot->b, st);
+  }
+};
+
+extern "C" int nosa_timing_enable(NosaCtx* ctx, int max_launches) {
+  if (!ctx || max_launches < 0) return NOSA_ERR_VALUE;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (auto& t : ctx->timing) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  ctx->timing.clear();
+  ctx->timing_used = 0;
+  for (int i = 0; i < max_launches; ++i) {
+    NosaCtx::Timed t{};
+    CUDA_TRY(ctx, cudaEventCreate(&t.a));
+    CUDA_TRY(ctx, cudaEventCreate(&t.b));
+    ctx->timing.push_back(t);
+  }
+  return NOSA_OK;
+}
+
+extern "C" int nosa_timing_read(NosaCtx* ctx, double* total_ms, int64_t* launches) {
+  if (!ctx || !total_ms || !launches) return NOSA_ERR_VALUE;
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaDeviceSynchronize());
+  for (int k = 0; k < 3; ++k) {
+    total_ms[k] = 0.0;
+    launches[k] = 0;
+  }
+  for (size_t i = 0; i < ctx->timing_used; ++i) {
+    float ms = 0.0f;
+    CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->timing[i].a, ctx->timing[i].b));
+    total_ms[ctx->timing[i].kind] += ms;
+    launches[ctx->timing[i].kind] += 1;
+  }
+  return NOSA_OK;
+}
+
 static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, bool count) {
   const Dev& dv = ctx->dv;
   const size_t qstride = (size_t)dv.B * dv.Hq * dv.D * dv.elem;
@@ -484,17 +544,25 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   const char* kn = static_cast<const char*>(io->k_new);
   const char* vn = static_cast<const char*>(io->v_new);
   CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt, 0, (size_t)dv.L * 2 * sizeof(int), st));
+  const bool timed = count;  // eager steps only (never inside a graph capture)
   for (int l = 0; l < dv.L; ++l) {
-    CUDA_TRY(ctx, nosa::launch_select_plan(dv, l, q + l * qstride, io->selector, 1, nullptr, nullptr, st));
+    {
+      TimeScope ts(ctx, st, 0, timed);
+      CUDA_TRY(ctx, nosa::launch_select_plan(dv, l, q + l * qstride, io->selector, 1, nullptr, nullptr, st));
+    }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[l], st));
   }
   for (int l = 0; l < dv.L; ++l) {
     CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_plan[l], 0));
-    CUDA_TRY(ctx, nosa::launch_gather(dv, l, ctx->copy_stream, ctx->gather_grid));
+    {
+      TimeScope ts(ctx, ctx->copy_stream, 1, timed);
+      CUDA_TRY(ctx, nosa::launch_gather(dv, l, ctx->copy_stream, ctx->gather_grid));
+    }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[l], ctx->copy_stream));
   }
   for (int l = 0; l < dv.L; ++l) {
     CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_gather[l], 0));
+    TimeScope ts(ctx, st, 2, timed);
     CUDA_TRY(ctx, nosa::launch_attend(dv, l, q + l * qstride, kn + l * kstride, vn + l * kstride,
                                       io->out + l * ostride, st, ctx->num_sms));
   }
