@@ -7,31 +7,36 @@
 // attention.py:149-164), then w.V.  Masked tokens (outside Gamma(t)) contribute exactly zero,
 // so only the required blocks are read; the partial tail block is clipped at t
 // (selection.py:104-107).  After attention the new token is appended (decode.py:187-189) with
-// its ed-dma importance score (importance_scores, attention.py:121-146).
+// its importance score (importance_scores, attention.py:121-146).
 //
-// Work decomposition: each (b, h) required list is cut into chunks of kChunk blocks (fixed
-// split, so results do not depend on grid size or batch composition).  A persistent grid of
-// warps claims chunks from a per-layer counter; every warp streams its blocks through a
-// private ring of shared-memory stages filled by 1-D TMA bulk copies (cp.async.bulk, one
-// 32 KiB K|V block per copy, mbarrier completion).  bf16: QK^T and PV on tensor cores
-// (mma.m16n8k16, queries on M padded to 16, keys/dims on N), online softmax in registers.
-// The last warp to finish a (b, h) merges the chunk partials in chunk order (log-sum-exp) and
-// performs the append, so no other warp can still be reading the tail block.
+// Work decomposition: each (b, h) required list is cut into chunks of kChunk blocks (a fixed
+// split, so results do not depend on the grid, the batch composition or the GPU count).
+// bf16 kernel, one persistent CTA per SM, warp-specialised:
+//   scheduler warp  claims chunks from a per-layer counter and stages their metadata (slot,
+//                   token count, block bias) in a shared-memory queue;
+//   copy warp       streams each 32 KiB K|V block HBM -> shared memory with one 1-D TMA bulk
+//                   copy (cp.async.bulk, SASS UBLKCP) into a ring of stages (mbarrier
+//                   full/empty pairs), plus the chunk's query rows;
+//   4 consumer warps split every block by keys (16 keys each) and run QK^T and PV on the
+//                   tensor cores with keys on M and the GQA group's queries on N
+//                   (mma.m16n8k16, no padding for G = 8), online softmax in registers.
+// At a chunk end the consumer warps combine their partials through shared memory and write
+// one (m, l, O) record; the CTA finishing the last chunk of a (b, h) merges the records in
+// chunk order (log-sum-exp) and performs the append, so no warp can still be reading the
+// tail block.
 #include "nosa_device.cuh"
 
 namespace nosa {
 
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kBarConsumers = 1;  // named barrier id of the consumer warps
 
-struct AttnShared {
-  int* cbase;   // [BH + 1] exclusive prefix of chunk counts
-  int* ring;    // [NW][RING] claimed chunk ids per warp
-};
-
-// per-item geometry
-struct Item {
-  int bh, lbh, i;
-};
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
 __device__ __forceinline__ int find_bh(const int* cbase, int BH, int c) {
   int lo = 0, hi = BH;  // largest bh with cbase[bh] <= c
@@ -42,12 +47,12 @@ __device__ __forceinline__ int find_bh(const int* cbase, int BH, int c) {
   return lo;
 }
 
-// block-level exclusive scan of ceil(n_req/kChunk) over BH entries into cbase
+// block-level exclusive scan of ceil(n_req/kChunk) over the BH (b, h) entries into cbase
 __device__ void chunk_scan(const Dev& dv, int layer, int* cbase, int* tmp) {
   const int BH = dv.B * dv.H;
   const int nt = blockDim.x;
   const int per = (BH + nt - 1) / nt;
-  const int lo = threadIdx.x * per, hi = min(BH, lo + per);
+  const int lo = min(BH, (int)threadIdx.x * per), hi = min(BH, lo + per);
   int s = 0;
   for (int i = lo; i < hi; ++i) s += (dv.n_req[layer * BH + i] + kChunk - 1) / kChunk;
   tmp[threadIdx.x] = s;
@@ -70,6 +75,7 @@ __device__ void chunk_scan(const Dev& dv, int layer, int* cbase, int* tmp) {
   __syncthreads();
 }
 
+// beta of one block: block-mean score, the tail block over its t - blk*n_b live tokens
 __device__ __forceinline__ float block_beta(const Dev& dv, int lbh, int blk, int t) {
   const int n_b = dv.n_b;
   double m;
@@ -83,35 +89,45 @@ __device__ __forceinline__ float block_beta(const Dev& dv, int lbh, int blk, int
   return (float)m;
 }
 
-// ---------------------------------------------------------------- merge + append (one warp)
+// ---------------------------------------------------------------- merge + append (a thread group)
+// Threads [0, nthr) of the group (nthr a multiple of 32, warp 0 = threads 0..31) cooperate;
+// `bar` is a named barrier over exactly those threads (0 = a single warp: __syncwarp).
+__device__ __forceinline__ void group_sync(int bar, int nthr) {
+  if (bar == 0) __syncwarp(); else named_sync(bar, nthr);
+}
+
 template <typename T>
-__device__ void merge_and_append(const Dev& dv, int layer, int bh, int nc, const T* __restrict__ kn,
-                                 const T* __restrict__ vn, float* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
+__device__ void merge_append_group(const Dev& dv, int layer, int bh, int nc, const T* __restrict__ kn,
+                                   const T* __restrict__ vn, float* __restrict__ out, int tid, int nthr, int bar,
+                                   float* wsm) {
   const int b = bh / dv.H, h = bh % dv.H;
   const int lbh = (layer * dv.B + b) * dv.H + h;
   const int D = dv.D, G = dv.G;
+  const size_t pbase = (size_t)bh * dv.max_chunks;
   __threadfence();
-  // ---- merge chunk partials in chunk order (deterministic)
-  for (int g = 0; g < G; ++g) {
+  // (1) per (chunk, query) weights e^{m_c - M} / L in shared memory
+  for (int q = tid; q < G; q += nthr) {
     float M = -INFINITY;
-    for (int c = 0; c < nc; ++c) M = fmaxf(M, __ldcg(&dv.part_ml[((size_t)bh * dv.max_chunks + c) * G + g]).x);
-    float Lsum = 0.0f;
+    for (int c = 0; c < nc; ++c) M = fmaxf(M, __ldcg(&dv.part_ml[(pbase + c) * G + q]).x);
+    float L = 0.0f;
     for (int c = 0; c < nc; ++c) {
-      const float2 ml = __ldcg(&dv.part_ml[((size_t)bh * dv.max_chunks + c) * G + g]);
-      Lsum += ml.y * expf(ml.x - M);
+      const float2 ml = __ldcg(&dv.part_ml[(pbase + c) * G + q]);
+      L += ml.y * expf(ml.x - M);
     }
-    const float inv = 1.0f / Lsum;
-    for (int d = lane; d < D; d += 32) {
-      float acc = 0.0f;
-      for (int c = 0; c < nc; ++c) {
-        const float w = expf(__ldcg(&dv.part_ml[((size_t)bh * dv.max_chunks + c) * G + g]).x - M);
-        acc += w * __ldcg(&dv.part_o[(((size_t)bh * dv.max_chunks + c) * G + g) * D + d]);
-      }
-      out[((size_t)b * dv.Hq + h * G + g) * D + d] = acc * inv;
-    }
+    const float inv = 1.0f / L;
+    for (int c = 0; c < nc; ++c) wsm[c * G + q] = expf(__ldcg(&dv.part_ml[(pbase + c) * G + q]).x - M) * inv;
   }
-  // ---- append the new token (decode.py:187-189, HeadState.append decode.py:65-71)
+  group_sync(bar, nthr);
+  // (2) outputs: fixed chunk order -> deterministic
+  for (int x = tid; x < G * D; x += nthr) {
+    const int q = x / D, d = x - q * D;
+    const float* po = dv.part_o + (pbase * G + q) * D + d;
+    float acc = 0.0f;
+#pragma unroll 4
+    for (int c = 0; c < nc; ++c) acc = fmaf(wsm[c * G + q], __ldcg(po + (size_t)c * G * D), acc);
+    out[((size_t)b * dv.Hq + h * G + q) * D + d] = acc;
+  }
+  // (3) append the new token (decode.py:187-189, HeadState.append decode.py:65-71)
   const int t = dv.t[lbh];
   const int n_b = dv.n_b;
   const int blk = t / n_b, r = t - blk * n_b;
@@ -122,279 +138,401 @@ __device__ void merge_and_append(const Dev& dv, int layer, int bh, int nc, const
   const int slot = dv.slot_of[(size_t)lbh * dv.NB + blk];
   char* hblk = dv.host + ((size_t)lbh * dv.NB + blk) * dv.bpb;
   char* dblk = slot >= 0 ? dv.pool + ((size_t)lbh * dv.C + slot) * dv.bpb : nullptr;
-  const int chunks_per_row = D * elem / 16;
-  for (int c = lane; c < 2 * chunks_per_row; c += 32) {
-    const int which = c / chunks_per_row;  // 0 = K, 1 = V
-    const int ch = c - which * chunks_per_row;
+  const int cpr = D * elem / 16;  // 16-byte chunks per row
+  for (int c = tid; c < 2 * cpr; c += nthr) {
+    const int which = c / cpr;  // 0 = K, 1 = V
+    const int ch = c - which * cpr;
     const int4 val = reinterpret_cast<const int4*>(which ? (const void*)vr : (const void*)kr)[ch];
     const int off = which * plane + r * D * elem + ((ch ^ (r & 7)) << 4);
     *reinterpret_cast<int4*>(hblk + off) = val;
     if (dblk) *reinterpret_cast<int4*>(dblk + off) = val;
   }
-  if (r == 0) {  // a new block: the slow copy of its unwritten rows must read as zero
+  if (r == 0) {  // a new block: its not-yet-written rows must read as zero from the slow tier
     const int4 z = make_int4(0, 0, 0, 0);
-    const int row_chunks = D * elem / 16;
-    const int total = 2 * (n_b - 1) * row_chunks;
-    for (int c = lane; c < total; c += 32) {
-      const int which = c / ((n_b - 1) * row_chunks);
-      const int rem = c - which * (n_b - 1) * row_chunks;
-      const int row = 1 + rem / row_chunks;
-      const int ch = rem % row_chunks;
-      *reinterpret_cast<int4*>(hblk + which * plane + row * D * elem + (ch << 4)) = z;
+    const int per_plane = (n_b - 1) * cpr;
+    for (int c = tid; c < 2 * per_plane; c += nthr) {
+      const int which = c / per_plane;
+      const int rem = c - which * per_plane;
+      *reinterpret_cast<int4*>(hblk + which * plane + (1 + rem / cpr) * D * elem + ((rem % cpr) << 4)) = z;
     }
   }
-  // importance score of the new token and the tail-block running means
-  const double s = token_score_warp<T>(vr, dv.w1, dv.w2, D, dv.n_ev, dv.variant);
-  double* tks = dv.tail_ksum + (size_t)lbh * D;
-  for (int d = lane; d < D; d += 32) {
-    const double kv = to_f64(kr[d]);
-    const double acc = (r == 0) ? kv : tks[d] + kv;
-    if (r == n_b - 1) {
-      dv.kc[((size_t)lbh * dv.NB + blk) * D + d] = acc / (double)n_b;
-      tks[d] = 0.0;
-    } else {
-      tks[d] = acc;
+  if (tid < 32) {
+    const int lane = tid;
+    const double s = token_score_warp<T>(vr, dv.w1, dv.w2, D, dv.n_ev, dv.variant);
+    double* tks = dv.tail_ksum + (size_t)lbh * D;
+    for (int d = lane; d < D; d += 32) {
+      const double kv = to_f64(kr[d]);
+      const double acc = (r == 0) ? kv : tks[d] + kv;
+      if (r == n_b - 1) {
+        dv.kc[((size_t)lbh * dv.NB + blk) * D + d] = acc / (double)n_b;
+        tks[d] = 0.0;
+      } else {
+        tks[d] = acc;
+      }
     }
-  }
-  if (lane == 0) {
-    const double acc = (r == 0) ? s : dv.tail_se[lbh] + s;
-    if (r == n_b - 1) {
-      dv.se[(size_t)lbh * dv.NB + blk] = acc / (double)n_b;
-      dv.tail_se[lbh] = 0.0;
-    } else {
-      dv.tail_se[lbh] = acc;
+    if (lane == 0) {
+      const double acc = (r == 0) ? s : dv.tail_se[lbh] + s;
+      if (r == n_b - 1) {
+        dv.se[(size_t)lbh * dv.NB + blk] = acc / (double)n_b;
+        dv.tail_se[lbh] = 0.0;
+      } else {
+        dv.tail_se[lbh] = acc;
+      }
+      dv.t[lbh] = t + 1;
     }
-    dv.t[lbh] = t + 1;
   }
   __threadfence_system();
+  group_sync(bar, nthr);
 }
 
 // ---------------------------------------------------------------- bf16 tensor-core kernel
-template <int NBK, int DH, int NW, int NS>
-__global__ void __launch_bounds__(NW * 32)
+template <int NBK, int DH, int NQT>
+struct BF {
+  static constexpr int BPB = 2 * NBK * DH * 2;
+  static constexpr int PLANE = NBK * DH * 2;
+  static constexpr int NCW = NBK >= 64 ? 4 : NBK / 16;  // consumer warps
+  static constexpr int KPW = NBK / NCW;                 // keys per consumer warp
+  static constexpr int MTK = KPW / 16;                  // key m-tiles per warp
+  static constexpr int MTD = DH / 16;                   // head-dim m-tiles (PV)
+  static constexpr int KS = DH / 16;                    // k-steps (QK)
+  static constexpr int QMAX = 8 * NQT;                  // queries per (b, h), padded to n-tiles
+  static constexpr int QSLOT = QMAX * DH * 2;
+  static constexpr int COMB = NCW * QMAX * DH * 4 + NCW * QMAX * 8;
+  static constexpr int NSR = (200 * 1024 - COMB) / (BPB + QSLOT);
+  static constexpr int NS = NSR > 8 ? 8 : (NSR < 2 ? 2 : NSR);  // ring stages
+  static constexpr int NQ = 3;                                  // chunk-metadata queue depth
+  static constexpr int THREADS = (NCW + 2) * 32;                // + copy warp + scheduler warp
+  static constexpr int WARP_COPY = NCW, WARP_SCHED = NCW + 1;
+};
+
+struct ItemInfo {
+  int bh, ci, flags, count;
+  float beta;
+  int nc, pad0, pad1;
+};
+enum { IF_FIRST = 1, IF_LAST = 2, IF_END = 4 };
+
+struct ChunkMeta {
+  int bh, ci, n, nc;
+  int slot[kChunk];
+  int count[kChunk];
+  float beta[kChunk];
+};
+
+template <int NBK, int DH, int NQT>
+__host__ __device__ constexpr size_t bf_smem_fixed() {
+  using T = BF<NBK, DH, NQT>;
+  return (size_t)T::NS * T::BPB + (size_t)T::NS * T::QSLOT + T::COMB + 2 * T::NS * 8 + 2 * T::NQ * 8 +
+         T::NS * sizeof(ItemInfo) + T::NQ * sizeof(ChunkMeta) + T::THREADS * 4 + 64;
+}
+
+template <int NBK, int DH, int NQT>
+__global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
     attend_bf16_kernel(Dev dv, int layer, const __nv_bfloat16* __restrict__ q,
                        const __nv_bfloat16* __restrict__ kn, const __nv_bfloat16* __restrict__ vn,
                        float* __restrict__ out) {
-  constexpr int BPB = 2 * NBK * DH * 2;
-  constexpr int PLANE = NBK * DH * 2;
-  constexpr int RING = NS + 2;
-  constexpr int NT = NBK / 8;   // key n-tiles
-  constexpr int KS = DH / 16;   // k-steps over head dims
-  constexpr int ON = DH / 8;    // output n-tiles
+  using T = BF<NBK, DH, NQT>;
   extern __shared__ __align__(128) char smem_raw[];
   const int BH = dv.B * dv.H;
-  char* stages = smem_raw;                                          // [NW][NS][BPB]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NW * NS * BPB);  // [NW][NS]
-  int* cbase = reinterpret_cast<int*>(bars + NW * NS);              // [BH+1]
-  int* ring = cbase + BH + 1;                                       // [NW][RING]
-  int* tmp = ring + NW * RING;                                      // [blockDim]
+  const int G = dv.G;
+  char* p = smem_raw;
+  char* stages = p;                                   p += (size_t)T::NS * T::BPB;
+  char* qslots = p;                                   p += (size_t)T::NS * T::QSLOT;
+  float* comb_o = reinterpret_cast<float*>(p);        p += (size_t)T::NCW * T::QMAX * DH * 4;
+  float2* comb_ml = reinterpret_cast<float2*>(p);     p += (size_t)T::NCW * T::QMAX * 8;
+  uint64_t* full = reinterpret_cast<uint64_t*>(p);    p += T::NS * 8;
+  uint64_t* empty = reinterpret_cast<uint64_t*>(p);   p += T::NS * 8;
+  uint64_t* mq_full = reinterpret_cast<uint64_t*>(p); p += T::NQ * 8;
+  uint64_t* mq_empty = reinterpret_cast<uint64_t*>(p); p += T::NQ * 8;
+  ItemInfo* info = reinterpret_cast<ItemInfo*>(p);    p += T::NS * sizeof(ItemInfo);
+  ChunkMeta* meta = reinterpret_cast<ChunkMeta*>(p);  p += T::NQ * sizeof(ChunkMeta);
+  int* tmp = reinterpret_cast<int*>(p);               p += T::THREADS * 4;
+  int* flag = reinterpret_cast<int*>(p);              p += 64;
+  int* cbase = reinterpret_cast<int*>(p);             p += (size_t)(BH + 1) * 4;
+  float* wsm = reinterpret_cast<float*>(p);           // [max_chunks * G]
 
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, tq = lane & 3;
-  if (lane == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&bars[warp * NS + s], 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < T::NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], T::NCW);
+    }
+    for (int s = 0; s < T::NQ; ++s) {
+      mbar_init(&mq_full[s], 1);
+      mbar_init(&mq_empty[s], 1);
+    }
     fence_mbar_init();
   }
-  chunk_scan(dv, layer, cbase, tmp);
+  chunk_scan(dv, layer, cbase, tmp);  // also publishes the barrier inits (__syncthreads)
   const int total = cbase[BH];
-  __syncwarp();
 
-  char* my_stages = stages + (size_t)warp * NS * BPB;
-  uint64_t* my_bars = bars + warp * NS;
-  int* my_ring = ring + warp * RING;
-
-  // loader state (warp-uniform)
-  int ld_seq = 0, ld_chunk_n = 0;       // items issued, chunks claimed
-  int ld_bh = 0, ld_i = 0, ld_end = 0;  // current loader chunk
-  bool ld_done = false;
-  auto advance_loader = [&]() {
-    if (ld_done) return;
-    if (ld_i >= ld_end) {
+  if (warp == T::WARP_SCHED) {
+    // ------------------------------------------------------------ scheduler warp
+    for (int qs = 0;; ++qs) {
       int c = 0;
       if (lane == 0) c = atomicAdd(dv.cnt + 2 * layer + 1, 1);
       c = __shfl_sync(0xffffffffu, c, 0);
-      if (c >= total) { ld_done = true; return; }
-      ld_bh = find_bh(cbase, BH, c);
-      const int ci = c - cbase[ld_bh];
-      const int nreq = dv.n_req[layer * BH + ld_bh];
-      ld_i = ci * kChunk;
-      ld_end = min(ld_i + kChunk, nreq);
-      if (lane == 0) my_ring[ld_chunk_n % RING] = c;
-      ++ld_chunk_n;
+      const int slot = qs % T::NQ;
+      mbar_wait(&mq_empty[slot], ((qs / T::NQ) & 1) ^ 1);
+      ChunkMeta& m = meta[slot];
+      if (c >= total) {
+        if (lane == 0) {
+          m.n = -1;
+          mbar_arrive(&mq_full[slot]);
+        }
+        break;
+      }
+      const int bh = find_bh(cbase, BH, c);
+      const int lbh = layer * BH + bh;
+      const int ci = c - cbase[bh];
+      const int nreq = dv.n_req[lbh];
+      const int t = dv.t[lbh];
+      const int i0 = ci * kChunk;
+      const int n = min(kChunk, nreq - i0);
+      if (lane < n) {
+        const int blk = dv.req[(size_t)lbh * dv.C + i0 + lane];
+        m.slot[lane] = dv.req_slot[(size_t)lbh * dv.C + i0 + lane];
+        m.count[lane] = min(NBK, t - blk * NBK);
+        m.beta[lane] = block_beta(dv, lbh, blk, t);
+      }
+      if (lane == 0) {
+        m.bh = bh;
+        m.ci = ci;
+        m.n = n;
+        m.nc = (nreq + kChunk - 1) / kChunk;
+      }
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&mq_full[slot]);
     }
-    const int lbh = layer * BH + ld_bh;
-    const int slot = dv.req_slot[(size_t)lbh * dv.C + ld_i];
-    const int st = ld_seq % NS;
+  } else if (warp == T::WARP_COPY) {
+    // ------------------------------------------------------------ copy warp (TMA producer)
+    int seq = 0;
+    for (int qs = 0;; ++qs) {
+      const int slot = qs % T::NQ;
+      mbar_wait(&mq_full[slot], (qs / T::NQ) & 1);
+      const ChunkMeta& m = meta[slot];
+      const int n = m.n;
+      if (n < 0) break;
+      const int bh = m.bh, ci = m.ci, nc = m.nc;
+      const int lbh = layer * BH + bh;
+      const int b = bh / dv.H, h = bh - (bh / dv.H) * dv.H;
+      for (int i = 0; i < n; ++i, ++seq) {
+        const int s = seq % T::NS;
+        mbar_wait(&empty[s], ((seq / T::NS) & 1) ^ 1);
+        if (i == 0) {  // the chunk's query rows (zero padded to QMAX)
+          const __nv_bfloat16* qb = q + ((size_t)b * dv.Hq + h * G) * DH;
+          int4* dst = reinterpret_cast<int4*>(qslots + (size_t)s * T::QSLOT);
+          for (int x = lane; x < T::QSLOT / 16; x += 32) {
+            const int row = x / (DH / 8);
+            dst[x] = row < G ? reinterpret_cast<const int4*>(qb)[x] : make_int4(0, 0, 0, 0);
+          }
+        }
+        if (lane == 0) {
+          ItemInfo& it = info[s];
+          it.bh = bh;
+          it.ci = ci;
+          it.flags = (i == 0 ? IF_FIRST : 0) | (i == n - 1 ? IF_LAST : 0);
+          it.count = m.count[i];
+          it.beta = m.beta[i];
+          it.nc = nc;
+        }
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0) {
+          fence_proxy_async();
+          mbar_expect_tx(&full[s], T::BPB);
+          bulk_g2s(stages + (size_t)s * T::BPB, dv.pool + ((size_t)lbh * dv.C + m.slot[i]) * (size_t)T::BPB, T::BPB,
+                   &full[s]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&mq_empty[slot]);
+    }
+    const int s = seq % T::NS;  // end-of-work marker for the consumers
+    mbar_wait(&empty[s], ((seq / T::NS) & 1) ^ 1);
     if (lane == 0) {
-      fence_proxy_async();
-      mbar_expect_tx(&my_bars[st], BPB);
-      bulk_g2s(my_stages + (size_t)st * BPB, dv.pool + ((size_t)lbh * dv.C + slot) * (size_t)BPB, BPB,
-               &my_bars[st]);
+      info[s].flags = IF_END;
+      mbar_arrive(&full[s]);
     }
-    ++ld_i;
-    ++ld_seq;
-  };
-
-  for (int s = 0; s < NS; ++s) advance_loader();
-  __syncwarp();
-
-  int cp_seq = 0, cp_chunk_n = 0;
-  int cp_bh = 0, cp_i = 0, cp_end = 0, cp_c = 0, cp_ci = 0;
-  int cp_t = 0;
-  unsigned qa[KS][4];
-  float o[ON][4];
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
-  const bool v0 = g < dv.G, v1 = (g + 8) < dv.G;
-
-  while (cp_seq < ld_seq) {
-    if (cp_i >= cp_end) {  // start of a new chunk
+  } else {
+    // ------------------------------------------------------------ consumer warps
+    const int g = lane >> 2, tq = lane & 3;
+    const int w = warp;
+    unsigned qb[T::KS][NQT][2];
+    float o[T::MTD][NQT][4];
+    float mrun[NQT][2], lrun[NQT][2];
+    for (int seq = 0;; ++seq) {
+      const int s = seq % T::NS;
+      mbar_wait(&full[s], (seq / T::NS) & 1);
+      const ItemInfo it = info[s];
+      if (it.flags & IF_END) break;
+      if (it.flags & IF_FIRST) {
+        const char* qs = qslots + (size_t)s * T::QSLOT;
+#pragma unroll
+        for (int ks = 0; ks < T::KS; ++ks)
+#pragma unroll
+          for (int nq = 0; nq < NQT; ++nq) {
+            const char* row = qs + (size_t)(8 * nq + g) * DH * 2;
+            qb[ks][nq][0] = *reinterpret_cast<const unsigned*>(row + (16 * ks + 2 * tq) * 2);
+            qb[ks][nq][1] = *reinterpret_cast<const unsigned*>(row + (16 * ks + 8 + 2 * tq) * 2);
+          }
+#pragma unroll
+        for (int md = 0; md < T::MTD; ++md)
+#pragma unroll
+          for (int nq = 0; nq < NQT; ++nq) o[md][nq][0] = o[md][nq][1] = o[md][nq][2] = o[md][nq][3] = 0.0f;
+#pragma unroll
+        for (int nq = 0; nq < NQT; ++nq) {
+          mrun[nq][0] = mrun[nq][1] = -INFINITY;
+          lrun[nq][0] = lrun[nq][1] = 0.0f;
+        }
+      }
+      const unsigned kbase = smem_u32(stages + (size_t)s * T::BPB);
+      const unsigned vbase = kbase + T::PLANE;
+      const int key0 = w * T::KPW;
+      // ---- S^T = K Q^T : keys on M (16 per m-tile), queries on N
+      float sc[T::MTK][NQT][4];
+#pragma unroll
+      for (int mk = 0; mk < T::MTK; ++mk)
+#pragma unroll
+        for (int nq = 0; nq < NQT; ++nq) sc[mk][nq][0] = sc[mk][nq][1] = sc[mk][nq][2] = sc[mk][nq][3] = 0.0f;
+#pragma unroll
+      for (int ks = 0; ks < T::KS; ++ks) {
+#pragma unroll
+        for (int mk = 0; mk < T::MTK; ++mk) {
+          const int mi = lane >> 3;
+          const int key = key0 + mk * 16 + (lane & 7) + 8 * (mi & 1);
+          const int chunk = 2 * ks + (mi >> 1);
+          unsigned a0, a1, a2, a3;
+          ldsm_x4(kbase + key * (DH * 2) + ((chunk ^ (key & 7)) << 4), a0, a1, a2, a3);
+#pragma unroll
+          for (int nq = 0; nq < NQT; ++nq) mma_bf16(sc[mk][nq], a0, a1, a2, a3, qb[ks][nq][0], qb[ks][nq][1]);
+        }
+      }
+      // ---- online softmax over this warp's keys, per query column
+      const float beta = it.beta;
+      const int count = it.count;
+#pragma unroll
+      for (int nq = 0; nq < NQT; ++nq) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          float mx = -INFINITY;
+#pragma unroll
+          for (int mk = 0; mk < T::MTK; ++mk) {
+            const int klo = key0 + mk * 16 + g;
+            sc[mk][nq][e] = klo < count ? sc[mk][nq][e] + beta : -INFINITY;
+            sc[mk][nq][2 + e] = klo + 8 < count ? sc[mk][nq][2 + e] + beta : -INFINITY;
+            mx = fmaxf(mx, fmaxf(sc[mk][nq][e], sc[mk][nq][2 + e]));
+          }
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+          const float mn = fmaxf(mrun[nq][e], mx);
+          const bool live = mn != -INFINITY;
+          const float scale = live ? exp2f((mrun[nq][e] - mn) * kLog2e) : 1.0f;
+          const float mb = live ? mn * kLog2e : 0.0f;
+          float sum = 0.0f;
+#pragma unroll
+          for (int mk = 0; mk < T::MTK; ++mk) {
+            sc[mk][nq][e] = exp2f(fmaf(sc[mk][nq][e], kLog2e, -mb));
+            sc[mk][nq][2 + e] = exp2f(fmaf(sc[mk][nq][2 + e], kLog2e, -mb));
+            sum += sc[mk][nq][e] + sc[mk][nq][2 + e];
+          }
+          lrun[nq][e] = lrun[nq][e] * scale + sum;
+          mrun[nq][e] = mn;
+#pragma unroll
+          for (int md = 0; md < T::MTD; ++md) {
+            o[md][nq][e] *= scale;
+            o[md][nq][2 + e] *= scale;
+          }
+        }
+      }
+      // ---- O^T += V^T P^T : head dims on M, queries on N, this warp's keys on K
+      const int src0 = 8 * tq + (g >> 1);
+      const unsigned sel = (g & 1) ? 0x7632u : 0x5410u;
+#pragma unroll
+      for (int mk = 0; mk < T::MTK; ++mk) {
+        unsigned pb[NQT][2];
+#pragma unroll
+        for (int nq = 0; nq < NQT; ++nq) {
+          const unsigned x01 = pack_bf16(sc[mk][nq][0], sc[mk][nq][1]);
+          const unsigned x23 = pack_bf16(sc[mk][nq][2], sc[mk][nq][3]);
+          const unsigned v0 = __shfl_sync(0xffffffffu, x01, src0);
+          const unsigned v1 = __shfl_sync(0xffffffffu, x01, src0 + 4);
+          const unsigned v2 = __shfl_sync(0xffffffffu, x23, src0);
+          const unsigned v3 = __shfl_sync(0xffffffffu, x23, src0 + 4);
+          pb[nq][0] = __byte_perm(v0, v1, sel);
+          pb[nq][1] = __byte_perm(v2, v3, sel);
+        }
+#pragma unroll
+        for (int md = 0; md < T::MTD; ++md) {
+          const int mi = lane >> 3;
+          const int key = key0 + mk * 16 + (lane & 7) + 8 * (mi >> 1);
+          const int chunk = 2 * md + (mi & 1);
+          unsigned a0, a1, a2, a3;
+          ldsm_x4_t(vbase + key * (DH * 2) + ((chunk ^ (key & 7)) << 4), a0, a1, a2, a3);
+#pragma unroll
+          for (int nq = 0; nq < NQT; ++nq) mma_bf16(o[md][nq], a0, a1, a2, a3, pb[nq][0], pb[nq][1]);
+        }
+      }
       __syncwarp();
-      cp_c = my_ring[cp_chunk_n % RING];
-      ++cp_chunk_n;
-      cp_bh = find_bh(cbase, BH, cp_c);
-      cp_ci = cp_c - cbase[cp_bh];
-      const int nreq = dv.n_req[layer * BH + cp_bh];
-      cp_i = cp_ci * kChunk;
-      cp_end = min(cp_i + kChunk, nreq);
-      const int b = cp_bh / dv.H, h = cp_bh % dv.H;
-      cp_t = dv.t[layer * BH + cp_bh];
-      const __nv_bfloat16* qb = q + ((size_t)b * dv.Hq + h * dv.G) * DH;
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        const int c0 = ks * 16 + 2 * tq;
-        qa[ks][0] = v0 ? *reinterpret_cast<const unsigned*>(qb + (size_t)g * DH + c0) : 0u;
-        qa[ks][1] = v1 ? *reinterpret_cast<const unsigned*>(qb + (size_t)(g + 8) * DH + c0) : 0u;
-        qa[ks][2] = v0 ? *reinterpret_cast<const unsigned*>(qb + (size_t)g * DH + c0 + 8) : 0u;
-        qa[ks][3] = v1 ? *reinterpret_cast<const unsigned*>(qb + (size_t)(g + 8) * DH + c0 + 8) : 0u;
-      }
-#pragma unroll
-      for (int n = 0; n < ON; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.0f;
-      m0 = m1 = -INFINITY;
-      l0 = l1 = 0.0f;
-    }
-    const int lbh = layer * BH + cp_bh;
-    const int blk = dv.req[(size_t)lbh * dv.C + cp_i];
-    const int count = min(NBK, cp_t - blk * NBK);
-    const float beta = block_beta(dv, lbh, blk, cp_t);
-    const int st = cp_seq % NS;
-    mbar_wait(&my_bars[st], (cp_seq / NS) & 1);
-    const unsigned kbase = smem_u32(my_stages + (size_t)st * BPB);
-    const unsigned vbase = kbase + PLANE;
+      if (lane == 0) mbar_arrive(&empty[s]);  // stage (and its query slot) may be refilled
 
-    // ---- S = Q K^T  (rows: query heads, cols: keys)
-    float s[NT][4];
+      if (it.flags & IF_LAST) {
+        // ---- chunk end: combine the consumer warps' partials, write one record
 #pragma unroll
-    for (int j = 0; j < NT; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.0f;
+        for (int nq = 0; nq < NQT; ++nq)
 #pragma unroll
-    for (int p = 0; p < KS / 2; ++p) {
+          for (int e = 0; e < 2; ++e) {
+            float l = lrun[nq][e];
+            l += __shfl_xor_sync(0xffffffffu, l, 4);
+            l += __shfl_xor_sync(0xffffffffu, l, 8);
+            l += __shfl_xor_sync(0xffffffffu, l, 16);
+            if (g == 0) comb_ml[w * T::QMAX + 8 * nq + 2 * tq + e] = make_float2(mrun[nq][e], l);
+          }
 #pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        const int row = j * 8 + (lane & 7);
-        const int chunk = p * 4 + (lane >> 3);
-        unsigned b0, b1, b2, b3;
-        ldsm_x4(kbase + row * (DH * 2) + ((chunk ^ (row & 7)) << 4), b0, b1, b2, b3);
-        mma_bf16(s[j], qa[2 * p][0], qa[2 * p][1], qa[2 * p][2], qa[2 * p][3], b0, b1);
-        mma_bf16(s[j], qa[2 * p + 1][0], qa[2 * p + 1][1], qa[2 * p + 1][2], qa[2 * p + 1][3], b2, b3);
-      }
-    }
-    // ---- online softmax over this block
-    float mx0 = -INFINITY, mx1 = -INFINITY;
+        for (int md = 0; md < T::MTD; ++md)
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
+          for (int nq = 0; nq < NQT; ++nq)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const bool valid = (j * 8 + 2 * tq + e) < count;
-        s[j][e] = valid ? s[j][e] + beta : -INFINITY;
-        s[j][2 + e] = valid ? s[j][2 + e] + beta : -INFINITY;
-        mx0 = fmaxf(mx0, s[j][e]);
-        mx1 = fmaxf(mx1, s[j][2 + e]);
-      }
-    }
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-    const float sc0 = v0 ? exp2f((m0 - mn0) * kLog2e) : 1.0f;
-    const float sc1 = v1 ? exp2f((m1 - mn1) * kLog2e) : 1.0f;
-    m0 = mn0;
-    m1 = mn1;
-    const float mb0 = mn0 * kLog2e, mb1 = mn1 * kLog2e;
-    l0 *= sc0;
-    l1 *= sc1;
+            for (int e = 0; e < 2; ++e) {
+              float* row = comb_o + ((size_t)w * T::QMAX + 8 * nq + 2 * tq + e) * DH;
+              row[16 * md + g] = o[md][nq][e];
+              row[16 * md + g + 8] = o[md][nq][2 + e];
+            }
+        named_sync(kBarConsumers, T::NCW * 32);
+        const int bh = it.bh, ci = it.ci;
+        const size_t pb0 = (size_t)bh * dv.max_chunks + ci;
+        for (int x = tid; x < G * DH; x += T::NCW * 32) {
+          const int qq = x / DH, d = x - qq * DH;
+          float M = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
+          for (int ww = 0; ww < T::NCW; ++ww) M = fmaxf(M, comb_ml[ww * T::QMAX + qq].x);
+          float acc = 0.0f, L = 0.0f;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        s[j][e] = v0 ? exp2f(fmaf(s[j][e], kLog2e, -mb0)) : 0.0f;
-        s[j][2 + e] = v1 ? exp2f(fmaf(s[j][2 + e], kLog2e, -mb1)) : 0.0f;
-        l0 += s[j][e];
-        l1 += s[j][2 + e];
-      }
-    }
-#pragma unroll
-    for (int n = 0; n < ON; ++n) {
-      o[n][0] *= sc0; o[n][1] *= sc0;
-      o[n][2] *= sc1; o[n][3] *= sc1;
-    }
-    // ---- O += P V  (P re-used from the S accumulators as bf16 A fragments)
-#pragma unroll
-    for (int kk = 0; kk < NBK / 16; ++kk) {
-      const unsigned pa0 = pack_bf16(s[2 * kk][0], s[2 * kk][1]);
-      const unsigned pa1 = pack_bf16(s[2 * kk][2], s[2 * kk][3]);
-      const unsigned pa2 = pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]);
-      const unsigned pa3 = pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3]);
-#pragma unroll
-      for (int np = 0; np < ON / 2; ++np) {
-        const int row = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-        const int chunk = np * 2 + (lane >> 4);
-        unsigned b0, b1, b2, b3;
-        ldsm_x4_t(vbase + row * (DH * 2) + ((chunk ^ (row & 7)) << 4), b0, b1, b2, b3);
-        mma_bf16(o[2 * np], pa0, pa1, pa2, pa3, b0, b1);
-        mma_bf16(o[2 * np + 1], pa0, pa1, pa2, pa3, b2, b3);
-      }
-    }
-    __syncwarp();
-    ++cp_seq;
-    ++cp_i;
-    advance_loader();  // refill the stage just released
-
-    if (cp_i >= cp_end) {  // end of chunk: write the partial, maybe merge + append
-      float lr0 = l0 + __shfl_xor_sync(0xffffffffu, l0, 1);
-      lr0 += __shfl_xor_sync(0xffffffffu, lr0, 2);
-      float lr1 = l1 + __shfl_xor_sync(0xffffffffu, l1, 1);
-      lr1 += __shfl_xor_sync(0xffffffffu, lr1, 2);
-      const size_t pbase = (size_t)cp_bh * dv.max_chunks + cp_ci;
-      if (v0) {
-        float* po = dv.part_o + (pbase * dv.G + g) * DH;
-#pragma unroll
-        for (int n = 0; n < ON; ++n) *reinterpret_cast<float2*>(po + n * 8 + 2 * tq) = make_float2(o[n][0], o[n][1]);
-        if (tq == 0) dv.part_ml[pbase * dv.G + g] = make_float2(m0, lr0);
-      }
-      if (v1) {
-        float* po = dv.part_o + (pbase * dv.G + g + 8) * DH;
-#pragma unroll
-        for (int n = 0; n < ON; ++n) *reinterpret_cast<float2*>(po + n * 8 + 2 * tq) = make_float2(o[n][2], o[n][3]);
-        if (tq == 0) dv.part_ml[pbase * dv.G + g + 8] = make_float2(m1, lr1);
-      }
-      __threadfence();
-      __syncwarp();
-      const int nc = (dv.n_req[layer * BH + cp_bh] + kChunk - 1) / kChunk;
-      int last = 0;
-      if (lane == 0) last = atomicAdd(dv.done + layer * BH + cp_bh, 1) == nc - 1;
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) {
-        const int b = cp_bh / dv.H;
-        merge_and_append<__nv_bfloat16>(dv, layer, cp_bh, nc, kn, vn, out);
-        (void)b;
+          for (int ww = 0; ww < T::NCW; ++ww) {
+            const float2 ml = comb_ml[ww * T::QMAX + qq];
+            const float f = ml.x == -INFINITY ? 0.0f : exp2f((ml.x - M) * kLog2e);
+            acc = fmaf(f, comb_o[((size_t)ww * T::QMAX + qq) * DH + d], acc);
+            L = fmaf(f, ml.y, L);
+          }
+          dv.part_o[(pb0 * G + qq) * DH + d] = acc;
+          if (d == 0) dv.part_ml[pb0 * G + qq] = make_float2(M, L);
+        }
+        __threadfence();
+        named_sync(kBarConsumers, T::NCW * 32);
+        if (tid == 0) flag[0] = atomicAdd(dv.done + layer * BH + bh, 1) == it.nc - 1;
+        named_sync(kBarConsumers, T::NCW * 32);
+        if (flag[0])
+          merge_append_group<__nv_bfloat16>(dv, layer, bh, it.nc, kn, vn, out, tid, T::NCW * 32, kBarConsumers, wsm);
       }
     }
   }
 }
 
 // ---------------------------------------------------------------- fp32 CUDA-core kernel
-// Parity path for fp32 storage (tolerance 1e-5): same decomposition, one warp per CTA,
-// logits and P.V in fp32 FMA with accurate expf.
+// Parity path for fp32 storage (tolerance 1e-5): same chunk decomposition and merge, one warp
+// per CTA with a private double-buffered ring, logits and P.V in fp32 FMA with accurate expf.
 template <int NBK, int DH, int NS>
 __global__ void __launch_bounds__(32)
     attend_f32_kernel(Dev dv, int layer, const float* __restrict__ q, const float* __restrict__ kn,
@@ -410,9 +548,10 @@ __global__ void __launch_bounds__(32)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NS * BPB);
   float* qs = reinterpret_cast<float*>(bars + NS);      // [GM][DH]
   float* ps = qs + GM * DH;                              // [GM][NBK]
-  int* cbase = reinterpret_cast<int*>(ps + GM * NBK);    // [BH+1]
-  int* ring = cbase + BH + 1;                            // [RING]
+  int* ring = reinterpret_cast<int*>(ps + GM * NBK);     // [RING]
   int* tmp = ring + RING;                                // [32]
+  int* cbase = tmp + 32;                                 // [BH+1]
+  float* wsm = reinterpret_cast<float*>(cbase + BH + 1); // [max_chunks * G]
   const int lane = threadIdx.x;
   const int G = dv.G;
   if (lane == 0) {
@@ -485,7 +624,6 @@ __global__ void __launch_bounds__(32)
     mbar_wait(&bars[st], (cp_seq / NS) & 1);
     const char* kb = stages + (size_t)st * BPB;
     const char* vb = kb + PLANE;
-    // logits: lane owns keys lane, lane+32, ...
     for (int key = lane; key < NBK; key += 32) {
       float acc[GM];
 #pragma unroll
@@ -520,9 +658,9 @@ __global__ void __launch_bounds__(32)
       const float sc = expf(m[gg] - mn);
       float sum = 0.0f;
       for (int key = lane; key < NBK; key += 32) {
-        const float p = expf(ps[gg * NBK + key] - mn);
-        ps[gg * NBK + key] = p;
-        sum += p;
+        const float pr = expf(ps[gg * NBK + key] - mn);
+        ps[gg * NBK + key] = pr;
+        sum += pr;
       }
 #pragma unroll
       for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
@@ -539,9 +677,9 @@ __global__ void __launch_bounds__(32)
 #pragma unroll
       for (int gg = 0; gg < GM; ++gg) {
         if (gg >= G) break;
-        const float p = ps[gg * NBK + key];
+        const float pr = ps[gg * NBK + key];
 #pragma unroll
-        for (int x = 0; x < DL; ++x) o[gg][x] = fmaf(p, vv[x], o[gg][x]);
+        for (int x = 0; x < DL; ++x) o[gg][x] = fmaf(pr, vv[x], o[gg][x]);
       }
     }
     __syncwarp();
@@ -564,39 +702,38 @@ __global__ void __launch_bounds__(32)
       int last = 0;
       if (lane == 0) last = atomicAdd(dv.done + layer * BH + cp_bh, 1) == nc - 1;
       last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) merge_and_append<float>(dv, layer, cp_bh, nc, kn, vn, out);
+      if (last) merge_append_group<float>(dv, layer, cp_bh, nc, kn, vn, out, lane, 32, 0, wsm);
     }
   }
 }
 
 // ---------------------------------------------------------------- launchers
-template <int NBK, int DH>
-static cudaError_t launch_bf16(const Dev& dv, int layer, const void* q, const void* kn,
-                               const void* vn, float* out, cudaStream_t st, int num_sms) {
-  constexpr int BPB = 2 * NBK * DH * 2;
-  // ~192 KiB of stages per CTA (one CTA per SM): 3 stages per warp, as many warps as fit
-  constexpr int NS = 3;
-  constexpr int NW = BPB >= 65536 ? 1 : (BPB >= 32768 ? 2 : 4);
+template <int NBK, int DH, int NQT>
+static cudaError_t launch_bf16(const Dev& dv, int layer, const void* q, const void* kn, const void* vn,
+                               float* out, cudaStream_t st, int num_sms) {
+  using T = BF<NBK, DH, NQT>;
   const int BH = dv.B * dv.H;
-  const size_t smem = (size_t)NW * NS * BPB + NW * NS * 8 + (BH + 1) * 4 + NW * (NS + 2) * 4 + NW * 32 * 4 + 64;
-  auto k = attend_bf16_kernel<NBK, DH, NW, NS>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = num_sms;
-  k<<<grid, NW * 32, smem, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(q),
-                                 static_cast<const __nv_bfloat16*>(kn),
-                                 static_cast<const __nv_bfloat16*>(vn), out);
+  const size_t smem = bf_smem_fixed<NBK, DH, NQT>() + (size_t)(BH + 1) * 4 + (size_t)dv.max_chunks * dv.G * 4 + 64;
+  auto k = attend_bf16_kernel<NBK, DH, NQT>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<num_sms, T::THREADS, smem, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(q),
+                                       static_cast<const __nv_bfloat16*>(kn),
+                                       static_cast<const __nv_bfloat16*>(vn), out);
   return cudaGetLastError();
 }
 
 template <int NBK, int DH>
-static cudaError_t launch_f32(const Dev& dv, int layer, const void* q, const void* kn,
-                              const void* vn, float* out, cudaStream_t st, int num_sms) {
+static cudaError_t launch_f32(const Dev& dv, int layer, const void* q, const void* kn, const void* vn, float* out,
+                              cudaStream_t st, int num_sms) {
   constexpr int NS = 2;
   constexpr int BPB = 2 * NBK * DH * 4;
   const int BH = dv.B * dv.H;
-  const size_t smem = (size_t)NS * BPB + NS * 8 + 16 * DH * 4 + 16 * NBK * 4 + (BH + 1) * 4 + (NS + 2) * 4 + 32 * 4 + 64;
+  const size_t smem = (size_t)NS * BPB + NS * 8 + 16 * DH * 4 + 16 * NBK * 4 + (NS + 2) * 4 + 32 * 4 +
+                      (BH + 1) * 4 + (size_t)dv.max_chunks * dv.G * 4 + 64;
   auto k = attend_f32_kernel<NBK, DH, NS>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   k<<<num_sms, 32, smem, st>>>(dv, layer, static_cast<const float*>(q), static_cast<const float*>(kn),
                                static_cast<const float*>(vn), out);
   return cudaGetLastError();
@@ -605,16 +742,23 @@ static cudaError_t launch_f32(const Dev& dv, int layer, const void* q, const voi
 bool attend_supported(int n_b, int d_head, int dtype) {
   const bool nb_ok = n_b == 16 || n_b == 32 || n_b == 64 || n_b == 128;
   const bool d_ok = d_head == 64 || d_head == 128;
-  if (dtype == 1 && n_b == 128 && d_head == 128) return false;  // 128 KiB blocks: no double buffer
+  if (dtype == 1 && n_b == 128 && d_head == 128) return false;  // 128 KiB fp32 blocks: no double buffer
   return nb_ok && d_ok;
 }
 
-cudaError_t launch_attend(const Dev& dv, int layer, const void* q, const void* kn, const void* vn,
-                          float* out, cudaStream_t st, int num_sms) {
-#define NOSA_DISPATCH(NBK, DH)                                                     \
-  if (dv.n_b == NBK && dv.D == DH) {                                               \
-    return dv.dtype == 0 ? launch_bf16<NBK, DH>(dv, layer, q, kn, vn, out, st, num_sms) \
-                         : launch_f32<NBK, DH>(dv, layer, q, kn, vn, out, st, 2 * num_sms); \
+template <int NBK, int DH>
+static cudaError_t dispatch_bf16(const Dev& dv, int layer, const void* q, const void* kn, const void* vn, float* out,
+                                 cudaStream_t st, int num_sms) {
+  return dv.G <= 8 ? launch_bf16<NBK, DH, 1>(dv, layer, q, kn, vn, out, st, num_sms)
+                   : launch_bf16<NBK, DH, 2>(dv, layer, q, kn, vn, out, st, num_sms);
+}
+
+cudaError_t launch_attend(const Dev& dv, int layer, const void* q, const void* kn, const void* vn, float* out,
+                          cudaStream_t st, int num_sms) {
+#define NOSA_DISPATCH(NBK, DH)                                                                  \
+  if (dv.n_b == NBK && dv.D == DH) {                                                            \
+    return dv.dtype == 0 ? dispatch_bf16<NBK, DH>(dv, layer, q, kn, vn, out, st, num_sms)       \
+                         : launch_f32<NBK, DH>(dv, layer, q, kn, vn, out, st, 2 * num_sms);     \
   }
   NOSA_DISPATCH(64, 128)
   NOSA_DISPATCH(64, 64)
@@ -622,11 +766,8 @@ cudaError_t launch_attend(const Dev& dv, int layer, const void* q, const void* k
   NOSA_DISPATCH(32, 64)
   NOSA_DISPATCH(16, 128)
   NOSA_DISPATCH(16, 64)
-  if (dv.n_b == 128 && dv.D == 64) {
-    return dv.dtype == 0 ? launch_bf16<128, 64>(dv, layer, q, kn, vn, out, st, num_sms)
-                         : launch_f32<128, 64>(dv, layer, q, kn, vn, out, st, 2 * num_sms);
-  }
-  if (dv.n_b == 128 && dv.D == 128 && dv.dtype == 0) return launch_bf16<128, 128>(dv, layer, q, kn, vn, out, st, num_sms);
+  NOSA_DISPATCH(128, 64)
+  if (dv.n_b == 128 && dv.D == 128 && dv.dtype == 0) return dispatch_bf16<128, 128>(dv, layer, q, kn, vn, out, st, num_sms);
 #undef NOSA_DISPATCH
   return cudaErrorInvalidValue;
 }
