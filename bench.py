@@ -198,7 +198,7 @@ def run_native(args, rank, world, local_rank):
     eng.reset_stats()
 
     # ---------------- timed region (value): inputs resident in HBM
-    eng.timing_enable(3 * L * args.steps + 8)
+    eng.timing_enable(4 * L * args.steps + 8)
     launches0 = eng.launch_count
     if world > 1:
         dist.barrier()
@@ -263,9 +263,10 @@ def run_native(args, rank, world, local_rank):
         "select_plan": (B * cfg.n_kv_head * P * cfg.d_head * 8 + B * cfg.n_head * cfg.d_head * 2),
         # K3: each missed block crosses PCIe once and is written to HBM once
         "gather": st.misses * bpb / calls,
-        # K4+K5: K|V of every attended block + its bias + q in + f32 out + append row
-        "attend": (R_total * (bpb + 4)) / calls + B * cfg.n_head * cfg.d_head * (2 + 4)
-                  + B * cfg.n_kv_head * 2 * cfg.d_head * 2,
+        # K4: K|V of every attended block + its bias + the query rows
+        "attend": (R_total * (bpb + 4)) / calls + B * cfg.n_head * cfg.d_head * 2,
+        # K4 merge + K5: f32 outputs + the appended K/V row (HBM slot)
+        "finalize": B * cfg.n_head * cfg.d_head * 4 + B * cfg.n_kv_head * 2 * cfg.d_head * 2,
     }
     for k_ in kern:
         kern[k_]["bytes_per_launch"] = per_launch[k_]
@@ -279,7 +280,7 @@ def run_native(args, rank, world, local_rank):
                 "peak": hbm_peak, "unit": "GB/s", "frac": round(att["gbs"] / hbm_peak, 4), "traffic": traffic,
                 "peak_kind": peak_kind, "bytes_per_launch": int(per_launch["attend"]),
                 "avg_launch_ms": round(att["avg_ms"], 5)}
-    hbm_step = (per_launch["select_plan"] + per_launch["attend"] + per_launch["gather"]) * L
+    hbm_step = (per_launch["select_plan"] + per_launch["attend"] + per_launch["finalize"] + per_launch["gather"]) * L
     h2d_step = st.misses * bpb / args.steps
     t_roof = max(hbm_step / 8e12, h2d_step / (link_gbs * 1e9))
     step_ms = ms_max / args.steps

@@ -218,10 +218,11 @@ int nosa_check_errors(NosaCtx* ctx, uint32_t* flags);
 
 /* Device timing of every kernel of subsequent eager steps, bracketed by CUDA events on the
  * stream each kernel runs on (bench evidence).  Kinds: 0 = select+plan (K1+K2), 1 = gather (K3),
- * 2 = attend+append (K4+K5).  enable(0) turns it off; read synchronises and returns the summed
- * milliseconds and launch counts per kind since enable. */
+ * 2 = attention (K4, split-K records), 3 = finalize (K4 log-sum-exp merge + K5 append).
+ * enable(0) turns it off; read synchronises and returns the summed milliseconds and launch
+ * counts per kind since enable. */
 int nosa_timing_enable(NosaCtx* ctx, int max_launches);
-int nosa_timing_read(NosaCtx* ctx, double* total_ms /* [3] */, int64_t* launches /* [3] */);
+int nosa_timing_read(NosaCtx* ctx, double* total_ms /* [4] */, int64_t* launches /* [4] */);
 
 /* kernel launches issued by this library since context creation (bench evidence) */
 int64_t nosa_launch_count(const NosaCtx* ctx);

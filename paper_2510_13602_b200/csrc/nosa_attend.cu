@@ -21,9 +21,9 @@
 //                   tensor cores with keys on M and the GQA group's queries on N
 //                   (mma.m16n8k16, no padding for G = 8), online softmax in registers.
 // At a chunk end the consumer warps combine their partials through shared memory and write
-// one (m, l, O) record; the CTA finishing the last chunk of a (b, h) merges the records in
-// chunk order (log-sum-exp) and performs the append, so no warp can still be reading the
-// tail block.
+// one (m, l, O) record.  The finalize kernel (one CTA per (b, h), launched right after) merges
+// the records in chunk order (log-sum-exp) and performs the append; keeping that latency-bound
+// work out of the streaming kernel keeps the persistent CTAs on the HBM stream.
 #include "nosa_device.cuh"
 
 namespace nosa {
@@ -93,7 +93,7 @@ __device__ __forceinline__ float block_beta(const Dev& dv, int lbh, int blk, int
 // Threads [0, nthr) of the group (nthr a multiple of 32, warp 0 = threads 0..31) cooperate;
 // `bar` is a named barrier over exactly those threads (0 = a single warp: __syncwarp).
 __device__ __forceinline__ void group_sync(int bar, int nthr) {
-  if (bar == 0) __syncwarp(); else named_sync(bar, nthr);
+  if (bar < 0) __syncthreads(); else if (bar == 0) __syncwarp(); else named_sync(bar, nthr);
 }
 
 template <typename T>
@@ -104,7 +104,6 @@ __device__ void merge_append_group(const Dev& dv, int layer, int bh, int nc, con
   const int lbh = (layer * dv.B + b) * dv.H + h;
   const int D = dv.D, G = dv.G;
   const size_t pbase = (size_t)bh * dv.max_chunks;
-  __threadfence();
   // (1) per (chunk, query) weights e^{m_c - M} / L in shared memory
   for (int q = tid; q < G; q += nthr) {
     float M = -INFINITY;
@@ -263,6 +262,8 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
     }
     fence_mbar_init();
   }
+  if (G < T::QMAX)  // query rows past the group stay zero (only G rows are ever copied in)
+    for (int x = tid; x < T::NS * T::QSLOT / 16; x += blockDim.x) reinterpret_cast<int4*>(qslots)[x] = make_int4(0, 0, 0, 0);
   chunk_scan(dv, layer, cbase, tmp);  // also publishes the barrier inits (__syncthreads)
   const int total = cbase[BH];
 
@@ -316,18 +317,10 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
       if (n < 0) break;
       const int bh = m.bh, ci = m.ci, nc = m.nc;
       const int lbh = layer * BH + bh;
-      const int b = bh / dv.H, h = bh - (bh / dv.H) * dv.H;
+      const int b = bh / dv.H, h = bh - b * dv.H;
       for (int i = 0; i < n; ++i, ++seq) {
         const int s = seq % T::NS;
         mbar_wait(&empty[s], ((seq / T::NS) & 1) ^ 1);
-        if (i == 0) {  // the chunk's query rows (zero padded to QMAX)
-          const __nv_bfloat16* qb = q + ((size_t)b * dv.Hq + h * G) * DH;
-          int4* dst = reinterpret_cast<int4*>(qslots + (size_t)s * T::QSLOT);
-          for (int x = lane; x < T::QSLOT / 16; x += 32) {
-            const int row = x / (DH / 8);
-            dst[x] = row < G ? reinterpret_cast<const int4*>(qb)[x] : make_int4(0, 0, 0, 0);
-          }
-        }
         if (lane == 0) {
           ItemInfo& it = info[s];
           it.bh = bh;
@@ -341,9 +334,12 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
         __syncwarp();
         if (lane == 0) {
           fence_proxy_async();
-          mbar_expect_tx(&full[s], T::BPB);
+          const unsigned qbytes = i == 0 ? (unsigned)(G * DH * 2) : 0u;  // the chunk's query rows
+          mbar_expect_tx(&full[s], T::BPB + qbytes);
           bulk_g2s(stages + (size_t)s * T::BPB, dv.pool + ((size_t)lbh * dv.C + m.slot[i]) * (size_t)T::BPB, T::BPB,
                    &full[s]);
+          if (qbytes)
+            bulk_g2s(qslots + (size_t)s * T::QSLOT, q + ((size_t)b * dv.Hq + h * G) * DH, qbytes, &full[s]);
         }
       }
       __syncwarp();
@@ -519,12 +515,7 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
           dv.part_o[(pb0 * G + qq) * DH + d] = acc;
           if (d == 0) dv.part_ml[pb0 * G + qq] = make_float2(M, L);
         }
-        __threadfence();
-        named_sync(kBarConsumers, T::NCW * 32);
-        if (tid == 0) flag[0] = atomicAdd(dv.done + layer * BH + bh, 1) == it.nc - 1;
-        named_sync(kBarConsumers, T::NCW * 32);
-        if (flag[0])
-          merge_append_group<__nv_bfloat16>(dv, layer, bh, it.nc, kn, vn, out, tid, T::NCW * 32, kBarConsumers, wsm);
+        named_sync(kBarConsumers, T::NCW * 32);  // comb_* may be overwritten at the next chunk end
       }
     }
   }
@@ -696,15 +687,38 @@ __global__ void __launch_bounds__(32)
         for (int x = 0; x < DL; ++x) po[lane + 32 * x] = o[gg][x];
         if (lane == 0) dv.part_ml[pbase * G + gg] = make_float2(m[gg], l[gg]);
       }
-      __threadfence();
       __syncwarp();
-      const int nc = (dv.n_req[layer * BH + cp_bh] + kChunk - 1) / kChunk;
-      int last = 0;
-      if (lane == 0) last = atomicAdd(dv.done + layer * BH + cp_bh, 1) == nc - 1;
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) merge_append_group<float>(dv, layer, cp_bh, nc, kn, vn, out, lane, 32, 0, wsm);
     }
   }
+}
+
+// ---------------------------------------------------------------- finalize (merge + append)
+// One CTA per (b, h): log-sum-exp merge of the chunk records in chunk order, then the append.
+// Runs after the attention kernel of the layer, so every chunk record is complete and no
+// thread can still be reading the tail block.
+template <typename T>
+__global__ void __launch_bounds__(128)
+    finalize_kernel(Dev dv, int layer, const T* __restrict__ kn, const T* __restrict__ vn, float* __restrict__ out) {
+  extern __shared__ float wsm[];  // [max_chunks * G]
+  const int bh = blockIdx.x;
+  const int nc = (dv.n_req[layer * dv.B * dv.H + bh] + kChunk - 1) / kChunk;
+  if (nc == 0) return;  // the plan failed for this manager (CapacityExceeded): no step
+  merge_append_group<T>(dv, layer, bh, nc, kn, vn, out, threadIdx.x, blockDim.x, -1, wsm);
+}
+
+cudaError_t launch_finalize(const Dev& dv, int layer, const void* kn, const void* vn, float* out, cudaStream_t st) {
+  const size_t smem = (size_t)dv.max_chunks * dv.G * 4;
+  if (dv.dtype == 0) {
+    auto k = finalize_kernel<__nv_bfloat16>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<dv.B * dv.H, 128, smem, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(kn),
+                                       static_cast<const __nv_bfloat16*>(vn), out);
+  } else {
+    auto k = finalize_kernel<float>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<dv.B * dv.H, 128, smem, st>>>(dv, layer, static_cast<const float*>(kn), static_cast<const float*>(vn), out);
+  }
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- launchers

@@ -28,6 +28,7 @@ cudaError_t launch_unswizzle(const char* src, char* dst, int nblocks, int n_b, i
                              cudaStream_t st);
 cudaError_t launch_attend(const Dev& dv, int layer, const void* q, const void* kn, const void* vn,
                           float* out, cudaStream_t st, int num_sms);
+cudaError_t launch_finalize(const Dev& dv, int layer, const void* kn, const void* vn, float* out, cudaStream_t st);
 bool attend_supported(int n_b, int d_head, int dtype);
 }  // namespace nosa
 
@@ -256,7 +257,6 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   ALLOC(dv.plan_n, LBH * 3);
   ALLOC(dv.cnt, (size_t)dv.L * 2);
   ALLOC(dv.miss_list, (size_t)dv.L * BH * dv.C);
-  ALLOC(dv.done, (size_t)dv.L * BH);
   ALLOC(dv.part_o, BH * dv.max_chunks * dv.G * dv.D);
   ALLOC(dv.part_ml, BH * dv.max_chunks * dv.G);
   ALLOC(dv.w1, (size_t)dv.D * dv.n_ev);
@@ -478,7 +478,8 @@ extern "C" int nosa_attend(NosaCtx* ctx, int layer, const void* q, const void* k
   if (!q || !k_new || !v_new || !out) return fail(ctx, NOSA_ERR_VALUE, "attend: NULL tensor");
   cudaSetDevice(ctx->device);
   CUDA_TRY(ctx, nosa::launch_attend(ctx->dv, layer, q, k_new, v_new, out, S(stream), ctx->num_sms));
-  ctx->launches += 1;
+  CUDA_TRY(ctx, nosa::launch_finalize(ctx->dv, layer, k_new, v_new, out, S(stream)));
+  ctx->launches += 2;
   return NOSA_OK;
 }
 
@@ -522,7 +523,7 @@ extern "C" int nosa_timing_read(NosaCtx* ctx, double* total_ms, int64_t* launche
   if (!ctx || !total_ms || !launches) return NOSA_ERR_VALUE;
   cudaSetDevice(ctx->device);
   CUDA_TRY(ctx, cudaDeviceSynchronize());
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < 4; ++k) {
     total_ms[k] = 0.0;
     launches[k] = 0;
   }
@@ -562,11 +563,15 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   }
   for (int l = 0; l < dv.L; ++l) {
     CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_gather[l], 0));
-    TimeScope ts(ctx, st, 2, timed);
-    CUDA_TRY(ctx, nosa::launch_attend(dv, l, q + l * qstride, kn + l * kstride, vn + l * kstride,
-                                      io->out + l * ostride, st, ctx->num_sms));
+    {
+      TimeScope ts(ctx, st, 2, timed);
+      CUDA_TRY(ctx, nosa::launch_attend(dv, l, q + l * qstride, kn + l * kstride, vn + l * kstride,
+                                        io->out + l * ostride, st, ctx->num_sms));
+    }
+    TimeScope ts(ctx, st, 3, timed);
+    CUDA_TRY(ctx, nosa::launch_finalize(dv, l, kn + l * kstride, vn + l * kstride, io->out + l * ostride, st));
   }
-  if (count) ctx->launches += 3LL * dv.L;
+  if (count) ctx->launches += 4LL * dv.L;
   return NOSA_OK;
 }
 
@@ -610,7 +615,7 @@ extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {
   if (e != cudaSuccess) return fail(ctx, NOSA_ERR_CUDA, "stream capture: %s", cudaGetErrorString(e));
   ctx->graph = g;
   CUDA_TRY(ctx, cudaGraphInstantiate(&ctx->graph_exec, g, 0));
-  ctx->graph_kernels = 3 * ctx->dv.L;
+  ctx->graph_kernels = 4 * ctx->dv.L;
   return NOSA_OK;
 }
 

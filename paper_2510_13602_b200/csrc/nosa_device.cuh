@@ -60,7 +60,6 @@ struct Dev {
   int* plan_n;                   // [lbh][3] n_fetch, n_evict, n_hit
   int* cnt;                      // [L][2]: miss count, attention work counter
   int4* miss_list;               // [L][B*H*C]  {lbh, blk, slot, 0}
-  int* done;                     // [L][B*H]
   float* part_o;                 // [B*H][max_chunks][G][D]
   float2* part_ml;               // [B*H][max_chunks][G]
   double* w1;                    // [D][n_ev]

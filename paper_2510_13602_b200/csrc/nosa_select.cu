@@ -404,7 +404,6 @@ __global__ void __launch_bounds__(256)
   const int lbh = (layer * dv.B + b) * dv.H + h;
   const int Pp = next_pow2(dv.NB);
   SelSmem sm = carve_sel_smem(smem_raw, dv.D, Pp, dv.C);
-  if (threadIdx.x == 0) dv.done[layer * dv.B * dv.H + bh] = 0;  // attention split-K counter
 
   if (mode == 2) {
     const int n = ext_nreq[bh];

@@ -354,15 +354,15 @@ class NosaEngine:
             self._call(_lib.lib.nosa_reset_stats, _lib.stream_ptr())
 
     # ------------------------------------------------------------------ device timing
-    KERNEL_KINDS = ("select_plan", "gather", "attend")
+    KERNEL_KINDS = ("select_plan", "gather", "attend", "finalize")
 
     def timing_enable(self, max_launches: int):
         """Bracket every kernel of the following eager steps with CUDA events on its stream."""
         self._call(_lib.lib.nosa_timing_enable, max_launches)
 
     def timing_read(self) -> dict:
-        ms = (ctypes.c_double * 3)()
-        n = (ctypes.c_int64 * 3)()
+        ms = (ctypes.c_double * 4)()
+        n = (ctypes.c_int64 * 4)()
         self._call(_lib.lib.nosa_timing_read, ms, n)
         return {k: {"total_ms": ms[i], "launches": n[i], "avg_ms": ms[i] / n[i] if n[i] else 0.0}
                 for i, k in enumerate(self.KERNEL_KINDS)}

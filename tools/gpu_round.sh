@@ -1,9 +1,13 @@
 #!/bin/bash
-# tests + a small bench + the default bench on one GPU box; logs under gpurun_out/
+# tests + timing profile + the default bench on one GPU box; logs under gpurun_out/
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=clocks.sm,clocks.max.sm --format=csv > gpurun_out/clocks0.txt 2>&1
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/gpu_tests.log 2>&1; echo rc=$? >> gpurun_out/gpu_tests.log
-timeout 600 python bench.py --layers 2 --batch 16 --steps 4 --warmup 3 > gpurun_out/bench_small.log 2>&1; echo rc=$? >> gpurun_out/bench_small.log
+timeout 300 python tools/profile_step.py --batch 128 --layers 2 --context 32768 --cache 0.25 --steps 6 > gpurun_out/prof_offload.txt 2>&1
 if [ "$1" == "full" ]; then
   timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1; echo rc=$? >> gpurun_out/bench_full.log
+fi
+if [ "$2" == "ncu" ]; then
+  ARGS="--batch 128 --layers 2 --context 32768 --cache 0.25 --steps 5"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:attend_bf16 -s 4 -c 1 \
+    -o gpurun_out/prof_attend -f python tools/profile_step.py $ARGS > gpurun_out/ncu_attend_stdout.txt 2>&1
 fi

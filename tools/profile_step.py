@@ -1,0 +1,77 @@
+"""Run a few decode steps of one workload shape for ncu / timing experiments.
+
+    python tools/profile_step.py --batch 128 --layers 2 --context 32768 --cache 0.25 --steps 6
+Prints per-kernel device times (CUDA events bracketing each launch on its stream)."""
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+from paper_2510_13602_b200 import NosaEngine, one_b_config, workload  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batch", type=int, default=128)
+    ap.add_argument("--layers", type=int, default=2)
+    ap.add_argument("--context", type=int, default=32768)
+    ap.add_argument("--cache", type=float, default=0.25, help="fraction of blocks in HBM; 1 = resident")
+    ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--rho", type=float, default=0.95)
+    ap.add_argument("--selector", default="nosa")
+    ap.add_argument("--gather", default="uva")
+    ap.add_argument("--layer-by-layer", action="store_true", help="use the per-layer C-ABI calls")
+    a = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    cfg = one_b_config(65536)
+    max_tokens = a.context + a.steps + 4
+    nblk = -(-max_tokens // cfg.n_b)
+    fast = nblk if a.cache >= 1 else int(a.cache * nblk)
+    w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, 0)
+    t0 = time.time()
+    eng = NosaEngine(cfg, batch=a.batch, layers=a.layers, max_tokens=max_tokens, fast_slots=fast, w1=w1, w2=w2)
+    for l in range(a.layers):
+        shape = (a.batch, cfg.n_kv_head, a.context, cfg.d_head)
+        eng.prefill(workload.torch_prefix_kv(2 * l, shape, dev, torch.bfloat16),
+                    workload.torch_prefix_kv(2 * l + 1, shape, dev, torch.bfloat16), layer=l)
+    eng.start_run()
+    torch.cuda.synchronize()
+    print(f"setup {time.time() - t0:.1f}s", flush=True)
+    qs = workload.TorchQueryStream(7, a.layers, a.batch, cfg.n_head, cfg.n_kv_head, cfg.d_head, a.rho, dev,
+                                   torch.bfloat16)
+    out = torch.empty((a.layers, a.batch, cfg.n_head, cfg.d_head), dtype=torch.float32, device=dev)
+    eng.timing_enable(4 * a.layers * a.steps + 8)
+    for s in range(a.steps):
+        q, k, v = qs.next()
+        if s == 2:
+            eng.reset_stats()
+            eng.timing_enable(4 * a.layers * a.steps + 8)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        if a.layer_by_layer:
+            for l in range(a.layers):
+                eng.step_layer(l, q[l], k[l], v[l], selector=a.selector, out=out[l], gather=a.gather)
+            eng._t[:] = eng._t[0]  # step_layer advances per layer
+        else:
+            eng.step(q, k, v, selector=a.selector, out=out, gather=a.gather, check=False)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e1.record()
+    torch.cuda.synchronize()
+    st = eng.residency_stats()
+    res = {"ms_per_step": e0.elapsed_time(e1) / (a.steps - 2), "kernels": eng.timing_read(),
+           "hit_rate": st.hit_rate, "misses": st.misses, "hits": st.hits}
+    print(json.dumps(res, indent=1))
+    eng.check_errors()
+    eng.close()
+
+
+if __name__ == "__main__":
+    main()
