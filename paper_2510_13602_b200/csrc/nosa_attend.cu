@@ -89,44 +89,52 @@ __device__ __forceinline__ float block_beta(const Dev& dv, int lbh, int blk, int
   return (float)m;
 }
 
-// ---------------------------------------------------------------- merge + append (a thread group)
-// Threads [0, nthr) of the group (nthr a multiple of 32, warp 0 = threads 0..31) cooperate;
-// `bar` is a named barrier over exactly those threads (0 = a single warp: __syncwarp).
-__device__ __forceinline__ void group_sync(int bar, int nthr) {
-  if (bar < 0) __syncthreads(); else if (bar == 0) __syncwarp(); else named_sync(bar, nthr);
-}
+// ---------------------------------------------------------------- finalize (merge + append)
+// One CTA (kFinThreads threads) per (b, h).  Every phase issues all of its loads before using
+// them: the kernel is latency-bound, so the number of dependent L2 round trips is the cost.
+constexpr int kFinThreads = 256;
 
 template <typename T>
-__device__ void merge_append_group(const Dev& dv, int layer, int bh, int nc, const T* __restrict__ kn,
-                                   const T* __restrict__ vn, float* __restrict__ out, int tid, int nthr, int bar,
-                                   float* wsm) {
+__device__ void finalize_bh(const Dev& dv, int layer, int bh, int nc, const T* __restrict__ kn,
+                            const T* __restrict__ vn, float* __restrict__ out, float* wsm, double* zsm) {
+  const int tid = threadIdx.x;
   const int b = bh / dv.H, h = bh % dv.H;
   const int lbh = (layer * dv.B + b) * dv.H + h;
   const int D = dv.D, G = dv.G;
   const size_t pbase = (size_t)bh * dv.max_chunks;
-  // (1) per (chunk, query) weights e^{m_c - M} / L in shared memory
-  for (int q = tid; q < G; q += nthr) {
+  // (1) chunk records (m, l) -> shared, then per-query weights e^{m_c - M} / L
+  float2* mls = reinterpret_cast<float2*>(wsm);  // [nc][G], reused in place as weights
+  for (int x = tid; x < nc * G; x += blockDim.x) mls[x] = __ldcg(&dv.part_ml[pbase * G + x]);
+  __syncthreads();
+  if (tid < G) {
     float M = -INFINITY;
-    for (int c = 0; c < nc; ++c) M = fmaxf(M, __ldcg(&dv.part_ml[(pbase + c) * G + q]).x);
+    for (int c = 0; c < nc; ++c) M = fmaxf(M, mls[c * G + tid].x);
     float L = 0.0f;
-    for (int c = 0; c < nc; ++c) {
-      const float2 ml = __ldcg(&dv.part_ml[(pbase + c) * G + q]);
-      L += ml.y * expf(ml.x - M);
-    }
+    for (int c = 0; c < nc; ++c) L = fmaf(mls[c * G + tid].y, expf(mls[c * G + tid].x - M), L);
     const float inv = 1.0f / L;
-    for (int c = 0; c < nc; ++c) wsm[c * G + q] = expf(__ldcg(&dv.part_ml[(pbase + c) * G + q]).x - M) * inv;
+    for (int c = 0; c < nc; ++c) mls[c * G + tid].y = expf(mls[c * G + tid].x - M) * inv;
   }
-  group_sync(bar, nthr);
-  // (2) outputs: fixed chunk order -> deterministic
-  for (int x = tid; x < G * D; x += nthr) {
-    const int q = x / D, d = x - q * D;
-    const float* po = dv.part_o + (pbase * G + q) * D + d;
-    float acc = 0.0f;
-#pragma unroll 4
-    for (int c = 0; c < nc; ++c) acc = fmaf(wsm[c * G + q], __ldcg(po + (size_t)c * G * D), acc);
-    out[((size_t)b * dv.Hq + h * G + q) * D + d] = acc;
+  __syncthreads();
+  // (2) outputs, float4 per thread, chunks summed in chunk order (deterministic)
+  const int D4 = D / 4;
+  for (int x = tid; x < G * D4; x += blockDim.x) {
+    const int q = x / D4, d4 = x - q * D4;
+    const float4* po = reinterpret_cast<const float4*>(dv.part_o + (pbase * G + q) * D) + d4;
+    const size_t cstride = (size_t)G * D4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+    for (int c = 0; c < nc; ++c) {
+      const float w = mls[c * G + q].y;
+      const float4 v = __ldcg(po + c * cstride);
+      acc.x = fmaf(w, v.x, acc.x);
+      acc.y = fmaf(w, v.y, acc.y);
+      acc.z = fmaf(w, v.z, acc.z);
+      acc.w = fmaf(w, v.w, acc.w);
+    }
+    reinterpret_cast<float4*>(out + ((size_t)b * dv.Hq + h * G + q) * D)[d4] = acc;
   }
   // (3) append the new token (decode.py:187-189, HeadState.append decode.py:65-71)
+  const int nthr = blockDim.x;
   const int t = dv.t[lbh];
   const int n_b = dv.n_b;
   const int blk = t / n_b, r = t - blk * n_b;
@@ -155,33 +163,44 @@ __device__ void merge_append_group(const Dev& dv, int layer, int bh, int nc, con
       *reinterpret_cast<int4*>(hblk + which * plane + (1 + rem / cpr) * D * elem + ((rem % cpr) << 4)) = z;
     }
   }
-  if (tid < 32) {
-    const int lane = tid;
-    const double s = token_score_warp<T>(vr, dv.w1, dv.w2, D, dv.n_ev, dv.variant);
-    double* tks = dv.tail_ksum + (size_t)lbh * D;
-    for (int d = lane; d < D; d += 32) {
-      const double kv = to_f64(kr[d]);
-      const double acc = (r == 0) ? kv : tks[d] + kv;
-      if (r == n_b - 1) {
-        dv.kc[((size_t)lbh * dv.NB + blk) * D + d] = acc / (double)n_b;
-        tks[d] = 0.0;
-      } else {
-        tks[d] = acc;
-      }
-    }
-    if (lane == 0) {
-      const double acc = (r == 0) ? s : dv.tail_se[lbh] + s;
-      if (r == n_b - 1) {
-        dv.se[(size_t)lbh * dv.NB + blk] = acc / (double)n_b;
-        dv.tail_se[lbh] = 0.0;
-      } else {
-        dv.tail_se[lbh] = acc;
-      }
-      dv.t[lbh] = t + 1;
+  // importance score of the new token: the arithmetic of token_score_warp (prefill), with the
+  // eviction-head columns spread over the warps
+  {
+    const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+    for (int j = warp; j < dv.n_ev; j += nwarps) {
+      double part = 0.0;
+      for (int i = lane; i < D; i += 32) part = fma(to_f64(vr[i]), dv.w1[i * dv.n_ev + j], part);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane == 0) zsm[j] = silu64(part);
     }
   }
-  __threadfence_system();
-  group_sync(bar, nthr);
+  double* tks = dv.tail_ksum + (size_t)lbh * D;
+  for (int d = tid; d < D; d += nthr) {
+    const double kv = to_f64(kr[d]);
+    const double acc = (r == 0) ? kv : tks[d] + kv;
+    if (r == n_b - 1) {
+      dv.kc[((size_t)lbh * dv.NB + blk) * D + d] = acc / (double)n_b;
+      tks[d] = 0.0;
+    } else {
+      tks[d] = acc;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double z = 0.0;
+    for (int j = 0; j < dv.n_ev; ++j) z = fma(zsm[j], dv.w2[j], z);
+    const double s = dv.variant == 2 ? exp(z) : z;
+    const double acc = (r == 0) ? s : dv.tail_se[lbh] + s;
+    if (r == n_b - 1) {
+      dv.se[(size_t)lbh * dv.NB + blk] = acc / (double)n_b;
+      dv.tail_se[lbh] = 0.0;
+    } else {
+      dv.tail_se[lbh] = acc;
+    }
+    dv.t[lbh] = t + 1;
+  }
+  __threadfence_system();  // the host-mirror rows are visible before any later gather reads them
 }
 
 // ---------------------------------------------------------------- bf16 tensor-core kernel
@@ -697,26 +716,29 @@ __global__ void __launch_bounds__(32)
 // Runs after the attention kernel of the layer, so every chunk record is complete and no
 // thread can still be reading the tail block.
 template <typename T>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kFinThreads)
     finalize_kernel(Dev dv, int layer, const T* __restrict__ kn, const T* __restrict__ vn, float* __restrict__ out) {
-  extern __shared__ float wsm[];  // [max_chunks * G]
+  extern __shared__ __align__(16) char fin_smem[];
+  double* zsm = reinterpret_cast<double*>(fin_smem);           // [n_ev]
+  float* wsm = reinterpret_cast<float*>(zsm + dv.n_ev);         // [max_chunks * G] float2
   const int bh = blockIdx.x;
   const int nc = (dv.n_req[layer * dv.B * dv.H + bh] + kChunk - 1) / kChunk;
   if (nc == 0) return;  // the plan failed for this manager (CapacityExceeded): no step
-  merge_append_group<T>(dv, layer, bh, nc, kn, vn, out, threadIdx.x, blockDim.x, -1, wsm);
+  finalize_bh<T>(dv, layer, bh, nc, kn, vn, out, wsm, zsm);
 }
 
 cudaError_t launch_finalize(const Dev& dv, int layer, const void* kn, const void* vn, float* out, cudaStream_t st) {
-  const size_t smem = (size_t)dv.max_chunks * dv.G * 4;
+  const size_t smem = (size_t)dv.n_ev * 8 + (size_t)dv.max_chunks * dv.G * 8;
   if (dv.dtype == 0) {
     auto k = finalize_kernel<__nv_bfloat16>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<dv.B * dv.H, 128, smem, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(kn),
-                                       static_cast<const __nv_bfloat16*>(vn), out);
+    k<<<dv.B * dv.H, kFinThreads, smem, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(kn),
+                                               static_cast<const __nv_bfloat16*>(vn), out);
   } else {
     auto k = finalize_kernel<float>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<dv.B * dv.H, 128, smem, st>>>(dv, layer, static_cast<const float*>(kn), static_cast<const float*>(vn), out);
+    k<<<dv.B * dv.H, kFinThreads, smem, st>>>(dv, layer, static_cast<const float*>(kn),
+                                               static_cast<const float*>(vn), out);
   }
   return cudaGetLastError();
 }

@@ -203,15 +203,26 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
   if (selector == 0 && warp == 0) {
     const int m_e_eff = min(dv.m_e, P - m_q_eff);
     const int* rank = dv.rank_e + (size_t)lbh * dv.NB;
+    // at most m_q_eff of the first m_q_eff + m_e_eff ranked blocks are query picks, so only
+    // that prefix is read; 4 x 32 entries are loaded before any is used
+    const int need = min(P, m_q_eff + m_e_eff);
     int cnt = 0;
-    for (int base = 0; base < P && cnt < m_e_eff; base += 32) {
-      const int i = base + lane;
-      const int p = (i < P) ? rank[i] : 0;
-      const bool ok = (i < P) && !((sm.bm_q[p >> 5] >> (p & 31)) & 1u);
-      const unsigned bal = __ballot_sync(0xffffffffu, ok);
-      const int pos = cnt + __popc(bal & ((1u << lane) - 1u));
-      if (ok && pos < m_e_eff) atomicOr(&sm.bm_e[p >> 5], 1u << (p & 31));
-      cnt += __popc(bal);
+    for (int g0 = 0; g0 < need && cnt < m_e_eff; g0 += 128) {
+      int pr[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = g0 + 32 * k + lane;
+        pr[k] = i < need ? __ldg(rank + i) : -1;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int p = pr[k];
+        const bool ok = p >= 0 && !((sm.bm_q[p >> 5] >> (p & 31)) & 1u);
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        const int pos = cnt + __popc(bal & ((1u << lane) - 1u));
+        if (ok && pos < m_e_eff) atomicOr(&sm.bm_e[p >> 5], 1u << (p & 31));
+        cnt += __popc(bal);
+      }
     }
   }
   __syncthreads();
@@ -281,22 +292,30 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
   if (warp == 0) {
     const int clock = dv.clock[lbh] + 1;
     int nf = 0;
-    for (int base = 0; base < n_req; base += 32) {
-      const int i = base + lane;
-      const int blk = (i < n_req) ? sm.req[i] : 0;
-      const int s = (i < n_req) ? slot_of[blk] : 0;
-      const bool miss = (i < n_req) && s < 0;
-      if (i < n_req && s >= 0) {
-        lastreq[s] = clock;
-        sm.reqslot[i] = s;
+    for (int g0 = 0; g0 < n_req; g0 += 128) {
+      int blk[4], sl[4];  // 4 x 32 table lookups in flight before any is used
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = g0 + 32 * k + lane;
+        blk[k] = i < n_req ? sm.req[i] : 0;
+        sl[k] = i < n_req ? slot_of[blk[k]] : 0;
       }
-      const unsigned bal = __ballot_sync(0xffffffffu, miss);
-      if (miss) {
-        const int pos = nf + __popc(bal & ((1u << lane) - 1u));
-        sm.fetch[pos] = blk;
-        sm.fpos[pos] = i;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = g0 + 32 * k + lane;
+        const bool miss = i < n_req && sl[k] < 0;
+        if (i < n_req && sl[k] >= 0) {
+          lastreq[sl[k]] = clock;
+          sm.reqslot[i] = sl[k];
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, miss);
+        if (miss) {
+          const int pos = nf + __popc(bal & ((1u << lane) - 1u));
+          sm.fetch[pos] = blk[k];
+          sm.fpos[pos] = i;
+        }
+        nf += __popc(bal);
       }
-      nf += __popc(bal);
     }
     if (lane == 0) {
       dv.clock[lbh] = clock;
