@@ -153,6 +153,7 @@ __device__ void finalize_bh(const Dev& dv, int layer, int bh, int nc, const T* _
     const int off = which * plane + r * D * elem + ((ch ^ (r & 7)) << 4);
     *reinterpret_cast<int4*>(hblk + off) = val;
     if (dblk) *reinterpret_cast<int4*>(dblk + off) = val;
+    if (r == 0) reinterpret_cast<int4*>(dv.newrow + (size_t)lbh * 2 * D * elem)[c] = val;  // see gather_kernel
   }
   if (r == 0) {  // a new block: its not-yet-written rows must read as zero from the slow tier
     const int4 z = make_int4(0, 0, 0, 0);
@@ -200,7 +201,8 @@ __device__ void finalize_bh(const Dev& dv, int layer, int bh, int nc, const T* _
     }
     dv.t[lbh] = t + 1;
   }
-  __threadfence_system();  // the host-mirror rows are visible before any later gather reads them
+  // No system fence: within a run the slow copy of a just-written row is never read back (a
+  // block born by this append is rebuilt from dv.newrow); later readers follow a host sync.
 }
 
 // ---------------------------------------------------------------- bf16 tensor-core kernel

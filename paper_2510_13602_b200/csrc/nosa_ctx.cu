@@ -59,6 +59,30 @@ struct NosaCtx {
   size_t timing_used = 0;
   std::atomic<long long> launches{0};
   std::string err;
+  // copy-engine gather (NOSA_GATHER_MEMCPY): pinned readback of the miss list + batch arrays
+  cudaStream_t meta_stream = nullptr;
+  int* h_cnt = nullptr;
+  int4* h_list = nullptr;
+  std::vector<void*> b_dst, b_src;
+  std::vector<size_t> b_size;
+  long long batch_fallbacks = 0;
+};
+
+// brackets one launch with timing events when timing is enabled (eager steps only)
+struct TimeScope {
+  NosaCtx* ctx;
+  cudaStream_t st;
+  NosaCtx::Timed* slot = nullptr;
+  TimeScope(NosaCtx* c, cudaStream_t s, int kind, bool on) : ctx(c), st(s) {
+    if (on && ctx->timing_used < ctx->timing.size()) {
+      slot = &ctx->timing[ctx->timing_used++];
+      slot->kind = kind;
+      cudaEventRecord(slot->a, st);
+    }
+  }
+  ~TimeScope() {
+    if (slot) cudaEventRecord(slot->b, st);
+  }
 };
 
 static thread_local std::string g_create_error;
@@ -156,6 +180,9 @@ static void release(NosaCtx* ctx) {
   for (auto e : ctx->ev_plan) cudaEventDestroy(e);
   for (auto e : ctx->ev_gather) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->meta_stream) cudaStreamDestroy(ctx->meta_stream);
+  if (ctx->h_list) cudaFreeHost(ctx->h_list);
+  if (ctx->h_cnt) cudaFreeHost(ctx->h_cnt);
   for (auto& t : ctx->timing) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
@@ -259,6 +286,7 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   ALLOC(dv.miss_list, (size_t)dv.L * BH * dv.C);
   ALLOC(dv.part_o, BH * dv.max_chunks * dv.G * dv.D);
   ALLOC(dv.part_ml, BH * dv.max_chunks * dv.G);
+  ALLOC(dv.newrow, LBH * 2 * dv.D * (size_t)dv.elem);
   ALLOC(dv.w1, (size_t)dv.D * dv.n_ev);
   ALLOC(dv.w2, (size_t)dv.n_ev);
   ALLOC(dv.err, 1);
@@ -430,21 +458,33 @@ extern "C" int nosa_cache_plan(NosaCtx* ctx, int layer, const int32_t* req, cons
   return NOSA_OK;
 }
 
-static int gather_memcpy(NosaCtx* ctx, int layer, cudaStream_t st) {
-  // copy-engine mover: the host learns the miss list (one sync) and batches the DMA copies
+// Copy-engine mover: once the layer's plan (recorded as `plan_done`) has executed, the host
+// reads the miss list back through pinned memory and submits every 32 KiB block copy as one
+// cudaMemcpyBatchAsync on `copy_st`.  Costs one host wait per layer; frees the SMs and L2
+// request queues that the zero-copy gather kernel occupies.
+static int gather_memcpy(NosaCtx* ctx, int layer, cudaEvent_t plan_done, cudaStream_t copy_st, bool timed) {
   const Dev& dv = ctx->dv;
-  CUDA_TRY(ctx, cudaStreamSynchronize(st));
-  int n = 0;
-  CUDA_TRY(ctx, cudaMemcpy(&n, dv.cnt + 2 * layer, sizeof(int), cudaMemcpyDeviceToHost));
+  if (!ctx->h_list) {
+    const size_t cap = (size_t)dv.B * dv.H * dv.C;
+    CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_list), cap * sizeof(int4), cudaHostAllocDefault));
+    CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_cnt), 16, cudaHostAllocDefault));
+    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->meta_stream, cudaStreamNonBlocking));
+  }
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->meta_stream, plan_done, 0));
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_cnt, dv.cnt + 2 * layer, sizeof(int), cudaMemcpyDeviceToHost, ctx->meta_stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->meta_stream));
+  const int n = ctx->h_cnt[0];
   if (n == 0) return NOSA_OK;
-  std::vector<int4> list(n);
-  CUDA_TRY(ctx, cudaMemcpy(list.data(), dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C, n * sizeof(int4),
-                           cudaMemcpyDeviceToHost));
-  std::vector<void*> dsts(n), srcs(n);
-  std::vector<size_t> sizes(n, (size_t)dv.bpb);
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_list, dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C, n * sizeof(int4),
+                                cudaMemcpyDeviceToHost, ctx->meta_stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->meta_stream));
+  ctx->b_dst.resize(n);
+  ctx->b_src.resize(n);
+  ctx->b_size.assign(n, (size_t)dv.bpb);
   for (int i = 0; i < n; ++i) {
-    srcs[i] = ctx->host_mirror + ((size_t)list[i].x * dv.NB + list[i].y) * dv.bpb;
-    dsts[i] = dv.pool + ((size_t)list[i].x * dv.C + list[i].z) * dv.bpb;
+    const int4 m = ctx->h_list[i];
+    ctx->b_src[i] = ctx->host_mirror + ((size_t)m.x * dv.NB + m.y) * dv.bpb;
+    ctx->b_dst[i] = dv.pool + ((size_t)m.x * dv.C + m.z) * dv.bpb;
   }
   cudaMemcpyAttributes attr{};
   attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
@@ -452,10 +492,14 @@ static int gather_memcpy(NosaCtx* ctx, int layer, cudaStream_t st) {
   attr.dstLocHint.type = cudaMemLocationTypeDevice;
   attr.dstLocHint.id = ctx->device;
   size_t idx0 = 0, fail_idx = 0;
-  cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &idx0, 1, &fail_idx, st);
-  if (e != cudaSuccess) {
+  TimeScope ts(ctx, copy_st, 1, timed);
+  cudaError_t e = cudaMemcpyBatchAsync(ctx->b_dst.data(), ctx->b_src.data(), ctx->b_size.data(), n, &attr, &idx0, 1,
+                                       &fail_idx, copy_st);
+  if (e != cudaSuccess) {  // driver without batched copies: one call per block
     cudaGetLastError();
-    for (int i = 0; i < n; ++i) CUDA_TRY(ctx, cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyHostToDevice, st));
+    ctx->batch_fallbacks += 1;
+    for (int i = 0; i < n; ++i)
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b_dst[i], ctx->b_src[i], ctx->b_size[i], cudaMemcpyHostToDevice, copy_st));
   }
   return NOSA_OK;
 }
@@ -464,7 +508,10 @@ extern "C" int nosa_gather(NosaCtx* ctx, int layer, int mode, void* stream) {
   int rc = check_layer(ctx, layer);
   if (rc) return rc;
   cudaSetDevice(ctx->device);
-  if (mode == NOSA_GATHER_MEMCPY) return gather_memcpy(ctx, layer, S(stream));
+  if (mode == NOSA_GATHER_MEMCPY) {
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[layer], S(stream)));
+    return gather_memcpy(ctx, layer, ctx->ev_plan[layer], S(stream), false);
+  }
   if (mode != NOSA_GATHER_UVA) return fail(ctx, NOSA_ERR_VALUE, "unknown gather mode %d", mode);
   CUDA_TRY(ctx, nosa::launch_gather(ctx->dv, layer, S(stream), ctx->gather_grid));
   ctx->launches += 1;
@@ -482,23 +529,6 @@ extern "C" int nosa_attend(NosaCtx* ctx, int layer, const void* q, const void* k
   ctx->launches += 2;
   return NOSA_OK;
 }
-
-// brackets one launch with timing events when timing is enabled (eager steps only)
-struct TimeScope {
-  NosaCtx* ctx;
-  cudaStream_t st;
-  NosaCtx::Timed* slot = nullptr;
-  TimeScope(NosaCtx* c, cudaStream_t s, int kind, bool on) : ctx(c), st(s) {
-    if (on && ctx->timing_used < ctx->timing.size()) {
-      slot = &ctx->timing[ctx->timing_used++];
-      slot->kind = kind;
-      cudaEventRecord(slot->a, st);
-    }
-  }
-  ~TimeScope() {
-    if (slot) cudaEventRecord(slot->b, st);
-  }
-};
 
 extern "C" int nosa_timing_enable(NosaCtx* ctx, int max_launches) {
   if (!ctx || max_launches < 0) return NOSA_ERR_VALUE;
@@ -555,9 +585,13 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   }
   for (int l = 0; l < dv.L; ++l) {
     CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_plan[l], 0));
-    {
+    if (io->gather_mode == NOSA_GATHER_MEMCPY) {
+      const int rc = gather_memcpy(ctx, l, ctx->ev_plan[l], ctx->copy_stream, timed);
+      if (rc) return rc;
+    } else {
       TimeScope ts(ctx, ctx->copy_stream, 1, timed);
       CUDA_TRY(ctx, nosa::launch_gather(dv, l, ctx->copy_stream, ctx->gather_grid));
+      if (count) ctx->launches += 1;
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[l], ctx->copy_stream));
   }
@@ -571,7 +605,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
     TimeScope ts(ctx, st, 3, timed);
     CUDA_TRY(ctx, nosa::launch_finalize(dv, l, kn + l * kstride, vn + l * kstride, io->out + l * ostride, st));
   }
-  if (count) ctx->launches += 4LL * dv.L;
+  if (count) ctx->launches += 3LL * dv.L;  // + the gather kernels counted above
   return NOSA_OK;
 }
 
@@ -580,24 +614,6 @@ extern "C" int nosa_decode_step(NosaCtx* ctx, const NosaStepIO* io, void* stream
     return fail(ctx, NOSA_ERR_VALUE, "decode_step: NULL io");
   if (io->selector != 0 && io->selector != 1) return fail(ctx, NOSA_ERR_VALUE, "selector must be nosa or infllmv2");
   cudaSetDevice(ctx->device);
-  if (io->gather_mode == NOSA_GATHER_MEMCPY) {
-    // host-planned copies: per layer, select+plan, sync, batched DMA, attend
-    const Dev& dv = ctx->dv;
-    const size_t qstride = (size_t)dv.B * dv.Hq * dv.D * dv.elem;
-    const size_t kstride = (size_t)dv.B * dv.H * dv.D * dv.elem;
-    const size_t ostride = (size_t)dv.B * dv.Hq * dv.D;
-    for (int l = 0; l < dv.L; ++l) {
-      int rc = nosa_select_plan(ctx, l, static_cast<const char*>(io->q) + l * qstride, io->selector, stream);
-      if (rc) return rc;
-      rc = gather_memcpy(ctx, l, S(stream));
-      if (rc) return rc;
-      rc = nosa_attend(ctx, l, static_cast<const char*>(io->q) + l * qstride,
-                       static_cast<const char*>(io->k_new) + l * kstride,
-                       static_cast<const char*>(io->v_new) + l * kstride, io->out + l * ostride, stream);
-      if (rc) return rc;
-    }
-    return NOSA_OK;
-  }
   return enqueue_step(ctx, io, S(stream), true);
 }
 

@@ -62,6 +62,7 @@ struct Dev {
   int4* miss_list;               // [L][B*H*C]  {lbh, blk, slot, 0}
   float* part_o;                 // [B*H][max_chunks][G][D]
   float2* part_ml;               // [B*H][max_chunks][G]
+  char* newrow;                  // [lbh][2][D] (elem): K and V row of the last block born by an append
   double* w1;                    // [D][n_ev]
   double* w2;                    // [n_ev]
   unsigned* err;

@@ -17,8 +17,17 @@ __global__ void __launch_bounds__(256) gather_kernel(Dev dv, int layer) {
   const int vecs = (int)(dv.bpb / 16);
   for (int e = blockIdx.x; e < n; e += gridDim.x) {
     const int4 m = list[e];
-    const int4* src = reinterpret_cast<const int4*>(dv.host + ((size_t)m.x * dv.NB + m.y) * dv.bpb);
     int4* dst = reinterpret_cast<int4*>(dv.pool + ((size_t)m.x * dv.C + m.z) * dv.bpb);
+    if (m.w) {  // born at the previous step: row 0 from the device stash, zeros elsewhere
+      const int row_vecs = dv.D * dv.elem / 16, plane_vecs = vecs / 2;
+      const int4* stash = reinterpret_cast<const int4*>(dv.newrow + (size_t)m.x * 2 * dv.D * dv.elem);
+      for (int i = threadIdx.x; i < vecs; i += blockDim.x) {
+        const int which = i / plane_vecs, in_plane = i - which * plane_vecs;
+        dst[i] = in_plane < row_vecs ? stash[which * row_vecs + in_plane] : make_int4(0, 0, 0, 0);
+      }
+      continue;
+    }
+    const int4* src = reinterpret_cast<const int4*>(dv.host + ((size_t)m.x * dv.NB + m.y) * dv.bpb);
     for (int base = threadIdx.x; base < vecs; base += blockDim.x * UNROLL) {
       int4 v[UNROLL];
 #pragma unroll

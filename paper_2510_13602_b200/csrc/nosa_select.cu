@@ -390,7 +390,14 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
     if (lane == 0 && nf > 0) base = atomicAdd(dv.cnt + 2 * layer, nf);
     base = __shfl_sync(0xffffffffu, base, 0);
     int4* ml = dv.miss_list + (size_t)layer * dv.B * dv.H * C;
-    for (int f = lane; f < nf; f += 32) ml[base + f] = make_int4(lbh, sm.fetch[f], sm.reqslot[sm.fpos[f]], 0);
+    // a block whose only token was appended at the previous step of this run is rebuilt from
+    // the device-side stash of that row (the slow copy holds the same bytes)
+    const int t_now = dv.t[lbh];
+    for (int f = lane; f < nf; f += 32) {
+      const int blk = sm.fetch[f];
+      const int born = (blk * dv.n_b == t_now - 1) && (t_now - 1 >= t0);
+      ml[base + f] = make_int4(lbh, blk, sm.reqslot[sm.fpos[f]], born);
+    }
     if (lane == 0) {
       dv.ftop[lbh] = top;
       long long* st = dv.stats + (size_t)lbh * ST_N;
