@@ -54,7 +54,8 @@ extern "C" {
 #define NOSA_DTYPE_FP32 1
 
 #define NOSA_GATHER_UVA 0     /* zero-copy SM gather kernel over mapped pinned memory     */
-#define NOSA_GATHER_MEMCPY 1  /* copy-engine path: host-planned cudaMemcpyAsync per miss  */
+#define NOSA_GATHER_MEMCPY 1  /* copy-engine path: host-planned cudaMemcpyBatchAsync        */
+#define NOSA_GATHER_TMA 2     /* TMA bulk copies pinned host -> shared -> HBM slot         */
 
 /* AttentionConfig (config.py:15-36) plus the engine extents of one GPU. */
 typedef struct NosaConfig {
@@ -86,6 +87,8 @@ typedef struct NosaStepIO {
   float* out;
   int32_t selector;    /* NOSA_SELECTOR_* */
   int32_t gather_mode; /* NOSA_GATHER_*   */
+  int32_t schedule;    /* 0 = layer-pipelined (gather of layer l overlaps scoring of l+1..),
+                          1 = layer-serial (select of layer l+1 after layer l completes) */
 } NosaStepIO;
 
 typedef struct NosaCtx NosaCtx;

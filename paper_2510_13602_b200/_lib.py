@@ -28,7 +28,8 @@ NOSA_ERR_STATE = 6
 SELECTOR = {"nosa": 0, "infllmv2": 1}
 VARIANT = {"ed-dma": 0, "s-dma": 1, "dma": 2}
 DTYPE = {"bf16": 0, "fp32": 1}
-GATHER = {"uva": 0, "memcpy": 1}
+GATHER = {"uva": 0, "memcpy": 1, "tma": 2}
+SCHEDULE = {"pipelined": 0, "serial": 1}
 
 
 class NosaConfig(ctypes.Structure):
@@ -44,7 +45,8 @@ class NosaStats(ctypes.Structure):
 
 class NosaStepIO(ctypes.Structure):
     _fields_ = [("q", ctypes.c_void_p), ("k_new", ctypes.c_void_p), ("v_new", ctypes.c_void_p),
-                ("out", ctypes.c_void_p), ("selector", ctypes.c_int32), ("gather_mode", ctypes.c_int32)]
+                ("out", ctypes.c_void_p), ("selector", ctypes.c_int32), ("gather_mode", ctypes.c_int32),
+                ("schedule", ctypes.c_int32)]
 
 
 # every symbol include/nosa_b200.h declares, with its ctypes signature

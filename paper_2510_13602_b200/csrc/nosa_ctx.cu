@@ -21,7 +21,7 @@ cudaError_t launch_start_run(const Dev& dv, int seq_begin, int seq_count, cudaSt
 cudaError_t launch_select_scores(int n_prob, const double* s_q, const double* s_e, int stride,
                                  const int* lo, const int* hi, int m_q, int m_e, int selector,
                                  int* out_q, int* n_q, int* out_e, int* n_e, cudaStream_t st);
-cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid);
+cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, bool tma);
 cudaError_t launch_prefill(const Dev& dv, int layer, int seq_begin, int S, const void* k,
                            const void* v, int t, char* staging, cudaStream_t st);
 cudaError_t launch_unswizzle(const char* src, char* dst, int nblocks, int n_b, int D, int elem,
@@ -39,7 +39,8 @@ struct NosaCtx {
   Dev dv{};
   int device = 0;
   int num_sms = 148;
-  int gather_grid = 32;
+  int gather_grid = 8;       // UVA gather CTAs: enough bytes in flight for the link, few SMs taken
+  int tma_gather_grid = 24;  // TMA gather CTAs (one warp, 4 x 32 KiB stages each)
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> ev_plan, ev_gather;
   char* host_mirror = nullptr;
@@ -220,7 +221,7 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   ctx->cfg = *cfg;
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;
-  if (const char* g = getenv("NOSA_GATHER_CTAS")) ctx->gather_grid = std::max(1, atoi(g));
+  if (const char* g = getenv("NOSA_GATHER_CTAS")) ctx->gather_grid = ctx->tma_gather_grid = std::max(1, atoi(g));
   const NosaConfig& c = *cfg;
   Dev& dv = ctx->dv;
   dv.B = c.batch;
@@ -512,8 +513,10 @@ extern "C" int nosa_gather(NosaCtx* ctx, int layer, int mode, void* stream) {
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[layer], S(stream)));
     return gather_memcpy(ctx, layer, ctx->ev_plan[layer], S(stream), false);
   }
-  if (mode != NOSA_GATHER_UVA) return fail(ctx, NOSA_ERR_VALUE, "unknown gather mode %d", mode);
-  CUDA_TRY(ctx, nosa::launch_gather(ctx->dv, layer, S(stream), ctx->gather_grid));
+  if (mode != NOSA_GATHER_UVA && mode != NOSA_GATHER_TMA)
+    return fail(ctx, NOSA_ERR_VALUE, "unknown gather mode %d", mode);
+  const bool tma = mode == NOSA_GATHER_TMA;
+  CUDA_TRY(ctx, nosa::launch_gather(ctx->dv, layer, S(stream), tma ? ctx->tma_gather_grid : ctx->gather_grid, tma));
   ctx->launches += 1;
   return NOSA_OK;
 }
@@ -576,26 +579,36 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   const char* vn = static_cast<const char*>(io->v_new);
   CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt, 0, (size_t)dv.L * 2 * sizeof(int), st));
   const bool timed = count;  // eager steps only (never inside a graph capture)
-  for (int l = 0; l < dv.L; ++l) {
+  // Layer-pipelined schedule: every layer's select+plan is issued first, so the miss gather of
+  // layer l overlaps the scoring of layers l+1.. (valid when each layer's query is known up
+  // front, as with per-layer query streams).  Layer-serial schedule: select(l) waits for
+  // finalize(l-1), as when q_{l+1} is computed from layer l's output.
+  const bool serial = io->schedule == 1;
+  auto select = [&](int l) -> int {
     {
       TimeScope ts(ctx, st, 0, timed);
       CUDA_TRY(ctx, nosa::launch_select_plan(dv, l, q + l * qstride, io->selector, 1, nullptr, nullptr, st));
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[l], st));
-  }
+    return NOSA_OK;
+  };
+  if (!serial)
+    for (int l = 0; l < dv.L; ++l)
+      if (int rc = select(l)) return rc;
   for (int l = 0; l < dv.L; ++l) {
+    if (serial)
+      if (int rc = select(l)) return rc;
     CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_plan[l], 0));
     if (io->gather_mode == NOSA_GATHER_MEMCPY) {
       const int rc = gather_memcpy(ctx, l, ctx->ev_plan[l], ctx->copy_stream, timed);
       if (rc) return rc;
     } else {
       TimeScope ts(ctx, ctx->copy_stream, 1, timed);
-      CUDA_TRY(ctx, nosa::launch_gather(dv, l, ctx->copy_stream, ctx->gather_grid));
+      const bool tma = io->gather_mode == NOSA_GATHER_TMA;
+      CUDA_TRY(ctx, nosa::launch_gather(dv, l, ctx->copy_stream, tma ? ctx->tma_gather_grid : ctx->gather_grid, tma));
       if (count) ctx->launches += 1;
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[l], ctx->copy_stream));
-  }
-  for (int l = 0; l < dv.L; ++l) {
     CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_gather[l], 0));
     {
       TimeScope ts(ctx, st, 2, timed);
@@ -619,7 +632,8 @@ extern "C" int nosa_decode_step(NosaCtx* ctx, const NosaStepIO* io, void* stream
 
 extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {
   if (!ctx || !io) return NOSA_ERR_VALUE;
-  if (io->gather_mode != NOSA_GATHER_UVA) return fail(ctx, NOSA_ERR_VALUE, "graph capture needs the UVA gather");
+  if (io->gather_mode == NOSA_GATHER_MEMCPY)
+    return fail(ctx, NOSA_ERR_VALUE, "graph capture needs a device-driven gather (uva or tma)");
   cudaSetDevice(ctx->device);
   if (ctx->graph_exec) { cudaGraphExecDestroy(ctx->graph_exec); ctx->graph_exec = nullptr; }
   if (ctx->graph) { cudaGraphDestroy(ctx->graph); ctx->graph = nullptr; }

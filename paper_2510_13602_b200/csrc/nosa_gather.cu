@@ -44,8 +44,78 @@ __global__ void __launch_bounds__(256) gather_kernel(Dev dv, int layer) {
   }
 }
 
-cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid) {
-  gather_kernel<8><<<grid, 256, 0, st>>>(dv, layer);
+// TMA variant: one warp per CTA streams blocks host -> shared (cp.async.bulk, mbarrier) ->
+// HBM slot (cp.async.bulk shared -> global, bulk groups) through a ring of stages, so the PCIe
+// reads are issued by the TMA engine in large requests instead of 16-byte SM loads.
+constexpr int kTmaStages = 4;
+
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__global__ void __launch_bounds__(32) gather_tma_kernel(Dev dv, int layer) {
+  extern __shared__ __align__(128) char smem_raw[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kTmaStages * dv.bpb);
+  const int n = *reinterpret_cast<volatile int*>(dv.cnt + 2 * layer);
+  const int4* list = dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C;
+  const int lane = threadIdx.x;
+  const int m = n > (int)blockIdx.x ? (n - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;  // items of this CTA
+  if (lane == 0) {
+    for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto item = [&](int k) { return list[blockIdx.x + (size_t)k * gridDim.x]; };
+  auto issue = [&](int k) {  // host -> stage (born blocks are written directly, see below)
+    const int4 e = item(k);
+    const int s = k % kTmaStages;
+    if (e.w) {
+      mbar_arrive_plain(&bars[s]);
+      return;
+    }
+    mbar_expect_tx(&bars[s], (unsigned)dv.bpb);
+    bulk_g2s(smem_raw + (size_t)s * dv.bpb, dv.host + ((size_t)e.x * dv.NB + e.y) * dv.bpb, (unsigned)dv.bpb, &bars[s]);
+  };
+  if (lane == 0)
+    for (int k = 0; k < min(kTmaStages, m); ++k) issue(k);
+  for (int k = 0; k < m; ++k) {
+    const int s = k % kTmaStages;
+    const int4 e = item(k);
+    char* dst = dv.pool + ((size_t)e.x * dv.C + e.z) * dv.bpb;
+    mbar_wait(&bars[s], (k / kTmaStages) & 1);
+    if (e.w) {  // born at the previous step: row 0 from the device stash, zeros elsewhere
+      const int vecs = (int)(dv.bpb / 16), row_vecs = dv.D * dv.elem / 16, plane_vecs = vecs / 2;
+      const int4* stash = reinterpret_cast<const int4*>(dv.newrow + (size_t)e.x * 2 * dv.D * dv.elem);
+      for (int i = lane; i < vecs; i += 32) {
+        const int which = i / plane_vecs, in_plane = i - which * plane_vecs;
+        reinterpret_cast<int4*>(dst)[i] = in_plane < row_vecs ? stash[which * row_vecs + in_plane] : make_int4(0, 0, 0, 0);
+      }
+      __syncwarp();
+    } else if (lane == 0) {
+      bulk_s2g(dst, smem_raw + (size_t)s * dv.bpb, (unsigned)dv.bpb);
+      bulk_commit();
+    }
+    if (lane == 0 && k + kTmaStages < m) {
+      bulk_wait_read_all();  // the store has finished reading stage s
+      issue(k + kTmaStages);
+    }
+  }
+  if (lane == 0) bulk_wait_all();
+}
+
+cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, bool tma) {
+  if (tma) {
+    const size_t smem = (size_t)kTmaStages * dv.bpb + kTmaStages * 8;
+    cudaFuncSetAttribute(gather_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    gather_tma_kernel<<<grid, 32, smem, st>>>(dv, layer);
+  } else {
+    gather_kernel<8><<<grid, 256, 0, st>>>(dv, layer);
+  }
   return cudaGetLastError();
 }
 

@@ -196,13 +196,18 @@ class NosaEngine:
             raise ValueError("head cache capacity exhausted")
 
     def step(self, q, k_new, v_new, selector: str = "nosa", out: torch.Tensor | None = None,
-             gather: str = "uva", check: bool = True) -> torch.Tensor:
+             gather: str = "uva", check: bool = True, schedule: str = "pipelined") -> torch.Tensor:
         """One decode step of every layer (DecodeEngine.step, decode.py:152-190).
 
         q: [layers][batch][n_head][d_head]; k_new, v_new: [layers][batch][n_kv_head][d_head].
-        Returns out [layers][batch][n_head][d_head] float32 (attention over tokens [0, t))."""
+        Returns out [layers][batch][n_head][d_head] float32 (attention over tokens [0, t)).
+        gather: "uva" (zero-copy SM kernel), "tma" (TMA bulk kernel) or "memcpy" (copy engine).
+        schedule: "pipelined" overlaps layer l's gather with the scoring of later layers;
+        "serial" runs layer by layer (results are identical)."""
         if selector not in SELECTORS:
             raise ValueError(f"selector must be one of {SELECTORS}")
+        if gather not in _lib.GATHER or schedule not in _lib.SCHEDULE:
+            raise ValueError(f"gather must be one of {tuple(_lib.GATHER)}, schedule one of {tuple(_lib.SCHEDULE)}")
         self._check_step()
         L, B, cfg = self.layers, self.batch, self.config
         q = self._dev(q).reshape(L, B, cfg.n_head, cfg.d_head)
@@ -211,7 +216,7 @@ class NosaEngine:
         if out is None:
             out = torch.empty((L, B, cfg.n_head, cfg.d_head), dtype=torch.float32, device=self.device)
         io = _lib.NosaStepIO(q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), out.data_ptr(),
-                             _lib.SELECTOR[selector], _lib.GATHER[gather])
+                             _lib.SELECTOR[selector], _lib.GATHER[gather], _lib.SCHEDULE[schedule])
         with torch.cuda.device(self.device):
             self._call(_lib.lib.nosa_decode_step, ctypes.byref(io), _lib.stream_ptr())
         self._t += 1
@@ -242,14 +247,14 @@ class NosaEngine:
 
     # ------------------------------------------------------------------ CUDA graph
     def capture(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, out: torch.Tensor,
-                selector: str = "nosa"):
+                selector: str = "nosa", gather: str = "uva", schedule: str = "pipelined"):
         """Capture one full step on fixed device buffers; replay() re-runs it."""
         self._check_step()
         for x in (q, k_new, v_new, out):
             if not x.is_contiguous() or x.device != self.device:
                 raise ValueError("graph buffers must be contiguous tensors on the engine's device")
         self._graph_io = _lib.NosaStepIO(q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), out.data_ptr(),
-                                         _lib.SELECTOR[selector], 0)
+                                         _lib.SELECTOR[selector], _lib.GATHER[gather], _lib.SCHEDULE[schedule])
         self._graph_bufs = (q, k_new, v_new, out)
         with torch.cuda.device(self.device):
             self._call(_lib.lib.nosa_step_graph_capture, ctypes.byref(self._graph_io))

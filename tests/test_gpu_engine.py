@@ -72,7 +72,7 @@ def test_engine_vs_reference_golden(golden, name, dtype):
 
 
 def _run_pair(cfg, *, batch, t0s, steps, fast_slots, seed, rho, selector="nosa", dtype="bf16", layers=1,
-              variant="ed-dma", check_residency=True, gather="uva"):
+              variant="ed-dma", check_residency=True, gather="uva", schedule="pipelined"):
     """GPU engine and oracle on identical inputs; returns the worst relative output error."""
     w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, seed)
     if variant == "dma":
@@ -97,7 +97,7 @@ def _run_pair(cfg, *, batch, t0s, steps, fast_slots, seed, rho, selector="nosa",
     worst = 0.0
     for s in range(steps):
         q, kn, vn = stream.next()
-        out = eng.step(q, kn, vn, selector=selector, gather=gather).cpu().numpy()
+        out = eng.step(q, kn, vn, selector=selector, gather=gather, schedule=schedule).cpu().numpy()
         ref, recs = orc.step(q, kn, vn, selector)
         for l in range(layers):
             sels, plans = eng.selections(l), eng.plans(l)
@@ -184,9 +184,31 @@ def test_block_sizes(n_b):
     _run_pair(cfg, batch=2, t0s=[40 * n_b + 3, 30 * n_b], steps=5, fast_slots=20, seed=10, rho=0.5)
 
 
-def test_memcpy_gather_matches_uva():
-    a = _run_pair(SMALL, batch=2, t0s=[900, 800], steps=5, fast_slots=36, seed=12, rho=0.0, gather="memcpy")
+@pytest.mark.parametrize("gather", ["memcpy", "tma"])
+def test_other_gather_paths_vs_oracle(gather):
+    a = _run_pair(SMALL, batch=2, t0s=[900, 800], steps=20, fast_slots=36, seed=12, rho=0.0, gather=gather)
     assert a <= TOL["bf16"]
+
+
+def test_gather_paths_and_schedules_bitwise_identical():
+    """The mover and the layer schedule change when bytes move, never what is computed."""
+    cfg = ONE_B_SMALL
+    w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, 2)
+    K, V = workload.prefix_kv(2, 6, cfg.n_kv_head, 3000, cfg.d_head)
+    K, V = K.reshape(3, 2, cfg.n_kv_head, 3000, cfg.d_head), V.reshape(3, 2, cfg.n_kv_head, 3000, cfg.d_head)
+    results = []
+    for gather, schedule in [("uva", "pipelined"), ("tma", "pipelined"), ("memcpy", "pipelined"), ("uva", "serial")]:
+        eng = NosaEngine(cfg, batch=2, layers=3, max_tokens=3100, fast_slots=70, w1=w1, w2=w2)
+        eng.prefill(torch.from_numpy(K), torch.from_numpy(V))
+        eng.start_run()
+        stream = workload.QueryStream(2, 3, 2, cfg.n_head, cfg.n_kv_head, cfg.d_head, 0.0)
+        outs = [eng.step(*stream.next(), gather=gather, schedule=schedule).cpu().numpy() for _ in range(70)]
+        st = eng.residency_stats()
+        results.append((np.stack(outs), st.hits, st.misses, st.evictions))
+        eng.close()
+    for r in results[1:]:
+        np.testing.assert_array_equal(r[0], results[0][0])
+        assert r[1:] == results[0][1:]
 
 
 def test_capacity_exceeded_is_raised():
