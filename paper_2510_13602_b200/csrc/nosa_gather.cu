@@ -5,42 +5,77 @@
 // whole layer at once: every (lbh, block, slot) entry the planner enqueued is copied from the
 // pinned, mapped host mirror into its HBM slot.  The SMs read host memory directly over PCIe
 // (zero-copy UVA), so the copy needs no host round trip to learn the miss list.
+#include <cstdlib>
+
 #include "nosa_device.cuh"
 
 namespace nosa {
 
 // grid = a few dozen CTAs (latency-bound on PCIe, leaves SMs to the attention kernel)
-template <int UNROLL>
+// 16-byte load from pinned host memory; with L2HINT the L2 fetches whole 256-byte lines
+// (ld.global.nc.L2::256B), so the PCIe read requests are larger.
+template <bool L2HINT>
+__device__ __forceinline__ int4 ld_host(const int4* p) {
+  if constexpr (L2HINT) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+  } else {
+    return __ldcs(p);
+  }
+}
+
+__device__ __forceinline__ void write_born_block(const Dev& dv, int4 m, int4* dst, int vecs) {
+  // born at the previous step: row 0 from the device stash, zeros elsewhere
+  const int row_vecs = dv.D * dv.elem / 16, plane_vecs = vecs / 2;
+  const int4* stash = reinterpret_cast<const int4*>(dv.newrow + (size_t)m.x * 2 * dv.D * dv.elem);
+  for (int i = threadIdx.x; i < vecs; i += blockDim.x) {
+    const int which = i / plane_vecs, in_plane = i - which * plane_vecs;
+    dst[i] = in_plane < row_vecs ? stash[which * row_vecs + in_plane] : make_int4(0, 0, 0, 0);
+  }
+}
+
+// Each CTA copies NBLK list entries per iteration: NBLK * bpb / (256 * 16) 16-byte loads per
+// thread are issued before any store, so NBLK * 32 KiB per CTA are in flight on the link.
+template <int NBLK, bool L2HINT>
 __global__ void __launch_bounds__(256) gather_kernel(Dev dv, int layer) {
+  constexpr int PER = 8;  // 16-byte vectors per thread per 32 KiB block at 256 threads
   const int n = *reinterpret_cast<volatile int*>(dv.cnt + 2 * layer);
   const int4* list = dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C;
   const int vecs = (int)(dv.bpb / 16);
-  for (int e = blockIdx.x; e < n; e += gridDim.x) {
-    const int4 m = list[e];
-    int4* dst = reinterpret_cast<int4*>(dv.pool + ((size_t)m.x * dv.C + m.z) * dv.bpb);
-    if (m.w) {  // born at the previous step: row 0 from the device stash, zeros elsewhere
-      const int row_vecs = dv.D * dv.elem / 16, plane_vecs = vecs / 2;
-      const int4* stash = reinterpret_cast<const int4*>(dv.newrow + (size_t)m.x * 2 * dv.D * dv.elem);
-      for (int i = threadIdx.x; i < vecs; i += blockDim.x) {
-        const int which = i / plane_vecs, in_plane = i - which * plane_vecs;
-        dst[i] = in_plane < row_vecs ? stash[which * row_vecs + in_plane] : make_int4(0, 0, 0, 0);
-      }
-      continue;
-    }
-    const int4* src = reinterpret_cast<const int4*>(dv.host + ((size_t)m.x * dv.NB + m.y) * dv.bpb);
-    for (int base = threadIdx.x; base < vecs; base += blockDim.x * UNROLL) {
-      int4 v[UNROLL];
+  for (int e0 = blockIdx.x * NBLK; e0 < n; e0 += gridDim.x * NBLK) {
+    int4 m[NBLK];
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        const int i = base + u * blockDim.x;
-        if (i < vecs) v[u] = __ldcs(src + i);
+    for (int j = 0; j < NBLK; ++j) m[j] = e0 + j < n ? list[e0 + j] : make_int4(-1, 0, 0, 0);
+    for (int base = threadIdx.x; base < vecs; base += blockDim.x * PER) {
+      int4 v[NBLK][PER];
+#pragma unroll
+      for (int j = 0; j < NBLK; ++j) {
+        if (m[j].x < 0 || m[j].w) continue;
+        const int4* src = reinterpret_cast<const int4*>(dv.host + ((size_t)m[j].x * dv.NB + m[j].y) * dv.bpb);
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int i = base + u * blockDim.x;
+          if (i < vecs) v[j][u] = ld_host<L2HINT>(src + i);
+        }
       }
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        const int i = base + u * blockDim.x;
-        if (i < vecs) dst[i] = v[u];
+      for (int j = 0; j < NBLK; ++j) {
+        if (m[j].x < 0 || m[j].w) continue;
+        int4* dst = reinterpret_cast<int4*>(dv.pool + ((size_t)m[j].x * dv.C + m[j].z) * dv.bpb);
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int i = base + u * blockDim.x;
+          if (i < vecs) dst[i] = v[j][u];
+        }
       }
     }
+#pragma unroll
+    for (int j = 0; j < NBLK; ++j)
+      if (m[j].x >= 0 && m[j].w)
+        write_born_block(dv, m[j], reinterpret_cast<int4*>(dv.pool + ((size_t)m[j].x * dv.C + m[j].z) * dv.bpb), vecs);
   }
 }
 
@@ -114,7 +149,14 @@ cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, b
     cudaFuncSetAttribute(gather_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     gather_tma_kernel<<<grid, 32, smem, st>>>(dv, layer);
   } else {
-    gather_kernel<8><<<grid, 256, 0, st>>>(dv, layer);
+    // NOSA_GATHER_VARIANT (experiments): bit 0 = two blocks per CTA iteration, bit 1 = L2::256B
+    static const int variant = getenv("NOSA_GATHER_VARIANT") ? atoi(getenv("NOSA_GATHER_VARIANT")) : 0;
+    switch (variant & 3) {
+      case 0: gather_kernel<1, false><<<grid, 256, 0, st>>>(dv, layer); break;
+      case 1: gather_kernel<2, false><<<grid, 256, 0, st>>>(dv, layer); break;
+      case 2: gather_kernel<1, true><<<grid, 256, 0, st>>>(dv, layer); break;
+      default: gather_kernel<2, true><<<grid, 256, 0, st>>>(dv, layer); break;
+    }
   }
   return cudaGetLastError();
 }
