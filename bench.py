@@ -77,8 +77,10 @@ def workload_dims(args, world):
         w["layers"] = args.layers
     if args.batch:
         w["batch"] = args.batch
-    w["batch_local"] = w["batch"] // world if w.get("strong") else w["batch"]
-    w["global_batch"] = w["batch"] if w.get("strong") else w["batch"] * world
+    from paper_2510_13602_b200.dist import shard_batch
+    rank = int(os.environ.get("RANK", "0"))
+    shard = shard_batch(w["batch"], world, rank, bool(w.get("strong")))
+    w["batch_local"], w["global_batch"] = shard.seq_count, shard.global_batch
     return w
 
 
@@ -159,6 +161,7 @@ def run_native(args, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2510_13602_b200 import NosaEngine, workload
+    from paper_2510_13602_b200.dist import max_over_ranks, rank_seed
 
     device = torch.device("cuda", local_rank)
     torch.cuda.set_device(device)
@@ -177,12 +180,12 @@ def run_native(args, rank, world, local_rank):
     eng = NosaEngine(cfg, batch=B, layers=L, max_tokens=max_tokens, fast_slots=fast, w1=w1, w2=w2, dtype="bf16",
                      device=local_rank)
     t_alloc = time.time() - t_setup
-    seed_base = args.seed * 1000003 + rank * 7919
+    seed_base = rank_seed(args.seed, rank)
     for l in range(L):
         shape = (B, cfg.n_kv_head, ctx_len, cfg.d_head)
         k = workload.torch_prefix_kv(seed_base + 2 * l, shape, device, dtype)
         v = workload.torch_prefix_kv(seed_base + 2 * l + 1, shape, device, dtype)
-        eng.prefill(k, v, layer=l)
+        eng.prefill(k, v, layer=l, resident=w["cache"] == "resident")
         del k, v
     eng.start_run()
     torch.cuda.synchronize(device)
@@ -227,11 +230,8 @@ def run_native(args, rank, world, local_rank):
     kern = eng.timing_read()
     eng.check_errors()
     st = eng.residency_stats()
-    ms_t = torch.tensor([ms], device=device)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    tokens = B * world * args.steps if not w.get("strong") else w["global_batch"] * args.steps
+    ms_max = max_over_ranks(ms, device)  # the slowest rank bounds the whole job
+    tokens = w["global_batch"] * args.steps
 
     # ---------------- end to end: host inputs H2D + step + D2H of the outputs, every step
     e2e = None
@@ -251,13 +251,11 @@ def run_native(args, rank, world, local_rank):
             host_out.copy_(out, non_blocking=True)
         e1.record()
         torch.cuda.synchronize(device)
-        e_ms = torch.tensor([e0.elapsed_time(e1)], device=device)
-        if world > 1:
-            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e_ms = max_over_ranks(e0.elapsed_time(e1), device)
         h2d = sum(x.numel() * x.element_size() for x in host_in[0])
-        e2e = {"value": round(tokens / (float(e_ms.item()) * 1e-3), 2), "unit": "tokens/s",
+        e2e = {"value": round(tokens / (e_ms * 1e-3), 2), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": host_out.numel() * 4,
-               "ms_per_step": round(float(e_ms.item()) / args.steps, 4),
+               "ms_per_step": round(e_ms / args.steps, 4),
                "api": "NosaEngine.step (C ABI nosa_decode_step) on host-copied inputs"}
         eng.check_errors()
 

@@ -129,6 +129,13 @@ int nosa_set_eviction_head(NosaCtx* ctx, const double* w1, const double* w2);
 int nosa_prefill(NosaCtx* ctx, int layer, int seq_begin, int seq_count, const void* k,
                  const void* v, int t, void* stream);
 
+/* nosa_prefill, then every cached block is also made fast-resident: block i of each
+ * (sequence, head) in slot i, as TieredBlockManager.allocate(FAST, ...) in block order
+ * (kv_manager.py:171-183).  The all-resident configuration; needs fast_slots >= blocks,
+ * else NOSA_ERR_CAPACITY. */
+int nosa_prefill_resident(NosaCtx* ctx, int layer, int seq_begin, int seq_count, const void* k,
+                          const void* v, int t, void* stream);
+
 /* BlockGeometry.for_run (selection.py:46-50) for every layer of the sequences: freezes
  * recent_start at the current cache length and ranks the frozen pool by its query-agnostic
  * score (the second phase of nosa_select, selection.py:151-156). */

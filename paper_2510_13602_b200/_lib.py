@@ -63,6 +63,7 @@ SIGNATURES = {
     "nosa_ctx_memory": (_I, [_P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "nosa_set_eviction_head": (_I, [_P, _F64P, _F64P]),
     "nosa_prefill": (_I, [_P, _I, _I, _I, _P, _P, _I, _P]),
+    "nosa_prefill_resident": (_I, [_P, _I, _I, _I, _P, _P, _I, _P]),
     "nosa_start_run": (_I, [_P, _I, _I, _P]),
     "nosa_select_plan": (_I, [_P, _I, _P, _I, _P]),
     "nosa_select": (_I, [_P, _I, _P, _I, _P]),

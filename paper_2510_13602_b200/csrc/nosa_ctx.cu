@@ -24,6 +24,7 @@ cudaError_t launch_select_scores(int n_prob, const double* s_q, const double* s_
 cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, bool tma);
 cudaError_t launch_prefill(const Dev& dv, int layer, int seq_begin, int S, const void* k,
                            const void* v, int t, char* staging, cudaStream_t st);
+cudaError_t launch_make_resident(const Dev& dv, int layer, int seq_begin, int S, int nblk, cudaStream_t st);
 cudaError_t launch_unswizzle(const char* src, char* dst, int nblocks, int n_b, int D, int elem,
                              cudaStream_t st);
 cudaError_t launch_attend(const Dev& dv, int layer, const void* q, const void* kn, const void* vn,
@@ -414,6 +415,27 @@ extern "C" int nosa_prefill(NosaCtx* ctx, int layer, int seq_begin, int seq_coun
   const size_t lbh0 = ((size_t)layer * dv.B + seq_begin) * dv.H;
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_mirror + lbh0 * dv.NB * (size_t)dv.bpb, ctx->staging, need,
                                 cudaMemcpyDeviceToHost, S(stream)));
+  return NOSA_OK;
+}
+
+extern "C" int nosa_prefill_resident(NosaCtx* ctx, int layer, int seq_begin, int seq_count, const void* k,
+                                     const void* v, int t, void* stream) {
+  int rc = nosa_prefill(ctx, layer, seq_begin, seq_count, k, v, t, stream);
+  if (rc) return rc;
+  const Dev& dv = ctx->dv;
+  const int nblk = (t + dv.n_b - 1) / dv.n_b;
+  if (nblk > dv.C)
+    return fail(ctx, NOSA_ERR_CAPACITY, "resident prefill of %d blocks needs fast_slots >= %d (have %d)", nblk, nblk,
+                dv.C);
+  if (nblk == 0) return NOSA_OK;
+  // the swizzled blocks are still in the staging buffer: copy them to slots [0, nblk) of every
+  // (sequence, head) and map block i -> slot i (allocate(FAST, ...) in block order)
+  const size_t lbh0 = ((size_t)layer * dv.B + seq_begin) * dv.H;
+  CUDA_TRY(ctx, cudaMemcpy2DAsync(dv.pool + lbh0 * dv.C * (size_t)dv.bpb, (size_t)dv.C * dv.bpb, ctx->staging,
+                                  (size_t)dv.NB * dv.bpb, (size_t)nblk * dv.bpb, (size_t)seq_count * dv.H,
+                                  cudaMemcpyDeviceToDevice, S(stream)));
+  CUDA_TRY(ctx, nosa::launch_make_resident(dv, layer, seq_begin, seq_count, nblk, S(stream)));
+  ctx->launches += 1;
   return NOSA_OK;
 }
 

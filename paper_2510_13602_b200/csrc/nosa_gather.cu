@@ -267,6 +267,24 @@ __global__ void reset_residency_kernel(Dev dv, int layer, int seq_begin, int S, 
     for (int d = threadIdx.x; d < dv.D; d += blockDim.x) dv.tail_ksum[(size_t)lbh * dv.D + d] = 0.0;
 }
 
+// Blocks [0, nblk) of S consecutive sequences become fast-resident in slots [0, nblk):
+// block i -> slot i, free stack holds [C-1 .. nblk] (what nblk LIFO pops leave behind).
+__global__ void make_resident_kernel(Dev dv, int layer, int seq_begin, int nblk) {
+  const int lbh = (layer * dv.B + seq_begin) * dv.H + blockIdx.x;
+  for (int i = threadIdx.x; i < dv.C; i += blockDim.x) {
+    dv.blk_of[(size_t)lbh * dv.C + i] = i < nblk ? i : -1;
+    dv.lastreq[(size_t)lbh * dv.C + i] = 0;
+    dv.fstack[(size_t)lbh * dv.C + i] = dv.C - 1 - i;
+  }
+  for (int i = threadIdx.x; i < dv.NB; i += blockDim.x) dv.slot_of[(size_t)lbh * dv.NB + i] = i < nblk ? i : -1;
+  if (threadIdx.x == 0) dv.ftop[lbh] = dv.C - nblk;
+}
+
+cudaError_t launch_make_resident(const Dev& dv, int layer, int seq_begin, int S, int nblk, cudaStream_t st) {
+  make_resident_kernel<<<S * dv.H, 256, 0, st>>>(dv, layer, seq_begin, nblk);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_prefill(const Dev& dv, int layer, int seq_begin, int S, const void* k,
                            const void* v, int t, char* staging, cudaStream_t st) {
   const int nblk = (t + dv.n_b - 1) / dv.n_b;

@@ -150,17 +150,19 @@ class NosaEngine:
         return d.value, h.value
 
     # ------------------------------------------------------------------ run setup
-    def prefill(self, k, v, layer: int | None = None, seq_begin: int = 0):
+    def prefill(self, k, v, layer: int | None = None, seq_begin: int = 0, resident: bool = False):
         """Cache a prefix (DecodeEngine.prefill, decode.py:139-146).
 
-        k, v: [layers][S][n_kv_head][t][d_head] (layer=None) or [S][n_kv_head][t][d_head]."""
+        k, v: [layers][S][n_kv_head][t][d_head] (layer=None) or [S][n_kv_head][t][d_head].
+        Every block starts in the slow tier (offload_sim.py:262-266); resident=True also places
+        all of them in HBM slots (the all-resident configuration)."""
         k = self._dev(k)
         v = self._dev(v)
         if layer is None:
             if k.dim() != 5:
                 raise ValueError("prefill over all layers expects [layers][S][H][t][D]")
             for l in range(k.shape[0]):
-                self.prefill(k[l], v[l], layer=l, seq_begin=seq_begin)
+                self.prefill(k[l], v[l], layer=l, seq_begin=seq_begin, resident=resident)
             return
         if k.dim() != 4 or k.shape != v.shape:
             raise ValueError("prefill expects k, v of shape [S][n_kv_head][t][d_head]")
@@ -170,7 +172,8 @@ class NosaEngine:
         if t > self.max_tokens:
             raise ValueError("head cache capacity exhausted")
         with torch.cuda.device(self.device):
-            self._call(_lib.lib.nosa_prefill, layer, seq_begin, S, k.data_ptr(), v.data_ptr(), t, _lib.stream_ptr())
+            fn = _lib.lib.nosa_prefill_resident if resident else _lib.lib.nosa_prefill
+            self._call(fn, layer, seq_begin, S, k.data_ptr(), v.data_ptr(), t, _lib.stream_ptr())
             torch.cuda.current_stream().synchronize()
         self._t[layer, seq_begin:seq_begin + S] = t
         for b in range(seq_begin, seq_begin + S):

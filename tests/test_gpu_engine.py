@@ -72,7 +72,7 @@ def test_engine_vs_reference_golden(golden, name, dtype):
 
 
 def _run_pair(cfg, *, batch, t0s, steps, fast_slots, seed, rho, selector="nosa", dtype="bf16", layers=1,
-              variant="ed-dma", check_residency=True, gather="uva", schedule="pipelined"):
+              variant="ed-dma", check_residency=True, gather="uva", schedule="pipelined", resident=False):
     """GPU engine and oracle on identical inputs; returns the worst relative output error."""
     w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, seed)
     if variant == "dma":
@@ -89,8 +89,12 @@ def _run_pair(cfg, *, batch, t0s, steps, fast_slots, seed, rho, selector="nosa",
         for b in range(batch):
             t = t0s[b]
             eng.prefill(torch.from_numpy(np.ascontiguousarray(K[l, b:b + 1, :, :t])),
-                        torch.from_numpy(np.ascontiguousarray(V[l, b:b + 1, :, :t])), layer=l, seq_begin=b)
+                        torch.from_numpy(np.ascontiguousarray(V[l, b:b + 1, :, :t])), layer=l, seq_begin=b,
+                        resident=resident)
             orc.prefill(l, b, K[l, b, :, :t], V[l, b, :, :t])
+            if resident:
+                for h in range(cfg.n_kv_head):
+                    orc.managers[l][b].make_resident(h, -(-t // cfg.n_b))
     eng.start_run()
     orc.start_run()
     stream = workload.QueryStream(seed, layers, batch, cfg.n_head, cfg.n_kv_head, cfg.d_head, rho)
@@ -182,6 +186,13 @@ def test_block_sizes(n_b):
     cfg = AttentionConfig(n=8192, d=1024, n_head=4, n_kv_head=2, d_head=128, n_b=n_b, n_s=n_b, n_w=4 * n_b,
                           k=16 * n_b, k_q=4 * n_b, k_e=12 * n_b)
     _run_pair(cfg, batch=2, t0s=[40 * n_b + 3, 30 * n_b], steps=5, fast_slots=20, seed=10, rho=0.5)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_resident_prefill(dtype):
+    # all-resident configuration: every prefix block placed in HBM at prefill (allocate(FAST))
+    _run_pair(SMALL, batch=2, t0s=[1000, 777], steps=30, fast_slots=70, seed=13, rho=0.0, dtype=dtype,
+              resident=True)
 
 
 @pytest.mark.parametrize("gather", ["memcpy", "tma"])
