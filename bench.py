@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--cpu-pairs", type=int, default=8, help="(sequence, layer) pairs in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="replay the step as one captured CUDA graph")
     return ap.parse_args()
 
 
@@ -209,7 +210,10 @@ def run_native(args, rank, world, local_rank):
     eng.reset_stats()
 
     # ---------------- timed region (value): inputs resident in HBM
-    eng.timing_enable(4 * L * args.steps + 8)
+    if args.graph:  # the whole step as one CUDA graph on fixed buffers, fed by D2D copies
+        gq, gk, gv = (torch.empty_like(x) for x in inputs[0])
+        eng.capture(gq, gk, gv, out, selector=args.selector, gather=args.gather, schedule=args.schedule)
+    eng.timing_enable(0 if args.graph else 4 * L * args.steps + 8)
     launches0 = eng.launch_count
     if world > 1:
         dist.barrier()
@@ -219,17 +223,27 @@ def run_native(args, rank, world, local_rank):
         ev0.record()
         for i in range(args.steps):
             q, kn, vn = inputs[i]
-            eng.step(q, kn, vn, selector=args.selector, out=out, gather=args.gather, check=False,
-                     schedule=args.schedule)
+            if args.graph:
+                gq.copy_(q); gk.copy_(kn); gv.copy_(vn)
+                eng.replay()
+            else:
+                eng.step(q, kn, vn, selector=args.selector, out=out, gather=args.gather, check=False,
+                         schedule=args.schedule)
         ev1.record()
         torch.cuda.synchronize(device)
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
     launches = eng.launch_count - launches0
-    kern = eng.timing_read()
     eng.check_errors()
     st = eng.residency_stats()
+    if args.graph:  # per-kernel durations from two eager steps right after (events need eager launches)
+        eng.timing_enable(4 * L * 2 + 8)
+        for i in range(2):
+            q, kn, vn = inputs[i]
+            eng.step(q, kn, vn, selector=args.selector, out=out, gather=args.gather, check=False,
+                     schedule=args.schedule)
+    kern = eng.timing_read()
     ms_max = max_over_ranks(ms, device)  # the slowest rank bounds the whole job
     tokens = w["global_batch"] * args.steps
 
@@ -321,6 +335,7 @@ def run_native(args, rank, world, local_rank):
                        "fast_slots_per_seq_head": fast, "blocks_per_seq_head": nblk,
                        "parallelism": f"dp{world} (batch-sharded, no data-path collective)",
                        "gather": args.gather, "schedule": args.schedule, "burn_in_steps": args.burn_in,
+                       "cuda_graph": bool(args.graph),
                        "l2": "no flush needed: attended KV per layer-step exceeds the 126 MB L2"},
             "h2d_miss_gbs": round(h2d_step / (step_ms * 1e-3) / 1e9, 3),
             "hit_rate": round(st.hit_rate, 4),
