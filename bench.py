@@ -213,7 +213,7 @@ def run_native(args, rank, world, local_rank):
     if args.graph:  # the whole step as one CUDA graph on fixed buffers, fed by D2D copies
         gq, gk, gv = (torch.empty_like(x) for x in inputs[0])
         eng.capture(gq, gk, gv, out, selector=args.selector, gather=args.gather, schedule=args.schedule)
-    eng.timing_enable(0 if args.graph else 4 * L * args.steps + 8)
+    eng.timing_enable(4 * L * args.steps + 8)  # eager steps and graph replays are timed per kernel
     launches0 = eng.launch_count
     if world > 1:
         dist.barrier()
@@ -237,12 +237,6 @@ def run_native(args, rank, world, local_rank):
     launches = eng.launch_count - launches0
     eng.check_errors()
     st = eng.residency_stats()
-    if args.graph:  # per-kernel durations from two eager steps right after (events need eager launches)
-        eng.timing_enable(4 * L * 2 + 8)
-        for i in range(2):
-            q, kn, vn = inputs[i]
-            eng.step(q, kn, vn, selector=args.selector, out=out, gather=args.gather, check=False,
-                     schedule=args.schedule)
     kern = eng.timing_read()
     ms_max = max_over_ranks(ms, device)  # the slowest rank bounds the whole job
     tokens = w["global_batch"] * args.steps

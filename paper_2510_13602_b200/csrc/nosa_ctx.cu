@@ -59,6 +59,12 @@ struct NosaCtx {
   struct Timed { cudaEvent_t a, b; int kind; };
   std::vector<Timed> timing;       // pre-created event pairs
   size_t timing_used = 0;
+  // graph capture of the timing scopes: placeholder events and the event-record nodes
+  bool capturing = false;
+  std::vector<Timed> cap_events;
+  size_t cap_used = 0;
+  struct EvNode { cudaGraphNode_t node; int slot; int end; };
+  std::vector<EvNode> ev_nodes;
   std::atomic<long long> launches{0};
   std::string err;
   // copy-engine gather (NOSA_GATHER_MEMCPY): pinned readback of the miss list + batch arrays
@@ -71,19 +77,32 @@ struct NosaCtx {
 };
 
 // brackets one launch with timing events when timing is enabled (eager steps only)
+// During graph capture the same scope records into placeholder events as external event-record
+// nodes; every replay re-points those nodes at fresh events of the timing pool, so a graph
+// replay is timed per kernel exactly like an eager step.
 struct TimeScope {
   NosaCtx* ctx;
   cudaStream_t st;
   NosaCtx::Timed* slot = nullptr;
+  bool capture = false;
   TimeScope(NosaCtx* c, cudaStream_t s, int kind, bool on) : ctx(c), st(s) {
-    if (on && ctx->timing_used < ctx->timing.size()) {
+    if (ctx->capturing) {
+      if (ctx->cap_used < ctx->cap_events.size()) {
+        slot = &ctx->cap_events[ctx->cap_used++];
+        slot->kind = kind;
+        capture = true;
+        cudaEventRecordWithFlags(slot->a, st, cudaEventRecordExternal);
+      }
+    } else if (on && ctx->timing_used < ctx->timing.size()) {
       slot = &ctx->timing[ctx->timing_used++];
       slot->kind = kind;
       cudaEventRecord(slot->a, st);
     }
   }
   ~TimeScope() {
-    if (slot) cudaEventRecord(slot->b, st);
+    if (!slot) return;
+    if (capture) cudaEventRecordWithFlags(slot->b, st, cudaEventRecordExternal);
+    else cudaEventRecord(slot->b, st);
   }
 };
 
@@ -185,10 +204,11 @@ static void release(NosaCtx* ctx) {
   if (ctx->meta_stream) cudaStreamDestroy(ctx->meta_stream);
   if (ctx->h_list) cudaFreeHost(ctx->h_list);
   if (ctx->h_cnt) cudaFreeHost(ctx->h_cnt);
-  for (auto& t : ctx->timing) {
-    cudaEventDestroy(t.a);
-    cudaEventDestroy(t.b);
-  }
+  for (auto* pool : {&ctx->timing, &ctx->cap_events})
+    for (auto& t : *pool) {
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
+    }
   for (void* p : ctx->dev_allocs) cudaFree(p);
   if (ctx->staging) cudaFree(ctx->staging);
   if (ctx->host_mirror) {
@@ -659,20 +679,61 @@ extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {
   cudaSetDevice(ctx->device);
   if (ctx->graph_exec) { cudaGraphExecDestroy(ctx->graph_exec); ctx->graph_exec = nullptr; }
   if (ctx->graph) { cudaGraphDestroy(ctx->graph); ctx->graph = nullptr; }
+  // placeholder events for the per-kernel timing scopes (4 kernels per layer)
+  const size_t nslots = 4 * (size_t)ctx->dv.L;
+  while (ctx->cap_events.size() < nslots) {
+    NosaCtx::Timed t{};
+    CUDA_TRY(ctx, cudaEventCreate(&t.a));
+    CUDA_TRY(ctx, cudaEventCreate(&t.b));
+    ctx->cap_events.push_back(t);
+  }
+  ctx->cap_used = 0;
+  ctx->capturing = true;
   CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->capture_stream, cudaStreamCaptureModeThreadLocal));
   int rc = enqueue_step(ctx, io, ctx->capture_stream, false);
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(ctx->capture_stream, &g);
+  ctx->capturing = false;
   if (rc) return rc;
   if (e != cudaSuccess) return fail(ctx, NOSA_ERR_CUDA, "stream capture: %s", cudaGetErrorString(e));
   ctx->graph = g;
   CUDA_TRY(ctx, cudaGraphInstantiate(&ctx->graph_exec, g, 0));
   ctx->graph_kernels = 4 * ctx->dv.L;
+  // map every event-record node back to its timing scope
+  ctx->ev_nodes.clear();
+  size_t n = 0;
+  CUDA_TRY(ctx, cudaGraphGetNodes(g, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  CUDA_TRY(ctx, cudaGraphGetNodes(g, nodes.data(), &n));
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType ty;
+    CUDA_TRY(ctx, cudaGraphNodeGetType(nd, &ty));
+    if (ty != cudaGraphNodeTypeEventRecord) continue;
+    cudaEvent_t ev;
+    CUDA_TRY(ctx, cudaGraphEventRecordNodeGetEvent(nd, &ev));
+    for (size_t i = 0; i < ctx->cap_used; ++i) {
+      if (ctx->cap_events[i].a == ev) ctx->ev_nodes.push_back({nd, (int)i, 0});
+      if (ctx->cap_events[i].b == ev) ctx->ev_nodes.push_back({nd, (int)i, 1});
+    }
+  }
   return NOSA_OK;
 }
 
 extern "C" int nosa_step_graph_launch(NosaCtx* ctx, void* stream) {
   if (!ctx || !ctx->graph_exec) return fail(ctx, NOSA_ERR_STATE, "no captured step graph");
+  const size_t slots = ctx->cap_used;
+  if (slots && ctx->timing_used + slots <= ctx->timing.size()) {  // time this replay per kernel
+    for (const auto& en : ctx->ev_nodes) {
+      NosaCtx::Timed& t = ctx->timing[ctx->timing_used + en.slot];
+      t.kind = ctx->cap_events[en.slot].kind;
+      CUDA_TRY(ctx, cudaGraphExecEventRecordNodeSetEvent(ctx->graph_exec, en.node, en.end ? t.b : t.a));
+    }
+    ctx->timing_used += slots;
+  } else if (slots) {  // timing pool exhausted: park the nodes on the placeholders
+    for (const auto& en : ctx->ev_nodes)
+      CUDA_TRY(ctx, cudaGraphExecEventRecordNodeSetEvent(
+                        ctx->graph_exec, en.node, en.end ? ctx->cap_events[en.slot].b : ctx->cap_events[en.slot].a));
+  }
   CUDA_TRY(ctx, cudaGraphLaunch(ctx->graph_exec, S(stream)));
   ctx->launches += ctx->graph_kernels;
   return NOSA_OK;

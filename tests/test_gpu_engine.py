@@ -264,10 +264,15 @@ def test_graph_replay_matches_eager():
             if use_graph:
                 if s == 0:
                     eng.capture(qb, kb, vb, ob)
+                    eng.timing_enable(4 * 3 + 1)  # room for three timed replays
                 eng.replay()
             else:
                 eng.step(qb, kb, vb, out=ob)
             res.append(ob.cpu().numpy().copy())
+        if use_graph:  # replays are timed per kernel through the re-pointed event-record nodes
+            timing = eng.timing_read()
+            assert [timing[k]["launches"] for k in eng.KERNEL_KINDS] == [3, 3, 3, 3]
+            assert all(timing[k]["total_ms"] > 0 for k in ("select_plan", "attend", "finalize"))
         outs.append(np.stack(res))
         eng.close()
     np.testing.assert_array_equal(outs[0], outs[1])  # same kernels, same decomposition: bitwise equal
