@@ -63,7 +63,8 @@ def parse():
     ap.add_argument("--cpu-pairs", type=int, default=8, help="(sequence, layer) pairs in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--graph", action="store_true", help="replay the step as one captured CUDA graph")
+    ap.add_argument("--eager", action="store_true",
+                    help="launch every kernel from the host instead of replaying the captured step graph")
     return ap.parse_args()
 
 
@@ -205,15 +206,26 @@ def run_native(args, rank, world, local_rank):
         if i < cpu_steps:
             first_inputs.append((q, kn, vn))
             warm_out.append(out.clone())
-    inputs = [stream.next() for _ in range(args.steps * (1 if args.no_e2e else 2))]
+    # K steps for the clean timed region, K for the instrumented pass, K for the e2e pass
+    inputs = [stream.next() for _ in range(args.steps * (2 if args.no_e2e else 3))]
     torch.cuda.synchronize(device)
     eng.reset_stats()
-
-    # ---------------- timed region (value): inputs resident in HBM
-    if args.graph:  # the whole step as one CUDA graph on fixed buffers, fed by D2D copies
+    use_graph = args.gather != "memcpy" and not args.eager
+    if use_graph:  # the whole step as one CUDA graph on fixed buffers, fed by D2D copies
         gq, gk, gv = (torch.empty_like(x) for x in inputs[0])
         eng.capture(gq, gk, gv, out, selector=args.selector, gather=args.gather, schedule=args.schedule)
-    eng.timing_enable(4 * L * args.steps + 8)  # eager steps and graph replays are timed per kernel
+
+    def run_steps(batch_inputs):
+        for q, kn, vn in batch_inputs:
+            if use_graph:
+                gq.copy_(q); gk.copy_(kn); gv.copy_(vn)
+                eng.replay()
+            else:
+                eng.step(q, kn, vn, selector=args.selector, out=out, gather=args.gather, check=False,
+                         schedule=args.schedule)
+
+    # ---------------- timed region (value): inputs resident in HBM, no instrumentation
+    eng.timing_enable(0)
     launches0 = eng.launch_count
     if world > 1:
         dist.barrier()
@@ -221,14 +233,7 @@ def run_native(args, rank, world, local_rank):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clocks:
         ev0.record()
-        for i in range(args.steps):
-            q, kn, vn = inputs[i]
-            if args.graph:
-                gq.copy_(q); gk.copy_(kn); gv.copy_(vn)
-                eng.replay()
-            else:
-                eng.step(q, kn, vn, selector=args.selector, out=out, gather=args.gather, check=False,
-                         schedule=args.schedule)
+        run_steps(inputs[:args.steps])
         ev1.record()
         torch.cuda.synchronize(device)
     if world > 1:
@@ -237,14 +242,28 @@ def run_native(args, rank, world, local_rank):
     launches = eng.launch_count - launches0
     eng.check_errors()
     st = eng.residency_stats()
-    kern = eng.timing_read()
     ms_max = max_over_ranks(ms, device)  # the slowest rank bounds the whole job
     tokens = w["global_batch"] * args.steps
+
+    # ---------------- instrumented pass: the next K steps with every kernel bracketed by CUDA
+    # events on its own stream (event nodes inside the graph); gives the per-kernel durations
+    eng.reset_stats()
+    eng.timing_enable(4 * L * args.steps + 8)
+    ei0, ei1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ei0.record()
+    run_steps(inputs[args.steps:2 * args.steps])
+    ei1.record()
+    torch.cuda.synchronize(device)
+    kern = eng.timing_read()
+    st_i = eng.residency_stats()
+    instrumented_ms = ei0.elapsed_time(ei1) / args.steps
+    eng.timing_enable(0)
+    inputs_e2e = inputs[2 * args.steps:]
 
     # ---------------- end to end: host inputs H2D + step + D2H of the outputs, every step
     e2e = None
     if not args.no_e2e:
-        host_in = [tuple(x.cpu().pin_memory() for x in inputs[i]) for i in range(args.steps, 2 * args.steps)]
+        host_in = [tuple(x.cpu().pin_memory() for x in step_in) for step_in in inputs_e2e]
         dq, dk, dv = (torch.empty_like(x) for x in inputs[0])
         host_out = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
         if world > 1:
@@ -253,9 +272,13 @@ def run_native(args, rank, world, local_rank):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for hq, hk, hv in host_in:
-            dq.copy_(hq, non_blocking=True); dk.copy_(hk, non_blocking=True); dv.copy_(hv, non_blocking=True)
-            eng.step(dq, dk, dv, selector=args.selector, out=out, gather=args.gather, check=False,
-                     schedule=args.schedule)
+            if use_graph:  # straight into the graph's input buffers
+                gq.copy_(hq, non_blocking=True); gk.copy_(hk, non_blocking=True); gv.copy_(hv, non_blocking=True)
+                eng.replay()
+            else:
+                dq.copy_(hq, non_blocking=True); dk.copy_(hk, non_blocking=True); dv.copy_(hv, non_blocking=True)
+                eng.step(dq, dk, dv, selector=args.selector, out=out, gather=args.gather, check=False,
+                         schedule=args.schedule)
             host_out.copy_(out, non_blocking=True)
         e1.record()
         torch.cuda.synchronize(device)
@@ -264,22 +287,24 @@ def run_native(args, rank, world, local_rank):
         e2e = {"value": round(tokens / (e_ms * 1e-3), 2), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": host_out.numel() * 4,
                "ms_per_step": round(e_ms / args.steps, 4),
-               "api": "NosaEngine.step (C ABI nosa_decode_step) on host-copied inputs"}
+               "api": ("NosaEngine.capture/replay (C ABI nosa_step_graph_launch)" if use_graph else
+                       "NosaEngine.step (C ABI nosa_decode_step)") + " on inputs copied from pinned host memory"}
         eng.check_errors()
 
     # ---------------- roofline arithmetic (algorithmic bytes, SURVEY.md §8d / DESIGN.md)
     hbm_peak, peak_kind = peaks()
     bpb = eng.bytes_per_block
-    calls = L * args.steps  # launches per kernel kind in the timed region
-    R_total = st.hits + st.misses                     # attended blocks, summed
+    calls = L * args.steps  # launches per kernel kind in the instrumented pass
+    R_total = st.hits + st.misses                     # attended blocks, summed (timed region)
+    R_inst = st_i.hits + st_i.misses                  # the same over the instrumented pass
     P = eng.geometry[0].pool_blocks.stop - eng.geometry[0].pool_blocks.start
     per_launch = {
         # K1+K2: f64 K_c pool scan + q read + tables (reads of required-list metadata are small)
         "select_plan": (B * cfg.n_kv_head * P * cfg.d_head * 8 + B * cfg.n_head * cfg.d_head * 2),
         # K3: each missed block crosses PCIe once and is written to HBM once
-        "gather": st.misses * bpb / calls,
+        "gather": (st_i.misses - st_i.new_blocks) * bpb / calls,
         # K4: K|V of every attended block + its bias + the query rows
-        "attend": (R_total * (bpb + 4)) / calls + B * cfg.n_head * cfg.d_head * 2,
+        "attend": (R_inst * (bpb + 4)) / calls + B * cfg.n_head * cfg.d_head * 2,
         # K4 merge + K5: f32 outputs + the appended K/V row (HBM slot)
         "finalize": B * cfg.n_head * cfg.d_head * 4 + B * cfg.n_kv_head * 2 * cfg.d_head * 2,
     }
@@ -295,12 +320,17 @@ def run_native(args, rank, world, local_rank):
                 "peak": hbm_peak, "unit": "GB/s", "frac": round(att["gbs"] / hbm_peak, 4), "traffic": traffic,
                 "peak_kind": peak_kind, "bytes_per_launch": int(per_launch["attend"]),
                 "avg_launch_ms": round(att["avg_ms"], 5)}
-    hbm_step = (per_launch["select_plan"] + per_launch["attend"] + per_launch["finalize"] + per_launch["gather"]) * L
-    h2d_step = st.misses * bpb / args.steps
+    # step-level bytes from the uninstrumented timed region; blocks born by an append are rebuilt
+    # on the device and never cross PCIe (the reference still counts them as misses)
+    h2d_step = (st.misses - st.new_blocks) * bpb / args.steps
+    hbm_step = (per_launch["select_plan"] + per_launch["finalize"]) * L + \
+        (R_total * (bpb + 4) / args.steps + L * B * cfg.n_head * cfg.d_head * 2) + h2d_step
     t_roof = max(hbm_step / 8e12, h2d_step / (link_gbs * 1e9))
     step_ms = ms_max / args.steps
     g = kern["gather"]
-    link_roofline = {"bound": "pcie-h2d", "kernel": "gather_kernel (K3, UVA zero-copy)",
+    gather_name = {"uva": "gather_kernel (K3, UVA zero-copy SM loads)", "tma": "gather_tma_kernel (K3, TMA bulk)",
+                   "memcpy": "cudaMemcpyBatchAsync (K3, copy engine)"}[args.gather]
+    link_roofline = {"bound": "pcie-h2d", "kernel": gather_name,
                      "achieved": round(g["gbs"], 2) if g["gbs"] else 0.0, "peak": round(link_gbs, 2), "unit": "GB/s",
                      "frac": round(g["gbs"] / link_gbs, 4) if g["gbs"] else 0.0,
                      "peak_kind": "measured pinned 1 GiB H2D cudaMemcpyAsync, best of 10"}
@@ -329,7 +359,10 @@ def run_native(args, rank, world, local_rank):
                        "fast_slots_per_seq_head": fast, "blocks_per_seq_head": nblk,
                        "parallelism": f"dp{world} (batch-sharded, no data-path collective)",
                        "gather": args.gather, "schedule": args.schedule, "burn_in_steps": args.burn_in,
-                       "cuda_graph": bool(args.graph),
+                       "cuda_graph": use_graph,
+                       "kernel_timing": "instrumented pass: the K steps after the timed region with CUDA events "
+                                        "around every kernel on its own stream (event nodes in the graph); "
+                                        "value comes from the uninstrumented region",
                        "l2": "no flush needed: attended KV per layer-step exceeds the 126 MB L2"},
             "h2d_miss_gbs": round(h2d_step / (step_ms * 1e-3) / 1e9, 3),
             "hit_rate": round(st.hit_rate, 4),
@@ -339,6 +372,7 @@ def run_native(args, rank, world, local_rank):
             "roofline": roofline, "link_roofline": link_roofline, "step_roofline": step_roofline,
             "kernels": {k_: {"avg_ms": round(v["avg_ms"], 5), "launches": v["launches"],
                              "gbs": round(v["gbs"], 2) if v["gbs"] else None} for k_, v in kern.items()},
+            "instrumented_ms_per_step": round(instrumented_ms, 4),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(),
             "setup_s": {"alloc_and_pin": round(t_alloc, 1), "prefill": round(t_prefill, 1)},

@@ -1,5 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/gpu_tests.log 2>&1; echo rc=$? >> gpurun_out/gpu_tests.log
-timeout 900 python bench.py --graph > gpurun_out/bench_full_graph.log 2>&1; echo rc=$? >> gpurun_out/bench_full_graph.log
-timeout 900 python bench.py --workload cfg2 --graph --no-cpu-baseline > gpurun_out/bench_cfg2_graph.log 2>&1; echo rc=$? >> gpurun_out/bench_cfg2_graph.log
+timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1; echo rc=$? >> gpurun_out/bench_full.log
+timeout 900 python bench.py --workload cfg2 --no-cpu-baseline > gpurun_out/bench_cfg2.log 2>&1; echo rc=$? >> gpurun_out/bench_cfg2.log
+timeout 900 python bench.py --gather memcpy --no-cpu-baseline > gpurun_out/bench_full_memcpy.log 2>&1; echo rc=$? >> gpurun_out/bench_full_memcpy.log
