@@ -170,7 +170,7 @@ def run_native(args, rank, world, local_rank):
     w = workload_dims(args, world)
     cfg = attention_config(w["shape"])
     L, B, ctx_len = w["layers"], w["batch_local"], w["context"]
-    total_steps = args.burn_in + args.warmup + args.steps * (1 if args.no_e2e else 2)
+    total_steps = args.burn_in + args.warmup + args.steps * (2 if args.no_e2e else 3)
     max_tokens = ctx_len + total_steps + 2
     nblk = -(-max_tokens // cfg.n_b)
     fast = nblk if w["cache"] == "resident" else int(w["cache"] * nblk)
