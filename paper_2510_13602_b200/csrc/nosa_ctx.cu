@@ -65,6 +65,7 @@ struct NosaCtx {
   size_t cap_used = 0;
   struct EvNode { cudaGraphNode_t node; int slot; int end; };
   std::vector<EvNode> ev_nodes;
+  bool nodes_on_pool = false;  // the nodes currently point at timing-pool events
   std::atomic<long long> launches{0};
   std::string err;
   // copy-engine gather (NOSA_GATHER_MEMCPY): pinned readback of the miss list + batch arrays
@@ -121,8 +122,10 @@ static int fail(NosaCtx* ctx, int code, const char* fmt, ...) {
 #define CUDA_TRY(ctx, expr)                                                                   \
   do {                                                                                       \
     cudaError_t _e = (expr);                                                                 \
-    if (_e != cudaSuccess)                                                                   \
+    if (_e != cudaSuccess) {                                                                 \
+      cudaGetLastError(); /* a non-sticky error must not leak into the next call */          \
       return fail(ctx, NOSA_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));       \
+    }                                                                                        \
   } while (0)
 
 static int budgets(const NosaConfig& c, int* bq, int* be, int* bt) {
@@ -579,6 +582,14 @@ extern "C" int nosa_timing_enable(NosaCtx* ctx, int max_launches) {
   if (!ctx || max_launches < 0) return NOSA_ERR_VALUE;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
+  // captured event-record nodes may point into the pool: park them on their placeholders
+  // before the pool's events are destroyed
+  if (ctx->graph_exec && ctx->nodes_on_pool) {
+    for (const auto& en : ctx->ev_nodes)
+      CUDA_TRY(ctx, cudaGraphExecEventRecordNodeSetEvent(
+                        ctx->graph_exec, en.node, en.end ? ctx->cap_events[en.slot].b : ctx->cap_events[en.slot].a));
+    ctx->nodes_on_pool = false;
+  }
   for (auto& t : ctx->timing) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
@@ -701,6 +712,7 @@ extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {
   ctx->graph_kernels = 4 * ctx->dv.L;
   // map every event-record node back to its timing scope
   ctx->ev_nodes.clear();
+  ctx->nodes_on_pool = false;  // freshly instantiated: the nodes hold the placeholders
   size_t n = 0;
   CUDA_TRY(ctx, cudaGraphGetNodes(g, nullptr, &n));
   std::vector<cudaGraphNode_t> nodes(n);
@@ -729,10 +741,12 @@ extern "C" int nosa_step_graph_launch(NosaCtx* ctx, void* stream) {
       CUDA_TRY(ctx, cudaGraphExecEventRecordNodeSetEvent(ctx->graph_exec, en.node, en.end ? t.b : t.a));
     }
     ctx->timing_used += slots;
-  } else if (slots) {  // timing pool exhausted: park the nodes on the placeholders
+    ctx->nodes_on_pool = true;
+  } else if (slots && ctx->nodes_on_pool) {  // timing off or pool exhausted: back to placeholders
     for (const auto& en : ctx->ev_nodes)
       CUDA_TRY(ctx, cudaGraphExecEventRecordNodeSetEvent(
                         ctx->graph_exec, en.node, en.end ? ctx->cap_events[en.slot].b : ctx->cap_events[en.slot].a));
+    ctx->nodes_on_pool = false;
   }
   CUDA_TRY(ctx, cudaGraphLaunch(ctx->graph_exec, S(stream)));
   ctx->launches += ctx->graph_kernels;
