@@ -52,8 +52,8 @@ struct NosaCtx {
   char* staging = nullptr;
   size_t staging_bytes = 0;
   bool have_evhead = false;
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t graph_exec = nullptr;
+  cudaGraph_t graph = nullptr, graph_timed = nullptr;              // clean / instrumented step
+  cudaGraphExec_t graph_exec = nullptr, graph_exec_timed = nullptr;
   cudaStream_t capture_stream = nullptr;
   int graph_kernels = 0;
   struct Timed { cudaEvent_t a, b; int kind; };
@@ -198,8 +198,10 @@ static void release(NosaCtx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
-  if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
-  if (ctx->graph) cudaGraphDestroy(ctx->graph);
+  for (cudaGraphExec_t x : {ctx->graph_exec, ctx->graph_exec_timed})
+    if (x) cudaGraphExecDestroy(x);
+  for (cudaGraph_t x : {ctx->graph, ctx->graph_timed})
+    if (x) cudaGraphDestroy(x);
   if (ctx->capture_stream) cudaStreamDestroy(ctx->capture_stream);
   for (auto e : ctx->ev_plan) cudaEventDestroy(e);
   for (auto e : ctx->ev_gather) cudaEventDestroy(e);
@@ -584,10 +586,10 @@ extern "C" int nosa_timing_enable(NosaCtx* ctx, int max_launches) {
   cudaDeviceSynchronize();
   // captured event-record nodes may point into the pool: park them on their placeholders
   // before the pool's events are destroyed
-  if (ctx->graph_exec && ctx->nodes_on_pool) {
+  if (ctx->graph_exec_timed && ctx->nodes_on_pool) {
     for (const auto& en : ctx->ev_nodes)
       CUDA_TRY(ctx, cudaGraphExecEventRecordNodeSetEvent(
-                        ctx->graph_exec, en.node, en.end ? ctx->cap_events[en.slot].b : ctx->cap_events[en.slot].a));
+                        ctx->graph_exec_timed, en.node, en.end ? ctx->cap_events[en.slot].b : ctx->cap_events[en.slot].a));
     ctx->nodes_on_pool = false;
   }
   for (auto& t : ctx->timing) {
@@ -688,9 +690,26 @@ extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {
   if (io->gather_mode == NOSA_GATHER_MEMCPY)
     return fail(ctx, NOSA_ERR_VALUE, "graph capture needs a device-driven gather (uva or tma)");
   cudaSetDevice(ctx->device);
-  if (ctx->graph_exec) { cudaGraphExecDestroy(ctx->graph_exec); ctx->graph_exec = nullptr; }
-  if (ctx->graph) { cudaGraphDestroy(ctx->graph); ctx->graph = nullptr; }
-  // placeholder events for the per-kernel timing scopes (4 kernels per layer)
+  for (cudaGraphExec_t* x : {&ctx->graph_exec, &ctx->graph_exec_timed})
+    if (*x) { cudaGraphExecDestroy(*x); *x = nullptr; }
+  for (cudaGraph_t* x : {&ctx->graph, &ctx->graph_timed})
+    if (*x) { cudaGraphDestroy(*x); *x = nullptr; }
+  auto capture = [&](bool instrumented, cudaGraph_t* g) -> int {
+    ctx->cap_used = 0;
+    ctx->capturing = instrumented;
+    CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->capture_stream, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_step(ctx, io, ctx->capture_stream, false);
+    cudaError_t e = cudaStreamEndCapture(ctx->capture_stream, g);
+    ctx->capturing = false;
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(ctx, NOSA_ERR_CUDA, "stream capture: %s", cudaGetErrorString(e));
+    return NOSA_OK;
+  };
+  // the clean graph: what a replay runs unless per-kernel timing is on
+  if (int rc = capture(false, &ctx->graph)) return rc;
+  CUDA_TRY(ctx, cudaGraphInstantiate(&ctx->graph_exec, ctx->graph, 0));
+  ctx->graph_kernels = 4 * ctx->dv.L;
+  // the instrumented twin: an external event-record node around every kernel (placeholders)
   const size_t nslots = 4 * (size_t)ctx->dv.L;
   while (ctx->cap_events.size() < nslots) {
     NosaCtx::Timed t{};
@@ -698,18 +717,9 @@ extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {
     CUDA_TRY(ctx, cudaEventCreate(&t.b));
     ctx->cap_events.push_back(t);
   }
-  ctx->cap_used = 0;
-  ctx->capturing = true;
-  CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->capture_stream, cudaStreamCaptureModeThreadLocal));
-  int rc = enqueue_step(ctx, io, ctx->capture_stream, false);
-  cudaGraph_t g = nullptr;
-  cudaError_t e = cudaStreamEndCapture(ctx->capture_stream, &g);
-  ctx->capturing = false;
-  if (rc) return rc;
-  if (e != cudaSuccess) return fail(ctx, NOSA_ERR_CUDA, "stream capture: %s", cudaGetErrorString(e));
-  ctx->graph = g;
-  CUDA_TRY(ctx, cudaGraphInstantiate(&ctx->graph_exec, g, 0));
-  ctx->graph_kernels = 4 * ctx->dv.L;
+  if (int rc = capture(true, &ctx->graph_timed)) return rc;
+  cudaGraph_t g = ctx->graph_timed;
+  CUDA_TRY(ctx, cudaGraphInstantiate(&ctx->graph_exec_timed, g, 0));
   // map every event-record node back to its timing scope
   ctx->ev_nodes.clear();
   ctx->nodes_on_pool = false;  // freshly instantiated: the nodes hold the placeholders
@@ -734,19 +744,18 @@ extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {
 extern "C" int nosa_step_graph_launch(NosaCtx* ctx, void* stream) {
   if (!ctx || !ctx->graph_exec) return fail(ctx, NOSA_ERR_STATE, "no captured step graph");
   const size_t slots = ctx->cap_used;
-  if (slots && ctx->timing_used + slots <= ctx->timing.size()) {  // time this replay per kernel
+  if (ctx->graph_exec_timed && slots && ctx->timing_used + slots <= ctx->timing.size()) {
+    // time this replay per kernel: point the instrumented twin's nodes at fresh pool events
     for (const auto& en : ctx->ev_nodes) {
       NosaCtx::Timed& t = ctx->timing[ctx->timing_used + en.slot];
       t.kind = ctx->cap_events[en.slot].kind;
-      CUDA_TRY(ctx, cudaGraphExecEventRecordNodeSetEvent(ctx->graph_exec, en.node, en.end ? t.b : t.a));
+      CUDA_TRY(ctx, cudaGraphExecEventRecordNodeSetEvent(ctx->graph_exec_timed, en.node, en.end ? t.b : t.a));
     }
     ctx->timing_used += slots;
     ctx->nodes_on_pool = true;
-  } else if (slots && ctx->nodes_on_pool) {  // timing off or pool exhausted: back to placeholders
-    for (const auto& en : ctx->ev_nodes)
-      CUDA_TRY(ctx, cudaGraphExecEventRecordNodeSetEvent(
-                        ctx->graph_exec, en.node, en.end ? ctx->cap_events[en.slot].b : ctx->cap_events[en.slot].a));
-    ctx->nodes_on_pool = false;
+    CUDA_TRY(ctx, cudaGraphLaunch(ctx->graph_exec_timed, S(stream)));
+    ctx->launches += ctx->graph_kernels;
+    return NOSA_OK;
   }
   CUDA_TRY(ctx, cudaGraphLaunch(ctx->graph_exec, S(stream)));
   ctx->launches += ctx->graph_kernels;
