@@ -104,7 +104,7 @@ __device__ void finalize_bh(const Dev& dv, int layer, int bh, int nc, const T* _
   const size_t pbase = (size_t)bh * dv.max_chunks;
   // (1) chunk records (m, l) -> shared, then per-query weights e^{m_c - M} / L
   float2* mls = reinterpret_cast<float2*>(wsm);  // [nc][G], reused in place as weights
-  for (int x = tid; x < nc * G; x += blockDim.x) mls[x] = __ldcg(&dv.part_ml[pbase * G + x]);
+  for (int x = tid; x < nc * G; x += blockDim.x) mls[x] = __ldcg(&part_ml_of(dv, layer)[pbase * G + x]);
   __syncthreads();
   if (tid < G) {
     float M = -INFINITY;
@@ -119,7 +119,7 @@ __device__ void finalize_bh(const Dev& dv, int layer, int bh, int nc, const T* _
   const int D4 = D / 4;
   for (int x = tid; x < G * D4; x += blockDim.x) {
     const int q = x / D4, d4 = x - q * D4;
-    const float4* po = reinterpret_cast<const float4*>(dv.part_o + (pbase * G + q) * D) + d4;
+    const float4* po = reinterpret_cast<const float4*>(part_o_of(dv, layer) +(pbase * G + q) * D) + d4;
     const size_t cstride = (size_t)G * D4;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
@@ -533,8 +533,8 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
             acc = fmaf(f, comb_o[((size_t)ww * T::QMAX + qq) * DH + d], acc);
             L = fmaf(f, ml.y, L);
           }
-          dv.part_o[(pb0 * G + qq) * DH + d] = acc;
-          if (d == 0) dv.part_ml[pb0 * G + qq] = make_float2(M, L);
+          part_o_of(dv, layer)[(pb0 * G + qq) * DH + d] = acc;
+          if (d == 0) part_ml_of(dv, layer)[pb0 * G + qq] = make_float2(M, L);
         }
         named_sync(kBarConsumers, T::NCW * 32);  // comb_* may be overwritten at the next chunk end
       }
@@ -703,10 +703,10 @@ __global__ void __launch_bounds__(32)
 #pragma unroll
       for (int gg = 0; gg < GM; ++gg) {
         if (gg >= G) break;
-        float* po = dv.part_o + (pbase * G + gg) * DH;
+        float* po = part_o_of(dv, layer) +(pbase * G + gg) * DH;
 #pragma unroll
         for (int x = 0; x < DL; ++x) po[lane + 32 * x] = o[gg][x];
-        if (lane == 0) dv.part_ml[pbase * G + gg] = make_float2(m[gg], l[gg]);
+        if (lane == 0) part_ml_of(dv, layer)[pbase * G + gg] = make_float2(m[gg], l[gg]);
       }
       __syncwarp();
     }

@@ -43,7 +43,9 @@ struct NosaCtx {
   int gather_grid = 8;       // UVA gather CTAs: enough bytes in flight for the link, few SMs taken
   int tma_gather_grid = 24;  // TMA gather CTAs (one warp, 4 x 32 KiB stages each)
   cudaStream_t copy_stream = nullptr;
-  std::vector<cudaEvent_t> ev_plan, ev_gather;
+  cudaStream_t att_stream = nullptr, fin_stream = nullptr;  // attention / finalize stages
+  std::vector<cudaEvent_t> ev_plan, ev_gather, ev_att, ev_fin;
+  cudaEvent_t ev_fork = nullptr;
   char* host_mirror = nullptr;
   size_t host_bytes = 0;
   bool host_registered = false;  // mmap + cudaHostRegister (else cudaHostAlloc)
@@ -202,11 +204,11 @@ static void release(NosaCtx* ctx) {
     if (x) cudaGraphExecDestroy(x);
   for (cudaGraph_t x : {ctx->graph, ctx->graph_timed})
     if (x) cudaGraphDestroy(x);
-  if (ctx->capture_stream) cudaStreamDestroy(ctx->capture_stream);
-  for (auto e : ctx->ev_plan) cudaEventDestroy(e);
-  for (auto e : ctx->ev_gather) cudaEventDestroy(e);
-  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
-  if (ctx->meta_stream) cudaStreamDestroy(ctx->meta_stream);
+  for (auto* evs : {&ctx->ev_plan, &ctx->ev_gather, &ctx->ev_att, &ctx->ev_fin})
+    for (auto e : *evs) cudaEventDestroy(e);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  for (cudaStream_t s : {ctx->copy_stream, ctx->capture_stream, ctx->att_stream, ctx->fin_stream, ctx->meta_stream})
+    if (s) cudaStreamDestroy(s);
   if (ctx->h_list) cudaFreeHost(ctx->h_list);
   if (ctx->h_cnt) cudaFreeHost(ctx->h_cnt);
   for (auto* pool : {&ctx->timing, &ctx->cap_events})
@@ -311,8 +313,8 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   ALLOC(dv.plan_n, LBH * 3);
   ALLOC(dv.cnt, (size_t)dv.L * 2);
   ALLOC(dv.miss_list, (size_t)dv.L * BH * dv.C);
-  ALLOC(dv.part_o, BH * dv.max_chunks * dv.G * dv.D);
-  ALLOC(dv.part_ml, BH * dv.max_chunks * dv.G);
+  ALLOC(dv.part_o, 2 * BH * dv.max_chunks * dv.G * dv.D);
+  ALLOC(dv.part_ml, 2 * BH * dv.max_chunks * dv.G);
   ALLOC(dv.newrow, LBH * 2 * dv.D * (size_t)dv.elem);
   ALLOC(dv.w1, (size_t)dv.D * dv.n_ev);
   ALLOC(dv.w2, (size_t)dv.n_ev);
@@ -363,13 +365,12 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   cudaHostGetDevicePointer(&hdev, ctx->host_mirror, 0);
   dv.host = static_cast<char*>(hdev);
 
-  cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
-  cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking);
-  ctx->ev_plan.resize(dv.L);
-  ctx->ev_gather.resize(dv.L);
-  for (int l = 0; l < dv.L; ++l) {
-    cudaEventCreateWithFlags(&ctx->ev_plan[l], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ctx->ev_gather[l], cudaEventDisableTiming);
+  for (cudaStream_t* s : {&ctx->copy_stream, &ctx->capture_stream, &ctx->att_stream, &ctx->fin_stream})
+    cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+  for (auto* evs : {&ctx->ev_plan, &ctx->ev_gather, &ctx->ev_att, &ctx->ev_fin}) {
+    evs->resize(dv.L);
+    for (int l = 0; l < dv.L; ++l) cudaEventCreateWithFlags(&(*evs)[l], cudaEventDisableTiming);
   }
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -632,14 +633,20 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   const char* q = static_cast<const char*>(io->q);
   const char* kn = static_cast<const char*>(io->k_new);
   const char* vn = static_cast<const char*>(io->v_new);
-  CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt, 0, (size_t)dv.L * 2 * sizeof(int), st));
   const bool timed = count;  // eager steps only (never inside a graph capture)
-  // Layer-pipelined schedule: every layer's select+plan is issued first, so the miss gather of
-  // layer l overlaps the scoring of layers l+1.. (valid when each layer's query is known up
-  // front, as with per-layer query streams).  Layer-serial schedule: select(l) waits for
-  // finalize(l-1), as when q_{l+1} is computed from layer l's output.
+  // Four streams, one per stage, linked per layer by events:
+  //   select(l) [st] -> gather(l) [copy] -> attend(l) [att] -> finalize(l) [fin]
+  // so the selection, miss transfer, attention and merge/append of different layers overlap.
+  // attend(l) also waits finalize(l-2): the split-K records are double-buffered by layer parity.
+  // Layer-pipelined schedule: every select is issued first (valid when each layer's query is
+  // known up front, as with per-layer query streams).  Layer-serial schedule: select(l) waits
+  // for finalize(l-1), as when q_{l+1} is computed from layer l's output.
   const bool serial = io->schedule == 1;
+  cudaStream_t cp = ctx->copy_stream, at = ctx->att_stream, fn = ctx->fin_stream;
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, st));  // side streams start after the caller's work
+  for (cudaStream_t s : {cp, at, fn}) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_fork, 0));
   auto select = [&](int l) -> int {
+    CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt + 2 * l, 0, 2 * sizeof(int), st));
     {
       TimeScope ts(ctx, st, 0, timed);
       CUDA_TRY(ctx, nosa::launch_select_plan(dv, l, q + l * qstride, io->selector, 1, nullptr, nullptr, st));
@@ -651,28 +658,40 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
     for (int l = 0; l < dv.L; ++l)
       if (int rc = select(l)) return rc;
   for (int l = 0; l < dv.L; ++l) {
-    if (serial)
+    if (serial) {
+      if (l > 0) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_fin[l - 1], 0));
       if (int rc = select(l)) return rc;
-    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_plan[l], 0));
+    }
+    CUDA_TRY(ctx, cudaStreamWaitEvent(cp, ctx->ev_plan[l], 0));
     if (io->gather_mode == NOSA_GATHER_MEMCPY) {
-      const int rc = gather_memcpy(ctx, l, ctx->ev_plan[l], ctx->copy_stream, timed);
+      const int rc = gather_memcpy(ctx, l, ctx->ev_plan[l], cp, timed);
       if (rc) return rc;
     } else {
-      TimeScope ts(ctx, ctx->copy_stream, 1, timed);
+      TimeScope ts(ctx, cp, 1, timed);
       const bool tma = io->gather_mode == NOSA_GATHER_TMA;
-      CUDA_TRY(ctx, nosa::launch_gather(dv, l, ctx->copy_stream, tma ? ctx->tma_gather_grid : ctx->gather_grid, tma));
+      CUDA_TRY(ctx, nosa::launch_gather(dv, l, cp, tma ? ctx->tma_gather_grid : ctx->gather_grid, tma));
       if (count) ctx->launches += 1;
     }
-    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[l], ctx->copy_stream));
-    CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_gather[l], 0));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[l], cp));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(at, ctx->ev_gather[l], 0));
+    if (l >= 2) CUDA_TRY(ctx, cudaStreamWaitEvent(at, ctx->ev_fin[l - 2], 0));
     {
-      TimeScope ts(ctx, st, 2, timed);
+      TimeScope ts(ctx, at, 2, timed);
       CUDA_TRY(ctx, nosa::launch_attend(dv, l, q + l * qstride, kn + l * kstride, vn + l * kstride,
-                                        io->out + l * ostride, st, ctx->num_sms));
+                                        io->out + l * ostride, at, ctx->num_sms));
     }
-    TimeScope ts(ctx, st, 3, timed);
-    CUDA_TRY(ctx, nosa::launch_finalize(dv, l, kn + l * kstride, vn + l * kstride, io->out + l * ostride, st));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_att[l], at));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(fn, ctx->ev_att[l], 0));
+    {
+      TimeScope ts(ctx, fn, 3, timed);
+      CUDA_TRY(ctx, nosa::launch_finalize(dv, l, kn + l * kstride, vn + l * kstride, io->out + l * ostride, fn));
+    }
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fin[l], fn));
   }
+  // join every side stream back into the caller's stream
+  CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_gather[dv.L - 1], 0));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_att[dv.L - 1], 0));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_fin[dv.L - 1], 0));
   if (count) ctx->launches += 3LL * dv.L;  // + the gather kernels counted above
   return NOSA_OK;
 }

@@ -60,8 +60,8 @@ struct Dev {
   int* plan_n;                   // [lbh][3] n_fetch, n_evict, n_hit
   int* cnt;                      // [L][2]: miss count, attention work counter
   int4* miss_list;               // [L][B*H*C]  {lbh, blk, slot, 0}
-  float* part_o;                 // [B*H][max_chunks][G][D]
-  float2* part_ml;               // [B*H][max_chunks][G]
+  float* part_o;                 // [2][B*H][max_chunks][G][D]  split-K records, layer parity
+  float2* part_ml;               // [2][B*H][max_chunks][G]     (attend(l+1) overlaps finalize(l))
   char* newrow;                  // [lbh][2][D] (elem): K and V row of the last block born by an append
   double* w1;                    // [D][n_ev]
   double* w2;                    // [n_ev]
@@ -69,6 +69,14 @@ struct Dev {
 };
 
 enum StatIdx { ST_HITS = 0, ST_MISSES, ST_NEW, ST_EVICT, ST_STEPS, ST_N = 8 };
+
+// the split-K record buffer of a layer (double-buffered by layer parity)
+__host__ __device__ __forceinline__ float* part_o_of(const Dev& dv, int layer) {
+  return dv.part_o + (size_t)(layer & 1) * dv.B * dv.H * dv.max_chunks * dv.G * dv.D;
+}
+__host__ __device__ __forceinline__ float2* part_ml_of(const Dev& dv, int layer) {
+  return dv.part_ml + (size_t)(layer & 1) * dv.B * dv.H * dv.max_chunks * dv.G;
+}
 
 // ---------------------------------------------------------------- small helpers
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
