@@ -84,7 +84,31 @@ def workload_dims(args, world):
     rank = int(os.environ.get("RANK", "0"))
     shard = shard_batch(w["batch"], world, rank, bool(w.get("strong")))
     w["batch_local"], w["global_batch"] = shard.seq_count, shard.global_batch
+    w["host_limited"] = False
+    if args.impl == "native":  # the pinned slow tier of every rank on this node must fit in RAM
+        local = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+        n_blocks = -(-(w["context"] + 256) // 64)
+        per_seq = w["layers"] * 2 * n_blocks * 2 * 64 * 128 * 2  # [layers][kv heads][blocks] x 32 KiB
+        avail = host_mem_available()
+        budget = int(0.8 * avail / local) if avail else None
+        if budget is not None and per_seq * w["batch_local"] > budget:
+            fit = max(1, budget // per_seq)
+            print(f"bench: host RAM {avail / 2**30:.0f} GiB for {local} ranks holds {fit} of "
+                  f"{w['batch_local']} sequences per rank; batch reduced", file=sys.stderr)
+            w["batch_local"] = fit
+            w["global_batch"] = fit * world
+            w["host_limited"] = True
     return w
+
+
+def host_mem_available() -> int | None:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return None
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -366,6 +390,7 @@ def run_native(args, rank, world, local_rank):
                        "kernel_timing": "instrumented pass: the K steps after the timed region with CUDA events "
                                         "around every kernel on its own stream (event nodes in the graph); "
                                         "value comes from the uninstrumented region",
+                       "host_memory_limited_batch": w["host_limited"],
                        "l2": "no flush needed: attended KV per layer-step exceeds the 126 MB L2"},
             "h2d_miss_gbs": round(h2d_step / (step_ms * 1e-3) / 1e9, 3),
             "hit_rate": round(st.hit_rate, 4),

@@ -67,7 +67,14 @@ typedef struct NosaConfig {
   int32_t fast_slots; /* HBM slots per (layer, sequence, kv head) = fast-tier num_blocks */
   int32_t dtype;      /* NOSA_DTYPE_*: K/V/q storage type                               */
   int32_t variant;    /* NOSA_VARIANT_*                                                 */
+  int32_t residency;  /* NOSA_RESIDENCY_*                                               */
 } NosaConfig;
+
+/* residency contract */
+#define NOSA_RESIDENCY_PER_SEQUENCE 0 /* one manager per (layer, sequence, head): SURVEY §8a   */
+#define NOSA_RESIDENCY_SHARED 1       /* one fast pool of batch*fast_slots per (layer, head)
+                                         shared by the batch, planned in batch order: the
+                                         reference simulator (offload_sim.py:254-299)          */
 
 /* ResidencyStats (kv_manager.py:101-122), summed over a (layer, sequence, head) range. */
 typedef struct NosaStats {

@@ -30,12 +30,13 @@ VARIANT = {"ed-dma": 0, "s-dma": 1, "dma": 2}
 DTYPE = {"bf16": 0, "fp32": 1}
 GATHER = {"uva": 0, "memcpy": 1, "tma": 2}
 SCHEDULE = {"pipelined": 0, "serial": 1}
+RESIDENCY = {"per-sequence": 0, "shared": 1}
 
 
 class NosaConfig(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int32) for name in (
         "n", "d", "n_head", "n_kv_head", "d_head", "n_b", "n_s", "n_w", "k", "k_q", "k_e",
-        "accounting", "batch", "layers", "max_tokens", "fast_slots", "dtype", "variant")]
+        "accounting", "batch", "layers", "max_tokens", "fast_slots", "dtype", "variant", "residency")]
 
 
 class NosaStats(ctypes.Structure):

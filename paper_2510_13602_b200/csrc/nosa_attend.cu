@@ -142,9 +142,10 @@ __device__ void finalize_bh(const Dev& dv, int layer, int bh, int nc, const T* _
   const T* vr = vn + ((size_t)b * dv.H + h) * D;
   const int elem = dv.elem;
   const int plane = n_b * D * elem;
-  const int slot = dv.slot_of[(size_t)lbh * dv.NB + blk];
+  const int sl = dv.slot_of[(size_t)lbh * dv.NB + blk];
+  const long long slot = sl < 0 ? -1 : (dv.shared ? shared_rel(dv, b, sl) : sl);  // relative to this row
   char* hblk = dv.host + ((size_t)lbh * dv.NB + blk) * dv.bpb;
-  char* dblk = slot >= 0 ? dv.pool + ((size_t)lbh * dv.C + slot) * dv.bpb : nullptr;
+  char* dblk = sl >= 0 ? dv.pool + ((long long)lbh * dv.C + slot) * dv.bpb : nullptr;
   const int cpr = D * elem / 16;  // 16-byte chunks per row
   for (int c = tid; c < 2 * cpr; c += nthr) {
     const int which = c / cpr;  // 0 = K, 1 = V

@@ -18,6 +18,7 @@ namespace nosa {
 cudaError_t launch_select_plan(const Dev& dv, int layer, const void* q, int selector, int mode,
                                const int* ext_req, const int* ext_nreq, cudaStream_t st);
 cudaError_t launch_start_run(const Dev& dv, int seq_begin, int seq_count, cudaStream_t st);
+cudaError_t launch_plan_shared(const Dev& dv, int layer, const int* ext_req, const int* ext_nreq, cudaStream_t st);
 cudaError_t launch_select_scores(int n_prob, const double* s_q, const double* s_e, int stride,
                                  const int* lo, const int* hi, int m_q, int m_e, int selector,
                                  int* out_q, int* n_q, int* out_e, int* n_e, cudaStream_t st);
@@ -168,6 +169,8 @@ extern "C" int nosa_config_validate(const NosaConfig* c, char* msg, int msg_len)
   if (c->fast_slots <= 0) return bad("fast_slots must be positive");
   if (c->dtype != NOSA_DTYPE_BF16 && c->dtype != NOSA_DTYPE_FP32) return bad("dtype must be bf16 or fp32");
   if (c->variant < 0 || c->variant > 2) return bad("variant must be ed-dma, s-dma or dma");
+  if (c->residency != NOSA_RESIDENCY_PER_SEQUENCE && c->residency != NOSA_RESIDENCY_SHARED)
+    return bad("residency must be per-sequence or shared");
   if (c->n_head / c->n_kv_head > 16) return bad("group size n_head/n_kv_head must be <= 16");
   if (!nosa::attend_supported(c->n_b, c->d_head, c->dtype))
     return bad("unsupported (n_b=%d, d_head=%d, dtype=%d): n_b in {16,32,64,128}, d_head in {64,128}",
@@ -270,6 +273,7 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   dv.n_ev = c.n_head;
   dv.dtype = c.dtype;
   dv.variant = c.variant;
+  dv.shared = c.residency == NOSA_RESIDENCY_SHARED;
   dv.elem = c.dtype == NOSA_DTYPE_BF16 ? 2 : 4;
   dv.bpb = 2LL * c.n_b * c.d_head * dv.elem;
   dv.max_chunks = (dv.C + nosa::kChunk - 1) / nosa::kChunk;
@@ -427,6 +431,8 @@ extern "C" int nosa_prefill(NosaCtx* ctx, int layer, int seq_begin, int seq_coun
     return fail(ctx, NOSA_ERR_VALUE, "head cache capacity exhausted: prefill of %d tokens > max_tokens %d", t,
                 ctx->cfg.max_tokens);
   if (t > 0 && (!k || !v)) return fail(ctx, NOSA_ERR_VALUE, "k/v are NULL");
+  if (dv.shared && (seq_begin != 0 || seq_count != dv.B))
+    return fail(ctx, NOSA_ERR_VALUE, "a shared-pool context prefills the whole batch of a layer at once");
   cudaSetDevice(ctx->device);
   const size_t need = (size_t)seq_count * dv.H * dv.NB * (size_t)dv.bpb;
   if (need > ctx->staging_bytes) {
@@ -446,6 +452,7 @@ extern "C" int nosa_prefill(NosaCtx* ctx, int layer, int seq_begin, int seq_coun
 
 extern "C" int nosa_prefill_resident(NosaCtx* ctx, int layer, int seq_begin, int seq_count, const void* k,
                                      const void* v, int t, void* stream) {
+  if (ctx && ctx->dv.shared) return fail(ctx, NOSA_ERR_VALUE, "resident prefill needs per-sequence residency");
   int rc = nosa_prefill(ctx, layer, seq_begin, seq_count, k, v, t, stream);
   if (rc) return rc;
   const Dev& dv = ctx->dv;
@@ -475,14 +482,24 @@ extern "C" int nosa_start_run(NosaCtx* ctx, int seq_begin, int seq_count, void* 
   return NOSA_OK;
 }
 
+// K1+K2 for one layer: fused per-(sequence, head) select+plan, or select then the ordered
+// shared-pool planner (NOSA_RESIDENCY_SHARED)
+static cudaError_t plan_layer(NosaCtx* ctx, int layer, const void* q, int selector, cudaStream_t st) {
+  const Dev& dv = ctx->dv;
+  if (!dv.shared) return nosa::launch_select_plan(dv, layer, q, selector, 1, nullptr, nullptr, st);
+  cudaError_t e = nosa::launch_select_plan(dv, layer, q, selector, 0, nullptr, nullptr, st);
+  if (e != cudaSuccess) return e;
+  return nosa::launch_plan_shared(dv, layer, nullptr, nullptr, st);
+}
+
 extern "C" int nosa_select_plan(NosaCtx* ctx, int layer, const void* q, int selector, void* stream) {
   int rc = check_layer(ctx, layer);
   if (rc) return rc;
   if (selector != 0 && selector != 1) return fail(ctx, NOSA_ERR_VALUE, "selector must be nosa or infllmv2");
   cudaSetDevice(ctx->device);
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->dv.cnt + 2 * layer, 0, 2 * sizeof(int), S(stream)));
-  CUDA_TRY(ctx, nosa::launch_select_plan(ctx->dv, layer, q, selector, 1, nullptr, nullptr, S(stream)));
-  ctx->launches += 1;
+  CUDA_TRY(ctx, plan_layer(ctx, layer, q, selector, S(stream)));
+  ctx->launches += ctx->dv.shared ? 2 : 1;
   return NOSA_OK;
 }
 
@@ -502,7 +519,10 @@ extern "C" int nosa_cache_plan(NosaCtx* ctx, int layer, const int32_t* req, cons
   if (!req || !n_req) return fail(ctx, NOSA_ERR_VALUE, "required sets are NULL");
   cudaSetDevice(ctx->device);
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->dv.cnt + 2 * layer, 0, 2 * sizeof(int), S(stream)));
-  CUDA_TRY(ctx, nosa::launch_select_plan(ctx->dv, layer, nullptr, 0, 2, req, n_req, S(stream)));
+  if (ctx->dv.shared)
+    CUDA_TRY(ctx, nosa::launch_plan_shared(ctx->dv, layer, req, n_req, S(stream)));
+  else
+    CUDA_TRY(ctx, nosa::launch_select_plan(ctx->dv, layer, nullptr, 0, 2, req, n_req, S(stream)));
   ctx->launches += 1;
   return NOSA_OK;
 }
@@ -649,7 +669,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
     CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt + 2 * l, 0, 2 * sizeof(int), st));
     {
       TimeScope ts(ctx, st, 0, timed);
-      CUDA_TRY(ctx, nosa::launch_select_plan(dv, l, q + l * qstride, io->selector, 1, nullptr, nullptr, st));
+      CUDA_TRY(ctx, plan_layer(ctx, l, q + l * qstride, io->selector, st));
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[l], st));
     return NOSA_OK;
@@ -692,7 +712,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_gather[dv.L - 1], 0));
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_att[dv.L - 1], 0));
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_fin[dv.L - 1], 0));
-  if (count) ctx->launches += 3LL * dv.L;  // + the gather kernels counted above
+  if (count) ctx->launches += (dv.shared ? 4LL : 3LL) * dv.L;  // + the gather kernels counted above
   return NOSA_OK;
 }
 
@@ -727,7 +747,7 @@ extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {
   // the clean graph: what a replay runs unless per-kernel timing is on
   if (int rc = capture(false, &ctx->graph)) return rc;
   CUDA_TRY(ctx, cudaGraphInstantiate(&ctx->graph_exec, ctx->graph, 0));
-  ctx->graph_kernels = 4 * ctx->dv.L;
+  ctx->graph_kernels = (ctx->dv.shared ? 5 : 4) * ctx->dv.L;
   // the instrumented twin: an external event-record node around every kernel (placeholders)
   const size_t nslots = 4 * (size_t)ctx->dv.L;
   while (ctx->cap_events.size() < nslots) {

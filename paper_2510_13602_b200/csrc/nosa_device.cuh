@@ -27,6 +27,9 @@ struct Dev {
   int m_q, m_e, m_topk, MQ, ME;  // blocks_q, blocks_e, blocks_topk; selection capacities
   int L, C, NB, n_ev;            // layers, fast slots, max blocks, eviction-head width (n_head)
   int dtype, variant, elem;
+  int shared;                    // 1: one fast pool of B*C slots per (layer, head) shared by the batch
+                                 //    (the reference simulator, offload_sim.py:254-256); slot_of then
+                                 //    holds the shared slot id s, stored at (lbh of batch s/C, slot s%C)
   long long bpb;                 // bytes per block
   int max_chunks;                // ceil(C / kChunk)
   // ---- persistent state ----------------------------------------------------------------
@@ -69,6 +72,15 @@ struct Dev {
 };
 
 enum StatIdx { ST_HITS = 0, ST_MISSES, ST_NEW, ST_EVICT, ST_STEPS, ST_N = 8 };
+
+// shared-pool mode: storage index of shared slot s of (layer, head) in the [lbh][C] arrays, and
+// the slot offset relative to sequence b's own pool row (pool + (lbh*C + rel)*bpb addresses it)
+__host__ __device__ __forceinline__ size_t shared_idx(const Dev& dv, int layer, int h, int s) {
+  return ((size_t)(layer * dv.B + s / dv.C) * dv.H + h) * dv.C + s % dv.C;
+}
+__host__ __device__ __forceinline__ int shared_rel(const Dev& dv, int b, int s) {
+  return (s / dv.C - b) * dv.H * dv.C + s % dv.C;
+}
 
 // the split-K record buffer of a layer (double-buffered by layer parity)
 __host__ __device__ __forceinline__ float* part_o_of(const Dev& dv, int layer) {

@@ -248,13 +248,17 @@ __global__ void reset_residency_kernel(Dev dv, int layer, int seq_begin, int S, 
   const int sh = blockIdx.x;
   const int lbh = (layer * dv.B + seq_begin) * dv.H + sh;  // S*H consecutive lbh
   for (int i = threadIdx.x; i < dv.NB; i += blockDim.x) dv.slot_of[(size_t)lbh * dv.NB + i] = -1;
+  // shared pool: this row holds entries [b*C, b*C + C) of the layer-head's B*C-slot free stack
+  const int b = seq_begin + sh / dv.H;
+  const int n_free = dv.shared ? dv.B * dv.C : dv.C;
+  const int first = dv.shared ? b * dv.C : 0;
   for (int i = threadIdx.x; i < dv.C; i += blockDim.x) {
     dv.blk_of[(size_t)lbh * dv.C + i] = -1;
     dv.lastreq[(size_t)lbh * dv.C + i] = 0;
-    dv.fstack[(size_t)lbh * dv.C + i] = dv.C - 1 - i;
+    dv.fstack[(size_t)lbh * dv.C + i] = n_free - 1 - (first + i);
   }
   if (threadIdx.x == 0) {
-    dv.ftop[lbh] = dv.C;
+    dv.ftop[lbh] = n_free;
     dv.clock[lbh] = 0;
     dv.t[lbh] = t;
     dv.t0[lbh] = t;

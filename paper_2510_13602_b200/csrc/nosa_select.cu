@@ -531,6 +531,176 @@ __global__ void __launch_bounds__(256)
 }
 
 // ------------------------------------------------------------------------------------------
+// Shared-pool planner: the reference simulator's residency (offload_sim.py:254-299) — one fast
+// pool of B*C slots per (layer, head) shared by every sequence, plan + apply per sequence in
+// batch order, least-recently-required victims over all sequences by (clock, batch, block)
+// (kv_manager.py:125-127), LIFO slot reuse.  Inherently serial in b: one CTA per head.
+constexpr int kSharedThreads = 512;
+
+__global__ void __launch_bounds__(kSharedThreads)
+    plan_shared_kernel(Dev dv, int layer, const int* __restrict__ ext_req, const int* __restrict__ ext_nreq) {
+  extern __shared__ __align__(16) char smem_raw[];
+  const int h = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int B = dv.B, C = dv.C, H = dv.H, NB = dv.NB, N = B * C;
+  int* req = reinterpret_cast<int*>(smem_raw);      // [C]
+  int* reqslot = req + C;                           // [C] shared slot ids
+  int* fetch = reqslot + C;                         // [C]
+  int* fpos = fetch + C;                            // [C]
+  int* victims = fpos + C;                          // [C]
+  unsigned* chosen = reinterpret_cast<unsigned*>(victims + C);  // [N/32 + 1] bitmap
+  unsigned long long* red_k = reinterpret_cast<unsigned long long*>(chosen + N / 32 + 2);  // [32]
+  int* red_s = reinterpret_cast<int*>(red_k + 32);  // [32]
+  int* misc = red_s + 32;                           // [8]
+  const size_t head0 = (size_t)(layer * B) * H + h;  // (layer, b = 0, h): per-(layer, head) scalars
+  if (tid == 0) {
+    misc[0] = dv.clock[head0];
+    misc[1] = dv.ftop[head0];
+  }
+  __syncthreads();
+  for (int b = 0; b < B; ++b) {
+    const int lbh = (layer * B + b) * H + h;
+    const int n = ext_nreq ? ext_nreq[b * H + h] : dv.n_req[lbh];
+    if (n < 0) continue;  // not part of this call
+    if (n > C) {          // CapacityExceeded for this sequence's share (kv_manager.py:215-219)
+      if (tid == 0) {
+        atomicOr(dv.err, 1u);
+        dv.n_req[lbh] = 0;
+      }
+      continue;
+    }
+    for (int i = tid; i < n; i += blockDim.x) req[i] = ext_req ? ext_req[((size_t)b * H + h) * C + i] : dv.req[(size_t)lbh * C + i];
+    for (int w = tid; w < N / 32 + 1; w += blockDim.x) chosen[w] = 0u;
+    __syncthreads();
+    const int clock = misc[0] + 1;
+    // (1) hit test and fetch list in required order
+    if (warp == 0) {
+      int nf = 0;
+      for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        const int blk = i < n ? req[i] : 0;
+        const int s = i < n ? dv.slot_of[(size_t)lbh * NB + blk] : 0;
+        const bool miss = i < n && s < 0;
+        if (i < n && s >= 0) {
+          dv.lastreq[shared_idx(dv, layer, h, s)] = clock;
+          reqslot[i] = s;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, miss);
+        if (miss) {
+          const int pos = nf + __popc(bal & ((1u << lane) - 1u));
+          fetch[pos] = blk;
+          fpos[pos] = i;
+        }
+        nf += __popc(bal);
+      }
+      if (lane == 0) {
+        misc[0] = clock;
+        misc[2] = nf;
+        misc[3] = nf - misc[1];  // shortfall against the shared free list
+      }
+    }
+    __syncthreads();
+    const int nf = misc[2], shortfall = misc[3];
+    // (2) victims: repeated block-wide argmin of (last_required, batch, block) over the pool,
+    //     excluding blocks required now (they carry this call's clock)
+    for (int r = 0; r < shortfall; ++r) {
+      unsigned long long best = ~0ull;
+      int best_s = -1;
+      for (int s = tid; s < N; s += blockDim.x) {
+        const size_t x = shared_idx(dv, layer, h, s);
+        const int key = dv.blk_of[x];
+        if (key < 0 || dv.lastreq[x] == clock || ((chosen[s >> 5] >> (s & 31)) & 1u)) continue;
+        const unsigned long long k = ((unsigned long long)(unsigned)dv.lastreq[x] << 32) |
+                                     ((unsigned long long)(key / NB) << 16) | (unsigned long long)(key % NB);
+        if (k < best) { best = k; best_s = s; }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long ok = __shfl_xor_sync(0xffffffffu, best, o);
+        const int os = __shfl_xor_sync(0xffffffffu, best_s, o);
+        if (ok < best) { best = ok; best_s = os; }
+      }
+      if (lane == 0) { red_k[warp] = best; red_s[warp] = best_s; }
+      __syncthreads();
+      if (tid == 0) {
+        unsigned long long k = ~0ull;
+        int s = -1;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+          if (red_k[w] < k) { k = red_k[w]; s = red_s[w]; }
+        victims[r] = s;
+        if (s >= 0) chosen[s >> 5] |= 1u << (s & 31);
+        else atomicOr(dv.err, 1u);  // not enough evictable blocks
+      }
+      __syncthreads();
+    }
+    // (3) apply: victims release their slots in LRR order, fetches pop in required order
+    if (tid == 0) {
+      int top = misc[1];
+      const int nev = shortfall > 0 ? shortfall : 0;
+      int* pe = dv.plan_evict + (size_t)lbh * C;
+      int* pf = dv.plan_fetch + (size_t)lbh * C;
+      for (int r = 0; r < nev; ++r) {
+        const int s = victims[r];
+        if (s < 0) break;
+        const size_t x = shared_idx(dv, layer, h, s);
+        const int key = dv.blk_of[x];
+        dv.slot_of[(size_t)((layer * B + key / NB) * H + h) * NB + key % NB] = -1;
+        dv.blk_of[x] = -1;
+        dv.fstack[shared_idx(dv, layer, h, top + r)] = s;
+        pe[r] = key;  // owner * NB + block
+      }
+      top += nev;
+      const int t = dv.t[lbh], t0 = dv.t0[lbh];
+      int n_new = 0;
+      int base = nf ? atomicAdd(dv.cnt + 2 * layer, nf) : 0;
+      int4* ml = dv.miss_list + (size_t)layer * B * H * C;
+      for (int f = 0; f < nf; ++f) {
+        const int s = dv.fstack[shared_idx(dv, layer, h, top - 1 - f)];
+        const int blk = fetch[f];
+        const size_t x = shared_idx(dv, layer, h, s);
+        dv.slot_of[(size_t)lbh * NB + blk] = s;
+        dv.blk_of[x] = b * NB + blk;
+        dv.lastreq[x] = clock;
+        reqslot[fpos[f]] = s;
+        pf[f] = blk;
+        n_new += blk * dv.n_b >= t0;
+        const int born = (blk * dv.n_b == t - 1) && (t - 1 >= t0);
+        ml[base + f] = make_int4(lbh, blk, shared_rel(dv, b, s), born);
+      }
+      top -= nf;
+      misc[1] = top;
+      long long* st = dv.stats + (size_t)lbh * ST_N;
+      st[ST_HITS] += n - nf;
+      st[ST_MISSES] += nf;
+      st[ST_NEW] += n_new;
+      st[ST_EVICT] += nev;
+      st[ST_STEPS] += 1;
+      dv.plan_n[lbh * 3 + 0] = nf;
+      dv.plan_n[lbh * 3 + 1] = nev;
+      dv.plan_n[lbh * 3 + 2] = n - nf;
+      dv.n_req[lbh] = n;
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) {
+      dv.req[(size_t)lbh * C + i] = req[i];
+      dv.req_slot[(size_t)lbh * C + i] = shared_rel(dv, b, reqslot[i]);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    dv.clock[head0] = misc[0];
+    dv.ftop[head0] = misc[1];
+  }
+}
+
+cudaError_t launch_plan_shared(const Dev& dv, int layer, const int* ext_req, const int* ext_nreq, cudaStream_t st) {
+  const int N = dv.B * dv.C;
+  const size_t smem = 5 * (size_t)dv.C * 4 + ((size_t)N / 32 + 2) * 4 + 32 * 8 + 32 * 4 + 8 * 4 + 64;
+  cudaFuncSetAttribute(plan_shared_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  plan_shared_kernel<<<dv.H, kSharedThreads, smem, st>>>(dv, layer, ext_req, ext_nreq);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
 // host-side launchers
 cudaError_t launch_select_plan(const Dev& dv, int layer, const void* q, int selector, int mode,
                                const int* ext_req, const int* ext_nreq, cudaStream_t st) {

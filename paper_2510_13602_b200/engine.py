@@ -82,9 +82,15 @@ class StepOutput:
 class NosaEngine:
     def __init__(self, config: AttentionConfig, *, batch: int, max_tokens: int, fast_slots: int,
                  w1, w2, layers: int = 1, variant: str = "ed-dma", dtype: str = "bf16",
-                 device: int = 0):
+                 device: int = 0, residency: str = "per-sequence"):
+        """residency "per-sequence": one manager per (layer, sequence, head) with `fast_slots`
+        slots; "shared": one pool of batch*fast_slots slots per (layer, head)
+        shared by the batch and planned in batch order, the reference simulator's residency."""
         if variant not in _lib.VARIANT:
             raise ValueError(f"variant must be one of {tuple(_lib.VARIANT)} (retaining needs hidden states)")
+        if residency not in _lib.RESIDENCY:
+            raise ValueError(f"residency must be one of {tuple(_lib.RESIDENCY)}")
+        self.residency = residency
         if dtype not in _lib.DTYPE:
             raise ValueError(f"dtype must be one of {tuple(_lib.DTYPE)}")
         self.config = config
@@ -98,6 +104,7 @@ class NosaEngine:
         c.accounting = 0 if config.accounting == "inclusive" else 1
         c.batch, c.layers, c.max_tokens, c.fast_slots = batch, layers, max_tokens, fast_slots
         c.dtype, c.variant = _lib.DTYPE[dtype], _lib.VARIANT[variant]
+        c.residency = _lib.RESIDENCY[residency]
         self._cfg = c
         msg = ctypes.create_string_buffer(512)
         if _lib.lib.nosa_config_validate(ctypes.byref(c), msg, 512) != _lib.NOSA_OK:
@@ -322,8 +329,8 @@ class NosaEngine:
 
     def fast_resident(self, layer: int, seq: int, head: int) -> set[int]:
         """TieredBlockManager.fast_resident (kv_manager.py:338-339)."""
-        _, block_of = self.residency(layer, seq, head)
-        return {int(b) for b in block_of if b >= 0}
+        slot_of, _ = self.residency(layer, seq, head)
+        return {int(b) for b in np.flatnonzero(slot_of >= 0)}
 
     def block_scores(self, layer: int) -> np.ndarray:
         out = np.zeros((self.batch, self.config.n_kv_head, self.max_blocks), np.float64)

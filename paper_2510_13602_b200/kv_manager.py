@@ -45,17 +45,26 @@ class TransferPlan:
 
 
 class GpuTieredBlockManager:
+    """fast_blocks: fast slots per head of each sequence's manager, or with shared=True the size
+    of the one per-head pool the whole batch shares (the reference simulator's layout,
+    offload_sim.py:254-256; planned in batch order).  slow_blocks: blocks per (sequence, head)."""
+
     def __init__(self, fast_blocks: int, slow_blocks: int, heads: int = 1, batch: int = 1, n_b: int = 16,
-                 d_head: int = 64, element_width: int = 2, device: int = 0):
+                 d_head: int = 64, element_width: int = 2, device: int = 0, shared: bool = False):
         if element_width not in (2, 4):
             raise ValueError("element_width must be 2 or 4 bytes")
+        if shared and fast_blocks % batch:
+            raise ValueError("a shared pool is allocated as batch equal shares: fast_blocks % batch must be 0")
         self.heads, self.batch, self.fast_blocks, self.slow_blocks = heads, batch, fast_blocks, slow_blocks
+        self.shared = shared
+        self.per_seq = fast_blocks // batch if shared else fast_blocks
         # a selection-free engine: the budgets are irrelevant to explicit required sets
         cfg = AttentionConfig(n=max(slow_blocks * n_b, n_b), d=d_head, n_head=heads, n_kv_head=heads, d_head=d_head,
                               n_b=n_b, n_s=0, n_w=0, k=0, k_q=0, k_e=0)
-        self._engine = NosaEngine(cfg, batch=batch, max_tokens=slow_blocks * n_b, fast_slots=fast_blocks,
+        self._engine = NosaEngine(cfg, batch=batch, max_tokens=slow_blocks * n_b, fast_slots=self.per_seq,
                                   w1=np.zeros((d_head, heads)), w2=np.zeros(heads),
-                                  dtype="bf16" if element_width == 2 else "fp32", device=device)
+                                  dtype="bf16" if element_width == 2 else "fp32", device=device,
+                                  residency="shared" if shared else "per-sequence")
         self.bytes_per_block = self._engine.bytes_per_block
         self.version = 0
 
@@ -64,14 +73,15 @@ class GpuTieredBlockManager:
 
     def plan_batch(self, required: dict[tuple[int, int], set]) -> dict[tuple[int, int], TransferPlan]:
         """Plan + apply for several (batch, head) managers in one kernel launch."""
-        B, H, C = self.batch, self.heads, self.fast_blocks
+        B, H, C = self.batch, self.heads, self.per_seq
         req = np.zeros((B, H, C), np.int32)
         n = np.full((B, H), -1, np.int32)
         for (b, h), blocks in required.items():
             blocks = sorted({int(x) for x in blocks})
             if len(blocks) > C:
                 raise CapacityExceeded(
-                    f"step requires {len(blocks)} blocks but the fast tier holds {C} per head")
+                    f"step requires {len(blocks)} blocks but the fast tier holds {C} per head"
+                    + (" per sequence share" if self.shared else ""))
             if blocks and (blocks[0] < 0 or blocks[-1] >= self.slow_blocks):
                 raise UnknownKey(f"required block {(b, h, blocks[-1])} exists in no tier")
             req[b, h, :len(blocks)] = blocks
@@ -85,9 +95,12 @@ class GpuTieredBlockManager:
         views = self._engine.plans(0)
         self.version += 1
         out = {}
+        NB = self._engine.max_blocks
         for (b, h) in required:
             v = views[b][h]
-            out[(b, h)] = TransferPlan(fetch=[(b, h, x) for x in v.fetch], evict=[(b, h, x) for x in v.evict],
+            # shared pool: a victim may belong to another sequence (key = owner * NB + block)
+            evict = [(x // NB, h, x % NB) for x in v.evict] if self.shared else [(b, h, x) for x in v.evict]
+            out[(b, h)] = TransferPlan(fetch=[(b, h, x) for x in v.fetch], evict=evict,
                                        bytes_up=v.bytes_up, bytes_down=v.bytes_down, hits=v.hits,
                                        misses=v.misses, version=self.version)
         return out

@@ -205,9 +205,70 @@ def engine_run(name, cfg_kw, batch, t0, steps, fast_slots, seed, rho, selector="
     print(name, "done")
 
 
+def shared_pool_simulation():
+    """The reference simulator itself (offload_sim.simulate_decode, shared per-head pool across
+    the batch, scripted AR(1) selections): its SimReport plus every per-(step, b, h) required set
+    and the fetch/evict lists of a replay through one shared TieredBlockManager, b-major order."""
+    from nosa_sim.decode import scripted_selection_trace
+    from nosa_sim.offload_sim import DEFAULT_PARAMS, fast_slots_per_seq, simulate_decode
+    cfg = AttentionConfig(n=4096, d=8, n_head=2, n_kv_head=2, d_head=8, n_b=16, n_s=32, n_w=64, k=288,
+                          k_q=64, k_e=224)
+    out = {}
+    for policy, rho in (("nosa", 0.5), ("infllmv2-offload", 0.0)):
+        B, t0, steps, seed = 4, 1000, 8, 3
+        rep = simulate_decode(cfg, DEFAULT_PARAMS, policy, batch=B, t0=t0, steps=steps, seed=seed,
+                              query_smoothness=rho)
+        # replay the same loop to record the required sets and plans (offload_sim.py:224-299)
+        selector = "nosa" if policy == "nosa" else "infllmv2"
+        geom = BlockGeometry.for_run(cfg, t0)
+        seeds = np.random.SeedSequence(seed).generate_state(B)
+        traces = [scripted_selection_trace(cfg, int(s), t0, steps + 1, selector=selector, query_smoothness=rho,
+                                           n_heads=cfg.n_kv_head) for s in seeds]
+        slots = fast_slots_per_seq(cfg, t0, steps + 1)
+        H, total = cfg.n_kv_head, geom.n_blocks(t0 + steps + 1)
+        mgr = TieredBlockManager(PhysicalLayout(FAST, B * slots, H, cfg.n_b, cfg.d_head),
+                                 PhysicalLayout(SLOW, B * total, H, cfg.n_b, cfg.d_head))
+        for b in range(B):
+            for h in range(H):
+                for i in range(geom.n_blocks(t0)):
+                    mgr.allocate(SLOW, b, h, i)
+        R = 64
+        req = np.full((steps + 1, B, H, R), -1, np.int64)
+        fetch = np.full((steps + 1, B, H, R), -1, np.int64)
+        evict = np.full((steps + 1, B, H, R, 2), -1, np.int64)  # (batch, block) of each victim
+        topk = np.full((steps + 1, B, H, R), -1, np.int64)
+        for i in range(steps + 1):
+            for b in range(B):
+                for h in range(H):
+                    sel = traces[b].steps[i][h]
+                    r = sorted(set(sel.blocks_fixed) | sel.topk_blocks)
+                    for blk in r:
+                        if mgr.lookup(b, h, blk) is None:
+                            mgr.allocate(SLOW, b, h, blk)
+                    plan = mgr.plan_transfers(set(r), b, h)
+                    mgr.apply_transfers(plan)
+                    req[i, b, h, :len(r)] = r
+                    tk = sorted(sel.topk_blocks)
+                    topk[i, b, h, :len(tk)] = tk
+                    fetch[i, b, h, :len(plan.fetch)] = [k[2] for k in plan.fetch]
+                    for j, key in enumerate(plan.evict):
+                        evict[i, b, h, j] = (key[0], key[2])
+            if i == 0:
+                mgr.reset_stats()
+        st = mgr.residency_stats()
+        assert st.hit_rate == rep.hit_rate and st.bytes_up == rep.bytes_up
+        tag = "nosa" if policy == "nosa" else "infllmv2"
+        out.update({f"{tag}_req": req, f"{tag}_fetch": fetch, f"{tag}_evict": evict, f"{tag}_topk": topk,
+                    f"{tag}_report": np.array([rep.hit_rate, rep.hit_rate_topk, rep.bytes_up, rep.bytes_down]),
+                    f"{tag}_shape": np.array([B, H, slots, total, t0, steps])})
+    np.savez_compressed(OUT / "shared_pool_sim.npz", **out)
+    print("shared_pool_sim: nosa hit", out["nosa_report"][0], "infllmv2 hit", out["infllmv2_report"][0])
+
+
 def main():
     selection_kats()
     manager_trace()
+    shared_pool_simulation()
     small = dict(n=4096, d=512, n_head=4, n_kv_head=2, d_head=64, n_b=16, n_s=32, n_w=128, k=512, k_q=128, k_e=384)
     engine_run("engine_small", small, batch=2, t0=1000, steps=24, fast_slots=40, seed=5, rho=0.5)
     engine_run("engine_small_infllmv2", small, batch=2, t0=1000, steps=8, fast_slots=40, seed=6, rho=0.0,

@@ -34,6 +34,6 @@ def assert_same_selection(got: list, want: list, scores: np.ndarray, pool: list,
     return gap
 
 
-def oracle_for(cfg, batch, layers, capacity, fast_slots, w1, w2, variant="ed-dma"):
+def oracle_for(cfg, batch, layers, capacity, fast_slots, w1, w2, variant="ed-dma", shared=False):
     oc = O.OracleConfig.from_attention_config(cfg, variant)
-    return O.OracleEngine(oc, batch, layers, capacity, fast_slots, w1, w2)
+    return O.OracleEngine(oc, batch, layers, capacity, fast_slots, w1, w2, shared=shared)

@@ -72,7 +72,8 @@ def test_engine_vs_reference_golden(golden, name, dtype):
 
 
 def _run_pair(cfg, *, batch, t0s, steps, fast_slots, seed, rho, selector="nosa", dtype="bf16", layers=1,
-              variant="ed-dma", check_residency=True, gather="uva", schedule="pipelined", resident=False):
+              variant="ed-dma", check_residency=True, gather="uva", schedule="pipelined", resident=False,
+              shared=False):
     """GPU engine and oracle on identical inputs; returns the worst relative output error."""
     w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, seed)
     if variant == "dma":
@@ -80,12 +81,19 @@ def _run_pair(cfg, *, batch, t0s, steps, fast_slots, seed, rho, selector="nosa",
     tmax = max(t0s)
     cap = tmax + steps + 1
     eng = NosaEngine(cfg, batch=batch, layers=layers, max_tokens=cap, fast_slots=fast_slots, w1=w1, w2=w2,
-                     dtype=dtype, variant=variant)
-    orc = oracle_for(cfg, batch, layers, cap, fast_slots, w1, w2, variant)
+                     dtype=dtype, variant=variant, residency="shared" if shared else "per-sequence")
+    orc = oracle_for(cfg, batch, layers, cap, fast_slots, w1, w2, variant, shared=shared)
     K, V = workload.prefix_kv(seed, batch * layers, cfg.n_kv_head, tmax, cfg.d_head)
     K = K.reshape(layers, batch, cfg.n_kv_head, tmax, cfg.d_head)
     V = V.reshape(layers, batch, cfg.n_kv_head, tmax, cfg.d_head)
-    for l in range(layers):
+    if shared:  # one pool per (layer, head): the whole batch is prefilled at once
+        assert len(set(t0s)) == 1
+        for l in range(layers):
+            eng.prefill(torch.from_numpy(np.ascontiguousarray(K[l])), torch.from_numpy(np.ascontiguousarray(V[l])),
+                        layer=l)
+            for b in range(batch):
+                orc.prefill(l, b, K[l, b], V[l, b])
+    for l in range(layers if not shared else 0):
         for b in range(batch):
             t = t0s[b]
             eng.prefill(torch.from_numpy(np.ascontiguousarray(K[l, b:b + 1, :, :t])),
@@ -118,12 +126,15 @@ def _run_pair(cfg, *, batch, t0s, steps, fast_slots, seed, rho, selector="nosa",
                     assert list(sels[b][h].blocks_e) == r.blocks_e.tolist(), (l, s, b, h)
                     assert req[b, h, :nreq[b, h]].tolist() == r.required, (l, s, b, h)
                     assert plans[b][h].fetch == r.fetch, (l, s, b, h)
-                    assert plans[b][h].evict == r.evict, (l, s, b, h)
+                    want_evict = [o * eng.max_blocks + x for o, x in r.evict] if shared else r.evict
+                    assert plans[b][h].evict == want_evict, (l, s, b, h)
                     assert plans[b][h].hits == r.hits
                     np.testing.assert_allclose(s_q[b, h, lo:hi], r.s_q, rtol=1e-12, atol=1e-12)
                     if check_residency and s == steps - 1:
                         slot_of, block_of = eng.residency(l, b, h)
                         want = orc.managers[l][b].slot_of[h]
+                        if shared:  # shared-pool slot ids of this sequence's blocks
+                            want = {blk: sl for (ob, blk), sl in want.items() if ob == b}
                         got = {int(blk): int(sl) for blk, sl in enumerate(slot_of) if sl >= 0}
                         assert got == want, (l, b, h)
         worst = max(worst, rel_err(out, ref))
@@ -186,6 +197,14 @@ def test_block_sizes(n_b):
     cfg = AttentionConfig(n=8192, d=1024, n_head=4, n_kv_head=2, d_head=128, n_b=n_b, n_s=n_b, n_w=4 * n_b,
                           k=16 * n_b, k_q=4 * n_b, k_e=12 * n_b)
     _run_pair(cfg, batch=2, t0s=[40 * n_b + 3, 30 * n_b], steps=5, fast_slots=20, seed=10, rho=0.5)
+
+
+@pytest.mark.parametrize("selector", ["nosa", "infllmv2"])
+def test_shared_pool_residency_vs_oracle(selector):
+    """The reference simulator's residency: one pool per (layer, head) shared by the batch,
+    planned in batch order; victims may belong to other sequences."""
+    _run_pair(SMALL, batch=4, t0s=[1000] * 4, steps=16, fast_slots=36, seed=14, rho=0.0, layers=2,
+              selector=selector, shared=True)
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "fp32"])

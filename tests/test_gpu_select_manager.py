@@ -160,3 +160,35 @@ def test_payload_round_trip_through_gather():
             np.testing.assert_array_equal(kv[0, :n], K[0, h, rows])
             np.testing.assert_array_equal(kv[1, :n], V[0, h, rows])
     eng.close()
+
+
+@pytest.mark.parametrize("tag", ["nosa", "infllmv2"])
+def test_shared_pool_manager_reproduces_reference_simulator(golden, tag):
+    """GPU shared-pool planner fed the reference simulator's own required sets
+    (offload_sim.simulate_decode, scripted AR(1) selections): identical fetch and evict lists
+    (victims across sequences) and the simulator's SimReport hit rates and bytes."""
+    g = golden("shared_pool_sim")
+    B, H, slots, total, _, steps = (int(x) for x in g[f"{tag}_shape"])
+    m = GpuTieredBlockManager(B * slots, total, heads=H, batch=B, n_b=16, d_head=64, shared=True)
+    topk_hits = topk_total = 0
+    for i in range(steps + 1):
+        if i == 1:
+            m.reset_stats()  # warm-up with step 0 (offload_sim.py:268-274)
+        req = {(b, h): {int(x) for x in g[f"{tag}_req"][i, b, h] if x >= 0} for b in range(B) for h in range(H)}
+        plans = m.plan_batch(req)
+        for b in range(B):
+            for h in range(H):
+                p = plans[(b, h)]
+                assert [k[2] for k in p.fetch] == [x for x in g[f"{tag}_fetch"][i, b, h] if x >= 0], (i, b, h)
+                assert [[k[0], k[2]] for k in p.evict] == [list(e) for e in g[f"{tag}_evict"][i, b, h] if e[0] >= 0]
+                if i:
+                    tk = {x for x in g[f"{tag}_topk"][i, b, h] if x >= 0}
+                    topk_hits += len(tk - {k[2] for k in p.fetch})
+                    topk_total += len(tk)
+    hit_rate, hit_rate_topk, bytes_up, bytes_down = g[f"{tag}_report"]
+    st = m.residency_stats()
+    assert st.hit_rate == hit_rate
+    assert topk_hits / topk_total == hit_rate_topk
+    # the reference's layout counts 2 bytes per element for a d_head-8 head; scale by block size
+    assert st.misses * (2 * 16 * 8 * 2) == bytes_up and st.evictions * (2 * 16 * 8 * 2) == bytes_down
+    m.close()

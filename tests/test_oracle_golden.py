@@ -47,6 +47,32 @@ def test_manager_trace_bit_exact(golden):
     assert (mgr.hits, mgr.misses, mgr.steps) == (hits, misses, calls)
 
 
+@pytest.mark.parametrize("tag", ["nosa", "infllmv2"])
+def test_shared_pool_matches_reference_simulator(golden, tag):
+    """One manager shared by the batch, b-major calls: the reference simulate_decode's residency."""
+    g = golden("shared_pool_sim")
+    B, H, slots, _, _, steps = (int(x) for x in g[f"{tag}_shape"])
+    mgr = O.SharedManager(H, B * slots)
+    topk_hits = topk_total = 0
+    for i in range(steps + 1):
+        if i == 1:
+            mgr.hits = mgr.misses = mgr.evictions = mgr.steps = 0
+        for b in range(B):
+            for h in range(H):
+                req = [x for x in g[f"{tag}_req"][i, b, h] if x >= 0]
+                fetch, evict, _ = mgr.plan_apply(req, b, h)
+                assert fetch == [x for x in g[f"{tag}_fetch"][i, b, h] if x >= 0], (i, b, h)
+                assert [list(k) for k in evict] == [list(e) for e in g[f"{tag}_evict"][i, b, h] if e[0] >= 0]
+                if i:
+                    tk = {x for x in g[f"{tag}_topk"][i, b, h] if x >= 0}
+                    topk_hits += len(tk - set(fetch))
+                    topk_total += len(tk)
+    hit_rate, hit_rate_topk, bytes_up, _ = g[f"{tag}_report"]
+    assert mgr.hits / (mgr.hits + mgr.misses) == hit_rate
+    assert mgr.misses * 2 * 16 * 8 * 2 == bytes_up
+    assert topk_hits / topk_total == hit_rate_topk
+
+
 @pytest.mark.parametrize("name", ["engine_small", "engine_small_infllmv2", "engine_cfg1"])
 def test_engine_matches_reference(golden, name):
     from paper_2510_13602_b200 import workload
