@@ -329,9 +329,14 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
     std::vector<int> neg((size_t)std::max<size_t>(LBH * dv.NB, LBH * dv.C), -1);
     cudaMemcpy(dv.slot_of, neg.data(), LBH * dv.NB * sizeof(int), cudaMemcpyHostToDevice);
     cudaMemcpy(dv.blk_of, neg.data(), LBH * dv.C * sizeof(int), cudaMemcpyHostToDevice);
-    std::vector<int> stack(LBH * dv.C), top(LBH, dv.C);
-    for (size_t x = 0; x < LBH; ++x)
-      for (int i = 0; i < dv.C; ++i) stack[x * dv.C + i] = dv.C - 1 - i;
+    // per-sequence pools: [C-1 .. 0] per row; shared pools: row (l, b, h) holds entries
+    // [b*C, b*C + C) of the (l, h) stack [B*C-1 .. 0] (kv_manager.py:147-150)
+    const int n_free = dv.shared ? dv.B * dv.C : dv.C;
+    std::vector<int> stack(LBH * dv.C), top(LBH, n_free);
+    for (size_t x = 0; x < LBH; ++x) {
+      const int b = (int)((x / dv.H) % dv.B);
+      for (int i = 0; i < dv.C; ++i) stack[x * dv.C + i] = n_free - 1 - ((dv.shared ? b * dv.C : 0) + i);
+    }
     cudaMemcpy(dv.fstack, stack.data(), stack.size() * sizeof(int), cudaMemcpyHostToDevice);
     cudaMemcpy(dv.ftop, top.data(), top.size() * sizeof(int), cudaMemcpyHostToDevice);
   }

@@ -90,7 +90,7 @@ class NosaEngine:
             raise ValueError(f"variant must be one of {tuple(_lib.VARIANT)} (retaining needs hidden states)")
         if residency not in _lib.RESIDENCY:
             raise ValueError(f"residency must be one of {tuple(_lib.RESIDENCY)}")
-        self.residency = residency
+        self.residency_mode = residency
         if dtype not in _lib.DTYPE:
             raise ValueError(f"dtype must be one of {tuple(_lib.DTYPE)}")
         self.config = config
