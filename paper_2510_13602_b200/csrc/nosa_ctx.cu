@@ -374,8 +374,15 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   cudaHostGetDevicePointer(&hdev, ctx->host_mirror, 0);
   dv.host = static_cast<char*>(hdev);
 
-  for (cudaStream_t* s : {&ctx->copy_stream, &ctx->capture_stream, &ctx->att_stream, &ctx->fin_stream})
-    cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+  // the miss transfer is the critical path when blocks are offloaded, attention when they are
+  // resident: both get the highest priority, so selection kernels of later layers only fill gaps
+  int prio_low = 0, prio_high = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
+  const bool use_prio = !(getenv("NOSA_NO_STREAM_PRIORITY"));
+  cudaStreamCreateWithPriority(&ctx->copy_stream, cudaStreamNonBlocking, use_prio ? prio_high : 0);
+  cudaStreamCreateWithPriority(&ctx->att_stream, cudaStreamNonBlocking, use_prio ? prio_high : 0);
+  cudaStreamCreateWithPriority(&ctx->fin_stream, cudaStreamNonBlocking, use_prio ? prio_high : 0);
+  cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   for (auto* evs : {&ctx->ev_plan, &ctx->ev_gather, &ctx->ev_att, &ctx->ev_fin}) {
     evs->resize(dv.L);
