@@ -44,7 +44,9 @@ struct NosaCtx {
   int gather_grid = 8;       // UVA gather CTAs: enough bytes in flight for the link, few SMs taken
   int tma_gather_grid = 24;  // TMA gather CTAs (one warp, 4 x 32 KiB stages each)
   cudaStream_t copy_stream = nullptr;
-  cudaStream_t att_stream = nullptr, fin_stream = nullptr;  // attention / finalize stages
+  cudaStream_t att_stream = nullptr, att_stream2 = nullptr, fin_stream = nullptr;  // attention (even /
+  // odd layers, so one layer's attention tail overlaps the next) and finalize stages
+  bool two_att = true;
   std::vector<cudaEvent_t> ev_plan, ev_gather, ev_att, ev_fin;
   cudaEvent_t ev_fork = nullptr;
   char* host_mirror = nullptr;
@@ -210,7 +212,8 @@ static void release(NosaCtx* ctx) {
   for (auto* evs : {&ctx->ev_plan, &ctx->ev_gather, &ctx->ev_att, &ctx->ev_fin})
     for (auto e : *evs) cudaEventDestroy(e);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
-  for (cudaStream_t s : {ctx->copy_stream, ctx->capture_stream, ctx->att_stream, ctx->fin_stream, ctx->meta_stream})
+  for (cudaStream_t s : {ctx->copy_stream, ctx->capture_stream, ctx->att_stream, ctx->att_stream2, ctx->fin_stream,
+                         ctx->meta_stream})
     if (s) cudaStreamDestroy(s);
   if (ctx->h_list) cudaFreeHost(ctx->h_list);
   if (ctx->h_cnt) cudaFreeHost(ctx->h_cnt);
@@ -381,6 +384,8 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   const bool use_prio = !(getenv("NOSA_NO_STREAM_PRIORITY"));
   cudaStreamCreateWithPriority(&ctx->copy_stream, cudaStreamNonBlocking, use_prio ? prio_high : 0);
   cudaStreamCreateWithPriority(&ctx->att_stream, cudaStreamNonBlocking, use_prio ? prio_high : 0);
+  cudaStreamCreateWithPriority(&ctx->att_stream2, cudaStreamNonBlocking, use_prio ? prio_high : 0);
+  ctx->two_att = !getenv("NOSA_ONE_ATT_STREAM");
   cudaStreamCreateWithPriority(&ctx->fin_stream, cudaStreamNonBlocking, use_prio ? prio_high : 0);
   cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
@@ -676,7 +681,8 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   const bool serial = io->schedule == 1;
   cudaStream_t cp = ctx->copy_stream, at = ctx->att_stream, fn = ctx->fin_stream;
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, st));  // side streams start after the caller's work
-  for (cudaStream_t s : {cp, at, fn}) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_fork, 0));
+  cudaStream_t at2 = ctx->two_att ? ctx->att_stream2 : at;
+  for (cudaStream_t s : {cp, at, at2, fn}) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_fork, 0));
   auto select = [&](int l) -> int {
     CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt + 2 * l, 0, 2 * sizeof(int), st));
     {
@@ -705,14 +711,15 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
       if (count) ctx->launches += 1;
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[l], cp));
-    CUDA_TRY(ctx, cudaStreamWaitEvent(at, ctx->ev_gather[l], 0));
-    if (l >= 2) CUDA_TRY(ctx, cudaStreamWaitEvent(at, ctx->ev_fin[l - 2], 0));
+    cudaStream_t a = (l & 1) ? at2 : at;
+    CUDA_TRY(ctx, cudaStreamWaitEvent(a, ctx->ev_gather[l], 0));
+    if (l >= 2) CUDA_TRY(ctx, cudaStreamWaitEvent(a, ctx->ev_fin[l - 2], 0));
     {
-      TimeScope ts(ctx, at, 2, timed);
+      TimeScope ts(ctx, a, 2, timed);
       CUDA_TRY(ctx, nosa::launch_attend(dv, l, q + l * qstride, kn + l * kstride, vn + l * kstride,
-                                        io->out + l * ostride, at, ctx->num_sms));
+                                        io->out + l * ostride, a, ctx->num_sms));
     }
-    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_att[l], at));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_att[l], a));
     CUDA_TRY(ctx, cudaStreamWaitEvent(fn, ctx->ev_att[l], 0));
     {
       TimeScope ts(ctx, fn, 3, timed);
@@ -723,6 +730,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   // join every side stream back into the caller's stream
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_gather[dv.L - 1], 0));
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_att[dv.L - 1], 0));
+  if (dv.L > 1) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_att[dv.L - 2], 0));
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_fin[dv.L - 1], 0));
   if (count) ctx->launches += (dv.shared ? 4LL : 3LL) * dv.L;  // + the gather kernels counted above
   return NOSA_OK;
