@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--cpu-pairs", type=int, default=8, help="(sequence, layer) pairs in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--trace-out", default=None, help="write the device timeline of one instrumented step here")
     ap.add_argument("--eager", action="store_true",
                     help="launch every kernel from the host instead of replaying the captured step graph")
     return ap.parse_args()
@@ -282,6 +283,15 @@ def run_native(args, rank, world, local_rank):
     ei1.record()
     torch.cuda.synchronize(device)
     kern = eng.timing_read()
+    if args.trace_out:  # device timeline of the last instrumented step (one line per kernel)
+        tr = eng.timing_trace()
+        last = tr[-(len(tr) // args.steps):]
+        base, seen = min(x[1] for x in last), {}
+        with open(args.trace_out, "w") as f:
+            f.write("kind layer start_us end_us dur_us\n")
+            for k, s0, s1 in last:
+                seen[k] = seen.get(k, -1) + 1
+                f.write(f"{k} {seen[k]} {1000 * (s0 - base):.1f} {1000 * (s1 - base):.1f} {1000 * (s1 - s0):.1f}\n")
     st_i = eng.residency_stats()
     instrumented_ms = ei0.elapsed_time(ei1) / args.steps
     eng.timing_enable(0)
@@ -302,11 +312,10 @@ def run_native(args, rank, world, local_rank):
             if use_graph:  # straight into the graph's input buffers
                 gq.copy_(hq, non_blocking=True); gk.copy_(hk, non_blocking=True); gv.copy_(hv, non_blocking=True)
                 eng.replay()
-            else:
-                dq.copy_(hq, non_blocking=True); dk.copy_(hk, non_blocking=True); dv.copy_(hv, non_blocking=True)
-                eng.step(dq, dk, dv, selector=args.selector, out=out, gather=args.gather, check=False,
-                         schedule=args.schedule)
-            host_out.copy_(out, non_blocking=True)
+                host_out.copy_(out, non_blocking=True)
+            else:  # the host-buffer C ABI call: per-layer H2D of inputs, D2H of outputs inside the step
+                eng.step_host(hq, hk, hv, selector=args.selector, out=host_out, gather=args.gather,
+                              schedule=args.schedule, sync=False)
         e1.record()
         torch.cuda.synchronize(device)
         e_ms = max_over_ranks(e0.elapsed_time(e1), device)
@@ -315,7 +324,9 @@ def run_native(args, rank, world, local_rank):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": host_out.numel() * 4,
                "ms_per_step": round(e_ms / args.steps, 4),
                "api": ("NosaEngine.capture/replay (C ABI nosa_step_graph_launch)" if use_graph else
-                       "NosaEngine.step (C ABI nosa_decode_step)") + " on inputs copied from pinned host memory"}
+                       "NosaEngine.step_host (C ABI nosa_decode_step_host: per-layer H2D of q/k/v on the copy "
+                       "stream, D2H of each layer's output overlapping later layers)") +
+                      " on inputs in pinned host memory"}
         eng.check_errors()
 
     # ---------------- roofline arithmetic (algorithmic bytes, SURVEY.md §8d / DESIGN.md)
@@ -335,9 +346,9 @@ def run_native(args, rank, world, local_rank):
         # K4 merge + K5: f32 outputs + the appended K/V row (HBM slot)
         "finalize": B * cfg.n_head * cfg.d_head * 4 + B * cfg.n_kv_head * 2 * cfg.d_head * 2,
     }
-    for k_ in kern:
-        kern[k_]["bytes_per_launch"] = per_launch[k_]
-        kern[k_]["gbs"] = per_launch[k_] / (kern[k_]["avg_ms"] * 1e-3) / 1e9 if kern[k_]["avg_ms"] else None
+    for k_ in kern:  # per_launch holds bytes per layer; selection may cover several layers per launch
+        kern[k_]["bytes_per_launch"] = per_launch[k_] * calls / max(kern[k_]["launches"], 1)
+        kern[k_]["gbs"] = per_launch[k_] * calls / (kern[k_]["total_ms"] * 1e-3) / 1e9 if kern[k_]["total_ms"] else None
     traffic = None
     tpath = ROOT / "profiles" / "traffic.json"
     if tpath.exists():

@@ -98,6 +98,18 @@ typedef struct NosaStepIO {
                           1 = layer-serial (select of layer l+1 after layer l completes) */
 } NosaStepIO;
 
+/* nosa_decode_step_host: the same tensors in HOST memory (pinned for asynchronous copies;
+ * pageable works but serialises).  Same layouts and meanings as NosaStepIO. */
+typedef struct NosaHostStepIO {
+  const void* q;
+  const void* k_new;
+  const void* v_new;
+  float* out;
+  int32_t selector;
+  int32_t gather_mode;
+  int32_t schedule;
+} NosaHostStepIO;
+
 typedef struct NosaCtx NosaCtx;
 
 /* ---- configuration ---------------------------------------------------------------- */
@@ -181,6 +193,14 @@ int nosa_attend(NosaCtx* ctx, int layer, const void* q, const void* k_new, const
  * layer's gather.  Equivalent to per-layer nosa_select_plan, nosa_gather, nosa_attend. */
 int nosa_decode_step(NosaCtx* ctx, const NosaStepIO* io, void* stream);
 
+/* nosa_decode_step on host buffers: the reference's own calling convention
+ * (DecodeEngine.step takes and returns host arrays, decode.py:152-190), batched.  Layer l's
+ * q/k/v go host->device on the copy stream ahead of the miss gathers, its output comes back on
+ * a device->host stream as soon as layer l is done (overlapping later layers).  Asynchronous on
+ * `stream`: the host buffers must stay valid, and `out` is complete, once `stream` reaches this
+ * point (cudaStreamSynchronize).  The context owns the device staging. */
+int nosa_decode_step_host(NosaCtx* ctx, const NosaHostStepIO* io, void* stream);
+
 /* CUDA-graph form of nosa_decode_step for fixed io pointers: capture once, replay per step. */
 int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io);
 int nosa_step_graph_launch(NosaCtx* ctx, void* stream);
@@ -240,6 +260,11 @@ int nosa_check_errors(NosaCtx* ctx, uint32_t* flags);
  * counts per kind since enable. */
 int nosa_timing_enable(NosaCtx* ctx, int max_launches);
 int nosa_timing_read(NosaCtx* ctx, double* total_ms /* [4] */, int64_t* launches /* [4] */);
+
+/* The timed launches since enable, in issue order: kind and start/end milliseconds relative to
+ * the first one (a device timeline of the step's streams).  Synchronises. */
+int nosa_timing_trace(NosaCtx* ctx, int cap, int32_t* kind, float* start_ms, float* end_ms,
+                      int32_t* n);
 
 /* kernel launches issued by this library since context creation (bench evidence) */
 int64_t nosa_launch_count(const NosaCtx* ctx);

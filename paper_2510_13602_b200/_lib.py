@@ -50,6 +50,10 @@ class NosaStepIO(ctypes.Structure):
                 ("schedule", ctypes.c_int32)]
 
 
+class NosaHostStepIO(NosaStepIO):
+    """Same fields as NosaStepIO; the pointers are host addresses (nosa_decode_step_host)."""
+
+
 # every symbol include/nosa_b200.h declares, with its ctypes signature
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -72,6 +76,7 @@ SIGNATURES = {
     "nosa_gather": (_I, [_P, _I, _I, _P]),
     "nosa_attend": (_I, [_P, _I, _P, _P, _P, _P, _P]),
     "nosa_decode_step": (_I, [_P, ctypes.POINTER(NosaStepIO), _P]),
+    "nosa_decode_step_host": (_I, [_P, ctypes.POINTER(NosaHostStepIO), _P]),
     "nosa_step_graph_capture": (_I, [_P, ctypes.POINTER(NosaStepIO)]),
     "nosa_step_graph_launch": (_I, [_P, _P]),
     "nosa_select_scores": (_I, [_I, _P, _P, _I, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P]),
@@ -88,6 +93,7 @@ SIGNATURES = {
     "nosa_launch_count": (ctypes.c_int64, [_P]),
     "nosa_timing_enable": (_I, [_P, _I]),
     "nosa_timing_read": (_I, [_P, _F64P, ctypes.POINTER(ctypes.c_int64)]),
+    "nosa_timing_trace": (_I, [_P, _I, _I32P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float), _I32P]),
 }
 
 

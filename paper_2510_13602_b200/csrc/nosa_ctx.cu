@@ -16,7 +16,7 @@
 
 namespace nosa {
 cudaError_t launch_select_plan(const Dev& dv, int layer, const void* q, int selector, int mode,
-                               const int* ext_req, const int* ext_nreq, cudaStream_t st);
+                               const int* ext_req, const int* ext_nreq, cudaStream_t st, int layers = 1);
 cudaError_t launch_start_run(const Dev& dv, int seq_begin, int seq_count, cudaStream_t st);
 cudaError_t launch_plan_shared(const Dev& dv, int layer, const int* ext_req, const int* ext_nreq, cudaStream_t st);
 cudaError_t launch_select_scores(int n_prob, const double* s_q, const double* s_e, int stride,
@@ -80,6 +80,15 @@ struct NosaCtx {
   std::vector<void*> b_dst, b_src;
   std::vector<size_t> b_size;
   long long batch_fallbacks = 0;
+  // host-buffer step (nosa_decode_step_host): device staging of the step's inputs and outputs,
+  // per-layer input-arrival / output-ready events, and the device->host stream
+  cudaStream_t d2h_stream = nullptr;
+  std::vector<cudaEvent_t> ev_in;
+  cudaEvent_t ev_d2h = nullptr;
+  char* io_buf = nullptr;
+  size_t io_bytes = 0;
+  bool select_per_layer = false;  // NOSA_SELECT_PER_LAYER: one selection launch per layer
+  long long select_launches = 0;  // grouped selection launches of the step being enqueued
 };
 
 // brackets one launch with timing events when timing is enabled (eager steps only)
@@ -209,11 +218,12 @@ static void release(NosaCtx* ctx) {
     if (x) cudaGraphExecDestroy(x);
   for (cudaGraph_t x : {ctx->graph, ctx->graph_timed})
     if (x) cudaGraphDestroy(x);
-  for (auto* evs : {&ctx->ev_plan, &ctx->ev_gather, &ctx->ev_att, &ctx->ev_fin})
+  for (auto* evs : {&ctx->ev_plan, &ctx->ev_gather, &ctx->ev_att, &ctx->ev_fin, &ctx->ev_in})
     for (auto e : *evs) cudaEventDestroy(e);
-  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_d2h})
+    if (e) cudaEventDestroy(e);
   for (cudaStream_t s : {ctx->copy_stream, ctx->capture_stream, ctx->att_stream, ctx->att_stream2, ctx->fin_stream,
-                         ctx->meta_stream})
+                         ctx->meta_stream, ctx->d2h_stream})
     if (s) cudaStreamDestroy(s);
   if (ctx->h_list) cudaFreeHost(ctx->h_list);
   if (ctx->h_cnt) cudaFreeHost(ctx->h_cnt);
@@ -224,6 +234,7 @@ static void release(NosaCtx* ctx) {
     }
   for (void* p : ctx->dev_allocs) cudaFree(p);
   if (ctx->staging) cudaFree(ctx->staging);
+  if (ctx->io_buf) cudaFree(ctx->io_buf);
   if (ctx->host_mirror) {
     if (ctx->host_registered) {
       cudaHostUnregister(ctx->host_mirror);
@@ -386,6 +397,7 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   cudaStreamCreateWithPriority(&ctx->att_stream, cudaStreamNonBlocking, use_prio ? prio_high : 0);
   cudaStreamCreateWithPriority(&ctx->att_stream2, cudaStreamNonBlocking, use_prio ? prio_high : 0);
   ctx->two_att = !getenv("NOSA_ONE_ATT_STREAM");
+  ctx->select_per_layer = getenv("NOSA_SELECT_PER_LAYER") != nullptr;
   cudaStreamCreateWithPriority(&ctx->fin_stream, cudaStreamNonBlocking, use_prio ? prio_high : 0);
   cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
@@ -455,6 +467,7 @@ extern "C" int nosa_prefill(NosaCtx* ctx, int layer, int seq_begin, int seq_coun
   if (need > ctx->staging_bytes) {
     cudaStreamSynchronize(S(stream));
     if (ctx->staging) cudaFree(ctx->staging);
+  if (ctx->io_buf) cudaFree(ctx->io_buf);
     ctx->staging = nullptr;
     CUDA_TRY(ctx, cudaMalloc(&ctx->staging, need));
     ctx->staging_bytes = need;
@@ -662,7 +675,27 @@ extern "C" int nosa_timing_read(NosaCtx* ctx, double* total_ms, int64_t* launche
   return NOSA_OK;
 }
 
-static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, bool count) {
+// `hio` (optional): the step's tensors live in host memory.  `io` then points at the
+// context's device staging; layer l's q/k/v are copied in on the copy stream ahead of the miss
+// gathers (select(l) waits for its own layer only) and its output is copied back on the d2h
+// stream as soon as finalize(l) is done, so the read-back of layer l overlaps layer l+1.
+extern "C" int nosa_timing_trace(NosaCtx* ctx, int cap, int32_t* kind, float* start_ms, float* end_ms, int32_t* n) {
+  if (!ctx || !n || (cap > 0 && (!kind || !start_ms || !end_ms))) return NOSA_ERR_VALUE;
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaDeviceSynchronize());
+  const int m = (int)std::min<size_t>(ctx->timing_used, (size_t)std::max(cap, 0));
+  for (int i = 0; i < m; ++i) {
+    const NosaCtx::Timed& t = ctx->timing[i];
+    kind[i] = t.kind;
+    CUDA_TRY(ctx, cudaEventElapsedTime(&start_ms[i], ctx->timing[0].a, t.a));
+    CUDA_TRY(ctx, cudaEventElapsedTime(&end_ms[i], ctx->timing[0].a, t.b));
+  }
+  *n = m;
+  return NOSA_OK;
+}
+
+static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, bool count,
+                        const NosaHostStepIO* hio = nullptr) {
   const Dev& dv = ctx->dv;
   const size_t qstride = (size_t)dv.B * dv.Hq * dv.D * dv.elem;
   const size_t kstride = (size_t)dv.B * dv.H * dv.D * dv.elem;
@@ -683,7 +716,22 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, st));  // side streams start after the caller's work
   cudaStream_t at2 = ctx->two_att ? ctx->att_stream2 : at;
   for (cudaStream_t s : {cp, at, at2, fn}) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_fork, 0));
+  if (hio) {
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_fork, 0));
+    for (int l = 0; l < dv.L; ++l) {
+      CUDA_TRY(ctx, cudaMemcpyAsync(const_cast<char*>(q) + l * qstride, static_cast<const char*>(hio->q) + l * qstride,
+                                    qstride, cudaMemcpyHostToDevice, cp));
+      CUDA_TRY(ctx, cudaMemcpyAsync(const_cast<char*>(kn) + l * kstride,
+                                    static_cast<const char*>(hio->k_new) + l * kstride, kstride,
+                                    cudaMemcpyHostToDevice, cp));
+      CUDA_TRY(ctx, cudaMemcpyAsync(const_cast<char*>(vn) + l * kstride,
+                                    static_cast<const char*>(hio->v_new) + l * kstride, kstride,
+                                    cudaMemcpyHostToDevice, cp));
+      CUDA_TRY(ctx, cudaEventRecord(ctx->ev_in[l], cp));
+    }
+  }
   auto select = [&](int l) -> int {
+    if (hio) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_in[l], 0));
     CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt + 2 * l, 0, 2 * sizeof(int), st));
     {
       TimeScope ts(ctx, st, 0, timed);
@@ -692,9 +740,31 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[l], st));
     return NOSA_OK;
   };
-  if (!serial)
-    for (int l = 0; l < dv.L; ++l)
-      if (int rc = select(l)) return rc;
+  // Pipelined: the layers' selections are launched in groups of doubling size (1, 1, 2, 4, 8,
+  // ...), one grid of (B*H, layers) per group, so layer 0's plan (and its miss transfer) starts
+  // at once while the later layers' selections fill the whole GPU in a few launches.
+  auto select_group = [&](int l0, int n) -> int {
+    if (hio) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_in[l0 + n - 1], 0));
+    CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt + 2 * l0, 0, 2 * n * sizeof(int), st));
+    {
+      TimeScope ts(ctx, st, 0, timed);
+      CUDA_TRY(ctx, nosa::launch_select_plan(dv, l0, q + l0 * qstride, io->selector, 1, nullptr, nullptr, st, n));
+    }
+    for (int l = l0; l < l0 + n; ++l) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[l], st));
+    return NOSA_OK;
+  };
+  if (!serial) {
+    if (dv.shared || ctx->select_per_layer) {
+      for (int l = 0; l < dv.L; ++l)
+        if (int rc = select(l)) return rc;
+    } else {
+      for (int l0 = 0, n = 1; l0 < dv.L; l0 += n, n = (l0 <= 1 ? 1 : l0)) {
+        n = std::min(n, dv.L - l0);
+        if (int rc = select_group(l0, n)) return rc;
+        if (count) ctx->select_launches += 1;
+      }
+    }
+  }
   for (int l = 0; l < dv.L; ++l) {
     if (serial) {
       if (l > 0) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_fin[l - 1], 0));
@@ -726,13 +796,24 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
       CUDA_TRY(ctx, nosa::launch_finalize(dv, l, kn + l * kstride, vn + l * kstride, io->out + l * ostride, fn));
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fin[l], fn));
+    if (hio) {
+      CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_fin[l], 0));
+      CUDA_TRY(ctx, cudaMemcpyAsync(hio->out + l * ostride, io->out + l * ostride, ostride * sizeof(float),
+                                    cudaMemcpyDeviceToHost, ctx->d2h_stream));
+    }
+  }
+  if (hio) {
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_d2h, ctx->d2h_stream));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_d2h, 0));
   }
   // join every side stream back into the caller's stream
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_gather[dv.L - 1], 0));
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_att[dv.L - 1], 0));
   if (dv.L > 1) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_att[dv.L - 2], 0));
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_fin[dv.L - 1], 0));
-  if (count) ctx->launches += (dv.shared ? 4LL : 3LL) * dv.L;  // + the gather kernels counted above
+  // + the gather kernels counted above; grouped selections counted in select_group
+  if (count) ctx->launches += (dv.shared ? 4LL : 3LL) * dv.L - (ctx->select_launches ? dv.L - ctx->select_launches : 0);
+  ctx->select_launches = 0;
   return NOSA_OK;
 }
 
@@ -742,6 +823,34 @@ extern "C" int nosa_decode_step(NosaCtx* ctx, const NosaStepIO* io, void* stream
   if (io->selector != 0 && io->selector != 1) return fail(ctx, NOSA_ERR_VALUE, "selector must be nosa or infllmv2");
   cudaSetDevice(ctx->device);
   return enqueue_step(ctx, io, S(stream), true);
+}
+
+extern "C" int nosa_decode_step_host(NosaCtx* ctx, const NosaHostStepIO* hio, void* stream) {
+  if (!ctx || !hio || !hio->q || !hio->k_new || !hio->v_new || !hio->out)
+    return fail(ctx, NOSA_ERR_VALUE, "decode_step_host: NULL io");
+  if (hio->selector != 0 && hio->selector != 1) return fail(ctx, NOSA_ERR_VALUE, "selector must be nosa or infllmv2");
+  cudaSetDevice(ctx->device);
+  const Dev& dv = ctx->dv;
+  const size_t qb = (size_t)dv.L * dv.B * dv.Hq * dv.D * dv.elem, kb = (size_t)dv.L * dv.B * dv.H * dv.D * dv.elem;
+  const size_t ob = (size_t)dv.L * dv.B * dv.Hq * dv.D * sizeof(float);
+  const size_t need = qb + 2 * kb + ob;
+  if (!ctx->io_buf) {
+    CUDA_TRY(ctx, cudaMalloc(reinterpret_cast<void**>(&ctx->io_buf), need));
+    ctx->io_bytes = need;
+    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_d2h, cudaEventDisableTiming));
+    ctx->ev_in.resize(dv.L);
+    for (int l = 0; l < dv.L; ++l) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_in[l], cudaEventDisableTiming));
+  }
+  NosaStepIO io{};
+  io.q = ctx->io_buf;
+  io.k_new = ctx->io_buf + qb;
+  io.v_new = ctx->io_buf + qb + kb;
+  io.out = reinterpret_cast<float*>(ctx->io_buf + qb + 2 * kb);
+  io.selector = hio->selector;
+  io.gather_mode = hio->gather_mode;
+  io.schedule = hio->schedule;
+  return enqueue_step(ctx, &io, S(stream), true, hio);
 }
 
 extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {
@@ -768,6 +877,11 @@ extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {
   if (int rc = capture(false, &ctx->graph)) return rc;
   CUDA_TRY(ctx, cudaGraphInstantiate(&ctx->graph_exec, ctx->graph, 0));
   ctx->graph_kernels = (ctx->dv.shared ? 5 : 4) * ctx->dv.L;
+  if (!ctx->dv.shared && !ctx->select_per_layer && io->schedule != 1) {  // grouped selections
+    int groups = 0;
+    for (int l0 = 0, n = 1; l0 < ctx->dv.L; l0 += n, n = (l0 <= 1 ? 1 : l0)) ++groups;
+    ctx->graph_kernels -= ctx->dv.L - groups;
+  }
   // the instrumented twin: an external event-record node around every kernel (placeholders)
   const size_t nslots = 4 * (size_t)ctx->dv.L;
   while (ctx->cap_events.size() < nslots) {

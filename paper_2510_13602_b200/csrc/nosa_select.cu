@@ -419,12 +419,15 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
   }
 }
 
-// grid = B*H, block = 256.  mode: 0 = select only, 1 = select + plan, 2 = plan on ext_req.
+// grid = (B*H, layers), block = 256: layer = layer0 + blockIdx.y with its queries at
+// q + blockIdx.y * q_layer_stride.  mode: 0 = select only, 1 = select + plan, 2 = plan on ext_req.
 template <typename T>
 __global__ void __launch_bounds__(256)
-    select_plan_kernel(Dev dv, int layer, const T* __restrict__ q, int selector, int mode,
-                       const int* __restrict__ ext_req, const int* __restrict__ ext_nreq) {
+    select_plan_kernel(Dev dv, int layer0, const T* __restrict__ q0, size_t q_layer_stride, int selector,
+                       int mode, const int* __restrict__ ext_req, const int* __restrict__ ext_nreq) {
   extern __shared__ __align__(16) char smem_raw[];
+  const int layer = layer0 + blockIdx.y;
+  const T* q = q0 + blockIdx.y * q_layer_stride;
   const int bh = blockIdx.x;
   const int b = bh / dv.H, h = bh % dv.H;
   const int lbh = (layer * dv.B + b) * dv.H + h;
@@ -703,20 +706,21 @@ cudaError_t launch_plan_shared(const Dev& dv, int layer, const int* ext_req, con
 // ------------------------------------------------------------------------------------------
 // host-side launchers
 cudaError_t launch_select_plan(const Dev& dv, int layer, const void* q, int selector, int mode,
-                               const int* ext_req, const int* ext_nreq, cudaStream_t st) {
+                               const int* ext_req, const int* ext_nreq, cudaStream_t st, int layers) {
   int Pp = 32;
   while (Pp < dv.NB) Pp <<= 1;
   const size_t smem = sel_smem_bytes(dv.D, Pp, dv.C);
+  const size_t qs = (size_t)dv.B * dv.Hq * dv.D;  // elements per layer of q
+  const dim3 grid(dv.B * dv.H, layers);
   if (dv.dtype == 0) {
     auto k = select_plan_kernel<__nv_bfloat16>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<dv.B * dv.H, 256, smem, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(q), selector,
-                                      mode, ext_req, ext_nreq);
+    k<<<grid, 256, smem, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(q), qs, selector, mode, ext_req,
+                               ext_nreq);
   } else {
     auto k = select_plan_kernel<float>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<dv.B * dv.H, 256, smem, st>>>(dv, layer, static_cast<const float*>(q), selector, mode,
-                                      ext_req, ext_nreq);
+    k<<<grid, 256, smem, st>>>(dv, layer, static_cast<const float*>(q), qs, selector, mode, ext_req, ext_nreq);
   }
   return cudaGetLastError();
 }

@@ -234,6 +234,49 @@ class NosaEngine:
             self.check_errors()
         return out
 
+    def step_host(self, q, k_new, v_new, selector: str = "nosa", out: torch.Tensor | None = None,
+                  gather: str = "uva", schedule: str = "pipelined", sync: bool = True) -> torch.Tensor:
+        """`step` on host tensors (the reference's calling convention: host arrays in, host
+        array out).  q/k_new/v_new: CPU tensors of the engine dtype in the `step` layouts, pinned
+        for asynchronous copies.  Layer l's inputs are copied in ahead of the miss gathers and
+        its output is copied back while later layers run.  Returns `out`, a CPU float32
+        [layers][batch][n_head][d_head] (pinned if allocated here); with sync=False it is only
+        complete once torch's current stream reaches this point."""
+        if selector not in SELECTORS:
+            raise ValueError(f"selector must be one of {SELECTORS}")
+        if gather not in _lib.GATHER or schedule not in _lib.SCHEDULE:
+            raise ValueError(f"gather must be one of {tuple(_lib.GATHER)}, schedule one of {tuple(_lib.SCHEDULE)}")
+        self._check_step()
+        L, B, cfg = self.layers, self.batch, self.config
+        dt = _TORCH_DTYPE[self.dtype]
+        shapes = ((L, B, cfg.n_head, cfg.d_head), (L, B, cfg.n_kv_head, cfg.d_head), (L, B, cfg.n_kv_head, cfg.d_head))
+        host = []
+        for name, x, shp in zip(("q", "k_new", "v_new"), (q, k_new, v_new), shapes):
+            if isinstance(x, np.ndarray):
+                x = torch.from_numpy(np.ascontiguousarray(x))
+            if not isinstance(x, torch.Tensor) or x.device.type != "cpu":
+                raise ValueError(f"{name} must be a host array or CPU tensor")
+            if x.dtype != dt or not x.is_contiguous():  # converted once here; pass pinned dt tensors to avoid it
+                x = x.to(dt).contiguous().pin_memory()
+            if x.numel() != int(np.prod(shp)):
+                raise ValueError(f"{name} has {x.numel()} elements, expected {shp}")
+            host.append(x)
+        q, k_new, v_new = host
+        if out is None:
+            out = torch.empty((L, B, cfg.n_head, cfg.d_head), dtype=torch.float32, pin_memory=True)
+        elif out.device.type != "cpu" or out.dtype != torch.float32 or not out.is_contiguous() \
+                or out.numel() != L * B * cfg.n_head * cfg.d_head:
+            raise ValueError("out must be a contiguous CPU float32 tensor of the output shape")
+        io = _lib.NosaHostStepIO(q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), out.data_ptr(),
+                                 _lib.SELECTOR[selector], _lib.GATHER[gather], _lib.SCHEDULE[schedule])
+        with torch.cuda.device(self.device):
+            self._call(_lib.lib.nosa_decode_step_host, ctypes.byref(io), _lib.stream_ptr())
+            self._t += 1
+            if sync:
+                torch.cuda.current_stream().synchronize()
+                self.check_errors()
+        return out
+
     def step_layer(self, layer: int, q, k_new, v_new, selector: str = "nosa", out=None,
                    gather: str = "uva") -> torch.Tensor:
         """The same step for one layer, stage by stage through the C ABI."""
@@ -381,3 +424,14 @@ class NosaEngine:
         self._call(_lib.lib.nosa_timing_read, ms, n)
         return {k: {"total_ms": ms[i], "launches": n[i], "avg_ms": ms[i] / n[i] if n[i] else 0.0}
                 for i, k in enumerate(self.KERNEL_KINDS)}
+
+    def timing_trace(self, cap: int = 65536) -> list[tuple[str, float, float]]:
+        """(kind, start_ms, end_ms) of every timed launch since timing_enable, in issue order,
+        relative to the first launch: the device timeline of the step's streams."""
+        kind = np.zeros(cap, np.int32)
+        t0, t1 = np.zeros(cap, np.float32), np.zeros(cap, np.float32)
+        n = ctypes.c_int32()
+        F = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        self._call(_lib.lib.nosa_timing_trace, cap, kind.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), F(t0), F(t1),
+                   ctypes.byref(n))
+        return [(self.KERNEL_KINDS[kind[i]], float(t0[i]), float(t1[i])) for i in range(n.value)]

@@ -227,12 +227,18 @@ def test_gather_paths_and_schedules_bitwise_identical():
     K, V = workload.prefix_kv(2, 6, cfg.n_kv_head, 3000, cfg.d_head)
     K, V = K.reshape(3, 2, cfg.n_kv_head, 3000, cfg.d_head), V.reshape(3, 2, cfg.n_kv_head, 3000, cfg.d_head)
     results = []
-    for gather, schedule in [("uva", "pipelined"), ("tma", "pipelined"), ("memcpy", "pipelined"), ("uva", "serial")]:
+    runs = [("uva", "pipelined", False), ("tma", "pipelined", False), ("memcpy", "pipelined", False),
+            ("uva", "serial", False), ("memcpy", "pipelined", True), ("uva", "serial", True)]
+    for gather, schedule, host in runs:
         eng = NosaEngine(cfg, batch=2, layers=3, max_tokens=3100, fast_slots=70, w1=w1, w2=w2)
         eng.prefill(torch.from_numpy(K), torch.from_numpy(V))
         eng.start_run()
         stream = workload.QueryStream(2, 3, 2, cfg.n_head, cfg.n_kv_head, cfg.d_head, 0.0)
-        outs = [eng.step(*stream.next(), gather=gather, schedule=schedule).cpu().numpy() for _ in range(70)]
+        if host:  # nosa_decode_step_host: pinned host tensors in, host outputs back
+            outs = [eng.step_host(*stream.next(), gather=gather,
+                                  schedule=schedule).clone().numpy() for _ in range(70)]
+        else:
+            outs = [eng.step(*stream.next(), gather=gather, schedule=schedule).cpu().numpy() for _ in range(70)]
         st = eng.residency_stats()
         results.append((np.stack(outs), st.hits, st.misses, st.evictions))
         eng.close()

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--selector", default="nosa")
     ap.add_argument("--gather", default="uva")
     ap.add_argument("--layer-by-layer", action="store_true", help="use the per-layer C-ABI calls")
+    ap.add_argument("--trace", action="store_true", help="print the device timeline of the last step")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     cfg = one_b_config(65536)
@@ -69,6 +70,17 @@ def main():
     res = {"ms_per_step": e0.elapsed_time(e1) / (a.steps - 2), "kernels": eng.timing_read(),
            "hit_rate": st.hit_rate, "misses": st.misses, "hits": st.hits}
     print(json.dumps(res, indent=1))
+    if a.trace:
+        tr = eng.timing_trace()
+        per_step = len(tr) // (a.steps - 2)
+        last = tr[-per_step:]
+        base = min(x[1] for x in last)
+        seen = {}
+        print("kind        layer   start_us   end_us   dur_us")
+        for k, s0, s1 in last:
+            l = seen.get(k, 0)
+            seen[k] = l + 1
+            print(f"{k:11s} {l:5d} {1000 * (s0 - base):10.1f} {1000 * (s1 - base):8.1f} {1000 * (s1 - s0):8.1f}")
     eng.check_errors()
     eng.close()
 
