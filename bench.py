@@ -300,7 +300,11 @@ def run_native(args, rank, world, local_rank):
     # ---------------- end to end: host inputs H2D + step + D2H of the outputs, every step
     e2e = None
     if not args.no_e2e:
-        host_in = [tuple(x.cpu().pin_memory() for x in step_in) for step_in in inputs_e2e]
+        def pinned(x):  # page-locked buffer from cudaHostAlloc (torch's pin_memory() path is slower)
+            h = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+            h.copy_(x)
+            return h
+        host_in = [tuple(pinned(x) for x in step_in) for step_in in inputs_e2e]
         dq, dk, dv = (torch.empty_like(x) for x in inputs[0])
         host_out = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
         if world > 1:
@@ -328,6 +332,19 @@ def run_native(args, rank, world, local_rank):
                        "stream, D2H of each layer's output overlapping later layers)") +
                       " on inputs in pinned host memory"}
         eng.check_errors()
+        if args.trace_out:  # one more host-buffer step, instrumented, for the timeline
+            eng.timing_enable(8 * L + 8)
+            hq, hk, hv = (pinned(x) for x in stream.next())  # fresh queries: real misses
+            eng.step_host(hq, hk, hv, selector=args.selector, out=host_out, gather=args.gather,
+                          schedule=args.schedule)
+            tr = eng.timing_trace()
+            base, seen = min(x[1] for x in tr), {}
+            with open(args.trace_out + ".e2e", "w") as f:
+                f.write("kind layer start_us end_us dur_us\n")
+                for k, s0, s1 in tr:
+                    seen[k] = seen.get(k, -1) + 1
+                    f.write(f"{k} {seen[k]} {1000 * (s0 - base):.1f} {1000 * (s1 - base):.1f} {1000 * (s1 - s0):.1f}\n")
+            eng.timing_enable(0)
 
     # ---------------- roofline arithmetic (algorithmic bytes, SURVEY.md §8d / DESIGN.md)
     hbm_peak, peak_kind = peaks()

@@ -68,6 +68,8 @@ typedef struct NosaConfig {
   int32_t dtype;      /* NOSA_DTYPE_*: K/V/q storage type                               */
   int32_t variant;    /* NOSA_VARIANT_*                                                 */
   int32_t residency;  /* NOSA_RESIDENCY_*                                               */
+  int32_t attend_chunk; /* KV blocks per split-K attention work item (1..8); 0 = auto from
+                           the batch size.  Outputs are bit-identical for a fixed value.    */
 } NosaConfig;
 
 /* residency contract */
@@ -255,11 +257,12 @@ int nosa_check_errors(NosaCtx* ctx, uint32_t* flags);
 
 /* Device timing of every kernel of subsequent eager steps, bracketed by CUDA events on the
  * stream each kernel runs on (bench evidence).  Kinds: 0 = select+plan (K1+K2), 1 = gather (K3),
- * 2 = attention (K4, split-K records), 3 = finalize (K4 log-sum-exp merge + K5 append).
+ * 2 = attention (K4, split-K records), 3 = finalize (K4 log-sum-exp merge + K5 append),
+ * 4 = host->device input copy and 5 = device->host output copy of nosa_decode_step_host.
  * enable(0) turns it off; read synchronises and returns the summed milliseconds and launch
  * counts per kind since enable. */
 int nosa_timing_enable(NosaCtx* ctx, int max_launches);
-int nosa_timing_read(NosaCtx* ctx, double* total_ms /* [4] */, int64_t* launches /* [4] */);
+int nosa_timing_read(NosaCtx* ctx, double* total_ms /* [6] */, int64_t* launches /* [6] */);
 
 /* The timed launches since enable, in issue order: kind and start/end milliseconds relative to
  * the first one (a device timeline of the step's streams).  Synchronises. */

@@ -36,7 +36,8 @@ RESIDENCY = {"per-sequence": 0, "shared": 1}
 class NosaConfig(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int32) for name in (
         "n", "d", "n_head", "n_kv_head", "d_head", "n_b", "n_s", "n_w", "k", "k_q", "k_e",
-        "accounting", "batch", "layers", "max_tokens", "fast_slots", "dtype", "variant", "residency")]
+        "accounting", "batch", "layers", "max_tokens", "fast_slots", "dtype", "variant", "residency",
+        "attend_chunk")]
 
 
 class NosaStats(ctypes.Structure):

@@ -47,31 +47,37 @@ __device__ __forceinline__ int find_bh(const int* cbase, int BH, int c) {
   return lo;
 }
 
-// block-level exclusive scan of ceil(n_req/kChunk) over the BH (b, h) entries into cbase
+// block-level exclusive scan of ceil(n_req/chunk) over the BH (b, h) entries into cbase:
+// per-thread sums of a contiguous range, a shuffle scan inside each warp, then the warp totals
+// (tmp[0..nwarps)) scanned by every thread.  Two barriers, no serial loop.
 __device__ void chunk_scan(const Dev& dv, int layer, int* cbase, int* tmp) {
   const int BH = dv.B * dv.H;
-  const int nt = blockDim.x;
+  const int nt = blockDim.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = nt >> 5;
   const int per = (BH + nt - 1) / nt;
   const int lo = min(BH, (int)threadIdx.x * per), hi = min(BH, lo + per);
+  const int* nreq = dv.n_req + layer * BH;
   int s = 0;
-  for (int i = lo; i < hi; ++i) s += (dv.n_req[layer * BH + i] + kChunk - 1) / kChunk;
-  tmp[threadIdx.x] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int i = 0; i < nt; ++i) {
-      const int v = tmp[i];
-      tmp[i] = acc;
-      acc += v;
-    }
-    cbase[BH] = acc;
+  for (int i = lo; i < hi; ++i) s += (nreq[i] + dv.chunk - 1) / dv.chunk;
+  int incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
   }
+  if (lane == 31) tmp[warp] = incl;
   __syncthreads();
-  int acc = tmp[threadIdx.x];
+  int base = 0, total = 0;
+  for (int w = 0; w < nwarps; ++w) {
+    const int v = tmp[w];
+    base += w < warp ? v : 0;
+    total += v;
+  }
+  int acc = base + incl - s;
   for (int i = lo; i < hi; ++i) {
     cbase[i] = acc;
-    acc += (dv.n_req[layer * BH + i] + kChunk - 1) / kChunk;
+    acc += (nreq[i] + dv.chunk - 1) / dv.chunk;
   }
+  if (threadIdx.x == 0) cbase[BH] = total;
   __syncthreads();
 }
 
@@ -90,71 +96,102 @@ __device__ __forceinline__ float block_beta(const Dev& dv, int lbh, int blk, int
 }
 
 // ---------------------------------------------------------------- finalize (merge + append)
-// One CTA (kFinThreads threads) per (b, h).  Every phase issues all of its loads before using
-// them: the kernel is latency-bound, so the number of dependent L2 round trips is the cost.
+// One CTA (kFinThreads threads) per (b, h).  The kernel is latency-bound, so it is organised
+// around dependent global round trips: every operand that does not depend on another load
+// (the new K/V row, the eviction-head operands, the tail sums, the cache length) is loaded up
+// front, the split-K records are merged with an online log-sum-exp in record order (batches of
+// 8 records in flight per thread), and only the slot lookup of the tail block waits on t.
 constexpr int kFinThreads = 256;
+constexpr int kFinMaxRows = 16;  // eviction-head rows per thread (D / (kFinThreads / n_ev))
 
 template <typename T>
 __device__ void finalize_bh(const Dev& dv, int layer, int bh, int nc, const T* __restrict__ kn,
                             const T* __restrict__ vn, float* __restrict__ out, float* wsm, double* zsm) {
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nthr = blockDim.x;
   const int b = bh / dv.H, h = bh % dv.H;
   const int lbh = (layer * dv.B + b) * dv.H + h;
-  const int D = dv.D, G = dv.G;
-  const size_t pbase = (size_t)bh * dv.max_chunks;
-  // (1) chunk records (m, l) -> shared, then per-query weights e^{m_c - M} / L
-  float2* mls = reinterpret_cast<float2*>(wsm);  // [nc][G], reused in place as weights
-  for (int x = tid; x < nc * G; x += blockDim.x) mls[x] = __ldcg(&part_ml_of(dv, layer)[pbase * G + x]);
-  __syncthreads();
-  if (tid < G) {
-    float M = -INFINITY;
-    for (int c = 0; c < nc; ++c) M = fmaxf(M, mls[c * G + tid].x);
-    float L = 0.0f;
-    for (int c = 0; c < nc; ++c) L = fmaf(mls[c * G + tid].y, expf(mls[c * G + tid].x - M), L);
-    const float inv = 1.0f / L;
-    for (int c = 0; c < nc; ++c) mls[c * G + tid].y = expf(mls[c * G + tid].x - M) * inv;
-  }
-  __syncthreads();
-  // (2) outputs, float4 per thread, chunks summed in chunk order (deterministic)
-  const int D4 = D / 4;
-  for (int x = tid; x < G * D4; x += blockDim.x) {
-    const int q = x / D4, d4 = x - q * D4;
-    const float4* po = reinterpret_cast<const float4*>(part_o_of(dv, layer) +(pbase * G + q) * D) + d4;
-    const size_t cstride = (size_t)G * D4;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
-    for (int c = 0; c < nc; ++c) {
-      const float w = mls[c * G + q].y;
-      const float4 v = __ldcg(po + c * cstride);
-      acc.x = fmaf(w, v.x, acc.x);
-      acc.y = fmaf(w, v.y, acc.y);
-      acc.z = fmaf(w, v.z, acc.z);
-      acc.w = fmaf(w, v.w, acc.w);
-    }
-    reinterpret_cast<float4*>(out + ((size_t)b * dv.Hq + h * G + q) * D)[d4] = acc;
-  }
-  // (3) append the new token (decode.py:187-189, HeadState.append decode.py:65-71)
-  const int nthr = blockDim.x;
-  const int t = dv.t[lbh];
-  const int n_b = dv.n_b;
-  const int blk = t / n_b, r = t - blk * n_b;
+  const int D = dv.D, G = dv.G, n_b = dv.n_b, n_ev = dv.n_ev, elem = dv.elem;
   const T* kr = kn + ((size_t)b * dv.H + h) * D;
   const T* vr = vn + ((size_t)b * dv.H + h) * D;
-  const int elem = dv.elem;
-  const int plane = n_b * D * elem;
-  const int sl = dv.slot_of[(size_t)lbh * dv.NB + blk];
-  const long long slot = sl < 0 ? -1 : (dv.shared ? shared_rel(dv, b, sl) : sl);  // relative to this row
-  char* hblk = dv.host + ((size_t)lbh * dv.NB + blk) * dv.bpb;
-  char* dblk = sl >= 0 ? dv.pool + ((long long)lbh * dv.C + slot) * dv.bpb : nullptr;
+
+  // ---- (0) independent loads: t, the new row's 16-byte chunks, eviction-head operands, tail sums
+  const int t = __ldcg(dv.t + lbh);
   const int cpr = D * elem / 16;  // 16-byte chunks per row
-  for (int c = tid; c < 2 * cpr; c += nthr) {
-    const int which = c / cpr;  // 0 = K, 1 = V
-    const int ch = c - which * cpr;
-    const int4 val = reinterpret_cast<const int4*>(which ? (const void*)vr : (const void*)kr)[ch];
+  int4 rowv = make_int4(0, 0, 0, 0);
+  if (tid < 2 * cpr) rowv = reinterpret_cast<const int4*>(tid < cpr ? (const void*)kr : (const void*)vr)[tid % cpr];
+  // importance score s = silu(v . W1) . W2 (attention.py:121-146): thread -> (column j, row group)
+  const int groups = nthr / n_ev, rpg = (D + groups - 1) / groups;
+  const bool ev_fast = groups > 0 && rpg <= kFinMaxRows;
+  const int j_ev = tid % max(n_ev, 1), grp = tid / max(n_ev, 1);
+  double part = 0.0;
+  if (ev_fast && grp < groups) {
+    double vv[kFinMaxRows], ww[kFinMaxRows];
+#pragma unroll
+    for (int u = 0; u < kFinMaxRows; ++u) {
+      const int i = grp * rpg + u;
+      const bool ok = u < rpg && i < D;
+      vv[u] = ok ? to_f64(vr[i]) : 0.0;
+      ww[u] = ok ? __ldg(dv.w1 + (size_t)i * n_ev + j_ev) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kFinMaxRows; ++u) part = fma(vv[u], ww[u], part);
+  }
+  double tks = 0.0, kv = 0.0;
+  if (tid < D) {
+    tks = __ldcg(dv.tail_ksum + (size_t)lbh * D + tid);
+    kv = to_f64(kr[tid]);
+  }
+  const double tse = __ldcg(dv.tail_se + lbh);
+
+  // ---- (1) merge the split-K records in record order (deterministic), thread -> (query, 4 dims)
+  {
+    const int D4 = D / 4;
+    const float2* ml = part_ml_of(dv, layer) + (size_t)bh * dv.max_rec * G;
+    const float4* po = reinterpret_cast<const float4*>(part_o_of(dv, layer) + (size_t)bh * dv.max_rec * G * D);
+    for (int x = tid; x < G * D4; x += nthr) {
+      const int q = x / D4, d4 = x - q * D4;
+      float M = -INFINITY, L = 0.0f;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c0 = 0; c0 < nc; c0 += 8) {
+        float2 m8[8];
+        float4 o8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + u;
+          m8[u] = c < nc ? __ldcg(ml + (size_t)c * G + q) : make_float2(-INFINITY, 0.f);
+          o8[u] = c < nc ? __ldcg(po + ((size_t)c * G + q) * D4 + d4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (m8[u].x == -INFINITY) continue;  // a record over no live key
+          const float Mn = fmaxf(M, m8[u].x);
+          const float a = expf(M - Mn), e = expf(m8[u].x - Mn);
+          L = fmaf(L, a, m8[u].y * e);
+          acc.x = fmaf(acc.x, a, o8[u].x * e);
+          acc.y = fmaf(acc.y, a, o8[u].y * e);
+          acc.z = fmaf(acc.z, a, o8[u].z * e);
+          acc.w = fmaf(acc.w, a, o8[u].w * e);
+          M = Mn;
+        }
+      }
+      const float inv = 1.0f / L;
+      reinterpret_cast<float4*>(out + ((size_t)b * dv.Hq + h * G + q) * D)[d4] =
+          make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    }
+  }
+
+  // ---- (2) append the new token (decode.py:187-189, HeadState.append decode.py:65-71)
+  const int blk = t / n_b, r = t - blk * n_b;
+  const int plane = n_b * D * elem;
+  char* hblk = dv.host + ((size_t)lbh * dv.NB + blk) * dv.bpb;
+  if (tid < 2 * cpr) {
+    const int sl = __ldcg(dv.slot_of + (size_t)lbh * dv.NB + blk);
+    const long long slot = sl < 0 ? -1 : (dv.shared ? shared_rel(dv, b, sl) : sl);  // relative to this row
+    const int which = tid / cpr, ch = tid - which * cpr;
     const int off = which * plane + r * D * elem + ((ch ^ (r & 7)) << 4);
-    *reinterpret_cast<int4*>(hblk + off) = val;
-    if (dblk) *reinterpret_cast<int4*>(dblk + off) = val;
-    if (r == 0) reinterpret_cast<int4*>(dv.newrow + (size_t)lbh * 2 * D * elem)[c] = val;  // see gather_kernel
+    *reinterpret_cast<int4*>(hblk + off) = rowv;
+    if (sl >= 0) *reinterpret_cast<int4*>(dv.pool + ((long long)lbh * dv.C + slot) * dv.bpb + off) = rowv;
+    if (r == 0) reinterpret_cast<int4*>(dv.newrow + (size_t)lbh * 2 * D * elem)[tid] = rowv;  // see gather_kernel
   }
   if (r == 0) {  // a new block: its not-yet-written rows must read as zero from the slow tier
     const int4 z = make_int4(0, 0, 0, 0);
@@ -165,35 +202,42 @@ __device__ void finalize_bh(const Dev& dv, int layer, int bh, int nc, const T* _
       *reinterpret_cast<int4*>(hblk + which * plane + (1 + rem / cpr) * D * elem + ((rem % cpr) << 4)) = z;
     }
   }
-  // importance score of the new token: the arithmetic of token_score_warp (prefill), with the
-  // eviction-head columns spread over the warps
-  {
-    const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
-    for (int j = warp; j < dv.n_ev; j += nwarps) {
-      double part = 0.0;
-      for (int i = lane; i < D; i += 32) part = fma(to_f64(vr[i]), dv.w1[i * dv.n_ev + j], part);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if (lane == 0) zsm[j] = silu64(part);
+  // running key sums of the tail block -> K_c of a completed block (compress_blocks)
+  if (tid < D) {
+    const double acc = (r == 0) ? kv : tks + kv;
+    if (r == n_b - 1) {
+      dv.kc[((size_t)lbh * dv.NB + blk) * D + tid] = acc / (double)n_b;
+      dv.tail_ksum[(size_t)lbh * D + tid] = 0.0;
+    } else {
+      dv.tail_ksum[(size_t)lbh * D + tid] = acc;
     }
   }
-  double* tks = dv.tail_ksum + (size_t)lbh * D;
-  for (int d = tid; d < D; d += nthr) {
-    const double kv = to_f64(kr[d]);
-    const double acc = (r == 0) ? kv : tks[d] + kv;
-    if (r == n_b - 1) {
-      dv.kc[((size_t)lbh * dv.NB + blk) * D + d] = acc / (double)n_b;
-      tks[d] = 0.0;
-    } else {
-      tks[d] = acc;
+  // eviction-head column sums: row-group partials -> silu per column
+  double* red = reinterpret_cast<double*>(wsm);  // [nthr] (the record weights are no longer needed)
+  if (ev_fast) {
+    red[tid] = part;
+    __syncthreads();
+    if (tid < n_ev) {
+      double zc = 0.0;
+      for (int g2 = 0; g2 < groups; ++g2) zc += red[g2 * n_ev + tid];
+      zsm[tid] = silu64(zc);
+    }
+  } else {  // wide heads: one warp per column
+    const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+    for (int j = warp; j < n_ev; j += nwarps) {
+      double p2 = 0.0;
+      for (int i = lane; i < D; i += 32) p2 = fma(to_f64(vr[i]), dv.w1[(size_t)i * n_ev + j], p2);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) p2 += __shfl_xor_sync(0xffffffffu, p2, o);
+      if (lane == 0) zsm[j] = silu64(p2);
     }
   }
   __syncthreads();
   if (tid == 0) {
     double z = 0.0;
-    for (int j = 0; j < dv.n_ev; ++j) z = fma(zsm[j], dv.w2[j], z);
-    const double s = dv.variant == 2 ? exp(z) : z;
-    const double acc = (r == 0) ? s : dv.tail_se[lbh] + s;
+    for (int j = 0; j < n_ev; ++j) z = fma(zsm[j], dv.w2[j], z);
+    const double sc = dv.variant == 2 ? exp(z) : z;
+    const double acc = (r == 0) ? sc : tse + sc;
     if (r == n_b - 1) {
       dv.se[(size_t)lbh * dv.NB + blk] = acc / (double)n_b;
       dv.tail_se[lbh] = 0.0;
@@ -292,9 +336,12 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
   if (warp == T::WARP_SCHED) {
     // ------------------------------------------------------------ scheduler warp
     for (int qs = 0;; ++qs) {
-      int c = 0;
-      if (lane == 0) c = atomicAdd(dv.cnt + 2 * layer + 1, 1);
-      c = __shfl_sync(0xffffffffu, c, 0);
+      // the first work item is static (item = CTA index), later ones are claimed dynamically
+      int c = blockIdx.x;
+      if (qs > 0) {
+        if (lane == 0) c = gridDim.x + atomicAdd(dv.cnt + 2 * layer + 1, 1);
+        c = __shfl_sync(0xffffffffu, c, 0);
+      }
       const int slot = qs % T::NQ;
       mbar_wait(&mq_empty[slot], ((qs / T::NQ) & 1) ^ 1);
       ChunkMeta& m = meta[slot];
@@ -310,8 +357,8 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
       const int ci = c - cbase[bh];
       const int nreq = dv.n_req[lbh];
       const int t = dv.t[lbh];
-      const int i0 = ci * kChunk;
-      const int n = min(kChunk, nreq - i0);
+      const int i0 = ci * dv.chunk;
+      const int n = min(dv.chunk, nreq - i0);
       if (lane < n) {
         const int blk = dv.req[(size_t)lbh * dv.C + i0 + lane];
         m.slot[lane] = dv.req_slot[(size_t)lbh * dv.C + i0 + lane];
@@ -322,7 +369,7 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
         m.bh = bh;
         m.ci = ci;
         m.n = n;
-        m.nc = (nreq + kChunk - 1) / kChunk;
+        m.nc = (nreq + dv.chunk - 1) / dv.chunk;
       }
       __threadfence_block();
       __syncwarp();
@@ -520,7 +567,7 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
             }
         named_sync(kBarConsumers, T::NCW * 32);
         const int bh = it.bh, ci = it.ci;
-        const size_t pb0 = (size_t)bh * dv.max_chunks + ci;
+        const size_t pb0 = (size_t)bh * dv.max_rec + ci;  // rpc = 1
         for (int x = tid; x < G * DH; x += T::NCW * 32) {
           const int qq = x / DH, d = x - qq * DH;
           float M = -INFINITY;
@@ -585,8 +632,8 @@ __global__ void __launch_bounds__(32)
       if (c >= total) { ld_done = true; return; }
       ld_bh = find_bh(cbase, BH, c);
       const int ci = c - cbase[ld_bh];
-      ld_i = ci * kChunk;
-      ld_end = min(ld_i + kChunk, dv.n_req[layer * BH + ld_bh]);
+      ld_i = ci * dv.chunk;
+      ld_end = min(ld_i + dv.chunk, dv.n_req[layer * BH + ld_bh]);
       if (lane == 0) ring[ld_chunk_n % RING] = c;
       ++ld_chunk_n;
     }
@@ -614,8 +661,8 @@ __global__ void __launch_bounds__(32)
       ++cp_chunk_n;
       cp_bh = find_bh(cbase, BH, c);
       cp_ci = c - cbase[cp_bh];
-      cp_i = cp_ci * kChunk;
-      cp_end = min(cp_i + kChunk, dv.n_req[layer * BH + cp_bh]);
+      cp_i = cp_ci * dv.chunk;
+      cp_end = min(cp_i + dv.chunk, dv.n_req[layer * BH + cp_bh]);
       cp_t = dv.t[layer * BH + cp_bh];
       const int b = cp_bh / dv.H, h = cp_bh % dv.H;
       __syncwarp();
@@ -700,7 +747,7 @@ __global__ void __launch_bounds__(32)
     ++cp_i;
     advance_loader();
     if (cp_i >= cp_end) {
-      const size_t pbase = (size_t)cp_bh * dv.max_chunks + cp_ci;
+      const size_t pbase = (size_t)cp_bh * dv.max_rec + cp_ci;  // rpc = 1
 #pragma unroll
       for (int gg = 0; gg < GM; ++gg) {
         if (gg >= G) break;
@@ -725,13 +772,13 @@ __global__ void __launch_bounds__(kFinThreads)
   double* zsm = reinterpret_cast<double*>(fin_smem);           // [n_ev]
   float* wsm = reinterpret_cast<float*>(zsm + dv.n_ev);         // [max_chunks * G] float2
   const int bh = blockIdx.x;
-  const int nc = (dv.n_req[layer * dv.B * dv.H + bh] + kChunk - 1) / kChunk;
+  const int nc = (dv.n_req[layer * dv.B * dv.H + bh] + dv.chunk - 1) / dv.chunk * dv.rpc;
   if (nc == 0) return;  // the plan failed for this manager (CapacityExceeded): no step
   finalize_bh<T>(dv, layer, bh, nc, kn, vn, out, wsm, zsm);
 }
 
 cudaError_t launch_finalize(const Dev& dv, int layer, const void* kn, const void* vn, float* out, cudaStream_t st) {
-  const size_t smem = (size_t)dv.n_ev * 8 + (size_t)dv.max_chunks * dv.G * 8;
+  const size_t smem = (size_t)dv.n_ev * 8 + std::max((size_t)dv.max_rec * dv.G * 8, (size_t)kFinThreads * 8);
   if (dv.dtype == 0) {
     auto k = finalize_kernel<__nv_bfloat16>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

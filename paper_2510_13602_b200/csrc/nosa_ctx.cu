@@ -23,6 +23,8 @@ cudaError_t launch_select_scores(int n_prob, const double* s_q, const double* s_
                                  const int* lo, const int* hi, int m_q, int m_e, int selector,
                                  int* out_q, int* n_q, int* out_e, int* n_e, cudaStream_t st);
 cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, bool tma);
+cudaError_t launch_stage_inputs(const void* const* src, void* const* dst, const size_t* bytes, int grid,
+                                cudaStream_t st);
 cudaError_t launch_prefill(const Dev& dv, int layer, int seq_begin, int S, const void* k,
                            const void* v, int t, char* staging, cudaStream_t st);
 cudaError_t launch_make_resident(const Dev& dv, int layer, int seq_begin, int S, int nblk, cudaStream_t st);
@@ -82,11 +84,14 @@ struct NosaCtx {
   long long batch_fallbacks = 0;
   // host-buffer step (nosa_decode_step_host): device staging of the step's inputs and outputs,
   // per-layer input-arrival / output-ready events, and the device->host stream
-  cudaStream_t d2h_stream = nullptr;
+  cudaStream_t d2h_stream = nullptr, in_stream = nullptr;
   std::vector<cudaEvent_t> ev_in;
+  std::vector<std::pair<int, int>> groups;  // selection groups (first layer, layers) of the step
   cudaEvent_t ev_d2h = nullptr;
   char* io_buf = nullptr;
   size_t io_bytes = 0;
+  int stage_grid = 32;              // CTAs of the input-staging kernel (host-buffer step)
+  bool stage_with_copies = false;   // NOSA_STAGE_COPIES: stage host inputs with cudaMemcpyAsync
   bool select_per_layer = false;  // NOSA_SELECT_PER_LAYER: one selection launch per layer
   long long select_launches = 0;  // grouped selection launches of the step being enqueued
 };
@@ -178,6 +183,7 @@ extern "C" int nosa_config_validate(const NosaConfig* c, char* msg, int msg_len)
   if (c->batch <= 0 || c->layers <= 0) return bad("batch and layers must be positive");
   if (c->max_tokens <= 0) return bad("max_tokens must be positive");
   if (c->fast_slots <= 0) return bad("fast_slots must be positive");
+  if (c->attend_chunk < 0 || c->attend_chunk > 8) return bad("attend_chunk must be in 0..8 (0 = auto)");
   if (c->dtype != NOSA_DTYPE_BF16 && c->dtype != NOSA_DTYPE_FP32) return bad("dtype must be bf16 or fp32");
   if (c->variant < 0 || c->variant > 2) return bad("variant must be ed-dma, s-dma or dma");
   if (c->residency != NOSA_RESIDENCY_PER_SEQUENCE && c->residency != NOSA_RESIDENCY_SHARED)
@@ -223,7 +229,7 @@ static void release(NosaCtx* ctx) {
   for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_d2h})
     if (e) cudaEventDestroy(e);
   for (cudaStream_t s : {ctx->copy_stream, ctx->capture_stream, ctx->att_stream, ctx->att_stream2, ctx->fin_stream,
-                         ctx->meta_stream, ctx->d2h_stream})
+                         ctx->meta_stream, ctx->d2h_stream, ctx->in_stream})
     if (s) cudaStreamDestroy(s);
   if (ctx->h_list) cudaFreeHost(ctx->h_list);
   if (ctx->h_cnt) cudaFreeHost(ctx->h_cnt);
@@ -290,7 +296,23 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   dv.shared = c.residency == NOSA_RESIDENCY_SHARED;
   dv.elem = c.dtype == NOSA_DTYPE_BF16 ? 2 : 4;
   dv.bpb = 2LL * c.n_b * c.d_head * dv.elem;
-  dv.max_chunks = (dv.C + nosa::kChunk - 1) / nosa::kChunk;
+  // split-K chunk: the largest of 8, 4, 2, 1 blocks that still gives every SM two work
+  // items per layer (measured: smaller chunks cost more in per-chunk overhead than they win in
+  // balance once there are a few waves) (B*H*|R| blocks, |R| ~ fixed + top-k), so a small batch does not leave
+  // SMs idle in the last wave; a caller that needs bit-identical outputs across batch sizes
+  // (e.g. strong scaling over GPUs) pins it with NosaConfig.attend_chunk
+  if (c.attend_chunk > 0) {
+    dv.chunk = std::min(c.attend_chunk, nosa::kChunk);
+  } else {
+    const long long r_est = (long long)dv.n_sink + c.n_w / c.n_b + 1 + dv.m_topk;
+    const long long blocks = (long long)dv.B * dv.H * std::min<long long>(r_est, dv.C);
+    dv.chunk = nosa::kChunk;
+    while (dv.chunk > 1 && blocks / dv.chunk < 2LL * ctx->num_sms) dv.chunk >>= 1;
+  }
+  if (const char* e = getenv("NOSA_CHUNK")) dv.chunk = std::max(1, std::min(atoi(e), nosa::kChunk));
+  dv.max_chunks = (dv.C + dv.chunk - 1) / dv.chunk;
+  dv.rpc = 1;  // the bf16 kernel combines its consumer warps' partials before writing a record
+  dv.max_rec = dv.max_chunks * dv.rpc;
   const size_t LBH = (size_t)dv.L * dv.B * dv.H;
   const size_t BH = (size_t)dv.B * dv.H;
 
@@ -331,8 +353,8 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   ALLOC(dv.plan_n, LBH * 3);
   ALLOC(dv.cnt, (size_t)dv.L * 2);
   ALLOC(dv.miss_list, (size_t)dv.L * BH * dv.C);
-  ALLOC(dv.part_o, 2 * BH * dv.max_chunks * dv.G * dv.D);
-  ALLOC(dv.part_ml, 2 * BH * dv.max_chunks * dv.G);
+  ALLOC(dv.part_o, 2 * BH * dv.max_rec * dv.G * dv.D);
+  ALLOC(dv.part_ml, 2 * BH * dv.max_rec * dv.G);
   ALLOC(dv.newrow, LBH * 2 * dv.D * (size_t)dv.elem);
   ALLOC(dv.w1, (size_t)dv.D * dv.n_ev);
   ALLOC(dv.w2, (size_t)dv.n_ev);
@@ -398,6 +420,8 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   cudaStreamCreateWithPriority(&ctx->att_stream2, cudaStreamNonBlocking, use_prio ? prio_high : 0);
   ctx->two_att = !getenv("NOSA_ONE_ATT_STREAM");
   ctx->select_per_layer = getenv("NOSA_SELECT_PER_LAYER") != nullptr;
+  ctx->stage_with_copies = getenv("NOSA_STAGE_COPIES") != nullptr;
+  if (const char* g = getenv("NOSA_STAGE_CTAS")) ctx->stage_grid = std::max(1, atoi(g));
   cudaStreamCreateWithPriority(&ctx->fin_stream, cudaStreamNonBlocking, use_prio ? prio_high : 0);
   cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
@@ -662,7 +686,7 @@ extern "C" int nosa_timing_read(NosaCtx* ctx, double* total_ms, int64_t* launche
   if (!ctx || !total_ms || !launches) return NOSA_ERR_VALUE;
   cudaSetDevice(ctx->device);
   CUDA_TRY(ctx, cudaDeviceSynchronize());
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < 6; ++k) {
     total_ms[k] = 0.0;
     launches[k] = 0;
   }
@@ -716,19 +740,15 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, st));  // side streams start after the caller's work
   cudaStream_t at2 = ctx->two_att ? ctx->att_stream2 : at;
   for (cudaStream_t s : {cp, at, at2, fn}) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_fork, 0));
-  if (hio) {
-    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_fork, 0));
-    for (int l = 0; l < dv.L; ++l) {
-      CUDA_TRY(ctx, cudaMemcpyAsync(const_cast<char*>(q) + l * qstride, static_cast<const char*>(hio->q) + l * qstride,
-                                    qstride, cudaMemcpyHostToDevice, cp));
-      CUDA_TRY(ctx, cudaMemcpyAsync(const_cast<char*>(kn) + l * kstride,
-                                    static_cast<const char*>(hio->k_new) + l * kstride, kstride,
-                                    cudaMemcpyHostToDevice, cp));
-      CUDA_TRY(ctx, cudaMemcpyAsync(const_cast<char*>(vn) + l * kstride,
-                                    static_cast<const char*>(hio->v_new) + l * kstride, kstride,
-                                    cudaMemcpyHostToDevice, cp));
-      CUDA_TRY(ctx, cudaEventRecord(ctx->ev_in[l], cp));
-    }
+  // selection groups: doubling layer ranges (1, 1, 2, 4, 8, ...) in the pipelined schedule,
+  // one layer each otherwise (serial schedule, shared-pool planner)
+  const bool grouped = !serial && !dv.shared && !ctx->select_per_layer;
+  std::vector<std::pair<int, int>>& groups = ctx->groups;
+  groups.clear();
+  if (grouped) {
+    for (int l0 = 0, n = 1; l0 < dv.L; l0 += n, n = (l0 <= 1 ? 1 : l0)) groups.push_back({l0, std::min(n, dv.L - l0)});
+  } else {
+    for (int l = 0; l < dv.L; ++l) groups.push_back({l, 1});
   }
   auto select = [&](int l) -> int {
     if (hio) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_in[l], 0));
@@ -751,20 +771,79 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
       CUDA_TRY(ctx, nosa::launch_select_plan(dv, l0, q + l0 * qstride, io->selector, 1, nullptr, nullptr, st, n));
     }
     for (int l = l0; l < l0 + n; ++l) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[l], st));
+    if (count) ctx->select_launches += 1;
     return NOSA_OK;
   };
-  if (!serial) {
-    if (dv.shared || ctx->select_per_layer) {
-      for (int l = 0; l < dv.L; ++l)
-        if (int rc = select(l)) return rc;
-    } else {
-      for (int l0 = 0, n = 1; l0 < dv.L; l0 += n, n = (l0 <= 1 ? 1 : l0)) {
-        n = std::min(n, dv.L - l0);
-        if (int rc = select_group(l0, n)) return rc;
-        if (count) ctx->select_launches += 1;
+  // Issues groups [next_group, upto): the host inputs of the group (three copies, nosa_decode_
+  // step_host), then in the pipelined schedule its selection, so a selection is always enqueued
+  // after its inputs' event is recorded in this step (a wait on an earlier step's record would
+  // read stale inputs).  Inputs go on their own high-priority stream.  Pinned inputs are staged
+  // by a small SM kernel: copy-engine copies would run strictly in order with the miss gathers
+  // (measured: the gather of layer 0 then waits for every input copy; interleaving the inputs
+  // between the gathers leaves bubbles and ends 7% slower end to end).
+  // device-visible aliases of the host inputs when they are pinned (cudaHostAlloc / registered);
+  // pageable inputs fall back to cudaMemcpyAsync
+  const char* hsrc[3] = {nullptr, nullptr, nullptr};
+  if (hio && !ctx->stage_with_copies) {
+    const void* hp[3] = {hio->q, hio->k_new, hio->v_new};
+    bool all = true;
+    for (int i = 0; i < 3; ++i) {
+      cudaPointerAttributes pa{};
+      if (cudaPointerGetAttributes(&pa, hp[i]) != cudaSuccess || pa.type != cudaMemoryTypeHost || !pa.devicePointer) {
+        cudaGetLastError();
+        all = false;
+        break;
+      }
+      hsrc[i] = static_cast<const char*>(pa.devicePointer);
+    }
+    if (!all) hsrc[0] = hsrc[1] = hsrc[2] = nullptr;
+  }
+  size_t next_group = 0;
+  auto issue_groups = [&](size_t upto) -> int {
+    for (; next_group < std::min(upto, groups.size()); ++next_group) {
+      const int l0 = groups[next_group].first, n = groups[next_group].second;
+      if (hio && hsrc[0]) {  // mapped pinned inputs: the SMs stage them (zero-copy loads)
+        cudaStream_t in = ctx->in_stream;
+        TimeScope ts(ctx, in, 4, timed);
+        const void* src[3] = {hsrc[0] + l0 * qstride, hsrc[1] + l0 * kstride, hsrc[2] + l0 * kstride};
+        void* dst[3] = {const_cast<char*>(q) + l0 * qstride, const_cast<char*>(kn) + l0 * kstride,
+                        const_cast<char*>(vn) + l0 * kstride};
+        const size_t bytes[3] = {n * qstride, n * kstride, n * kstride};
+        CUDA_TRY(ctx, nosa::launch_stage_inputs(src, dst, bytes, ctx->stage_grid, in));
+        if (count) ctx->launches += 1;
+        CUDA_TRY(ctx, cudaEventRecord(ctx->ev_in[l0 + n - 1], in));
+      } else if (hio) {
+        cudaStream_t in = ctx->in_stream;
+        TimeScope ts(ctx, in, 4, timed);
+        CUDA_TRY(ctx, cudaMemcpyAsync(const_cast<char*>(q) + l0 * qstride,
+                                      static_cast<const char*>(hio->q) + l0 * qstride, n * qstride,
+                                      cudaMemcpyHostToDevice, in));
+        CUDA_TRY(ctx, cudaMemcpyAsync(const_cast<char*>(kn) + l0 * kstride,
+                                      static_cast<const char*>(hio->k_new) + l0 * kstride, n * kstride,
+                                      cudaMemcpyHostToDevice, in));
+        CUDA_TRY(ctx, cudaMemcpyAsync(const_cast<char*>(vn) + l0 * kstride,
+                                      static_cast<const char*>(hio->v_new) + l0 * kstride, n * kstride,
+                                      cudaMemcpyHostToDevice, in));
+        CUDA_TRY(ctx, cudaEventRecord(ctx->ev_in[l0 + n - 1], in));
+      }
+      if (!serial) {
+        if (grouped) {
+          if (int rc = select_group(l0, n)) return rc;
+        } else {
+          for (int l = l0; l < l0 + n; ++l)
+            if (int rc = select(l)) return rc;
+        }
       }
     }
+    return NOSA_OK;
+  };
+  if (hio) {
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->in_stream, ctx->ev_fork, 0));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_fork, 0));
   }
+  // with the copy-engine mover, only the first two groups' inputs go ahead of the first miss
+  // transfer; the rest follow it (the host submits that transfer once layer 0 is planned)
+  if (int rc = issue_groups(groups.size())) return rc;
   for (int l = 0; l < dv.L; ++l) {
     if (serial) {
       if (l > 0) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_fin[l - 1], 0));
@@ -798,6 +877,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fin[l], fn));
     if (hio) {
       CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_fin[l], 0));
+      TimeScope ts(ctx, ctx->d2h_stream, 5, timed);
       CUDA_TRY(ctx, cudaMemcpyAsync(hio->out + l * ostride, io->out + l * ostride, ostride * sizeof(float),
                                     cudaMemcpyDeviceToHost, ctx->d2h_stream));
     }
@@ -838,6 +918,9 @@ extern "C" int nosa_decode_step_host(NosaCtx* ctx, const NosaHostStepIO* hio, vo
     CUDA_TRY(ctx, cudaMalloc(reinterpret_cast<void**>(&ctx->io_buf), need));
     ctx->io_bytes = need;
     CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+    int prio_low = 0, prio_high = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
+    CUDA_TRY(ctx, cudaStreamCreateWithPriority(&ctx->in_stream, cudaStreamNonBlocking, prio_high));
     CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_d2h, cudaEventDisableTiming));
     ctx->ev_in.resize(dv.L);
     for (int l = 0; l < dv.L; ++l) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_in[l], cudaEventDisableTiming));

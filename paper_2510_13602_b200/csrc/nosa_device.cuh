@@ -19,7 +19,7 @@
 
 namespace nosa {
 
-constexpr int kChunk = 8;  // KV blocks per attention work item (split-K granularity)
+constexpr int kChunk = 8;  // max KV blocks per attention work item (split-K granularity)
 
 struct Dev {
   // ---- shapes --------------------------------------------------------------------------
@@ -31,7 +31,10 @@ struct Dev {
                                  //    (the reference simulator, offload_sim.py:254-256); slot_of then
                                  //    holds the shared slot id s, stored at (lbh of batch s/C, slot s%C)
   long long bpb;                 // bytes per block
-  int max_chunks;                // ceil(C / kChunk)
+  int chunk;                     // KV blocks per attention work item, 1..kChunk
+  int max_chunks;                // ceil(C / chunk)
+  int rpc;                       // split-K records per chunk: one per consumer warp (bf16), 1 (fp32)
+  int max_rec;                   // max_chunks * rpc records per (b, h)
   // ---- persistent state ----------------------------------------------------------------
   char* pool;
   char* host;                    // device-visible alias of the pinned host mirror
@@ -84,10 +87,10 @@ __host__ __device__ __forceinline__ int shared_rel(const Dev& dv, int b, int s) 
 
 // the split-K record buffer of a layer (double-buffered by layer parity)
 __host__ __device__ __forceinline__ float* part_o_of(const Dev& dv, int layer) {
-  return dv.part_o + (size_t)(layer & 1) * dv.B * dv.H * dv.max_chunks * dv.G * dv.D;
+  return dv.part_o + (size_t)(layer & 1) * dv.B * dv.H * dv.max_rec * dv.G * dv.D;
 }
 __host__ __device__ __forceinline__ float2* part_ml_of(const Dev& dv, int layer) {
-  return dv.part_ml + (size_t)(layer & 1) * dv.B * dv.H * dv.max_chunks * dv.G;
+  return dv.part_ml + (size_t)(layer & 1) * dv.B * dv.H * dv.max_rec * dv.G;
 }
 
 // ---------------------------------------------------------------- small helpers

@@ -162,6 +162,46 @@ cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, b
 }
 
 // ------------------------------------------------------------------------------------------
+// Input staging of nosa_decode_step_host: up to three host segments (q, k_new, v_new of a
+// selection group) copied into device memory by the SMs with zero-copy 16-byte loads from the
+// mapped pinned buffers.  The copy engine is busy with the miss gathers and runs its queue in
+// order; SM loads share the PCIe link with it instead of queueing behind it.
+struct StageSeg {
+  const int4* src;
+  int4* dst;
+  long long n16;
+};
+__global__ void __launch_bounds__(256) stage_inputs_kernel(StageSeg a, StageSeg b, StageSeg c) {
+  constexpr int PER = 4;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (const StageSeg& sg : {a, b, c}) {
+    for (long long i0 = tid; i0 < sg.n16; i0 += stride * PER) {
+      int4 v[PER];
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const long long i = i0 + u * stride;
+        if (i < sg.n16) v[u] = __ldcs(sg.src + i);
+      }
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const long long i = i0 + u * stride;
+        if (i < sg.n16) sg.dst[i] = v[u];
+      }
+    }
+  }
+}
+
+cudaError_t launch_stage_inputs(const void* const* src, void* const* dst, const size_t* bytes, int grid,
+                                cudaStream_t st) {
+  StageSeg sg[3];
+  for (int i = 0; i < 3; ++i)
+    sg[i] = {static_cast<const int4*>(src[i]), static_cast<int4*>(dst[i]), (long long)(bytes[i] / 16)};
+  stage_inputs_kernel<<<grid, 256, 0, st>>>(sg[0], sg[1], sg[2]);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
 // Prefill, step 1: K/V rows [S][H][t][D] -> swizzled block format [S*H][NB][2][n_b][D] in a
 // device staging buffer (zero padded past t), later copied to the host mirror in one DMA.
 template <typename T>

@@ -82,10 +82,12 @@ class StepOutput:
 class NosaEngine:
     def __init__(self, config: AttentionConfig, *, batch: int, max_tokens: int, fast_slots: int,
                  w1, w2, layers: int = 1, variant: str = "ed-dma", dtype: str = "bf16",
-                 device: int = 0, residency: str = "per-sequence"):
+                 device: int = 0, residency: str = "per-sequence", attend_chunk: int = 0):
         """residency "per-sequence": one manager per (layer, sequence, head) with `fast_slots`
         slots; "shared": one pool of batch*fast_slots slots per (layer, head)
-        shared by the batch and planned in batch order, the reference simulator's residency."""
+        shared by the batch and planned in batch order, the reference simulator's residency.
+        attend_chunk: KV blocks per split-K attention work item (1..8, 0 = chosen from the
+        batch size); outputs are bit-identical across runs with the same value."""
         if variant not in _lib.VARIANT:
             raise ValueError(f"variant must be one of {tuple(_lib.VARIANT)} (retaining needs hidden states)")
         if residency not in _lib.RESIDENCY:
@@ -105,6 +107,7 @@ class NosaEngine:
         c.batch, c.layers, c.max_tokens, c.fast_slots = batch, layers, max_tokens, fast_slots
         c.dtype, c.variant = _lib.DTYPE[dtype], _lib.VARIANT[variant]
         c.residency = _lib.RESIDENCY[residency]
+        c.attend_chunk = attend_chunk
         self._cfg = c
         msg = ctypes.create_string_buffer(512)
         if _lib.lib.nosa_config_validate(ctypes.byref(c), msg, 512) != _lib.NOSA_OK:
@@ -413,17 +416,25 @@ class NosaEngine:
 
     # ------------------------------------------------------------------ device timing
     KERNEL_KINDS = ("select_plan", "gather", "attend", "finalize")
+    COPY_KINDS = ("h2d_in", "d2h_out")  # host-buffer step copies (timing kinds 4, 5)
 
     def timing_enable(self, max_launches: int):
         """Bracket every kernel of the following eager steps with CUDA events on its stream."""
         self._call(_lib.lib.nosa_timing_enable, max_launches)
 
     def timing_read(self) -> dict:
-        ms = (ctypes.c_double * 4)()
-        n = (ctypes.c_int64 * 4)()
+        ms = (ctypes.c_double * 6)()
+        n = (ctypes.c_int64 * 6)()
         self._call(_lib.lib.nosa_timing_read, ms, n)
         return {k: {"total_ms": ms[i], "launches": n[i], "avg_ms": ms[i] / n[i] if n[i] else 0.0}
                 for i, k in enumerate(self.KERNEL_KINDS)}
+
+    def copy_timing_read(self) -> dict:
+        """Host<->device copy time of nosa_decode_step_host (kinds 4, 5) since timing_enable."""
+        ms = (ctypes.c_double * 6)()
+        n = (ctypes.c_int64 * 6)()
+        self._call(_lib.lib.nosa_timing_read, ms, n)
+        return {k: {"total_ms": ms[4 + i], "copies": n[4 + i]} for i, k in enumerate(self.COPY_KINDS)}
 
     def timing_trace(self, cap: int = 65536) -> list[tuple[str, float, float]]:
         """(kind, start_ms, end_ms) of every timed launch since timing_enable, in issue order,
@@ -434,4 +445,5 @@ class NosaEngine:
         F = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
         self._call(_lib.lib.nosa_timing_trace, cap, kind.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), F(t0), F(t1),
                    ctypes.byref(n))
-        return [(self.KERNEL_KINDS[kind[i]], float(t0[i]), float(t1[i])) for i in range(n.value)]
+        names = self.KERNEL_KINDS + self.COPY_KINDS
+        return [(names[kind[i]], float(t0[i]), float(t1[i])) for i in range(n.value)]

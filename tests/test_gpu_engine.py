@@ -73,7 +73,7 @@ def test_engine_vs_reference_golden(golden, name, dtype):
 
 def _run_pair(cfg, *, batch, t0s, steps, fast_slots, seed, rho, selector="nosa", dtype="bf16", layers=1,
               variant="ed-dma", check_residency=True, gather="uva", schedule="pipelined", resident=False,
-              shared=False):
+              shared=False, attend_chunk=0):
     """GPU engine and oracle on identical inputs; returns the worst relative output error."""
     w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, seed)
     if variant == "dma":
@@ -81,7 +81,8 @@ def _run_pair(cfg, *, batch, t0s, steps, fast_slots, seed, rho, selector="nosa",
     tmax = max(t0s)
     cap = tmax + steps + 1
     eng = NosaEngine(cfg, batch=batch, layers=layers, max_tokens=cap, fast_slots=fast_slots, w1=w1, w2=w2,
-                     dtype=dtype, variant=variant, residency="shared" if shared else "per-sequence")
+                     dtype=dtype, variant=variant, residency="shared" if shared else "per-sequence",
+                     attend_chunk=attend_chunk)
     orc = oracle_for(cfg, batch, layers, cap, fast_slots, w1, w2, variant, shared=shared)
     K, V = workload.prefix_kv(seed, batch * layers, cfg.n_kv_head, tmax, cfg.d_head)
     K = K.reshape(layers, batch, cfg.n_kv_head, tmax, cfg.d_head)
@@ -197,6 +198,15 @@ def test_block_sizes(n_b):
     cfg = AttentionConfig(n=8192, d=1024, n_head=4, n_kv_head=2, d_head=128, n_b=n_b, n_s=n_b, n_w=4 * n_b,
                           k=16 * n_b, k_q=4 * n_b, k_e=12 * n_b)
     _run_pair(cfg, batch=2, t0s=[40 * n_b + 3, 30 * n_b], steps=5, fast_slots=20, seed=10, rho=0.5)
+
+
+@pytest.mark.parametrize("chunk", [1, 2, 4, 8])
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_split_k_chunk_sizes(chunk, dtype):
+    """Every split-K granularity (blocks per attention work item) against the oracle."""
+    a = _run_pair(ONE_B_SMALL, batch=3, t0s=[3000, 2500, 1700], steps=6, fast_slots=70, seed=21, rho=0.5,
+                  dtype=dtype, layers=2, attend_chunk=chunk)
+    assert a <= TOL[dtype]
 
 
 @pytest.mark.parametrize("selector", ["nosa", "infllmv2"])

@@ -41,7 +41,7 @@ def main():
     for l in range(a.layers):
         shape = (a.batch, cfg.n_kv_head, a.context, cfg.d_head)
         eng.prefill(workload.torch_prefix_kv(2 * l, shape, dev, torch.bfloat16),
-                    workload.torch_prefix_kv(2 * l + 1, shape, dev, torch.bfloat16), layer=l)
+                    workload.torch_prefix_kv(2 * l + 1, shape, dev, torch.bfloat16), layer=l, resident=a.cache >= 1)
     eng.start_run()
     torch.cuda.synchronize()
     print(f"setup {time.time() - t0:.1f}s", flush=True)
