@@ -70,6 +70,8 @@ typedef struct NosaConfig {
   int32_t residency;  /* NOSA_RESIDENCY_*                                               */
   int32_t attend_chunk; /* KV blocks per split-K attention work item (1..8); 0 = auto from
                            the batch size.  Outputs are bit-identical for a fixed value.    */
+  int32_t attend_layers; /* layers per persistent attention launch in the pipelined schedule;
+                            0 = auto (4 when every block fits in HBM, else 1)               */
 } NosaConfig;
 
 /* residency contract */

@@ -50,12 +50,12 @@ __device__ __forceinline__ int find_bh(const int* cbase, int BH, int c) {
 // block-level exclusive scan of ceil(n_req/chunk) over the BH (b, h) entries into cbase:
 // per-thread sums of a contiguous range, a shuffle scan inside each warp, then the warp totals
 // (tmp[0..nwarps)) scanned by every thread.  Two barriers, no serial loop.
-__device__ void chunk_scan(const Dev& dv, int layer, int* cbase, int* tmp) {
-  const int BH = dv.B * dv.H;
+__device__ void chunk_scan(const Dev& dv, int layer, int* cbase, int* tmp, int units = -1) {
+  const int BH = units < 0 ? dv.B * dv.H : units;  // units of layers [layer, ...) are contiguous
   const int nt = blockDim.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = nt >> 5;
   const int per = (BH + nt - 1) / nt;
   const int lo = min(BH, (int)threadIdx.x * per), hi = min(BH, lo + per);
-  const int* nreq = dv.n_req + layer * BH;
+  const int* nreq = dv.n_req + layer * dv.B * dv.H;
   int s = 0;
   for (int i = lo; i < hi; ++i) s += (nreq[i] + dv.chunk - 1) / dv.chunk;
   int incl = s;
@@ -293,12 +293,13 @@ __host__ __device__ constexpr size_t bf_smem_fixed() {
 
 template <int NBK, int DH, int NQT>
 __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
-    attend_bf16_kernel(Dev dv, int layer, const __nv_bfloat16* __restrict__ q,
-                       const __nv_bfloat16* __restrict__ kn, const __nv_bfloat16* __restrict__ vn,
-                       float* __restrict__ out) {
+    attend_bf16_kernel(Dev dv, int layer, int nl, const __nv_bfloat16* __restrict__ q, size_t q_layer_stride) {
+  // layers [layer, layer + nl) in one persistent launch: work unit u = (layer - layer0) * B*H + bh,
+  // so lbh = layer0 * B*H + u and the units of all layers form one contiguous list
   using T = BF<NBK, DH, NQT>;
   extern __shared__ __align__(128) char smem_raw[];
-  const int BH = dv.B * dv.H;
+  const int BHL = dv.B * dv.H;
+  const int BH = nl * BHL;
   const int G = dv.G;
   char* p = smem_raw;
   char* stages = p;                                   p += (size_t)T::NS * T::BPB;
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
   }
   if (G < T::QMAX)  // query rows past the group stay zero (only G rows are ever copied in)
     for (int x = tid; x < T::NS * T::QSLOT / 16; x += blockDim.x) reinterpret_cast<int4*>(qslots)[x] = make_int4(0, 0, 0, 0);
-  chunk_scan(dv, layer, cbase, tmp);  // also publishes the barrier inits (__syncthreads)
+  chunk_scan(dv, layer, cbase, tmp, BH);  // also publishes the barrier inits (__syncthreads)
   const int total = cbase[BH];
 
   if (warp == T::WARP_SCHED) {
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
         break;
       }
       const int bh = find_bh(cbase, BH, c);
-      const int lbh = layer * BH + bh;
+      const int lbh = layer * BHL + bh;
       const int ci = c - cbase[bh];
       const int nreq = dv.n_req[lbh];
       const int t = dv.t[lbh];
@@ -385,8 +386,9 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
       const int n = m.n;
       if (n < 0) break;
       const int bh = m.bh, ci = m.ci, nc = m.nc;
-      const int lbh = layer * BH + bh;
-      const int b = bh / dv.H, h = bh - b * dv.H;
+      const int lbh = layer * BHL + bh;
+      const int bhl = bh % BHL, b = bhl / dv.H, h = bhl - b * dv.H;
+      const __nv_bfloat16* ql = q + (size_t)(bh / BHL) * q_layer_stride;
       for (int i = 0; i < n; ++i, ++seq) {
         const int s = seq % T::NS;
         mbar_wait(&empty[s], ((seq / T::NS) & 1) ^ 1);
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
           bulk_g2s(stages + (size_t)s * T::BPB, dv.pool + ((size_t)lbh * dv.C + m.slot[i]) * (size_t)T::BPB, T::BPB,
                    &full[s]);
           if (qbytes)
-            bulk_g2s(qslots + (size_t)s * T::QSLOT, q + ((size_t)b * dv.Hq + h * G) * DH, qbytes, &full[s]);
+            bulk_g2s(qslots + (size_t)s * T::QSLOT, ql + ((size_t)b * dv.Hq + h * G) * DH, qbytes, &full[s]);
         }
       }
       __syncwarp();
@@ -566,8 +568,8 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
               row[16 * md + g + 8] = o[md][nq][2 + e];
             }
         named_sync(kBarConsumers, T::NCW * 32);
-        const int bh = it.bh, ci = it.ci;
-        const size_t pb0 = (size_t)bh * dv.max_rec + ci;  // rpc = 1
+        const int ci = it.ci, rl = layer + it.bh / BHL;  // the record's layer and (b, h)
+        const size_t pb0 = (size_t)(it.bh % BHL) * dv.max_rec + ci;  // rpc = 1
         for (int x = tid; x < G * DH; x += T::NCW * 32) {
           const int qq = x / DH, d = x - qq * DH;
           float M = -INFINITY;
@@ -581,8 +583,8 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
             acc = fmaf(f, comb_o[((size_t)ww * T::QMAX + qq) * DH + d], acc);
             L = fmaf(f, ml.y, L);
           }
-          part_o_of(dv, layer)[(pb0 * G + qq) * DH + d] = acc;
-          if (d == 0) part_ml_of(dv, layer)[pb0 * G + qq] = make_float2(M, L);
+          part_o_of(dv, rl)[(pb0 * G + qq) * DH + d] = acc;
+          if (d == 0) part_ml_of(dv, rl)[pb0 * G + qq] = make_float2(M, L);
         }
         named_sync(kBarConsumers, T::NCW * 32);  // comb_* may be overwritten at the next chunk end
       }
@@ -767,45 +769,47 @@ __global__ void __launch_bounds__(32)
 // thread can still be reading the tail block.
 template <typename T>
 __global__ void __launch_bounds__(kFinThreads)
-    finalize_kernel(Dev dv, int layer, const T* __restrict__ kn, const T* __restrict__ vn, float* __restrict__ out) {
+    finalize_kernel(Dev dv, int layer0, const T* __restrict__ kn0, const T* __restrict__ vn0, float* __restrict__ out0) {
+  // grid (B*H, layers): layer = layer0 + blockIdx.y, its k/v rows and outputs one layer stride on
   extern __shared__ __align__(16) char fin_smem[];
   double* zsm = reinterpret_cast<double*>(fin_smem);           // [n_ev]
   float* wsm = reinterpret_cast<float*>(zsm + dv.n_ev);         // [max_chunks * G] float2
-  const int bh = blockIdx.x;
+  const int bh = blockIdx.x, layer = layer0 + blockIdx.y;
+  const size_t kst = (size_t)dv.B * dv.H * dv.D, ost = (size_t)dv.B * dv.Hq * dv.D;
   const int nc = (dv.n_req[layer * dv.B * dv.H + bh] + dv.chunk - 1) / dv.chunk * dv.rpc;
   if (nc == 0) return;  // the plan failed for this manager (CapacityExceeded): no step
-  finalize_bh<T>(dv, layer, bh, nc, kn, vn, out, wsm, zsm);
+  finalize_bh<T>(dv, layer, bh, nc, kn0 + blockIdx.y * kst, vn0 + blockIdx.y * kst, out0 + blockIdx.y * ost, wsm, zsm);
 }
 
-cudaError_t launch_finalize(const Dev& dv, int layer, const void* kn, const void* vn, float* out, cudaStream_t st) {
+// layers [layer, layer + nl): kn/vn/out point at layer `layer`'s rows
+cudaError_t launch_finalize(const Dev& dv, int layer, const void* kn, const void* vn, float* out, cudaStream_t st,
+                            int nl) {
   const size_t smem = (size_t)dv.n_ev * 8 + std::max((size_t)dv.max_rec * dv.G * 8, (size_t)kFinThreads * 8);
+  const dim3 grid(dv.B * dv.H, nl);
   if (dv.dtype == 0) {
     auto k = finalize_kernel<__nv_bfloat16>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<dv.B * dv.H, kFinThreads, smem, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(kn),
-                                               static_cast<const __nv_bfloat16*>(vn), out);
+    k<<<grid, kFinThreads, smem, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(kn),
+                                        static_cast<const __nv_bfloat16*>(vn), out);
   } else {
     auto k = finalize_kernel<float>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<dv.B * dv.H, kFinThreads, smem, st>>>(dv, layer, static_cast<const float*>(kn),
-                                               static_cast<const float*>(vn), out);
+    k<<<grid, kFinThreads, smem, st>>>(dv, layer, static_cast<const float*>(kn), static_cast<const float*>(vn), out);
   }
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- launchers
 template <int NBK, int DH, int NQT>
-static cudaError_t launch_bf16(const Dev& dv, int layer, const void* q, const void* kn, const void* vn,
-                               float* out, cudaStream_t st, int num_sms) {
+static cudaError_t launch_bf16(const Dev& dv, int layer, int nl, const void* q, cudaStream_t st, int num_sms) {
   using T = BF<NBK, DH, NQT>;
-  const int BH = dv.B * dv.H;
+  const int BH = nl * dv.B * dv.H;
   const size_t smem = bf_smem_fixed<NBK, DH, NQT>() + (size_t)(BH + 1) * 4 + (size_t)dv.max_chunks * dv.G * 4 + 64;
   auto k = attend_bf16_kernel<NBK, DH, NQT>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k<<<num_sms, T::THREADS, smem, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(q),
-                                       static_cast<const __nv_bfloat16*>(kn),
-                                       static_cast<const __nv_bfloat16*>(vn), out);
+  k<<<num_sms, T::THREADS, smem, st>>>(dv, layer, nl, static_cast<const __nv_bfloat16*>(q),
+                                       (size_t)dv.B * dv.Hq * DH);
   return cudaGetLastError();
 }
 
@@ -833,17 +837,18 @@ bool attend_supported(int n_b, int d_head, int dtype) {
 }
 
 template <int NBK, int DH>
-static cudaError_t dispatch_bf16(const Dev& dv, int layer, const void* q, const void* kn, const void* vn, float* out,
-                                 cudaStream_t st, int num_sms) {
-  return dv.G <= 8 ? launch_bf16<NBK, DH, 1>(dv, layer, q, kn, vn, out, st, num_sms)
-                   : launch_bf16<NBK, DH, 2>(dv, layer, q, kn, vn, out, st, num_sms);
+static cudaError_t dispatch_bf16(const Dev& dv, int layer, int nl, const void* q, cudaStream_t st, int num_sms) {
+  return dv.G <= 8 ? launch_bf16<NBK, DH, 1>(dv, layer, nl, q, st, num_sms)
+                   : launch_bf16<NBK, DH, 2>(dv, layer, nl, q, st, num_sms);
 }
 
-cudaError_t launch_attend(const Dev& dv, int layer, const void* q, const void* kn, const void* vn, float* out,
+// layers [layer, layer + nl) in one launch (bf16); the fp32 parity kernel runs one layer at a time
+cudaError_t launch_attend(const Dev& dv, int layer, int nl, const void* q, const void* kn, const void* vn, float* out,
                           cudaStream_t st, int num_sms) {
+  if (dv.dtype != 0 && nl != 1) return cudaErrorInvalidValue;
 #define NOSA_DISPATCH(NBK, DH)                                                                  \
   if (dv.n_b == NBK && dv.D == DH) {                                                            \
-    return dv.dtype == 0 ? dispatch_bf16<NBK, DH>(dv, layer, q, kn, vn, out, st, num_sms)       \
+    return dv.dtype == 0 ? dispatch_bf16<NBK, DH>(dv, layer, nl, q, st, num_sms)                \
                          : launch_f32<NBK, DH>(dv, layer, q, kn, vn, out, st, 2 * num_sms);     \
   }
   NOSA_DISPATCH(64, 128)
@@ -853,7 +858,7 @@ cudaError_t launch_attend(const Dev& dv, int layer, const void* q, const void* k
   NOSA_DISPATCH(16, 128)
   NOSA_DISPATCH(16, 64)
   NOSA_DISPATCH(128, 64)
-  if (dv.n_b == 128 && dv.D == 128 && dv.dtype == 0) return dispatch_bf16<128, 128>(dv, layer, q, kn, vn, out, st, num_sms);
+  if (dv.n_b == 128 && dv.D == 128 && dv.dtype == 0) return dispatch_bf16<128, 128>(dv, layer, nl, q, st, num_sms);
 #undef NOSA_DISPATCH
   return cudaErrorInvalidValue;
 }

@@ -30,9 +30,10 @@ cudaError_t launch_prefill(const Dev& dv, int layer, int seq_begin, int S, const
 cudaError_t launch_make_resident(const Dev& dv, int layer, int seq_begin, int S, int nblk, cudaStream_t st);
 cudaError_t launch_unswizzle(const char* src, char* dst, int nblocks, int n_b, int D, int elem,
                              cudaStream_t st);
-cudaError_t launch_attend(const Dev& dv, int layer, const void* q, const void* kn, const void* vn,
+cudaError_t launch_attend(const Dev& dv, int layer, int nl, const void* q, const void* kn, const void* vn,
                           float* out, cudaStream_t st, int num_sms);
-cudaError_t launch_finalize(const Dev& dv, int layer, const void* kn, const void* vn, float* out, cudaStream_t st);
+cudaError_t launch_finalize(const Dev& dv, int layer, const void* kn, const void* vn, float* out, cudaStream_t st,
+                            int nl = 1);
 bool attend_supported(int n_b, int d_head, int dtype);
 }  // namespace nosa
 
@@ -92,8 +93,9 @@ struct NosaCtx {
   size_t io_bytes = 0;
   int stage_grid = 32;              // CTAs of the input-staging kernel (host-buffer step)
   bool stage_with_copies = false;   // NOSA_STAGE_COPIES: stage host inputs with cudaMemcpyAsync
+  int attend_layers = 1;            // layers per attention launch (pipelined schedule)
+  int step_kernels = 0;             // kernels launched by the last enqueued step
   bool select_per_layer = false;  // NOSA_SELECT_PER_LAYER: one selection launch per layer
-  long long select_launches = 0;  // grouped selection launches of the step being enqueued
 };
 
 // brackets one launch with timing events when timing is enabled (eager steps only)
@@ -184,6 +186,7 @@ extern "C" int nosa_config_validate(const NosaConfig* c, char* msg, int msg_len)
   if (c->max_tokens <= 0) return bad("max_tokens must be positive");
   if (c->fast_slots <= 0) return bad("fast_slots must be positive");
   if (c->attend_chunk < 0 || c->attend_chunk > 8) return bad("attend_chunk must be in 0..8 (0 = auto)");
+  if (c->attend_layers < 0) return bad("attend_layers must be >= 0 (0 = auto)");
   if (c->dtype != NOSA_DTYPE_BF16 && c->dtype != NOSA_DTYPE_FP32) return bad("dtype must be bf16 or fp32");
   if (c->variant < 0 || c->variant > 2) return bad("variant must be ed-dma, s-dma or dma");
   if (c->residency != NOSA_RESIDENCY_PER_SEQUENCE && c->residency != NOSA_RESIDENCY_SHARED)
@@ -313,6 +316,19 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   dv.max_chunks = (dv.C + dv.chunk - 1) / dv.chunk;
   dv.rpc = 1;  // the bf16 kernel combines its consumer warps' partials before writing a record
   dv.max_rec = dv.max_chunks * dv.rpc;
+  // layers per attention launch (pipelined schedule): when every block of a sequence fits in
+  // HBM the step is HBM-bound and per-launch ramp-up/drain is the loss, so 4 layers share one
+  // persistent launch; with offloaded blocks each layer's attention waits only for its own
+  // miss transfer.  fp32 runs one layer per launch.
+  if (c.attend_layers > 0) {
+    ctx->attend_layers = c.attend_layers;
+  } else {
+    ctx->attend_layers = (dv.C >= dv.NB && c.dtype == NOSA_DTYPE_BF16) ? 4 : 1;
+  }
+  if (const char* e = getenv("NOSA_ATTEND_LAYERS")) ctx->attend_layers = std::max(1, atoi(e));
+  if (c.dtype != NOSA_DTYPE_BF16) ctx->attend_layers = 1;
+  ctx->attend_layers = std::min(ctx->attend_layers, dv.L);
+  dv.nbuf = 2 * ctx->attend_layers;
   const size_t LBH = (size_t)dv.L * dv.B * dv.H;
   const size_t BH = (size_t)dv.B * dv.H;
 
@@ -353,8 +369,8 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   ALLOC(dv.plan_n, LBH * 3);
   ALLOC(dv.cnt, (size_t)dv.L * 2);
   ALLOC(dv.miss_list, (size_t)dv.L * BH * dv.C);
-  ALLOC(dv.part_o, 2 * BH * dv.max_rec * dv.G * dv.D);
-  ALLOC(dv.part_ml, 2 * BH * dv.max_rec * dv.G);
+  ALLOC(dv.part_o, (size_t)dv.nbuf * BH * dv.max_rec * dv.G * dv.D);
+  ALLOC(dv.part_ml, (size_t)dv.nbuf * BH * dv.max_rec * dv.G);
   ALLOC(dv.newrow, LBH * 2 * dv.D * (size_t)dv.elem);
   ALLOC(dv.w1, (size_t)dv.D * dv.n_ev);
   ALLOC(dv.w2, (size_t)dv.n_ev);
@@ -649,7 +665,7 @@ extern "C" int nosa_attend(NosaCtx* ctx, int layer, const void* q, const void* k
   if (rc) return rc;
   if (!q || !k_new || !v_new || !out) return fail(ctx, NOSA_ERR_VALUE, "attend: NULL tensor");
   cudaSetDevice(ctx->device);
-  CUDA_TRY(ctx, nosa::launch_attend(ctx->dv, layer, q, k_new, v_new, out, S(stream), ctx->num_sms));
+  CUDA_TRY(ctx, nosa::launch_attend(ctx->dv, layer, 1, q, k_new, v_new, out, S(stream), ctx->num_sms));
   CUDA_TRY(ctx, nosa::launch_finalize(ctx->dv, layer, k_new, v_new, out, S(stream)));
   ctx->launches += 2;
   return NOSA_OK;
@@ -746,7 +762,9 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   std::vector<std::pair<int, int>>& groups = ctx->groups;
   groups.clear();
   if (grouped) {
-    for (int l0 = 0, n = 1; l0 < dv.L; l0 += n, n = (l0 <= 1 ? 1 : l0)) groups.push_back({l0, std::min(n, dv.L - l0)});
+    // sizes nl, nl, 2nl, 4nl, ... (nl = layers per attention batch): batch k's plans complete together
+    const int nlb = ctx->attend_layers;
+    for (int l0 = 0, n = nlb; l0 < dv.L; l0 += n, n = std::max(nlb, l0)) groups.push_back({l0, std::min(n, dv.L - l0)});
   } else {
     for (int l = 0; l < dv.L; ++l) groups.push_back({l, 1});
   }
@@ -771,7 +789,6 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
       CUDA_TRY(ctx, nosa::launch_select_plan(dv, l0, q + l0 * qstride, io->selector, 1, nullptr, nullptr, st, n));
     }
     for (int l = l0; l < l0 + n; ++l) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[l], st));
-    if (count) ctx->select_launches += 1;
     return NOSA_OK;
   };
   // Issues groups [next_group, upto): the host inputs of the group (three copies, nosa_decode_
@@ -810,7 +827,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
                         const_cast<char*>(vn) + l0 * kstride};
         const size_t bytes[3] = {n * qstride, n * kstride, n * kstride};
         CUDA_TRY(ctx, nosa::launch_stage_inputs(src, dst, bytes, ctx->stage_grid, in));
-        if (count) ctx->launches += 1;
+        if (count) ctx->launches += 1;  // (not part of step_kernels: host-buffer steps are never captured)
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev_in[l0 + n - 1], in));
       } else if (hio) {
         cudaStream_t in = ctx->in_stream;
@@ -844,6 +861,11 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   // with the copy-engine mover, only the first two groups' inputs go ahead of the first miss
   // transfer; the rest follow it (the host submits that transfer once layer 0 is planned)
   if (int rc = issue_groups(groups.size())) return rc;
+  // attention batches: nl consecutive layers per persistent launch (layer-serial: one, since
+  // select(l+1) waits for layer l to finish)
+  const int nl = serial ? 1 : ctx->attend_layers;
+  int n_att = 0, n_gather_kernels = 0;
+  cudaEvent_t last_att[2] = {nullptr, nullptr};
   for (int l = 0; l < dv.L; ++l) {
     if (serial) {
       if (l > 0) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_fin[l - 1], 0));
@@ -857,28 +879,33 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
       TimeScope ts(ctx, cp, 1, timed);
       const bool tma = io->gather_mode == NOSA_GATHER_TMA;
       CUDA_TRY(ctx, nosa::launch_gather(dv, l, cp, tma ? ctx->tma_gather_grid : ctx->gather_grid, tma));
-      if (count) ctx->launches += 1;
+      ++n_gather_kernels;
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[l], cp));
-    cudaStream_t a = (l & 1) ? at2 : at;
-    CUDA_TRY(ctx, cudaStreamWaitEvent(a, ctx->ev_gather[l], 0));
-    if (l >= 2) CUDA_TRY(ctx, cudaStreamWaitEvent(a, ctx->ev_fin[l - 2], 0));
+    if ((l + 1) % nl != 0 && l != dv.L - 1) continue;  // not the last layer of an attention batch
+    const int l0 = l - l % nl, n = l - l0 + 1;
+    cudaStream_t a = (n_att & 1) ? at2 : at;
+    CUDA_TRY(ctx, cudaStreamWaitEvent(a, ctx->ev_gather[l], 0));  // gathers run in order on cp
+    // record buffers: layer l' uses buffer l' % nbuf, last written for layer l' - nbuf
+    if (l - dv.nbuf >= 0) CUDA_TRY(ctx, cudaStreamWaitEvent(a, ctx->ev_fin[l - dv.nbuf], 0));
     {
       TimeScope ts(ctx, a, 2, timed);
-      CUDA_TRY(ctx, nosa::launch_attend(dv, l, q + l * qstride, kn + l * kstride, vn + l * kstride,
-                                        io->out + l * ostride, a, ctx->num_sms));
+      CUDA_TRY(ctx, nosa::launch_attend(dv, l0, n, q + l0 * qstride, kn + l0 * kstride, vn + l0 * kstride,
+                                        io->out + l0 * ostride, a, ctx->num_sms));
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_att[l], a));
+    last_att[n_att & 1] = ctx->ev_att[l];
+    ++n_att;
     CUDA_TRY(ctx, cudaStreamWaitEvent(fn, ctx->ev_att[l], 0));
-    {
+    {  // merge + append of the batch's layers in one launch
       TimeScope ts(ctx, fn, 3, timed);
-      CUDA_TRY(ctx, nosa::launch_finalize(dv, l, kn + l * kstride, vn + l * kstride, io->out + l * ostride, fn));
+      CUDA_TRY(ctx, nosa::launch_finalize(dv, l0, kn + l0 * kstride, vn + l0 * kstride, io->out + l0 * ostride, fn, n));
     }
-    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fin[l], fn));
+    for (int lf = l0; lf <= l; ++lf) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fin[lf], fn));
     if (hio) {
       CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_fin[l], 0));
       TimeScope ts(ctx, ctx->d2h_stream, 5, timed);
-      CUDA_TRY(ctx, cudaMemcpyAsync(hio->out + l * ostride, io->out + l * ostride, ostride * sizeof(float),
+      CUDA_TRY(ctx, cudaMemcpyAsync(hio->out + l0 * ostride, io->out + l0 * ostride, n * ostride * sizeof(float),
                                     cudaMemcpyDeviceToHost, ctx->d2h_stream));
     }
   }
@@ -888,12 +915,14 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   }
   // join every side stream back into the caller's stream
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_gather[dv.L - 1], 0));
-  CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_att[dv.L - 1], 0));
-  if (dv.L > 1) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_att[dv.L - 2], 0));
+  for (cudaEvent_t e : last_att)
+    if (e) CUDA_TRY(ctx, cudaStreamWaitEvent(st, e, 0));
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_fin[dv.L - 1], 0));
-  // + the gather kernels counted above; grouped selections counted in select_group
-  if (count) ctx->launches += (dv.shared ? 4LL : 3LL) * dv.L - (ctx->select_launches ? dv.L - ctx->select_launches : 0);
-  ctx->select_launches = 0;
+  // kernels of this step: selections (grouped, per layer, or per layer + shared planner),
+  // gathers (device movers), attention batches, finalizes, input staging (counted inline)
+  const int n_sel = grouped ? (int)groups.size() : (dv.shared ? 2 : 1) * dv.L;
+  ctx->step_kernels = n_sel + n_gather_kernels + 2 * n_att;  // one finalize per attention batch
+  if (count) ctx->launches += ctx->step_kernels;
   return NOSA_OK;
 }
 
@@ -959,12 +988,7 @@ extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {
   // the clean graph: what a replay runs unless per-kernel timing is on
   if (int rc = capture(false, &ctx->graph)) return rc;
   CUDA_TRY(ctx, cudaGraphInstantiate(&ctx->graph_exec, ctx->graph, 0));
-  ctx->graph_kernels = (ctx->dv.shared ? 5 : 4) * ctx->dv.L;
-  if (!ctx->dv.shared && !ctx->select_per_layer && io->schedule != 1) {  // grouped selections
-    int groups = 0;
-    for (int l0 = 0, n = 1; l0 < ctx->dv.L; l0 += n, n = (l0 <= 1 ? 1 : l0)) ++groups;
-    ctx->graph_kernels -= ctx->dv.L - groups;
-  }
+  ctx->graph_kernels = ctx->step_kernels;
   // the instrumented twin: an external event-record node around every kernel (placeholders)
   const size_t nslots = 4 * (size_t)ctx->dv.L;
   while (ctx->cap_events.size() < nslots) {

@@ -35,6 +35,7 @@ struct Dev {
   int max_chunks;                // ceil(C / chunk)
   int rpc;                       // split-K records per chunk: one per consumer warp (bf16), 1 (fp32)
   int max_rec;                   // max_chunks * rpc records per (b, h)
+  int nbuf;                      // split-K record buffers (layer l uses buffer l % nbuf)
   // ---- persistent state ----------------------------------------------------------------
   char* pool;
   char* host;                    // device-visible alias of the pinned host mirror
@@ -85,12 +86,12 @@ __host__ __device__ __forceinline__ int shared_rel(const Dev& dv, int b, int s) 
   return (s / dv.C - b) * dv.H * dv.C + s % dv.C;
 }
 
-// the split-K record buffer of a layer (double-buffered by layer parity)
+// the split-K record buffer of a layer (nbuf buffers: attention batches are double-buffered)
 __host__ __device__ __forceinline__ float* part_o_of(const Dev& dv, int layer) {
-  return dv.part_o + (size_t)(layer & 1) * dv.B * dv.H * dv.max_rec * dv.G * dv.D;
+  return dv.part_o + (size_t)(layer % dv.nbuf) * dv.B * dv.H * dv.max_rec * dv.G * dv.D;
 }
 __host__ __device__ __forceinline__ float2* part_ml_of(const Dev& dv, int layer) {
-  return dv.part_ml + (size_t)(layer & 1) * dv.B * dv.H * dv.max_rec * dv.G;
+  return dv.part_ml + (size_t)(layer % dv.nbuf) * dv.B * dv.H * dv.max_rec * dv.G;
 }
 
 // ---------------------------------------------------------------- small helpers

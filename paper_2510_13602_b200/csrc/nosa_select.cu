@@ -130,50 +130,47 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
   }
   __syncthreads();
 
-  // (2) s_q = K_c[pool] . q_sum.  Each warp streams 8 block rows per iteration; lane l holds
+  // (2) s_q = K_c[pool] . q_sum.  Each warp streams 4 block rows per iteration; lane l holds
   //     dims [l*D/32, (l+1)*D/32) of every row, all loads issued before the FMAs, then a
-  //     butterfly reduce-scatter leaves row (l>>2)&7 fully summed on lanes with l%4 == 0.
+  //     butterfly reduce-scatter leaves row (l>>3)&3 fully summed on lanes with l%8 == 0.
+  //     (4 rows, not 8, keep the CTA at <= 80 registers: 3 CTAs per SM, so one CTA's scan
+  //     overlaps another's sort and plan.)
   const double* kc = dv.kc + (size_t)lbh * dv.NB * D;
   double* s_q_out = dv.s_q + (size_t)lbh * dv.NB;
   const int nv = D / 64;  // double2 loads per lane per row (1 or 2)
   const double* qs = sm.qsum + lane * 2 * nv;
-  for (int p0 = warp * 8; p0 < P; p0 += nwarps * 8) {
-    double2 v[8][2];
+  for (int p0 = warp * 4; p0 < P; p0 += nwarps * 4) {
+    double2 v[4][2];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 4; ++u) {
       const int p = p0 + u;
       const double2* row = reinterpret_cast<const double2*>(kc + (size_t)(pool_lo + min(p, P - 1)) * D) + lane * nv;
       v[u][0] = __ldg(row);
       v[u][1] = nv == 2 ? __ldg(row + 1) : make_double2(0.0, 0.0);
     }
-    double a[8];
+    double a[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 4; ++u) {
       a[u] = fma(v[u][0].y, qs[1], v[u][0].x * qs[0]);
       if (nv == 2) a[u] = fma(v[u][1].y, qs[3], fma(v[u][1].x, qs[2], a[u]));
     }
-    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const double send = b4 ? a[i] : a[i + 4];
-      const double keep = b4 ? a[i + 4] : a[i];
-      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
+    const bool b4 = lane & 16, b3 = lane & 8;
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      const double send = b3 ? a[i] : a[i + 2];
-      const double keep = b3 ? a[i + 2] : a[i];
-      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      const double send = b4 ? a[i] : a[i + 2];
+      const double keep = b4 ? a[i + 2] : a[i];
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
     {
-      const double send = b2 ? a[0] : a[1];
-      const double keep = b2 ? a[1] : a[0];
-      a[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      const double send = b3 ? a[0] : a[1];
+      const double keep = b3 ? a[1] : a[0];
+      a[0] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
     }
+    a[0] += __shfl_xor_sync(0xffffffffu, a[0], 4);
     a[0] += __shfl_xor_sync(0xffffffffu, a[0], 2);
     a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
-    const int p = p0 + (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
-    if ((lane & 3) == 0 && p < P) {
+    const int p = p0 + (b4 ? 2 : 0) + (b3 ? 1 : 0);
+    if ((lane & 7) == 0 && p < P) {
       sm.key[p] = order_key(a[0]);
       sm.idx[p] = p;
       s_q_out[pool_lo + p] = a[0];
@@ -422,7 +419,7 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
 // grid = (B*H, layers), block = 256: layer = layer0 + blockIdx.y with its queries at
 // q + blockIdx.y * q_layer_stride.  mode: 0 = select only, 1 = select + plan, 2 = plan on ext_req.
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)  // 3 CTAs per SM: one CTA's scan overlaps another's sort/plan
     select_plan_kernel(Dev dv, int layer0, const T* __restrict__ q0, size_t q_layer_stride, int selector,
                        int mode, const int* __restrict__ ext_req, const int* __restrict__ ext_nreq) {
   extern __shared__ __align__(16) char smem_raw[];

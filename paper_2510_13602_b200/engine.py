@@ -82,12 +82,15 @@ class StepOutput:
 class NosaEngine:
     def __init__(self, config: AttentionConfig, *, batch: int, max_tokens: int, fast_slots: int,
                  w1, w2, layers: int = 1, variant: str = "ed-dma", dtype: str = "bf16",
-                 device: int = 0, residency: str = "per-sequence", attend_chunk: int = 0):
+                 device: int = 0, residency: str = "per-sequence", attend_chunk: int = 0,
+                 attend_layers: int = 0):
         """residency "per-sequence": one manager per (layer, sequence, head) with `fast_slots`
         slots; "shared": one pool of batch*fast_slots slots per (layer, head)
         shared by the batch and planned in batch order, the reference simulator's residency.
         attend_chunk: KV blocks per split-K attention work item (1..8, 0 = chosen from the
-        batch size); outputs are bit-identical across runs with the same value."""
+        batch size); outputs are bit-identical across runs with the same value.
+        attend_layers: layers per persistent attention launch in the pipelined schedule (0 =
+        4 when every block fits in HBM, else 1); results do not depend on it."""
         if variant not in _lib.VARIANT:
             raise ValueError(f"variant must be one of {tuple(_lib.VARIANT)} (retaining needs hidden states)")
         if residency not in _lib.RESIDENCY:
@@ -108,6 +111,7 @@ class NosaEngine:
         c.dtype, c.variant = _lib.DTYPE[dtype], _lib.VARIANT[variant]
         c.residency = _lib.RESIDENCY[residency]
         c.attend_chunk = attend_chunk
+        c.attend_layers = attend_layers
         self._cfg = c
         msg = ctypes.create_string_buffer(512)
         if _lib.lib.nosa_config_validate(ctypes.byref(c), msg, 512) != _lib.NOSA_OK:

@@ -224,6 +224,13 @@ def test_resident_prefill(dtype):
               resident=True)
 
 
+def test_resident_multilayer_batched_attention():
+    """All blocks in HBM: attention runs 4 layers per persistent launch (6 layers = 4 + 2)."""
+    a = _run_pair(ONE_B_SMALL, batch=2, t0s=[3000, 2900], steps=8, fast_slots=48, seed=17, rho=0.3, layers=6,
+                  resident=True)
+    assert a <= TOL["bf16"]
+
+
 @pytest.mark.parametrize("gather", ["memcpy", "tma"])
 def test_other_gather_paths_vs_oracle(gather):
     a = _run_pair(SMALL, batch=2, t0s=[900, 800], steps=20, fast_slots=36, seed=12, rho=0.0, gather=gather)
@@ -237,10 +244,12 @@ def test_gather_paths_and_schedules_bitwise_identical():
     K, V = workload.prefix_kv(2, 6, cfg.n_kv_head, 3000, cfg.d_head)
     K, V = K.reshape(3, 2, cfg.n_kv_head, 3000, cfg.d_head), V.reshape(3, 2, cfg.n_kv_head, 3000, cfg.d_head)
     results = []
-    runs = [("uva", "pipelined", False), ("tma", "pipelined", False), ("memcpy", "pipelined", False),
-            ("uva", "serial", False), ("memcpy", "pipelined", True), ("uva", "serial", True)]
-    for gather, schedule, host in runs:
-        eng = NosaEngine(cfg, batch=2, layers=3, max_tokens=3100, fast_slots=70, w1=w1, w2=w2)
+    runs = [("uva", "pipelined", False, 1), ("tma", "pipelined", False, 1), ("memcpy", "pipelined", False, 1),
+            ("uva", "serial", False, 1), ("memcpy", "pipelined", True, 1), ("uva", "serial", True, 1),
+            ("uva", "pipelined", False, 2), ("memcpy", "pipelined", True, 3)]
+    for gather, schedule, host, att_layers in runs:
+        eng = NosaEngine(cfg, batch=2, layers=3, max_tokens=3100, fast_slots=70, w1=w1, w2=w2,
+                         attend_layers=att_layers)
         eng.prefill(torch.from_numpy(K), torch.from_numpy(V))
         eng.start_run()
         stream = workload.QueryStream(2, 3, 2, cfg.n_head, cfg.n_kv_head, cfg.d_head, 0.0)
