@@ -354,8 +354,10 @@ def run_native(args, rank, world, local_rank):
     R_inst = st_i.hits + st_i.misses                  # the same over the instrumented pass
     P = eng.geometry[0].pool_blocks.stop - eng.geometry[0].pool_blocks.start
     per_launch = {
-        # K1+K2: f64 K_c pool scan + q read + tables (reads of required-list metadata are small)
-        "select_plan": (B * cfg.n_kv_head * P * cfg.d_head * 8 + B * cfg.n_head * cfg.d_head * 2),
+        # K1+K2: screened pool scan (bf16 K_c + the f32 rounding-error bound per row) + f64 rows of
+        # the candidates + q read (reads of required-list metadata are small); exact scan: f64 K_c
+        "select_plan": ((B * cfg.n_kv_head * P * (cfg.d_head * 2 + 4) + st_i.candidates * cfg.d_head * 8 / calls)
+                        if eng.screened else B * cfg.n_kv_head * P * cfg.d_head * 8) + B * cfg.n_head * cfg.d_head * 2,
         # K3: each missed block crosses PCIe once and is written to HBM once
         "gather": (st_i.misses - st_i.new_blocks) * bpb / calls,
         # K4: K|V of every attended block + its bias + the query rows
@@ -424,6 +426,10 @@ def run_native(args, rank, world, local_rank):
             "hit_rate": round(st.hit_rate, 4),
             "misses_per_seq_head_step": round(st.misses / (B * cfg.n_kv_head * L * args.steps), 3),
             "attended_blocks_per_seq_head": round(R_total / (B * cfg.n_kv_head * L * args.steps), 2),
+            "selection": {"scan": "screened: bf16 K_c pre-scan with a proven error bound, f64 rescoring of "
+                                  "the candidates (same picks as a full f64 scan)" if eng.screened else "full f64",
+                          "pool_blocks": P,
+                          "f64_rows_per_selection": round(st.candidates / (B * cfg.n_kv_head * L * args.steps), 2)},
             "link_gbs_measured": round(link_gbs, 2),
             "roofline": roofline, "link_roofline": link_roofline, "step_roofline": step_roofline,
             "kernels": {k_: {"avg_ms": round(v["avg_ms"], 5), "launches": v["launches"],

@@ -72,6 +72,8 @@ typedef struct NosaConfig {
                            the batch size.  Outputs are bit-identical for a fixed value.    */
   int32_t attend_layers; /* layers per persistent attention launch in the pipelined schedule;
                             0 = auto (4 when every block fits in HBM, else 1)               */
+  int32_t exact_scan;    /* 0: screened selection (bf16 pre-scan of the pool, f64 rescoring of
+                            the candidates: the same picks as a full f64 scan); 1: full f64  */
 } NosaConfig;
 
 /* residency contract */
@@ -84,6 +86,7 @@ typedef struct NosaConfig {
 typedef struct NosaStats {
   int64_t hits, misses, new_blocks, evictions, steps;
   int64_t bytes_up, bytes_down; /* misses * bytes_per_block, evictions * bytes_per_block */
+  int64_t candidates;           /* pool rows rescored in f64 by the screened selector     */
 } NosaStats;
 
 /* Per-step inputs/outputs of nosa_decode_step: one pointer per tensor, layer-major.

@@ -37,12 +37,12 @@ class NosaConfig(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int32) for name in (
         "n", "d", "n_head", "n_kv_head", "d_head", "n_b", "n_s", "n_w", "k", "k_q", "k_e",
         "accounting", "batch", "layers", "max_tokens", "fast_slots", "dtype", "variant", "residency",
-        "attend_chunk", "attend_layers")]
+        "attend_chunk", "attend_layers", "exact_scan")]
 
 
 class NosaStats(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in (
-        "hits", "misses", "new_blocks", "evictions", "steps", "bytes_up", "bytes_down")]
+        "hits", "misses", "new_blocks", "evictions", "steps", "bytes_up", "bytes_down", "candidates")]
 
 
 class NosaStepIO(ctypes.Structure):

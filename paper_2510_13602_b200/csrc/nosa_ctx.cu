@@ -18,6 +18,8 @@ namespace nosa {
 cudaError_t launch_select_plan(const Dev& dv, int layer, const void* q, int selector, int mode,
                                const int* ext_req, const int* ext_nreq, cudaStream_t st, int layers = 1);
 cudaError_t launch_start_run(const Dev& dv, int seq_begin, int seq_count, cudaStream_t st);
+cudaError_t launch_screen_build(const Dev& dv, int seq_begin, int seq_count, cudaStream_t st);
+cudaError_t launch_score_readback(const Dev& dv, int layer, cudaStream_t st);
 cudaError_t launch_plan_shared(const Dev& dv, int layer, const int* ext_req, const int* ext_nreq, cudaStream_t st);
 cudaError_t launch_select_scores(int n_prob, const double* s_q, const double* s_e, int stride,
                                  const int* lo, const int* hi, int m_q, int m_e, int selector,
@@ -187,6 +189,7 @@ extern "C" int nosa_config_validate(const NosaConfig* c, char* msg, int msg_len)
   if (c->fast_slots <= 0) return bad("fast_slots must be positive");
   if (c->attend_chunk < 0 || c->attend_chunk > 8) return bad("attend_chunk must be in 0..8 (0 = auto)");
   if (c->attend_layers < 0) return bad("attend_layers must be >= 0 (0 = auto)");
+  if (c->exact_scan < 0 || c->exact_scan > 1) return bad("exact_scan must be 0 or 1");
   if (c->dtype != NOSA_DTYPE_BF16 && c->dtype != NOSA_DTYPE_FP32) return bad("dtype must be bf16 or fp32");
   if (c->variant < 0 || c->variant > 2) return bad("variant must be ed-dma, s-dma or dma");
   if (c->residency != NOSA_RESIDENCY_PER_SEQUENCE && c->residency != NOSA_RESIDENCY_SHARED)
@@ -297,6 +300,7 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   dv.dtype = c.dtype;
   dv.variant = c.variant;
   dv.shared = c.residency == NOSA_RESIDENCY_SHARED;
+  dv.screen = (c.exact_scan == 0 && (c.d_head == 128 || c.d_head == 64) && !getenv("NOSA_EXACT_SCAN")) ? 1 : 0;
   dv.elem = c.dtype == NOSA_DTYPE_BF16 ? 2 : 4;
   dv.bpb = 2LL * c.n_b * c.d_head * dv.elem;
   // split-K chunk: the largest of 8, 4, 2, 1 blocks that still gives every SM two work
@@ -364,6 +368,11 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   ALLOC(dv.sel_e, LBH * dv.ME);
   ALLOC(dv.n_sele, LBH);
   ALLOC(dv.s_q, LBH * dv.NB);
+  if (dv.screen) {
+    ALLOC(dv.kc16, LBH * dv.NB * dv.D);
+    ALLOC(dv.kc_err, LBH * dv.NB);
+    ALLOC(dv.qsum_buf, LBH * dv.D);
+  }
   ALLOC(dv.plan_fetch, LBH * dv.C);
   ALLOC(dv.plan_evict, LBH * dv.C);
   ALLOC(dv.plan_n, LBH * 3);
@@ -549,6 +558,10 @@ extern "C" int nosa_start_run(NosaCtx* ctx, int seq_begin, int seq_count, void* 
   cudaSetDevice(ctx->device);
   CUDA_TRY(ctx, nosa::launch_start_run(ctx->dv, seq_begin, seq_count, S(stream)));
   ctx->launches += 1;
+  if (ctx->dv.screen) {
+    CUDA_TRY(ctx, nosa::launch_screen_build(ctx->dv, seq_begin, seq_count, S(stream)));
+    ctx->launches += 1;
+  }
   return NOSA_OK;
 }
 
@@ -1088,7 +1101,13 @@ extern "C" int nosa_read_selection(NosaCtx* ctx, int layer, int cap, int32_t* bq
       if (req) req[x * cap + i] = i < cr[x] && i < dv.C ? tr[x * dv.C + i] : -1;
     }
   }
-  if (s_q) CUDA_TRY(ctx, cudaMemcpy(s_q, dv.s_q + off * dv.NB, BH * dv.NB * 8, cudaMemcpyDeviceToHost));
+  if (s_q) {
+    if (dv.screen) {  // the hot path scored only the candidates: recompute every pool row in f64
+      CUDA_TRY(ctx, nosa::launch_score_readback(dv, layer, nullptr));
+      SYNC_OR_FAIL(ctx);
+    }
+    CUDA_TRY(ctx, cudaMemcpy(s_q, dv.s_q + off * dv.NB, BH * dv.NB * 8, cudaMemcpyDeviceToHost));
+  }
   return NOSA_OK;
 }
 
@@ -1198,6 +1217,7 @@ extern "C" int nosa_read_stats(NosaCtx* ctx, int l0, int l1, int s0, int s1, Nos
         out->new_blocks += p[nosa::ST_NEW];
         out->evictions += p[nosa::ST_EVICT];
         out->steps += p[nosa::ST_STEPS];
+        out->candidates += p[nosa::ST_CAND];
       }
   out->bytes_up = out->misses * dv.bpb;
   out->bytes_down = out->evictions * dv.bpb;

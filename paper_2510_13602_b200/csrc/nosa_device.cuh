@@ -62,6 +62,11 @@ struct Dev {
   int* sel_e;                    // [lbh][ME]
   int* n_sele;
   double* s_q;                   // [lbh][NB] pool scores (kept for parity readback)
+  // ---- screened selection (exact top-k from a bf16 pre-scan + f64 refinement) -----------
+  int screen;                    // 1: screened scan (default), 0: full f64 scan of the pool
+  __nv_bfloat16* kc16;           // [lbh][NB][D] bf16(K_c) of the frozen pool (built at start_run)
+  float* kc_err;                 // [lbh][NB] sum_i |K_c - bf16(K_c)| of each pool row (rounded up)
+  double* qsum_buf;              // [lbh][D] the step's q_sum (parity readback recomputes s_q)
   int* plan_fetch;               // [lbh][C]
   int* plan_evict;               // [lbh][C]
   int* plan_n;                   // [lbh][3] n_fetch, n_evict, n_hit
@@ -75,7 +80,7 @@ struct Dev {
   unsigned* err;
 };
 
-enum StatIdx { ST_HITS = 0, ST_MISSES, ST_NEW, ST_EVICT, ST_STEPS, ST_N = 8 };
+enum StatIdx { ST_HITS = 0, ST_MISSES, ST_NEW, ST_EVICT, ST_STEPS, ST_CAND, ST_N = 8 };  // ST_CAND: rows rescored in f64
 
 // shared-pool mode: storage index of shared slot s of (layer, head) in the [lbh][C] arrays, and
 // the slot offset relative to sequence b's own pool row (pool + (lbh*C + rel)*bpb addresses it)

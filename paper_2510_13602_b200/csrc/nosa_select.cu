@@ -69,6 +69,9 @@ struct SelSmem {
   int* fpos;
   int* victims;
   unsigned long long* ckey;
+  unsigned* lo_key;  // [Pp] screened lower bound of each pool row (monotone u32 of the float)
+  float* up;         // [Pp] screened upper bound
+  int* hist;         // [256] radix-select histogram
   int* misc;  // [16]
 };
 
@@ -91,6 +94,9 @@ __device__ SelSmem carve_sel_smem(char* base, int D, int Pp, int C) {
   s.fpos = reinterpret_cast<int*>(take(sizeof(int) * C));
   s.victims = reinterpret_cast<int*>(take(sizeof(int) * C));
   s.ckey = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * C));
+  s.lo_key = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * Pp));
+  s.up = reinterpret_cast<float*>(take(sizeof(float) * Pp));
+  s.hist = reinterpret_cast<int*>(take(sizeof(int) * 256));
   s.misc = reinterpret_cast<int*>(take(sizeof(int) * 16));
   return s;
 }
@@ -98,10 +104,164 @@ __device__ SelSmem carve_sel_smem(char* base, int D, int Pp, int C) {
 size_t sel_smem_bytes(int D, int Pp, int C) {
   auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
   return r(8 * D) + r(8 * (size_t)Pp) + r(4 * (size_t)Pp) + 2 * r(4 * (size_t)(Pp / 32)) +
-         5 * r(4 * (size_t)C) + r(8 * (size_t)C) + r(64);
+         5 * r(4 * (size_t)C) + r(8 * (size_t)C) + 2 * r(4 * (size_t)Pp) + r(4 * 256) + r(64);
 }
 
-enum { M_NREQ = 0, M_NF, M_SHORT, M_NCAND, M_CLOCK, M_ERR, M_NQ, M_NE };
+enum { M_NREQ = 0, M_NF, M_SHORT, M_NCAND, M_CLOCK, M_ERR, M_NQ, M_NE, M_QMAX, M_BIN, M_REM, M_NC };
+
+// monotone u32 image of a float (larger float -> larger key), and back
+__device__ __forceinline__ unsigned f2key(float f) {
+  const unsigned b = __float_as_uint(f == 0.0f ? 0.0f : f);
+  return (b >> 31) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(unsigned k) {
+  return __uint_as_float((k >> 31) ? (k & 0x7fffffffu) : ~k);
+}
+
+// f64 dot of one K_c row with q_sum by one warp, every lane ends with the sum.  The screened
+// selector's refinement and the parity readback of s_q both use exactly this order.
+__device__ __forceinline__ double row_dot64(const double* __restrict__ row, const double* qs, int D) {
+  const int lane = threadIdx.x & 31;
+  double a = 0.0;
+  for (int i = lane * 2; i < D; i += 64) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(row + i));
+    a = fma(v.y, qs[i + 1], fma(v.x, qs[i], a));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  return a;
+}
+
+// Exact top-m of the pool by s_q = K_c . q_sum (f64), from a bf16 pre-scan.  Every pool row
+// gets an interval [lo, up] that provably contains its f64 score: the bf16 dot in fp32 plus
+// (fp32 accumulation bound) + (rounding of K_c to bf16: sum|K_c - bf16(K_c)| * max|q_sum|) +
+// (rounding of q_sum to fp32) + (f64 accumulation bound).  T = the m-th largest lower bound
+// (radix select); a row with up < T has m rows strictly above it, so only rows with up >= T
+// are candidates, rescored in f64 and ranked by (score desc, index asc) = argtopk's order.
+// Sets the picked bits in sm.bm_q.  bf16 rows are 4x fewer bytes than the f64 scan.
+__device__ void screened_topk(const Dev& dv, int lbh, int pool_lo, int P, int m, SelSmem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int D = dv.D;
+  const __nv_bfloat16* k16 = dv.kc16 + ((size_t)lbh * dv.NB + pool_lo) * D;
+  const float* kerr = dv.kc_err + (size_t)lbh * dv.NB + pool_lo;
+  const float qmax = __int_as_float(sm.misc[M_QMAX]);
+  const float gam = (float)(D + 8) * 5.9604645e-08f + 1.1920929e-07f;  // (D+8) 2^-24 + 2^-23 (+ f64 slack)
+  // lane's q_sum dims in fp32: D=128 -> 4 dims [4*lane, 4*lane+4), D=64 -> 2 dims
+  const int per = D / 32;
+  float qf[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) qf[j] = j < per ? (float)sm.qsum[lane * per + j] : 0.0f;
+  // (a) screen: 8 rows per warp iteration, all loads first
+  for (int p0 = warp * 8; p0 < P; p0 += nwarps * 8) {
+    uint2 raw[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const __nv_bfloat16* row = k16 + (size_t)min(p0 + u, P - 1) * D + lane * per;
+      if (per == 4) raw[u] = __ldg(reinterpret_cast<const uint2*>(row));
+      else raw[u] = make_uint2(__ldg(reinterpret_cast<const unsigned*>(row)), 0u);
+    }
+    float sv[8], av[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const __nv_bfloat162 x01 = *reinterpret_cast<const __nv_bfloat162*>(&raw[u].x);
+      const __nv_bfloat162 x23 = *reinterpret_cast<const __nv_bfloat162*>(&raw[u].y);
+      const float k0 = __low2float(x01), k1 = __high2float(x01), k2 = __low2float(x23), k3 = __high2float(x23);
+      sv[u] = fmaf(k3, qf[3], fmaf(k2, qf[2], fmaf(k1, qf[1], k0 * qf[0])));
+      av[u] = fmaf(fabsf(k3), fabsf(qf[3]), fmaf(fabsf(k2), fabsf(qf[2]), fmaf(fabsf(k1), fabsf(qf[1]), fabsf(k0 * qf[0]))));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        sv[u] += __shfl_xor_sync(0xffffffffu, sv[u], o);
+        av[u] += __shfl_xor_sync(0xffffffffu, av[u], o);
+      }
+    }
+    if (lane < 8 && p0 + lane < P) {
+      float s_ = sv[0], a_ = av[0];
+#pragma unroll
+      for (int u = 1; u < 8; ++u)
+        if (lane == u) s_ = sv[u], a_ = av[u];
+      const int p = p0 + lane;
+      const float bound = (gam * a_ + __ldg(kerr + p) * qmax) * 1.001f + fabsf(s_) * 2.4e-7f + 1e-30f;
+      sm.lo_key[p] = f2key(__fsub_rd(s_, bound));
+      sm.up[p] = __fadd_ru(s_, bound);
+    }
+  }
+  __syncthreads();
+  // (b) T = m-th largest lower bound: 4 passes of an 8-bit radix select
+  unsigned prefix = 0u, pmask = 0u;
+  int remaining = m;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    for (int i = tid; i < 256; i += blockDim.x) sm.hist[i] = 0;
+    __syncthreads();
+    for (int p = tid; p < P; p += blockDim.x) {
+      const unsigned k = sm.lo_key[p];
+      if ((k & pmask) == prefix) atomicAdd(&sm.hist[(k >> shift) & 255u], 1);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int c[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = sm.hist[255 - 8 * lane - j];
+        sum += c[j];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int excl = incl - sum;
+      if (excl < remaining && remaining <= incl) {
+        int acc = excl;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (acc + c[j] >= remaining) {
+            sm.misc[M_BIN] = 255 - 8 * lane - j;
+            sm.misc[M_REM] = remaining - acc;
+            break;
+          }
+          acc += c[j];
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= (unsigned)sm.misc[M_BIN] << shift;
+    pmask |= 255u << shift;
+    remaining = sm.misc[M_REM];
+  }
+  const float T = key2f(prefix);
+  // (c) candidates: up >= T, rescored in f64 (one warp per row)
+  if (tid == 0) sm.misc[M_NC] = 0;
+  __syncthreads();
+  for (int p = tid; p < P; p += blockDim.x)
+    if (sm.up[p] >= T) sm.idx[atomicAdd(&sm.misc[M_NC], 1)] = p;
+  __syncthreads();
+  const int nc = sm.misc[M_NC];
+  if (tid == 0) dv.stats[(size_t)lbh * ST_N + ST_CAND] += nc;
+  double* cs = reinterpret_cast<double*>(sm.key);  // candidate scores
+  const double* kc = dv.kc + ((size_t)lbh * dv.NB + pool_lo) * D;
+  for (int i = warp; i < nc; i += nwarps) {
+    const double v = row_dot64(kc + (size_t)sm.idx[i] * D, sm.qsum, D);
+    if (lane == 0) cs[i] = v;
+  }
+  __syncthreads();
+  // (d) rank the candidates by (score desc, index asc); the first m are the picks
+  for (int i = tid; i < nc; i += blockDim.x) {
+    const double si = cs[i];
+    const int pi = sm.idx[i];
+    int rank = 0;
+    for (int j = 0; j < nc; ++j) {
+      const double sj = cs[j];
+      rank += (sj > si) || (sj == si && sm.idx[j] < pi);
+    }
+    if (rank < m) atomicOr(&sm.bm_q[pi >> 5], 1u << (pi & 31));
+  }
+  __syncthreads();
+}
 
 // ------------------------------------------------------------------------------------------
 // Selection phase: fills sm.req[0..n_req) (sorted) and the selection buffers.
@@ -123,12 +283,32 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
   const int Pp = next_pow2(P);
 
   // (1) q_sum = sum of the group's query heads (decode.py:171-172), f64
+  if (tid == 0) sm.misc[M_QMAX] = 0;
+  __syncthreads();
   for (int i = tid; i < D; i += blockDim.x) {
     double acc = 0.0;
     for (int g = 0; g < dv.G; ++g) acc += to_f64(q[((size_t)b * dv.Hq + h * dv.G + g) * D + i]);
     sm.qsum[i] = acc;
+    if (dv.screen) {
+      dv.qsum_buf[(size_t)lbh * D + i] = acc;
+      atomicMax(&sm.misc[M_QMAX], __float_as_int(__double2float_ru(fabs(acc))));  // |q| bits order as ints
+    }
   }
   __syncthreads();
+  const int m_q_eff = min(selector == 0 ? dv.m_q : dv.m_topk, P);
+  if (dv.screen) {
+    for (int w = tid; w < Pp / 32; w += blockDim.x) {
+      sm.bm_q[w] = 0u;
+      sm.bm_e[w] = 0u;
+    }
+    __syncthreads();
+    if (m_q_eff >= P) {  // the whole pool is picked: no scores needed
+      for (int p = tid; p < P; p += blockDim.x) atomicOr(&sm.bm_q[p >> 5], 1u << (p & 31));
+      __syncthreads();
+    } else if (m_q_eff > 0) {
+      screened_topk(dv, lbh, pool_lo, P, m_q_eff, sm);
+    }
+  } else {
 
   // (2) s_q = K_c[pool] . q_sum.  Each warp streams 4 block rows per iteration; lane l holds
   //     dims [l*D/32, (l+1)*D/32) of every row, all loads issued before the FMAs, then a
@@ -188,12 +368,12 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
 
   // (3) query-aware top-k over the pool (argtopk order)
   if (P > 0) block_sort_best_first(sm.key, sm.idx, Pp);
-  const int m_q_eff = min(selector == 0 ? dv.m_q : dv.m_topk, P);
   for (int r = tid; r < m_q_eff; r += blockDim.x) {
     const int p = sm.idx[r];
     atomicOr(&sm.bm_q[p >> 5], 1u << (p & 31));
   }
   __syncthreads();
+  }  // full f64 scan
 
   // (4) NOSA: query-agnostic picks = first m_e pool blocks of the frozen s_e rank order that
   //     were not picked by the query (selection.py:151-156)
@@ -477,6 +657,60 @@ __global__ void __launch_bounds__(256) start_run_kernel(Dev dv, int seq_begin, i
   int* rank = dv.rank_e + (size_t)lbh * dv.NB;
   for (int p = threadIdx.x; p < P; p += blockDim.x) rank[p] = idx[p];
   if (threadIdx.x == 0) dv.t0[lbh] = t;
+}
+
+// ------------------------------------------------------------------------------------------
+// Screened-selection state of the frozen pool, built at start_run: bf16(K_c) of every pool
+// row and the L1 norm of its rounding error (rounded up).  One warp per row.
+__global__ void __launch_bounds__(256) screen_build_kernel(Dev dv, int seq_begin, int seq_count) {
+  const int i = blockIdx.x;  // over layers x seq_count x H
+  const int h = i % dv.H;
+  const int s = (i / dv.H) % seq_count;
+  const int l = i / (dv.H * seq_count);
+  const int lbh = (l * dv.B + seq_begin + s) * dv.H + h;
+  const int D = dv.D, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int recent_start = max(0, dv.t0[lbh] - dv.n_w + 1);
+  const int pool_lo = dv.n_sink, pool_hi = max(pool_lo, recent_start / dv.n_b);
+  for (int p = pool_lo + warp; p < pool_hi; p += nwarps) {
+    const double* row = dv.kc + ((size_t)lbh * dv.NB + p) * D;
+    __nv_bfloat16* out = dv.kc16 + ((size_t)lbh * dv.NB + p) * D;
+    double e = 0.0;
+    for (int d = lane; d < D; d += 32) {
+      const double x = row[d];
+      const __nv_bfloat16 y = __double2bfloat16(x);
+      out[d] = y;
+      e += fabs(x - (double)__bfloat162float(y));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+    if (lane == 0) dv.kc_err[(size_t)lbh * dv.NB + p] = __double2float_ru(e * (1.0 + 1e-12));
+  }
+}
+
+// Parity readback of the screened selector: s_q of every pool row in f64, from the step's q_sum,
+// in the refinement's order (row_dot64).  grid = B*H of one layer.
+__global__ void __launch_bounds__(256) score_readback_kernel(Dev dv, int layer) {
+  const int lbh = layer * dv.B * dv.H + blockIdx.x;
+  const int D = dv.D, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int recent_start = max(0, dv.t0[lbh] - dv.n_w + 1);
+  const int pool_lo = dv.n_sink, pool_hi = max(pool_lo, recent_start / dv.n_b);
+  extern __shared__ double qsum_sm[];
+  for (int i = threadIdx.x; i < D; i += blockDim.x) qsum_sm[i] = dv.qsum_buf[(size_t)lbh * D + i];
+  __syncthreads();
+  for (int p = pool_lo + warp; p < pool_hi; p += nwarps) {
+    const double v = row_dot64(dv.kc + ((size_t)lbh * dv.NB + p) * D, qsum_sm, D);
+    if (lane == 0) dv.s_q[(size_t)lbh * dv.NB + p] = v;
+  }
+}
+
+cudaError_t launch_screen_build(const Dev& dv, int seq_begin, int seq_count, cudaStream_t st) {
+  screen_build_kernel<<<dv.L * seq_count * dv.H, 256, 0, st>>>(dv, seq_begin, seq_count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_score_readback(const Dev& dv, int layer, cudaStream_t st) {
+  score_readback_kernel<<<dv.B * dv.H, 256, dv.D * sizeof(double), st>>>(dv, layer);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------------------------------

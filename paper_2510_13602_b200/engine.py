@@ -13,6 +13,7 @@ HBM on a side stream), K4+K5 block-sparse attention + append.  Q/K/V are supplie
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -37,6 +38,7 @@ class ResidencyStats:
     steps: int = 0
     new_blocks: int = 0
     evictions: int = 0
+    candidates: int = 0   # pool rows rescored in f64 by the screened selector
 
     @property
     def hit_rate(self) -> float:
@@ -83,14 +85,16 @@ class NosaEngine:
     def __init__(self, config: AttentionConfig, *, batch: int, max_tokens: int, fast_slots: int,
                  w1, w2, layers: int = 1, variant: str = "ed-dma", dtype: str = "bf16",
                  device: int = 0, residency: str = "per-sequence", attend_chunk: int = 0,
-                 attend_layers: int = 0):
+                 attend_layers: int = 0, exact_scan: bool = False):
         """residency "per-sequence": one manager per (layer, sequence, head) with `fast_slots`
         slots; "shared": one pool of batch*fast_slots slots per (layer, head)
         shared by the batch and planned in batch order, the reference simulator's residency.
         attend_chunk: KV blocks per split-K attention work item (1..8, 0 = chosen from the
         batch size); outputs are bit-identical across runs with the same value.
         attend_layers: layers per persistent attention launch in the pipelined schedule (0 =
-        4 when every block fits in HBM, else 1); results do not depend on it."""
+        4 when every block fits in HBM, else 1); results do not depend on it.
+        exact_scan: score the whole pool in f64 instead of the screened selector (bf16 pre-scan,
+        f64 rescoring of the candidates); both pick the same blocks."""
         if variant not in _lib.VARIANT:
             raise ValueError(f"variant must be one of {tuple(_lib.VARIANT)} (retaining needs hidden states)")
         if residency not in _lib.RESIDENCY:
@@ -112,6 +116,7 @@ class NosaEngine:
         c.residency = _lib.RESIDENCY[residency]
         c.attend_chunk = attend_chunk
         c.attend_layers = attend_layers
+        c.exact_scan = int(exact_scan)
         self._cfg = c
         msg = ctypes.create_string_buffer(512)
         if _lib.lib.nosa_config_validate(ctypes.byref(c), msg, 512) != _lib.NOSA_OK:
@@ -131,6 +136,7 @@ class NosaEngine:
         self.geometry: list[BlockGeometry | None] = [None] * batch
         self._t = np.zeros((layers, batch), dtype=np.int64)
         self._graph_io = None
+        self.screened = not exact_scan and config.d_head in (64, 128) and not os.environ.get("NOSA_EXACT_SCAN")
 
     # ------------------------------------------------------------------ plumbing
     def _call(self, fn, *args):
@@ -412,7 +418,8 @@ class NosaEngine:
         st = _lib.NosaStats()
         self._call(_lib.lib.nosa_read_stats, layers.start, layers.stop, seqs.start, seqs.stop, ctypes.byref(st))
         return ResidencyStats(hits=st.hits, misses=st.misses, bytes_up=st.bytes_up, bytes_down=st.bytes_down,
-                              steps=st.steps, new_blocks=st.new_blocks, evictions=st.evictions)
+                              steps=st.steps, new_blocks=st.new_blocks, evictions=st.evictions,
+                              candidates=st.candidates)
 
     def reset_stats(self):
         with torch.cuda.device(self.device):

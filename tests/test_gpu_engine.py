@@ -224,6 +224,37 @@ def test_resident_prefill(dtype):
               resident=True)
 
 
+@pytest.mark.parametrize("selector", ["nosa", "infllmv2"])
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_screened_selection_equals_full_f64_scan(selector, dtype):
+    """The screened selector (bf16 pre-scan + f64 rescoring of the candidates) picks exactly the
+    blocks a full f64 scan of the pool picks, so every later quantity is bitwise identical."""
+    cfg = ONE_B_SMALL
+    w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, 4)
+    K, V = workload.prefix_kv(4, 6, cfg.n_kv_head, 6000, cfg.d_head)
+    K, V = K.reshape(2, 3, cfg.n_kv_head, 6000, cfg.d_head), V.reshape(2, 3, cfg.n_kv_head, 6000, cfg.d_head)
+    runs = []
+    for exact in (True, False):
+        eng = NosaEngine(cfg, batch=3, layers=2, max_tokens=6100, fast_slots=75, w1=w1, w2=w2, dtype=dtype,
+                         exact_scan=exact)
+        eng.prefill(torch.from_numpy(K), torch.from_numpy(V))
+        eng.start_run()
+        stream = workload.QueryStream(4, 2, 3, cfg.n_head, cfg.n_kv_head, cfg.d_head, 0.2)
+        outs, sels = [], []
+        for _ in range(25):
+            outs.append(eng.step(*stream.next(), selector=selector).cpu().numpy())
+            sels.append([eng.raw_selection(l)[:4] for l in range(2)])
+        st = eng.residency_stats()
+        runs.append((np.stack(outs), sels, (st.hits, st.misses, st.evictions)))
+        eng.close()
+    np.testing.assert_array_equal(runs[0][0], runs[1][0])
+    assert runs[0][2] == runs[1][2]
+    for a, b in zip(runs[0][1], runs[1][1]):
+        for la, lb in zip(a, b):
+            for x, y in zip(la, lb):
+                np.testing.assert_array_equal(x, y)
+
+
 def test_resident_multilayer_batched_attention():
     """All blocks in HBM: attention runs 4 layers per persistent launch (6 layers = 4 + 2)."""
     a = _run_pair(ONE_B_SMALL, batch=2, t0s=[3000, 2900], steps=8, fast_slots=48, seed=17, rho=0.3, layers=6,
