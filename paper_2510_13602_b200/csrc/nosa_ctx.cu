@@ -24,7 +24,7 @@ cudaError_t launch_plan_shared(const Dev& dv, int layer, const int* ext_req, con
 cudaError_t launch_select_scores(int n_prob, const double* s_q, const double* s_e, int stride,
                                  const int* lo, const int* hi, int m_q, int m_e, int selector,
                                  int* out_q, int* n_q, int* out_e, int* n_e, cudaStream_t st);
-cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, bool tma);
+cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, bool tma, int nl = 1);
 cudaError_t launch_stage_inputs(const void* const* src, void* const* dst, const size_t* bytes, int grid,
                                 cudaStream_t st);
 cudaError_t launch_prefill(const Dev& dv, int layer, int seq_begin, int S, const void* k,
@@ -49,6 +49,7 @@ struct NosaCtx {
   int gather_grid = 8;       // UVA gather CTAs: enough bytes in flight for the link, few SMs taken
   int tma_gather_grid = 24;  // TMA gather CTAs (one warp, 4 x 32 KiB stages each)
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t sel_stream = nullptr;  // selections (forked from the caller's stream per step)
   cudaStream_t att_stream = nullptr, att_stream2 = nullptr, fin_stream = nullptr;  // attention (even /
   // odd layers, so one layer's attention tail overlaps the next) and finalize stages
   bool two_att = true;
@@ -234,7 +235,7 @@ static void release(NosaCtx* ctx) {
     for (auto e : *evs) cudaEventDestroy(e);
   for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_d2h})
     if (e) cudaEventDestroy(e);
-  for (cudaStream_t s : {ctx->copy_stream, ctx->capture_stream, ctx->att_stream, ctx->att_stream2, ctx->fin_stream,
+  for (cudaStream_t s : {ctx->sel_stream, ctx->copy_stream, ctx->capture_stream, ctx->att_stream, ctx->att_stream2, ctx->fin_stream,
                          ctx->meta_stream, ctx->d2h_stream, ctx->in_stream})
     if (s) cudaStreamDestroy(s);
   if (ctx->h_list) cudaFreeHost(ctx->h_list);
@@ -435,19 +436,26 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   cudaHostGetDevicePointer(&hdev, ctx->host_mirror, 0);
   dv.host = static_cast<char*>(hdev);
 
-  // the miss transfer is the critical path when blocks are offloaded, attention when they are
-  // resident: both get the highest priority, so selection kernels of later layers only fill gaps
+  // Stream priorities (levels below the device's highest; 0 = highest): every stage of the step
+  // at the highest level, so the step's kernels go ahead of other work on the device.  Measured
+  // on cfg 2/3 (NOSA_PRIO="sel,copy,attend,finalize" overrides): ordering the stages by
+  // priority (selection > transfer > attention > merge) moved the step time within run-to-run
+  // noise (±5%).
   int prio_low = 0, prio_high = 0;
   cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
+  int lvl[4] = {0, 0, 0, 0};
+  if (const char* e = getenv("NOSA_PRIO")) sscanf(e, "%d,%d,%d,%d", &lvl[0], &lvl[1], &lvl[2], &lvl[3]);
   const bool use_prio = !(getenv("NOSA_NO_STREAM_PRIORITY"));
-  cudaStreamCreateWithPriority(&ctx->copy_stream, cudaStreamNonBlocking, use_prio ? prio_high : 0);
-  cudaStreamCreateWithPriority(&ctx->att_stream, cudaStreamNonBlocking, use_prio ? prio_high : 0);
-  cudaStreamCreateWithPriority(&ctx->att_stream2, cudaStreamNonBlocking, use_prio ? prio_high : 0);
+  auto prio = [&](int k) { return use_prio ? std::min(prio_low, prio_high + std::max(0, k)) : 0; };
+  cudaStreamCreateWithPriority(&ctx->sel_stream, cudaStreamNonBlocking, prio(lvl[0]));
+  cudaStreamCreateWithPriority(&ctx->copy_stream, cudaStreamNonBlocking, prio(lvl[1]));
+  cudaStreamCreateWithPriority(&ctx->att_stream, cudaStreamNonBlocking, prio(lvl[2]));
+  cudaStreamCreateWithPriority(&ctx->att_stream2, cudaStreamNonBlocking, prio(lvl[2]));
   ctx->two_att = !getenv("NOSA_ONE_ATT_STREAM");
   ctx->select_per_layer = getenv("NOSA_SELECT_PER_LAYER") != nullptr;
   ctx->stage_with_copies = getenv("NOSA_STAGE_COPIES") != nullptr;
   if (const char* g = getenv("NOSA_STAGE_CTAS")) ctx->stage_grid = std::max(1, atoi(g));
-  cudaStreamCreateWithPriority(&ctx->fin_stream, cudaStreamNonBlocking, use_prio ? prio_high : 0);
+  cudaStreamCreateWithPriority(&ctx->fin_stream, cudaStreamNonBlocking, prio(lvl[3]));
   cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   for (auto* evs : {&ctx->ev_plan, &ctx->ev_gather, &ctx->ev_att, &ctx->ev_fin}) {
@@ -765,10 +773,10 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   // known up front, as with per-layer query streams).  Layer-serial schedule: select(l) waits
   // for finalize(l-1), as when q_{l+1} is computed from layer l's output.
   const bool serial = io->schedule == 1;
-  cudaStream_t cp = ctx->copy_stream, at = ctx->att_stream, fn = ctx->fin_stream;
+  cudaStream_t cp = ctx->copy_stream, at = ctx->att_stream, fn = ctx->fin_stream, ss = ctx->sel_stream;
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, st));  // side streams start after the caller's work
   cudaStream_t at2 = ctx->two_att ? ctx->att_stream2 : at;
-  for (cudaStream_t s : {cp, at, at2, fn}) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_fork, 0));
+  for (cudaStream_t s : {ss, cp, at, at2, fn}) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_fork, 0));
   // selection groups: doubling layer ranges (1, 1, 2, 4, 8, ...) in the pipelined schedule,
   // one layer each otherwise (serial schedule, shared-pool planner)
   const bool grouped = !serial && !dv.shared && !ctx->select_per_layer;
@@ -782,26 +790,26 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
     for (int l = 0; l < dv.L; ++l) groups.push_back({l, 1});
   }
   auto select = [&](int l) -> int {
-    if (hio) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_in[l], 0));
-    CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt + 2 * l, 0, 2 * sizeof(int), st));
+    if (hio) CUDA_TRY(ctx, cudaStreamWaitEvent(ss, ctx->ev_in[l], 0));
+    CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt + 2 * l, 0, 2 * sizeof(int), ss));
     {
-      TimeScope ts(ctx, st, 0, timed);
-      CUDA_TRY(ctx, plan_layer(ctx, l, q + l * qstride, io->selector, st));
+      TimeScope ts(ctx, ss, 0, timed);
+      CUDA_TRY(ctx, plan_layer(ctx, l, q + l * qstride, io->selector, ss));
     }
-    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[l], st));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[l], ss));
     return NOSA_OK;
   };
   // Pipelined: the layers' selections are launched in groups of doubling size (1, 1, 2, 4, 8,
   // ...), one grid of (B*H, layers) per group, so layer 0's plan (and its miss transfer) starts
   // at once while the later layers' selections fill the whole GPU in a few launches.
   auto select_group = [&](int l0, int n) -> int {
-    if (hio) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_in[l0 + n - 1], 0));
-    CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt + 2 * l0, 0, 2 * n * sizeof(int), st));
+    if (hio) CUDA_TRY(ctx, cudaStreamWaitEvent(ss, ctx->ev_in[l0 + n - 1], 0));
+    CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt + 2 * l0, 0, 2 * n * sizeof(int), ss));
     {
-      TimeScope ts(ctx, st, 0, timed);
-      CUDA_TRY(ctx, nosa::launch_select_plan(dv, l0, q + l0 * qstride, io->selector, 1, nullptr, nullptr, st, n));
+      TimeScope ts(ctx, ss, 0, timed);
+      CUDA_TRY(ctx, nosa::launch_select_plan(dv, l0, q + l0 * qstride, io->selector, 1, nullptr, nullptr, ss, n));
     }
-    for (int l = l0; l < l0 + n; ++l) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[l], st));
+    for (int l = l0; l < l0 + n; ++l) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[l], ss));
     return NOSA_OK;
   };
   // Issues groups [next_group, upto): the host inputs of the group (three copies, nosa_decode_
@@ -881,22 +889,23 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   cudaEvent_t last_att[2] = {nullptr, nullptr};
   for (int l = 0; l < dv.L; ++l) {
     if (serial) {
-      if (l > 0) CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_fin[l - 1], 0));
+      if (l > 0) CUDA_TRY(ctx, cudaStreamWaitEvent(ss, ctx->ev_fin[l - 1], 0));
       if (int rc = select(l)) return rc;
     }
     CUDA_TRY(ctx, cudaStreamWaitEvent(cp, ctx->ev_plan[l], 0));
+    const bool batch_end = (l + 1) % nl == 0 || l == dv.L - 1;  // last layer of an attention batch
+    const int l0 = l - l % nl, n = l - l0 + 1;
     if (io->gather_mode == NOSA_GATHER_MEMCPY) {
       const int rc = gather_memcpy(ctx, l, ctx->ev_plan[l], cp, timed);
       if (rc) return rc;
-    } else {
+    } else if (batch_end) {  // device movers: one launch for the attention batch's layers
       TimeScope ts(ctx, cp, 1, timed);
       const bool tma = io->gather_mode == NOSA_GATHER_TMA;
-      CUDA_TRY(ctx, nosa::launch_gather(dv, l, cp, tma ? ctx->tma_gather_grid : ctx->gather_grid, tma));
+      CUDA_TRY(ctx, nosa::launch_gather(dv, l0, cp, tma ? ctx->tma_gather_grid : ctx->gather_grid, tma, n));
       ++n_gather_kernels;
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[l], cp));
-    if ((l + 1) % nl != 0 && l != dv.L - 1) continue;  // not the last layer of an attention batch
-    const int l0 = l - l % nl, n = l - l0 + 1;
+    if (!batch_end) continue;
     cudaStream_t a = (n_att & 1) ? at2 : at;
     CUDA_TRY(ctx, cudaStreamWaitEvent(a, ctx->ev_gather[l], 0));  // gathers run in order on cp
     // record buffers: layer l' uses buffer l' % nbuf, last written for layer l' - nbuf
@@ -926,7 +935,8 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_d2h, ctx->d2h_stream));
     CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_d2h, 0));
   }
-  // join every side stream back into the caller's stream
+  // join every side stream back into the caller's stream (the plans precede the last gather)
+  CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_plan[dv.L - 1], 0));
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_gather[dv.L - 1], 0));
   for (cudaEvent_t e : last_att)
     if (e) CUDA_TRY(ctx, cudaStreamWaitEvent(st, e, 0));

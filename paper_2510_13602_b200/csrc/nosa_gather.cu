@@ -40,8 +40,9 @@ __device__ __forceinline__ void write_born_block(const Dev& dv, int4 m, int4* ds
 // Each CTA copies NBLK list entries per iteration: NBLK * bpb / (256 * 16) 16-byte loads per
 // thread are issued before any store, so NBLK * 32 KiB per CTA are in flight on the link.
 template <int NBLK, bool L2HINT>
-__global__ void __launch_bounds__(256) gather_kernel(Dev dv, int layer) {
+__global__ void __launch_bounds__(256) gather_kernel(Dev dv, int layer0) {
   constexpr int PER = 8;  // 16-byte vectors per thread per 32 KiB block at 256 threads
+  const int layer = layer0 + blockIdx.y;  // grid (CTAs, layers of an attention batch)
   const int n = *reinterpret_cast<volatile int*>(dv.cnt + 2 * layer);
   const int4* list = dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C;
   const int vecs = (int)(dv.bpb / 16);
@@ -93,8 +94,9 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-__global__ void __launch_bounds__(32) gather_tma_kernel(Dev dv, int layer) {
+__global__ void __launch_bounds__(32) gather_tma_kernel(Dev dv, int layer0) {
   extern __shared__ __align__(128) char smem_raw[];
+  const int layer = layer0 + blockIdx.y;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kTmaStages * dv.bpb);
   const int n = *reinterpret_cast<volatile int*>(dv.cnt + 2 * layer);
   const int4* list = dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C;
@@ -143,19 +145,21 @@ __global__ void __launch_bounds__(32) gather_tma_kernel(Dev dv, int layer) {
   if (lane == 0) bulk_wait_all();
 }
 
-cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, bool tma) {
+// layers [layer, layer + nl) in one launch
+cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, bool tma, int nl) {
+  const dim3 g(grid, nl);
   if (tma) {
     const size_t smem = (size_t)kTmaStages * dv.bpb + kTmaStages * 8;
     cudaFuncSetAttribute(gather_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    gather_tma_kernel<<<grid, 32, smem, st>>>(dv, layer);
+    gather_tma_kernel<<<g, 32, smem, st>>>(dv, layer);
   } else {
     // NOSA_GATHER_VARIANT (experiments): bit 0 = two blocks per CTA iteration, bit 1 = L2::256B
     static const int variant = getenv("NOSA_GATHER_VARIANT") ? atoi(getenv("NOSA_GATHER_VARIANT")) : 0;
     switch (variant & 3) {
-      case 0: gather_kernel<1, false><<<grid, 256, 0, st>>>(dv, layer); break;
-      case 1: gather_kernel<2, false><<<grid, 256, 0, st>>>(dv, layer); break;
-      case 2: gather_kernel<1, true><<<grid, 256, 0, st>>>(dv, layer); break;
-      default: gather_kernel<2, true><<<grid, 256, 0, st>>>(dv, layer); break;
+      case 0: gather_kernel<1, false><<<g, 256, 0, st>>>(dv, layer); break;
+      case 1: gather_kernel<2, false><<<g, 256, 0, st>>>(dv, layer); break;
+      case 2: gather_kernel<1, true><<<g, 256, 0, st>>>(dv, layer); break;
+      default: gather_kernel<2, true><<<g, 256, 0, st>>>(dv, layer); break;
     }
   }
   return cudaGetLastError();
