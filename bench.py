@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--trace-out", default=None, help="write the device timeline of one instrumented step here")
+    ap.add_argument("--slow-tier", default="host",
+                    help="'host' (pinned host memory over PCIe) or 'peer' (another GPU's HBM over NVLink: "
+                         "device (local_rank + 1) %% GPUs on the node, the own device when alone = loopback)")
     ap.add_argument("--eager", action="store_true",
                     help="launch every kernel from the host instead of replaying the captured step graph")
     return ap.parse_args()
@@ -86,6 +89,17 @@ def workload_dims(args, world):
     shard = shard_batch(w["batch"], world, rank, bool(w.get("strong")))
     w["batch_local"], w["global_batch"] = shard.seq_count, shard.global_batch
     w["host_limited"] = False
+    if args.impl == "native" and args.slow_tier == "peer":  # slow tier + cache + K_c must fit in HBM
+        import torch
+        n_blocks = -(-(w["context"] + 256) // 64)
+        frac = 1.0 if w["cache"] == "resident" else 1.0 + w["cache"]
+        per_seq = w["layers"] * 2 * n_blocks * (2 * 64 * 128 * 2 * frac + 128 * 10)
+        budget = int(0.55 * torch.cuda.get_device_properties(0).total_memory)
+        if per_seq * w["batch_local"] > budget:
+            w["batch_local"] = max(1, budget // int(per_seq))
+            w["global_batch"] = w["batch_local"] * world
+            w["host_limited"] = True
+        return w
     if args.impl == "native":  # the pinned slow tier of every rank on this node must fit in RAM
         local = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
         n_blocks = -(-(w["context"] + 256) // 64)
@@ -160,8 +174,13 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ native arm
-def measure_link_gbs(torch, device):
-    x = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+def measure_link_gbs(torch, device, src_device=None):
+    """Best of 10 1 GiB copies into `device`: from pinned host memory, or from `src_device`'s HBM
+    (the peer slow tier; the same device = a local HBM copy)."""
+    if src_device is None:
+        x = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+    else:
+        x = torch.empty(1 << 30, dtype=torch.uint8, device=torch.device("cuda", src_device))
     y = torch.empty(1 << 30, dtype=torch.uint8, device=device)
     for _ in range(2):
         y.copy_(x, non_blocking=True)
@@ -194,8 +213,9 @@ def run_native(args, rank, world, local_rank):
     device = torch.device("cuda", local_rank)
     torch.cuda.set_device(device)
     w = workload_dims(args, world)
-    if args.gather == "auto":  # measured: the copy engine moves offloaded misses fastest
-        args.gather = "uva" if w["cache"] == "resident" else "memcpy"
+    if args.gather == "auto":  # measured: the copy engine moves offloaded misses fastest over PCIe;
+        # from a peer's HBM the SM gather is 30x faster than device-to-device copy-engine batches
+        args.gather = "uva" if (w["cache"] == "resident" or args.slow_tier == "peer") else "memcpy"
     cfg = attention_config(w["shape"])
     L, B, ctx_len = w["layers"], w["batch_local"], w["context"]
     total_steps = args.burn_in + args.warmup + args.steps * (2 if args.no_e2e else 3)
@@ -203,12 +223,19 @@ def run_native(args, rank, world, local_rank):
     nblk = -(-max_tokens // cfg.n_b)
     fast = nblk if w["cache"] == "resident" else int(w["cache"] * nblk)
     dtype = torch.bfloat16
-    link_gbs = measure_link_gbs(torch, device)
+    peer_dev = None
+    if args.slow_tier == "peer":  # the slow tier in another GPU's HBM (alone on the box: loopback)
+        ngpu = torch.cuda.device_count()
+        peer_dev = (local_rank + 1) % ngpu if ngpu > 1 else local_rank
+        slow_tier = f"peer:{peer_dev}"
+    else:
+        slow_tier = "host"
+    link_gbs = measure_link_gbs(torch, device, peer_dev)
 
     w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, args.seed)
     t_setup = time.time()
     eng = NosaEngine(cfg, batch=B, layers=L, max_tokens=max_tokens, fast_slots=fast, w1=w1, w2=w2, dtype="bf16",
-                     device=local_rank)
+                     device=local_rank, slow_tier=slow_tier)
     t_alloc = time.time() - t_setup
     seed_base = rank_seed(args.seed, rank)
     for l in range(L):
@@ -387,10 +414,11 @@ def run_native(args, rank, world, local_rank):
     g = kern["gather"]
     gather_name = {"uva": "gather_kernel (K3, UVA zero-copy SM loads)", "tma": "gather_tma_kernel (K3, TMA bulk)",
                    "memcpy": "cudaMemcpyBatchAsync (K3, copy engine)"}[args.gather]
-    link_roofline = {"bound": "pcie-h2d", "kernel": gather_name,
+    link_roofline = {"bound": "pcie-h2d" if peer_dev is None else "peer-hbm", "kernel": gather_name,
                      "achieved": round(g["gbs"], 2) if g["gbs"] else 0.0, "peak": round(link_gbs, 2), "unit": "GB/s",
                      "frac": round(g["gbs"] / link_gbs, 4) if g["gbs"] else 0.0,
-                     "peak_kind": "measured pinned 1 GiB H2D cudaMemcpyAsync, best of 10"}
+                     "peak_kind": ("measured pinned 1 GiB H2D cudaMemcpyAsync, best of 10" if peer_dev is None else
+                                   f"measured 1 GiB device {peer_dev} -> {local_rank} cudaMemcpyAsync, best of 10")}
     step_roofline = {"definition": "t_roof = max(HBM bytes / 8 TB/s, H2D miss bytes / measured link GB/s)",
                      "hbm_bytes_per_step": int(hbm_step), "h2d_bytes_per_step": int(h2d_step),
                      "t_roof_ms": round(t_roof * 1e3, 4), "t_step_ms": round(step_ms, 4),
@@ -421,6 +449,8 @@ def run_native(args, rank, world, local_rank):
                                         "around every kernel on its own stream (event nodes in the graph); "
                                         "value comes from the uninstrumented region",
                        "host_memory_limited_batch": w["host_limited"],
+                       "slow_tier": slow_tier + (" (loopback: the own HBM stands in for a peer)"
+                                                 if peer_dev == local_rank else ""),
                        "l2": "no flush needed: attended KV per layer-step exceeds the 126 MB L2"},
             "h2d_miss_gbs": round(h2d_step / (step_ms * 1e-3) / 1e9, 3),
             "hit_rate": round(st.hit_rate, 4),

@@ -74,6 +74,9 @@ typedef struct NosaConfig {
                             0 = auto (4 when every block fits in HBM, else 1)               */
   int32_t exact_scan;    /* 0: screened selection (bf16 pre-scan of the pool, f64 rescoring of
                             the candidates: the same picks as a full f64 scan); 1: full f64  */
+  int32_t slow_tier_device; /* -1: slow tier in pinned host memory (PCIe); >= 0: in that GPU's
+                               HBM, read by peer access over NVLink (the context's own device =
+                               loopback, for single-GPU testing)                                */
 } NosaConfig;
 
 /* residency contract */

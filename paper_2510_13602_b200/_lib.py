@@ -37,7 +37,7 @@ class NosaConfig(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int32) for name in (
         "n", "d", "n_head", "n_kv_head", "d_head", "n_b", "n_s", "n_w", "k", "k_q", "k_e",
         "accounting", "batch", "layers", "max_tokens", "fast_slots", "dtype", "variant", "residency",
-        "attend_chunk", "attend_layers", "exact_scan")]
+        "attend_chunk", "attend_layers", "exact_scan", "slow_tier_device")]
 
 
 class NosaStats(ctypes.Structure):

@@ -58,6 +58,7 @@ struct NosaCtx {
   char* host_mirror = nullptr;
   size_t host_bytes = 0;
   bool host_registered = false;  // mmap + cudaHostRegister (else cudaHostAlloc)
+  int mirror_device = -1;        // >= 0: the slow tier lives in this GPU's HBM (peer tier)
   std::vector<void*> dev_allocs;
   size_t dev_bytes = 0;
   char* staging = nullptr;
@@ -191,6 +192,7 @@ extern "C" int nosa_config_validate(const NosaConfig* c, char* msg, int msg_len)
   if (c->attend_chunk < 0 || c->attend_chunk > 8) return bad("attend_chunk must be in 0..8 (0 = auto)");
   if (c->attend_layers < 0) return bad("attend_layers must be >= 0 (0 = auto)");
   if (c->exact_scan < 0 || c->exact_scan > 1) return bad("exact_scan must be 0 or 1");
+  if (c->slow_tier_device < -1) return bad("slow_tier_device must be -1 (pinned host) or a device index");
   if (c->dtype != NOSA_DTYPE_BF16 && c->dtype != NOSA_DTYPE_FP32) return bad("dtype must be bf16 or fp32");
   if (c->variant < 0 || c->variant > 2) return bad("variant must be ed-dma, s-dma or dma");
   if (c->residency != NOSA_RESIDENCY_PER_SEQUENCE && c->residency != NOSA_RESIDENCY_SHARED)
@@ -248,7 +250,11 @@ static void release(NosaCtx* ctx) {
   for (void* p : ctx->dev_allocs) cudaFree(p);
   if (ctx->staging) cudaFree(ctx->staging);
   if (ctx->io_buf) cudaFree(ctx->io_buf);
-  if (ctx->host_mirror) {
+  if (ctx->host_mirror && ctx->mirror_device >= 0) {
+    cudaSetDevice(ctx->mirror_device);
+    cudaFree(ctx->host_mirror);
+    cudaSetDevice(ctx->device);
+  } else if (ctx->host_mirror) {
     if (ctx->host_registered) {
       cudaHostUnregister(ctx->host_mirror);
       munmap(ctx->host_mirror, ctx->host_bytes);
@@ -403,12 +409,48 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
     cudaMemcpy(dv.ftop, top.data(), top.size() * sizeof(int), cudaMemcpyHostToDevice);
   }
 
-  // slow tier: pinned + mapped host mirror
+  // slow tier: pinned + mapped host mirror, or (slow_tier_device >= 0) a buffer in that GPU's
+  // HBM, read over NVLink by peer access; the same device = loopback
   ctx->host_bytes = LBH * dv.NB * (size_t)dv.bpb;
   const char* hmode = getenv("NOSA_HOST_ALLOC");
   const bool use_register = !(hmode && strcmp(hmode, "hostalloc") == 0);
   cudaError_t he = cudaErrorMemoryAllocation;
-  if (use_register) {
+  if (c.slow_tier_device >= 0) {
+    const int peer = c.slow_tier_device;
+    if (peer != device) {
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, device, peer);
+      if (!can) {
+        fail(ctx, NOSA_ERR_VALUE, "device %d cannot access device %d's memory (no peer path)", device, peer);
+        g_create_error = ctx->err;
+        release(ctx);
+        return NOSA_ERR_VALUE;
+      }
+      cudaError_t pe = cudaDeviceEnablePeerAccess(peer, 0);
+      if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) {
+        fail(ctx, NOSA_ERR_CUDA, "enable peer access %d -> %d: %s", device, peer, cudaGetErrorString(pe));
+        g_create_error = ctx->err;
+        release(ctx);
+        return NOSA_ERR_CUDA;
+      }
+      cudaGetLastError();
+      cudaSetDevice(peer);
+    }
+    he = cudaMalloc(reinterpret_cast<void**>(&ctx->host_mirror), std::max<size_t>(ctx->host_bytes, 16));
+    cudaSetDevice(device);
+    if (he != cudaSuccess) {
+      ctx->host_mirror = nullptr;
+      fail(ctx, NOSA_ERR_CUDA, "slow tier of %zu bytes on device %d: %s", ctx->host_bytes, peer, cudaGetErrorString(he));
+      g_create_error = ctx->err;
+      release(ctx);
+      return NOSA_ERR_CUDA;
+    }
+    ctx->mirror_device = peer;
+    // over NVLink the SM mover is bounded by loads in flight, not by a 55 GB/s link: one CTA
+    // per SM (measured on the loopback tier: 8 CTAs 117 GB/s, 64 CTAs 258 GB/s; the copy
+    // engine moves 32 KiB device-to-device blocks at 8 GB/s)
+    if (!getenv("NOSA_GATHER_CTAS")) ctx->gather_grid = ctx->num_sms;
+  } else if (use_register) {
     void* p = mmap(nullptr, ctx->host_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
     if (p != MAP_FAILED) {
       madvise(p, ctx->host_bytes, MADV_HUGEPAGE);
@@ -432,8 +474,8 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
       return NOSA_ERR_CUDA;
     }
   }
-  void* hdev = nullptr;
-  cudaHostGetDevicePointer(&hdev, ctx->host_mirror, 0);
+  void* hdev = ctx->host_mirror;
+  if (ctx->mirror_device < 0) cudaHostGetDevicePointer(&hdev, ctx->host_mirror, 0);
   dv.host = static_cast<char*>(hdev);
 
   // Stream priorities (levels below the device's highest; 0 = highest): every stage of the step
@@ -533,7 +575,7 @@ extern "C" int nosa_prefill(NosaCtx* ctx, int layer, int seq_begin, int seq_coun
   ctx->launches += 3;
   const size_t lbh0 = ((size_t)layer * dv.B + seq_begin) * dv.H;
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_mirror + lbh0 * dv.NB * (size_t)dv.bpb, ctx->staging, need,
-                                cudaMemcpyDeviceToHost, S(stream)));
+                                cudaMemcpyDefault, S(stream)));  // host, or a peer GPU's HBM
   return NOSA_OK;
 }
 
@@ -648,7 +690,8 @@ static int gather_memcpy(NosaCtx* ctx, int layer, cudaEvent_t plan_done, cudaStr
   }
   cudaMemcpyAttributes attr{};
   attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.srcLocHint.type = cudaMemLocationTypeHost;
+  attr.srcLocHint.type = ctx->mirror_device >= 0 ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
+  attr.srcLocHint.id = ctx->mirror_device >= 0 ? ctx->mirror_device : 0;
   attr.dstLocHint.type = cudaMemLocationTypeDevice;
   attr.dstLocHint.id = ctx->device;
   size_t idx0 = 0, fail_idx = 0;
@@ -659,7 +702,7 @@ static int gather_memcpy(NosaCtx* ctx, int layer, cudaEvent_t plan_done, cudaStr
     cudaGetLastError();
     ctx->batch_fallbacks += 1;
     for (int i = 0; i < n; ++i)
-      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b_dst[i], ctx->b_src[i], ctx->b_size[i], cudaMemcpyHostToDevice, copy_st));
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b_dst[i], ctx->b_src[i], ctx->b_size[i], cudaMemcpyDefault, copy_st));
   }
   return NOSA_OK;
 }

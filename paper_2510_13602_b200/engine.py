@@ -85,7 +85,7 @@ class NosaEngine:
     def __init__(self, config: AttentionConfig, *, batch: int, max_tokens: int, fast_slots: int,
                  w1, w2, layers: int = 1, variant: str = "ed-dma", dtype: str = "bf16",
                  device: int = 0, residency: str = "per-sequence", attend_chunk: int = 0,
-                 attend_layers: int = 0, exact_scan: bool = False):
+                 attend_layers: int = 0, exact_scan: bool = False, slow_tier: str = "host"):
         """residency "per-sequence": one manager per (layer, sequence, head) with `fast_slots`
         slots; "shared": one pool of batch*fast_slots slots per (layer, head)
         shared by the batch and planned in batch order, the reference simulator's residency.
@@ -94,7 +94,9 @@ class NosaEngine:
         attend_layers: layers per persistent attention launch in the pipelined schedule (0 =
         4 when every block fits in HBM, else 1); results do not depend on it.
         exact_scan: score the whole pool in f64 instead of the screened selector (bf16 pre-scan,
-        f64 rescoring of the candidates); both pick the same blocks."""
+        f64 rescoring of the candidates); both pick the same blocks.
+        slow_tier: "host" (pinned host memory over PCIe, the reference's SLOW tier) or
+        "peer:<device>" (that GPU's HBM over NVLink; the engine's own device = loopback)."""
         if variant not in _lib.VARIANT:
             raise ValueError(f"variant must be one of {tuple(_lib.VARIANT)} (retaining needs hidden states)")
         if residency not in _lib.RESIDENCY:
@@ -117,6 +119,13 @@ class NosaEngine:
         c.attend_chunk = attend_chunk
         c.attend_layers = attend_layers
         c.exact_scan = int(exact_scan)
+        if slow_tier == "host":
+            c.slow_tier_device = -1
+        elif slow_tier.startswith("peer:") and slow_tier[5:].isdigit():
+            c.slow_tier_device = int(slow_tier[5:])
+        else:
+            raise ValueError(f"slow_tier must be 'host' or 'peer:<device>', got {slow_tier!r}")
+        self.slow_tier = slow_tier
         self._cfg = c
         msg = ctypes.create_string_buffer(512)
         if _lib.lib.nosa_config_validate(ctypes.byref(c), msg, 512) != _lib.NOSA_OK:

@@ -73,7 +73,7 @@ def test_engine_vs_reference_golden(golden, name, dtype):
 
 def _run_pair(cfg, *, batch, t0s, steps, fast_slots, seed, rho, selector="nosa", dtype="bf16", layers=1,
               variant="ed-dma", check_residency=True, gather="uva", schedule="pipelined", resident=False,
-              shared=False, attend_chunk=0):
+              shared=False, attend_chunk=0, slow_tier="host"):
     """GPU engine and oracle on identical inputs; returns the worst relative output error."""
     w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, seed)
     if variant == "dma":
@@ -82,7 +82,7 @@ def _run_pair(cfg, *, batch, t0s, steps, fast_slots, seed, rho, selector="nosa",
     cap = tmax + steps + 1
     eng = NosaEngine(cfg, batch=batch, layers=layers, max_tokens=cap, fast_slots=fast_slots, w1=w1, w2=w2,
                      dtype=dtype, variant=variant, residency="shared" if shared else "per-sequence",
-                     attend_chunk=attend_chunk)
+                     attend_chunk=attend_chunk, slow_tier=slow_tier)
     orc = oracle_for(cfg, batch, layers, cap, fast_slots, w1, w2, variant, shared=shared)
     K, V = workload.prefix_kv(seed, batch * layers, cfg.n_kv_head, tmax, cfg.d_head)
     K = K.reshape(layers, batch, cfg.n_kv_head, tmax, cfg.d_head)
@@ -253,6 +253,15 @@ def test_screened_selection_equals_full_f64_scan(selector, dtype):
         for la, lb in zip(a, b):
             for x, y in zip(la, lb):
                 np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("gather", ["memcpy", "uva", "tma"])
+def test_peer_slow_tier_loopback(gather):
+    """The slow tier in GPU memory (SURVEY §8f row 4: misses served from a peer's HBM over NVLink);
+    on one GPU the peer is the engine's own device.  Same selections, residency and outputs."""
+    a = _run_pair(ONE_B_SMALL, batch=2, t0s=[3000, 2600], steps=12, fast_slots=70, seed=19, rho=0.0, layers=2,
+                  gather=gather, slow_tier="peer:0")
+    assert a <= TOL["bf16"]
 
 
 def test_resident_multilayer_batched_attention():
