@@ -48,7 +48,7 @@ WORKLOADS = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
@@ -68,6 +68,7 @@ def parse():
     ap.add_argument("--slow-tier", default="host",
                     help="'host' (pinned host memory over PCIe) or 'peer' (another GPU's HBM over NVLink: "
                          "device (local_rank + 1) %% GPUs on the node, the own device when alone = loopback)")
+    ap.add_argument("--per-step", action="store_true", help="print each timed step's ms to stderr (diagnostics)")
     ap.add_argument("--eager", action="store_true",
                     help="launch every kernel from the host instead of replaying the captured step graph")
     return ap.parse_args()
@@ -137,6 +138,9 @@ class ClockSampler:
         self.index, self.rows, self.stop = index, [], threading.Event()
 
     def __enter__(self):
+        if os.environ.get("NOSA_BENCH_NO_CLOCKS"):  # diagnostics: no sampling thread
+            self.nvml = None
+            return self
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -158,7 +162,7 @@ class ClockSampler:
                 self.rows.append((sm, mask))
             except Exception:
                 pass
-            self.stop.wait(0.02)
+            self.stop.wait(float(os.environ.get("NOSA_CLOCK_POLL_S", "0.02")))
 
     def __exit__(self, *exc):
         self.stop.set()
@@ -219,7 +223,7 @@ def run_native(args, rank, world, local_rank):
     cfg = attention_config(w["shape"])
     L, B, ctx_len = w["layers"], w["batch_local"], w["context"]
     total_steps = args.burn_in + args.warmup + args.steps * (2 if args.no_e2e else 3)
-    max_tokens = ctx_len + total_steps + 2
+    max_tokens = ctx_len + total_steps + 4  # + the e2e graph warm-up and the traced step
     nblk = -(-max_tokens // cfg.n_b)
     fast = nblk if w["cache"] == "resident" else int(w["cache"] * nblk)
     dtype = torch.bfloat16
@@ -270,8 +274,13 @@ def run_native(args, rank, world, local_rank):
         gq, gk, gv = (torch.empty_like(x) for x in inputs[0])
         eng.capture(gq, gk, gv, out, selector=args.selector, gather=args.gather, schedule=args.schedule)
 
-    def run_steps(batch_inputs):
+    step_events = []
+
+    def run_steps(batch_inputs, per_step=False):
         for q, kn, vn in batch_inputs:
+            if per_step:
+                step_events.append(torch.cuda.Event(enable_timing=True))
+                step_events[-1].record()
             if use_graph:
                 gq.copy_(q); gk.copy_(kn); gv.copy_(vn)
                 eng.replay()
@@ -288,9 +297,12 @@ def run_native(args, rank, world, local_rank):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clocks:
         ev0.record()
-        run_steps(inputs[:args.steps])
+        run_steps(inputs[:args.steps], per_step=args.per_step)
         ev1.record()
         torch.cuda.synchronize(device)
+    if args.per_step:
+        marks = step_events + [ev1]
+        print("per-step ms:", [round(a.elapsed_time(b), 3) for a, b in zip(marks, marks[1:])], file=sys.stderr)
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
@@ -339,12 +351,17 @@ def run_native(args, rank, world, local_rank):
         torch.cuda.synchronize(device)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
+        if use_graph:  # the host-buffer step as a CUDA graph, re-pointed at each step's buffers;
+            # one untimed replay uploads the new executable graph
+            eng.capture_host(*host_in[0], host_out, selector=args.selector, gather=args.gather,
+                             schedule=args.schedule)
+            warm = tuple(pinned(x) for x in stream.next())
+            eng.replay_host(*warm, host_out)
+            torch.cuda.synchronize(device)
         for hq, hk, hv in host_in:
-            if use_graph:  # straight into the graph's input buffers
-                gq.copy_(hq, non_blocking=True); gk.copy_(hk, non_blocking=True); gv.copy_(hv, non_blocking=True)
-                eng.replay()
-                host_out.copy_(out, non_blocking=True)
-            else:  # the host-buffer C ABI call: per-layer H2D of inputs, D2H of outputs inside the step
+            if use_graph:
+                eng.replay_host(hq, hk, hv, host_out)
+            else:  # the host-buffer C ABI call: inputs staged and outputs copied back inside the step
                 eng.step_host(hq, hk, hv, selector=args.selector, out=host_out, gather=args.gather,
                               schedule=args.schedule, sync=False)
         e1.record()
@@ -354,7 +371,7 @@ def run_native(args, rank, world, local_rank):
         e2e = {"value": round(tokens / (e_ms * 1e-3), 2), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": host_out.numel() * 4,
                "ms_per_step": round(e_ms / args.steps, 4),
-               "api": ("NosaEngine.capture/replay (C ABI nosa_step_graph_launch)" if use_graph else
+               "api": ("NosaEngine.capture_host/replay_host (C ABI nosa_step_graph_launch_host)" if use_graph else
                        "NosaEngine.step_host (C ABI nosa_decode_step_host: per-layer H2D of q/k/v on the copy "
                        "stream, D2H of each layer's output overlapping later layers)") +
                       " on inputs in pinned host memory"}

@@ -211,6 +211,12 @@ int nosa_decode_step(NosaCtx* ctx, const NosaStepIO* io, void* stream);
  * point (cudaStreamSynchronize).  The context owns the device staging. */
 int nosa_decode_step_host(NosaCtx* ctx, const NosaHostStepIO* io, void* stream);
 
+/* CUDA-graph form of nosa_decode_step_host (device movers only: uva / tma): capture once on
+ * pinned host buffers; every launch may pass other pinned buffers of the same shapes (the
+ * graph's input-staging and output-copy nodes are re-pointed before the launch). */
+int nosa_step_graph_capture_host(NosaCtx* ctx, const NosaHostStepIO* io);
+int nosa_step_graph_launch_host(NosaCtx* ctx, const NosaHostStepIO* io, void* stream);
+
 /* CUDA-graph form of nosa_decode_step for fixed io pointers: capture once, replay per step. */
 int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io);
 int nosa_step_graph_launch(NosaCtx* ctx, void* stream);

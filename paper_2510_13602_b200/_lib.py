@@ -78,6 +78,8 @@ SIGNATURES = {
     "nosa_attend": (_I, [_P, _I, _P, _P, _P, _P, _P]),
     "nosa_decode_step": (_I, [_P, ctypes.POINTER(NosaStepIO), _P]),
     "nosa_decode_step_host": (_I, [_P, ctypes.POINTER(NosaHostStepIO), _P]),
+    "nosa_step_graph_capture_host": (_I, [_P, ctypes.POINTER(NosaHostStepIO)]),
+    "nosa_step_graph_launch_host": (_I, [_P, ctypes.POINTER(NosaHostStepIO), _P]),
     "nosa_step_graph_capture": (_I, [_P, ctypes.POINTER(NosaStepIO)]),
     "nosa_step_graph_launch": (_I, [_P, _P]),
     "nosa_select_scores": (_I, [_I, _P, _P, _I, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P]),

@@ -27,6 +27,8 @@ cudaError_t launch_select_scores(int n_prob, const double* s_q, const double* s_
 cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, bool tma, int nl = 1);
 cudaError_t launch_stage_inputs(const void* const* src, void* const* dst, const size_t* bytes, int grid,
                                 cudaStream_t st);
+const void* stage_inputs_kernel_fn();
+
 cudaError_t launch_prefill(const Dev& dv, int layer, int seq_begin, int S, const void* k,
                            const void* v, int t, char* staging, cudaStream_t st);
 cudaError_t launch_make_resident(const Dev& dv, int layer, int seq_begin, int S, int nblk, cudaStream_t st);
@@ -99,7 +101,17 @@ struct NosaCtx {
   bool stage_with_copies = false;   // NOSA_STAGE_COPIES: stage host inputs with cudaMemcpyAsync
   int attend_layers = 1;            // layers per attention launch (pipelined schedule)
   int step_kernels = 0;             // kernels launched by the last enqueued step
-  bool select_per_layer = false;  // NOSA_SELECT_PER_LAYER: one selection launch per layer
+  bool select_per_layer = false;
+  // graph of the host-buffer step and its host-address nodes (kind 0 = staging kernel, 1 = D2H copy)
+  cudaGraph_t graph_host = nullptr;
+  cudaGraphExec_t graph_exec_host = nullptr;
+  int graph_host_kernels = 0;
+  struct HostNode { cudaGraphNode_t node; int kind; };
+  std::vector<HostNode> host_nodes;
+  const char* cap_hs[3] = {nullptr, nullptr, nullptr};
+  const char* cur_hs[3] = {nullptr, nullptr, nullptr};
+  float* cap_out = nullptr;
+  float* cur_out = nullptr;  // NOSA_SELECT_PER_LAYER: one selection launch per layer
 };
 
 // brackets one launch with timing events when timing is enabled (eager steps only)
@@ -229,9 +241,9 @@ static void release(NosaCtx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
-  for (cudaGraphExec_t x : {ctx->graph_exec, ctx->graph_exec_timed})
+  for (cudaGraphExec_t x : {ctx->graph_exec, ctx->graph_exec_timed, ctx->graph_exec_host})
     if (x) cudaGraphExecDestroy(x);
-  for (cudaGraph_t x : {ctx->graph, ctx->graph_timed})
+  for (cudaGraph_t x : {ctx->graph, ctx->graph_timed, ctx->graph_host})
     if (x) cudaGraphDestroy(x);
   for (auto* evs : {&ctx->ev_plan, &ctx->ev_gather, &ctx->ev_att, &ctx->ev_fin, &ctx->ev_in})
     for (auto e : *evs) cudaEventDestroy(e);
@@ -412,8 +424,12 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   // slow tier: pinned + mapped host mirror, or (slow_tier_device >= 0) a buffer in that GPU's
   // HBM, read over NVLink by peer access; the same device = loopback
   ctx->host_bytes = LBH * dv.NB * (size_t)dv.bpb;
+  // cudaHostAlloc by default.  Measured: an mmap(MADV_HUGEPAGE) + cudaHostRegister mirror pins
+  // 2.4x faster at setup, but over a few dozen steps the GPU's writes and reads to it stall for
+  // milliseconds at random (cfg 3: 8.6 -> 10.5 ms/step, cfg 2 steps from 0.8 to 8 ms), so it is
+  // opt-in (NOSA_HOST_ALLOC=register).
   const char* hmode = getenv("NOSA_HOST_ALLOC");
-  const bool use_register = !(hmode && strcmp(hmode, "hostalloc") == 0);
+  const bool use_register = hmode && strcmp(hmode, "register") == 0;
   cudaError_t he = cudaErrorMemoryAllocation;
   if (c.slow_tier_device >= 0) {
     const int peer = c.slow_tier_device;
@@ -1000,8 +1016,9 @@ extern "C" int nosa_decode_step(NosaCtx* ctx, const NosaStepIO* io, void* stream
   return enqueue_step(ctx, io, S(stream), true);
 }
 
-extern "C" int nosa_decode_step_host(NosaCtx* ctx, const NosaHostStepIO* hio, void* stream) {
-  if (!ctx || !hio || !hio->q || !hio->k_new || !hio->v_new || !hio->out)
+// device staging of the host-buffer step: allocated on first use, `io` pointed at it
+static int host_staging(NosaCtx* ctx, const NosaHostStepIO* hio, NosaStepIO* io_out) {
+  if (!hio || !hio->q || !hio->k_new || !hio->v_new || !hio->out)
     return fail(ctx, NOSA_ERR_VALUE, "decode_step_host: NULL io");
   if (hio->selector != 0 && hio->selector != 1) return fail(ctx, NOSA_ERR_VALUE, "selector must be nosa or infllmv2");
   cudaSetDevice(ctx->device);
@@ -1020,7 +1037,8 @@ extern "C" int nosa_decode_step_host(NosaCtx* ctx, const NosaHostStepIO* hio, vo
     ctx->ev_in.resize(dv.L);
     for (int l = 0; l < dv.L; ++l) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_in[l], cudaEventDisableTiming));
   }
-  NosaStepIO io{};
+  NosaStepIO& io = *io_out;
+  io = NosaStepIO{};
   io.q = ctx->io_buf;
   io.k_new = ctx->io_buf + qb;
   io.v_new = ctx->io_buf + qb + kb;
@@ -1028,7 +1046,113 @@ extern "C" int nosa_decode_step_host(NosaCtx* ctx, const NosaHostStepIO* hio, vo
   io.selector = hio->selector;
   io.gather_mode = hio->gather_mode;
   io.schedule = hio->schedule;
+  return NOSA_OK;
+}
+
+extern "C" int nosa_decode_step_host(NosaCtx* ctx, const NosaHostStepIO* hio, void* stream) {
+  if (!ctx) return NOSA_ERR_VALUE;
+  NosaStepIO io;
+  if (int rc = host_staging(ctx, hio, &io)) return rc;
   return enqueue_step(ctx, &io, S(stream), true, hio);
+}
+
+// device-visible aliases of pinned host buffers (NULL when a buffer is pageable)
+static bool mapped_alias(const void* p, const char** out) {
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, p) != cudaSuccess || pa.type != cudaMemoryTypeHost || !pa.devicePointer) {
+    cudaGetLastError();
+    return false;
+  }
+  *out = static_cast<const char*>(pa.devicePointer);
+  return true;
+}
+
+// CUDA graph of the host-buffer step (device movers only).  The host buffers of a replay may
+// differ from the captured ones: the input-staging kernel nodes and the output copy nodes are
+// re-pointed in the executable graph before the launch (launches already in flight keep theirs).
+extern "C" int nosa_step_graph_capture_host(NosaCtx* ctx, const NosaHostStepIO* hio) {
+  if (!ctx) return NOSA_ERR_VALUE;
+  if (hio && hio->gather_mode == NOSA_GATHER_MEMCPY)
+    return fail(ctx, NOSA_ERR_VALUE, "graph capture needs a device-driven gather (uva or tma)");
+  NosaStepIO io;
+  if (int rc = host_staging(ctx, hio, &io)) return rc;
+  const char* hs[3];
+  if (ctx->stage_with_copies || !mapped_alias(hio->q, &hs[0]) || !mapped_alias(hio->k_new, &hs[1]) ||
+      !mapped_alias(hio->v_new, &hs[2]))
+    return fail(ctx, NOSA_ERR_VALUE, "graph host step needs pinned (mapped) input buffers");
+  if (ctx->graph_exec_host) { cudaGraphExecDestroy(ctx->graph_exec_host); ctx->graph_exec_host = nullptr; }
+  if (ctx->graph_host) { cudaGraphDestroy(ctx->graph_host); ctx->graph_host = nullptr; }
+  ctx->capturing = false;
+  CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->capture_stream, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue_step(ctx, &io, ctx->capture_stream, false, hio);
+  cudaError_t e = cudaStreamEndCapture(ctx->capture_stream, &ctx->graph_host);
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail(ctx, NOSA_ERR_CUDA, "stream capture: %s", cudaGetErrorString(e));
+  CUDA_TRY(ctx, cudaGraphInstantiate(&ctx->graph_exec_host, ctx->graph_host, 0));
+  ctx->graph_host_kernels = ctx->step_kernels + (int)ctx->groups.size();  // + one staging kernel per group
+  // the nodes that hold host addresses
+  ctx->host_nodes.clear();
+  size_t n = 0;
+  CUDA_TRY(ctx, cudaGraphGetNodes(ctx->graph_host, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  CUDA_TRY(ctx, cudaGraphGetNodes(ctx->graph_host, nodes.data(), &n));
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType ty;
+    CUDA_TRY(ctx, cudaGraphNodeGetType(nd, &ty));
+    if (ty == cudaGraphNodeTypeKernel) {
+      cudaKernelNodeParams kp{};
+      CUDA_TRY(ctx, cudaGraphKernelNodeGetParams(nd, &kp));
+      if (kp.func == nosa::stage_inputs_kernel_fn()) ctx->host_nodes.push_back({nd, 0});
+    } else if (ty == cudaGraphNodeTypeMemcpy) {
+      ctx->host_nodes.push_back({nd, 1});
+    }
+  }
+  ctx->cap_hs[0] = hs[0]; ctx->cap_hs[1] = hs[1]; ctx->cap_hs[2] = hs[2];
+  ctx->cap_out = hio->out;
+  ctx->cur_hs[0] = hs[0]; ctx->cur_hs[1] = hs[1]; ctx->cur_hs[2] = hs[2];
+  ctx->cur_out = hio->out;
+  return NOSA_OK;
+}
+
+extern "C" int nosa_step_graph_launch_host(NosaCtx* ctx, const NosaHostStepIO* hio, void* stream) {
+  if (!ctx || !ctx->graph_exec_host) return fail(ctx, NOSA_ERR_STATE, "no captured host step graph");
+  if (!hio || !hio->q || !hio->k_new || !hio->v_new || !hio->out) return fail(ctx, NOSA_ERR_VALUE, "NULL io");
+  const char* hs[3];
+  if (!mapped_alias(hio->q, &hs[0]) || !mapped_alias(hio->k_new, &hs[1]) || !mapped_alias(hio->v_new, &hs[2]))
+    return fail(ctx, NOSA_ERR_VALUE, "graph host step needs pinned (mapped) input buffers");
+  const bool moved = hs[0] != ctx->cur_hs[0] || hs[1] != ctx->cur_hs[1] || hs[2] != ctx->cur_hs[2] ||
+                     hio->out != ctx->cur_out;
+  if (moved) {  // re-point every host-address node at the new buffers (same offsets)
+    for (const auto& hn : ctx->host_nodes) {
+      if (hn.kind == 0) {
+        cudaKernelNodeParams kp{};
+        CUDA_TRY(ctx, cudaGraphKernelNodeGetParams(hn.node, &kp));  // the captured arguments
+        nosa::StageSeg seg[3];
+        for (int i = 0; i < 3; ++i) {
+          seg[i] = *static_cast<const nosa::StageSeg*>(kp.kernelParams[i]);
+          const char* src = reinterpret_cast<const char*>(seg[i].src);
+          seg[i].src = reinterpret_cast<const int4*>(hs[i] + (src - ctx->cap_hs[i]));
+        }
+        void* args[3] = {&seg[0], &seg[1], &seg[2]};
+        kp.kernelParams = args;
+        kp.extra = nullptr;
+        CUDA_TRY(ctx, cudaGraphExecKernelNodeSetParams(ctx->graph_exec_host, hn.node, &kp));
+      } else {
+        cudaMemcpy3DParms mp{};
+        CUDA_TRY(ctx, cudaGraphMemcpyNodeGetParams(hn.node, &mp));
+        char* dst = static_cast<char*>(mp.dstPtr.ptr);
+        const size_t bytes = mp.extent.width * mp.extent.height * mp.extent.depth;
+        char* ndst = reinterpret_cast<char*>(hio->out) + (dst - reinterpret_cast<char*>(ctx->cap_out));
+        CUDA_TRY(ctx, cudaGraphExecMemcpyNodeSetParams1D(ctx->graph_exec_host, hn.node, ndst, mp.srcPtr.ptr, bytes,
+                                                         cudaMemcpyDeviceToHost));
+      }
+    }
+    ctx->cur_hs[0] = hs[0]; ctx->cur_hs[1] = hs[1]; ctx->cur_hs[2] = hs[2];
+    ctx->cur_out = hio->out;
+  }
+  CUDA_TRY(ctx, cudaGraphLaunch(ctx->graph_exec_host, S(stream)));
+  ctx->launches += ctx->graph_host_kernels;
+  return NOSA_OK;
 }
 
 extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {

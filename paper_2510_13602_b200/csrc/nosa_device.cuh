@@ -80,6 +80,14 @@ struct Dev {
   unsigned* err;
 };
 
+// one host segment of the input-staging kernel (nosa_gather.cu); the host-step graph re-points
+// `src` between replays (nosa_ctx.cu)
+struct StageSeg {
+  const int4* src;
+  int4* dst;
+  long long n16;
+};
+
 enum StatIdx { ST_HITS = 0, ST_MISSES, ST_NEW, ST_EVICT, ST_STEPS, ST_CAND, ST_N = 8 };  // ST_CAND: rows rescored in f64
 
 // shared-pool mode: storage index of shared slot s of (layer, head) in the [lbh][C] arrays, and

@@ -170,11 +170,6 @@ cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, b
 // selection group) copied into device memory by the SMs with zero-copy 16-byte loads from the
 // mapped pinned buffers.  The copy engine is busy with the miss gathers and runs its queue in
 // order; SM loads share the PCIe link with it instead of queueing behind it.
-struct StageSeg {
-  const int4* src;
-  int4* dst;
-  long long n16;
-};
 __global__ void __launch_bounds__(256) stage_inputs_kernel(StageSeg a, StageSeg b, StageSeg c) {
   constexpr int PER = 4;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -195,6 +190,8 @@ __global__ void __launch_bounds__(256) stage_inputs_kernel(StageSeg a, StageSeg 
     }
   }
 }
+
+const void* stage_inputs_kernel_fn() { return reinterpret_cast<const void*>(stage_inputs_kernel); }
 
 cudaError_t launch_stage_inputs(const void* const* src, void* const* dst, const size_t* bytes, int grid,
                                 cudaStream_t st) {

@@ -334,6 +334,36 @@ class NosaEngine:
         with torch.cuda.device(self.device):
             self._call(_lib.lib.nosa_step_graph_capture, ctypes.byref(self._graph_io))
 
+    def _host_io(self, q, k_new, v_new, out, selector, gather, schedule):
+        L, B, cfg = self.layers, self.batch, self.config
+        dt = _TORCH_DTYPE[self.dtype]
+        for name, x, h in (("q", q, cfg.n_head), ("k_new", k_new, cfg.n_kv_head), ("v_new", v_new, cfg.n_kv_head)):
+            if not (isinstance(x, torch.Tensor) and x.device.type == "cpu" and x.is_pinned() and x.dtype == dt
+                    and x.is_contiguous() and x.numel() == L * B * h * cfg.d_head):
+                raise ValueError(f"{name} must be a pinned contiguous CPU tensor of {dt} with the step's shape")
+        if not (out.device.type == "cpu" and out.is_pinned() and out.dtype == torch.float32 and out.is_contiguous()
+                and out.numel() == L * B * cfg.n_head * cfg.d_head):
+            raise ValueError("out must be a pinned contiguous CPU float32 tensor of the output shape")
+        return _lib.NosaHostStepIO(q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), out.data_ptr(),
+                                   _lib.SELECTOR[selector], _lib.GATHER[gather], _lib.SCHEDULE[schedule])
+
+    def capture_host(self, q, k_new, v_new, out, selector: str = "nosa", gather: str = "uva",
+                     schedule: str = "pipelined"):
+        """Capture one host-buffer step (step_host) as a CUDA graph; replay_host() re-runs it on
+        these or other pinned buffers of the same shapes."""
+        self._check_step()
+        io = self._host_io(q, k_new, v_new, out, selector, gather, schedule)
+        with torch.cuda.device(self.device):
+            self._call(_lib.lib.nosa_step_graph_capture_host, ctypes.byref(io))
+        self._host_graph_cfg = (selector, gather, schedule)
+
+    def replay_host(self, q, k_new, v_new, out, stream=None):
+        io = self._host_io(q, k_new, v_new, out, *self._host_graph_cfg)
+        with torch.cuda.device(self.device):
+            self._call(_lib.lib.nosa_step_graph_launch_host, ctypes.byref(io), _lib.stream_ptr(stream))
+        self._t += 1
+        return out
+
     def replay(self, stream=None):
         with torch.cuda.device(self.device):
             self._call(_lib.lib.nosa_step_graph_launch, _lib.stream_ptr(stream))

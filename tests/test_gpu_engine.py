@@ -306,6 +306,35 @@ def test_gather_paths_and_schedules_bitwise_identical():
         assert r[1:] == results[0][1:]
 
 
+def test_host_step_graph_replay_matches_eager():
+    """nosa_step_graph_launch_host re-points the captured graph at each step's pinned buffers."""
+    cfg = ONE_B_SMALL
+    w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, 5)
+    K, V = workload.prefix_kv(5, 4, cfg.n_kv_head, 4000, cfg.d_head)
+    K, V = K.reshape(2, 2, cfg.n_kv_head, 4000, cfg.d_head), V.reshape(2, 2, cfg.n_kv_head, 4000, cfg.d_head)
+    outs = []
+    for use_graph in (False, True):
+        eng = NosaEngine(cfg, batch=2, layers=2, max_tokens=4100, fast_slots=70, w1=w1, w2=w2)
+        eng.prefill(torch.from_numpy(K), torch.from_numpy(V))
+        eng.start_run()
+        stream = workload.QueryStream(5, 2, 2, cfg.n_head, cfg.n_kv_head, cfg.d_head, 0.3)
+        res = []
+        for s in range(8):
+            hq, hk, hv = (torch.from_numpy(x).to(torch.bfloat16).pin_memory() for x in stream.next())
+            ho = torch.empty((2, 2, cfg.n_head, cfg.d_head), dtype=torch.float32, pin_memory=True)
+            if use_graph:
+                if s == 0:
+                    eng.capture_host(hq, hk, hv, ho)
+                eng.replay_host(hq, hk, hv, ho)  # new buffers every step
+                torch.cuda.synchronize()
+            else:
+                eng.step_host(hq, hk, hv, out=ho, gather="uva")
+            res.append(ho.numpy().copy())
+        outs.append(np.stack(res))
+        eng.close()
+    np.testing.assert_array_equal(outs[0], outs[1])
+
+
 def test_capacity_exceeded_is_raised():
     w1, w2 = workload.eviction_head(SMALL.n_head, SMALL.d_head, 0)
     eng = NosaEngine(SMALL, batch=1, max_tokens=1100, fast_slots=10, w1=w1, w2=w2)
