@@ -223,7 +223,7 @@ def run_native(args, rank, world, local_rank):
     cfg = attention_config(w["shape"])
     L, B, ctx_len = w["layers"], w["batch_local"], w["context"]
     total_steps = args.burn_in + args.warmup + args.steps * (2 if args.no_e2e else 3)
-    max_tokens = ctx_len + total_steps + 4  # + the e2e graph warm-up and the traced step
+    max_tokens = ctx_len + total_steps + 8  # + the device-clock pass, e2e graph warm-up, traced step
     nblk = -(-max_tokens // cfg.n_b)
     fast = nblk if w["cache"] == "resident" else int(w["cache"] * nblk)
     dtype = torch.bfloat16
@@ -266,7 +266,9 @@ def run_native(args, rank, world, local_rank):
             first_inputs.append((q, kn, vn))
             warm_out.append(out.clone())
     # K steps for the clean timed region, K for the instrumented pass, K for the e2e pass
-    inputs = [stream.next() for _ in range(args.steps * (2 if args.no_e2e else 3))]
+    # K steps for the timed region, K for the instrumented pass, then (e2e) one warm-up + K, all
+    # consecutive in the query stream
+    inputs = [stream.next() for _ in range(args.steps * 2 + (0 if args.no_e2e else args.steps + 1))]
     torch.cuda.synchronize(device)
     eng.reset_stats()
     use_graph = args.gather != "memcpy" and not args.eager
@@ -334,7 +336,7 @@ def run_native(args, rank, world, local_rank):
     st_i = eng.residency_stats()
     instrumented_ms = ei0.elapsed_time(ei1) / args.steps
     eng.timing_enable(0)
-    inputs_e2e = inputs[2 * args.steps:]
+    inputs_e2e = inputs[2 * args.steps + 1:]
 
     # ---------------- end to end: host inputs H2D + step + D2H of the outputs, every step
     e2e = None
@@ -348,17 +350,24 @@ def run_native(args, rank, world, local_rank):
         host_out = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
         if world > 1:
             dist.barrier()
+        warm = tuple(pinned(x) for x in inputs[2 * args.steps])  # untimed first host-buffer step
+        if use_graph:  # the host-buffer step as a CUDA graph, re-pointed at each step's buffers;
+            # the warm-up replay uploads the new executable graph
+            eng.capture_host(*host_in[0], host_out, selector=args.selector, gather=args.gather,
+                             schedule=args.schedule)
+            eng.replay_host(*warm, host_out)
+        else:
+            eng.step_host(*warm, selector=args.selector, out=host_out, gather=args.gather, schedule=args.schedule,
+                          sync=False)
         torch.cuda.synchronize(device)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        if use_graph:  # the host-buffer step as a CUDA graph, re-pointed at each step's buffers;
-            # one untimed replay uploads the new executable graph
-            eng.capture_host(*host_in[0], host_out, selector=args.selector, gather=args.gather,
-                             schedule=args.schedule)
-            warm = tuple(pinned(x) for x in stream.next())
-            eng.replay_host(*warm, host_out)
-            torch.cuda.synchronize(device)
+        e2e_marks, e2e_host = [], []
         for hq, hk, hv in host_in:
+            if args.per_step:
+                e2e_marks.append(torch.cuda.Event(enable_timing=True))
+                e2e_marks[-1].record()
+                e2e_host.append(time.perf_counter())
             if use_graph:
                 eng.replay_host(hq, hk, hv, host_out)
             else:  # the host-buffer C ABI call: inputs staged and outputs copied back inside the step
@@ -366,14 +375,18 @@ def run_native(args, rank, world, local_rank):
                               schedule=args.schedule, sync=False)
         e1.record()
         torch.cuda.synchronize(device)
+        if args.per_step:
+            marks = e2e_marks + [e1]
+            print("e2e per-step ms:", [round(a.elapsed_time(b), 3) for a, b in zip(marks, marks[1:])],
+                  "host enqueue ms:", [round(1e3 * (b - a), 3) for a, b in zip(e2e_host, e2e_host[1:])], file=sys.stderr)
         e_ms = max_over_ranks(e0.elapsed_time(e1), device)
         h2d = sum(x.numel() * x.element_size() for x in host_in[0])
         e2e = {"value": round(tokens / (e_ms * 1e-3), 2), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": host_out.numel() * 4,
                "ms_per_step": round(e_ms / args.steps, 4),
                "api": ("NosaEngine.capture_host/replay_host (C ABI nosa_step_graph_launch_host)" if use_graph else
-                       "NosaEngine.step_host (C ABI nosa_decode_step_host: per-layer H2D of q/k/v on the copy "
-                       "stream, D2H of each layer's output overlapping later layers)") +
+                       "NosaEngine.step_host (C ABI nosa_decode_step_host: q/k/v staged per selection group by "
+                       "an SM zero-copy kernel, outputs copied back per attention batch while later layers run)") +
                       " on inputs in pinned host memory"}
         eng.check_errors()
         if args.trace_out:  # one more host-buffer step, instrumented, for the timeline
@@ -389,6 +402,19 @@ def run_native(args, rank, world, local_rank):
                     seen[k] = seen.get(k, -1) + 1
                     f.write(f"{k} {seen[k]} {1000 * (s0 - base):.1f} {1000 * (s1 - base):.1f} {1000 * (s1 - s0):.1f}\n")
             eng.timing_enable(0)
+
+    # device-clock span of the attention launches (diagnostic, untimed, after the e2e pass so the
+    # query stream stays in order): first CTA start to last
+    # CTA end, read back after each step; the event-timed launch also holds the launch latency
+    # after the cross-stream wait on the layer's miss transfer
+    eng.ktime_enable(True)
+    spans = []
+    for _ in range(3):  # eager launches (a captured graph holds the pre-diagnostic kernel arguments)
+        eng.step(*stream.next(), selector=args.selector, out=out, gather=args.gather, check=False,
+                 schedule=args.schedule)
+        spans += [x for x in eng.ktime_read() if x > 0]
+    eng.ktime_enable(False)
+    attend_exec_ms = statistics.mean(spans) * 1e-3 if spans else None
 
     # ---------------- roofline arithmetic (algorithmic bytes, SURVEY.md §8d / DESIGN.md)
     hbm_peak, peak_kind = peaks()
@@ -420,7 +446,13 @@ def run_native(args, rank, world, local_rank):
     roofline = {"bound": "hbm", "kernel": "attend_bf16_kernel (K4+K5)", "achieved": round(att["gbs"], 1),
                 "peak": hbm_peak, "unit": "GB/s", "frac": round(att["gbs"] / hbm_peak, 4), "traffic": traffic,
                 "peak_kind": peak_kind, "bytes_per_launch": int(per_launch["attend"]),
-                "avg_launch_ms": round(att["avg_ms"], 5)}
+                "avg_launch_ms": round(att["avg_ms"], 5),
+                "device_clock": None if attend_exec_ms is None else {
+                    "exec_span_ms": round(attend_exec_ms, 5),
+                    "achieved": round(per_launch["attend"] * calls / max(att["launches"], 1) / (attend_exec_ms * 1e-3) / 1e9, 1),
+                    "frac": round(per_launch["attend"] * calls / max(att["launches"], 1) / (attend_exec_ms * 1e-3) / 1e9 / hbm_peak, 4),
+                    "note": "first CTA start to last CTA end (%globaltimer), 3 untimed steps; the event-timed "
+                            "launch above also holds the dependency-resolution and launch latency"}}
     # step-level bytes from the uninstrumented timed region; blocks born by an append are rebuilt
     # on the device and never cross PCIe (the reference still counts them as misses)
     h2d_step = (st.misses - st.new_blocks) * bpb / args.steps

@@ -283,6 +283,12 @@ int nosa_timing_read(NosaCtx* ctx, double* total_ms /* [6] */, int64_t* launches
 int nosa_timing_trace(NosaCtx* ctx, int cap, int32_t* kind, float* start_ms, float* end_ms,
                       int32_t* n);
 
+/* Diagnostics: device-clock (%globaltimer) span of each attention launch, first CTA start to
+ * last CTA end, indexed by the launch's first layer; read returns microseconds of the last
+ * launch per layer (0 = none) and resets.  Both synchronise. */
+int nosa_ktime_enable(NosaCtx* ctx, int on);
+int nosa_ktime_read(NosaCtx* ctx, double* span_us /* [layers] */);
+
 /* kernel launches issued by this library since context creation (bench evidence) */
 int64_t nosa_launch_count(const NosaCtx* ctx);
 

@@ -96,6 +96,8 @@ SIGNATURES = {
     "nosa_launch_count": (ctypes.c_int64, [_P]),
     "nosa_timing_enable": (_I, [_P, _I]),
     "nosa_timing_read": (_I, [_P, _F64P, ctypes.POINTER(ctypes.c_int64)]),
+    "nosa_ktime_enable": (_I, [_P, _I]),
+    "nosa_ktime_read": (_I, [_P, _F64P]),
     "nosa_timing_trace": (_I, [_P, _I, _I32P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float), _I32P]),
 }
 

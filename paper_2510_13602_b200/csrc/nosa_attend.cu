@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
   float* wsm = reinterpret_cast<float*>(p);           // [max_chunks * G]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned long long t_start = dv.ktime ? globaltimer_ns() : 0ull;
   if (tid == 0) {
     for (int s = 0; s < T::NS; ++s) {
       mbar_init(&full[s], 1);
@@ -588,6 +589,13 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
         }
         named_sync(kBarConsumers, T::NCW * 32);  // comb_* may be overwritten at the next chunk end
       }
+    }
+  }
+  if (dv.ktime) {  // diagnostics: device-clock span of the launch (first CTA start .. last CTA end)
+    __syncthreads();
+    if (tid == 0) {
+      atomicMin(dv.ktime + 2 * layer, t_start);
+      atomicMax(dv.ktime + 2 * layer + 1, globaltimer_ns());
     }
   }
 }

@@ -262,6 +262,7 @@ static void release(NosaCtx* ctx) {
   for (void* p : ctx->dev_allocs) cudaFree(p);
   if (ctx->staging) cudaFree(ctx->staging);
   if (ctx->io_buf) cudaFree(ctx->io_buf);
+  if (ctx->dv.ktime) cudaFree(ctx->dv.ktime);
   if (ctx->host_mirror && ctx->mirror_device >= 0) {
     cudaSetDevice(ctx->mirror_device);
     cudaFree(ctx->host_mirror);
@@ -799,6 +800,36 @@ extern "C" int nosa_timing_read(NosaCtx* ctx, double* total_ms, int64_t* launche
 // context's device staging; layer l's q/k/v are copied in on the copy stream ahead of the miss
 // gathers (select(l) waits for its own layer only) and its output is copied back on the d2h
 // stream as soon as finalize(l) is done, so the read-back of layer l overlaps layer l+1.
+extern "C" int nosa_ktime_enable(NosaCtx* ctx, int on) {
+  if (!ctx) return NOSA_ERR_VALUE;
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaDeviceSynchronize());
+  if (on && !ctx->dv.ktime) {
+    CUDA_TRY(ctx, cudaMalloc(reinterpret_cast<void**>(&ctx->dv.ktime), 2 * sizeof(unsigned long long) * ctx->dv.L));
+  } else if (!on && ctx->dv.ktime) {
+    cudaFree(ctx->dv.ktime);
+    ctx->dv.ktime = nullptr;
+    return NOSA_OK;
+  }
+  if (ctx->dv.ktime) {
+    std::vector<unsigned long long> init(2 * ctx->dv.L);
+    for (int l = 0; l < ctx->dv.L; ++l) init[2 * l] = ~0ull, init[2 * l + 1] = 0ull;
+    CUDA_TRY(ctx, cudaMemcpy(ctx->dv.ktime, init.data(), init.size() * 8, cudaMemcpyHostToDevice));
+  }
+  return NOSA_OK;
+}
+
+extern "C" int nosa_ktime_read(NosaCtx* ctx, double* span_us) {
+  if (!ctx || !span_us || !ctx->dv.ktime) return NOSA_ERR_VALUE;
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaDeviceSynchronize());
+  std::vector<unsigned long long> v(2 * ctx->dv.L);
+  CUDA_TRY(ctx, cudaMemcpy(v.data(), ctx->dv.ktime, v.size() * 8, cudaMemcpyDeviceToHost));
+  for (int l = 0; l < ctx->dv.L; ++l)
+    span_us[l] = v[2 * l + 1] > v[2 * l] && v[2 * l] != ~0ull ? (double)(v[2 * l + 1] - v[2 * l]) * 1e-3 : 0.0;
+  return nosa_ktime_enable(ctx, 1);  // reset
+}
+
 extern "C" int nosa_timing_trace(NosaCtx* ctx, int cap, int32_t* kind, float* start_ms, float* end_ms, int32_t* n) {
   if (!ctx || !n || (cap > 0 && (!kind || !start_ms || !end_ms))) return NOSA_ERR_VALUE;
   cudaSetDevice(ctx->device);

@@ -75,6 +75,7 @@ struct Dev {
   float* part_o;                 // [2][B*H][max_chunks][G][D]  split-K records, layer parity
   float2* part_ml;               // [2][B*H][max_chunks][G]     (attend(l+1) overlaps finalize(l))
   char* newrow;                  // [lbh][2][D] (elem): K and V row of the last block born by an append
+  unsigned long long* ktime;     // diagnostics (NULL = off): [L][2] device-clock start/end of attention launches
   double* w1;                    // [D][n_ev]
   double* w2;                    // [n_ev]
   unsigned* err;
@@ -108,6 +109,11 @@ __host__ __device__ __forceinline__ float2* part_ml_of(const Dev& dv, int layer)
 }
 
 // ---------------------------------------------------------------- small helpers
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }

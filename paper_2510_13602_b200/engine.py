@@ -486,6 +486,17 @@ class NosaEngine:
         self._call(_lib.lib.nosa_timing_read, ms, n)
         return {k: {"total_ms": ms[4 + i], "copies": n[4 + i]} for i, k in enumerate(self.COPY_KINDS)}
 
+    def ktime_enable(self, on: bool = True):
+        """Diagnostics: record the device-clock span of every attention launch."""
+        self._call(_lib.lib.nosa_ktime_enable, int(on))
+
+    def ktime_read(self) -> list[float]:
+        """Microseconds from the first CTA's start to the last CTA's end of the last attention
+        launch of each layer (0.0 = no launch started at that layer); resets."""
+        out = np.zeros(self.layers, np.float64)
+        self._call(_lib.lib.nosa_ktime_read, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        return out.tolist()
+
     def timing_trace(self, cap: int = 65536) -> list[tuple[str, float, float]]:
         """(kind, start_ms, end_ms) of every timed launch since timing_enable, in issue order,
         relative to the first launch: the device timeline of the step's streams."""

@@ -27,6 +27,35 @@ def test_library_exports_every_declared_symbol():
     assert declared == set(_lib.SIGNATURES), declared ^ set(_lib.SIGNATURES)
 
 
+def _header_struct_fields(header: str, name: str) -> list[str]:
+    body = re.search(r"typedef struct " + name + r" \{(.*?)\} " + name + ";", header, re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = []
+    for decl in body.split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        fields += [re.search(r"(\w+)\s*$", part).group(1) for part in decl.split(",")]
+    return fields
+
+
+@pytest.mark.parametrize("name", ["NosaConfig", "NosaStats", "NosaStepIO", "NosaHostStepIO"])
+def test_ctypes_structs_match_header(name):
+    """The ctypes mirrors (and INTEGRATION.md's stub) lay the structs out as the header does."""
+    header = (ROOT / "include" / "nosa_b200.h").read_text()
+    want = _header_struct_fields(header, name)
+    got = [f for f, _ in getattr(_lib, name)._fields_]
+    assert got == want
+
+
+def test_integration_stub_config_fields_match_header():
+    header = (ROOT / "include" / "nosa_b200.h").read_text()
+    doc = (ROOT / "INTEGRATION.md").read_text()
+    stub = re.search(r"class NosaConfig\(ctypes.Structure\):.*?_fields_ = \[.*?for f in \((.*?)\)\]", doc, re.S)
+    names = re.findall(r'"(\w+)"', stub.group(1))
+    assert names == _header_struct_fields(header, "NosaConfig")
+
+
 def _c_config(**over):
     c = _lib.NosaConfig()
     base = dict(n=16384, d=1024, n_head=8, n_kv_head=2, d_head=128, n_b=64, n_s=64, n_w=512, k=1024, k_q=256,
