@@ -797,11 +797,13 @@ cudaError_t launch_finalize(const Dev& dv, int layer, const void* kn, const void
   if (dv.dtype == 0) {
     auto k = finalize_kernel<__nv_bfloat16>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    max_shared_carveout(k);
     k<<<grid, kFinThreads, smem, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(kn),
                                         static_cast<const __nv_bfloat16*>(vn), out);
   } else {
     auto k = finalize_kernel<float>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    max_shared_carveout(k);
     k<<<grid, kFinThreads, smem, st>>>(dv, layer, static_cast<const float*>(kn), static_cast<const float*>(vn), out);
   }
   return cudaGetLastError();
@@ -816,6 +818,7 @@ static cudaError_t launch_bf16(const Dev& dv, int layer, int nl, const void* q, 
   auto k = attend_bf16_kernel<NBK, DH, NQT>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  max_shared_carveout(k);
   k<<<num_sms, T::THREADS, smem, st>>>(dv, layer, nl, static_cast<const __nv_bfloat16*>(q),
                                        (size_t)dv.B * dv.Hq * DH);
   return cudaGetLastError();

@@ -14,6 +14,7 @@
 //   blk_of / lastreq / fstack [lbh][C]  slot -> block, last-required clock, LIFO free stack
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <stdint.h>
 
@@ -106,6 +107,15 @@ __host__ __device__ __forceinline__ float* part_o_of(const Dev& dv, int layer) {
 }
 __host__ __device__ __forceinline__ float2* part_ml_of(const Dev& dv, int layer) {
   return dv.part_ml + (size_t)(layer % dv.nbuf) * dv.B * dv.H * dv.max_rec * dv.G;
+}
+
+// Every kernel of the step asks for the maximum shared-memory carveout, so an SM never has to
+// change its L1/shared split (and drain its resident CTAs) between the persistent attention
+// kernel and the kernels that run beside it.  NOSA_NO_CARVEOUT=1 turns this off (A/B).
+template <typename F>
+inline void max_shared_carveout(F* kernel) {
+  static const bool on = getenv("NOSA_NO_CARVEOUT") == nullptr;
+  if (on) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
 // ---------------------------------------------------------------- small helpers

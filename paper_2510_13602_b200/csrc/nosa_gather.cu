@@ -151,10 +151,15 @@ cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, b
   if (tma) {
     const size_t smem = (size_t)kTmaStages * dv.bpb + kTmaStages * 8;
     cudaFuncSetAttribute(gather_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    max_shared_carveout(gather_tma_kernel);
     gather_tma_kernel<<<g, 32, smem, st>>>(dv, layer);
   } else {
     // NOSA_GATHER_VARIANT (experiments): bit 0 = two blocks per CTA iteration, bit 1 = L2::256B
     static const int variant = getenv("NOSA_GATHER_VARIANT") ? atoi(getenv("NOSA_GATHER_VARIANT")) : 0;
+    max_shared_carveout(gather_kernel<1, false>);
+    max_shared_carveout(gather_kernel<2, false>);
+    max_shared_carveout(gather_kernel<1, true>);
+    max_shared_carveout(gather_kernel<2, true>);
     switch (variant & 3) {
       case 0: gather_kernel<1, false><<<g, 256, 0, st>>>(dv, layer); break;
       case 1: gather_kernel<2, false><<<g, 256, 0, st>>>(dv, layer); break;
@@ -198,6 +203,7 @@ cudaError_t launch_stage_inputs(const void* const* src, void* const* dst, const 
   StageSeg sg[3];
   for (int i = 0; i < 3; ++i)
     sg[i] = {static_cast<const int4*>(src[i]), static_cast<int4*>(dst[i]), (long long)(bytes[i] / 16)};
+  max_shared_carveout(stage_inputs_kernel);
   stage_inputs_kernel<<<grid, 256, 0, st>>>(sg[0], sg[1], sg[2]);
   return cudaGetLastError();
 }

@@ -930,6 +930,7 @@ cudaError_t launch_plan_shared(const Dev& dv, int layer, const int* ext_req, con
   const int N = dv.B * dv.C;
   const size_t smem = 5 * (size_t)dv.C * 4 + ((size_t)N / 32 + 2) * 4 + 32 * 8 + 32 * 4 + 8 * 4 + 64;
   cudaFuncSetAttribute(plan_shared_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  max_shared_carveout(plan_shared_kernel);
   plan_shared_kernel<<<dv.H, kSharedThreads, smem, st>>>(dv, layer, ext_req, ext_nreq);
   return cudaGetLastError();
 }
@@ -946,11 +947,13 @@ cudaError_t launch_select_plan(const Dev& dv, int layer, const void* q, int sele
   if (dv.dtype == 0) {
     auto k = select_plan_kernel<__nv_bfloat16>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    max_shared_carveout(k);
     k<<<grid, 256, smem, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(q), qs, selector, mode, ext_req,
                                ext_nreq);
   } else {
     auto k = select_plan_kernel<float>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    max_shared_carveout(k);
     k<<<grid, 256, smem, st>>>(dv, layer, static_cast<const float*>(q), qs, selector, mode, ext_req, ext_nreq);
   }
   return cudaGetLastError();
