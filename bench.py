@@ -359,6 +359,7 @@ def run_native(args, rank, world, local_rank):
         else:
             eng.step_host(*warm, selector=args.selector, out=host_out, gather=args.gather, schedule=args.schedule,
                           sync=False)
+        eng.reset_stats()  # the e2e pass's own miss traffic is reported beside its rate
         torch.cuda.synchronize(device)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -380,9 +381,11 @@ def run_native(args, rank, world, local_rank):
             print("e2e per-step ms:", [round(a.elapsed_time(b), 3) for a, b in zip(marks, marks[1:])],
                   "host enqueue ms:", [round(1e3 * (b - a), 3) for a, b in zip(e2e_host, e2e_host[1:])], file=sys.stderr)
         e_ms = max_over_ranks(e0.elapsed_time(e1), device)
+        st_e = eng.residency_stats()
         h2d = sum(x.numel() * x.element_size() for x in host_in[0])
         e2e = {"value": round(tokens / (e_ms * 1e-3), 2), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": host_out.numel() * 4,
+               "miss_bytes_per_step": int((st_e.misses - st_e.new_blocks) * eng.bytes_per_block / args.steps),
                "ms_per_step": round(e_ms / args.steps, 4),
                "api": ("NosaEngine.capture_host/replay_host (C ABI nosa_step_graph_launch_host)" if use_graph else
                        "NosaEngine.step_host (C ABI nosa_decode_step_host: q/k/v staged per selection group by "

@@ -264,6 +264,51 @@ def test_peer_slow_tier_loopback(gather):
     assert a <= TOL["bf16"]
 
 
+@pytest.mark.parametrize("exact", [False, True])
+@pytest.mark.parametrize("selector", ["nosa", "infllmv2"])
+def test_exact_score_ties_pick_the_lower_block(exact, selector):
+    """Duplicated KV blocks have bitwise equal block means, so their scores tie exactly; the
+    selectors must break the tie by the lower block index like argtopk (numerics.py:59-73),
+    with no tolerance (selection given scores is pinned exactly)."""
+    cfg = ONE_B_SMALL
+    B, t0, steps, C, seed = 2, 5000, 10, 72, 31
+    w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, seed)
+    K, V = workload.prefix_kv(seed, B, cfg.n_kv_head, t0, cfg.d_head)
+    n_b = cfg.n_b
+    for b in range(B):  # blocks 10..39 copy block 9, blocks 45..64 copy block 44 (pool = 1..62)
+        for src, dsts in ((9, range(10, 40)), (44, range(45, 65))):
+            for d in dsts:
+                K[b, :, d * n_b:(d + 1) * n_b] = K[b, :, src * n_b:(src + 1) * n_b]
+                V[b, :, d * n_b:(d + 1) * n_b] = V[b, :, src * n_b:(src + 1) * n_b]
+    eng = NosaEngine(cfg, batch=B, max_tokens=t0 + steps + 1, fast_slots=C, w1=w1, w2=w2, exact_scan=exact)
+    orc = oracle_for(cfg, B, 1, t0 + steps + 1, C, w1, w2)
+    eng.prefill(torch.from_numpy(K), torch.from_numpy(V), layer=0)
+    for b in range(B):
+        orc.prefill(0, b, K[b], V[b])
+    eng.start_run()
+    orc.start_run()
+    stream = workload.QueryStream(seed, 1, B, cfg.n_head, cfg.n_kv_head, cfg.d_head, 0.0)
+    ties_at_boundary = 0
+    for _ in range(steps):
+        q, kn, vn = stream.next()
+        out = eng.step(q, kn, vn, selector=selector).cpu().numpy()
+        ref, recs = orc.step(q, kn, vn, selector)
+        sels = eng.selections(0)
+        for b in range(B):
+            for h in range(cfg.n_kv_head):
+                r = recs[0][b][h]
+                assert list(sels[b][h].blocks_q) == r.blocks_q.tolist()
+                assert list(sels[b][h].blocks_e) == r.blocks_e.tolist()
+                lo = orc.geom[b].pool[0]
+                chosen = set(r.blocks_q.tolist())
+                inside = [r.s_q[p - lo] for p in chosen]
+                outside = [r.s_q[i] for i in range(len(r.s_q)) if i + lo not in chosen]
+                ties_at_boundary += bool(inside and outside and min(inside) == max(outside))
+        assert rel_err(out, ref) <= TOL["bf16"]
+    assert ties_at_boundary > 0  # the duplicates did straddle the top-k boundary
+    eng.close()
+
+
 def test_resident_multilayer_batched_attention():
     """All blocks in HBM: attention runs 4 layers per persistent launch (6 layers = 4 + 2)."""
     a = _run_pair(ONE_B_SMALL, batch=2, t0s=[3000, 2900], steps=8, fast_slots=48, seed=17, rho=0.3, layers=6,
