@@ -289,6 +289,12 @@ int nosa_timing_trace(NosaCtx* ctx, int cap, int32_t* kind, float* start_ms, flo
 int nosa_ktime_enable(NosaCtx* ctx, int on);
 int nosa_ktime_read(NosaCtx* ctx, double* span_us /* [layers] */);
 
+/* Diagnostics: cycles spent per phase of the selection kernel, summed over CTAs (cycles[15] =
+ * CTAs).  Phases: 1 q_sum, 2 screen scan, 3 radix threshold, 4 f64 rescoring, 5 ranking,
+ * 6 NOSA walk, 7 outputs + required list, 8 hit test, 9 victims, 11 apply + writes.
+ * Reads (if cycles != NULL) then resets (on = 1) or disables (on = 0).  Synchronises. */
+int nosa_select_profile(NosaCtx* ctx, int on, double* cycles /* [16] */);
+
 /* kernel launches issued by this library since context creation (bench evidence) */
 int64_t nosa_launch_count(const NosaCtx* ctx);
 

@@ -97,6 +97,7 @@ SIGNATURES = {
     "nosa_timing_enable": (_I, [_P, _I]),
     "nosa_timing_read": (_I, [_P, _F64P, ctypes.POINTER(ctypes.c_int64)]),
     "nosa_ktime_enable": (_I, [_P, _I]),
+    "nosa_select_profile": (_I, [_P, _I, _F64P]),
     "nosa_ktime_read": (_I, [_P, _F64P]),
     "nosa_timing_trace": (_I, [_P, _I, _I32P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float), _I32P]),
 }

@@ -263,6 +263,7 @@ static void release(NosaCtx* ctx) {
   if (ctx->staging) cudaFree(ctx->staging);
   if (ctx->io_buf) cudaFree(ctx->io_buf);
   if (ctx->dv.ktime) cudaFree(ctx->dv.ktime);
+  if (ctx->dv.sel_prof) cudaFree(ctx->dv.sel_prof);
   if (ctx->host_mirror && ctx->mirror_device >= 0) {
     cudaSetDevice(ctx->mirror_device);
     cudaFree(ctx->host_mirror);
@@ -828,6 +829,25 @@ extern "C" int nosa_ktime_read(NosaCtx* ctx, double* span_us) {
   for (int l = 0; l < ctx->dv.L; ++l)
     span_us[l] = v[2 * l + 1] > v[2 * l] && v[2 * l] != ~0ull ? (double)(v[2 * l + 1] - v[2 * l]) * 1e-3 : 0.0;
   return nosa_ktime_enable(ctx, 1);  // reset
+}
+
+extern "C" int nosa_select_profile(NosaCtx* ctx, int on, double* cycles) {
+  if (!ctx) return NOSA_ERR_VALUE;
+  cudaSetDevice(ctx->device);
+  CUDA_TRY(ctx, cudaDeviceSynchronize());
+  if (cycles && ctx->dv.sel_prof) {
+    long long v[16];
+    CUDA_TRY(ctx, cudaMemcpy(v, ctx->dv.sel_prof, sizeof(v), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 16; ++i) cycles[i] = (double)v[i];
+  }
+  if (on) {
+    if (!ctx->dv.sel_prof) CUDA_TRY(ctx, cudaMalloc(reinterpret_cast<void**>(&ctx->dv.sel_prof), 16 * sizeof(long long)));
+    CUDA_TRY(ctx, cudaMemset(ctx->dv.sel_prof, 0, 16 * sizeof(long long)));
+  } else if (ctx->dv.sel_prof) {
+    cudaFree(ctx->dv.sel_prof);
+    ctx->dv.sel_prof = nullptr;
+  }
+  return NOSA_OK;
 }
 
 extern "C" int nosa_timing_trace(NosaCtx* ctx, int cap, int32_t* kind, float* start_ms, float* end_ms, int32_t* n) {

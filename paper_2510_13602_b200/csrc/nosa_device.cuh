@@ -77,6 +77,7 @@ struct Dev {
   float2* part_ml;               // [2][B*H][max_chunks][G]     (attend(l+1) overlaps finalize(l))
   char* newrow;                  // [lbh][2][D] (elem): K and V row of the last block born by an append
   unsigned long long* ktime;     // diagnostics (NULL = off): [L][2] device-clock start/end of attention launches
+  long long* sel_prof;           // diagnostics (NULL = off): [16] select_plan cycles per phase, [15] = CTAs
   double* w1;                    // [D][n_ev]
   double* w2;                    // [n_ev]
   unsigned* err;

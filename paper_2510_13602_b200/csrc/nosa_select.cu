@@ -73,6 +73,7 @@ struct SelSmem {
   float* up;         // [Pp] screened upper bound
   int* hist;         // [256] radix-select histogram
   int* misc;  // [16]
+  long long* marks;  // diagnostics: clock64 at phase boundaries (NULL = off)
 };
 
 __device__ SelSmem carve_sel_smem(char* base, int D, int Pp, int C) {
@@ -108,6 +109,11 @@ size_t sel_smem_bytes(int D, int Pp, int C) {
 }
 
 enum { M_NREQ = 0, M_NF, M_SHORT, M_NCAND, M_CLOCK, M_ERR, M_NQ, M_NE, M_QMAX, M_BIN, M_REM, M_NC };
+
+// diagnostics (Dev.sel_prof): phase boundary i of this CTA
+__device__ __forceinline__ void sel_mark(const SelSmem& sm, int i) {
+  if (sm.marks && threadIdx.x == 0) sm.marks[i] = clock64();
+}
 
 // monotone u32 image of a float (larger float -> larger key), and back
 __device__ __forceinline__ unsigned f2key(float f) {
@@ -146,53 +152,82 @@ __device__ void screened_topk(const Dev& dv, int lbh, int pool_lo, int P, int m,
   const float* kerr = dv.kc_err + (size_t)lbh * dv.NB + pool_lo;
   const float qmax = __int_as_float(sm.misc[M_QMAX]);
   const float gam = (float)(D + 8) * 5.9604645e-08f + 1.1920929e-07f;  // (D+8) 2^-24 + 2^-23 (+ f64 slack)
-  // lane's q_sum dims in fp32: D=128 -> 4 dims [4*lane, 4*lane+4), D=64 -> 2 dims
-  const int per = D / 32;
-  float qf[4];
+  // (a) screen: a half-warp per row (16 lanes x D/16 dims: one 16-byte load per lane at D=128),
+  //     16 rows per warp iteration with every load issued first, then a reduce-scatter over the
+  //     16 lanes leaves row u's dot and abs-dot on lane 2*u' (u' = bit-reversed position)
+  const int E = D / 16;  // dims per lane: 8 (D=128) or 4 (D=64)
+  const int hl = lane & 15, half = lane >> 4;
+  float qf[8];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) qf[j] = j < per ? (float)sm.qsum[lane * per + j] : 0.0f;
-  // (a) screen: 8 rows per warp iteration, all loads first
-  for (int p0 = warp * 8; p0 < P; p0 += nwarps * 8) {
-    uint2 raw[8];
+  for (int j = 0; j < 8; ++j) qf[j] = j < E ? (float)sm.qsum[hl * E + j] : 0.0f;
+  for (int p0 = warp * 16; p0 < P; p0 += nwarps * 16) {
+    uint4 raw[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const __nv_bfloat16* row = k16 + (size_t)min(p0 + u, P - 1) * D + lane * per;
-      if (per == 4) raw[u] = __ldg(reinterpret_cast<const uint2*>(row));
-      else raw[u] = make_uint2(__ldg(reinterpret_cast<const unsigned*>(row)), 0u);
+      const __nv_bfloat16* row = k16 + (size_t)min(p0 + 2 * u + half, P - 1) * D + hl * E;
+      if (E == 8) {
+        raw[u] = __ldg(reinterpret_cast<const uint4*>(row));
+      } else {
+        const uint2 r2 = __ldg(reinterpret_cast<const uint2*>(row));
+        raw[u] = make_uint4(r2.x, r2.y, 0u, 0u);
+      }
     }
     float sv[8], av[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const __nv_bfloat162 x01 = *reinterpret_cast<const __nv_bfloat162*>(&raw[u].x);
-      const __nv_bfloat162 x23 = *reinterpret_cast<const __nv_bfloat162*>(&raw[u].y);
-      const float k0 = __low2float(x01), k1 = __high2float(x01), k2 = __low2float(x23), k3 = __high2float(x23);
-      sv[u] = fmaf(k3, qf[3], fmaf(k2, qf[2], fmaf(k1, qf[1], k0 * qf[0])));
-      av[u] = fmaf(fabsf(k3), fabsf(qf[3]), fmaf(fabsf(k2), fabsf(qf[2]), fmaf(fabsf(k1), fabsf(qf[1]), fabsf(k0 * qf[0]))));
-    }
+      const unsigned w[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
+      float sacc = 0.0f, aacc = 0.0f;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        sv[u] += __shfl_xor_sync(0xffffffffu, sv[u], o);
-        av[u] += __shfl_xor_sync(0xffffffffu, av[u], o);
+      for (int j = 0; j < 4; ++j) {
+        const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(&w[j]);
+        const float k0 = __low2float(x), k1 = __high2float(x);
+        sacc = fmaf(k1, qf[2 * j + 1], fmaf(k0, qf[2 * j], sacc));
+        aacc = fmaf(fabsf(k1), fabsf(qf[2 * j + 1]), fmaf(fabsf(k0), fabsf(qf[2 * j]), aacc));
       }
+      sv[u] = sacc;
+      av[u] = aacc;
     }
-    if (lane < 8 && p0 + lane < P) {
-      float s_ = sv[0], a_ = av[0];
+    const bool b3 = hl & 8, b2 = hl & 4, b1 = hl & 2;
 #pragma unroll
-      for (int u = 1; u < 8; ++u)
-        if (lane == u) s_ = sv[u], a_ = av[u];
-      const int p = p0 + lane;
+    for (int i = 0; i < 4; ++i) {
+      const float ss = b3 ? sv[i] : sv[i + 4], sk = b3 ? sv[i + 4] : sv[i];
+      const float as = b3 ? av[i] : av[i + 4], ak = b3 ? av[i + 4] : av[i];
+      sv[i] = sk + __shfl_xor_sync(0xffffffffu, ss, 8);
+      av[i] = ak + __shfl_xor_sync(0xffffffffu, as, 8);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float ss = b2 ? sv[i] : sv[i + 2], sk = b2 ? sv[i + 2] : sv[i];
+      const float as = b2 ? av[i] : av[i + 2], ak = b2 ? av[i + 2] : av[i];
+      sv[i] = sk + __shfl_xor_sync(0xffffffffu, ss, 4);
+      av[i] = ak + __shfl_xor_sync(0xffffffffu, as, 4);
+    }
+    {
+      const float ss = b1 ? sv[0] : sv[1], sk = b1 ? sv[1] : sv[0];
+      const float as = b1 ? av[0] : av[1], ak = b1 ? av[1] : av[0];
+      sv[0] = sk + __shfl_xor_sync(0xffffffffu, ss, 2);
+      av[0] = ak + __shfl_xor_sync(0xffffffffu, as, 2);
+    }
+    sv[0] += __shfl_xor_sync(0xffffffffu, sv[0], 1);
+    av[0] += __shfl_xor_sync(0xffffffffu, av[0], 1);
+    const int u = (b3 ? 4 : 0) + (b2 ? 2 : 0) + (b1 ? 1 : 0);
+    const int p = p0 + 2 * u + half;
+    if (!(hl & 1) && p < P) {
+      const float s_ = sv[0], a_ = av[0];
       const float bound = (gam * a_ + __ldg(kerr + p) * qmax) * 1.001f + fabsf(s_) * 2.4e-7f + 1e-30f;
       sm.lo_key[p] = f2key(__fsub_rd(s_, bound));
       sm.up[p] = __fadd_ru(s_, bound);
     }
   }
   __syncthreads();
-  // (b) T = m-th largest lower bound: 4 passes of an 8-bit radix select
+  sel_mark(sm, 2);
+  // (b) T = (a lower bound of) the m-th largest lower bound: two 8-bit radix passes fix the top
+  //     16 bits of its key (sign, exponent, 7 mantissa bits: bins ~1% wide) and T is the bin's
+  //     lower edge.  T at or below the exact m-th value keeps the candidate test exact; it only
+  //     admits the few rows of the same bin.
   unsigned prefix = 0u, pmask = 0u;
   int remaining = m;
-  for (int pass = 0; pass < 4; ++pass) {
+  for (int pass = 0; pass < 2; ++pass) {
     const int shift = 24 - 8 * pass;
     for (int i = tid; i < 256; i += blockDim.x) sm.hist[i] = 0;
     __syncthreads();
@@ -234,6 +269,7 @@ __device__ void screened_topk(const Dev& dv, int lbh, int pool_lo, int P, int m,
     remaining = sm.misc[M_REM];
   }
   const float T = key2f(prefix);
+  sel_mark(sm, 3);
   // (c) candidates: up >= T, rescored in f64 (one warp per row)
   if (tid == 0) sm.misc[M_NC] = 0;
   __syncthreads();
@@ -244,11 +280,29 @@ __device__ void screened_topk(const Dev& dv, int lbh, int pool_lo, int P, int m,
   if (tid == 0) dv.stats[(size_t)lbh * ST_N + ST_CAND] += nc;
   double* cs = reinterpret_cast<double*>(sm.key);  // candidate scores
   const double* kc = dv.kc + ((size_t)lbh * dv.NB + pool_lo) * D;
-  for (int i = warp; i < nc; i += nwarps) {
-    const double v = row_dot64(kc + (size_t)sm.idx[i] * D, sm.qsum, D);
-    if (lane == 0) cs[i] = v;
+  for (int i = warp; i < nc; i += 2 * nwarps) {  // two rows per warp in flight, same order as row_dot64
+    const int i2 = i + nwarps;
+    const double* r1 = kc + (size_t)sm.idx[i] * D;
+    const double* r2 = kc + (size_t)sm.idx[i2 < nc ? i2 : i] * D;
+    double a1 = 0.0, a2 = 0.0;
+    for (int d = lane * 2; d < D; d += 64) {
+      const double2 v1 = __ldg(reinterpret_cast<const double2*>(r1 + d));
+      const double2 v2 = __ldg(reinterpret_cast<const double2*>(r2 + d));
+      a1 = fma(v1.y, sm.qsum[d + 1], fma(v1.x, sm.qsum[d], a1));
+      a2 = fma(v2.y, sm.qsum[d + 1], fma(v2.x, sm.qsum[d], a2));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    if (lane == 0) {
+      cs[i] = a1;
+      if (i2 < nc) cs[i2] = a2;
+    }
   }
   __syncthreads();
+  sel_mark(sm, 4);
   // (d) rank the candidates by (score desc, index asc); the first m are the picks
   for (int i = tid; i < nc; i += blockDim.x) {
     const double si = cs[i];
@@ -261,6 +315,7 @@ __device__ void screened_topk(const Dev& dv, int lbh, int pool_lo, int P, int m,
     if (rank < m) atomicOr(&sm.bm_q[pi >> 5], 1u << (pi & 31));
   }
   __syncthreads();
+  sel_mark(sm, 5);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -295,6 +350,7 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
     }
   }
   __syncthreads();
+  sel_mark(sm, 1);
   const int m_q_eff = min(selector == 0 ? dv.m_q : dv.m_topk, P);
   if (dv.screen) {
     for (int w = tid; w < Pp / 32; w += blockDim.x) {
@@ -404,40 +460,40 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
   }
   __syncthreads();
 
-  // (5) sorted outputs: blocks_q, blocks_e, required = sink U picked U recent
+  sel_mark(sm, 6);
+  // (5) sorted outputs: blocks_q, blocks_e, required = sink U picked U recent, one part per warp
+  const int nw = Pp / 32;
+  int n_picked = 0;  // every thread counts the picks (broadcast reads of <= 32 words)
+  for (int w = 0; w < nw; ++w) n_picked += __popc(sm.bm_q[w] | sm.bm_e[w]);
+  const int n_req = a_end + n_picked + (nblk - r_begin);
   if (warp == 0) {
-    const int nw = Pp / 32;
-    int* sel_q = dv.sel_q + (size_t)lbh * dv.MQ;
-    int* sel_e = dv.sel_e + (size_t)lbh * dv.ME;
-    const int nq = warp_bits_to_sorted(sm.bm_q, nw, pool_lo, sel_q);
-    const int ne = warp_bits_to_sorted(sm.bm_e, nw, pool_lo, sel_e);
-    // merged picked list, written after the sink part of req
-    int n_picked = 0;
-    const int cap = dv.C;
+    const int nq = warp_bits_to_sorted(sm.bm_q, nw, pool_lo, dv.sel_q + (size_t)lbh * dv.MQ);
+    if (lane == 0) {
+      sm.misc[M_NQ] = nq;
+      dv.n_selq[lbh] = nq;
+      sm.misc[M_NREQ] = n_req;
+    }
+  } else if (warp == 1) {
+    const int ne = warp_bits_to_sorted(sm.bm_e, nw, pool_lo, dv.sel_e + (size_t)lbh * dv.ME);
+    if (lane == 0) {
+      sm.misc[M_NE] = ne;
+      dv.n_sele[lbh] = ne;
+    }
+  } else if (warp == 2) {  // merged picked list, after the sink part of req
+    int n = 0;
     for (int w = 0; w < nw; ++w) {
       const unsigned word = sm.bm_q[w] | sm.bm_e[w];
       if (word == 0u) continue;
       if ((word >> lane) & 1u) {
-        const int pos = a_end + n_picked + __popc(word & ((1u << lane) - 1u));
-        if (pos < cap) sm.req[pos] = pool_lo + w * 32 + lane;
+        const int pos = a_end + n + __popc(word & ((1u << lane) - 1u));
+        if (pos < dv.C) sm.req[pos] = pool_lo + w * 32 + lane;
       }
-      n_picked += __popc(word);
+      n += __popc(word);
     }
-    const int n_req = a_end + n_picked + (nblk - r_begin);
-    if (lane == 0) {
-      sm.misc[M_NREQ] = n_req;
-      sm.misc[M_NQ] = nq;
-      sm.misc[M_NE] = ne;
-      dv.n_selq[lbh] = nq;
-      dv.n_sele[lbh] = ne;
-    }
-  }
-  __syncthreads();
-  const int n_req = sm.misc[M_NREQ];
-  const int n_picked = n_req - a_end - (nblk - r_begin);
-  if (n_req <= dv.C) {
-    for (int j = tid; j < a_end; j += blockDim.x) sm.req[j] = j;
-    for (int j = r_begin + tid; j < nblk; j += blockDim.x) sm.req[a_end + n_picked + (j - r_begin)] = j;
+  } else if (n_req <= dv.C) {  // sink and recent parts
+    const int t3 = tid - 96, n3 = blockDim.x - 96;
+    for (int j = t3; j < a_end; j += n3) sm.req[j] = j;
+    for (int j = r_begin + t3; j < nblk; j += n3) sm.req[a_end + n_picked + (j - r_begin)] = j;
   }
   __syncthreads();
 }
@@ -507,6 +563,7 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
   const int shortfall = sm.misc[M_SHORT];
   const int clock = sm.misc[M_CLOCK];
 
+  sel_mark(sm, 8);
   // (2) victims: least-recently-required resident blocks not required now (kv_manager.py:233-246)
   if (shortfall > 0) {
     for (int s = tid; s < C; s += blockDim.x) {
@@ -531,6 +588,7 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
     }
   }
 
+  sel_mark(sm, 9);
   // (3) apply: evictions push their slots (LRR order), fetches pop (required order)
   if (warp == 0) {
     int top = dv.ftop[lbh];
@@ -610,6 +668,11 @@ __global__ void __launch_bounds__(256, 3)  // 3 CTAs per SM: one CTA's scan over
   const int lbh = (layer * dv.B + b) * dv.H + h;
   const int Pp = next_pow2(dv.NB);
   SelSmem sm = carve_sel_smem(smem_raw, dv.D, Pp, dv.C);
+  __shared__ long long marks[16];
+  sm.marks = dv.sel_prof ? marks : nullptr;
+  if (sm.marks && threadIdx.x == 0)
+    for (int i = 0; i < 16; ++i) marks[i] = 0;
+  sel_mark(sm, 0);
 
   if (mode == 2) {
     const int n = ext_nreq[bh];
@@ -626,7 +689,19 @@ __global__ void __launch_bounds__(256, 3)  // 3 CTAs per SM: one CTA's scan over
       dv.req[(size_t)lbh * dv.C + i] = sm.req[i];
     return;
   }
+  sel_mark(sm, 7);
   plan_phase(dv, layer, b, h, sm);
+  __syncthreads();
+  sel_mark(sm, 11);
+  if (sm.marks && threadIdx.x == 0) {  // cycles per phase, summed over CTAs; [15] counts CTAs
+    long long prev = marks[0];
+    for (int i = 1; i < 12; ++i) {
+      if (marks[i] == 0) continue;  // phase skipped
+      atomicAdd(reinterpret_cast<unsigned long long*>(dv.sel_prof + i), (unsigned long long)(marks[i] - prev));
+      prev = marks[i];
+    }
+    atomicAdd(reinterpret_cast<unsigned long long*>(dv.sel_prof + 15), 1ull);
+  }
 }
 
 // ------------------------------------------------------------------------------------------

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--gather", default="uva")
     ap.add_argument("--layer-by-layer", action="store_true", help="use the per-layer C-ABI calls")
     ap.add_argument("--trace", action="store_true", help="print the device timeline of the last step")
+    ap.add_argument("--sel-prof", action="store_true", help="print the selection kernel's cycles per phase")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     cfg = one_b_config(65536)
@@ -66,6 +67,23 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     e1.record()
     torch.cuda.synchronize()
+    if a.sel_prof:  # one more step with the phase profiler on
+        import ctypes
+        import numpy as np
+        from paper_2510_13602_b200 import _lib
+        cyc = np.zeros(16)
+        P = lambda: cyc.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        eng._call(_lib.lib.nosa_select_profile, 1, None)
+        q, k, v = qs.next()
+        eng.step(q, k, v, selector=a.selector, out=out, gather=a.gather, check=False)
+        eng._call(_lib.lib.nosa_select_profile, 0, P())
+        names = {1: "q_sum", 2: "screen scan", 3: "radix threshold", 4: "f64 rescoring", 5: "ranking", 6: "NOSA walk",
+                 7: "outputs+required", 8: "hit test", 9: "victims", 11: "apply+writes"}
+        n = max(cyc[15], 1)
+        tot = sum(cyc[i] for i in names)
+        print(f"select_plan: {int(cyc[15])} CTAs, {tot / n:.0f} cycles per CTA ({tot / n / 1.965e3:.1f} us at 1965 MHz)")
+        for i, nm in names.items():
+            print(f"  {nm:18s} {cyc[i] / n:8.0f} cycles  {100 * cyc[i] / max(tot, 1):5.1f}%")
     st = eng.residency_stats()
     res = {"ms_per_step": e0.elapsed_time(e1) / (a.steps - 2), "kernels": eng.timing_read(),
            "hit_rate": st.hit_rate, "misses": st.misses, "hits": st.hits}
