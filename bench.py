@@ -216,6 +216,8 @@ def run_native(args, rank, world, local_rank):
 
     device = torch.device("cuda", local_rank)
     torch.cuda.set_device(device)
+    from paper_2510_13602_b200.dist import bind_to_gpu_numa_node
+    numa_node = bind_to_gpu_numa_node(local_rank)  # before the pinned slow tier is allocated
     w = workload_dims(args, world)
     if args.gather == "auto":  # measured: the copy engine moves offloaded misses fastest over PCIe;
         # from a peer's HBM the SM gather is 30x faster than device-to-device copy-engine batches
@@ -501,6 +503,7 @@ def run_native(args, rank, world, local_rank):
                                         "around every kernel on its own stream (event nodes in the graph); "
                                         "value comes from the uninstrumented region",
                        "host_memory_limited_batch": w["host_limited"],
+                       "numa_node": numa_node,
                        "slow_tier": slow_tier + (" (loopback: the own HBM stands in for a peer)"
                                                  if peer_dev == local_rank else ""),
                        "l2": "no flush needed: attended KV per layer-step exceeds the 126 MB L2"},

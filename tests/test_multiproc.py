@@ -51,3 +51,13 @@ def test_gloo_world_size_two():
     assert res[0][1] == res[1][1] == 11.0
     assert res[0][2] == res[1][2] == [512.0, 300.0]
     assert res[0][0] == Shard(0, 2, 0, 256, 512) and res[1][0] == Shard(1, 2, 256, 256, 512)
+
+
+def test_cpulist_parsing_and_numa_binding(tmp_path):
+    from paper_2510_13602_b200.dist import bind_to_gpu_numa_node, parse_cpulist
+    assert parse_cpulist("0-3,8,10-11\n") == {0, 1, 2, 3, 8, 10, 11}
+    assert parse_cpulist("") == set()
+    # no GPU / NVML here: the binder must leave the affinity alone and report None
+    before = os.sched_getaffinity(0)
+    assert bind_to_gpu_numa_node(0, sysfs=str(tmp_path)) is None
+    assert os.sched_getaffinity(0) == before
