@@ -221,6 +221,16 @@ int nosa_step_graph_launch_host(NosaCtx* ctx, const NosaHostStepIO* io, void* st
 int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io);
 int nosa_step_graph_launch(NosaCtx* ctx, void* stream);
 
+/* ---- QKV projection (project_qkv, attention.py:67-90; DecodeEngine.step decode.py:162-164) --- */
+
+/* [q | k | v] = h · w_tᵀ on the tensor cores (tcgen05, fp32 accumulation in TMEM), rounded to bf16.
+ * h: device bf16 [m][k] (hidden states, row-major); w_t: device bf16 [n][k] (the columns of
+ * [W_q | W_k | W_v], each stored K-contiguous); q/k_out/v: device bf16 [m][nq], [m][nk],
+ * [m][n - nq - nk].  K is cut into `splits` ranges reduced in order (deterministic);
+ * work: device float32 [splits][m][n].  Needs n % 128 == 0 and k % (64 * splits) == 0. */
+int nosa_project_qkv(const void* h, int m, int k, const void* w_t, int n, int nq, int nk, void* q,
+                     void* k_out, void* v, float* work, int splits, void* stream);
+
 /* ---- standalone selector (drop-in for nosa_select / infllmv2_select on given scores) --- */
 
 /* n_prob independent selections.  s_q, s_e: device float64 [n_prob][stride] block scores.

@@ -4,9 +4,11 @@
 `step(h_t, selector) -> StepOutput` keeps the reference signatures and meanings
 (decode.py:106-194): hidden states in, per-KV-head `SelectionResult`s and
 (n_head, d_head) outputs out, the new token appended after attention.  The QKV projection
-(project_qkv, attention.py:67-90) runs on the GPU as one plain library GEMM (torch.matmul ->
-cuBLAS) into the engine's storage dtype; selection, attention, the eviction score and the
-append run in the sm_100a kernels behind the C ABI.  Like the reference engine, all KV stays
+(project_qkv, attention.py:67-90) runs on the GPU: for bf16 caches on the tensor cores
+(`projection.QKVProjection`, the tcgen05 GEMM behind `nosa_project_qkv`) when the shapes
+tile (n % 128 == 0, d % 64 == 0), otherwise and for fp32 caches as an fp32 library GEMM
+(torch.matmul -> cuBLAS); selection, attention, the eviction score and the append run in the
+sm_100a kernels behind the C ABI.  Like the reference engine, all KV stays
 resident (every block is placed in an HBM slot at prefill).
 
 `ModelWeights.random` and `EvictionHead` mirror decode.py:32-53 and attention.py:104-118
@@ -22,6 +24,7 @@ import torch
 
 from .config import AttentionConfig
 from .engine import NosaEngine
+from .projection import QKVProjection
 from .selection import SelectionResult
 
 VARIANTS = ("retaining", "dma", "ed-dma", "s-dma")
@@ -85,8 +88,12 @@ class DecodeEngine:
         w = np.concatenate([weights.w_q, weights.w_k, weights.w_v], axis=1)
         if w.shape[0] != config.d:
             raise ValueError(f"weights expect width {w.shape[0]}, config.d is {config.d}")
-        self._w = torch.as_tensor(w, dtype=torch.float32, device=dev)
         self._split = (config.n_head * config.d_head, config.n_kv_head * config.d_head)
+        self._tc = None
+        if dtype == "bf16" and w.shape[1] % 128 == 0 and config.d % 64 == 0:
+            self._tc = QKVProjection(weights.w_q, weights.w_k, weights.w_v, device=dev.index or 0)
+        else:
+            self._w = torch.as_tensor(w, dtype=torch.float32, device=dev)
         self.geometry = None
 
     @property
@@ -94,8 +101,10 @@ class DecodeEngine:
         return int(self._eng._t[0, 0])
 
     def _project(self, h: np.ndarray):
+        if self._tc is not None:  # tcgen05 GEMM, bf16 operands, fp32 accumulation
+            return self._tc(torch.as_tensor(np.asarray(h, dtype=np.float32)).to(self._tc.device))
         x = torch.as_tensor(np.asarray(h, dtype=np.float32), device=self._w.device)
-        y = x @ self._w  # the projection GEMM (cuBLAS)
+        y = x @ self._w  # the projection GEMM (cuBLAS, fp32)
         q, k, v = torch.split(y, [self._split[0], self._split[1], self._split[1]], dim=-1)
         return q, k, v
 

@@ -1,0 +1,35 @@
+"""Time the tcgen05 QKV projection (nosa_project_qkv) against cuBLAS (torch bf16 matmul) on the
+1B attention shape: d = 2048, n = (16 + 2 + 2) x 128 = 2560 (not product code)."""
+import json
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+import torch
+from paper_2510_13602_b200.projection import QKVProjection, _splits
+
+d, hq, hkv, dh = 2048, 16, 2, 128
+rng = np.random.default_rng(0)
+w_q, w_k, w_v = (rng.standard_normal((d, h * dh)) / np.sqrt(d) for h in (hq, hkv, hkv))
+proj = QKVProjection(w_q, w_k, w_v)
+wt = proj.w_t
+rows = []
+for m in (1, 32, 128, 512, 3584):
+    h = torch.randn(m, d, device="cuda").to(torch.bfloat16)
+    def timeit(fn, it=50):
+        for _ in range(5):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(it):
+            fn()
+        b.record(); torch.cuda.synchronize()
+        return a.elapsed_time(b) / it * 1e3
+    ours = timeit(lambda: proj(h))
+    cub = timeit(lambda: h @ wt.T)
+    byts = wt.numel() * 2 + h.numel() * 2 + m * wt.shape[0] * 2
+    flops = 2 * m * d * wt.shape[0]
+    rows.append({"m": m, "splits": _splits(m, wt.shape[0], d), "tcgen05_us": round(ours, 2), "cublas_us": round(cub, 2),
+                 "tcgen05_GBps": round(byts / ours / 1e3, 1), "tcgen05_TFLOPs": round(flops / ours / 1e6, 2)})
+print(json.dumps(rows, indent=1))
