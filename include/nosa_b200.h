@@ -226,10 +226,11 @@ int nosa_step_graph_launch(NosaCtx* ctx, void* stream);
 /* [q | k | v] = h · w_tᵀ on the tensor cores (tcgen05, fp32 accumulation in TMEM), rounded to bf16.
  * h: device bf16 [m][k] (hidden states, row-major); w_t: device bf16 [n][k] (the columns of
  * [W_q | W_k | W_v], each stored K-contiguous); q/k_out/v: device bf16 [m][nq], [m][nk],
- * [m][n - nq - nk].  K is cut into `splits` ranges reduced in order (deterministic);
- * work: device float32 [splits][m][n].  Needs n % 128 == 0 and k % (64 * splits) == 0. */
+ * [m][n - nq - nk].  K is cut into `splits` (1..8) ranges computed by one thread-block cluster
+ * and summed through distributed shared memory in rank order (deterministic).
+ * Needs n % 128 == 0 and k % (64 * splits) == 0. */
 int nosa_project_qkv(const void* h, int m, int k, const void* w_t, int n, int nq, int nk, void* q,
-                     void* k_out, void* v, float* work, int splits, void* stream);
+                     void* k_out, void* v, int splits, void* stream);
 
 /* ---- standalone selector (drop-in for nosa_select / infllmv2_select on given scores) --- */
 

@@ -28,8 +28,8 @@ cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, b
 cudaError_t launch_stage_inputs(const void* const* src, void* const* dst, const size_t* bytes, int grid,
                                 cudaStream_t st);
 const void* stage_inputs_kernel_fn();
-cudaError_t launch_project(const void* A, const void* Bt, int M, int N, int K, int splits, float* work, void* q,
-                           void* k, void* v, int nq, int nk, cudaStream_t st);
+cudaError_t launch_project(const void* A, const void* Bt, int M, int N, int K, int splits, void* q, void* k, void* v,
+                           int nq, int nk, cudaStream_t st);
 
 cudaError_t launch_prefill(const Dev& dv, int layer, int seq_begin, int S, const void* k,
                            const void* v, int t, char* staging, cudaStream_t st);
@@ -834,13 +834,13 @@ extern "C" int nosa_ktime_read(NosaCtx* ctx, double* span_us) {
 }
 
 extern "C" int nosa_project_qkv(const void* h, int m, int k, const void* w_t, int n, int nq, int nk, void* q,
-                                void* k_out, void* v, float* work, int splits, void* stream) {
-  if (!h || !w_t || !q || !k_out || !v || !work) return fail(nullptr, NOSA_ERR_VALUE, "project_qkv: NULL argument");
-  if (m <= 0 || k <= 0 || n <= 0 || splits <= 0 || nq < 0 || nk < 0 || nq + nk > n)
-    return fail(nullptr, NOSA_ERR_VALUE, "project_qkv: bad shape");
+                                void* k_out, void* v, int splits, void* stream) {
+  if (!h || !w_t || !q || !k_out || !v) return fail(nullptr, NOSA_ERR_VALUE, "project_qkv: NULL argument");
+  if (m <= 0 || k <= 0 || n <= 0 || splits <= 0 || splits > 8 || nq < 0 || nk < 0 || nq + nk > n)
+    return fail(nullptr, NOSA_ERR_VALUE, "project_qkv: bad shape or splits (1..8)");
   if (n % 128 != 0 || k % (64 * splits) != 0)
     return fail(nullptr, NOSA_ERR_VALUE, "project_qkv: needs N %% 128 == 0 and K %% (64 * splits) == 0 (N=%d K=%d)", n, k);
-  cudaError_t e = nosa::launch_project(h, w_t, m, n, k, splits, work, q, k_out, v, nq, nk, S(stream));
+  cudaError_t e = nosa::launch_project(h, w_t, m, n, k, splits, q, k_out, v, nq, nk, S(stream));
   if (e != cudaSuccess) return fail(nullptr, NOSA_ERR_CUDA, "project_qkv: %s", cudaGetErrorString(e));
   return NOSA_OK;
 }

@@ -4,12 +4,19 @@
 //   C[M][N] = A[M][K] · B[N][K]ᵀ,  A = hidden states (bf16, row-major), B = the concatenated
 //   [W_q | W_k | W_v] transposed to [N][K] (bf16, K-major), fp32 accumulation in TMEM.
 //
-// One CTA computes a 128 x 128 tile over a K range (deterministic split-K: partials go to a
-// [ksplit][M][N] f32 workspace, `project_reduce_kernel` sums them in split order and writes bf16
-// q / k / v).  Tiles of 128 rows x 64 bf16 (128 B) are staged with cp.async into 128B-swizzled
-// shared memory (16-byte chunk c of row r at c ^ (r & 7)), 4 stages deep; one elected thread
-// issues tcgen05.mma (M=128, N=128, K=16 per instruction, 4 per stage) and tcgen05.commit frees
-// each stage through an mbarrier; the epilogue reads the accumulator back with tcgen05.ld.
+// Grid (N/128, ceil(M/128), splits), clusters of `splits` CTAs along K.  Each CTA:
+//   warp 0 lane 0  TMA producer: 128 x 64 bf16 boxes of A and B (128B swizzle) into a 4-stage
+//                  ring, one mbarrier with the byte count per stage;
+//   warp 1 lane 0  MMA issuer: tcgen05.mma M=128 N=128 K=16 (4 per stage) into a 128-column
+//                  TMEM accumulator, tcgen05.commit frees each stage;
+//   all 4 warps    epilogue: tcgen05.ld of the accumulator (warp w = TMEM lanes 32w..) into
+//                  the CTA's shared memory.
+// The split-K partials are then summed across the cluster through distributed shared memory in
+// rank order (deterministic, no global workspace, no second launch): CTA rank j reduces rows
+// [j*128/S, (j+1)*128/S) of the tile and writes them as bf16 into q | k | v.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdint>
 
@@ -18,7 +25,9 @@
 namespace nosa {
 
 constexpr int PM = 128, PN = 128, PK = 64, PSTAGES = 4, PTHREADS = 128;
-constexpr int P_TILE_BYTES = PM * PK * 2;  // 16 KiB per operand tile
+constexpr int P_TILE_BYTES = PM * PK * 2;  // 16 KiB per operand box
+constexpr int P_EPI_LD = PN + 4;           // padded f32 row of the partial tile in smem
+constexpr int P_MAX_SPLITS = 8;            // portable cluster size
 
 // UMMA shared-memory descriptor: K-major operand, 128B swizzle, 8-row atoms 1024 B apart
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
@@ -36,41 +45,60 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int m, int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
-  const int bytes = valid ? 16 : 0;  // 0: zero-fill (rows past M)
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes));
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
 }
 
-// 128 rows x 64 bf16 of a row-major [rows][ld] matrix -> swizzled smem tile
-__device__ __forceinline__ void load_tile(uint32_t sdst, const __nv_bfloat16* __restrict__ g, int ld, int row0,
-                                          int rows, int k0) {
-#pragma unroll
-  for (int j = 0; j < (PM * PK / 8) / PTHREADS; ++j) {
-    const int c = threadIdx.x + j * PTHREADS;
-    const int r = c >> 3, ch = c & 7;
-    const bool ok = row0 + r < rows;
-    const __nv_bfloat16* src = g + (size_t)(ok ? row0 + r : 0) * ld + k0 + ch * 8;
-    cp_async16(sdst + r * 128 + ((ch ^ (r & 7)) << 4), src, ok);
-  }
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// (not volatile: the loads of all ranks may be issued back to back; the cluster barriers order
+// them against the partial-tile writes)
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t local_addr, uint32_t rank) {
+  uint32_t raddr;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(local_addr), "r"(rank));
+  float4 v;
+  asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(raddr));
+  return v;
 }
 
 __global__ void __launch_bounds__(PTHREADS, 1)
-    project_gemm_kernel(const __nv_bfloat16* __restrict__ A, const __nv_bfloat16* __restrict__ B, int M, int N,
-                        int K, int k_per_split, float* __restrict__ part) {
+    project_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
+                        int N, int k_per_split, int nq, int nk, __nv_bfloat16* __restrict__ q,
+                        __nv_bfloat16* __restrict__ k, __nv_bfloat16* __restrict__ v) {
   extern __shared__ __align__(1024) char smem_raw[];
-  // 1024-byte aligned stage buffers (the swizzle atoms must start on 1024 B)
-  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  char* base_ptr = smem_raw + (base - smem_u32(smem_raw));
+  // 1024-byte aligned stage buffers (the swizzle atoms must start on 1024 B); the same bytes
+  // hold the f32 partial tile after the main loop
+  const uint32_t raw = smem_u32(smem_raw), base = (raw + 1023u) & ~1023u;
+  char* base_ptr = smem_raw + (base - raw);
   const uint32_t sA = base, sB = base + PSTAGES * P_TILE_BYTES;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(base_ptr + 2 * PSTAGES * P_TILE_BYTES);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + PSTAGES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base_ptr + 2 * PSTAGES * P_TILE_BYTES);
+  uint64_t* empty = full + PSTAGES;
+  uint64_t* done = empty + PSTAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  float* tile = reinterpret_cast<float*>(base_ptr);  // [PM][P_EPI_LD] after the main loop
 
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int n0 = blockIdx.x * PN, m0 = blockIdx.y * PM, split = blockIdx.z;
-  const int kbeg = split * k_per_split, nk = k_per_split / PK;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n0 = blockIdx.x * PN, m0 = blockIdx.y * PM;
+  const int splits = gridDim.z;
+  const uint32_t rank = cluster_rank();  // = blockIdx.z: clusters span the whole K dimension
+  const int kbeg = blockIdx.z * k_per_split, nkt = k_per_split / PK;
 
   if (tid == 0) {
-    for (int s = 0; s < PSTAGES; ++s) mbar_init(&mbar[s], 1);
+    for (int s = 0; s < PSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
     fence_mbar_init();
   }
   if (warp == 0) {  // accumulator: 128 lanes x 128 f32 columns of TMEM
@@ -78,36 +106,27 @@ __global__ void __launch_bounds__(PTHREADS, 1)
                  "r"(PN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // prologue: k-tiles 0 .. PSTAGES-2 in flight
-  for (int s = 0; s < PSTAGES - 1; ++s) {
-    if (s < nk) {
-      load_tile(sA + s * P_TILE_BYTES, A, K, m0, M, kbeg + s * PK);
-      load_tile(sB + s * P_TILE_BYTES, B, K, n0, N, kbeg + s * PK);
-    }
-    asm volatile("cp.async.commit_group;");
-  }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
-  constexpr uint32_t idesc = idesc_bf16_f32(PM, PN);
 
-  for (int kt = 0; kt < nk; ++kt) {
-    // refill: k-tile kt + PSTAGES - 1 goes into the stage the MMA of k-tile kt - 1 used
-    const int nt = kt + PSTAGES - 1;
-    if (nt < nk) {
-      const int ns = nt % PSTAGES;
-      if (nt >= PSTAGES) mbar_wait(&mbar[ns], ((nt - PSTAGES) / PSTAGES) & 1);
-      load_tile(sA + ns * P_TILE_BYTES, A, K, m0, M, kbeg + nt * PK);
-      load_tile(sB + ns * P_TILE_BYTES, B, K, n0, N, kbeg + nt * PK);
-    }
-    asm volatile("cp.async.commit_group;");
-    asm volatile("cp.async.wait_group %0;" ::"n"(PSTAGES - 1));  // this thread's copies of k-tile kt landed
-    asm volatile("fence.proxy.async.shared::cta;");             // visible to the tensor core (async proxy)
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer
+    for (int kt = 0; kt < nkt; ++kt) {
       const int s = kt % PSTAGES;
+      if (kt >= PSTAGES) mbar_wait(&empty[s], ((kt / PSTAGES) - 1) & 1);
+      mbar_expect_tx(&full[s], 2 * P_TILE_BYTES);
+      tma_load_2d(sA + s * P_TILE_BYTES, &map_a, kbeg + kt * PK, m0, &full[s]);
+      tma_load_2d(sB + s * P_TILE_BYTES, &map_b, kbeg + kt * PK, n0, &full[s]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer
+    constexpr uint32_t idesc = idesc_bf16_f32(PM, PN);
+    for (int kt = 0; kt < nkt; ++kt) {
+      const int s = kt % PSTAGES;
+      mbar_wait(&full[s], (kt / PSTAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int ks = 0; ks < PK / 16; ++ks) {  // K = 16 per instruction: +32 B inside the swizzled row
         const uint64_t ad = umma_desc_sw128(sA + s * P_TILE_BYTES + ks * 32);
@@ -119,16 +138,16 @@ __global__ void __launch_bounds__(PTHREADS, 1)
             "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(&mbar[s])));
+          smem_u32(&empty[s])));
     }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(done)));
   }
-  // the last commit completes after every MMA of the tile
-  if (nk > 0) mbar_wait(&mbar[(nk - 1) % PSTAGES], ((nk - 1) / PSTAGES) & 1);
-  asm volatile("tcgen05.fence::after_thread_sync;");
+  __syncwarp();
 
-  // epilogue: warp w owns TMEM lanes (tile rows) 32w .. 32w+31; 32 columns per tcgen05.ld
-  const int row = m0 + warp * 32 + (tid & 31);
-  float* dst = part + ((size_t)split * M + row) * N + n0;
+  // ---- epilogue: accumulator -> this CTA's f32 partial tile in shared memory
+  mbar_wait(done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const int trow = warp * 32 + lane;
 #pragma unroll 1
   for (int c0 = 0; c0 < PN; c0 += 32) {
     uint32_t r[32];
@@ -142,52 +161,100 @@ __global__ void __launch_bounds__(PTHREADS, 1)
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;");
-    if (row < M) {
+    float* dst = tile + trow * P_EPI_LD + c0;
 #pragma unroll
-      for (int j = 0; j < 32; j += 4)
-        *reinterpret_cast<float4*>(dst + c0 + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                                               __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-    }
+    for (int j = 0; j < 32; j += 4)
+      *reinterpret_cast<float4*>(dst + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                        __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
+  cluster_sync();  // every CTA's partial is in its shared memory (and the MMA smem reads are over)
+
+  // ---- split-K reduction over the cluster in rank order; rank j owns rows [r0, r1) of the tile
+  const int r0 = (int)rank * PM / splits, r1 = ((int)rank + 1) * PM / splits;
+  const uint32_t tile_addr = smem_u32(tile);
+  for (int x = tid; x < (r1 - r0) * (PN / 4); x += PTHREADS) {
+    const int rr = r0 + x / (PN / 4), c4 = (x % (PN / 4)) * 4;
+    const uint32_t off = tile_addr + (uint32_t)(rr * P_EPI_LD + c4) * 4u;
+    float4 part[P_MAX_SPLITS];
+#pragma unroll
+    for (int j = 0; j < P_MAX_SPLITS; ++j)  // every rank's partial in flight before the sum
+      if (j < splits) part[j] = ld_dsmem_f4(off, (uint32_t)j);
+    float4 acc = part[0];
+#pragma unroll
+    for (int j = 1; j < P_MAX_SPLITS; ++j) {
+      if (j < splits) {
+        acc.x += part[j].x;
+        acc.y += part[j].y;
+        acc.z += part[j].z;
+        acc.w += part[j].w;
+      }
+    }
+    const int m = m0 + rr;
+    if (m < M) {
+      const float vals[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int n = n0 + c4 + e;
+        const __nv_bfloat16 b = __float2bfloat16_rn(vals[e]);
+        if (n < nq) q[(size_t)m * nq + n] = b;
+        else if (n < nq + nk) k[(size_t)m * nk + (n - nq)] = b;
+        else v[(size_t)m * (N - nq - nk) + (n - nq - nk)] = b;
+      }
+    }
+  }
+  cluster_sync();  // the partials stay readable until every rank is done
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(PN));
 }
 
-// sum of the split-K partials in split order, cast to bf16, columns split into q | k | v
-__global__ void project_reduce_kernel(const float* __restrict__ part, int splits, int M, int N, int nq, int nk,
-                                      __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ k,
-                                      __nv_bfloat16* __restrict__ v) {
-  const size_t total = (size_t)M * N;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    float acc = 0.0f;
-    for (int s = 0; s < splits; ++s) acc += part[(size_t)s * total + i];
-    const int m = (int)(i / N), n = (int)(i - (size_t)m * N);
-    const __nv_bfloat16 x = __float2bfloat16_rn(acc);
-    if (n < nq) q[(size_t)m * nq + n] = x;
-    else if (n < nq + nk) k[(size_t)m * nk + (n - nq)] = x;
-    else v[(size_t)m * (N - nq - nk) + (n - nq - nk)] = x;
-  }
+size_t project_smem_bytes() {
+  const size_t ring = 2 * (size_t)PSTAGES * P_TILE_BYTES, epi = (size_t)PM * P_EPI_LD * 4;
+  return 1024 + std::max(ring, epi) + (2 * PSTAGES + 1) * 8 + 16;
 }
 
-size_t project_smem_bytes() { return 1024 + 2 * (size_t)PSTAGES * P_TILE_BYTES + PSTAGES * 8 + 16; }
+static bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};  // innermost (K) first
+  const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  const cuuint32_t box[2] = {PK, PM};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;  // rows past M read as zeros
+}
 
-// splits: K is cut into `splits` ranges of whole 64-wide k-tiles (K % (64 * splits) == 0)
-cudaError_t launch_project(const void* A, const void* Bt, int M, int N, int K, int splits, float* work, void* q,
-                           void* k, void* v, int nq, int nk, cudaStream_t st) {
+// splits (1..8, a cluster along K): K is cut into `splits` ranges of whole 64-wide k-tiles
+cudaError_t launch_project(const void* A, const void* Bt, int M, int N, int K, int splits, void* q, void* k, void* v,
+                           int nq, int nk, cudaStream_t st) {
+  if (splits < 1 || splits > P_MAX_SPLITS || K % (PK * splits) || N % PN) return cudaErrorInvalidValue;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, M, K) || !make_map(&mb, Bt, N, K)) return cudaErrorInvalidValue;
   const size_t smem = project_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(project_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   max_shared_carveout(project_gemm_kernel);
-  const dim3 grid(N / PN, (M + PM - 1) / PM, splits);
-  project_gemm_kernel<<<grid, PTHREADS, smem, st>>>(static_cast<const __nv_bfloat16*>(A),
-                                                     static_cast<const __nv_bfloat16*>(Bt), M, N, K, K / splits, work);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  const int threads = 256, blocks = (int)std::min<size_t>(((size_t)M * N + threads - 1) / threads, 4096);
-  project_reduce_kernel<<<blocks, threads, 0, st>>>(work, splits, M, N, nq, nk, static_cast<__nv_bfloat16*>(q),
-                                                    static_cast<__nv_bfloat16*>(k), static_cast<__nv_bfloat16*>(v));
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(N / PN, (M + PM - 1) / PM, splits);
+  cfg.blockDim = dim3(PTHREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = splits;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, project_gemm_kernel, ma, mb, M, N, K / splits, nq, nk,
+                            static_cast<__nv_bfloat16*>(q), static_cast<__nv_bfloat16*>(k),
+                            static_cast<__nv_bfloat16*>(v));
 }
 
 }  // namespace nosa

@@ -3,13 +3,12 @@
 `QKVProjection` holds [W_q | W_k | W_v] as one bf16 [n][d] matrix on the device (each output
 column's weights contiguous, the K-major operand of the tcgen05 GEMM in csrc/nosa_project.cu)
 and maps hidden states h [m][d] to bf16 q [m][n_q], k [m][n_kv], v [m][n_kv] through the C ABI
-`nosa_project_qkv`.  fp32 accumulation in TMEM; split-K partials reduced in a fixed order, so a
-projection is bitwise reproducible.
+`nosa_project_qkv`.  fp32 accumulation in TMEM; the split-K partials of a thread-block cluster
+are summed through distributed shared memory in rank order, so a projection is bitwise
+reproducible.
 """
 
 from __future__ import annotations
-
-import ctypes
 
 import numpy as np
 import torch
@@ -20,10 +19,14 @@ NUM_SMS = 148
 
 
 def _splits(m: int, n: int, k: int) -> int:
-    """Enough K splits that the 128 x 128 tiles fill about one wave of SMs."""
+    """K splits per 128 x 128 tile (a cluster of that many CTAs).  Measured on the 1B shape
+    (d = 2048, n = 2560, profiles/r1_projection.txt): 4 splits are fastest while the tiles fill
+    well under a wave (m <= 128: 9 us; 8 splits 15 us, 1 split 15-19 us), one split once the
+    tiles alone fill the SMs."""
     tiles = (n // 128) * -(-m // 128)
     kt = k // 64
-    want = max(1, min(kt, -(-NUM_SMS // max(tiles, 1))))
+    want = 4 if tiles * 4 <= 2 * NUM_SMS else 1
+    want = max(1, min(want, kt))
     while kt % want:
         want -= 1
     return want
@@ -39,22 +42,18 @@ class QKVProjection:
         self.device = torch.device("cuda", device)
         self.w_t = torch.as_tensor(np.ascontiguousarray(w.T), dtype=torch.float32).to(
             device=self.device, dtype=torch.bfloat16).contiguous()
-        self._work = None
 
-    def __call__(self, h: torch.Tensor):
+    def __call__(self, h: torch.Tensor, splits: int | None = None):
         """h: [m][d] (any float dtype, on the device) -> bf16 (q, k, v) on the same device."""
         h = h.to(device=self.device, dtype=torch.bfloat16).contiguous()
         m = h.shape[0]
-        splits = _splits(m, self.n, self.d)
-        need = splits * m * self.n
-        if self._work is None or self._work.numel() < need:
-            self._work = torch.empty(need, dtype=torch.float32, device=self.device)
+        splits = splits or _splits(m, self.n, self.d)
         nv = self.n - self.nq - self.nk
         q = torch.empty((m, self.nq), dtype=torch.bfloat16, device=self.device)
         k = torch.empty((m, self.nk), dtype=torch.bfloat16, device=self.device)
         v = torch.empty((m, nv), dtype=torch.bfloat16, device=self.device)
         with torch.cuda.device(self.device):
             _lib.check(_lib.lib.nosa_project_qkv(h.data_ptr(), m, self.d, self.w_t.data_ptr(), self.n, self.nq, self.nk,
-                                                 q.data_ptr(), k.data_ptr(), v.data_ptr(),
-                                                 ctypes.c_void_p(self._work.data_ptr()), splits, _lib.stream_ptr()))
+                                                 q.data_ptr(), k.data_ptr(), v.data_ptr(), splits,
+                                                 _lib.stream_ptr()))
         return q, k, v
