@@ -348,7 +348,6 @@ def run_native(args, rank, world, local_rank):
             h.copy_(x)
             return h
         host_in = [tuple(pinned(x) for x in step_in) for step_in in inputs_e2e]
-        dq, dk, dv = (torch.empty_like(x) for x in inputs[0])
         host_out = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
         if world > 1:
             dist.barrier()

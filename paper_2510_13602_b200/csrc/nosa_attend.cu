@@ -146,8 +146,8 @@ __device__ void finalize_bh(const Dev& dv, int layer, int bh, int nc, const T* _
   // ---- (1) merge the split-K records in record order (deterministic), thread -> (query, 4 dims)
   {
     const int D4 = D / 4;
-    const float2* ml = part_ml_of(dv, layer) + (size_t)bh * dv.max_rec * G;
-    const float4* po = reinterpret_cast<const float4*>(part_o_of(dv, layer) + (size_t)bh * dv.max_rec * G * D);
+    const float2* ml = part_ml_of(dv, layer) + (size_t)bh * dv.max_chunks * G;
+    const float4* po = reinterpret_cast<const float4*>(part_o_of(dv, layer) + (size_t)bh * dv.max_chunks * G * D);
     for (int x = tid; x < G * D4; x += nthr) {
       const int q = x / D4, d4 = x - q * D4;
       float M = -INFINITY, L = 0.0f;
@@ -213,7 +213,7 @@ __device__ void finalize_bh(const Dev& dv, int layer, int bh, int nc, const T* _
     }
   }
   // eviction-head column sums: row-group partials -> silu per column
-  double* red = reinterpret_cast<double*>(wsm);  // [nthr] (the record weights are no longer needed)
+  double* red = reinterpret_cast<double*>(wsm);  // [nthr]
   if (ev_fast) {
     red[tid] = part;
     __syncthreads();
@@ -315,7 +315,6 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
   int* tmp = reinterpret_cast<int*>(p);               p += T::THREADS * 4;
   int* flag = reinterpret_cast<int*>(p);              p += 64;
   int* cbase = reinterpret_cast<int*>(p);             p += (size_t)(BH + 1) * 4;
-  float* wsm = reinterpret_cast<float*>(p);           // [max_chunks * G]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned long long t_start = dv.ktime ? globaltimer_ns() : 0ull;
@@ -570,7 +569,7 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
             }
         named_sync(kBarConsumers, T::NCW * 32);
         const int ci = it.ci, rl = layer + it.bh / BHL;  // the record's layer and (b, h)
-        const size_t pb0 = (size_t)(it.bh % BHL) * dv.max_rec + ci;  // rpc = 1
+        const size_t pb0 = (size_t)(it.bh % BHL) * dv.max_chunks + ci;
         for (int x = tid; x < G * DH; x += T::NCW * 32) {
           const int qq = x / DH, d = x - qq * DH;
           float M = -INFINITY;
@@ -621,7 +620,6 @@ __global__ void __launch_bounds__(32)
   int* ring = reinterpret_cast<int*>(ps + GM * NBK);     // [RING]
   int* tmp = ring + RING;                                // [32]
   int* cbase = tmp + 32;                                 // [BH+1]
-  float* wsm = reinterpret_cast<float*>(cbase + BH + 1); // [max_chunks * G]
   const int lane = threadIdx.x;
   const int G = dv.G;
   if (lane == 0) {
@@ -757,7 +755,7 @@ __global__ void __launch_bounds__(32)
     ++cp_i;
     advance_loader();
     if (cp_i >= cp_end) {
-      const size_t pbase = (size_t)cp_bh * dv.max_rec + cp_ci;  // rpc = 1
+      const size_t pbase = (size_t)cp_bh * dv.max_chunks + cp_ci;
 #pragma unroll
       for (int gg = 0; gg < GM; ++gg) {
         if (gg >= G) break;
@@ -781,10 +779,10 @@ __global__ void __launch_bounds__(kFinThreads)
   // grid (B*H, layers): layer = layer0 + blockIdx.y, its k/v rows and outputs one layer stride on
   extern __shared__ __align__(16) char fin_smem[];
   double* zsm = reinterpret_cast<double*>(fin_smem);           // [n_ev]
-  float* wsm = reinterpret_cast<float*>(zsm + dv.n_ev);         // [max_chunks * G] float2
+  float* wsm = reinterpret_cast<float*>(zsm + dv.n_ev);         // [kFinThreads] f64 reduction scratch
   const int bh = blockIdx.x, layer = layer0 + blockIdx.y;
   const size_t kst = (size_t)dv.B * dv.H * dv.D, ost = (size_t)dv.B * dv.Hq * dv.D;
-  const int nc = (dv.n_req[layer * dv.B * dv.H + bh] + dv.chunk - 1) / dv.chunk * dv.rpc;
+  const int nc = (dv.n_req[layer * dv.B * dv.H + bh] + dv.chunk - 1) / dv.chunk;
   if (nc == 0) return;  // the plan failed for this manager (CapacityExceeded): no step
   finalize_bh<T>(dv, layer, bh, nc, kn0 + blockIdx.y * kst, vn0 + blockIdx.y * kst, out0 + blockIdx.y * ost, wsm, zsm);
 }
@@ -792,7 +790,7 @@ __global__ void __launch_bounds__(kFinThreads)
 // layers [layer, layer + nl): kn/vn/out point at layer `layer`'s rows
 cudaError_t launch_finalize(const Dev& dv, int layer, const void* kn, const void* vn, float* out, cudaStream_t st,
                             int nl) {
-  const size_t smem = (size_t)dv.n_ev * 8 + std::max((size_t)dv.max_rec * dv.G * 8, (size_t)kFinThreads * 8);
+  const size_t smem = (size_t)dv.n_ev * 8 + (size_t)kFinThreads * 8;
   const dim3 grid(dv.B * dv.H, nl);
   if (dv.dtype == 0) {
     auto k = finalize_kernel<__nv_bfloat16>;
@@ -814,7 +812,7 @@ template <int NBK, int DH, int NQT>
 static cudaError_t launch_bf16(const Dev& dv, int layer, int nl, const void* q, cudaStream_t st, int num_sms) {
   using T = BF<NBK, DH, NQT>;
   const int BH = nl * dv.B * dv.H;
-  const size_t smem = bf_smem_fixed<NBK, DH, NQT>() + (size_t)(BH + 1) * 4 + (size_t)dv.max_chunks * dv.G * 4 + 64;
+  const size_t smem = bf_smem_fixed<NBK, DH, NQT>() + (size_t)(BH + 1) * 4 + 64;
   auto k = attend_bf16_kernel<NBK, DH, NQT>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -831,7 +829,7 @@ static cudaError_t launch_f32(const Dev& dv, int layer, const void* q, const voi
   constexpr int BPB = 2 * NBK * DH * 4;
   const int BH = dv.B * dv.H;
   const size_t smem = (size_t)NS * BPB + NS * 8 + 16 * DH * 4 + 16 * NBK * 4 + (NS + 2) * 4 + 32 * 4 +
-                      (BH + 1) * 4 + (size_t)dv.max_chunks * dv.G * 4 + 64;
+                      (BH + 1) * 4 + 64;
   auto k = attend_f32_kernel<NBK, DH, NS>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

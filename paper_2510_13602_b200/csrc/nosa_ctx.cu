@@ -341,8 +341,6 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   }
   if (const char* e = getenv("NOSA_CHUNK")) dv.chunk = std::max(1, std::min(atoi(e), nosa::kChunk));
   dv.max_chunks = (dv.C + dv.chunk - 1) / dv.chunk;
-  dv.rpc = 1;  // the bf16 kernel combines its consumer warps' partials before writing a record
-  dv.max_rec = dv.max_chunks * dv.rpc;
   // layers per attention launch (pipelined schedule): when every block of a sequence fits in
   // HBM the step is HBM-bound and per-launch ramp-up/drain is the loss, so 4 layers share one
   // persistent launch; with offloaded blocks each layer's attention waits only for its own
@@ -401,8 +399,8 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   ALLOC(dv.plan_n, LBH * 3);
   ALLOC(dv.cnt, (size_t)dv.L * 2);
   ALLOC(dv.miss_list, (size_t)dv.L * BH * dv.C);
-  ALLOC(dv.part_o, (size_t)dv.nbuf * BH * dv.max_rec * dv.G * dv.D);
-  ALLOC(dv.part_ml, (size_t)dv.nbuf * BH * dv.max_rec * dv.G);
+  ALLOC(dv.part_o, (size_t)dv.nbuf * BH * dv.max_chunks * dv.G * dv.D);
+  ALLOC(dv.part_ml, (size_t)dv.nbuf * BH * dv.max_chunks * dv.G);
   ALLOC(dv.newrow, LBH * 2 * dv.D * (size_t)dv.elem);
   ALLOC(dv.w1, (size_t)dv.D * dv.n_ev);
   ALLOC(dv.w2, (size_t)dv.n_ev);

@@ -34,8 +34,6 @@ struct Dev {
   long long bpb;                 // bytes per block
   int chunk;                     // KV blocks per attention work item, 1..kChunk
   int max_chunks;                // ceil(C / chunk)
-  int rpc;                       // split-K records per chunk: one per consumer warp (bf16), 1 (fp32)
-  int max_rec;                   // max_chunks * rpc records per (b, h)
   int nbuf;                      // split-K record buffers (layer l uses buffer l % nbuf)
   // ---- persistent state ----------------------------------------------------------------
   char* pool;
@@ -104,10 +102,10 @@ __host__ __device__ __forceinline__ int shared_rel(const Dev& dv, int b, int s) 
 
 // the split-K record buffer of a layer (nbuf buffers: attention batches are double-buffered)
 __host__ __device__ __forceinline__ float* part_o_of(const Dev& dv, int layer) {
-  return dv.part_o + (size_t)(layer % dv.nbuf) * dv.B * dv.H * dv.max_rec * dv.G * dv.D;
+  return dv.part_o + (size_t)(layer % dv.nbuf) * dv.B * dv.H * dv.max_chunks * dv.G * dv.D;
 }
 __host__ __device__ __forceinline__ float2* part_ml_of(const Dev& dv, int layer) {
-  return dv.part_ml + (size_t)(layer % dv.nbuf) * dv.B * dv.H * dv.max_rec * dv.G;
+  return dv.part_ml + (size_t)(layer % dv.nbuf) * dv.B * dv.H * dv.max_chunks * dv.G;
 }
 
 // Every kernel of the step asks for the maximum shared-memory carveout, so an SM never has to
