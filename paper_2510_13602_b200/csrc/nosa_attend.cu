@@ -261,8 +261,10 @@ struct BF {
   static constexpr int MTD = DH / 16;                   // head-dim m-tiles (PV)
   static constexpr int KS = DH / 16;                    // k-steps (QK)
   static constexpr int QMAX = 8 * NQT;                  // queries per (b, h), padded to n-tiles
-  static constexpr int QSLOT = QMAX * DH * 2;
-  static constexpr int COMB = NCW * QMAX * DH * 4 + NCW * QMAX * 8;
+  static constexpr int QROW = DH * 2 + 16;               // padded query row: fragment loads hit 8 banks
+  static constexpr int QSLOT = QMAX * QROW;
+  static constexpr int CLD = DH + 4;                     // padded f32 row of the warp-combine buffer
+  static constexpr int COMB = NCW * QMAX * CLD * 4 + NCW * QMAX * 8;
   static constexpr int NSR = (200 * 1024 - COMB) / (BPB + QSLOT);
   static constexpr int NS = NSR > 8 ? 8 : (NSR < 2 ? 2 : NSR);  // ring stages
   static constexpr int NQ = 3;                                  // chunk-metadata queue depth
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
   char* p = smem_raw;
   char* stages = p;                                   p += (size_t)T::NS * T::BPB;
   char* qslots = p;                                   p += (size_t)T::NS * T::QSLOT;
-  float* comb_o = reinterpret_cast<float*>(p);        p += (size_t)T::NCW * T::QMAX * DH * 4;
+  float* comb_o = reinterpret_cast<float*>(p);        p += (size_t)T::NCW * T::QMAX * T::CLD * 4;
   float2* comb_ml = reinterpret_cast<float2*>(p);     p += (size_t)T::NCW * T::QMAX * 8;
   uint64_t* full = reinterpret_cast<uint64_t*>(p);    p += T::NS * 8;
   uint64_t* empty = reinterpret_cast<uint64_t*>(p);   p += T::NS * 8;
@@ -410,7 +412,9 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
           bulk_g2s(stages + (size_t)s * T::BPB, dv.pool + ((size_t)lbh * dv.C + m.slot[i]) * (size_t)T::BPB, T::BPB,
                    &full[s]);
           if (qbytes)
-            bulk_g2s(qslots + (size_t)s * T::QSLOT, ql + ((size_t)b * dv.Hq + h * G) * DH, qbytes, &full[s]);
+            for (int r = 0; r < G; ++r)  // one bulk copy per query row into the padded slot
+              bulk_g2s(qslots + (size_t)s * T::QSLOT + r * T::QROW, ql + ((size_t)b * dv.Hq + h * G + r) * DH,
+                       DH * 2, &full[s]);
         }
       }
       __syncwarp();
@@ -440,7 +444,7 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
         for (int ks = 0; ks < T::KS; ++ks)
 #pragma unroll
           for (int nq = 0; nq < NQT; ++nq) {
-            const char* row = qs + (size_t)(8 * nq + g) * DH * 2;
+            const char* row = qs + (size_t)(8 * nq + g) * T::QROW;
             qb[ks][nq][0] = *reinterpret_cast<const unsigned*>(row + (16 * ks + 2 * tq) * 2);
             qb[ks][nq][1] = *reinterpret_cast<const unsigned*>(row + (16 * ks + 8 + 2 * tq) * 2);
           }
@@ -563,7 +567,7 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
           for (int nq = 0; nq < NQT; ++nq)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              float* row = comb_o + ((size_t)w * T::QMAX + 8 * nq + 2 * tq + e) * DH;
+              float* row = comb_o + ((size_t)w * T::QMAX + 8 * nq + 2 * tq + e) * T::CLD;
               row[16 * md + g] = o[md][nq][e];
               row[16 * md + g + 8] = o[md][nq][2 + e];
             }
@@ -580,7 +584,7 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
           for (int ww = 0; ww < T::NCW; ++ww) {
             const float2 ml = comb_ml[ww * T::QMAX + qq];
             const float f = ml.x == -INFINITY ? 0.0f : exp2f((ml.x - M) * kLog2e);
-            acc = fmaf(f, comb_o[((size_t)ww * T::QMAX + qq) * DH + d], acc);
+            acc = fmaf(f, comb_o[((size_t)ww * T::QMAX + qq) * T::CLD + d], acc);
             L = fmaf(f, ml.y, L);
           }
           part_o_of(dv, rl)[(pb0 * G + qq) * DH + d] = acc;
