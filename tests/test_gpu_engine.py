@@ -434,3 +434,53 @@ def test_graph_replay_matches_eager():
         outs.append(np.stack(res))
         eng.close()
     np.testing.assert_array_equal(outs[0], outs[1])  # same kernels, same decomposition: bitwise equal
+
+
+@pytest.mark.parametrize("selector", ["nosa", "infllmv2"])
+def test_full_context_invariants(selector):
+    """BASELINE config 3's context (32K tokens, 25% of blocks in HBM) through size-independent
+    properties: the picks are the argtopk of the exact f64 pool scores (read back), required =
+    sink U picks U recent, every required block is resident after the plan, the slot table is a
+    bijection on at most C slots, hits + misses = |required| and misses = |fetch|."""
+    from paper_2510_13602_b200 import one_b_config
+    cfg = one_b_config(65536)
+    B, L, T, steps = 4, 2, 32768, 4
+    max_tokens = T + steps + 2
+    nblk = -(-max_tokens // cfg.n_b)
+    C = nblk // 4
+    dev = torch.device("cuda", 0)
+    w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, 3)
+    eng = NosaEngine(cfg, batch=B, layers=L, max_tokens=max_tokens, fast_slots=C, w1=w1, w2=w2)
+    for l in range(L):
+        shape = (B, cfg.n_kv_head, T, cfg.d_head)
+        eng.prefill(workload.torch_prefix_kv(10 + 2 * l, shape, dev, torch.bfloat16),
+                    workload.torch_prefix_kv(11 + 2 * l, shape, dev, torch.bfloat16), layer=l)
+    eng.start_run()
+    qs = workload.TorchQueryStream(5, L, B, cfg.n_head, cfg.n_kv_head, cfg.d_head, 0.5, dev, torch.bfloat16)
+    m_q = cfg.blocks_q if selector == "nosa" else cfg.blocks_topk
+    for _ in range(steps):
+        q, kn, vn = qs.next()
+        eng.step(q, kn, vn, selector=selector, gather="memcpy")
+        for l in range(L):
+            bq, nq, be, ne, rq, nr, s_q = eng.raw_selection(l)
+            plans = eng.plans(l)
+            for b in range(B):
+                geom = eng.geometry[b]
+                lo, hi = geom.pool_blocks.start, geom.pool_blocks.stop
+                t = int(eng._t[l, b]) - 1
+                for h in range(cfg.n_kv_head):
+                    scores = s_q[b, h, lo:hi]
+                    want = sorted(lo + i for i in sorted(range(hi - lo), key=lambda i: (-scores[i], i))[:m_q])
+                    assert bq[b, h, :nq[b, h]].tolist() == want, (l, b, h)
+                    picks = set(bq[b, h, :nq[b, h]].tolist()) | set(be[b, h, :ne[b, h]].tolist())
+                    fixed = set(geom.fixed_blocks(t))
+                    req = rq[b, h, :nr[b, h]].tolist()
+                    assert req == sorted(fixed | picks) and not (fixed & picks)
+                    slot_of, block_of = eng.residency(l, b, h)
+                    resident = {blk: int(sl) for blk, sl in enumerate(slot_of) if sl >= 0}
+                    assert all(r in resident for r in req)
+                    assert len(resident) <= C and len(set(resident.values())) == len(resident)
+                    assert all(block_of[sl] == blk for blk, sl in resident.items())
+                    p = plans[b][h]
+                    assert p.hits + len(p.fetch) == len(req) and not (set(p.fetch) & set(p.evict))
+    eng.close()
