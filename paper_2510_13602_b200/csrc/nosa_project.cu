@@ -4,10 +4,10 @@
 //   C[M][N] = A[M][K] · B[N][K]ᵀ,  A = hidden states (bf16, row-major), B = the concatenated
 //   [W_q | W_k | W_v] transposed to [N][K] (bf16, K-major), fp32 accumulation in TMEM.
 //
-// Grid (N/128, ceil(M/128), splits), clusters of `splits` CTAs along K.  Each CTA:
-//   warp 0 lane 0  TMA producer: 128 x 64 bf16 boxes of A and B (128B swizzle) into a 4-stage
-//                  ring, one mbarrier with the byte count per stage;
-//   warp 1 lane 0  MMA issuer: tcgen05.mma M=128 N=128 K=16 (4 per stage) into a 128-column
+// Grid (N/256, ceil(M/128), splits), clusters of `splits` CTAs along K.  Each CTA:
+//   warp 0 lane 0  TMA producer: 64-wide bf16 boxes (128B swizzle), 128 rows of A and 256 of B
+//                  per stage, into a 4-stage ring, one mbarrier with the byte count per stage;
+//   warp 1 lane 0  MMA issuer: tcgen05.mma M=128 N=256 K=16 (4 per stage) into a 256-column
 //                  TMEM accumulator, tcgen05.commit frees each stage;
 //   all 4 warps    epilogue: tcgen05.ld of the accumulator (warp w = TMEM lanes 32w..) into
 //                  the CTA's shared memory.
@@ -24,9 +24,8 @@
 
 namespace nosa {
 
-constexpr int PM = 128, PN = 128, PK = 64, PSTAGES = 4, PTHREADS = 128;
-constexpr int P_TILE_BYTES = PM * PK * 2;  // 16 KiB per operand box
-constexpr int P_EPI_LD = PN + 4;           // padded f32 row of the partial tile in smem
+constexpr int PM = 128, PK = 64, PSTAGES = 4, PTHREADS = 128;
+constexpr int P_A_BYTES = PM * PK * 2;  // 16 KiB A box per stage
 constexpr int P_MAX_SPLITS = 8;            // portable cluster size
 
 // UMMA shared-memory descriptor: K-major operand, 128B swizzle, 8-row atoms 1024 B apart
@@ -71,17 +70,21 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t local_addr, uint32_t rank
   return v;
 }
 
+// PN = 128 or 256 output columns per CTA (B staged as PN / 128 boxes of 128 rows per stage)
+template <int PN>
 __global__ void __launch_bounds__(PTHREADS, 1)
     project_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
                         int N, int k_per_split, int nq, int nk, __nv_bfloat16* __restrict__ q,
                         __nv_bfloat16* __restrict__ k, __nv_bfloat16* __restrict__ v) {
+  constexpr int P_B_BYTES = PN * PK * 2;
+  constexpr int P_EPI_LD = PN + 4;  // padded f32 row of the partial tile in smem
   extern __shared__ __align__(1024) char smem_raw[];
   // 1024-byte aligned stage buffers (the swizzle atoms must start on 1024 B); the same bytes
   // hold the f32 partial tile after the main loop
   const uint32_t raw = smem_u32(smem_raw), base = (raw + 1023u) & ~1023u;
   char* base_ptr = smem_raw + (base - raw);
-  const uint32_t sA = base, sB = base + PSTAGES * P_TILE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(base_ptr + 2 * PSTAGES * P_TILE_BYTES);
+  const uint32_t sA = base, sB = base + PSTAGES * P_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base_ptr + PSTAGES * (P_A_BYTES + P_B_BYTES));
   uint64_t* empty = full + PSTAGES;
   uint64_t* done = empty + PSTAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
     mbar_init(done, 1);
     fence_mbar_init();
   }
-  if (warp == 0) {  // accumulator: 128 lanes x 128 f32 columns of TMEM
+  if (warp == 0) {  // accumulator: 128 lanes x 256 f32 columns of TMEM
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(PN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -116,9 +119,11 @@ __global__ void __launch_bounds__(PTHREADS, 1)
     for (int kt = 0; kt < nkt; ++kt) {
       const int s = kt % PSTAGES;
       if (kt >= PSTAGES) mbar_wait(&empty[s], ((kt / PSTAGES) - 1) & 1);
-      mbar_expect_tx(&full[s], 2 * P_TILE_BYTES);
-      tma_load_2d(sA + s * P_TILE_BYTES, &map_a, kbeg + kt * PK, m0, &full[s]);
-      tma_load_2d(sB + s * P_TILE_BYTES, &map_b, kbeg + kt * PK, n0, &full[s]);
+      mbar_expect_tx(&full[s], P_A_BYTES + P_B_BYTES);
+      tma_load_2d(sA + s * P_A_BYTES, &map_a, kbeg + kt * PK, m0, &full[s]);
+#pragma unroll
+      for (int bx = 0; bx < PN / 128; ++bx)  // 128-row boxes of B
+        tma_load_2d(sB + s * P_B_BYTES + bx * (P_B_BYTES * 128 / PN), &map_b, kbeg + kt * PK, n0 + 128 * bx, &full[s]);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer
@@ -129,8 +134,8 @@ __global__ void __launch_bounds__(PTHREADS, 1)
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int ks = 0; ks < PK / 16; ++ks) {  // K = 16 per instruction: +32 B inside the swizzled row
-        const uint64_t ad = umma_desc_sw128(sA + s * P_TILE_BYTES + ks * 32);
-        const uint64_t bd = umma_desc_sw128(sB + s * P_TILE_BYTES + ks * 32);
+        const uint64_t ad = umma_desc_sw128(sA + s * P_A_BYTES + ks * 32);
+        const uint64_t bd = umma_desc_sw128(sB + s * P_B_BYTES + ks * 32);  // 256 rows: 32 swizzle atoms
         const uint32_t acc = (kt > 0 || ks > 0) ? 1u : 0u;
         asm volatile(
             "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -207,8 +212,9 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(PN));
 }
 
+template <int PN>
 size_t project_smem_bytes() {
-  const size_t ring = 2 * (size_t)PSTAGES * P_TILE_BYTES, epi = (size_t)PM * P_EPI_LD * 4;
+  const size_t ring = (size_t)PSTAGES * (P_A_BYTES + PN * PK * 2), epi = (size_t)PM * (PN + 4) * 4;
   return 1024 + std::max(ring, epi) + (2 * PSTAGES + 1) * 8 + 16;
 }
 
@@ -223,23 +229,21 @@ static bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols) {
   }
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};  // innermost (K) first
   const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  const cuuint32_t box[2] = {PK, PM};
+  const cuuint32_t box[2] = {PK, 128};  // 64 x 128 boxes (B takes two per stage)
   const cuuint32_t estr[2] = {1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;  // rows past M read as zeros
 }
 
-// splits (1..8, a cluster along K): K is cut into `splits` ranges of whole 64-wide k-tiles
-cudaError_t launch_project(const void* A, const void* Bt, int M, int N, int K, int splits, void* q, void* k, void* v,
-                           int nq, int nk, cudaStream_t st) {
-  if (splits < 1 || splits > P_MAX_SPLITS || K % (PK * splits) || N % PN) return cudaErrorInvalidValue;
-  CUtensorMap ma, mb;
-  if (!make_map(&ma, A, M, K) || !make_map(&mb, Bt, N, K)) return cudaErrorInvalidValue;
-  const size_t smem = project_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(project_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int PN>
+static cudaError_t launch_project_tiles(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, int splits,
+                                        void* q, void* k, void* v, int nq, int nk, cudaStream_t st) {
+  const size_t smem = project_smem_bytes<PN>();
+  auto kern = project_gemm_kernel<PN>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  max_shared_carveout(project_gemm_kernel);
+  max_shared_carveout(kern);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(N / PN, (M + PM - 1) / PM, splits);
   cfg.blockDim = dim3(PTHREADS);
@@ -252,9 +256,21 @@ cudaError_t launch_project(const void* A, const void* Bt, int M, int N, int K, i
   attr[0].val.clusterDim.z = splits;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, project_gemm_kernel, ma, mb, M, N, K / splits, nq, nk,
-                            static_cast<__nv_bfloat16*>(q), static_cast<__nv_bfloat16*>(k),
-                            static_cast<__nv_bfloat16*>(v));
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, M, N, K / splits, nq, nk, static_cast<__nv_bfloat16*>(q),
+                            static_cast<__nv_bfloat16*>(k), static_cast<__nv_bfloat16*>(v));
+}
+
+// splits (1..8, a cluster along K): K is cut into `splits` ranges of whole 64-wide k-tiles.
+// 256-column tiles once the 128 x 256 tiles alone fill the SMs (prefill-sized m), else 128
+// (measured on the 1B shape, profiles/r1_projection.txt).
+cudaError_t launch_project(const void* A, const void* Bt, int M, int N, int K, int splits, void* q, void* k, void* v,
+                           int nq, int nk, cudaStream_t st) {
+  if (splits < 1 || splits > P_MAX_SPLITS || K % (PK * splits) || N % 128) return cudaErrorInvalidValue;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, M, K) || !make_map(&mb, Bt, N, K)) return cudaErrorInvalidValue;
+  const bool wide = N % 256 == 0 && (long long)(N / 256) * ((M + PM - 1) / PM) >= 148;
+  return wide ? launch_project_tiles<256>(ma, mb, M, N, K, splits, q, k, v, nq, nk, st)
+              : launch_project_tiles<128>(ma, mb, M, N, K, splits, q, k, v, nq, nk, st);
 }
 
 }  // namespace nosa

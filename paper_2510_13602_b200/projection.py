@@ -19,7 +19,7 @@ NUM_SMS = 148
 
 
 def _splits(m: int, n: int, k: int) -> int:
-    """K splits per 128 x 128 tile (a cluster of that many CTAs).  Measured on the 1B shape
+    """K splits per output tile (a cluster of that many CTAs).  Measured on the 1B shape
     (d = 2048, n = 2560, profiles/r1_projection.txt): 4 splits are fastest while the tiles fill
     well under a wave (m <= 128: 9 us; 8 splits 15 us, 1 split 15-19 us), one split once the
     tiles alone fill the SMs."""
