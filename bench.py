@@ -100,8 +100,7 @@ def workload_dims(args, world):
             w["batch_local"] = max(1, budget // int(per_seq))
             w["global_batch"] = w["batch_local"] * world
             w["host_limited"] = True
-        return w
-    if args.impl == "native":  # the pinned slow tier of every rank on this node must fit in RAM
+    elif args.impl == "native":  # the pinned slow tier of every rank on this node must fit in RAM
         local = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
         n_blocks = -(-(w["context"] + 256) // 64)
         per_seq = w["layers"] * 2 * n_blocks * 2 * 64 * 128 * 2  # [layers][kv heads][blocks] x 32 KiB
@@ -114,6 +113,17 @@ def workload_dims(args, world):
             w["batch_local"] = fit
             w["global_batch"] = fit * world
             w["host_limited"] = True
+    if world > 1:  # every rank runs the smallest shard any rank fits
+        import torch
+        import torch.distributed as dist
+        if dist.is_initialized():
+            t = torch.tensor([w["batch_local"], int(w["host_limited"])], dtype=torch.int64,
+                             device=torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))))
+            dist.all_reduce(t[:1], op=dist.ReduceOp.MIN)
+            dist.all_reduce(t[1:], op=dist.ReduceOp.MAX)
+            if not w.get("strong") or int(t[1]):
+                w["batch_local"], w["host_limited"] = int(t[0]), bool(t[1])
+                w["global_batch"] = w["batch_local"] * world
     return w
 
 
