@@ -117,8 +117,9 @@ def workload_dims(args, world):
         import torch
         import torch.distributed as dist
         if dist.is_initialized():
-            t = torch.tensor([w["batch_local"], int(w["host_limited"])], dtype=torch.int64,
-                             device=torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))))
+            dev = (torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))) if dist.get_backend() == "nccl"
+                   else torch.device("cpu"))
+            t = torch.tensor([w["batch_local"], int(w["host_limited"])], dtype=torch.int64, device=dev)
             dist.all_reduce(t[:1], op=dist.ReduceOp.MIN)
             dist.all_reduce(t[1:], op=dist.ReduceOp.MAX)
             if not w.get("strong") or int(t[1]):

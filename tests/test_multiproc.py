@@ -61,3 +61,31 @@ def test_cpulist_parsing_and_numa_binding(tmp_path):
     before = os.sched_getaffinity(0)
     assert bind_to_gpu_numa_node(0, sysfs=str(tmp_path)) is None
     assert os.sched_getaffinity(0) == before
+
+
+def _bench_shard_worker(rank, world, port, out):
+    """bench.workload_dims under a 2-rank gloo group whose ranks see different free host RAM."""
+    import sys
+    from argparse import Namespace
+    from pathlib import Path
+    import torch.distributed as dist
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), LOCAL_RANK=str(rank),
+                      LOCAL_WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    per_seq = 28 * 2 * 517 * 32768  # cfg3 slow tier per sequence (bench.workload_dims)
+    bench.host_mem_available = lambda: int((40 + 30 * rank) * per_seq * world / 0.8)  # rank 0 fits 40, rank 1 70
+    args = Namespace(workload="cfg3", layers=None, batch=None, impl="native", slow_tier="host")
+    w = bench.workload_dims(args, world)
+    out[rank] = (w["batch_local"], w["global_batch"], w["host_limited"])
+    dist.destroy_process_group()
+
+
+def test_bench_ranks_agree_on_the_host_limited_shard():
+    world, port = 2, _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_bench_shard_worker, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    assert res[0] == res[1] == (40, 80, True)
