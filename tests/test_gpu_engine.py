@@ -73,7 +73,7 @@ def test_engine_vs_reference_golden(golden, name, dtype):
 
 def _run_pair(cfg, *, batch, t0s, steps, fast_slots, seed, rho, selector="nosa", dtype="bf16", layers=1,
               variant="ed-dma", check_residency=True, gather="uva", schedule="pipelined", resident=False,
-              shared=False, attend_chunk=0, slow_tier="host"):
+              shared=False, attend_chunk=0, slow_tier="host", attend_layers=0):
     """GPU engine and oracle on identical inputs; returns the worst relative output error."""
     w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, seed)
     if variant == "dma":
@@ -82,7 +82,7 @@ def _run_pair(cfg, *, batch, t0s, steps, fast_slots, seed, rho, selector="nosa",
     cap = tmax + steps + 1
     eng = NosaEngine(cfg, batch=batch, layers=layers, max_tokens=cap, fast_slots=fast_slots, w1=w1, w2=w2,
                      dtype=dtype, variant=variant, residency="shared" if shared else "per-sequence",
-                     attend_chunk=attend_chunk, slow_tier=slow_tier)
+                     attend_chunk=attend_chunk, slow_tier=slow_tier, attend_layers=attend_layers)
     orc = oracle_for(cfg, batch, layers, cap, fast_slots, w1, w2, variant, shared=shared)
     K, V = workload.prefix_kv(seed, batch * layers, cfg.n_kv_head, tmax, cfg.d_head)
     K = K.reshape(layers, batch, cfg.n_kv_head, tmax, cfg.d_head)
@@ -310,7 +310,11 @@ def test_exact_score_ties_pick_the_lower_block(exact, selector):
 
 
 def test_resident_multilayer_batched_attention():
-    """All blocks in HBM: attention runs 4 layers per persistent launch (6 layers = 4 + 2)."""
+    """All blocks in HBM: several layers per persistent attention launch (6 layers = 4 + 2 here;
+    the default batch is 7)."""
+    a = _run_pair(ONE_B_SMALL, batch=2, t0s=[3000, 2900], steps=8, fast_slots=48, seed=17, rho=0.3, layers=6,
+                  resident=True, attend_layers=4)
+    assert a <= TOL["bf16"]
     a = _run_pair(ONE_B_SMALL, batch=2, t0s=[3000, 2900], steps=8, fast_slots=48, seed=17, rho=0.3, layers=6,
                   resident=True)
     assert a <= TOL["bf16"]
