@@ -166,17 +166,21 @@ __global__ void __launch_bounds__(PTHREADS, 1)
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;");
-    float* dst = tile + trow * P_EPI_LD + c0;
+    if (m0 + trow < M) {  // rows past M (decode-sized m) are never reduced
+      float* dst = tile + trow * P_EPI_LD + c0;
 #pragma unroll
-    for (int j = 0; j < 32; j += 4)
-      *reinterpret_cast<float4*>(dst + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                                        __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(dst + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                          __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   cluster_sync();  // every CTA's partial is in its shared memory (and the MMA smem reads are over)
 
   // ---- split-K reduction over the cluster in rank order; rank j owns rows [r0, r1) of the tile
-  const int r0 = (int)rank * PM / splits, r1 = ((int)rank + 1) * PM / splits;
+  // the tile's valid rows are split over the ranks (a decode-sized m leaves most ranks idle here)
+  const int valid = min(PM, M - m0);
+  const int r0 = (int)rank * valid / splits, r1 = ((int)rank + 1) * valid / splits;
   const uint32_t tile_addr = smem_u32(tile);
   for (int x = tid; x < (r1 - r0) * (PN / 4); x += PTHREADS) {
     const int rr = r0 + x / (PN / 4), c4 = (x % (PN / 4)) * 4;
