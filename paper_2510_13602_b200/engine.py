@@ -227,17 +227,29 @@ class NosaEngine:
         if (self._t >= self.max_tokens).any():
             raise ValueError("head cache capacity exhausted")
 
+    def _mover(self, gather: str, graph: bool = False) -> str:
+        """"auto": the copy engine (host-planned batches) when blocks live in pinned host memory
+        and some do not fit in HBM; the SM gather when every block is resident or the slow tier
+        is a GPU's HBM (measured: DESIGN.md §5), and for graph capture, which needs a
+        device-driven mover."""
+        if gather != "auto":
+            return gather
+        offloaded = self.fast_slots < self.max_blocks and self.slow_tier == "host"
+        return "memcpy" if offloaded and not graph else "uva"
+
     def step(self, q, k_new, v_new, selector: str = "nosa", out: torch.Tensor | None = None,
-             gather: str = "uva", check: bool = True, schedule: str = "pipelined") -> torch.Tensor:
+             gather: str = "auto", check: bool = True, schedule: str = "pipelined") -> torch.Tensor:
         """One decode step of every layer (DecodeEngine.step, decode.py:152-190).
 
         q: [layers][batch][n_head][d_head]; k_new, v_new: [layers][batch][n_kv_head][d_head].
         Returns out [layers][batch][n_head][d_head] float32 (attention over tokens [0, t)).
-        gather: "uva" (zero-copy SM kernel), "tma" (TMA bulk kernel) or "memcpy" (copy engine).
+        gather: "auto" (see _mover), "uva" (zero-copy SM kernel), "tma" (TMA bulk kernel) or
+        "memcpy" (copy engine).
         schedule: "pipelined" overlaps layer l's gather with the scoring of later layers;
         "serial" runs layer by layer (results are identical)."""
         if selector not in SELECTORS:
             raise ValueError(f"selector must be one of {SELECTORS}")
+        gather = self._mover(gather)
         if gather not in _lib.GATHER or schedule not in _lib.SCHEDULE:
             raise ValueError(f"gather must be one of {tuple(_lib.GATHER)}, schedule one of {tuple(_lib.SCHEDULE)}")
         self._check_step()
@@ -257,7 +269,7 @@ class NosaEngine:
         return out
 
     def step_host(self, q, k_new, v_new, selector: str = "nosa", out: torch.Tensor | None = None,
-                  gather: str = "uva", schedule: str = "pipelined", sync: bool = True) -> torch.Tensor:
+                  gather: str = "auto", schedule: str = "pipelined", sync: bool = True) -> torch.Tensor:
         """`step` on host tensors (the reference's calling convention: host arrays in, host
         array out).  q/k_new/v_new: CPU tensors of the engine dtype in the `step` layouts, pinned
         for asynchronous copies.  Layer l's inputs are copied in ahead of the miss gathers and
@@ -266,6 +278,7 @@ class NosaEngine:
         complete once torch's current stream reaches this point."""
         if selector not in SELECTORS:
             raise ValueError(f"selector must be one of {SELECTORS}")
+        gather = self._mover(gather)
         if gather not in _lib.GATHER or schedule not in _lib.SCHEDULE:
             raise ValueError(f"gather must be one of {tuple(_lib.GATHER)}, schedule one of {tuple(_lib.SCHEDULE)}")
         self._check_step()
@@ -300,7 +313,7 @@ class NosaEngine:
         return out
 
     def step_layer(self, layer: int, q, k_new, v_new, selector: str = "nosa", out=None,
-                   gather: str = "uva") -> torch.Tensor:
+                   gather: str = "auto") -> torch.Tensor:
         """The same step for one layer, stage by stage through the C ABI."""
         if selector not in SELECTORS:
             raise ValueError(f"selector must be one of {SELECTORS}")
@@ -312,6 +325,7 @@ class NosaEngine:
         if out is None:
             out = torch.empty((self.batch, cfg.n_head, cfg.d_head), dtype=torch.float32, device=self.device)
         s = _lib.stream_ptr
+        gather = self._mover(gather)
         with torch.cuda.device(self.device):
             self._call(_lib.lib.nosa_select_plan, layer, q.data_ptr(), _lib.SELECTOR[selector], s())
             self._call(_lib.lib.nosa_gather, layer, _lib.GATHER[gather], s())
@@ -322,8 +336,9 @@ class NosaEngine:
 
     # ------------------------------------------------------------------ CUDA graph
     def capture(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, out: torch.Tensor,
-                selector: str = "nosa", gather: str = "uva", schedule: str = "pipelined"):
+                selector: str = "nosa", gather: str = "auto", schedule: str = "pipelined"):
         """Capture one full step on fixed device buffers; replay() re-runs it."""
+        gather = self._mover(gather, graph=True)
         self._check_step()
         for x in (q, k_new, v_new, out):
             if not x.is_contiguous() or x.device != self.device:
@@ -347,11 +362,12 @@ class NosaEngine:
         return _lib.NosaHostStepIO(q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), out.data_ptr(),
                                    _lib.SELECTOR[selector], _lib.GATHER[gather], _lib.SCHEDULE[schedule])
 
-    def capture_host(self, q, k_new, v_new, out, selector: str = "nosa", gather: str = "uva",
+    def capture_host(self, q, k_new, v_new, out, selector: str = "nosa", gather: str = "auto",
                      schedule: str = "pipelined"):
         """Capture one host-buffer step (step_host) as a CUDA graph; replay_host() re-runs it on
         these or other pinned buffers of the same shapes."""
         self._check_step()
+        gather = self._mover(gather, graph=True)
         io = self._host_io(q, k_new, v_new, out, selector, gather, schedule)
         with torch.cuda.device(self.device):
             self._call(_lib.lib.nosa_step_graph_capture_host, ctypes.byref(io))
