@@ -74,6 +74,10 @@ def _c_config(**over):
     (dict(accounting=0, k_q=512, k_e=512), "inclusive accounting needs k_q <= k - n_s - n_w"),
     (dict(d_head=96), "unsupported"),
     (dict(batch=0), "batch and layers must be positive"),
+    (dict(attend_chunk=9), "attend_chunk must be in 0..8"),
+    (dict(attend_layers=-1), "attend_layers must be >= 0"),
+    (dict(exact_scan=2), "exact_scan must be 0 or 1"),
+    (dict(slow_tier_device=-2), "slow_tier_device must be -1"),
 ])
 def test_c_config_validation_messages(over, msg):
     buf = ctypes.create_string_buffer(512)
@@ -172,3 +176,13 @@ def test_query_stream_locality():
     qb = [b.next()[0] for _ in range(6)]
     corr = lambda qs: np.mean([np.corrcoef(qs[i].ravel(), qs[i + 1].ravel())[0, 1] for i in range(5)])
     assert corr(qa) > 0.8 and abs(corr(qb)) < 0.2
+
+
+def test_projection_rejects_untileable_shapes_without_a_gpu():
+    """nosa_project_qkv validates shapes before touching the device (ValueError-class status)."""
+    lib = _lib.lib
+    p = ctypes.c_void_p(16)  # never dereferenced: the shape checks fail first
+    assert lib.nosa_project_qkv(p, 4, 2048, p, 2500, 2048, 256, p, p, p, 4, None) == _lib.NOSA_ERR_VALUE
+    assert b"N % 128" in lib.nosa_last_error(None)
+    assert lib.nosa_project_qkv(p, 4, 2048, p, 2560, 2048, 256, p, p, p, 9, None) == _lib.NOSA_ERR_VALUE
+    assert lib.nosa_project_qkv(None, 4, 2048, p, 2560, 2048, 256, p, p, p, 4, None) == _lib.NOSA_ERR_VALUE
