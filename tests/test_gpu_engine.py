@@ -224,14 +224,19 @@ def test_resident_prefill(dtype):
               resident=True)
 
 
-@pytest.mark.parametrize("selector", ["nosa", "infllmv2"])
-@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
-def test_screened_selection_equals_full_f64_scan(selector, dtype):
+@pytest.mark.parametrize("selector,dtype,kscale,qscale", [
+    ("nosa", "bf16", 1.0, 1.0), ("infllmv2", "bf16", 1.0, 1.0), ("nosa", "fp32", 1.0, 1.0),
+    ("infllmv2", "fp32", 1.0, 1.0),
+    ("nosa", "fp32", 3e4, 1e-4),   # large keys, tiny queries: the bound's relative terms dominate
+    ("nosa", "fp32", 1.0, 0.0),    # zero queries: every pool score ties at 0, lowest blocks win
+])
+def test_screened_selection_equals_full_f64_scan(selector, dtype, kscale, qscale):
     """The screened selector (bf16 pre-scan + f64 rescoring of the candidates) picks exactly the
     blocks a full f64 scan of the pool picks, so every later quantity is bitwise identical."""
     cfg = ONE_B_SMALL
     w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, 4)
     K, V = workload.prefix_kv(4, 6, cfg.n_kv_head, 6000, cfg.d_head)
+    K = (K * kscale).astype(np.float32)
     K, V = K.reshape(2, 3, cfg.n_kv_head, 6000, cfg.d_head), V.reshape(2, 3, cfg.n_kv_head, 6000, cfg.d_head)
     runs = []
     for exact in (True, False):
@@ -242,7 +247,8 @@ def test_screened_selection_equals_full_f64_scan(selector, dtype):
         stream = workload.QueryStream(4, 2, 3, cfg.n_head, cfg.n_kv_head, cfg.d_head, 0.2)
         outs, sels = [], []
         for _ in range(25):
-            outs.append(eng.step(*stream.next(), selector=selector).cpu().numpy())
+            q, kn, vn = stream.next()
+            outs.append(eng.step((q * qscale).astype(np.float32), kn, vn, selector=selector).cpu().numpy())
             sels.append([eng.raw_selection(l)[:4] for l in range(2)])
         st = eng.residency_stats()
         runs.append((np.stack(outs), sels, (st.hits, st.misses, st.evictions)))
