@@ -120,6 +120,18 @@ typedef struct NosaHostStepIO {
   int32_t schedule;
 } NosaHostStepIO;
 
+/* nosa_decode_step_hidden: hidden states in (the reference's DecodeEngine.step(h_t) input),
+ * q/k/v projected on the GPU by the weights of nosa_set_projection.
+ *   h   [layers][batch][d]               (bf16, device)
+ *   out [layers][batch][n_head][d_head]  (float32, device)                                    */
+typedef struct NosaHiddenStepIO {
+  const void* h;
+  float* out;
+  int32_t selector;
+  int32_t gather_mode;
+  int32_t schedule;
+} NosaHiddenStepIO;
+
 typedef struct NosaCtx NosaCtx;
 
 /* ---- configuration ---------------------------------------------------------------- */
@@ -211,6 +223,19 @@ int nosa_decode_step(NosaCtx* ctx, const NosaStepIO* io, void* stream);
  * point (cudaStreamSynchronize).  The context owns the device staging. */
 int nosa_decode_step_host(NosaCtx* ctx, const NosaHostStepIO* io, void* stream);
 
+/* The QKV projection of one layer for nosa_decode_step_hidden (project_qkv, attention.py:67-90;
+ * DecodeEngine.step decode.py:162-164): w_t = [W_q | W_k | W_v]^T, device bf16 [n][d],
+ * n = (n_head + 2 n_kv_head) d_head, nq = n_head d_head, nk = n_kv_head d_head.  The buffer
+ * stays owned by the caller and must outlive the steps that use it.  bf16 storage only. */
+int nosa_set_projection(NosaCtx* ctx, int layer, const void* w_t, int d, int n, int nq, int nk);
+
+/* All layers of one decode step from hidden states: per selection group, the tcgen05
+ * projection of its layers (on the selection stream), then the step of nosa_decode_step on
+ * the projected q / k / v.  Same schedule, movers and results as nosa_decode_step fed with
+ * those q / k / v.  Graph form: nosa_step_graph_capture_hidden + nosa_step_graph_launch. */
+int nosa_decode_step_hidden(NosaCtx* ctx, const NosaHiddenStepIO* io, void* stream);
+int nosa_step_graph_capture_hidden(NosaCtx* ctx, const NosaHiddenStepIO* io);
+
 /* CUDA-graph form of nosa_decode_step_host (device movers only: uva / tma): capture once on
  * pinned host buffers; every launch may pass other pinned buffers of the same shapes (the
  * graph's input-staging and output-copy nodes are re-pointed before the launch). */
@@ -283,11 +308,12 @@ int nosa_check_errors(NosaCtx* ctx, uint32_t* flags);
 /* Device timing of every kernel of subsequent eager steps, bracketed by CUDA events on the
  * stream each kernel runs on (bench evidence).  Kinds: 0 = select+plan (K1+K2), 1 = gather (K3),
  * 2 = attention (K4, split-K records), 3 = finalize (K4 log-sum-exp merge + K5 append),
- * 4 = host->device input copy and 5 = device->host output copy of nosa_decode_step_host.
+ * 4 = host->device input copy and 5 = device->host output copy of nosa_decode_step_host,
+ * 6 = QKV projection of nosa_decode_step_hidden.
  * enable(0) turns it off; read synchronises and returns the summed milliseconds and launch
  * counts per kind since enable. */
 int nosa_timing_enable(NosaCtx* ctx, int max_launches);
-int nosa_timing_read(NosaCtx* ctx, double* total_ms /* [6] */, int64_t* launches /* [6] */);
+int nosa_timing_read(NosaCtx* ctx, double* total_ms /* [7] */, int64_t* launches /* [7] */);
 
 /* The timed launches since enable, in issue order: kind and start/end milliseconds relative to
  * the first one (a device timeline of the step's streams).  Synchronises. */

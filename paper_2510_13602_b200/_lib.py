@@ -55,6 +55,11 @@ class NosaHostStepIO(NosaStepIO):
     """Same fields as NosaStepIO; the pointers are host addresses (nosa_decode_step_host)."""
 
 
+class NosaHiddenStepIO(ctypes.Structure):
+    _fields_ = [("h", ctypes.c_void_p), ("out", ctypes.c_void_p), ("selector", ctypes.c_int32),
+                ("gather_mode", ctypes.c_int32), ("schedule", ctypes.c_int32)]
+
+
 # every symbol include/nosa_b200.h declares, with its ctypes signature
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -79,6 +84,9 @@ SIGNATURES = {
     "nosa_decode_step": (_I, [_P, ctypes.POINTER(NosaStepIO), _P]),
     "nosa_decode_step_host": (_I, [_P, ctypes.POINTER(NosaHostStepIO), _P]),
     "nosa_step_graph_capture_host": (_I, [_P, ctypes.POINTER(NosaHostStepIO)]),
+    "nosa_set_projection": (_I, [_P, _I, _P, _I, _I, _I, _I]),
+    "nosa_decode_step_hidden": (_I, [_P, ctypes.POINTER(NosaHiddenStepIO), _P]),
+    "nosa_step_graph_capture_hidden": (_I, [_P, ctypes.POINTER(NosaHiddenStepIO)]),
     "nosa_step_graph_launch_host": (_I, [_P, ctypes.POINTER(NosaHostStepIO), _P]),
     "nosa_step_graph_capture": (_I, [_P, ctypes.POINTER(NosaStepIO)]),
     "nosa_step_graph_launch": (_I, [_P, _P]),

@@ -102,6 +102,9 @@ struct NosaCtx {
   int stage_grid = 32;              // CTAs of the input-staging kernel (host-buffer step)
   bool stage_with_copies = false;   // NOSA_STAGE_COPIES: stage host inputs with cudaMemcpyAsync
   int attend_layers = 1;            // layers per attention launch (pipelined schedule)
+  // QKV projection of nosa_decode_step_hidden: per-layer [W_q | W_k | W_v]^T, bf16 [n][d] (caller-owned)
+  std::vector<const void*> proj_w;
+  int proj_d = 0;
   int step_kernels = 0;             // kernels launched by the last enqueued step
   bool select_per_layer = false;
   // graph of the host-buffer step and its host-address nodes (kind 0 = staging kernel, 1 = D2H copy)
@@ -785,7 +788,7 @@ extern "C" int nosa_timing_read(NosaCtx* ctx, double* total_ms, int64_t* launche
   if (!ctx || !total_ms || !launches) return NOSA_ERR_VALUE;
   cudaSetDevice(ctx->device);
   CUDA_TRY(ctx, cudaDeviceSynchronize());
-  for (int k = 0; k < 6; ++k) {
+  for (int k = 0; k < 7; ++k) {
     total_ms[k] = 0.0;
     launches[k] = 0;
   }
@@ -879,7 +882,7 @@ extern "C" int nosa_timing_trace(NosaCtx* ctx, int cap, int32_t* kind, float* st
 }
 
 static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, bool count,
-                        const NosaHostStepIO* hio = nullptr) {
+                        const NosaHostStepIO* hio = nullptr, const void* hidden = nullptr) {
   const Dev& dv = ctx->dv;
   const size_t qstride = (size_t)dv.B * dv.Hq * dv.D * dv.elem;
   const size_t kstride = (size_t)dv.B * dv.H * dv.D * dv.elem;
@@ -959,6 +962,26 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
     }
     if (!all) hsrc[0] = hsrc[1] = hsrc[2] = nullptr;
   }
+  // hidden-state step: layer l's q | k | v are projected from h[l] on the tensor cores on the
+  // selection stream, right before the layer's selection (project_qkv, attention.py:67-90)
+  int n_proj = 0;
+  auto project = [&](int l0, int n) -> int {
+    if (!hidden) return NOSA_OK;
+    const int N = (dv.Hq + 2 * dv.H) * dv.D, d = ctx->proj_d;
+    const int tiles = (N / 128) * ((dv.B + 127) / 128), kt = d / 64;
+    int splits = tiles * 4 <= 2 * ctx->num_sms ? 4 : 1;
+    splits = std::max(1, std::min(splits, kt));
+    while (kt % splits) --splits;
+    for (int l = l0; l < l0 + n; ++l) {
+      TimeScope ts(ctx, ss, 6, timed);
+      CUDA_TRY(ctx, nosa::launch_project(static_cast<const char*>(hidden) + (size_t)l * dv.B * d * 2, ctx->proj_w[l],
+                                         dv.B, N, d, splits, const_cast<char*>(q) + l * qstride,
+                                         const_cast<char*>(kn) + l * kstride, const_cast<char*>(vn) + l * kstride,
+                                         dv.Hq * dv.D, dv.H * dv.D, ss));
+      ++n_proj;
+    }
+    return NOSA_OK;
+  };
   size_t next_group = 0;
   auto issue_groups = [&](size_t upto) -> int {
     for (; next_group < std::min(upto, groups.size()); ++next_group) {
@@ -971,7 +994,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
                         const_cast<char*>(vn) + l0 * kstride};
         const size_t bytes[3] = {n * qstride, n * kstride, n * kstride};
         CUDA_TRY(ctx, nosa::launch_stage_inputs(src, dst, bytes, ctx->stage_grid, in));
-        if (count) ctx->launches += 1;  // (not part of step_kernels: host-buffer steps are never captured)
+        if (count) ctx->launches += 1;  // (counted apart from step_kernels: capture_host adds one per group)
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev_in[l0 + n - 1], in));
       } else if (hio) {
         cudaStream_t in = ctx->in_stream;
@@ -988,6 +1011,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev_in[l0 + n - 1], in));
       }
       if (!serial) {
+        if (int rc = project(l0, n)) return rc;
         if (grouped) {
           if (int rc = select_group(l0, n)) return rc;
         } else {
@@ -1013,6 +1037,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   for (int l = 0; l < dv.L; ++l) {
     if (serial) {
       if (l > 0) CUDA_TRY(ctx, cudaStreamWaitEvent(ss, ctx->ev_fin[l - 1], 0));
+      if (int rc = project(l, 1)) return rc;
       if (int rc = select(l)) return rc;
     }
     CUDA_TRY(ctx, cudaStreamWaitEvent(cp, ctx->ev_plan[l], 0));
@@ -1067,7 +1092,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   // kernels of this step: selections (grouped, per layer, or per layer + shared planner),
   // gathers (device movers), attention batches, finalizes, input staging (counted inline)
   const int n_sel = grouped ? (int)groups.size() : (dv.shared ? 2 : 1) * dv.L;
-  ctx->step_kernels = n_sel + n_gather_kernels + 2 * n_att;  // one finalize per attention batch
+  ctx->step_kernels = n_sel + n_gather_kernels + 2 * n_att + n_proj;  // one finalize per attention batch
   if (count) ctx->launches += ctx->step_kernels;
   return NOSA_OK;
 }
@@ -1118,6 +1143,45 @@ extern "C" int nosa_decode_step_host(NosaCtx* ctx, const NosaHostStepIO* hio, vo
   NosaStepIO io;
   if (int rc = host_staging(ctx, hio, &io)) return rc;
   return enqueue_step(ctx, &io, S(stream), true, hio);
+}
+
+extern "C" int nosa_set_projection(NosaCtx* ctx, int layer, const void* w_t, int d, int n, int nq, int nk) {
+  int rc = check_layer(ctx, layer);
+  if (rc) return rc;
+  const Dev& dv = ctx->dv;
+  if (dv.dtype != NOSA_DTYPE_BF16) return fail(ctx, NOSA_ERR_VALUE, "set_projection: the hidden-state step needs bf16 storage");
+  if (!w_t) return fail(ctx, NOSA_ERR_VALUE, "set_projection: NULL weights");
+  if (n != (dv.Hq + 2 * dv.H) * dv.D || nq != dv.Hq * dv.D || nk != dv.H * dv.D)
+    return fail(ctx, NOSA_ERR_VALUE, "set_projection: weights must be [n_head + 2 n_kv_head] x d_head columns");
+  if (d <= 0 || d % 64 || n % 128) return fail(ctx, NOSA_ERR_VALUE, "set_projection: needs d %% 64 == 0 and n %% 128 == 0");
+  if (ctx->proj_d && d != ctx->proj_d) return fail(ctx, NOSA_ERR_VALUE, "set_projection: every layer needs the same d");
+  ctx->proj_w.resize(dv.L, nullptr);
+  ctx->proj_w[layer] = w_t;
+  ctx->proj_d = d;
+  return NOSA_OK;
+}
+
+static int hidden_staging(NosaCtx* ctx, const NosaHiddenStepIO* hid, NosaStepIO* io) {
+  if (!hid || !hid->h || !hid->out) return fail(ctx, NOSA_ERR_VALUE, "decode_step_hidden: NULL io");
+  if (ctx->proj_w.size() != (size_t)ctx->dv.L ||
+      std::any_of(ctx->proj_w.begin(), ctx->proj_w.end(), [](const void* p) { return p == nullptr; }))
+    return fail(ctx, NOSA_ERR_STATE, "decode_step_hidden: nosa_set_projection missing for a layer");
+  NosaHostStepIO tmp{};  // device staging of q/k/v (the host-step buffers), `out` is the caller's
+  tmp.q = tmp.k_new = tmp.v_new = hid->h;
+  tmp.out = hid->out;
+  tmp.selector = hid->selector;
+  tmp.gather_mode = hid->gather_mode;
+  tmp.schedule = hid->schedule;
+  if (int rc = host_staging(ctx, &tmp, io)) return rc;
+  io->out = hid->out;
+  return NOSA_OK;
+}
+
+extern "C" int nosa_decode_step_hidden(NosaCtx* ctx, const NosaHiddenStepIO* hid, void* stream) {
+  if (!ctx) return NOSA_ERR_VALUE;
+  NosaStepIO io;
+  if (int rc = hidden_staging(ctx, hid, &io)) return rc;
+  return enqueue_step(ctx, &io, S(stream), true, nullptr, hid->h);
 }
 
 // device-visible aliases of pinned host buffers (NULL when a buffer is pageable)
@@ -1219,8 +1283,21 @@ extern "C" int nosa_step_graph_launch_host(NosaCtx* ctx, const NosaHostStepIO* h
   return NOSA_OK;
 }
 
+static int capture_step(NosaCtx* ctx, const NosaStepIO* io, const void* hidden);
+
 extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {
   if (!ctx || !io) return NOSA_ERR_VALUE;
+  return capture_step(ctx, io, nullptr);
+}
+
+extern "C" int nosa_step_graph_capture_hidden(NosaCtx* ctx, const NosaHiddenStepIO* hid) {
+  if (!ctx) return NOSA_ERR_VALUE;
+  NosaStepIO io;
+  if (int rc = hidden_staging(ctx, hid, &io)) return rc;
+  return capture_step(ctx, &io, hid->h);
+}
+
+static int capture_step(NosaCtx* ctx, const NosaStepIO* io, const void* hidden) {
   if (io->gather_mode == NOSA_GATHER_MEMCPY)
     return fail(ctx, NOSA_ERR_VALUE, "graph capture needs a device-driven gather (uva or tma)");
   cudaSetDevice(ctx->device);
@@ -1232,7 +1309,7 @@ extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {
     ctx->cap_used = 0;
     ctx->capturing = instrumented;
     CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->capture_stream, cudaStreamCaptureModeThreadLocal));
-    int rc = enqueue_step(ctx, io, ctx->capture_stream, false);
+    int rc = enqueue_step(ctx, io, ctx->capture_stream, false, nullptr, hidden);
     cudaError_t e = cudaStreamEndCapture(ctx->capture_stream, g);
     ctx->capturing = false;
     if (rc) return rc;
@@ -1244,7 +1321,7 @@ extern "C" int nosa_step_graph_capture(NosaCtx* ctx, const NosaStepIO* io) {
   CUDA_TRY(ctx, cudaGraphInstantiate(&ctx->graph_exec, ctx->graph, 0));
   ctx->graph_kernels = ctx->step_kernels;
   // the instrumented twin: an external event-record node around every kernel (placeholders)
-  const size_t nslots = 4 * (size_t)ctx->dv.L;
+  const size_t nslots = 5 * (size_t)ctx->dv.L;
   while (ctx->cap_events.size() < nslots) {
     NosaCtx::Timed t{};
     CUDA_TRY(ctx, cudaEventCreate(&t.a));

@@ -312,6 +312,57 @@ class NosaEngine:
                 self.check_errors()
         return out
 
+    def set_projection(self, layer: int, w_q, w_k, w_v):
+        """The QKV projection of one layer for step_hidden (project_qkv, attention.py:67-90):
+        w_q [d][n_head*d_head], w_k, w_v [d][n_kv_head*d_head], kept on the device as one bf16
+        [n][d] matrix (the K-major operand of the tcgen05 GEMM)."""
+        w = np.concatenate([np.asarray(w_q), np.asarray(w_k), np.asarray(w_v)], axis=1)
+        w_t = torch.as_tensor(np.ascontiguousarray(w.T), dtype=torch.float32).to(
+            device=self.device, dtype=torch.bfloat16).contiguous()
+        if not hasattr(self, "_proj_w"):
+            self._proj_w = [None] * self.layers
+        self._call(_lib.lib.nosa_set_projection, layer, w_t.data_ptr(), w.shape[0], w.shape[1],
+                   np.asarray(w_q).shape[1], np.asarray(w_k).shape[1])
+        self._proj_w[layer] = w_t  # the context borrows this buffer
+        self.hidden_dim = w.shape[0]
+
+    def _hidden_io(self, h, out, selector, gather, schedule):
+        L, B, cfg = self.layers, self.batch, self.config
+        h = self._dev(h, torch.bfloat16).reshape(L, B, self.hidden_dim)
+        if out is None:
+            out = torch.empty((L, B, cfg.n_head, cfg.d_head), dtype=torch.float32, device=self.device)
+        io = _lib.NosaHiddenStepIO(h.data_ptr(), out.data_ptr(), _lib.SELECTOR[selector], _lib.GATHER[gather],
+                                   _lib.SCHEDULE[schedule])
+        return h, out, io
+
+    def step_hidden(self, h, selector: str = "nosa", out: torch.Tensor | None = None, gather: str = "auto",
+                    check: bool = True, schedule: str = "pipelined") -> torch.Tensor:
+        """One decode step of every layer from hidden states h [layers][batch][d] (the input of
+        DecodeEngine.step, decode.py:152-190): q/k/v are projected on the tensor cores with the
+        weights of set_projection, then the step runs as `step` would on them."""
+        if selector not in SELECTORS:
+            raise ValueError(f"selector must be one of {SELECTORS}")
+        gather = self._mover(gather)
+        self._check_step()
+        h, out, io = self._hidden_io(h, out, selector, gather, schedule)
+        self._hidden_keep = h
+        with torch.cuda.device(self.device):
+            self._call(_lib.lib.nosa_decode_step_hidden, ctypes.byref(io), _lib.stream_ptr())
+        self._t += 1
+        if check:
+            self.check_errors()
+        return out
+
+    def capture_hidden(self, h: torch.Tensor, out: torch.Tensor, selector: str = "nosa", gather: str = "auto",
+                       schedule: str = "pipelined"):
+        """Capture one step_hidden on fixed device buffers as a CUDA graph; replay() re-runs it."""
+        self._check_step()
+        gather = self._mover(gather, graph=True)
+        h, out, io = self._hidden_io(h, out, selector, gather, schedule)
+        self._graph_bufs = (h, out)
+        with torch.cuda.device(self.device):
+            self._call(_lib.lib.nosa_step_graph_capture_hidden, ctypes.byref(io))
+
     def step_layer(self, layer: int, q, k_new, v_new, selector: str = "nosa", out=None,
                    gather: str = "auto") -> torch.Tensor:
         """The same step for one layer, stage by stage through the C ABI."""
@@ -483,22 +534,26 @@ class NosaEngine:
     # ------------------------------------------------------------------ device timing
     KERNEL_KINDS = ("select_plan", "gather", "attend", "finalize")
     COPY_KINDS = ("h2d_in", "d2h_out")  # host-buffer step copies (timing kinds 4, 5)
+    PROJECT_KIND = "project"            # QKV projection of step_hidden (timing kind 6)
 
     def timing_enable(self, max_launches: int):
         """Bracket every kernel of the following eager steps with CUDA events on its stream."""
         self._call(_lib.lib.nosa_timing_enable, max_launches)
 
     def timing_read(self) -> dict:
-        ms = (ctypes.c_double * 6)()
-        n = (ctypes.c_int64 * 6)()
+        ms = (ctypes.c_double * 7)()
+        n = (ctypes.c_int64 * 7)()
         self._call(_lib.lib.nosa_timing_read, ms, n)
+        kinds = {k: i for i, k in enumerate(self.KERNEL_KINDS)}
+        if n[6]:
+            kinds[self.PROJECT_KIND] = 6
         return {k: {"total_ms": ms[i], "launches": n[i], "avg_ms": ms[i] / n[i] if n[i] else 0.0}
-                for i, k in enumerate(self.KERNEL_KINDS)}
+                for k, i in kinds.items()}
 
     def copy_timing_read(self) -> dict:
         """Host<->device copy time of nosa_decode_step_host (kinds 4, 5) since timing_enable."""
-        ms = (ctypes.c_double * 6)()
-        n = (ctypes.c_int64 * 6)()
+        ms = (ctypes.c_double * 7)()
+        n = (ctypes.c_int64 * 7)()
         self._call(_lib.lib.nosa_timing_read, ms, n)
         return {k: {"total_ms": ms[4 + i], "copies": n[4 + i]} for i, k in enumerate(self.COPY_KINDS)}
 
@@ -522,5 +577,5 @@ class NosaEngine:
         F = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
         self._call(_lib.lib.nosa_timing_trace, cap, kind.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), F(t0), F(t1),
                    ctypes.byref(n))
-        names = self.KERNEL_KINDS + self.COPY_KINDS
+        names = self.KERNEL_KINDS + self.COPY_KINDS + (self.PROJECT_KIND,)
         return [(names[kind[i]], float(t0[i]), float(t1[i])) for i in range(n.value)]

@@ -44,3 +44,55 @@ def test_split_choice_and_exact_identity():
     h = torch.randn(77, d, device="cuda").to(torch.bfloat16)
     q, k, v = proj(h)
     assert torch.equal(torch.cat([q, k, v], 1), h)
+
+
+@pytest.mark.parametrize("schedule,graph", [("pipelined", False), ("serial", False), ("pipelined", True)])
+def test_hidden_state_step_matches_projected_step(schedule, graph):
+    """nosa_decode_step_hidden (projection of every layer inside the step, on the selection
+    stream) gives bitwise the outputs, selections and residency of nosa_decode_step fed with the
+    same tcgen05 projections computed outside."""
+    from paper_2510_13602_b200 import AttentionConfig, NosaEngine, workload
+    cfg = AttentionConfig(n=8192, d=1024, n_head=16, n_kv_head=2, d_head=128, n_b=64, n_s=64, n_w=1024, k=4096,
+                          k_q=1024, k_e=3072)
+    L, B, T, steps = 3, 4, 3000, 6
+    rng = np.random.default_rng(7)
+    ws = [[rng.standard_normal((cfg.d, h * cfg.d_head)) / np.sqrt(cfg.d) for h in (16, 2, 2)] for _ in range(L)]
+    w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, 7)
+    K, V = workload.prefix_kv(7, L * B, cfg.n_kv_head, T, cfg.d_head)
+    K, V = K.reshape(L, B, cfg.n_kv_head, T, cfg.d_head), V.reshape(L, B, cfg.n_kv_head, T, cfg.d_head)
+    hs = [torch.randn(L, B, cfg.d, device="cuda").to(torch.bfloat16) for _ in range(steps)]
+    runs = []
+    for hidden in (False, True):
+        eng = NosaEngine(cfg, batch=B, layers=L, max_tokens=T + steps + 1, fast_slots=70, w1=w1, w2=w2)
+        eng.prefill(torch.from_numpy(K), torch.from_numpy(V))
+        eng.start_run()
+        projs = [QKVProjection(*w) for w in ws]
+        for l in range(L):
+            eng.set_projection(l, *ws[l])
+        outs = []
+        if hidden and graph:
+            hb = torch.empty_like(hs[0])
+            ob = torch.empty((L, B, cfg.n_head, cfg.d_head), dtype=torch.float32, device="cuda")
+            eng.capture_hidden(hb, ob)
+        for s in range(steps):
+            if hidden and graph:
+                hb.copy_(hs[s])
+                eng.replay()
+                out = ob
+            elif hidden:
+                out = eng.step_hidden(hs[s], schedule=schedule)
+            else:
+                qkv = [p(hs[s][l]) for l, p in enumerate(projs)]
+                q = torch.stack([x[0] for x in qkv]).reshape(L, B, cfg.n_head, cfg.d_head)
+                k = torch.stack([x[1] for x in qkv]).reshape(L, B, cfg.n_kv_head, cfg.d_head)
+                v = torch.stack([x[2] for x in qkv]).reshape(L, B, cfg.n_kv_head, cfg.d_head)
+                out = eng.step(q, k, v, schedule=schedule)
+            outs.append(out.cpu().numpy().copy())
+        st = eng.residency_stats()
+        runs.append((np.stack(outs), (st.hits, st.misses, st.evictions), [eng.raw_selection(l)[:4] for l in range(L)]))
+        eng.close()
+    np.testing.assert_array_equal(runs[0][0], runs[1][0])
+    assert runs[0][1] == runs[1][1]
+    for a, b in zip(runs[0][2], runs[1][2]):
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
