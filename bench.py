@@ -69,6 +69,10 @@ def parse():
                     help="'host' (pinned host memory over PCIe) or 'peer' (another GPU's HBM over NVLink: "
                          "device (local_rank + 1) %% GPUs on the node, the own device when alone = loopback)")
     ap.add_argument("--per-step", action="store_true", help="print each timed step's ms to stderr (diagnostics)")
+    ap.add_argument("--inputs", choices=["qkv", "hidden"], default="qkv",
+                    help="qkv: the step's q/k/v are given (BASELINE's synthetic Q/K/V); hidden: hidden states "
+                         "h [layers][batch][d] with per-layer random projections, q/k/v projected on the tensor "
+                         "cores inside the step (DecodeEngine.step(h_t) at batch scale)")
     ap.add_argument("--eager", action="store_true",
                     help="launch every kernel from the host instead of replaying the captured step graph")
     return ap.parse_args()
@@ -265,18 +269,36 @@ def run_native(args, rank, world, local_rank):
     torch.cuda.synchronize(device)
     t_prefill = time.time() - t_setup - t_alloc
 
-    stream = workload.TorchQueryStream(seed_base + 99991, L, B, cfg.n_head, cfg.n_kv_head, cfg.d_head, w["rho"],
-                                       device, dtype)
+    hidden = args.inputs == "hidden"
+    if hidden:  # AR(1) hidden states through random per-layer projections (q keeps the 1/d_head scale)
+        import numpy as np
+        prng = np.random.default_rng(seed_base + 4242)
+        for l in range(L):
+            eng.set_projection(l, prng.standard_normal((cfg.d, cfg.n_head * cfg.d_head)) / np.sqrt(cfg.d * cfg.d_head),
+                               prng.standard_normal((cfg.d, cfg.n_kv_head * cfg.d_head)) / np.sqrt(cfg.d),
+                               prng.standard_normal((cfg.d, cfg.n_kv_head * cfg.d_head)) / np.sqrt(cfg.d))
+        stream = workload.TorchHiddenStream(seed_base + 99991, L, B, cfg.d, w["rho"], device, dtype)
+    else:
+        stream = workload.TorchQueryStream(seed_base + 99991, L, B, cfg.n_head, cfg.n_kv_head, cfg.d_head, w["rho"],
+                                           device, dtype)
     out = torch.empty((L, B, cfg.n_head, cfg.d_head), dtype=torch.float32, device=device)
+
+    def do_step(inp, check=True):
+        """One decode step of every layer on device inputs: (q, k_new, v_new) or (h,)."""
+        if hidden:
+            eng.step_hidden(inp[0], selector=args.selector, out=out, gather=args.gather, check=check,
+                            schedule=args.schedule)
+        else:
+            eng.step(*inp, selector=args.selector, out=out, gather=args.gather, check=check, schedule=args.schedule)
     # residency burn-in (the HBM cache fills to its steady state), then the W warm-up steps;
     # the first steps' inputs/outputs are kept for the CPU-oracle replay
     cpu_steps = min(3, args.burn_in + args.warmup)
     first_inputs, warm_out = [], []
     for i in range(args.burn_in + args.warmup):
-        q, kn, vn = stream.next()
-        eng.step(q, kn, vn, selector=args.selector, out=out, gather=args.gather, schedule=args.schedule)
-        if i < cpu_steps:
-            first_inputs.append((q, kn, vn))
+        inp = stream.next()
+        do_step(inp)
+        if i < cpu_steps and not hidden:
+            first_inputs.append(inp)
             warm_out.append(out.clone())
     # K steps for the clean timed region, K for the instrumented pass, K for the e2e pass
     # K steps for the timed region, K for the instrumented pass, then (e2e) one warm-up + K, all
@@ -286,22 +308,25 @@ def run_native(args, rank, world, local_rank):
     eng.reset_stats()
     use_graph = args.gather != "memcpy" and not args.eager
     if use_graph:  # the whole step as one CUDA graph on fixed buffers, fed by D2D copies
-        gq, gk, gv = (torch.empty_like(x) for x in inputs[0])
-        eng.capture(gq, gk, gv, out, selector=args.selector, gather=args.gather, schedule=args.schedule)
+        gbufs = tuple(torch.empty_like(x) for x in inputs[0])
+        if hidden:
+            eng.capture_hidden(gbufs[0], out, selector=args.selector, gather=args.gather, schedule=args.schedule)
+        else:
+            eng.capture(*gbufs, out, selector=args.selector, gather=args.gather, schedule=args.schedule)
 
     step_events = []
 
     def run_steps(batch_inputs, per_step=False):
-        for q, kn, vn in batch_inputs:
+        for inp in batch_inputs:
             if per_step:
                 step_events.append(torch.cuda.Event(enable_timing=True))
                 step_events[-1].record()
             if use_graph:
-                gq.copy_(q); gk.copy_(kn); gv.copy_(vn)
+                for buf, x in zip(gbufs, inp):
+                    buf.copy_(x)
                 eng.replay()
             else:
-                eng.step(q, kn, vn, selector=args.selector, out=out, gather=args.gather, check=False,
-                         schedule=args.schedule)
+                do_step(inp, check=False)
 
     # ---------------- timed region (value): inputs resident in HBM, no instrumentation
     eng.timing_enable(0)
@@ -363,29 +388,37 @@ def run_native(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
         warm = tuple(pinned(x) for x in inputs[2 * args.steps])  # untimed first host-buffer step
-        if use_graph:  # the host-buffer step as a CUDA graph, re-pointed at each step's buffers;
+        if hidden:  # hidden states: one H2D copy of h, the device step, the D2H read of the outputs
+            hbuf = torch.empty_like(inputs[0][0])
+
+            def e2e_step(hin):
+                hbuf.copy_(hin[0], non_blocking=True)
+                if use_graph:
+                    gbufs[0].copy_(hbuf)
+                    eng.replay()
+                else:
+                    do_step((hbuf,), check=False)
+                host_out.copy_(out, non_blocking=True)
+        elif use_graph:  # the host-buffer step as a CUDA graph, re-pointed at each step's buffers;
             # the warm-up replay uploads the new executable graph
             eng.capture_host(*host_in[0], host_out, selector=args.selector, gather=args.gather,
                              schedule=args.schedule)
-            eng.replay_host(*warm, host_out)
-        else:
-            eng.step_host(*warm, selector=args.selector, out=host_out, gather=args.gather, schedule=args.schedule,
-                          sync=False)
+            e2e_step = lambda hin: eng.replay_host(*hin, host_out)
+        else:  # the host-buffer C ABI call: inputs staged and outputs copied back inside the step
+            e2e_step = lambda hin: eng.step_host(*hin, selector=args.selector, out=host_out, gather=args.gather,
+                                                 schedule=args.schedule, sync=False)
+        e2e_step(warm)
         eng.reset_stats()  # the e2e pass's own miss traffic is reported beside its rate
         torch.cuda.synchronize(device)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         e2e_marks, e2e_host = [], []
-        for hq, hk, hv in host_in:
+        for hin in host_in:
             if args.per_step:
                 e2e_marks.append(torch.cuda.Event(enable_timing=True))
                 e2e_marks[-1].record()
                 e2e_host.append(time.perf_counter())
-            if use_graph:
-                eng.replay_host(hq, hk, hv, host_out)
-            else:  # the host-buffer C ABI call: inputs staged and outputs copied back inside the step
-                eng.step_host(hq, hk, hv, selector=args.selector, out=host_out, gather=args.gather,
-                              schedule=args.schedule, sync=False)
+            e2e_step(hin)
         e1.record()
         torch.cuda.synchronize(device)
         if args.per_step:
@@ -399,12 +432,14 @@ def run_native(args, rank, world, local_rank):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": host_out.numel() * 4,
                "miss_bytes_per_step": int((st_e.misses - st_e.new_blocks) * eng.bytes_per_block / args.steps),
                "ms_per_step": round(e_ms / args.steps, 4),
-               "api": ("NosaEngine.capture_host/replay_host (C ABI nosa_step_graph_launch_host)" if use_graph else
+               "api": ("NosaEngine.step_hidden / capture_hidden (C ABI nosa_decode_step_hidden) after one H2D copy "
+                       "of h" if hidden else
+                       "NosaEngine.capture_host/replay_host (C ABI nosa_step_graph_launch_host)" if use_graph else
                        "NosaEngine.step_host (C ABI nosa_decode_step_host: q/k/v staged per selection group by "
                        "an SM zero-copy kernel, outputs copied back per attention batch while later layers run)") +
                       " on inputs in pinned host memory"}
         eng.check_errors()
-        if args.trace_out:  # one more host-buffer step, instrumented, for the timeline
+        if args.trace_out and not hidden:  # one more host-buffer step, instrumented, for the timeline
             eng.timing_enable(8 * L + 8)
             hq, hk, hv = (pinned(x) for x in stream.next())  # fresh queries: real misses
             eng.step_host(hq, hk, hv, selector=args.selector, out=host_out, gather=args.gather,
@@ -425,8 +460,7 @@ def run_native(args, rank, world, local_rank):
     eng.ktime_enable(True)
     spans = []
     for _ in range(3):  # eager launches (a captured graph holds the pre-diagnostic kernel arguments)
-        eng.step(*stream.next(), selector=args.selector, out=out, gather=args.gather, check=False,
-                 schedule=args.schedule)
+        do_step(stream.next(), check=False)
         spans += [x for x in eng.ktime_read() if x > 0]
     eng.ktime_enable(False)
     attend_exec_ms = statistics.mean(spans) * 1e-3 if spans else None
@@ -449,6 +483,8 @@ def run_native(args, rank, world, local_rank):
         "attend": (R_inst * (bpb + 4)) / calls + B * cfg.n_head * cfg.d_head * 2,
         # K4 merge + K5: f32 outputs + the appended K/V row (HBM slot)
         "finalize": B * cfg.n_head * cfg.d_head * 4 + B * cfg.n_kv_head * 2 * cfg.d_head * 2,
+        # projection (hidden inputs): the layer's bf16 weights, its hidden states, its q/k/v
+        "project": ((cfg.n_head + 2 * cfg.n_kv_head) * cfg.d_head * (cfg.d + B) * 2 + B * cfg.d * 2),
     }
     for k_ in kern:  # per_launch holds bytes per layer; selection may cover several layers per launch
         kern[k_]["bytes_per_launch"] = per_launch[k_] * calls / max(kern[k_]["launches"], 1)
@@ -473,6 +509,9 @@ def run_native(args, rank, world, local_rank):
     h2d_step = (st.misses - st.new_blocks) * bpb / args.steps
     hbm_step = (per_launch["select_plan"] + per_launch["finalize"]) * L + \
         (R_total * (bpb + 4) / args.steps + L * B * cfg.n_head * cfg.d_head * 2) + h2d_step
+    if hidden:  # + the projection: every layer's bf16 weights, hidden states in, q/k/v out
+        n_qkv = (cfg.n_head + 2 * cfg.n_kv_head) * cfg.d_head
+        hbm_step += L * (n_qkv * cfg.d * 2 + B * cfg.d * 2 + B * n_qkv * 2)
     t_roof = max(hbm_step / 8e12, h2d_step / (link_gbs * 1e9))
     step_ms = ms_max / args.steps
     g = kern["gather"]
@@ -493,7 +532,7 @@ def run_native(args, rank, world, local_rank):
 
     # ---------------- CPU baseline: the oracle (reference algorithm) on a bounded sample
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not hidden:
         cpu = cpu_baseline_sample(args, eng, cfg, w, first_inputs, warm_out, seed_base, device, fast, max_tokens)
 
     if rank == 0:
@@ -502,13 +541,17 @@ def run_native(args, rank, world, local_rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
             "higher_is_better": True, "scaling": "strong" if w.get("strong") else "weak", "vs_baseline": None,
             "dtype": "bf16",
-            "data": f"synthetic: K/V ~ N(0,1) bf16, AR(1) queries rho={w['rho']} (torch Philox, seed {args.seed})",
+            "data": (f"synthetic: K/V ~ N(0,1) bf16, AR(1) hidden states rho={w['rho']} through random per-layer "
+                     f"projections (torch Philox / numpy PCG64, seed {args.seed})" if hidden else
+                     f"synthetic: K/V ~ N(0,1) bf16, AR(1) queries rho={w['rho']} (torch Philox, seed {args.seed})"),
             "config": {"workload": f"{args.workload}: {w['desc']}", "model": MODEL, "global_batch": w["global_batch"],
                        "seq_len": ctx_len, "layers": L, "selector": args.selector,
                        "fast_slots_per_seq_head": fast, "blocks_per_seq_head": nblk,
                        "parallelism": f"dp{world} (batch-sharded, no data-path collective)",
                        "gather": args.gather, "schedule": args.schedule, "burn_in_steps": args.burn_in,
                        "cuda_graph": use_graph,
+                       "inputs": ("hidden states [layers][batch][d], QKV projection (tcgen05) inside the step"
+                                  if hidden else "q / k_new / v_new per layer"),
                        "kernel_timing": "instrumented pass: the K steps after the timed region with CUDA events "
                                         "around every kernel on its own stream (event nodes in the graph); "
                                         "value comes from the uninstrumented region",

@@ -96,3 +96,24 @@ class TorchQueryStream:
         eps = t.randn(self.shape_q, generator=self.g, device=self.device) / self.d_head ** 0.5
         self.state = self.rho * self.state + (1.0 - self.rho ** 2) ** 0.5 * eps
         return q, k, v
+
+
+class TorchHiddenStream:
+    """GPU-side AR(1) hidden states h [layers][batch][d] (unit variance): q = h W_q inherits the
+    same per-block AR(1) score process as TorchQueryStream's queries (the projection is linear)."""
+
+    def __init__(self, seed: int, layers: int, batch: int, d: int, rho: float, device, dtype):
+        import torch
+        self.torch = torch
+        self.g = torch.Generator(device=device)
+        self.g.manual_seed(seed)
+        self.shape = (layers, batch, d)
+        self.rho, self.device, self.dtype = rho, device, dtype
+        self.state = torch.randn(self.shape, generator=self.g, device=device)
+
+    def next(self):
+        t = self.torch
+        h = self.state.to(self.dtype)
+        eps = t.randn(self.shape, generator=self.g, device=self.device)
+        self.state = self.rho * self.state + (1.0 - self.rho ** 2) ** 0.5 * eps
+        return (h,)
