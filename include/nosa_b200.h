@@ -225,8 +225,9 @@ int nosa_decode_step_host(NosaCtx* ctx, const NosaHostStepIO* io, void* stream);
 
 /* The QKV projection of one layer for nosa_decode_step_hidden (project_qkv, attention.py:67-90;
  * DecodeEngine.step decode.py:162-164): w_t = [W_q | W_k | W_v]^T, device bf16 [n][d],
- * n = (n_head + 2 n_kv_head) d_head, nq = n_head d_head, nk = n_kv_head d_head.  The buffer
- * stays owned by the caller and must outlive the steps that use it.  bf16 storage only. */
+ * n = (n_head + 2 n_kv_head) d_head, nq = n_head d_head, nk = n_kv_head d_head.  The weights are
+ * copied into the context (all layers side by side, so a selection group's projections run as
+ * one launch).  bf16 storage only. */
 int nosa_set_projection(NosaCtx* ctx, int layer, const void* w_t, int d, int n, int nq, int nk);
 
 /* All layers of one decode step from hidden states: per selection group, the tcgen05

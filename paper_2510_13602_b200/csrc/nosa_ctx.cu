@@ -29,7 +29,7 @@ cudaError_t launch_stage_inputs(const void* const* src, void* const* dst, const 
                                 cudaStream_t st);
 const void* stage_inputs_kernel_fn();
 cudaError_t launch_project(const void* A, const void* Bt, int M, int N, int K, int splits, void* q, void* k, void* v,
-                           int nq, int nk, cudaStream_t st);
+                           int nq, int nk, cudaStream_t st, int layers = 1);
 
 cudaError_t launch_prefill(const Dev& dv, int layer, int seq_begin, int S, const void* k,
                            const void* v, int t, char* staging, cudaStream_t st);
@@ -103,7 +103,8 @@ struct NosaCtx {
   bool stage_with_copies = false;   // NOSA_STAGE_COPIES: stage host inputs with cudaMemcpyAsync
   int attend_layers = 1;            // layers per attention launch (pipelined schedule)
   // QKV projection of nosa_decode_step_hidden: per-layer [W_q | W_k | W_v]^T, bf16 [n][d] (caller-owned)
-  std::vector<const void*> proj_w;
+  char* proj_wbuf = nullptr;         // [L][n][d] bf16, the layers' weights side by side
+  std::vector<char> proj_set;        // per layer: weights loaded
   int proj_d = 0;
   int step_kernels = 0;             // kernels launched by the last enqueued step
   bool select_per_layer = false;
@@ -269,6 +270,7 @@ static void release(NosaCtx* ctx) {
   if (ctx->io_buf) cudaFree(ctx->io_buf);
   if (ctx->dv.ktime) cudaFree(ctx->dv.ktime);
   if (ctx->dv.sel_prof) cudaFree(ctx->dv.sel_prof);
+  if (ctx->proj_wbuf) cudaFree(ctx->proj_wbuf);
   if (ctx->host_mirror && ctx->mirror_device >= 0) {
     cudaSetDevice(ctx->mirror_device);
     cudaFree(ctx->host_mirror);
@@ -968,16 +970,17 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   auto project = [&](int l0, int n) -> int {
     if (!hidden) return NOSA_OK;
     const int N = (dv.Hq + 2 * dv.H) * dv.D, d = ctx->proj_d;
+    // splits by one layer's tiles, as for a single projection (the same sums: bitwise equal results)
     const int tiles = (N / 128) * ((dv.B + 127) / 128), kt = d / 64;
     int splits = tiles * 4 <= 2 * ctx->num_sms ? 4 : 1;
     splits = std::max(1, std::min(splits, kt));
     while (kt % splits) --splits;
-    for (int l = l0; l < l0 + n; ++l) {
+    {  // the group's layers in one launch
       TimeScope ts(ctx, ss, 6, timed);
-      CUDA_TRY(ctx, nosa::launch_project(static_cast<const char*>(hidden) + (size_t)l * dv.B * d * 2, ctx->proj_w[l],
-                                         dv.B, N, d, splits, const_cast<char*>(q) + l * qstride,
-                                         const_cast<char*>(kn) + l * kstride, const_cast<char*>(vn) + l * kstride,
-                                         dv.Hq * dv.D, dv.H * dv.D, ss));
+      CUDA_TRY(ctx, nosa::launch_project(static_cast<const char*>(hidden) + (size_t)l0 * dv.B * d * 2,
+                                         ctx->proj_wbuf + (size_t)l0 * N * d * 2, dv.B, N, d, splits,
+                                         const_cast<char*>(q) + l0 * qstride, const_cast<char*>(kn) + l0 * kstride,
+                                         const_cast<char*>(vn) + l0 * kstride, dv.Hq * dv.D, dv.H * dv.D, ss, n));
       ++n_proj;
     }
     return NOSA_OK;
@@ -1155,16 +1158,22 @@ extern "C" int nosa_set_projection(NosaCtx* ctx, int layer, const void* w_t, int
     return fail(ctx, NOSA_ERR_VALUE, "set_projection: weights must be [n_head + 2 n_kv_head] x d_head columns");
   if (d <= 0 || d % 64 || n % 128) return fail(ctx, NOSA_ERR_VALUE, "set_projection: needs d %% 64 == 0 and n %% 128 == 0");
   if (ctx->proj_d && d != ctx->proj_d) return fail(ctx, NOSA_ERR_VALUE, "set_projection: every layer needs the same d");
-  ctx->proj_w.resize(dv.L, nullptr);
-  ctx->proj_w[layer] = w_t;
+  cudaSetDevice(ctx->device);
+  const size_t slab = (size_t)n * d * 2;
+  if (!ctx->proj_wbuf) {
+    CUDA_TRY(ctx, cudaMalloc(reinterpret_cast<void**>(&ctx->proj_wbuf), slab * dv.L));
+    ctx->proj_set.assign(dv.L, 0);
+  }
+  CUDA_TRY(ctx, cudaMemcpy(ctx->proj_wbuf + layer * slab, w_t, slab, cudaMemcpyDefault));
+  ctx->proj_set[layer] = 1;
   ctx->proj_d = d;
   return NOSA_OK;
 }
 
 static int hidden_staging(NosaCtx* ctx, const NosaHiddenStepIO* hid, NosaStepIO* io) {
   if (!hid || !hid->h || !hid->out) return fail(ctx, NOSA_ERR_VALUE, "decode_step_hidden: NULL io");
-  if (ctx->proj_w.size() != (size_t)ctx->dv.L ||
-      std::any_of(ctx->proj_w.begin(), ctx->proj_w.end(), [](const void* p) { return p == nullptr; }))
+  if (ctx->proj_set.size() != (size_t)ctx->dv.L ||
+      std::any_of(ctx->proj_set.begin(), ctx->proj_set.end(), [](char set) { return !set; }))
     return fail(ctx, NOSA_ERR_STATE, "decode_step_hidden: nosa_set_projection missing for a layer");
   NosaHostStepIO tmp{};  // device staging of q/k/v (the host-step buffers), `out` is the caller's
   tmp.q = tmp.k_new = tmp.v_new = hid->h;

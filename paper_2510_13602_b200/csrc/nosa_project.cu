@@ -44,11 +44,13 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int m, int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+// 3-D box load: coordinates (k, row, layer)
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -74,8 +76,14 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t local_addr, uint32_t rank
 template <int PN>
 __global__ void __launch_bounds__(PTHREADS, 1)
     project_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
-                        int N, int k_per_split, int nq, int nk, __nv_bfloat16* __restrict__ q,
-                        __nv_bfloat16* __restrict__ k, __nv_bfloat16* __restrict__ v) {
+                        int N, int k_per_split, int nq, int nk, __nv_bfloat16* __restrict__ q0,
+                        __nv_bfloat16* __restrict__ k0, __nv_bfloat16* __restrict__ v0, int mtiles) {
+  // blockIdx.y = layer * mtiles + m-tile: several layers' projections in one launch, the layer's
+  // hidden states / weights / outputs one [M][.] slab further on
+  const int layer = blockIdx.y / mtiles;
+  __nv_bfloat16* q = q0 + (size_t)layer * M * nq;
+  __nv_bfloat16* k = k0 + (size_t)layer * M * nk;
+  __nv_bfloat16* v = v0 + (size_t)layer * M * (N - nq - nk);
   constexpr int P_B_BYTES = PN * PK * 2;
   constexpr int P_EPI_LD = PN + 4;  // padded f32 row of the partial tile in smem
   extern __shared__ __align__(1024) char smem_raw[];
@@ -91,7 +99,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   float* tile = reinterpret_cast<float*>(base_ptr);  // [PM][P_EPI_LD] after the main loop
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n0 = blockIdx.x * PN, m0 = blockIdx.y * PM;
+  const int n0 = blockIdx.x * PN, m0 = (blockIdx.y % mtiles) * PM;
   const int splits = gridDim.z;
   const uint32_t rank = cluster_rank();  // = blockIdx.z: clusters span the whole K dimension
   const int kbeg = blockIdx.z * k_per_split, nkt = k_per_split / PK;
@@ -120,10 +128,11 @@ __global__ void __launch_bounds__(PTHREADS, 1)
       const int s = kt % PSTAGES;
       if (kt >= PSTAGES) mbar_wait(&empty[s], ((kt / PSTAGES) - 1) & 1);
       mbar_expect_tx(&full[s], P_A_BYTES + P_B_BYTES);
-      tma_load_2d(sA + s * P_A_BYTES, &map_a, kbeg + kt * PK, m0, &full[s]);
+      tma_load_3d(sA + s * P_A_BYTES, &map_a, kbeg + kt * PK, m0, layer, &full[s]);
 #pragma unroll
       for (int bx = 0; bx < PN / 128; ++bx)  // 128-row boxes of B
-        tma_load_2d(sB + s * P_B_BYTES + bx * (P_B_BYTES * 128 / PN), &map_b, kbeg + kt * PK, n0 + 128 * bx, &full[s]);
+        tma_load_3d(sB + s * P_B_BYTES + bx * (P_B_BYTES * 128 / PN), &map_b, kbeg + kt * PK, n0 + 128 * bx, layer,
+                    &full[s]);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer
@@ -222,7 +231,8 @@ size_t project_smem_bytes() {
   return 1024 + std::max(ring, epi) + (2 * PSTAGES + 1) * 8 + 16;
 }
 
-static bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols) {
+// [layers][rows][cols] bf16, 64 x 128 x 1 boxes with 128B swizzle
+static bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols, int layers) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -231,25 +241,26 @@ static bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols) {
         q != cudaDriverEntryPointSuccess)
       return false;
   }
-  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};  // innermost (K) first
-  const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  const cuuint32_t box[2] = {PK, 128};  // 64 x 128 boxes (B takes two per stage)
-  const cuuint32_t estr[2] = {1, 1};
-  return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+  const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)layers};  // innermost (K) first
+  const cuuint64_t strides[2] = {(cuuint64_t)cols * 2, (cuuint64_t)rows * cols * 2};
+  const cuuint32_t box[3] = {PK, 128, 1};  // 64 x 128 boxes (B takes PN / 128 per stage)
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;  // rows past M read as zeros
 }
 
 template <int PN>
 static cudaError_t launch_project_tiles(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, int splits,
-                                        void* q, void* k, void* v, int nq, int nk, cudaStream_t st) {
+                                        void* q, void* k, void* v, int nq, int nk, int layers, cudaStream_t st) {
   const size_t smem = project_smem_bytes<PN>();
   auto kern = project_gemm_kernel<PN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   max_shared_carveout(kern);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(N / PN, (M + PM - 1) / PM, splits);
+  const int mtiles = (M + PM - 1) / PM;
+  cfg.gridDim = dim3(N / PN, mtiles * layers, splits);
   cfg.blockDim = dim3(PTHREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -261,20 +272,22 @@ static cudaError_t launch_project_tiles(const CUtensorMap& ma, const CUtensorMap
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, ma, mb, M, N, K / splits, nq, nk, static_cast<__nv_bfloat16*>(q),
-                            static_cast<__nv_bfloat16*>(k), static_cast<__nv_bfloat16*>(v));
+                            static_cast<__nv_bfloat16*>(k), static_cast<__nv_bfloat16*>(v), mtiles);
 }
 
 // splits (1..8, a cluster along K): K is cut into `splits` ranges of whole 64-wide k-tiles.
 // 256-column tiles once the 128 x 256 tiles alone fill the SMs (prefill-sized m), else 128
 // (measured on the 1B shape, profiles/r1_projection.txt).
+// `layers` independent projections in one launch: A [layers][M][K], Bt [layers][N][K], outputs
+// [layers][M][n.] (the step's layer-major q / k / v)
 cudaError_t launch_project(const void* A, const void* Bt, int M, int N, int K, int splits, void* q, void* k, void* v,
-                           int nq, int nk, cudaStream_t st) {
-  if (splits < 1 || splits > P_MAX_SPLITS || K % (PK * splits) || N % 128) return cudaErrorInvalidValue;
+                           int nq, int nk, cudaStream_t st, int layers) {
+  if (splits < 1 || splits > P_MAX_SPLITS || K % (PK * splits) || N % 128 || layers < 1) return cudaErrorInvalidValue;
   CUtensorMap ma, mb;
-  if (!make_map(&ma, A, M, K) || !make_map(&mb, Bt, N, K)) return cudaErrorInvalidValue;
-  const bool wide = N % 256 == 0 && (long long)(N / 256) * ((M + PM - 1) / PM) >= 148;
-  return wide ? launch_project_tiles<256>(ma, mb, M, N, K, splits, q, k, v, nq, nk, st)
-              : launch_project_tiles<128>(ma, mb, M, N, K, splits, q, k, v, nq, nk, st);
+  if (!make_map(&ma, A, M, K, layers) || !make_map(&mb, Bt, N, K, layers)) return cudaErrorInvalidValue;
+  const bool wide = N % 256 == 0 && (long long)(N / 256) * ((M + PM - 1) / PM) >= 148;  // per layer: same sums
+  return wide ? launch_project_tiles<256>(ma, mb, M, N, K, splits, q, k, v, nq, nk, layers, st)
+              : launch_project_tiles<128>(ma, mb, M, N, K, splits, q, k, v, nq, nk, layers, st);
 }
 
 }  // namespace nosa

@@ -323,7 +323,7 @@ class NosaEngine:
             self._proj_w = [None] * self.layers
         self._call(_lib.lib.nosa_set_projection, layer, w_t.data_ptr(), w.shape[0], w.shape[1],
                    np.asarray(w_q).shape[1], np.asarray(w_k).shape[1])
-        self._proj_w[layer] = w_t  # the context borrows this buffer
+        self._proj_w[layer] = w_t  # (the context keeps its own copy)
         self.hidden_dim = w.shape[0]
 
     def _hidden_io(self, h, out, selector, gather, schedule):
