@@ -893,11 +893,13 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   const char* kn = static_cast<const char*>(io->k_new);
   const char* vn = static_cast<const char*>(io->v_new);
   const bool timed = count;  // eager steps only (never inside a graph capture)
-  // Four streams, one per stage, linked per layer by events:
-  //   select(l) [st] -> gather(l) [copy] -> attend(l) [att] -> finalize(l) [fin]
+  // One stream per stage, forked from the caller's stream `st` and linked per layer by events:
+  //   [project(group) ->] select(group) [sel] -> gather(l) [copy] -> attend(batch) [att / att2,
+  //   alternating] -> finalize(batch) [fin] [-> D2H of the outputs (host step)]
   // so the selection, miss transfer, attention and merge/append of different layers overlap.
-  // attend(l) also waits finalize(l-2): the split-K records are double-buffered by layer parity.
-  // Layer-pipelined schedule: every select is issued first (valid when each layer's query is
+  // An attention batch also waits for the finalize that last used its split-K record buffers
+  // (nbuf = 2 x layers per batch: double-buffered batches).
+  // Layer-pipelined schedule: the selections are issued first (valid when each layer's query is
   // known up front, as with per-layer query streams).  Layer-serial schedule: select(l) waits
   // for finalize(l-1), as when q_{l+1} is computed from layer l's output.
   const bool serial = io->schedule == 1;

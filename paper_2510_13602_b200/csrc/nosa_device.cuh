@@ -71,7 +71,7 @@ struct Dev {
   int* plan_n;                   // [lbh][3] n_fetch, n_evict, n_hit
   int* cnt;                      // [L][2]: miss count, attention work counter
   int4* miss_list;               // [L][B*H*C]  {lbh, blk, slot, 0}
-  float* part_o;                 // [2][B*H][max_chunks][G][D]  split-K records, layer parity
+  float* part_o;                 // [nbuf][B*H][max_chunks][G][D]  split-K records (layer % nbuf)
   float2* part_ml;               // [2][B*H][max_chunks][G]     (attend(l+1) overlaps finalize(l))
   char* newrow;                  // [lbh][2][D] (elem): K and V row of the last block born by an append
   unsigned long long* ktime;     // diagnostics (NULL = off): [L][2] device-clock start/end of attention launches
