@@ -72,7 +72,7 @@ struct Dev {
   int* cnt;                      // [L][2]: miss count, attention work counter
   int4* miss_list;               // [L][B*H*C]  {lbh, blk, slot, 0}
   float* part_o;                 // [nbuf][B*H][max_chunks][G][D]  split-K records (layer % nbuf)
-  float2* part_ml;               // [2][B*H][max_chunks][G]     (attend(l+1) overlaps finalize(l))
+  float2* part_ml;               // [nbuf][B*H][max_chunks][G]     (m, l) of each record
   char* newrow;                  // [lbh][2][D] (elem): K and V row of the last block born by an append
   unsigned long long* ktime;     // diagnostics (NULL = off): [L][2] device-clock start/end of attention launches
   long long* sel_prof;           // diagnostics (NULL = off): [16] select_plan cycles per phase, [15] = CTAs
