@@ -590,7 +590,6 @@ extern "C" int nosa_prefill(NosaCtx* ctx, int layer, int seq_begin, int seq_coun
   if (need > ctx->staging_bytes) {
     cudaStreamSynchronize(S(stream));
     if (ctx->staging) cudaFree(ctx->staging);
-  if (ctx->io_buf) cudaFree(ctx->io_buf);
     ctx->staging = nullptr;
     CUDA_TRY(ctx, cudaMalloc(&ctx->staging, need));
     ctx->staging_bytes = need;
