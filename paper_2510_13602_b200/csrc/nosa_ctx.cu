@@ -25,6 +25,7 @@ cudaError_t launch_select_scores(int n_prob, const double* s_q, const double* s_
                                  const int* lo, const int* hi, int m_q, int m_e, int selector,
                                  int* out_q, int* n_q, int* out_e, int* n_e, cudaStream_t st);
 cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, bool tma, int nl = 1);
+cudaError_t launch_born(const Dev& dv, int layer, cudaStream_t st, int grid);
 cudaError_t launch_stage_inputs(const void* const* src, void* const* dst, const size_t* bytes, int grid,
                                 cudaStream_t st);
 const void* stage_inputs_kernel_fn();
@@ -107,6 +108,7 @@ struct NosaCtx {
   std::vector<char> proj_set;        // per layer: weights loaded
   int proj_d = 0;
   int step_kernels = 0;             // kernels launched by the last enqueued step
+  int memcpy_born_launches = 0;     // born-block kernels of the copy-engine mover (this step)
   bool select_per_layer = false;
   // graph of the host-buffer step and its host-address nodes (kind 0 = staging kernel, 1 = D2H copy)
   cudaGraph_t graph_host = nullptr;
@@ -705,12 +707,24 @@ static int gather_memcpy(NosaCtx* ctx, int layer, cudaEvent_t plan_done, cudaStr
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->meta_stream));
   ctx->b_dst.resize(n);
   ctx->b_src.resize(n);
-  ctx->b_size.assign(n, (size_t)dv.bpb);
+  int nc = 0, n_born = 0;
   for (int i = 0; i < n; ++i) {
     const int4 m = ctx->h_list[i];
-    ctx->b_src[i] = ctx->host_mirror + ((size_t)m.x * dv.NB + m.y) * dv.bpb;
-    ctx->b_dst[i] = dv.pool + ((size_t)m.x * dv.C + m.z) * dv.bpb;
+    if (m.w) {  // born by the last append: rebuilt on the device from the stash, not copied
+      ++n_born;
+      continue;
+    }
+    ctx->b_src[nc] = ctx->host_mirror + ((size_t)m.x * dv.NB + m.y) * dv.bpb;
+    ctx->b_dst[nc] = dv.pool + ((size_t)m.x * dv.C + m.z) * dv.bpb;
+    ++nc;
   }
+  ctx->b_size.assign(nc, (size_t)dv.bpb);
+  TimeScope ts(ctx, copy_st, 1, timed);
+  if (n_born) {
+    CUDA_TRY(ctx, nosa::launch_born(dv, layer, copy_st, std::min(n_born, ctx->num_sms)));
+    ctx->memcpy_born_launches += 1;
+  }
+  if (nc == 0) return NOSA_OK;
   cudaMemcpyAttributes attr{};
   attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
   attr.srcLocHint.type = ctx->mirror_device >= 0 ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
@@ -718,13 +732,12 @@ static int gather_memcpy(NosaCtx* ctx, int layer, cudaEvent_t plan_done, cudaStr
   attr.dstLocHint.type = cudaMemLocationTypeDevice;
   attr.dstLocHint.id = ctx->device;
   size_t idx0 = 0, fail_idx = 0;
-  TimeScope ts(ctx, copy_st, 1, timed);
-  cudaError_t e = cudaMemcpyBatchAsync(ctx->b_dst.data(), ctx->b_src.data(), ctx->b_size.data(), n, &attr, &idx0, 1,
+  cudaError_t e = cudaMemcpyBatchAsync(ctx->b_dst.data(), ctx->b_src.data(), ctx->b_size.data(), nc, &attr, &idx0, 1,
                                        &fail_idx, copy_st);
   if (e != cudaSuccess) {  // driver without batched copies: one call per block
     cudaGetLastError();
     ctx->batch_fallbacks += 1;
-    for (int i = 0; i < n; ++i)
+    for (int i = 0; i < nc; ++i)
       CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b_dst[i], ctx->b_src[i], ctx->b_size[i], cudaMemcpyDefault, copy_st));
   }
   return NOSA_OK;
@@ -1037,6 +1050,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   // select(l+1) waits for layer l to finish)
   const int nl = serial ? 1 : ctx->attend_layers;
   int n_att = 0, n_gather_kernels = 0;
+  ctx->memcpy_born_launches = 0;
   cudaEvent_t last_att[2] = {nullptr, nullptr};
   for (int l = 0; l < dv.L; ++l) {
     if (serial) {
@@ -1096,7 +1110,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   // kernels of this step: selections (grouped, per layer, or per layer + shared planner),
   // gathers (device movers), attention batches, finalizes, input staging (counted inline)
   const int n_sel = grouped ? (int)groups.size() : (dv.shared ? 2 : 1) * dv.L;
-  ctx->step_kernels = n_sel + n_gather_kernels + 2 * n_att + n_proj;  // one finalize per attention batch
+  ctx->step_kernels = n_sel + n_gather_kernels + ctx->memcpy_born_launches + 2 * n_att + n_proj;  // one finalize per attention batch
   if (count) ctx->launches += ctx->step_kernels;
   return NOSA_OK;
 }

@@ -145,6 +145,23 @@ __global__ void __launch_bounds__(32) gather_tma_kernel(Dev dv, int layer0) {
   if (lane == 0) bulk_wait_all();
 }
 
+// Blocks born by the previous step's append, for the copy-engine mover: the memcpy batch skips
+// them (their only valid row is in the device stash), this kernel writes them into their slots.
+__global__ void __launch_bounds__(256) born_kernel(Dev dv, int layer) {
+  const int n = dv.cnt[2 * layer];
+  const int4* list = dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C;
+  const int vecs = (int)(dv.bpb / 16);
+  for (int e = blockIdx.x; e < n; e += gridDim.x) {
+    const int4 m = list[e];
+    if (m.w) write_born_block(dv, m, reinterpret_cast<int4*>(dv.pool + ((size_t)m.x * dv.C + m.z) * dv.bpb), vecs);
+  }
+}
+
+cudaError_t launch_born(const Dev& dv, int layer, cudaStream_t st, int grid) {
+  born_kernel<<<grid, 256, 0, st>>>(dv, layer);
+  return cudaGetLastError();
+}
+
 // layers [layer, layer + nl) in one launch
 cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, bool tma, int nl) {
   const dim3 g(grid, nl);
