@@ -1076,6 +1076,11 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
     CUDA_TRY(ctx, cudaStreamWaitEvent(a, ctx->ev_gather[l], 0));  // gathers run in order on cp
     // record buffers: layer l' uses buffer l' % nbuf, last written for layer l' - nbuf
     if (l - dv.nbuf >= 0) CUDA_TRY(ctx, cudaStreamWaitEvent(a, ctx->ev_fin[l - dv.nbuf], 0));
+    // Instrumented steps only: the batch's start event also waits for the previous batch (on the
+    // other attention stream), whose persistent CTAs hold every SM until they retire, so the
+    // event pair brackets this launch rather than its queueing behind the previous one.
+    if (n_att > 0 && (timed || (ctx->capturing && ctx->cap_used < ctx->cap_events.size())))
+      CUDA_TRY(ctx, cudaStreamWaitEvent(a, last_att[(n_att - 1) & 1], 0));
     {
       TimeScope ts(ctx, a, 2, timed);
       CUDA_TRY(ctx, nosa::launch_attend(dv, l0, n, q + l0 * qstride, kn + l0 * kstride, vn + l0 * kstride,
