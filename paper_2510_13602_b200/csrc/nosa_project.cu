@@ -5,26 +5,28 @@
 //   [W_q | W_k | W_v] transposed to [N][K] (bf16, K-major), fp32 accumulation in TMEM.
 //
 // Grid (N/256, ceil(M/128), splits), clusters of `splits` CTAs along K.  Each CTA:
-//   warp 0 lane 0  TMA producer: 64-wide bf16 boxes (128B swizzle), 128 rows of A and 256 of B
-//                  per stage, into a 4-stage ring, one mbarrier with the byte count per stage;
+//   warp 0 lane 0  TMA producer: 64-wide bf16 boxes (128B swizzle), up to 128 rows of A and PN
+//                  of B per stage, into a 6-stage ring (4 at PN = 256), one mbarrier per stage;
 //   warp 1 lane 0  MMA issuer: tcgen05.mma M=128 N=256 K=16 (4 per stage) into a 256-column
 //                  TMEM accumulator, tcgen05.commit frees each stage;
-//   all 4 warps    epilogue: tcgen05.ld of the accumulator (warp w = TMEM lanes 32w..) into
-//                  the CTA's shared memory.
-// The split-K partials are then summed across the cluster through distributed shared memory in
-// rank order (deterministic, no global workspace, no second launch): CTA rank j reduces rows
-// [j*128/S, (j+1)*128/S) of the tile and writes them as bf16 into q | k | v.
+//   all 4 warps    epilogue: tcgen05.ld of the accumulator (warp w = TMEM lanes 32w..).
+// One split: each thread converts its row to bf16 and stores it straight into q | k | v.
+// Split-K: the partial tiles go to each CTA's shared memory and are summed across the cluster
+// through distributed shared memory in rank order (deterministic, no global workspace, no
+// second launch): CTA rank j reduces rows [j*128/S, (j+1)*128/S) of the tile and writes them.
+// The A boxes hold the m-tile's rows only (M rounded up to 8 for decode-sized m).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "nosa_device.cuh"
 
 namespace nosa {
 
-constexpr int PM = 128, PK = 64, PSTAGES = 4, PTHREADS = 128;
+constexpr int PM = 128, PK = 64, PTHREADS = 128;
 constexpr int P_A_BYTES = PM * PK * 2;  // 16 KiB A box per stage
 constexpr int P_MAX_SPLITS = 8;            // portable cluster size
 
@@ -72,12 +74,14 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t local_addr, uint32_t rank
   return v;
 }
 
-// PN = 128 or 256 output columns per CTA (B staged as PN / 128 boxes of 128 rows per stage)
-template <int PN>
+// PN = 128 or 256 output columns per CTA (B staged as PN / 128 boxes of 128 rows per stage),
+// PSTAGES ring stages.  A boxes hold `arows` rows (M rounded up to 8, at most 128): the MMA rows
+// past them read stale shared memory and produce accumulator rows that are never stored.
+template <int PN, int PSTAGES>
 __global__ void __launch_bounds__(PTHREADS, 1)
     project_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
                         int N, int k_per_split, int nq, int nk, __nv_bfloat16* __restrict__ q0,
-                        __nv_bfloat16* __restrict__ k0, __nv_bfloat16* __restrict__ v0, int mtiles) {
+                        __nv_bfloat16* __restrict__ k0, __nv_bfloat16* __restrict__ v0, int mtiles, int arows) {
   // blockIdx.y = layer * mtiles + m-tile: several layers' projections in one launch, the layer's
   // hidden states / weights / outputs one [M][.] slab further on
   const int layer = blockIdx.y / mtiles;
@@ -127,7 +131,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
     for (int kt = 0; kt < nkt; ++kt) {
       const int s = kt % PSTAGES;
       if (kt >= PSTAGES) mbar_wait(&empty[s], ((kt / PSTAGES) - 1) & 1);
-      mbar_expect_tx(&full[s], P_A_BYTES + P_B_BYTES);
+      mbar_expect_tx(&full[s], arows * PK * 2 + P_B_BYTES);
       tma_load_3d(sA + s * P_A_BYTES, &map_a, kbeg + kt * PK, m0, layer, &full[s]);
 #pragma unroll
       for (int bx = 0; bx < PN / 128; ++bx)  // 128-row boxes of B
@@ -158,10 +162,52 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   }
   __syncwarp();
 
-  // ---- epilogue: accumulator -> this CTA's f32 partial tile in shared memory
   mbar_wait(done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;");
   const int trow = warp * 32 + lane;
+  if (splits == 1) {
+    // ---- epilogue without split-K: accumulator row -> bf16 -> q | k | v straight from registers
+    // (every 32-column group lies in one of q, k, v: nq and nk are multiples of 128)
+    const int m = m0 + trow;
+    // whole warps past M skip the loads (tcgen05.ld is warp-collective)
+    if (m0 + warp * 32 < M) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < PN; c0 += 32) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+              "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        if (m < M) {
+          const int n = n0 + c0;
+          __nv_bfloat16* dst = n < nq        ? q + (size_t)m * nq + n
+                               : n < nq + nk ? k + (size_t)m * nk + (n - nq)
+                                             : v + (size_t)m * (N - nq - nk) + (n - nq - nk);
+          uint4 w[4];
+          uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+            wp[j] = *reinterpret_cast<const uint32_t*>(&b2);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) reinterpret_cast<uint4*>(dst)[j] = w[j];
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(PN));
+    return;
+  }
+
+  // ---- epilogue: accumulator -> this CTA's f32 partial tile in shared memory
 #pragma unroll 1
   for (int c0 = 0; c0 < PN; c0 += 32) {
     uint32_t r[32];
@@ -225,14 +271,14 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(PN));
 }
 
-template <int PN>
+template <int PN, int PSTAGES>
 size_t project_smem_bytes() {
   const size_t ring = (size_t)PSTAGES * (P_A_BYTES + PN * PK * 2), epi = (size_t)PM * (PN + 4) * 4;
   return 1024 + std::max(ring, epi) + (2 * PSTAGES + 1) * 8 + 16;
 }
 
-// [layers][rows][cols] bf16, 64 x 128 x 1 boxes with 128B swizzle
-static bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols, int layers) {
+// [layers][rows][cols] bf16, 64 x box_rows x 1 boxes with 128B swizzle
+static bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols, int layers, int box_rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -243,18 +289,19 @@ static bool make_map(CUtensorMap* map, const void* ptr, int rows, int cols, int 
   }
   const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)layers};  // innermost (K) first
   const cuuint64_t strides[2] = {(cuuint64_t)cols * 2, (cuuint64_t)rows * cols * 2};
-  const cuuint32_t box[3] = {PK, 128, 1};  // 64 x 128 boxes (B takes PN / 128 per stage)
+  const cuuint32_t box[3] = {PK, (cuuint32_t)box_rows, 1};  // (B: 128-row boxes, PN / 128 per stage)
   const cuuint32_t estr[3] = {1, 1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;  // rows past M read as zeros
 }
 
-template <int PN>
+template <int PN, int PSTAGES>
 static cudaError_t launch_project_tiles(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, int splits,
-                                        void* q, void* k, void* v, int nq, int nk, int layers, cudaStream_t st) {
-  const size_t smem = project_smem_bytes<PN>();
-  auto kern = project_gemm_kernel<PN>;
+                                        void* q, void* k, void* v, int nq, int nk, int layers, int arows,
+                                        cudaStream_t st) {
+  const size_t smem = project_smem_bytes<PN, PSTAGES>();
+  auto kern = project_gemm_kernel<PN, PSTAGES>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   max_shared_carveout(kern);
@@ -272,7 +319,7 @@ static cudaError_t launch_project_tiles(const CUtensorMap& ma, const CUtensorMap
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, ma, mb, M, N, K / splits, nq, nk, static_cast<__nv_bfloat16*>(q),
-                            static_cast<__nv_bfloat16*>(k), static_cast<__nv_bfloat16*>(v), mtiles);
+                            static_cast<__nv_bfloat16*>(k), static_cast<__nv_bfloat16*>(v), mtiles, arows);
 }
 
 // splits (1..8, a cluster along K): K is cut into `splits` ranges of whole 64-wide k-tiles.
@@ -282,12 +329,18 @@ static cudaError_t launch_project_tiles(const CUtensorMap& ma, const CUtensorMap
 // [layers][M][n.] (the step's layer-major q / k / v)
 cudaError_t launch_project(const void* A, const void* Bt, int M, int N, int K, int splits, void* q, void* k, void* v,
                            int nq, int nk, cudaStream_t st, int layers) {
-  if (splits < 1 || splits > P_MAX_SPLITS || K % (PK * splits) || N % 128 || layers < 1) return cudaErrorInvalidValue;
+  if (splits < 1 || splits > P_MAX_SPLITS || K % (PK * splits) || N % 128 || layers < 1 ||
+      (splits == 1 && (nq % 32 || nk % 32)))  // the direct epilogue stores 32-column groups
+    return cudaErrorInvalidValue;
+  // A boxes: the m-tile's rows rounded up to 8 (a decode-sized m stages only its own rows)
+  const int arows = M >= PM ? PM : std::max(8, (M + 7) / 8 * 8);
   CUtensorMap ma, mb;
-  if (!make_map(&ma, A, M, K, layers) || !make_map(&mb, Bt, N, K, layers)) return cudaErrorInvalidValue;
+  if (!make_map(&ma, A, M, K, layers, arows) || !make_map(&mb, Bt, N, K, layers, 128)) return cudaErrorInvalidValue;
+  static const int stages = getenv("NOSA_PROJ_STAGES") ? atoi(getenv("NOSA_PROJ_STAGES")) : 6;
   const bool wide = N % 256 == 0 && (long long)(N / 256) * ((M + PM - 1) / PM) >= 148;  // per layer: same sums
-  return wide ? launch_project_tiles<256>(ma, mb, M, N, K, splits, q, k, v, nq, nk, layers, st)
-              : launch_project_tiles<128>(ma, mb, M, N, K, splits, q, k, v, nq, nk, layers, st);
+  if (wide) return launch_project_tiles<256, 4>(ma, mb, M, N, K, splits, q, k, v, nq, nk, layers, arows, st);
+  return stages <= 4 ? launch_project_tiles<128, 4>(ma, mb, M, N, K, splits, q, k, v, nq, nk, layers, arows, st)
+                     : launch_project_tiles<128, 6>(ma, mb, M, N, K, splits, q, k, v, nq, nk, layers, arows, st);
 }
 
 }  // namespace nosa

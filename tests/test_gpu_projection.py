@@ -82,7 +82,7 @@ def test_hidden_state_step_matches_projected_step(schedule, graph):
             elif hidden:
                 out = eng.step_hidden(hs[s], schedule=schedule)
             else:
-                qkv = [p(hs[s][l]) for l, p in enumerate(projs)]
+                qkv = [p(hs[s][l], 1) for l, p in enumerate(projs)]  # the step's split count
                 q = torch.stack([x[0] for x in qkv]).reshape(L, B, cfg.n_head, cfg.d_head)
                 k = torch.stack([x[1] for x in qkv]).reshape(L, B, cfg.n_kv_head, cfg.d_head)
                 v = torch.stack([x[2] for x in qkv]).reshape(L, B, cfg.n_kv_head, cfg.d_head)
