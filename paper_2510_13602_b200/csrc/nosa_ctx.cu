@@ -108,6 +108,7 @@ struct NosaCtx {
   std::vector<char> proj_set;        // per layer: weights loaded
   int proj_d = 0;
   int step_kernels = 0;             // kernels launched by the last enqueued step
+  std::vector<char> prefilled_resident;  // [L][B]: the last prefill of (layer, seq) placed every block in HBM
   int memcpy_born_launches = 0;     // born-block kernels of the copy-engine mover (this step)
   bool select_per_layer = false;
   // graph of the host-buffer step and its host-address nodes (kind 0 = staging kernel, 1 = D2H copy)
@@ -598,6 +599,8 @@ extern "C" int nosa_prefill(NosaCtx* ctx, int layer, int seq_begin, int seq_coun
   }
   CUDA_TRY(ctx, nosa::launch_prefill(dv, layer, seq_begin, seq_count, k, v, t, ctx->staging, S(stream)));
   ctx->launches += 3;
+  ctx->prefilled_resident.resize((size_t)dv.L * dv.B, 0);
+  for (int b = seq_begin; b < seq_begin + seq_count; ++b) ctx->prefilled_resident[(size_t)layer * dv.B + b] = 0;
   const size_t lbh0 = ((size_t)layer * dv.B + seq_begin) * dv.H;
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_mirror + lbh0 * dv.NB * (size_t)dv.bpb, ctx->staging, need,
                                 cudaMemcpyDefault, S(stream)));  // host, or a peer GPU's HBM
@@ -623,6 +626,7 @@ extern "C" int nosa_prefill_resident(NosaCtx* ctx, int layer, int seq_begin, int
                                   cudaMemcpyDeviceToDevice, S(stream)));
   CUDA_TRY(ctx, nosa::launch_make_resident(dv, layer, seq_begin, seq_count, nblk, S(stream)));
   ctx->launches += 1;
+  for (int b = seq_begin; b < seq_begin + seq_count; ++b) ctx->prefilled_resident[(size_t)layer * dv.B + b] = 1;
   return NOSA_OK;
 }
 
@@ -631,6 +635,16 @@ extern "C" int nosa_start_run(NosaCtx* ctx, int seq_begin, int seq_count, void* 
   if (seq_begin < 0 || seq_count <= 0 || seq_begin + seq_count > ctx->dv.B)
     return fail(ctx, NOSA_ERR_VALUE, "sequence range outside batch");
   cudaSetDevice(ctx->device);
+  // All-resident run: every (layer, sequence) prefilled into HBM and room for every block the
+  // run can create (fast_slots >= blocks of max_tokens), so nothing is ever evicted and the only
+  // misses are newborn blocks, which the planner rebuilds itself (no gather launch per layer).
+  {
+    Dev& dv = ctx->dv;
+    ctx->prefilled_resident.resize((size_t)dv.L * dv.B, 0);
+    bool all = !dv.shared && dv.C >= dv.NB && !getenv("NOSA_GATHER_ALWAYS");
+    for (char r : ctx->prefilled_resident) all = all && r;
+    dv.born_local = all ? 1 : 0;
+  }
   CUDA_TRY(ctx, nosa::launch_start_run(ctx->dv, seq_begin, seq_count, S(stream)));
   ctx->launches += 1;
   if (ctx->dv.screen) {
@@ -1060,22 +1074,25 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
       if (int rc = project(l, 1)) return rc;
       if (int rc = select(l)) return rc;
     }
-    CUDA_TRY(ctx, cudaStreamWaitEvent(cp, ctx->ev_plan[l], 0));
     const bool batch_end = (l + 1) % nl == 0 || l == dv.L - 1;  // last layer of an attention batch
     const int l0 = l - l % nl, n = l - l0 + 1;
-    if (io->gather_mode == NOSA_GATHER_MEMCPY) {
-      const int rc = gather_memcpy(ctx, l, ctx->ev_plan[l], cp, timed);
-      if (rc) return rc;
-    } else if (batch_end) {  // device movers: one launch for the attention batch's layers
-      TimeScope ts(ctx, cp, 1, timed);
-      const bool tma = io->gather_mode == NOSA_GATHER_TMA;
-      CUDA_TRY(ctx, nosa::launch_gather(dv, l0, cp, tma ? ctx->tma_gather_grid : ctx->gather_grid, tma, n));
-      ++n_gather_kernels;
+    if (!dv.born_local) {  // (all resident: the planner placed the newborn blocks, nothing to move)
+      CUDA_TRY(ctx, cudaStreamWaitEvent(cp, ctx->ev_plan[l], 0));
+      if (io->gather_mode == NOSA_GATHER_MEMCPY) {
+        const int rc = gather_memcpy(ctx, l, ctx->ev_plan[l], cp, timed);
+        if (rc) return rc;
+      } else if (batch_end) {  // device movers: one launch for the attention batch's layers
+        TimeScope ts(ctx, cp, 1, timed);
+        const bool tma = io->gather_mode == NOSA_GATHER_TMA;
+        CUDA_TRY(ctx, nosa::launch_gather(dv, l0, cp, tma ? ctx->tma_gather_grid : ctx->gather_grid, tma, n));
+        ++n_gather_kernels;
+      }
+      CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[l], cp));
     }
-    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[l], cp));
     if (!batch_end) continue;
     cudaStream_t a = (n_att & 1) ? at2 : at;
-    CUDA_TRY(ctx, cudaStreamWaitEvent(a, ctx->ev_gather[l], 0));  // gathers run in order on cp
+    // gathers run in order on cp; without gathers the plans complete in layer order on ss
+    CUDA_TRY(ctx, cudaStreamWaitEvent(a, dv.born_local ? ctx->ev_plan[l] : ctx->ev_gather[l], 0));
     // record buffers: layer l' uses buffer l' % nbuf, last written for layer l' - nbuf
     if (l - dv.nbuf >= 0) CUDA_TRY(ctx, cudaStreamWaitEvent(a, ctx->ev_fin[l - dv.nbuf], 0));
     // Instrumented steps only: the batch's start event also waits for the previous batch (on the
@@ -1110,6 +1127,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   }
   // join every side stream back into the caller's stream (the plans precede the last gather)
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_plan[dv.L - 1], 0));
+  if (dv.born_local) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[dv.L - 1], cp));  // (no gathers: joins cp)
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_gather[dv.L - 1], 0));
   for (cudaEvent_t e : last_att)
     if (e) CUDA_TRY(ctx, cudaStreamWaitEvent(st, e, 0));
@@ -1601,6 +1619,8 @@ extern "C" int nosa_check_errors(NosaCtx* ctx, uint32_t* flags) {
     cudaMemset(ctx->dv.err, 0, 4);
     if (f & NOSA_FLAG_CAPACITY)
       return fail(ctx, NOSA_ERR_CAPACITY, "step requires more blocks than the fast tier holds per head (%d)", ctx->dv.C);
+    if (f & NOSA_FLAG_NOT_RESIDENT)
+      return fail(ctx, NOSA_ERR_STATE, "all-resident run met a miss that is not a newborn block (flags 0x%x)", f);
     return fail(ctx, NOSA_ERR_VALUE, "device error flags 0x%x", f);
   }
   return NOSA_OK;

@@ -63,6 +63,8 @@ struct Dev {
   double* s_q;                   // [lbh][NB] pool scores (kept for parity readback)
   // ---- screened selection (exact top-k from a bf16 pre-scan + f64 refinement) -----------
   int screen;                    // 1: screened scan (default), 0: full f64 scan of the pool
+  int born_local;                // 1: every block is HBM-resident for the run, so a block born by an
+                                 // append is the only miss; the planner rebuilds it and no gather runs
   __nv_bfloat16* kc16;           // [lbh][NB][D] bf16(K_c) of the frozen pool (built at start_run)
   float* kc_err;                 // [lbh][NB] sum_i |K_c - bf16(K_c)| of each pool row (rounded up)
   double* qsum_buf;              // [lbh][D] the step's q_sum (parity readback recomputes s_q)
@@ -253,6 +255,17 @@ __device__ double token_score_warp(const T* v, const double* w1, const double* w
     z = fma(silu64(part), w2[j], z);
   }
   return variant == 2 ? exp(z) : z;
+}
+
+// A block born by the previous step's append: row 0 from the device stash, zeros elsewhere
+// (the miss gathers and, for all-resident runs, the planner)
+__device__ __forceinline__ void write_born_block(const Dev& dv, int4 m, int4* dst, int vecs) {
+  const int row_vecs = dv.D * dv.elem / 16, plane_vecs = vecs / 2;
+  const int4* stash = reinterpret_cast<const int4*>(dv.newrow + (size_t)m.x * 2 * dv.D * dv.elem);
+  for (int i = threadIdx.x; i < vecs; i += blockDim.x) {
+    const int which = i / plane_vecs, in_plane = i - which * plane_vecs;
+    dst[i] = in_plane < row_vecs ? stash[which * row_vecs + in_plane] : make_int4(0, 0, 0, 0);
+  }
 }
 
 }  // namespace nosa

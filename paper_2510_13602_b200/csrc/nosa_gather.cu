@@ -27,16 +27,6 @@ __device__ __forceinline__ int4 ld_host(const int4* p) {
   }
 }
 
-__device__ __forceinline__ void write_born_block(const Dev& dv, int4 m, int4* dst, int vecs) {
-  // born at the previous step: row 0 from the device stash, zeros elsewhere
-  const int row_vecs = dv.D * dv.elem / 16, plane_vecs = vecs / 2;
-  const int4* stash = reinterpret_cast<const int4*>(dv.newrow + (size_t)m.x * 2 * dv.D * dv.elem);
-  for (int i = threadIdx.x; i < vecs; i += blockDim.x) {
-    const int which = i / plane_vecs, in_plane = i - which * plane_vecs;
-    dst[i] = in_plane < row_vecs ? stash[which * row_vecs + in_plane] : make_int4(0, 0, 0, 0);
-  }
-}
-
 // Each CTA copies NBLK list entries per iteration: NBLK * bpb / (256 * 16) 16-byte loads per
 // thread are issued before any store, so NBLK * 32 KiB per CTA are in flight on the link.
 template <int NBLK, bool L2HINT>

@@ -652,6 +652,22 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
     dv.req[(size_t)lbh * C + i] = sm.req[i];
     dv.req_slot[(size_t)lbh * C + i] = sm.reqslot[i];
   }
+  if (dv.born_local && nf > 0) {
+    // all-resident run: the misses are blocks born by the last append (still counted as misses,
+    // offload_sim.py:286-289); the planner writes them into their new slots itself, so the
+    // step launches no gather.  Any other miss would break that invariant: flagged.
+    const int t_now = dv.t[lbh], t0 = dv.t0[lbh];
+    for (int f = 0; f < nf; ++f) {
+      const int blk = sm.fetch[f];
+      if (blk * dv.n_b == t_now - 1 && t_now - 1 >= t0) {
+        const int s = sm.reqslot[sm.fpos[f]];
+        write_born_block(dv, make_int4(lbh, blk, s, 1), reinterpret_cast<int4*>(dv.pool + ((size_t)lbh * C + s) * dv.bpb),
+                         (int)(dv.bpb / 16));
+      } else if (tid == 0) {
+        atomicOr(dv.err, 4u);
+      }
+    }
+  }
 }
 
 // grid = (B*H, layers), block = 256: layer = layer0 + blockIdx.y with its queries at
