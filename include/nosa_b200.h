@@ -72,7 +72,7 @@ typedef struct NosaConfig {
   int32_t attend_chunk; /* KV blocks per split-K attention work item (1..8); 0 = auto from
                            the batch size.  Outputs are bit-identical for a fixed value.    */
   int32_t attend_layers; /* layers per persistent attention launch in the pipelined schedule;
-                            0 = auto (7 when every block fits in HBM, else 1)               */
+                            0 = auto (8 when every block fits in HBM, else 1)               */
   int32_t exact_scan;    /* 0: screened selection (bf16 pre-scan of the pool, f64 rescoring of
                             the candidates: the same picks as a full f64 scan); 1: full f64  */
   int32_t slow_tier_device; /* -1: slow tier in pinned host memory (PCIe); >= 0: in that GPU's

@@ -350,14 +350,14 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   if (const char* e = getenv("NOSA_CHUNK")) dv.chunk = std::max(1, std::min(atoi(e), nosa::kChunk));
   dv.max_chunks = (dv.C + dv.chunk - 1) / dv.chunk;
   // layers per attention launch (pipelined schedule): when every block of a sequence fits in
-  // HBM the step is HBM-bound and per-launch ramp-up/drain is the loss, so 7 layers share one
-  // persistent launch (measured on cfg 2: 1 / 4 / 7 / 14 layers per launch = 37.0K / 44.7K /
-  // 45.3K / 45.5K tok/s); with offloaded blocks each layer's attention waits only for its own
-  // miss transfer.  fp32 runs one layer per launch.
+  // HBM the step is HBM-bound and per-launch ramp-up/drain is the loss, so 8 layers share one
+  // persistent launch (measured on cfg 2: 1 / 4 / 6 / 7 / 8 / 10 / 14 layers per launch =
+  // 37.0K / 44.7K / 45.7K / 45.4K / 46.3-46.5K / 46.5K / 45.7K tok/s); with offloaded blocks each
+  // layer's attention waits only for its own miss transfer.  fp32 runs one layer per launch.
   if (c.attend_layers > 0) {
     ctx->attend_layers = c.attend_layers;
   } else {
-    ctx->attend_layers = (dv.C >= dv.NB && c.dtype == NOSA_DTYPE_BF16) ? 7 : 1;
+    ctx->attend_layers = (dv.C >= dv.NB && c.dtype == NOSA_DTYPE_BF16) ? 8 : 1;
   }
   if (const char* e = getenv("NOSA_ATTEND_LAYERS")) ctx->attend_layers = std::max(1, atoi(e));
   if (c.dtype != NOSA_DTYPE_BF16) ctx->attend_layers = 1;

@@ -92,7 +92,7 @@ class NosaEngine:
         attend_chunk: KV blocks per split-K attention work item (1..8, 0 = chosen from the
         batch size); outputs are bit-identical across runs with the same value.
         attend_layers: layers per persistent attention launch in the pipelined schedule (0 =
-        7 when every block fits in HBM, else 1); results do not depend on it.
+        8 when every block fits in HBM, else 1); results do not depend on it.
         exact_scan: score the whole pool in f64 instead of the screened selector (bf16 pre-scan,
         f64 rescoring of the candidates); both pick the same blocks.
         slow_tier: "host" (pinned host memory over PCIe, the reference's SLOW tier) or

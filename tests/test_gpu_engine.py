@@ -317,7 +317,7 @@ def test_exact_score_ties_pick_the_lower_block(exact, selector):
 
 def test_resident_multilayer_batched_attention():
     """All blocks in HBM: several layers per persistent attention launch (6 layers = 4 + 2 here;
-    the default batch is 7)."""
+    the default batch is 8)."""
     a = _run_pair(ONE_B_SMALL, batch=2, t0s=[3000, 2900], steps=8, fast_slots=48, seed=17, rho=0.3, layers=6,
                   resident=True, attend_layers=4)
     assert a <= TOL["bf16"]
