@@ -369,8 +369,8 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
   // (2) s_q = K_c[pool] . q_sum.  Each warp streams 4 block rows per iteration; lane l holds
   //     dims [l*D/32, (l+1)*D/32) of every row, all loads issued before the FMAs, then a
   //     butterfly reduce-scatter leaves row (l>>3)&3 fully summed on lanes with l%8 == 0.
-  //     (4 rows, not 8, keep the CTA at <= 80 registers: 3 CTAs per SM, so one CTA's scan
-  //     overlaps another's sort and plan.)
+  //     (4 rows, not 8, keep the CTA within the 64-register budget of 4 CTAs per SM, so one
+  //     CTA's scan overlaps another's sort and plan.)
   const double* kc = dv.kc + (size_t)lbh * dv.NB * D;
   double* s_q_out = dv.s_q + (size_t)lbh * dv.NB;
   const int nv = D / 64;  // double2 loads per lane per row (1 or 2)
@@ -673,7 +673,7 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
 // grid = (B*H, layers), block = 256: layer = layer0 + blockIdx.y with its queries at
 // q + blockIdx.y * q_layer_stride.  mode: 0 = select only, 1 = select + plan, 2 = plan on ext_req.
 template <typename T>
-__global__ void __launch_bounds__(256, 3)  // 3 CTAs per SM: one CTA's scan overlaps another's sort/plan
+__global__ void __launch_bounds__(256, 4)  // 4 CTAs per SM: one CTA's scan overlaps another's sort/plan
     select_plan_kernel(Dev dv, int layer0, const T* __restrict__ q0, size_t q_layer_stride, int selector,
                        int mode, const int* __restrict__ ext_req, const int* __restrict__ ext_nreq) {
   extern __shared__ __align__(16) char smem_raw[];
