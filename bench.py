@@ -41,7 +41,8 @@ WORKLOADS = {
     "cfg4": dict(desc="1B-class shape, 28 layers, 32K ctx, batch 128, 25% HBM cache, adversarial random queries (rho=0)",
                  shape="1b", layers=28, batch=128, context=32768, cache=0.25, rho=0.0),
     "cfg5": dict(desc="1B-class shape, 64K ctx, batch 512 total batch-sharded over GPUs, 25% HBM cache, per-GPU host pools",
-                 shape="1b", layers=28, batch=512, context=65536, cache=0.25, rho=0.95, strong=True),
+                 shape="1b", layers=28, batch=512, context=65536, cache=0.25, rho=0.95, strong=True,
+                 burn_in=128),  # 256 slots over a 1007-block pool: the miss rate settles after ~100 steps
 }
 
 
@@ -59,8 +60,9 @@ def parse():
     ap.add_argument("--gather", choices=["auto", "uva", "tma", "memcpy"], default="auto",
                     help="auto = copy-engine batches when blocks are offloaded, graph-replayed UVA otherwise")
     ap.add_argument("--schedule", choices=["pipelined", "serial"], default="pipelined")
-    ap.add_argument("--burn-in", type=int, default=32,
-                    help="untimed decode steps before the warm-up so the HBM cache is in steady state")
+    ap.add_argument("--burn-in", type=int, default=None,
+                    help="untimed decode steps before the warm-up so the HBM cache is in steady state "
+                         "(default 32; 128 for cfg5)")
     ap.add_argument("--cpu-pairs", type=int, default=8, help="(sequence, layer) pairs in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -75,7 +77,10 @@ def parse():
                          "cores inside the step (DecodeEngine.step(h_t) at batch scale)")
     ap.add_argument("--eager", action="store_true",
                     help="launch every kernel from the host instead of replaying the captured step graph")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.burn_in is None:
+        a.burn_in = WORKLOADS[a.workload].get("burn_in", 32)
+    return a
 
 
 def attention_config(shape):
