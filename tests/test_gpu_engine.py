@@ -500,7 +500,8 @@ def test_all_resident_run_launches_no_gather(monkeypatch):
     """Resident prefill and room for every block the run can create: nothing is ever evicted,
     the only misses are newborn blocks, the planner writes those itself and the step launches no
     gather.  Bitwise the same outputs, selections, plans and residency as the run that gathers
-    (NOSA_GATHER_ALWAYS), across block boundaries of both sequences, with no device error flag."""
+    (NOSA_GATHER_ALWAYS) and as the captured step graph's replays, across block boundaries of
+    both sequences, with no device error flag."""
     cfg = ONE_B_SMALL
     B, L, steps, seed = 2, 3, 24, 23
     t0s = [3000, 2990]  # both cross the 3008 boundary inside the run
@@ -511,8 +512,8 @@ def test_all_resident_run_launches_no_gather(monkeypatch):
     K = K.reshape(L, B, cfg.n_kv_head, max(t0s), cfg.d_head)
     V = V.reshape(L, B, cfg.n_kv_head, max(t0s), cfg.d_head)
     runs = []
-    for always in (False, True):
-        if always:
+    for mode in ("local", "always", "graph"):
+        if mode == "always":
             monkeypatch.setenv("NOSA_GATHER_ALWAYS", "1")
         else:
             monkeypatch.delenv("NOSA_GATHER_ALWAYS", raising=False)
@@ -526,22 +527,36 @@ def test_all_resident_run_launches_no_gather(monkeypatch):
         eng.start_run()
         eng.timing_enable(4096)
         stream = workload.QueryStream(seed, L, B, cfg.n_head, cfg.n_kv_head, cfg.d_head, 0.3)
+        dev = eng.device
+        qb = torch.empty((L, B, cfg.n_head, cfg.d_head), dtype=torch.bfloat16, device=dev)
+        kb = torch.empty((L, B, cfg.n_kv_head, cfg.d_head), dtype=torch.bfloat16, device=dev)
+        vb = torch.empty_like(kb)
+        ob = torch.empty((L, B, cfg.n_head, cfg.d_head), dtype=torch.float32, device=dev)
         outs, plans = [], []
-        for _ in range(steps):
+        for s in range(steps):
             q, kn, vn = stream.next()
-            outs.append(eng.step(q, kn, vn).cpu().numpy())
+            if mode == "graph":
+                qb.copy_(torch.from_numpy(q)); kb.copy_(torch.from_numpy(kn)); vb.copy_(torch.from_numpy(vn))
+                if s == 0:
+                    eng.capture(qb, kb, vb, ob)
+                eng.replay()
+                outs.append(ob.cpu().numpy().copy())
+            else:
+                outs.append(eng.step(q, kn, vn).cpu().numpy())
             plans.append([[(p.fetch, p.evict, p.hits) for p in row] for l in range(L) for row in eng.plans(l)])
         eng.check_errors()
         st = eng.residency_stats()
-        gathers = eng.timing_read()["gather"]["launches"]
+        gathers = eng.timing_read()["gather"]["launches"] if mode != "graph" else None
         res = [eng.residency(l, b, h) for l in range(L) for b in range(B) for h in range(cfg.n_kv_head)]
         runs.append((np.stack(outs), plans, (st.hits, st.misses, st.evictions), gathers, res))
         eng.close()
-    (o0, p0, s0, g0, r0), (o1, p1, s1, g1, r1) = runs
-    assert g0 == 0 and g1 > 0
-    assert s0 == s1 and s0[2] == 0 and s0[1] > 0  # the newborn blocks are counted as misses
-    assert p0 == p1
-    np.testing.assert_array_equal(o0, o1)
-    for a, b in zip(r0, r1):
-        for x, y in zip(a, b):
-            np.testing.assert_array_equal(np.asarray(x), np.asarray(y))
+    (o0, p0, s0, g0, r0) = runs[0]
+    assert g0 == 0 and runs[1][3] > 0
+    assert s0[2] == 0 and s0[1] > 0  # the newborn blocks are counted as misses
+    for o1, p1, s1, _, r1 in runs[1:]:
+        assert s0 == s1
+        assert p0 == p1
+        np.testing.assert_array_equal(o0, o1)
+        for a, b in zip(r0, r1):
+            for x, y in zip(a, b):
+                np.testing.assert_array_equal(np.asarray(x), np.asarray(y))
