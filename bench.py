@@ -397,17 +397,9 @@ def run_native(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
         warm = tuple(pinned(x) for x in inputs[2 * args.steps])  # untimed first host-buffer step
-        if hidden:  # hidden states: one H2D copy of h, the device step, the D2H read of the outputs
-            hbuf = torch.empty_like(inputs[0][0])
-
-            def e2e_step(hin):
-                hbuf.copy_(hin[0], non_blocking=True)
-                if use_graph:
-                    gbufs[0].copy_(hbuf)
-                    eng.replay()
-                else:
-                    do_step((hbuf,), check=False)
-                host_out.copy_(out, non_blocking=True)
+        if hidden:  # hidden states: each group's rows staged inside the step, outputs back per batch
+            e2e_step = lambda hin: eng.step_hidden_host(hin[0], selector=args.selector, out=host_out,
+                                                        gather=args.gather, schedule=args.schedule, sync=False)
         elif use_graph:  # the host-buffer step as a CUDA graph, re-pointed at each step's buffers;
             # the warm-up replay uploads the new executable graph
             eng.capture_host(*host_in[0], host_out, selector=args.selector, gather=args.gather,
@@ -441,8 +433,8 @@ def run_native(args, rank, world, local_rank):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": host_out.numel() * 4,
                "miss_bytes_per_step": int((st_e.misses - st_e.new_blocks) * eng.bytes_per_block / args.steps),
                "ms_per_step": round(e_ms / args.steps, 4),
-               "api": ("NosaEngine.step_hidden / capture_hidden (C ABI nosa_decode_step_hidden) after one H2D copy "
-                       "of h" if hidden else
+               "api": ("NosaEngine.step_hidden_host (C ABI nosa_decode_step_hidden_host: h staged per selection "
+                       "group by an SM zero-copy kernel, outputs copied back per attention batch)" if hidden else
                        "NosaEngine.capture_host/replay_host (C ABI nosa_step_graph_launch_host)" if use_graph else
                        "NosaEngine.step_host (C ABI nosa_decode_step_host: q/k/v staged per selection group by "
                        "an SM zero-copy kernel, outputs copied back per attention batch while later layers run)") +

@@ -86,6 +86,7 @@ SIGNATURES = {
     "nosa_step_graph_capture_host": (_I, [_P, ctypes.POINTER(NosaHostStepIO)]),
     "nosa_set_projection": (_I, [_P, _I, _P, _I, _I, _I, _I]),
     "nosa_decode_step_hidden": (_I, [_P, ctypes.POINTER(NosaHiddenStepIO), _P]),
+    "nosa_decode_step_hidden_host": (_I, [_P, ctypes.POINTER(NosaHiddenStepIO), _P]),
     "nosa_step_graph_capture_hidden": (_I, [_P, ctypes.POINTER(NosaHiddenStepIO)]),
     "nosa_step_graph_launch_host": (_I, [_P, ctypes.POINTER(NosaHostStepIO), _P]),
     "nosa_step_graph_capture": (_I, [_P, ctypes.POINTER(NosaStepIO)]),

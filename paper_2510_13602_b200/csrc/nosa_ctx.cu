@@ -99,6 +99,8 @@ struct NosaCtx {
   std::vector<std::pair<int, int>> groups;  // selection groups (first layer, layers) of the step
   cudaEvent_t ev_d2h = nullptr;
   char* io_buf = nullptr;
+  char* hid_buf = nullptr;  // [L][B][d] bf16 device copy of host hidden states (nosa_decode_step_hidden_host)
+  size_t hid_bytes = 0;
   size_t io_bytes = 0;
   int stage_grid = 32;              // CTAs of the input-staging kernel (host-buffer step)
   bool stage_with_copies = false;   // NOSA_STAGE_COPIES: stage host inputs with cudaMemcpyAsync
@@ -271,6 +273,7 @@ static void release(NosaCtx* ctx) {
   for (void* p : ctx->dev_allocs) cudaFree(p);
   if (ctx->staging) cudaFree(ctx->staging);
   if (ctx->io_buf) cudaFree(ctx->io_buf);
+  if (ctx->hid_buf) cudaFree(ctx->hid_buf);
   if (ctx->dv.ktime) cudaFree(ctx->dv.ktime);
   if (ctx->dv.sel_prof) cudaFree(ctx->dv.sel_prof);
   if (ctx->proj_wbuf) cudaFree(ctx->proj_wbuf);
@@ -912,7 +915,8 @@ extern "C" int nosa_timing_trace(NosaCtx* ctx, int cap, int32_t* kind, float* st
 }
 
 static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, bool count,
-                        const NosaHostStepIO* hio = nullptr, const void* hidden = nullptr) {
+                        const NosaHostStepIO* hio = nullptr, const void* hidden = nullptr,
+                        const void* hidden_host = nullptr) {
   const Dev& dv = ctx->dv;
   const size_t qstride = (size_t)dv.B * dv.Hq * dv.D * dv.elem;
   const size_t kstride = (size_t)dv.B * dv.H * dv.D * dv.elem;
@@ -980,7 +984,15 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   // device-visible aliases of the host inputs when they are pinned (cudaHostAlloc / registered);
   // pageable inputs fall back to cudaMemcpyAsync
   const char* hsrc[3] = {nullptr, nullptr, nullptr};
-  if (hio && !ctx->stage_with_copies) {
+  const char* hsrc_h = nullptr;  // device alias of pinned host hidden states (hidden host step)
+  if (hidden_host && !ctx->stage_with_copies) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, hidden_host) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+      hsrc_h = static_cast<const char*>(pa.devicePointer);
+    else
+      cudaGetLastError();
+  }
+  if (hio && hio->q && !ctx->stage_with_copies) {
     const void* hp[3] = {hio->q, hio->k_new, hio->v_new};
     bool all = true;
     for (int i = 0; i < 3; ++i) {
@@ -999,6 +1011,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   int n_proj = 0;
   auto project = [&](int l0, int n) -> int {
     if (!hidden) return NOSA_OK;
+    if (hidden_host) CUDA_TRY(ctx, cudaStreamWaitEvent(ss, ctx->ev_in[l0 + n - 1], 0));  // staged h
     const int N = (dv.Hq + 2 * dv.H) * dv.D, d = ctx->proj_d;
     // One split: a group's layers fill the SMs, and each CTA streams its weight rows over the
     // whole K and stores straight from TMEM (measured on cfg 2 with hidden inputs: 42.1K tok/s
@@ -1019,7 +1032,23 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   auto issue_groups = [&](size_t upto) -> int {
     for (; next_group < std::min(upto, groups.size()); ++next_group) {
       const int l0 = groups[next_group].first, n = groups[next_group].second;
-      if (hio && hsrc[0]) {  // mapped pinned inputs: the SMs stage them (zero-copy loads)
+      if (hidden_host) {  // the group's hidden states, host -> the device buffer the projection reads
+        cudaStream_t in = ctx->in_stream;
+        TimeScope ts(ctx, in, 4, timed);
+        const size_t hstride = (size_t)dv.B * ctx->proj_d * 2;
+        char* dst = const_cast<char*>(static_cast<const char*>(hidden)) + l0 * hstride;
+        if (hsrc_h) {
+          const void* src[3] = {hsrc_h + l0 * hstride, nullptr, nullptr};
+          void* dsts[3] = {dst, nullptr, nullptr};
+          const size_t bytes[3] = {n * hstride, 0, 0};
+          CUDA_TRY(ctx, nosa::launch_stage_inputs(src, dsts, bytes, ctx->stage_grid, in));
+          if (count) ctx->launches += 1;
+        } else {
+          CUDA_TRY(ctx, cudaMemcpyAsync(dst, static_cast<const char*>(hidden_host) + l0 * hstride, n * hstride,
+                                        cudaMemcpyHostToDevice, in));
+        }
+        CUDA_TRY(ctx, cudaEventRecord(ctx->ev_in[l0 + n - 1], in));
+      } else if (hio && hsrc[0]) {  // mapped pinned inputs: the SMs stage them (zero-copy loads)
         cudaStream_t in = ctx->in_stream;
         TimeScope ts(ctx, in, 4, timed);
         const void* src[3] = {hsrc[0] + l0 * qstride, hsrc[1] + l0 * kstride, hsrc[2] + l0 * kstride};
@@ -1029,7 +1058,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
         CUDA_TRY(ctx, nosa::launch_stage_inputs(src, dst, bytes, ctx->stage_grid, in));
         if (count) ctx->launches += 1;  // (counted apart from step_kernels: capture_host adds one per group)
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev_in[l0 + n - 1], in));
-      } else if (hio) {
+      } else if (hio && hio->q) {
         cudaStream_t in = ctx->in_stream;
         TimeScope ts(ctx, in, 4, timed);
         CUDA_TRY(ctx, cudaMemcpyAsync(const_cast<char*>(q) + l0 * qstride,
@@ -1231,6 +1260,27 @@ extern "C" int nosa_decode_step_hidden(NosaCtx* ctx, const NosaHiddenStepIO* hid
   NosaStepIO io;
   if (int rc = hidden_staging(ctx, hid, &io)) return rc;
   return enqueue_step(ctx, &io, S(stream), true, nullptr, hid->h);
+}
+extern "C" int nosa_decode_step_hidden_host(NosaCtx* ctx, const NosaHiddenStepIO* hid, void* stream) {
+  if (!ctx) return NOSA_ERR_VALUE;
+  NosaStepIO io;
+  if (int rc = hidden_staging(ctx, hid, &io)) return rc;
+  // device copies: q/k/v and outputs in the host-step staging, h in its own buffer
+  const Dev& dv = ctx->dv;
+  const size_t hb = (size_t)dv.L * dv.B * ctx->proj_d * 2;
+  if (ctx->hid_bytes < hb) {
+    if (ctx->hid_buf) cudaFree(ctx->hid_buf);
+    ctx->hid_buf = nullptr;
+    CUDA_TRY(ctx, cudaMalloc(reinterpret_cast<void**>(&ctx->hid_buf), hb));
+    ctx->hid_bytes = hb;
+  }
+  io.out = reinterpret_cast<float*>(ctx->io_buf + ctx->io_bytes - (size_t)dv.L * dv.B * dv.Hq * dv.D * sizeof(float));
+  NosaHostStepIO out_only{};  // outputs back per attention batch (the host-step D2H path)
+  out_only.out = hid->out;
+  out_only.selector = hid->selector;
+  out_only.gather_mode = hid->gather_mode;
+  out_only.schedule = hid->schedule;
+  return enqueue_step(ctx, &io, S(stream), true, &out_only, ctx->hid_buf, hid->h);
 }
 
 // device-visible aliases of pinned host buffers (NULL when a buffer is pageable)

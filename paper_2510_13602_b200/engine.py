@@ -353,6 +353,42 @@ class NosaEngine:
             self.check_errors()
         return out
 
+    def step_hidden_host(self, h, selector: str = "nosa", out: torch.Tensor | None = None, gather: str = "auto",
+                         schedule: str = "pipelined", sync: bool = True) -> torch.Tensor:
+        """`step_hidden` on host tensors (DecodeEngine.step(h_t)'s convention, decode.py:152-190):
+        h a CPU bf16 [layers][batch][d] (pinned: the GPU stages each selection group's rows with
+        zero-copy loads), out a CPU float32 [layers][batch][n_head][d_head] filled per attention
+        batch while later layers run.  With sync=False `out` is complete once torch's current
+        stream reaches this point."""
+        if selector not in SELECTORS:
+            raise ValueError(f"selector must be one of {SELECTORS}")
+        gather = self._mover(gather)
+        self._check_step()
+        L, B, cfg = self.layers, self.batch, self.config
+        if isinstance(h, np.ndarray):
+            h = torch.from_numpy(np.ascontiguousarray(h))
+        if not isinstance(h, torch.Tensor) or h.device.type != "cpu":
+            raise ValueError("h must be a host array or CPU tensor")
+        if h.dtype != torch.bfloat16 or not h.is_contiguous():
+            h = h.to(torch.bfloat16).contiguous().pin_memory()
+        if h.numel() != L * B * self.hidden_dim:
+            raise ValueError(f"h has {h.numel()} elements, expected {(L, B, self.hidden_dim)}")
+        if out is None:
+            out = torch.empty((L, B, cfg.n_head, cfg.d_head), dtype=torch.float32, pin_memory=True)
+        elif out.device.type != "cpu" or out.dtype != torch.float32 or not out.is_contiguous() \
+                or out.numel() != L * B * cfg.n_head * cfg.d_head:
+            raise ValueError("out must be a contiguous CPU float32 tensor of the output shape")
+        io = _lib.NosaHiddenStepIO(h.data_ptr(), out.data_ptr(), _lib.SELECTOR[selector], _lib.GATHER[gather],
+                                   _lib.SCHEDULE[schedule])
+        self._hidden_keep = h
+        with torch.cuda.device(self.device):
+            self._call(_lib.lib.nosa_decode_step_hidden_host, ctypes.byref(io), _lib.stream_ptr())
+            self._t += 1
+            if sync:
+                torch.cuda.current_stream().synchronize()
+                self.check_errors()
+        return out
+
     def capture_hidden(self, h: torch.Tensor, out: torch.Tensor, selector: str = "nosa", gather: str = "auto",
                        schedule: str = "pipelined"):
         """Capture one step_hidden on fixed device buffers as a CUDA graph; replay() re-runs it."""

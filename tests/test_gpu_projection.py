@@ -46,8 +46,10 @@ def test_split_choice_and_exact_identity():
     assert torch.equal(torch.cat([q, k, v], 1), h)
 
 
-@pytest.mark.parametrize("schedule,graph", [("pipelined", False), ("serial", False), ("pipelined", True)])
-def test_hidden_state_step_matches_projected_step(schedule, graph):
+@pytest.mark.parametrize("schedule,graph,host", [("pipelined", False, False), ("serial", False, False),
+                                                 ("pipelined", True, False), ("pipelined", False, True),
+                                                 ("serial", False, True)])
+def test_hidden_state_step_matches_projected_step(schedule, graph, host):
     """nosa_decode_step_hidden (projection of every layer inside the step, on the selection
     stream) gives bitwise the outputs, selections and residency of nosa_decode_step fed with the
     same tcgen05 projections computed outside."""
@@ -79,6 +81,8 @@ def test_hidden_state_step_matches_projected_step(schedule, graph):
                 hb.copy_(hs[s])
                 eng.replay()
                 out = ob
+            elif hidden and host:  # host buffers in and out (nosa_decode_step_hidden_host)
+                out = eng.step_hidden_host(hs[s].cpu().pin_memory(), schedule=schedule)
             elif hidden:
                 out = eng.step_hidden(hs[s], schedule=schedule)
             else:
