@@ -81,8 +81,11 @@ def test_hidden_state_step_matches_projected_step(schedule, graph, host):
                 hb.copy_(hs[s])
                 eng.replay()
                 out = ob
-            elif hidden and host:  # host buffers in and out (nosa_decode_step_hidden_host)
-                out = eng.step_hidden_host(hs[s].cpu().pin_memory(), schedule=schedule)
+            elif hidden and host:  # host buffers in and out (nosa_decode_step_hidden_host): pinned
+                # (SM staging) in the pipelined case, pageable (cudaMemcpyAsync) in the serial one
+                h_host = hs[s].cpu()
+                out = eng.step_hidden_host(h_host.pin_memory() if schedule == "pipelined" else h_host,
+                                           schedule=schedule)
             elif hidden:
                 out = eng.step_hidden(hs[s], schedule=schedule)
             else:
