@@ -18,5 +18,5 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 -
   --log-file gpurun_out/launches_cfg3.csv python bench.py --steps 3 --warmup 3 --burn-in 2 --no-cpu-baseline --no-e2e \
   > gpurun_out/launches_cfg3.log 2>&1
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
-  --log-file gpurun_out/launches_cfg2.csv python bench.py --workload cfg2 --steps 3 --warmup 3 --burn-in 2 \
+  --log-file gpurun_out/launches_cfg2.csv python bench.py --workload cfg2 --eager --steps 3 --warmup 3 --burn-in 2 \
   --no-cpu-baseline --no-e2e > gpurun_out/launches_cfg2.log 2>&1
