@@ -297,22 +297,35 @@ __global__ void prefill_stats_kernel(Dev dv, int layer, int seq_begin, const T* 
 }
 
 // Prefill, step 2 (the path used): one CTA of 256 threads per (s, h, block), grid-striding over
-// blocks with W1 staged once per CTA.  The block's V rows go to shared memory (fp32, padded rows:
-// conflict-free column reads); each token's score is computed by 256 / n_b threads, one per
-// column subset (z_j = sum_i v_i W1[i][j] in index order, silu, times W2[j]), combined in
-// subset order; the block sums run over rows in order (as prefill_stats_kernel).  Measured on
-// one cfg 3 layer (B=128, 32K, ncu): 14-22 ms against 68-118 ms for the warp-per-block kernel.  The K sums
-// are exact in f64 (bf16 rows), so they match the warp kernel bit for bit.
+// blocks.  One pass over the block loads its V rows into shared memory (fp32, padded rows) and
+// sums K per column in registers.  The importance scores of the block's tokens are one small
+// fp64 GEMM, Z[n_b][n_ev] = V[n_b][D] . W1[D][n_ev], on the FP64 tensor cores
+// (mma.m8n8k4.f64: warp w owns 8-token tiles, W1 pre-arranged per lane as B fragments), then
+// silu(Z) . W2 per token from the accumulator fragments.  Every sum has a fixed order
+// (deterministic); the K sums are exact in f64 for bf16 / fp32 rows.  Measured on one cfg 3
+// layer (B=128, 32K, ncu): 10.2 ms against 117 ms for prefill_stats_kernel.
+__device__ __forceinline__ void dmma_m8n8k4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+constexpr int kPrefillNT = 4;  // up to 32 eviction-head columns (n-tiles of 8)
+
 template <typename T>
 __global__ void __launch_bounds__(256) prefill_block_kernel(Dev dv, int layer, int seq_begin, const T* __restrict__ k,
                                                             const T* __restrict__ v, int t, int S) {
   extern __shared__ __align__(16) char smem[];
-  const int D = dv.D, n_b = dv.n_b, n_ev = dv.n_ev, tid = threadIdx.x;
-  const int P = blockDim.x / n_b;  // threads per token
-  double* w1s = reinterpret_cast<double*>(smem);                    // [D][n_ev]
-  double* red = w1s + (size_t)D * n_ev;                              // [n_b][P]
-  float* vt = reinterpret_cast<float*>(red + (size_t)n_b * P);       // [n_b][D + 1]
-  for (int i = tid; i < D * n_ev; i += blockDim.x) w1s[i] = dv.w1[i];
+  const int D = dv.D, n_b = dv.n_b, n_ev = dv.n_ev, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = (n_ev + 7) / 8, KS = D / 4, VLD = D + 4;
+  double* w1f = reinterpret_cast<double*>(smem);         // [KS][NT][32] B fragments
+  double* red = w1f + (size_t)KS * NT * 32;               // [256] K partials, then token scores
+  float* vt = reinterpret_cast<float*>(red + 256);        // [n_b][D + 4]
+  for (int x = tid; x < KS * NT * 32; x += blockDim.x) {  // lane (k = lane % 4, n = lane / 4)
+    const int l = x & 31, f = x >> 5, nt = f % NT, ks = f / NT;
+    const int i = 4 * ks + (l & 3), j = 8 * nt + (l >> 2);
+    w1f[x] = j < n_ev ? dv.w1[(size_t)i * n_ev + j] : 0.0;
+  }
   const int nblk = (t + n_b - 1) / n_b;
   const int total = S * dv.H * nblk;
   for (int g = blockIdx.x; g < total; g += gridDim.x) {
@@ -322,41 +335,57 @@ __global__ void __launch_bounds__(256) prefill_block_kernel(Dev dv, int layer, i
     const int lo = blk * n_b, cnt = min(n_b, t - lo);
     const T* kb = k + ((size_t)sh * t + lo) * D;
     const T* vb = v + ((size_t)sh * t + lo) * D;
-    __syncthreads();  // W1 staged / the previous block's tile consumed
+    __syncthreads();  // W1 staged / the previous block's tile and scores consumed
+    // one pass over the tile: V rows into shared memory, K column partial sums in registers
+    // (D divides the CTA: thread tid always sees column tid % D; every load independent)
+    double kpart = 0.0;
+#pragma unroll 4
     for (int x = tid; x < cnt * D; x += blockDim.x) {
       const int r = x / D, i = x - r * D;
-      vt[r * (D + 1) + i] = (float)to_f64(vb[x]);
+      vt[r * VLD + i] = (float)to_f64(vb[x]);
+      kpart += to_f64(kb[x]);
     }
-    // K block sums: thread d, rows in order
-    if (tid < D) {
+    red[tid] = kpart;
+    __syncthreads();
+    if (tid < D) {  // K block sums
       double ks = 0.0;
-      for (int r = 0; r < cnt; ++r) ks += to_f64(kb[(size_t)r * D + tid]);
+      for (int u = tid; u < (int)blockDim.x; u += D) ks += red[u];
       if (cnt == n_b) dv.kc[((size_t)lbh * dv.NB + blk) * D + tid] = ks / (double)n_b;
       else dv.tail_ksum[(size_t)lbh * D + tid] = ks;
     }
     __syncthreads();
-    // token scores: token r = tid / P, columns j = sub, sub + P, ...
-    const int r = tid / P, sub = tid - r * P;
-    if (r < cnt) {
-      const float* vr = vt + r * (D + 1);
-      double acc = 0.0;
-      for (int j = sub; j < n_ev; j += P) {
-        double z = 0.0;
-        for (int i = 0; i < D; ++i) z = fma((double)vr[i], w1s[i * n_ev + j], z);
-        acc = fma(silu64(z), dv.w2[j], acc);
+    // token scores: 8-token tiles on the FP64 tensor cores (rows past cnt read stale shared
+    // memory; MMA rows are independent and theirs are dropped)
+    for (int mt = warp; mt < n_b / 8; mt += blockDim.x / 32) {
+      double acc[kPrefillNT][2];
+#pragma unroll
+      for (int nt = 0; nt < kPrefillNT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+      const float* arow = vt + (8 * mt + (lane >> 2)) * VLD + (lane & 3);
+      for (int ks = 0; ks < KS; ++ks) {
+        const double a = (double)arow[4 * ks];
+        const double* bf = w1f + (size_t)ks * NT * 32 + lane;
+#pragma unroll
+        for (int nt = 0; nt < kPrefillNT; ++nt)
+          if (nt < NT) dmma_m8n8k4(acc[nt], a, bf[nt * 32]);
       }
-      red[r * P + sub] = acc;
-    }
-    __syncthreads();
-    if (tid < cnt) {  // the token's score: subsets in order
-      double z = 0.0;
-      for (int u = 0; u < P; ++u) z += red[tid * P + u];
-      red[tid * P] = dv.variant == 2 ? exp(z) : z;
+      // lane holds Z[token 8 mt + lane / 4][columns 8 nt + 2 (lane % 4) + {0, 1}]
+      double part = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < kPrefillNT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = 8 * nt + 2 * (lane & 3) + e;
+          if (nt < NT && j < n_ev) part = fma(silu64(acc[nt][e]), dv.w2[j], part);
+        }
+      part += __shfl_xor_sync(0xffffffffu, part, 1);
+      part += __shfl_xor_sync(0xffffffffu, part, 2);
+      const int tok = 8 * mt + (lane >> 2);
+      if ((lane & 3) == 0 && tok < cnt) red[tok] = dv.variant == 2 ? exp(part) : part;
     }
     __syncthreads();
     if (tid == 0) {
       double se = 0.0;
-      for (int rr = 0; rr < cnt; ++rr) se += red[rr * P];
+      for (int rr = 0; rr < cnt; ++rr) se += red[rr];
       if (cnt == n_b) dv.se[(size_t)lbh * dv.NB + blk] = se / (double)n_b;
       else dv.tail_se[lbh] = se;
     }
@@ -416,12 +445,12 @@ cudaError_t launch_prefill(const Dev& dv, int layer, int seq_begin, int S, const
   reset_residency_kernel<<<S * dv.H, 256, 0, st>>>(dv, layer, seq_begin, S, t);
   const int warps = S * dv.H * nblk;
   const int blocks = (warps * 32 + 255) / 256;
-  // block kernel: n_b divides 256 and D <= 256 (every supported shape); NOSA_PREFILL_WARP=1
-  // keeps the warp-per-block kernel (experiments)
-  const size_t bsmem = (size_t)dv.D * dv.n_ev * 8 + (size_t)dv.n_b * (256 / std::max(dv.n_b, 1)) * 8 +
-                       (size_t)dv.n_b * (dv.D + 1) * 4 + (size_t)dv.n_b * dv.D * 4;
+  // block kernel: n_b % 8 == 0, D divides 256, n_ev <= 32 (every supported shape);
+  // NOSA_PREFILL_WARP=1 keeps the warp-per-block kernel (experiments)
+  const size_t bsmem = (size_t)(dv.D / 4) * ((dv.n_ev + 7) / 8) * 32 * 8 + 256 * 8 + (size_t)dv.n_b * (dv.D + 4) * 4;
   static const bool warp_env = getenv("NOSA_PREFILL_WARP") != nullptr;
-  const bool block_ok = !warp_env && dv.n_b <= 256 && 256 % dv.n_b == 0 && dv.D <= 256 && bsmem <= 200 * 1024;
+  const bool block_ok = !warp_env && dv.n_b % 8 == 0 && dv.n_b <= 256 && 256 % dv.D == 0 && dv.D % 4 == 0 &&
+                        dv.n_ev <= 8 * kPrefillNT && bsmem <= 200 * 1024;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
