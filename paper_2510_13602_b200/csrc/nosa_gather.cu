@@ -219,32 +219,28 @@ cudaError_t launch_stage_inputs(const void* const* src, void* const* dst, const 
 // Prefill, step 1: K/V rows [S][H][t][D] -> swizzled block format [S*H][NB][2][n_b][D] in a
 // device staging buffer (zero padded past t), later copied to the host mirror in one DMA.
 template <typename T>
-__global__ void prefill_layout_kernel(Dev dv, const T* __restrict__ k, const T* __restrict__ v,
-                                      int t, int S, char* __restrict__ staging) {
+__global__ void __launch_bounds__(256) prefill_layout_kernel(Dev dv, const T* __restrict__ k, const T* __restrict__ v,
+                                                             int t, int S, char* __restrict__ staging) {
+  // one CTA per (s*h, block), grid-striding: a block's K rows (and V rows) are n_b contiguous
+  // rows of the input, read as 16-byte chunks and written swizzled into its 32 KiB slot image
   const int elem = sizeof(T);
   const int D = dv.D, n_b = dv.n_b;
-  const int chunks_per_row = D * elem / 16;
-  const long long per_sh = (long long)dv.NB * 2 * n_b * chunks_per_row;  // 16-byte chunks
-  const long long total = (long long)S * dv.H * per_sh;
-  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
-       x += (long long)gridDim.x * blockDim.x) {
-    const long long sh = x / per_sh;
-    long long rem = x - sh * per_sh;
-    const int blk = (int)(rem / (2 * n_b * chunks_per_row));
-    rem -= (long long)blk * 2 * n_b * chunks_per_row;
-    const int which = (int)(rem / (n_b * chunks_per_row));
-    rem -= (long long)which * n_b * chunks_per_row;
-    const int row = (int)(rem / chunks_per_row);
-    const int ch = (int)(rem - (long long)row * chunks_per_row);
-    const int tok = blk * n_b + row;
-    int4 val = make_int4(0, 0, 0, 0);
-    if (tok < t) {
-      const T* src = (which ? v : k) + ((size_t)sh * t + tok) * D;
-      val = reinterpret_cast<const int4*>(src)[ch];
+  const int cpr = D * elem / 16;           // 16-byte chunks per row
+  const int per_plane = n_b * cpr;
+  const int total = S * dv.H * dv.NB;
+  for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    const int sh = g / dv.NB, blk = g - sh * dv.NB;
+    const int lo = blk * n_b;
+    char* dst_blk = staging + (size_t)g * dv.bpb;
+    for (int c = threadIdx.x; c < 2 * per_plane; c += blockDim.x) {
+      const int which = c >= per_plane, rem = c - which * per_plane;
+      const int row = rem / cpr, ch = rem - row * cpr;
+      const int tok = lo + row;
+      int4 val = make_int4(0, 0, 0, 0);
+      if (tok < t) val = reinterpret_cast<const int4*>((which ? v : k) + ((size_t)sh * t + tok) * D)[ch];
+      *reinterpret_cast<int4*>(dst_blk + (size_t)which * n_b * D * elem + (size_t)row * D * elem +
+                               ((ch ^ (row & 7)) << 4)) = val;
     }
-    char* dst = staging + ((size_t)sh * dv.NB + blk) * dv.bpb + (size_t)which * n_b * D * elem +
-                (size_t)row * D * elem + ((ch ^ (row & 7)) << 4);
-    *reinterpret_cast<int4*>(dst) = val;
   }
 }
 
@@ -456,7 +452,7 @@ cudaError_t launch_prefill(const Dev& dv, int layer, int seq_begin, int S, const
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int bgrid = std::max(1, std::min(warps, sms * 4));
   if (dv.dtype == 0) {
-    prefill_layout_kernel<__nv_bfloat16><<<2048, 256, 0, st>>>(
+    prefill_layout_kernel<__nv_bfloat16><<<sms * 8, 256, 0, st>>>(
         dv, static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), t, S, staging);
     if (warps > 0 && block_ok) {
       max_shared_carveout(prefill_block_kernel<__nv_bfloat16>);
@@ -470,7 +466,7 @@ cudaError_t launch_prefill(const Dev& dv, int layer, int seq_begin, int S, const
           static_cast<const __nv_bfloat16*>(v), t, S);
     }
   } else {
-    prefill_layout_kernel<float><<<2048, 256, 0, st>>>(dv, static_cast<const float*>(k),
+    prefill_layout_kernel<float><<<sms * 8, 256, 0, st>>>(dv, static_cast<const float*>(k),
                                                        static_cast<const float*>(v), t, S, staging);
     if (warps > 0 && block_ok) {
       max_shared_carveout(prefill_block_kernel<float>);
