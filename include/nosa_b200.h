@@ -238,7 +238,7 @@ int nosa_set_projection(NosaCtx* ctx, int layer, const void* w_t, int d, int n, 
 int nosa_decode_step_hidden(NosaCtx* ctx, const NosaHiddenStepIO* io, void* stream);
 int nosa_step_graph_capture_hidden(NosaCtx* ctx, const NosaHiddenStepIO* io);
 
-/* nosa_decode_step_hidden with HOST buffers (the reference's DecodeEngine.step(h_t) calling
+/* nosa_decode_step_hidden with HOST buffers (DecodeEngine.step(h_t), decode.py:152-190, calling
  * convention): io->h [layers][batch][d] bf16 and io->out [layers][batch][n_head][d_head] f32 in
  * host memory (pinned: the SMs stage each selection group's hidden states with zero-copy loads;
  * pageable: cudaMemcpyAsync), outputs copied back per attention batch as in
