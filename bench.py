@@ -545,7 +545,7 @@ def run_native(args, rank, world, local_rank):
             "data": (f"synthetic: K/V ~ N(0,1) bf16, AR(1) hidden states rho={w['rho']} through random per-layer "
                      f"projections (torch Philox / numpy PCG64, seed {args.seed})" if hidden else
                      f"synthetic: K/V ~ N(0,1) bf16, AR(1) queries rho={w['rho']} (torch Philox, seed {args.seed})"),
-            "config": {"workload": f"{args.workload}: {w['desc']}", "model": MODEL, "global_batch": w["global_batch"],
+            "config": {"workload": f"{args.workload}: {w['desc']}", "attention_shape": MODEL, "global_batch": w["global_batch"],
                        "seq_len": ctx_len, "layers": L, "selector": args.selector,
                        "fast_slots_per_seq_head": fast, "blocks_per_seq_head": nblk,
                        "parallelism": f"dp{world} (batch-sharded, no data-path collective)",
@@ -699,7 +699,7 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s_full * 1e3, 2),
             "higher_is_better": True, "scaling": "strong" if w.get("strong") else "weak", "vs_baseline": None,
             "dtype": "f64", "data": f"synthetic: K/V ~ N(0,1) bf16-representable, AR(1) queries rho={w['rho']} (numpy PCG64)",
-            "config": {"workload": f"{args.workload}: {w['desc']}", "model": MODEL, "global_batch": B,
+            "config": {"workload": f"{args.workload}: {w['desc']}", "attention_shape": MODEL, "global_batch": B,
                        "seq_len": w["context"], "layers": L, "selector": args.selector,
                        "fast_slots_per_seq_head": fast, "parallelism": f"{cores} host processes"},
             "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "cores": cores, "kind": "port",
