@@ -89,3 +89,16 @@ def test_bench_ranks_agree_on_the_host_limited_shard():
         mp.spawn(_bench_shard_worker, args=(world, port, out), nprocs=world, join=True)
         res = dict(out)
     assert res[0] == res[1] == (40, 80, True)
+
+
+def test_bench_burn_in_defaults(monkeypatch):
+    """Untimed burn-in before the warm-up: 32 steps, 128 for cfg5 (256 slots over a 1007-block
+    pool settle later); an explicit --burn-in wins."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    for argv, want in ((["bench.py"], 32), (["bench.py", "--workload", "cfg5"], 128),
+                       (["bench.py", "--workload", "cfg5", "--burn-in", "7"], 7)):
+        monkeypatch.setattr(sys, "argv", argv)
+        assert bench.parse().burn_in == want
