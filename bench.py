@@ -29,7 +29,33 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "batched decode tokens/s at 32K ctx w/ KV offload; H2D miss GB/s; % roofline"
-MODEL = "1B-class NOSA attention (16 q / 2 kv heads, d_head 128, block 64, k 4096, k_q 1024)"
+
+# AttentionConfig fields of the two attention shapes (config.one_b_config / cfg1_config), kept as
+# plain dicts so the reference arm never imports the package (which loads libnosa_b200.so)
+SHAPES = {
+    "cfg1": dict(n=16384, d=1024, n_head=8, n_kv_head=2, d_head=128, n_b=64, n_s=64, n_w=512, k=1024, k_q=256,
+                 k_e=768, accounting="exclusive"),
+    "1b": dict(n=65536 + 4096, d=2048, n_head=16, n_kv_head=2, d_head=128, n_b=64, n_s=64, n_w=1024, k=4096,
+               k_q=1024, k_e=3072, accounting="inclusive"),
+}
+
+
+def shape_text(c: dict) -> str:
+    return (f"{c['n_head']} q / {c['n_kv_head']} kv heads, d_head {c['d_head']}, block {c['n_b']}, sink {c['n_s']}, "
+            f"window {c['n_w']}, k {c['k']}, k_q {c['k_q']}, k_e {c['k_e']}, {c['accounting']} accounting")
+
+
+def load_path(name: str, rel: str):
+    """A pure-Python module of the package loaded by file path: no package __init__, so no
+    libnosa_b200.so (the reference arm and the CPU legs use the input generator this way)."""
+    import importlib.util
+    if name in sys.modules:
+        return sys.modules[name]
+    spec = importlib.util.spec_from_file_location(name, ROOT / rel)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[name] = mod  # (dataclasses look their module up here)
+    spec.loader.exec_module(mod)
+    return mod
 
 WORKLOADS = {
     "cfg1": dict(desc="single NOSA sparse-attention decode layer, batch 4, 8q/2kv, d128, 8K ctx, block 64, top-k 16",
@@ -42,7 +68,8 @@ WORKLOADS = {
                  shape="1b", layers=28, batch=128, context=32768, cache=0.25, rho=0.0),
     "cfg5": dict(desc="1B-class shape, 64K ctx, batch 512 total batch-sharded over GPUs, 25% HBM cache, per-GPU host pools",
                  shape="1b", layers=28, batch=512, context=65536, cache=0.25, rho=0.95, strong=True,
-                 burn_in=128),  # 256 slots over a 1007-block pool: the miss rate settles after ~100 steps
+                 burn_in=128,  # 256 slots over a 1007-block pool: the miss rate settles after ~100 steps
+                 parity_steps=72, parity_pairs=3),  # the parity sample reaches the first evictions
 }
 
 
@@ -63,7 +90,11 @@ def parse():
     ap.add_argument("--burn-in", type=int, default=None,
                     help="untimed decode steps before the warm-up so the HBM cache is in steady state "
                          "(default 32; 128 for cfg5)")
-    ap.add_argument("--cpu-pairs", type=int, default=8, help="(sequence, layer) pairs in the CPU baseline sample")
+    ap.add_argument("--cpu-pairs", type=int, default=None,
+                    help="(sequence, layer) pairs in the CPU baseline / parity sample (default 6)")
+    ap.add_argument("--parity-steps", type=int, default=None,
+                    help="first decode steps replayed through the oracle for the CPU baseline and the parity "
+                         "check (default: the burn-in + warm-up, at most 40; 72 for cfg5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--trace-out", default=None, help="write the device timeline of one instrumented step here")
@@ -80,12 +111,40 @@ def parse():
     a = ap.parse_args()
     if a.burn_in is None:
         a.burn_in = WORKLOADS[a.workload].get("burn_in", 32)
+    if a.cpu_pairs is None:
+        a.cpu_pairs = WORKLOADS[a.workload].get("parity_pairs", 6)
+    if a.parity_steps is None:
+        a.parity_steps = WORKLOADS[a.workload].get("parity_steps", 40)
+    a.parity_steps = min(a.parity_steps, a.burn_in + a.warmup)
     return a
 
 
 def attention_config(shape):
-    from paper_2510_13602_b200 import cfg1_config, one_b_config
-    return cfg1_config() if shape == "cfg1" else one_b_config(65536)
+    from paper_2510_13602_b200 import AttentionConfig
+    return AttentionConfig(**SHAPES[shape])
+
+
+def token_budget(args, w) -> tuple[int, int, int]:
+    """(max_tokens, blocks per (sequence, head), fast slots) of a run: both arms size the cache
+    the same way, so the reference arm decodes the identical configuration."""
+    total_steps = args.burn_in + args.warmup + args.steps * (2 if args.no_e2e else 3)
+    max_tokens = w["context"] + total_steps + 8  # + the device-clock pass, e2e graph warm-up, traced step
+    nblk = -(-max_tokens // SHAPES[w["shape"]]["n_b"])
+    fast = nblk if w["cache"] == "resident" else int(w["cache"] * nblk)
+    return max_tokens, nblk, fast
+
+
+def bench_config(args, w, world) -> dict:
+    """The `config` object of the JSON line, identical for the native and the reference arm."""
+    _, nblk, fast = token_budget(args, w)
+    return {"workload": f"{args.workload}: {w['desc']}", "attention_shape": shape_text(SHAPES[w["shape"]]),
+            "global_batch": w["global_batch"], "seq_len": w["context"], "layers": w["layers"],
+            "selector": args.selector, "rho": w["rho"], "fast_slots_per_seq_head": fast, "blocks_per_seq_head": nblk,
+            "parallelism": f"dp{world} (batch-sharded, no data-path collective)",
+            "inputs": f"counter-based synthetic q / k_new / v_new and prefix K/V (seed {args.seed}), identical bits "
+                      f"on the GPU and in the CPU oracle",
+            "host_memory_limited_batch": w["host_limited"],
+            "l2": "no flush needed: attended KV per layer-step exceeds the 126 MB L2"}
 
 
 def workload_dims(args, world):
@@ -94,10 +153,10 @@ def workload_dims(args, world):
         w["layers"] = args.layers
     if args.batch:
         w["batch"] = args.batch
-    from paper_2510_13602_b200.dist import shard_batch
+    shard_batch = load_path("nosa_dist", "paper_2510_13602_b200/dist.py").shard_batch
     rank = int(os.environ.get("RANK", "0"))
     shard = shard_batch(w["batch"], world, rank, bool(w.get("strong")))
-    w["batch_local"], w["global_batch"] = shard.seq_count, shard.global_batch
+    w["batch_local"], w["global_batch"], w["seq0"] = shard.seq_count, shard.global_batch, shard.seq_begin
     w["host_limited"] = False
     if args.impl == "native" and args.slow_tier == "peer":  # slow tier + cache + K_c must fit in HBM
         import torch
@@ -109,7 +168,8 @@ def workload_dims(args, world):
             w["batch_local"] = max(1, budget // int(per_seq))
             w["global_batch"] = w["batch_local"] * world
             w["host_limited"] = True
-    elif args.impl == "native":  # the pinned slow tier of every rank on this node must fit in RAM
+    elif args.slow_tier != "peer":  # the pinned slow tier of every rank on this node must fit in RAM
+        # (the reference arm sizes the same way, so both arms name the same batch)
         local = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
         n_blocks = -(-(w["context"] + 256) // 64)
         per_seq = w["layers"] * 2 * n_blocks * 2 * 64 * 128 * 2  # [layers][kv heads][blocks] x 32 KiB
@@ -122,7 +182,7 @@ def workload_dims(args, world):
             w["batch_local"] = fit
             w["global_batch"] = fit * world
             w["host_limited"] = True
-    if world > 1:  # every rank runs the smallest shard any rank fits
+    if world > 1 and args.impl == "native":  # every rank runs the smallest shard any rank fits
         import torch
         import torch.distributed as dist
         if dist.is_initialized():
@@ -134,6 +194,7 @@ def workload_dims(args, world):
             if not w.get("strong") or int(t[1]):
                 w["batch_local"], w["host_limited"] = int(t[0]), bool(t[1])
                 w["global_batch"] = w["batch_local"] * world
+                w["seq0"] = rank * w["batch_local"]
     return w
 
 
@@ -231,7 +292,7 @@ def run_native(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
-    from paper_2510_13602_b200 import NosaEngine, workload
+    from paper_2510_13602_b200 import NosaEngine, synth, workload
     from paper_2510_13602_b200.dist import max_over_ranks, rank_seed
 
     device = torch.device("cuda", local_rank)
@@ -247,11 +308,8 @@ def run_native(args, rank, world, local_rank):
         # from a peer's HBM the SM gather is 30x faster than device-to-device copy-engine batches
         args.gather = "uva" if (w["cache"] == "resident" or args.slow_tier == "peer") else "memcpy"
     cfg = attention_config(w["shape"])
-    L, B, ctx_len = w["layers"], w["batch_local"], w["context"]
-    total_steps = args.burn_in + args.warmup + args.steps * (2 if args.no_e2e else 3)
-    max_tokens = ctx_len + total_steps + 8  # + the device-clock pass, e2e graph warm-up, traced step
-    nblk = -(-max_tokens // cfg.n_b)
-    fast = nblk if w["cache"] == "resident" else int(w["cache"] * nblk)
+    L, B, ctx_len, seq0 = w["layers"], w["batch_local"], w["context"], w["seq0"]
+    max_tokens, nblk, fast = token_budget(args, w)
     dtype = torch.bfloat16
     peer_dev = None
     if args.slow_tier == "peer":  # the slow tier in another GPU's HBM (alone on the box: loopback)
@@ -267,11 +325,10 @@ def run_native(args, rank, world, local_rank):
     eng = NosaEngine(cfg, batch=B, layers=L, max_tokens=max_tokens, fast_slots=fast, w1=w1, w2=w2, dtype="bf16",
                      device=local_rank, slow_tier=slow_tier)
     t_alloc = time.time() - t_setup
-    seed_base = rank_seed(args.seed, rank)
+    # inputs: counter-based draws addressed by GLOBAL sequence id (a rank's shard draws the same
+    # bits a single GPU would), reproduced exactly by the CPU oracle (workload.synth_*)
     for l in range(L):
-        shape = (B, cfg.n_kv_head, ctx_len, cfg.d_head)
-        k = workload.torch_prefix_kv(seed_base + 2 * l, shape, device, dtype)
-        v = workload.torch_prefix_kv(seed_base + 2 * l + 1, shape, device, dtype)
+        k, v = synth.prefix_kv(args.seed, l, seq0, B, cfg.n_kv_head, ctx_len, cfg.d_head, device, dtype)
         eng.prefill(k, v, layer=l, resident=w["cache"] == "resident")
         del k, v
     eng.start_run()
@@ -281,6 +338,7 @@ def run_native(args, rank, world, local_rank):
     hidden = args.inputs == "hidden"
     if hidden:  # AR(1) hidden states through random per-layer projections (q keeps the 1/d_head scale)
         import numpy as np
+        seed_base = rank_seed(args.seed, rank)
         prng = np.random.default_rng(seed_base + 4242)
         for l in range(L):
             eng.set_projection(l, prng.standard_normal((cfg.d, cfg.n_head * cfg.d_head)) / np.sqrt(cfg.d * cfg.d_head),
@@ -288,8 +346,8 @@ def run_native(args, rank, world, local_rank):
                                prng.standard_normal((cfg.d, cfg.n_kv_head * cfg.d_head)) / np.sqrt(cfg.d))
         stream = workload.TorchHiddenStream(seed_base + 99991, L, B, cfg.d, w["rho"], device, dtype)
     else:
-        stream = workload.TorchQueryStream(seed_base + 99991, L, B, cfg.n_head, cfg.n_kv_head, cfg.d_head, w["rho"],
-                                           device, dtype)
+        stream = synth.GpuQueryStream(args.seed, L, seq0, B, cfg.n_head, cfg.n_kv_head, cfg.d_head, w["rho"], device,
+                                      dtype)
     out = torch.empty((L, B, cfg.n_head, cfg.d_head), dtype=torch.float32, device=device)
 
     def do_step(inp, check=True):
@@ -299,16 +357,33 @@ def run_native(args, rank, world, local_rank):
                             schedule=args.schedule)
         else:
             eng.step(*inp, selector=args.selector, out=out, gather=args.gather, check=check, schedule=args.schedule)
-    # residency burn-in (the HBM cache fills to its steady state), then the W warm-up steps;
-    # the first steps' inputs/outputs are kept for the CPU-oracle replay
-    cpu_steps = min(3, args.burn_in + args.warmup)
-    first_inputs, warm_out = [], []
+    # residency burn-in (the HBM cache fills to its steady state), then the W warm-up steps; for a
+    # random sample of (layer, sequence) pairs the first parity_steps steps' inputs, outputs,
+    # selections and cache plans are recorded for the oracle replay (CPU baseline + parity)
+    import numpy as np
+    prng_pairs = np.random.default_rng(5)
+    pairs = [] if hidden or rank != 0 or world != 1 or args.no_cpu_baseline else \
+        sorted({(int(prng_pairs.integers(L)), int(prng_pairs.integers(B))) for _ in range(args.cpu_pairs)})
+    rec = {p: [] for p in pairs}
     for i in range(args.burn_in + args.warmup):
         inp = stream.next()
         do_step(inp)
-        if i < cpu_steps and not hidden:
-            first_inputs.append(inp)
-            warm_out.append(out.clone())
+        if i < args.parity_steps and pairs:
+            for l in sorted({p[0] for p in pairs}):
+                bq, nq, be, ne, rq, nr, _ = eng.raw_selection(l)
+                plans = eng.plans(l)
+                o = out[l].cpu().numpy()
+                for (pl, b) in pairs:
+                    if pl != l:
+                        continue
+                    H = cfg.n_kv_head
+                    rec[(l, b)].append(dict(
+                        inputs=tuple(x[l, b].float().cpu().numpy() for x in inp), out=o[b].copy(),
+                        blocks_q=[bq[b, h, :nq[b, h]].tolist() for h in range(H)],
+                        blocks_e=[be[b, h, :ne[b, h]].tolist() for h in range(H)],
+                        required=[rq[b, h, :nr[b, h]].tolist() for h in range(H)],
+                        fetch=[plans[b][h].fetch for h in range(H)], evict=[plans[b][h].evict for h in range(H)],
+                        hits=[plans[b][h].hits for h in range(H)]))
     # K steps for the clean timed region, K for the instrumented pass, K for the e2e pass
     # K steps for the timed region, K for the instrumented pass, then (e2e) one warm-up + K, all
     # consecutive in the query stream
@@ -532,9 +607,9 @@ def run_native(args, rank, world, local_rank):
                                                    * 1e3 / step_ms, 4)}
 
     # ---------------- CPU baseline: the oracle (reference algorithm) on a bounded sample
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not hidden:
-        cpu = cpu_baseline_sample(args, eng, cfg, w, first_inputs, warm_out, seed_base, device, fast, max_tokens)
+    cpu, parity = None, None
+    if pairs:
+        cpu, parity = cpu_baseline_sample(args, cfg, w, rec, device, fast, max_tokens)
 
     if rank == 0:
         line = {
@@ -542,25 +617,22 @@ def run_native(args, rank, world, local_rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
             "higher_is_better": True, "scaling": "strong" if w.get("strong") else "weak", "vs_baseline": None,
             "dtype": "bf16",
-            "data": (f"synthetic: K/V ~ N(0,1) bf16, AR(1) hidden states rho={w['rho']} through random per-layer "
-                     f"projections (torch Philox / numpy PCG64, seed {args.seed})" if hidden else
-                     f"synthetic: K/V ~ N(0,1) bf16, AR(1) queries rho={w['rho']} (torch Philox, seed {args.seed})"),
-            "config": {"workload": f"{args.workload}: {w['desc']}", "attention_shape": MODEL, "global_batch": w["global_batch"],
-                       "seq_len": ctx_len, "layers": L, "selector": args.selector,
-                       "fast_slots_per_seq_head": fast, "blocks_per_seq_head": nblk,
-                       "parallelism": f"dp{world} (batch-sharded, no data-path collective)",
-                       "gather": args.gather, "schedule": args.schedule, "burn_in_steps": args.burn_in,
-                       "cuda_graph": use_graph,
-                       "inputs": ("hidden states [layers][batch][d], QKV projection (tcgen05) inside the step"
-                                  if hidden else "q / k_new / v_new per layer"),
-                       "kernel_timing": "instrumented pass: the K steps after the timed region with CUDA events "
-                                        "around every kernel on its own stream (event nodes in the graph); "
-                                        "value comes from the uninstrumented region",
-                       "host_memory_limited_batch": w["host_limited"],
-                       "numa_node": numa_node,
-                       "slow_tier": slow_tier + (" (loopback: the own HBM stands in for a peer)"
-                                                 if peer_dev == local_rank else ""),
-                       "l2": "no flush needed: attended KV per layer-step exceeds the 126 MB L2"},
+            "data": (f"synthetic: K/V ~ N(0,1) bf16 (counter-based), AR(1) hidden states rho={w['rho']} through "
+                     f"random per-layer projections (torch Philox / numpy PCG64, seed {args.seed})" if hidden else
+                     f"synthetic: K/V ~ N(0,1) bf16, AR(1) queries rho={w['rho']} (counter-based generator, seed "
+                     f"{args.seed}: the same bits on the GPU and in the CPU oracle)"),
+            "config": bench_config(args, w, world),
+            "run": {"gather": args.gather, "schedule": args.schedule, "burn_in_steps": args.burn_in,
+                    "cuda_graph": use_graph,
+                    "inputs": ("hidden states [layers][batch][d], QKV projection (tcgen05) inside the step"
+                               if hidden else "q / k_new / v_new per layer"),
+                    "kernel_timing": "instrumented pass: the K steps after the timed region with CUDA events "
+                                     "around every kernel on its own stream (event nodes in the graph); "
+                                     "value comes from the uninstrumented region",
+                    "numa_node": numa_node, "seq_range": [seq0, seq0 + B],
+                    "slow_tier": slow_tier + (" (loopback: the own HBM stands in for a peer)"
+                                              if peer_dev == local_rank else "")},
+            "parity": parity,
             "h2d_miss_gbs": round(h2d_step / (step_ms * 1e-3) / 1e9, 3),
             "hit_rate": round(st.hit_rate, 4),
             "misses_per_seq_head_step": round(st.misses / (B * cfg.n_kv_head * L * args.steps), 3),
@@ -582,96 +654,139 @@ def run_native(args, rank, world, local_rank):
     eng.close()
 
 
-def cpu_baseline_sample(args, eng, cfg, w, inputs, warm_out, seed_base, device, fast, max_tokens):
-    """Replay the warm-up steps of a few (sequence, layer) pairs through the oracle on one host
-    core, with the identical inputs, timing it and checking the GPU outputs on the way."""
+def cpu_baseline_sample(args, cfg, w, rec, device, fast, max_tokens):
+    """Replay the recorded first steps of a few (layer, sequence) pairs through the oracle on one
+    host core: the reference algorithm (attend_biased dense over every cached token, K re-pooled
+    every step, TieredBlockManager with 32 KiB payload copies) on the identical inputs.  Times it
+    (cpu_baseline) and compares every decision with the GPU's (parity): blocks_q, blocks_e,
+    required, fetch (plan order), evict (LRR order), hits exactly; outputs within 2e-2."""
     import numpy as np
-    import torch
 
     from oracle import nosa_oracle as O
-    from paper_2510_13602_b200 import workload
+    from paper_2510_13602_b200 import synth, workload
 
-    L, B = w["layers"], w["batch_local"]
-    rng = np.random.default_rng(5)
-    pairs = [(int(rng.integers(L)), int(rng.integers(B))) for _ in range(args.cpu_pairs)]
     oc = O.OracleConfig.from_attention_config(cfg)
     w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, args.seed)
-    steps = len(warm_out)
-    worst, sel_ok, prefill_s, step_s = 0.0, True, 0.0, 0.0
-    for (l, b) in pairs:
-        shape = (B, cfg.n_kv_head, w["context"], cfg.d_head)
-        k = workload.torch_prefix_kv(seed_base + 2 * l, shape, device, torch.bfloat16)[b].float().cpu().numpy()
-        v = workload.torch_prefix_kv(seed_base + 2 * l + 1, shape, device, torch.bfloat16)[b].float().cpu().numpy()
-        orc = O.OracleEngine(oc, 1, 1, max_tokens, fast, w1, w2, store_payload=True)
+    L, H = w["layers"], cfg.n_kv_head
+    worst, prefill_s, step_s, n_steps = 0.0, 0.0, 0.0, 0
+    mism = {"blocks_q": 0, "blocks_e": 0, "required": 0, "fetch": 0, "evict": 0, "hits": 0}
+    ties = evictions = fetches = 0
+    for (l, b), steps in rec.items():
+        k, v = synth.prefix_kv(args.seed, l, w["seq0"] + b, 1, H, w["context"], cfg.d_head, device)
+        k, v = k[0].float().cpu().numpy(), v[0].float().cpu().numpy()
+        orc = O.OracleEngine(oc, 1, 1, max_tokens, fast, w1, w2, store_payload=True, dense=True)
         t0 = time.perf_counter()
         orc.prefill(0, 0, k, v)
         orc.start_run()
-        t1 = time.perf_counter()
-        for s in range(steps):
-            q, kn, vn = (x[l, b].float().cpu().numpy() for x in inputs[s])
+        if w["cache"] == "resident":
+            for h in range(H):
+                orc.managers[0][0].make_resident(h, -(-w["context"] // cfg.n_b))
+        prefill_s += time.perf_counter() - t0
+        for g in steps:
+            q, kn, vn = g["inputs"]
             ts = time.perf_counter()
-            ref, _ = orc.step_seq(0, 0, q, kn, vn, args.selector)
+            ref, recs = orc.step_seq(0, 0, q, kn, vn, args.selector)
             step_s += time.perf_counter() - ts
-            got = warm_out[s][l, b].cpu().numpy()
-            worst = max(worst, float(np.max(np.abs(got - ref)) / np.max(np.abs(ref))))
-        prefill_s += t1 - t0
-    per_pair_step = step_s / (len(pairs) * steps)
-    return {"value": round(1.0 / (L * per_pair_step), 4), "unit": "tokens/s", "cores": 1, "kind": "port",
-            "sample": f"{len(pairs)} random (sequence, layer) pairs x {steps} decode steps of the oracle "
-                      f"(DecodeEngine.step re-pooling K every step + per-sequence TieredBlockManager with 32 KiB "
-                      f"payload copies), one host core; tokens/s = 1 / (layers x seconds per pair-step)",
-            "seconds_per_pair_step": round(per_pair_step, 5), "prefill_seconds_per_pair": round(prefill_s / len(pairs), 3),
-            "gpu_vs_oracle_max_rel_err": worst}
+            n_steps += 1
+            worst = max(worst, float(np.max(np.abs(g["out"] - ref)) / np.max(np.abs(ref))))
+            for h, r in enumerate(recs):
+                for key, want in (("blocks_q", r.blocks_q.tolist()), ("blocks_e", r.blocks_e.tolist()),
+                                  ("required", r.required), ("fetch", r.fetch), ("evict", r.evict), ("hits", r.hits)):
+                    if g[key][h] != want:
+                        if key in ("blocks_q", "blocks_e"):  # an exact score tie is reported, not a mismatch
+                            sc = dict(zip(range(*orc.geom[0].pool), r.s_q if key == "blocks_q" else r.s_e_c))
+                            if len({sc.get(x) for x in set(g[key][h]) ^ set(want)}) == 1:
+                                ties += 1
+                                continue
+                        mism[key] += 1
+                evictions += len(r.evict)
+                fetches += len(r.fetch)
+    per_pair_step = step_s / max(n_steps, 1)
+    cpu = {"value": round(1.0 / (L * per_pair_step), 4), "unit": "tokens/s", "cores": 1, "kind": "port",
+           "sample": f"{len(rec)} random (layer, sequence) pairs x their first {n_steps // max(len(rec), 1)} decode "
+                     f"steps through the oracle (the reference algorithm: attend_biased dense over every cached token, "
+                     f"K re-pooled every step, per-sequence TieredBlockManager with 32 KiB payload copies) on the "
+                     f"same inputs, one host core; tokens/s = 1 / (layers x seconds per pair-step)",
+           "seconds_per_pair_step": round(per_pair_step, 5), "prefill_seconds_per_pair": round(prefill_s / len(rec), 3)}
+    parity = {"pairs": len(rec), "steps": n_steps // max(len(rec), 1), "heads_checked": n_steps * H,
+              "sel_mismatch": mism["blocks_q"] + mism["blocks_e"], "required_mismatch": mism["required"],
+              "fetch_mismatch": mism["fetch"], "evict_mismatch": mism["evict"], "hit_mismatch": mism["hits"],
+              "ties_reported": ties, "fetches_checked": fetches, "evictions_checked": evictions,
+              "max_rel_err": worst, "tolerance": 2e-2,
+              "what": "GPU vs oracle on identical inputs, every (step, head) of the sampled pairs: blocks_q, "
+                      "blocks_e, required, fetch list, evict list, hits exactly; outputs max|o-o_ref|/max|o_ref|"}
+    return cpu, parity
 
 
 # ------------------------------------------------------------------------------ reference arm
-def _ref_worker(conn, cfg_d, layers, context, max_tokens, fast, rho, seed, selector):
+def _ref_worker(conn, pairs, cfg_d, context, max_tokens, fast, resident, rho, seed, selector):
+    """One host process of the reference arm: the oracle (the reference algorithm) for its
+    (layer, global sequence) pairs, on the exact inputs the GPU arm decodes for those pairs."""
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    import numpy as np
     from oracle import nosa_oracle as O
-    from paper_2510_13602_b200 import workload
-    oc = O.OracleConfig(**cfg_d)
-    w1, w2 = workload.eviction_head(oc.n_head, oc.d_head, 0)
-    K, V = workload.prefix_kv(seed, 1, oc.n_kv_head, context, oc.d_head)
-    orc = O.OracleEngine(oc, 1, 1, max_tokens, fast, w1, w2, store_payload=True)
-    orc.prefill(0, 0, K[0], V[0])
-    orc.start_run()
-    stream = workload.QueryStream(seed, 1, 1, oc.n_head, oc.n_kv_head, oc.d_head, rho)
+    wl = load_path("nosa_workload", "paper_2510_13602_b200/workload.py")
+    oc = O.OracleConfig(**{k: cfg_d[k] for k in ("n_head", "n_kv_head", "d_head", "n_b", "n_s", "n_w", "k", "k_q",
+                                                 "k_e", "accounting")})
+    w1, w2 = wl.eviction_head(oc.n_head, oc.d_head, seed)
+    units = []
+    for (l, gb) in pairs:
+        K, V = wl.synth_prefix_kv(seed, l, [gb], oc.n_kv_head, context, oc.d_head)
+        orc = O.OracleEngine(oc, 1, 1, max_tokens, fast, w1, w2, store_payload=True, dense=True)
+        orc.prefill(0, 0, K[0], V[0])
+        orc.start_run()
+        if resident:
+            for h in range(oc.n_kv_head):
+                orc.managers[0][0].make_resident(h, -(-context // oc.n_b))
+        stream = wl.SynthQueryStream(seed, [l], [gb], oc.n_head, oc.n_kv_head, oc.d_head, rho)
+        units.append((orc, stream))
+        del K, V
     conn.send("ready")
     while True:
         cmd = conn.recv()
         if cmd == "stop":
             break
-        q, kn, vn = stream.next()
-        orc.step_seq(0, 0, q[0, 0], kn[0, 0], vn[0, 0], selector)
+        for orc, stream in units:
+            q, kn, vn = stream.next()
+            orc.step_seq(0, 0, q[0, 0], kn[0, 0], vn[0, 0], selector)
         conn.send("done")
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the reference's CPU algorithm (oracle/nosa_oracle.py, attend_biased dense
+    over every cached token, re-pooled K, TieredBlockManager with payload copies; the reference
+    package itself cannot travel to the GPU box) on this host's cores.  A step decodes `S` whole
+    sequences of the workload through all layers, S chosen so the (layer, sequence) pairs spread
+    evenly over the cores; the inputs are the GPU arm's, bit for bit.  Does not import the package."""
+    import math
     import multiprocessing as mp
 
-    from paper_2510_13602_b200 import workload  # noqa: F401  (same generator as the native arm)
     if rank != 0:
         return
     w = workload_dims(args, world)
-    cfg = attention_config(w["shape"])
+    cfg_d = SHAPES[w["shape"]]
     cores = len(os.sched_getaffinity(0))
-    max_tokens = w["context"] + args.warmup + args.steps + 2
-    nblk = -(-max_tokens // cfg.n_b)
-    fast = nblk if w["cache"] == "resident" else int(w["cache"] * nblk)
-    cfg_d = dict(n_head=cfg.n_head, n_kv_head=cfg.n_kv_head, d_head=cfg.d_head, n_b=cfg.n_b, n_s=cfg.n_s,
-                 n_w=cfg.n_w, k=cfg.k, k_q=cfg.k_q, k_e=cfg.k_e, accounting=cfg.accounting)
+    max_tokens, nblk, fast = token_budget(args, w)
+    L = w["layers"]
+    S = max(1, cores // math.gcd(cores, L))          # S x L pairs = a whole number of rounds per core
+    per_pair = 2 * cfg_d["n_kv_head"] * max_tokens * cfg_d["d_head"] * 8 * 2   # oracle K, V (f64) + payloads
+    S = max(1, min(S, w["global_batch"], int(0.25 * (host_mem_available() or 8 << 30) // (per_pair * L))))
+    seqs = sorted(random_sample(w["global_batch"], S, args.seed))
+    pairs = [(l, gb) for gb in seqs for l in range(L)]
+    nproc = min(cores, len(pairs))
     ctx = mp.get_context("spawn")
     procs, conns = [], []
-    for i in range(cores):
+    t_setup = time.perf_counter()
+    for i in range(nproc):
         a, b = ctx.Pipe()
-        p = ctx.Process(target=_ref_worker, args=(b, cfg_d, w["layers"], w["context"], max_tokens, fast, w["rho"],
-                                                  args.seed * 1000 + i, args.selector), daemon=True)
+        p = ctx.Process(target=_ref_worker, args=(b, pairs[i::nproc], cfg_d, w["context"], max_tokens, fast,
+                                                  w["cache"] == "resident", w["rho"], args.seed, args.selector),
+                        daemon=True)
         p.start()
         procs.append(p)
         conns.append(a)
     for c in conns:
         assert c.recv() == "ready"
+    setup_s = time.perf_counter() - t_setup
 
     def one_step():
         for c in conns:
@@ -689,23 +804,32 @@ def run_reference(args, rank, world):
         c.send("stop")
     for p in procs:
         p.join(timeout=10)
-    # each step advanced `cores` (sequence, layer) pairs of the B x L a full decode step needs
-    L, B = w["layers"], w["global_batch"]
-    step_s_full = dt / args.steps * (B * L) / cores
-    value = B / step_s_full
-    sample = (f"each step = {cores} (sequence, layer) pairs of the {B} x {L} workload, one per host core "
-              f"(multiprocessing, OPENBLAS_NUM_THREADS=1), extrapolated linearly to the full step")
+    step_s = dt / args.steps
+    value = S / step_s                       # tokens/s: S sequences advance one token per step
+    sample = (f"each step decodes {S} of the {w['global_batch']} sequences (global ids {seqs}) through all {L} "
+              f"layers: {len(pairs)} (layer, sequence) pairs over {nproc} host processes (multiprocessing, "
+              f"OPENBLAS_NUM_THREADS=1), on the GPU arm's inputs for those pairs; sequences are independent, so "
+              f"tokens/s does not depend on how many of the batch a step holds")
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s_full * 1e3, 2),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 2),
             "higher_is_better": True, "scaling": "strong" if w.get("strong") else "weak", "vs_baseline": None,
-            "dtype": "f64", "data": f"synthetic: K/V ~ N(0,1) bf16-representable, AR(1) queries rho={w['rho']} (numpy PCG64)",
-            "config": {"workload": f"{args.workload}: {w['desc']}", "attention_shape": MODEL, "global_batch": B,
-                       "seq_len": w["context"], "layers": L, "selector": args.selector,
-                       "fast_slots_per_seq_head": fast, "parallelism": f"{cores} host processes"},
-            "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "cores": cores, "kind": "port",
+            "dtype": "f64",
+            "data": f"synthetic: K/V ~ N(0,1) bf16, AR(1) queries rho={w['rho']} (counter-based generator, seed "
+                    f"{args.seed}: the same bits on the GPU and in the CPU oracle)",
+            "config": bench_config(args, w, world),
+            "sample_batch": S,
+            "ms_per_full_step_extrapolated": round(step_s * 1e3 * w["global_batch"] / S, 1),
+            "setup_s": round(setup_s, 1),
+            "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "cores": nproc, "kind": "port",
                              "sample": sample},
             "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def random_sample(n: int, k: int, seed: int) -> list[int]:
+    """k distinct ids of range(n), seeded (pure Python: the reference arm imports no NumPy here)."""
+    import random
+    return random.Random(seed * 7 + 3).sample(range(n), min(k, n))
 
 
 def main():

@@ -341,6 +341,23 @@ int nosa_ktime_read(NosaCtx* ctx, double* span_us /* [layers] */);
  * Reads (if cycles != NULL) then resets (on = 1) or disables (on = 0).  Synchronises. */
 int nosa_select_profile(NosaCtx* ctx, int on, double* cycles /* [16] */);
 
+/* ---- seeded synthetic inputs (bench / parity tests; not part of the decode step) --------- */
+
+/* Counter-based N(0,1) draws (Irwin-Hall sum of four 16-bit hash fields, times `scale` in fp32),
+ * a pure function of (seed, kind, layer, global sequence, head, position, dim): any shard or
+ * subset of the batch draws the same bits as paper_2510_13602_b200/workload.py's NumPy twin.
+ * kind: 0 prefix K, 1 prefix V, 2 initial query state, 3 query innovations, 4 k_new, 5 v_new.
+ * out: device [n_layers][n_seq][heads][n_pos][d] in dtype (bf16: round to nearest even). */
+int nosa_synth_normal(uint64_t seed, int kind, int layer0, int n_layers, int seq0, int n_seq, int heads,
+                      long long pos0, long long n_pos, int d, float scale, int dtype, void* out, void* stream);
+
+/* One AR(1) query step over state [n_layers][n_seq][heads][d] (float32, device, in place):
+ * q_out = round(state); state = fl32(fl32(rho * state) + fl32(sigma * eps)), eps = the kind-3
+ * draws at position `step` times `scale`. */
+int nosa_synth_ar1_step(uint64_t seed, int layer0, int n_layers, int seq0, int n_seq, int heads, long long step,
+                        int d, float rho, float sigma, float scale, float* state, int dtype, void* q_out,
+                        void* stream);
+
 /* kernel launches issued by this library since context creation (bench evidence) */
 int64_t nosa_launch_count(const NosaCtx* ctx);
 

@@ -109,6 +109,10 @@ SIGNATURES = {
     "nosa_ktime_enable": (_I, [_P, _I]),
     "nosa_select_profile": (_I, [_P, _I, _F64P]),
     "nosa_ktime_read": (_I, [_P, _F64P]),
+    "nosa_synth_normal": (_I, [ctypes.c_uint64, _I, _I, _I, _I, _I, _I, ctypes.c_longlong, ctypes.c_longlong, _I,
+                               ctypes.c_float, _I, _P, _P]),
+    "nosa_synth_ar1_step": (_I, [ctypes.c_uint64, _I, _I, _I, _I, _I, ctypes.c_longlong, _I, ctypes.c_float,
+                                 ctypes.c_float, ctypes.c_float, _P, _I, _P, _P]),
     "nosa_timing_trace": (_I, [_P, _I, _I32P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float), _I32P]),
 }
 

@@ -15,6 +15,8 @@ Fixtures
                        (attention.py:104-118); selections, outputs, pool scores, plus the
                        per-sequence residency trace of the required sets (offload_sim.py:279-299)
   engine_cfg1.npz      the same at BASELINE config 1 (8q/2kv, d_head 128, 8K, block 64, top-k 16)
+  engine_1b_32k*.npz   the same at the 1B shape, 32K context, 25% fast tier (128 slots), on the
+                       counter-based inputs the bench draws (`make_golden.py headline`)
 """
 
 from __future__ import annotations
@@ -130,7 +132,10 @@ def manager_trace():
     print("manager_trace: hit rate", st.hit_rate)
 
 
-def engine_run(name, cfg_kw, batch, t0, steps, fast_slots, seed, rho, selector="nosa", out_dtype=np.float64):
+def engine_run(name, cfg_kw, batch, t0, steps, fast_slots, seed, rho, selector="nosa", out_dtype=np.float64,
+               synth=False):
+    """synth=True: the counter-based inputs (workload.synth_prefix_kv / SynthQueryStream) that the
+    GPU bench and the headline-config parity tests draw, for sequences 0..batch-1 of layer 0."""
     cfg = AttentionConfig(**cfg_kw)
     Hq, Hk, D = cfg.n_head, cfg.n_kv_head, cfg.d_head
     d = (Hq + 2 * Hk) * D
@@ -138,8 +143,12 @@ def engine_run(name, cfg_kw, batch, t0, steps, fast_slots, seed, rho, selector="
     w1, w2 = workload.eviction_head(Hq, D, seed)
     weights = ModelWeights(w_q=eye[:, :Hq * D], w_k=eye[:, Hq * D:(Hq + Hk) * D], w_v=eye[:, (Hq + Hk) * D:],
                            eviction=EvictionHead("ed-dma", w1, w2), seed=0)
-    K, V = workload.prefix_kv(seed, batch, Hk, t0, D)
-    stream = workload.QueryStream(seed, 1, batch, Hq, Hk, D, rho)
+    if synth:
+        K, V = workload.synth_prefix_kv(seed, 0, range(batch), Hk, t0, D)
+        stream = workload.SynthQueryStream(seed, [0], range(batch), Hq, Hk, D, rho)
+    else:
+        K, V = workload.prefix_kv(seed, batch, Hk, t0, D)
+        stream = workload.QueryStream(seed, 1, batch, Hq, Hk, D, rho)
     inputs = [stream.next() for _ in range(steps)]
     engines = []
     for b in range(batch):
@@ -200,7 +209,7 @@ def engine_run(name, cfg_kw, batch, t0, steps, fast_slots, seed, rho, selector="
     np.savez_compressed(OUT / f"{name}.npz", cfg=np.array([cfg_kw[k] for k in ("n", "d", "n_head", "n_kv_head",
                         "d_head", "n_b", "n_s", "n_w", "k", "k_q", "k_e")] + [1 if cfg.accounting == "exclusive" else 0]),
                         batch=batch, t0=t0, steps=steps, fast_slots=fast_slots, seed=seed, rho=rho,
-                        selector=selector, sel_q=sel_q, sel_e=sel_e, outputs=outs, s_q=s_q_all, s_e_pool=s_e_pool,
+                        selector=selector, synth=int(synth), sel_q=sel_q, sel_e=sel_e, outputs=outs, s_q=s_q_all, s_e_pool=s_e_pool,
                         fetch=fetch, evict=evict, hits=hits, pool=np.array([lo, hi]))
     print(name, "done")
 
@@ -265,7 +274,21 @@ def shared_pool_simulation():
     print("shared_pool_sim: nosa hit", out["nosa_report"][0], "infllmv2 hit", out["infllmv2_report"][0])
 
 
+def headline():
+    """The 1B attention shape at 32K context with 25% of the blocks in the fast tier (BASELINE config
+    3 / 4 per sequence), on the counter-based inputs: long enough for the cache to fill and evict."""
+    one_b = dict(n=65536, d=2560, n_head=16, n_kv_head=2, d_head=128, n_b=64, n_s=64, n_w=1024, k=4096, k_q=1024,
+                 k_e=3072)
+    engine_run("engine_1b_32k", one_b, batch=1, t0=32768, steps=40, fast_slots=128, seed=21, rho=0.95,
+               out_dtype=np.float32, synth=True)
+    engine_run("engine_1b_32k_infllmv2_rho0", one_b, batch=1, t0=32768, steps=12, fast_slots=128, seed=22, rho=0.0,
+               selector="infllmv2", out_dtype=np.float32, synth=True)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "headline":
+        headline()
+        return
     selection_kats()
     manager_trace()
     shared_pool_simulation()
