@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
       // the first work item is static (item = CTA index), later ones are claimed dynamically
       int c = blockIdx.x;
       if (qs > 0) {
-        if (lane == 0) c = gridDim.x + atomicAdd(dv.cnt + 2 * layer + 1, 1);
+        if (lane == 0) c = gridDim.x + atomicAdd(dv.cnt + kCntStride * layer + 1, 1);
         c = __shfl_sync(0xffffffffu, c, 0);
       }
       const int slot = qs % T::NQ;
@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(32)
     if (ld_done) return;
     if (ld_i >= ld_end) {
       int c = 0;
-      if (lane == 0) c = atomicAdd(dv.cnt + 2 * layer + 1, 1);
+      if (lane == 0) c = atomicAdd(dv.cnt + kCntStride * layer + 1, 1);
       c = __shfl_sync(0xffffffffu, c, 0);
       if (c >= total) { ld_done = true; return; }
       ld_bh = find_bh(cbase, BH, c);

@@ -92,6 +92,11 @@ struct NosaCtx {
   std::vector<void*> b_dst, b_src;
   std::vector<size_t> b_size;
   long long batch_fallbacks = 0;
+  // exported copy lists (Dev::x_*): mapped pinned host arrays the planner fills on the device
+  void** h_xsrc = nullptr;
+  void** h_xdst = nullptr;
+  int* h_xcnt = nullptr;
+  std::vector<size_t> x_sizes;
   // host-buffer step (nosa_decode_step_host): device staging of the step's inputs and outputs,
   // per-layer input-arrival / output-ready events, and the device->host stream
   cudaStream_t d2h_stream = nullptr, in_stream = nullptr;
@@ -265,6 +270,8 @@ static void release(NosaCtx* ctx) {
     if (s) cudaStreamDestroy(s);
   if (ctx->h_list) cudaFreeHost(ctx->h_list);
   if (ctx->h_cnt) cudaFreeHost(ctx->h_cnt);
+  for (void* p : {(void*)ctx->h_xsrc, (void*)ctx->h_xdst, (void*)ctx->h_xcnt})
+    if (p) cudaFreeHost(p);
   for (auto* pool : {&ctx->timing, &ctx->cap_events})
     for (auto& t : *pool) {
       cudaEventDestroy(t.a);
@@ -409,7 +416,7 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   ALLOC(dv.plan_fetch, LBH * dv.C);
   ALLOC(dv.plan_evict, LBH * dv.C);
   ALLOC(dv.plan_n, LBH * 3);
-  ALLOC(dv.cnt, (size_t)dv.L * 2);
+  ALLOC(dv.cnt, (size_t)dv.L * nosa::kCntStride);
   ALLOC(dv.miss_list, (size_t)dv.L * BH * dv.C);
   ALLOC(dv.part_o, (size_t)dv.nbuf * BH * dv.max_chunks * dv.G * dv.D);
   ALLOC(dv.part_ml, (size_t)dv.nbuf * BH * dv.max_chunks * dv.G);
@@ -659,9 +666,14 @@ extern "C" int nosa_start_run(NosaCtx* ctx, int seq_begin, int seq_count, void* 
 
 // K1+K2 for one layer: fused per-(sequence, head) select+plan, or select then the ordered
 // shared-pool planner (NOSA_RESIDENCY_SHARED)
-static cudaError_t plan_layer(NosaCtx* ctx, int layer, const void* q, int selector, cudaStream_t st) {
+static cudaError_t plan_layer(NosaCtx* ctx, int layer, const void* q, int selector, cudaStream_t st,
+                              bool export_misses = false) {
   const Dev& dv = ctx->dv;
-  if (!dv.shared) return nosa::launch_select_plan(dv, layer, q, selector, 1, nullptr, nullptr, st);
+  if (!dv.shared) {
+    Dev dx = dv;
+    dx.x_on = export_misses;
+    return nosa::launch_select_plan(dx, layer, q, selector, 1, nullptr, nullptr, st);
+  }
   cudaError_t e = nosa::launch_select_plan(dv, layer, q, selector, 0, nullptr, nullptr, st);
   if (e != cudaSuccess) return e;
   return nosa::launch_plan_shared(dv, layer, nullptr, nullptr, st);
@@ -672,7 +684,7 @@ extern "C" int nosa_select_plan(NosaCtx* ctx, int layer, const void* q, int sele
   if (rc) return rc;
   if (selector != 0 && selector != 1) return fail(ctx, NOSA_ERR_VALUE, "selector must be nosa or infllmv2");
   cudaSetDevice(ctx->device);
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->dv.cnt + 2 * layer, 0, 2 * sizeof(int), S(stream)));
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->dv.cnt + nosa::kCntStride * layer, 0, nosa::kCntStride * sizeof(int), S(stream)));
   CUDA_TRY(ctx, plan_layer(ctx, layer, q, selector, S(stream)));
   ctx->launches += ctx->dv.shared ? 2 : 1;
   return NOSA_OK;
@@ -693,7 +705,7 @@ extern "C" int nosa_cache_plan(NosaCtx* ctx, int layer, const int32_t* req, cons
   if (rc) return rc;
   if (!req || !n_req) return fail(ctx, NOSA_ERR_VALUE, "required sets are NULL");
   cudaSetDevice(ctx->device);
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->dv.cnt + 2 * layer, 0, 2 * sizeof(int), S(stream)));
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->dv.cnt + nosa::kCntStride * layer, 0, nosa::kCntStride * sizeof(int), S(stream)));
   if (ctx->dv.shared)
     CUDA_TRY(ctx, nosa::launch_plan_shared(ctx->dv, layer, req, n_req, S(stream)));
   else
@@ -715,7 +727,7 @@ static int gather_memcpy(NosaCtx* ctx, int layer, cudaEvent_t plan_done, cudaStr
     CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->meta_stream, cudaStreamNonBlocking));
   }
   CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->meta_stream, plan_done, 0));
-  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_cnt, dv.cnt + 2 * layer, sizeof(int), cudaMemcpyDeviceToHost, ctx->meta_stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_cnt, dv.cnt + nosa::kCntStride * layer, sizeof(int), cudaMemcpyDeviceToHost, ctx->meta_stream));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->meta_stream));
   const int n = ctx->h_cnt[0];
   if (n == 0) return NOSA_OK;
@@ -756,6 +768,63 @@ static int gather_memcpy(NosaCtx* ctx, int layer, cudaEvent_t plan_done, cudaStr
     ctx->batch_fallbacks += 1;
     for (int i = 0; i < nc; ++i)
       CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b_dst[i], ctx->b_src[i], ctx->b_size[i], cudaMemcpyDefault, copy_st));
+  }
+  return NOSA_OK;
+}
+
+// The mapped pinned host arrays the planner writes each layer's copy list into (Dev::x_*).
+static int ensure_export(NosaCtx* ctx) {
+  if (ctx->h_xsrc) return NOSA_OK;
+  Dev& dv = ctx->dv;
+  const size_t cap = (size_t)dv.B * dv.H * dv.C;
+  CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_xsrc), dv.L * cap * sizeof(void*), cudaHostAllocMapped));
+  CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_xdst), dv.L * cap * sizeof(void*), cudaHostAllocMapped));
+  CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_xcnt), 2 * dv.L * sizeof(int), cudaHostAllocMapped));
+  CUDA_TRY(ctx, cudaHostGetDevicePointer(reinterpret_cast<void**>(&dv.x_src), ctx->h_xsrc, 0));
+  CUDA_TRY(ctx, cudaHostGetDevicePointer(reinterpret_cast<void**>(&dv.x_dst), ctx->h_xdst, 0));
+  CUDA_TRY(ctx, cudaHostGetDevicePointer(reinterpret_cast<void**>(&dv.x_cnt), ctx->h_xcnt, 0));
+  dv.x_src_base = ctx->host_mirror;  // the address the copy engine reads (host or peer HBM)
+  ctx->x_sizes.assign(cap, (size_t)dv.bpb);
+  return NOSA_OK;
+}
+
+// Copy-engine mover inside a step: the layer's planner already wrote the copy list and its
+// counts into mapped host memory (select_plan_kernel with Dev::x_on), so once the plan has
+// executed (an event query: no device round trip, no copy) the host submits the whole list as
+// one cudaMemcpyBatchAsync.  Blocks born by the last append are rebuilt on the device.
+static int gather_exported(NosaCtx* ctx, int layer, cudaStream_t copy_st, bool timed) {
+  const Dev& dv = ctx->dv;
+  cudaError_t e;
+  while ((e = cudaEventQuery(ctx->ev_plan[layer])) == cudaErrorNotReady) {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+  CUDA_TRY(ctx, e);
+  const volatile int* xc = ctx->h_xcnt;
+  const int n = xc[2 * layer], n_born = xc[2 * layer + 1];
+  TimeScope ts(ctx, copy_st, 1, timed);
+  if (n_born) {
+    CUDA_TRY(ctx, nosa::launch_born(dv, layer, copy_st, std::min(n_born, ctx->num_sms)));
+    ctx->memcpy_born_launches += 1;
+  }
+  if (n == 0) return NOSA_OK;
+  const size_t cap = (size_t)dv.B * dv.H * dv.C;
+  void** dst = ctx->h_xdst + layer * cap;
+  void** src = ctx->h_xsrc + layer * cap;
+  cudaMemcpyAttributes attr{};
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  attr.srcLocHint.type = ctx->mirror_device >= 0 ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
+  attr.srcLocHint.id = ctx->mirror_device >= 0 ? ctx->mirror_device : 0;
+  attr.dstLocHint.type = cudaMemLocationTypeDevice;
+  attr.dstLocHint.id = ctx->device;
+  size_t idx0 = 0, fail_idx = 0;
+  e = cudaMemcpyBatchAsync(dst, src, ctx->x_sizes.data(), n, &attr, &idx0, 1, &fail_idx, copy_st);
+  if (e != cudaSuccess) {  // driver without batched copies: one call per block
+    cudaGetLastError();
+    ctx->batch_fallbacks += 1;
+    for (int i = 0; i < n; ++i)
+      CUDA_TRY(ctx, cudaMemcpyAsync(dst[i], src[i], (size_t)dv.bpb, cudaMemcpyDefault, copy_st));
   }
   return NOSA_OK;
 }
@@ -951,12 +1020,19 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   } else {
     for (int l = 0; l < dv.L; ++l) groups.push_back({l, 1});
   }
+  // copy-engine mover: the planner exports each layer's copy list to mapped host memory
+  const bool export_misses = io->gather_mode == NOSA_GATHER_MEMCPY && !dv.shared && !dv.born_local &&
+                             !ctx->capturing && !getenv("NOSA_MEMCPY_READBACK");
+  if (export_misses)
+    if (int rc = ensure_export(ctx)) return rc;
+  Dev dx = dv;  // (ensure_export filled the x_* pointers of ctx->dv)
+  dx.x_on = export_misses;
   auto select = [&](int l) -> int {
     if (hio) CUDA_TRY(ctx, cudaStreamWaitEvent(ss, ctx->ev_in[l], 0));
-    CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt + 2 * l, 0, 2 * sizeof(int), ss));
+    CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt + nosa::kCntStride * l, 0, nosa::kCntStride * sizeof(int), ss));
     {
       TimeScope ts(ctx, ss, 0, timed);
-      CUDA_TRY(ctx, plan_layer(ctx, l, q + l * qstride, io->selector, ss));
+      CUDA_TRY(ctx, plan_layer(ctx, l, q + l * qstride, io->selector, ss, export_misses));
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[l], ss));
     return NOSA_OK;
@@ -966,10 +1042,10 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   // at once while the later layers' selections fill the whole GPU in a few launches.
   auto select_group = [&](int l0, int n) -> int {
     if (hio) CUDA_TRY(ctx, cudaStreamWaitEvent(ss, ctx->ev_in[l0 + n - 1], 0));
-    CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt + 2 * l0, 0, 2 * n * sizeof(int), ss));
+    CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt + nosa::kCntStride * l0, 0, nosa::kCntStride * n * sizeof(int), ss));
     {
       TimeScope ts(ctx, ss, 0, timed);
-      CUDA_TRY(ctx, nosa::launch_select_plan(dv, l0, q + l0 * qstride, io->selector, 1, nullptr, nullptr, ss, n));
+      CUDA_TRY(ctx, nosa::launch_select_plan(dx, l0, q + l0 * qstride, io->selector, 1, nullptr, nullptr, ss, n));
     }
     for (int l = l0; l < l0 + n; ++l) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[l], ss));
     return NOSA_OK;
@@ -1108,7 +1184,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
     if (!dv.born_local) {  // (all resident: the planner placed the newborn blocks, nothing to move)
       CUDA_TRY(ctx, cudaStreamWaitEvent(cp, ctx->ev_plan[l], 0));
       if (io->gather_mode == NOSA_GATHER_MEMCPY) {
-        const int rc = gather_memcpy(ctx, l, ctx->ev_plan[l], cp, timed);
+        const int rc = export_misses ? gather_exported(ctx, l, cp, timed) : gather_memcpy(ctx, l, ctx->ev_plan[l], cp, timed);
         if (rc) return rc;
       } else if (batch_end) {  // device movers: one launch for the attention batch's layers
         TimeScope ts(ctx, cp, 1, timed);

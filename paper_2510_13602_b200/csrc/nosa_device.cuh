@@ -21,6 +21,7 @@
 namespace nosa {
 
 constexpr int kChunk = 8;  // max KV blocks per attention work item (split-K granularity)
+constexpr int kCntStride = 4;  // ints per layer in Dev::cnt
 
 struct Dev {
   // ---- shapes --------------------------------------------------------------------------
@@ -71,7 +72,16 @@ struct Dev {
   int* plan_fetch;               // [lbh][C]
   int* plan_evict;               // [lbh][C]
   int* plan_n;                   // [lbh][3] n_fetch, n_evict, n_hit
-  int* cnt;                      // [L][2]: miss count, attention work counter
+  int* cnt;                      // [L][kCntStride]: miss count, attention work counter, exported
+                                 // (copy-engine) misses, plan CTAs done
+  // copy-engine miss export (NOSA_GATHER_MEMCPY inside a step): the planner writes each layer's
+  // copy list straight into mapped pinned host memory, so the host submits the batch with no
+  // device round trip (nosa_ctx.cu gather_exported)
+  int x_on;                      // set per launch: export this launch's misses
+  void** x_src;                  // [L][B*H*C] device alias of the host array of source addresses
+  void** x_dst;                  // [L][B*H*C] destination slot addresses
+  int* x_cnt;                    // [L][2] device alias of host ints: exported misses, born blocks
+  const char* x_src_base;        // slow-tier base address as the copy engine sees it
   int4* miss_list;               // [L][B*H*C]  {lbh, blk, slot, 0}
   float* part_o;                 // [nbuf][B*H][max_chunks][G][D]  split-K records (layer % nbuf)
   float2* part_ml;               // [nbuf][B*H][max_chunks][G]     (m, l) of each record

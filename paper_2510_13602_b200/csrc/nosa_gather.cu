@@ -33,7 +33,7 @@ template <int NBLK, bool L2HINT>
 __global__ void __launch_bounds__(256) gather_kernel(Dev dv, int layer0) {
   constexpr int PER = 8;  // 16-byte vectors per thread per 32 KiB block at 256 threads
   const int layer = layer0 + blockIdx.y;  // grid (CTAs, layers of an attention batch)
-  const int n = *reinterpret_cast<volatile int*>(dv.cnt + 2 * layer);
+  const int n = *reinterpret_cast<volatile int*>(dv.cnt + kCntStride * layer);
   const int4* list = dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C;
   const int vecs = (int)(dv.bpb / 16);
   for (int e0 = blockIdx.x * NBLK; e0 < n; e0 += gridDim.x * NBLK) {
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(32) gather_tma_kernel(Dev dv, int layer0) {
   extern __shared__ __align__(128) char smem_raw[];
   const int layer = layer0 + blockIdx.y;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kTmaStages * dv.bpb);
-  const int n = *reinterpret_cast<volatile int*>(dv.cnt + 2 * layer);
+  const int n = *reinterpret_cast<volatile int*>(dv.cnt + kCntStride * layer);
   const int4* list = dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C;
   const int lane = threadIdx.x;
   const int m = n > (int)blockIdx.x ? (n - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;  // items of this CTA
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(32) gather_tma_kernel(Dev dv, int layer0) {
 // Blocks born by the previous step's append, for the copy-engine mover: the memcpy batch skips
 // them (their only valid row is in the device stash), this kernel writes them into their slots.
 __global__ void __launch_bounds__(256) born_kernel(Dev dv, int layer) {
-  const int n = dv.cnt[2 * layer];
+  const int n = dv.cnt[kCntStride * layer];
   const int4* list = dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C;
   const int vecs = (int)(dv.bpb / 16);
   for (int e = blockIdx.x; e < n; e += gridDim.x) {

@@ -622,7 +622,7 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
     top -= nf;
     // enqueue the misses for the gather (K3)
     int base = 0;
-    if (lane == 0 && nf > 0) base = atomicAdd(dv.cnt + 2 * layer, nf);
+    if (lane == 0 && nf > 0) base = atomicAdd(dv.cnt + kCntStride * layer, nf);
     base = __shfl_sync(0xffffffffu, base, 0);
     int4* ml = dv.miss_list + (size_t)layer * dv.B * dv.H * C;
     // a block whose only token was appended at the previous step of this run is rebuilt from
@@ -632,6 +632,22 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
       const int blk = sm.fetch[f];
       const int born = (blk * dv.n_b == t_now - 1) && (t_now - 1 >= t0);
       ml[base + f] = make_int4(lbh, blk, sm.reqslot[sm.fpos[f]], born);
+    }
+    if (dv.x_on) {
+      // copy list for the host: every miss but a block born by the last append (rebuilt on the
+      // device; it is the newest block, so always the last fetch); the layer's last CTA then
+      // publishes the counts (select_plan_kernel)
+      const int last_born = nf > 0 && sm.fetch[nf - 1] * dv.n_b == t_now - 1 && t_now - 1 >= t0;
+      const int nx = nf - last_born;
+      int xb = 0;
+      if (lane == 0 && nx > 0) xb = atomicAdd(dv.cnt + kCntStride * layer + 2, nx);
+      xb = __shfl_sync(0xffffffffu, xb, 0);
+      const size_t cap = (size_t)dv.B * dv.H * C;
+      for (int f = lane; f < nx; f += 32) {
+        const int blk = sm.fetch[f];
+        dv.x_src[layer * cap + xb + f] = const_cast<char*>(dv.x_src_base) + ((size_t)lbh * dv.NB + blk) * dv.bpb;
+        dv.x_dst[layer * cap + xb + f] = dv.pool + ((size_t)lbh * C + sm.reqslot[sm.fpos[f]]) * dv.bpb;
+      }
     }
     if (lane == 0) {
       dv.ftop[lbh] = top;
@@ -708,6 +724,18 @@ __global__ void __launch_bounds__(256, 4)  // 4 CTAs per SM: one CTA's scan over
   sel_mark(sm, 7);
   plan_phase(dv, layer, b, h, sm);
   __syncthreads();
+  if (dv.x_on && threadIdx.x == 0) {
+    // the layer's last CTA publishes the exported miss counts to the host (every CTA gets here,
+    // CapacityExceeded included); kernel completion makes them visible to the host
+    __threadfence();
+    if (atomicAdd(dv.cnt + kCntStride * layer + 3, 1) == (int)gridDim.x - 1) {
+      __threadfence();
+      const int total = atomicAdd(dv.cnt + kCntStride * layer, 0);
+      const int xn = atomicAdd(dv.cnt + kCntStride * layer + 2, 0);
+      reinterpret_cast<volatile int*>(dv.x_cnt)[2 * layer] = xn;
+      reinterpret_cast<volatile int*>(dv.x_cnt)[2 * layer + 1] = total - xn;
+    }
+  }
   sel_mark(sm, 11);
   if (sm.marks && threadIdx.x == 0) {  // cycles per phase, summed over CTAs; [15] counts CTAs
     long long prev = marks[0];
@@ -976,7 +1004,7 @@ __global__ void __launch_bounds__(kSharedThreads)
       top += nev;
       const int t = dv.t[lbh], t0 = dv.t0[lbh];
       int n_new = 0;
-      int base = nf ? atomicAdd(dv.cnt + 2 * layer, nf) : 0;
+      int base = nf ? atomicAdd(dv.cnt + kCntStride * layer, nf) : 0;
       int4* ml = dv.miss_list + (size_t)layer * B * H * C;
       for (int f = 0; f < nf; ++f) {
         const int s = dv.fstack[shared_idx(dv, layer, h, top - 1 - f)];

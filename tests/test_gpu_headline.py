@@ -175,7 +175,7 @@ def test_gpu_generator_matches_numpy():
         assert torch.equal(g.cpu(), torch.from_numpy(c)), kind
     gb = synth.normal(9, 0, 0, 1, 0, 3, 2, 0, 100, 64, DEV)
     cb = workload.bf16_round(workload.synth_normal(9, 0, 0, range(3), 2, 0, 100, 64))
-    assert torch.equal(gb.float().cpu(), torch.from_numpy(cb))
+    assert torch.equal(gb[0].float().cpu(), torch.from_numpy(cb))
     gs = synth.GpuQueryStream(4, 3, 10, 4, 16, 2, 128, 0.5, DEV, torch.float32)
     cs = workload.SynthQueryStream(4, range(3), range(10, 14), 16, 2, 128, 0.5, bf16=False)
     for _ in range(5):
