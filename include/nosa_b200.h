@@ -341,6 +341,48 @@ int nosa_ktime_read(NosaCtx* ctx, double* span_us /* [layers] */);
  * Reads (if cycles != NULL) then resets (on = 1) or disables (on = 0).  Synchronises. */
 int nosa_select_profile(NosaCtx* ctx, int on, double* cycles /* [16] */);
 
+/* ---- TieredBlockManager (kv_manager.py:130-363): the reference's exclusive two-tier block
+ *      manager with its tables, free lists, recency clock and payload in device memory -------- */
+
+/* One manager: per head, `fast_blocks` FAST slots (PhysicalLayout(FAST, ...)) and `slow_blocks` SLOW
+ * slots (PhysicalLayout(SLOW, ...)), LIFO free lists initialised [N-1 .. 0] (kv_manager.py:147-150).
+ * Keys are dense per-head ids in [0, fast_blocks + slow_blocks) chosen by the caller (the Python
+ * binding maps the reference's (batch, head, block) tuples onto them).  store_payload: FAST payload
+ * in HBM, SLOW payload in pinned host memory, (num_blocks, heads, 2, n_b, d_head) per tier. */
+typedef struct NosaMgr NosaMgr;
+int nosa_mgr_create(int heads, int fast_blocks, int slow_blocks, int n_b, int d_head, int element_width,
+                    int store_payload, int device, NosaMgr** out);
+void nosa_mgr_destroy(NosaMgr* mgr);
+const char* nosa_mgr_last_error(const NosaMgr* mgr);
+/* allocate (kv_manager.py:171-183): tier 0 FAST / 1 SLOW; NOSA_ERR_OUT_OF_BLOCKS, NOSA_ERR_VALUE
+ * (DuplicateKey) */
+int nosa_mgr_allocate(NosaMgr* mgr, int tier, int head, int id, int batch, int block, int32_t* slot);
+/* free_block (kv_manager.py:185-194): NOSA_ERR_UNKNOWN_KEY */
+int nosa_mgr_free(NosaMgr* mgr, int head, int id);
+/* plan_transfers (kv_manager.py:205-259) for (batch, head): ids of the required keys in ascending
+ * block order (-1 = a key mapped in no tier).  Ticks the clock and stamps last_required like the
+ * reference; changes no table.  Outputs fetch ids (required order) and evict ids
+ * (least-recently-required order by (last_required, batch, block)).  NOSA_ERR_CAPACITY,
+ * NOSA_ERR_UNKNOWN_KEY. */
+int nosa_mgr_plan(NosaMgr* mgr, int head, int batch, const int32_t* ids, int n, int32_t* fetch, int32_t* n_fetch,
+                  int32_t* evict, int32_t* n_evict, int32_t* hits);
+/* apply_transfers' moves (kv_manager.py:276-298): evictions FAST -> SLOW then fetches SLOW -> FAST,
+ * one _move at a time; copy_payload: the default mover's payload copies, on the device.
+ * moves (optional): [n_evict + n_fetch][2] source and destination slot of each move (-1, -1 =
+ * no-op move). */
+int nosa_mgr_apply(NosaMgr* mgr, int head, const int32_t* evict, int n_evict, const int32_t* fetch, int n_fetch,
+                   int copy_payload, int32_t* moves);
+/* lookup (kv_manager.py:185-190): tier (-1 unmapped, 0 FAST, 1 SLOW) and slot of one key */
+int nosa_mgr_lookup(NosaMgr* mgr, int head, int id, int32_t* tier, int32_t* slot);
+/* tier / slot of every id of a head ([fast_blocks + slow_blocks] each): dump_table_csv */
+int nosa_mgr_tables(NosaMgr* mgr, int head, int8_t* tier, int32_t* slot);
+/* the per-head LIFO free lists (bottom to top: the last entry is popped next), as kv_manager.free */
+int nosa_mgr_free_lists(NosaMgr* mgr, int head, int32_t* fast, int32_t* n_fast, int32_t* slow, int32_t* n_slow);
+/* audit (kv_manager.py:341-363): *bad = 0 when every (tier, head) slot partition holds */
+int nosa_mgr_audit(NosaMgr* mgr, int32_t* bad);
+/* write_block / read_block (kv_manager.py:305-321): one block's payload, host [2][n_b][d_head] */
+int nosa_mgr_block(NosaMgr* mgr, int head, int id, void* data, int write);
+
 /* ---- seeded synthetic inputs (bench / parity tests; not part of the decode step) --------- */
 
 /* Counter-based N(0,1) draws (Irwin-Hall sum of four 16-bit hash fields, times `scale` in fp32),

@@ -12,7 +12,8 @@ from .config import AttentionConfig, cfg1_config, one_b_config
 from .engine import NosaEngine, ResidencyStats, StepOutput, TransferPlanView
 from .errors import (CapacityExceeded, DuplicateKey, LayoutMismatch, ManagerError, OutOfBlocks, StalePlan,
                      UnknownKey)
-from .kv_manager import GpuTieredBlockManager, TransferPlan
+from .kv_manager import (FAST, SLOW, GpuTieredBlockManager, PhysicalLayout, TieredBlockManager, TransferPlan,
+                         least_recently_required)
 from .selection import BlockGeometry, SelectionResult, build_token_mask, infllmv2_select, nosa_select
 
 __all__ = [

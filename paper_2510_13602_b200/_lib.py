@@ -109,6 +109,18 @@ SIGNATURES = {
     "nosa_ktime_enable": (_I, [_P, _I]),
     "nosa_select_profile": (_I, [_P, _I, _F64P]),
     "nosa_ktime_read": (_I, [_P, _F64P]),
+    "nosa_mgr_create": (_I, [_I, _I, _I, _I, _I, _I, _I, _I, ctypes.POINTER(_P)]),
+    "nosa_mgr_destroy": (None, [_P]),
+    "nosa_mgr_last_error": (ctypes.c_char_p, [_P]),
+    "nosa_mgr_allocate": (_I, [_P, _I, _I, _I, _I, _I, _I32P]),
+    "nosa_mgr_free": (_I, [_P, _I, _I]),
+    "nosa_mgr_plan": (_I, [_P, _I, _I, _I32P, _I, _I32P, _I32P, _I32P, _I32P, _I32P]),
+    "nosa_mgr_apply": (_I, [_P, _I, _I32P, _I, _I32P, _I, _I, _I32P]),
+    "nosa_mgr_lookup": (_I, [_P, _I, _I, _I32P, _I32P]),
+    "nosa_mgr_tables": (_I, [_P, _I, _P, _I32P]),
+    "nosa_mgr_audit": (_I, [_P, _I32P]),
+    "nosa_mgr_free_lists": (_I, [_P, _I, _I32P, _I32P, _I32P, _I32P]),
+    "nosa_mgr_block": (_I, [_P, _I, _I, _P, _I]),
     "nosa_synth_normal": (_I, [ctypes.c_uint64, _I, _I, _I, _I, _I, _I, ctypes.c_longlong, ctypes.c_longlong, _I,
                                ctypes.c_float, _I, _P, _P]),
     "nosa_synth_ar1_step": (_I, [ctypes.c_uint64, _I, _I, _I, _I, _I, ctypes.c_longlong, _I, ctypes.c_float,
@@ -133,11 +145,11 @@ def _load():
 lib = _load()
 
 
-def check(rc: int, ctx=None) -> None:
+def check(rc: int, ctx=None, mgr=None) -> None:
     """Raise the reference exception type matching a status code."""
     if rc == NOSA_OK:
         return
-    msg = lib.nosa_last_error(ctx)
+    msg = lib.nosa_mgr_last_error(mgr) if mgr is not None else lib.nosa_last_error(ctx)
     msg = msg.decode() if msg else f"status {rc}"
     if rc == NOSA_ERR_VALUE:
         raise ValueError(msg)

@@ -186,3 +186,24 @@ def test_projection_rejects_untileable_shapes_without_a_gpu():
     assert b"N % 128" in lib.nosa_last_error(None)
     assert lib.nosa_project_qkv(p, 4, 2048, p, 2560, 2048, 256, p, p, p, 9, None) == _lib.NOSA_ERR_VALUE
     assert lib.nosa_project_qkv(None, 4, 2048, p, 2560, 2048, 256, p, p, p, 4, None) == _lib.NOSA_ERR_VALUE
+
+
+def test_tiered_block_manager_constructor_contract():
+    """The drop-in TieredBlockManager validates like the reference before touching the device
+    (kv_manager.py:59-81, 138-146): layout checks, tier order, the only supported policy."""
+    from paper_2510_13602_b200 import FAST, SLOW, LayoutMismatch, PhysicalLayout, TieredBlockManager
+    from paper_2510_13602_b200.kv_manager import least_recently_required
+    with pytest.raises(ValueError):
+        PhysicalLayout("warm", 4, 1, 4, 8)
+    with pytest.raises(ValueError):
+        PhysicalLayout(FAST, 4, 1, 4, 8, element_width=3)
+    assert PhysicalLayout(FAST, 4, 2, 4, 8).bytes_per_block == 2 * 4 * 8 * 2
+    fast, slow = PhysicalLayout(FAST, 4, 2, 4, 8), PhysicalLayout(SLOW, 8, 2, 4, 8)
+    with pytest.raises(LayoutMismatch):
+        TieredBlockManager(slow, fast)
+    with pytest.raises(LayoutMismatch, match="disagree"):
+        TieredBlockManager(fast, PhysicalLayout(SLOW, 8, 3, 4, 8))
+    with pytest.raises(ValueError, match="policy"):
+        TieredBlockManager(fast, slow, eviction_policy=lambda c, last: c)
+    keys = [(1, 0, 5), (0, 0, 9), (0, 0, 2)]
+    assert least_recently_required(keys, {(0, 0, 9): 3}) == [(0, 0, 2), (1, 0, 5), (0, 0, 9)]
