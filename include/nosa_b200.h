@@ -40,6 +40,7 @@ extern "C" {
 #define NOSA_FLAG_CAPACITY 1u
 #define NOSA_FLAG_EMPTY_SUPPORT 2u /* softmax over empty support (numerics.py:50-52)       */
 #define NOSA_FLAG_NOT_RESIDENT 4u  /* all-resident run met a miss that is not a newborn block      */
+#define NOSA_FLAG_FULL 8u          /* append past the head capacity (HeadState, decode.py:65-71); refused */
 
 /* selectors (decode.py:28 SELECTORS) */
 #define NOSA_SELECTOR_NOSA 0     /* selection.nosa_select      (selection.py:130-160)     */

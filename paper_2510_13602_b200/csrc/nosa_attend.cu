@@ -181,6 +181,10 @@ __device__ void finalize_bh(const Dev& dv, int layer, int bh, int nc, const T* _
   }
 
   // ---- (2) append the new token (decode.py:187-189, HeadState.append decode.py:65-71)
+  if (t >= dv.NB * n_b) {  // head cache full (HeadState capacity): refuse the append, flag it
+    if (tid == 0) atomicOr(dv.err, 8u);  // NOSA_FLAG_FULL
+    return;
+  }
   const int blk = t / n_b, r = t - blk * n_b;
   const int plane = n_b * D * elem;
   char* hblk = dv.host + ((size_t)lbh * dv.NB + blk) * dv.bpb;

@@ -225,6 +225,10 @@ extern "C" int nosa_config_validate(const NosaConfig* c, char* msg, int msg_len)
   if (c->variant < 0 || c->variant > 2) return bad("variant must be ed-dma, s-dma or dma");
   if (c->residency != NOSA_RESIDENCY_PER_SEQUENCE && c->residency != NOSA_RESIDENCY_SHARED)
     return bad("residency must be per-sequence or shared");
+  // the shared-pool victim key packs (last_required << 32 | batch << 16 | block)
+  if (c->residency == NOSA_RESIDENCY_SHARED &&
+      (c->batch >= 65536 || (c->max_tokens + c->n_b - 1) / c->n_b >= 65536))
+    return bad("shared residency needs batch < 65536 and fewer than 65536 blocks per head");
   if (c->n_head / c->n_kv_head > 16) return bad("group size n_head/n_kv_head must be <= 16");
   if (!nosa::attend_supported(c->n_b, c->d_head, c->dtype))
     return bad("unsupported (n_b=%d, d_head=%d, dtype=%d): n_b in {16,32,64,128}, d_head in {64,128}",
@@ -1745,6 +1749,9 @@ extern "C" int nosa_check_errors(NosaCtx* ctx, uint32_t* flags) {
     cudaMemset(ctx->dv.err, 0, 4);
     if (f & NOSA_FLAG_CAPACITY)
       return fail(ctx, NOSA_ERR_CAPACITY, "step requires more blocks than the fast tier holds per head (%d)", ctx->dv.C);
+    if (f & NOSA_FLAG_FULL)
+      return fail(ctx, NOSA_ERR_VALUE, "head cache capacity exhausted (%d blocks of %d tokens); append refused",
+                  ctx->dv.NB, ctx->dv.n_b);
     if (f & NOSA_FLAG_NOT_RESIDENT)
       return fail(ctx, NOSA_ERR_STATE, "all-resident run met a miss that is not a newborn block (flags 0x%x)", f);
     return fail(ctx, NOSA_ERR_VALUE, "device error flags 0x%x", f);

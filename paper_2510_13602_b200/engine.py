@@ -297,6 +297,9 @@ class NosaEngine:
                 raise ValueError(f"{name} has {x.numel()} elements, expected {shp}")
             host.append(x)
         q, k_new, v_new = host
+        # the staging kernel reads these after this call returns (sync=False): converted copies
+        # must outlive the step, or the caching host allocator could hand their pages out again
+        self._host_keep = host
         if out is None:
             out = torch.empty((L, B, cfg.n_head, cfg.d_head), dtype=torch.float32, pin_memory=True)
         elif out.device.type != "cpu" or out.dtype != torch.float32 or not out.is_contiguous() \
@@ -460,7 +463,14 @@ class NosaEngine:
             self._call(_lib.lib.nosa_step_graph_capture_host, ctypes.byref(io))
         self._host_graph_cfg = (selector, gather, schedule)
 
+    def _check_capacity(self):
+        # the graph replays append one token per (layer, seq, head) without a host-side check
+        # of their own; the device append also refuses (NOSA_FLAG_CAPACITY) past max_tokens
+        if (self._t >= self.max_tokens).any():
+            raise ValueError("head cache capacity exhausted")
+
     def replay_host(self, q, k_new, v_new, out, stream=None):
+        self._check_capacity()
         io = self._host_io(q, k_new, v_new, out, *self._host_graph_cfg)
         with torch.cuda.device(self.device):
             self._call(_lib.lib.nosa_step_graph_launch_host, ctypes.byref(io), _lib.stream_ptr(stream))
@@ -468,6 +478,7 @@ class NosaEngine:
         return out
 
     def replay(self, stream=None):
+        self._check_capacity()
         with torch.cuda.device(self.device):
             self._call(_lib.lib.nosa_step_graph_launch, _lib.stream_ptr(stream))
         self._t += 1
