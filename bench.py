@@ -322,8 +322,11 @@ def run_native(args, rank, world, local_rank):
 
     w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, args.seed)
     t_setup = time.time()
+    # strong scaling splits a fixed global batch: pin the split-K chunk (the automatic one follows
+    # the local batch) so every sequence's outputs are bit-identical at 1, 2, 4 and 8 GPUs
+    chunk = 8 if w.get("strong") else 0
     eng = NosaEngine(cfg, batch=B, layers=L, max_tokens=max_tokens, fast_slots=fast, w1=w1, w2=w2, dtype="bf16",
-                     device=local_rank, slow_tier=slow_tier)
+                     device=local_rank, slow_tier=slow_tier, attend_chunk=chunk)
     t_alloc = time.time() - t_setup
     # inputs: counter-based draws addressed by GLOBAL sequence id (a rank's shard draws the same
     # bits a single GPU would), reproduced exactly by the CPU oracle (workload.synth_*)
@@ -630,6 +633,7 @@ def run_native(args, rank, world, local_rank):
                                      "around every kernel on its own stream (event nodes in the graph); "
                                      "value comes from the uninstrumented region",
                     "numa_node": numa_node, "seq_range": [seq0, seq0 + B],
+                    "attend_chunk": chunk or "auto (from the local batch)",
                     "slow_tier": slow_tier + (" (loopback: the own HBM stands in for a peer)"
                                               if peer_dev == local_rank else "")},
             "parity": parity,

@@ -102,3 +102,23 @@ def test_bench_burn_in_defaults(monkeypatch):
                        (["bench.py", "--workload", "cfg5", "--burn-in", "7"], 7)):
         monkeypatch.setattr(sys, "argv", argv)
         assert bench.parse().burn_in == want
+
+
+def test_torchrun_two_ranks_reference_arm():
+    """The driver's N>1 launch (torch.distributed.run, 2 ranks on 127.0.0.1) of the reference arm:
+    rank 0 alone prints one JSON line with n_gpus = 2, rank 1 exits 0 without work."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--impl", "reference",
+           "--workload", "cfg1", "--gpus", "2", "--steps", "1", "--warmup", "0"]
+    p = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [json.loads(x) for x in p.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    line = lines[0]
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
