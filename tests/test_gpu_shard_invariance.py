@@ -59,7 +59,7 @@ def _split(results, layers, steps):
 
 @pytest.mark.parametrize("selector,rho", [("nosa", 0.95), ("infllmv2", 0.0)])
 def test_batch_split_is_bitwise_invariant(selector, rho):
-    kw = dict(t0=6000, fast=48, layers=2, steps=6, rho=rho, selector=selector, chunk=4)
+    kw = dict(t0=6000, fast=72, layers=2, steps=6, rho=rho, selector=selector, chunk=4)
     whole = _decode(0, 4, **kw)
     parts = _split([_decode(0, 2, **kw), _decode(2, 2, **kw)], kw["layers"], kw["steps"])
     assert whole[1] == parts[1], "selections differ between one B=4 context and two B=2 shards"
@@ -73,7 +73,7 @@ def test_batch_split_is_bitwise_invariant(selector, rho):
 
 
 def test_auto_chunk_changes_only_output_rounding():
-    kw = dict(t0=6000, fast=48, layers=1, steps=4, rho=0.95, selector="nosa", chunk=0)
+    kw = dict(t0=6000, fast=72, layers=1, steps=4, rho=0.95, selector="nosa", chunk=0)
     whole = _decode(0, 4, **kw)
     parts = _split([_decode(0, 2, **kw), _decode(2, 2, **kw)], kw["layers"], kw["steps"])
     assert whole[1] == parts[1] and whole[2] == parts[2] and whole[3] == parts[3]
