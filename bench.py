@@ -98,6 +98,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--trace-out", default=None, help="write the device timeline of one instrumented step here")
+    ap.add_argument("--report-dir", default=None,
+                    help="also write the run as a reference sim-report (sim_report.json / .csv) into this directory")
     ap.add_argument("--slow-tier", default="host",
                     help="'host' (pinned host memory over PCIe) or 'peer' (another GPU's HBM over NVLink: "
                          "device (local_rank + 1) %% GPUs on the node, the own device when alone = loopback)")
@@ -609,6 +611,23 @@ def run_native(args, rank, world, local_rank):
                      "frac_at_measured_hbm": round(max(hbm_step / (hbm_peak * 1e9), h2d_step / (link_gbs * 1e9))
                                                    * 1e3 / step_ms, 4)}
 
+    # ---------------- the run as a reference SimReport row (offload_sim.py:175-192; cli.py:214-218)
+    from paper_2510_13602_b200 import reports
+    from paper_2510_13602_b200.dist import sum_over_ranks
+    from paper_2510_13602_b200.engine import ResidencyStats
+    tot = sum_over_ranks([st.hits, st.misses, st.bytes_up, st.bytes_down, st.topk_required, st.topk_misses], device)
+    st_all = ResidencyStats(hits=int(tot[0]), misses=int(tot[1]), bytes_up=int(tot[2]), bytes_down=int(tot[3]),
+                            topk_required=int(tot[4]), topk_misses=int(tot[5]))
+    sim = reports.row_dict(reports.report_from_run(
+        selector=args.selector, resident=w["cache"] == "resident", batch=w["global_batch"], context=ctx_len,
+        steps=args.steps, seed=args.seed, stats=st_all, tokens_per_s=tokens / (ms_max * 1e-3),
+        attn_ms_per_step=kern["attend"]["total_ms"] / args.steps, ms_per_step=step_ms,
+        fast_slots_per_seq=fast, config=cfg.to_dict()))
+    if args.report_dir and rank == 0:
+        reports.write_sim_report([sim], args.report_dir,
+                                 params={"measured": True, "link_gbs": link_gbs, "hbm_gbs": hbm_peak,
+                                         "layers": L, "workload": args.workload})
+
     # ---------------- CPU baseline: the oracle (reference algorithm) on a bounded sample
     cpu, parity = None, None
     if pairs:
@@ -639,6 +658,7 @@ def run_native(args, rank, world, local_rank):
             "parity": parity,
             "h2d_miss_gbs": round(h2d_step / (step_ms * 1e-3) / 1e9, 3),
             "hit_rate": round(st.hit_rate, 4),
+            "sim_report": sim,
             "misses_per_seq_head_step": round(st.misses / (B * cfg.n_kv_head * L * args.steps), 3),
             "attended_blocks_per_seq_head": round(R_total / (B * cfg.n_kv_head * L * args.steps), 2),
             "selection": {"scan": "screened: bf16 K_c pre-scan with a proven error bound, f64 rescoring of "

@@ -92,6 +92,9 @@ typedef struct NosaStats {
   int64_t hits, misses, new_blocks, evictions, steps;
   int64_t bytes_up, bytes_down; /* misses * bytes_per_block, evictions * bytes_per_block */
   int64_t candidates;           /* pool rows rescored in f64 by the screened selector     */
+  int64_t topk_required;        /* required blocks from the selection pool (top-k picks)  */
+  int64_t topk_misses;          /* fetches among them: hit_rate_topk = 1 - misses/required
+                                   (offload_sim.py:291-293)                                */
 } NosaStats;
 
 /* Per-step inputs/outputs of nosa_decode_step: one pointer per tensor, layer-major.

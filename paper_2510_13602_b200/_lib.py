@@ -42,7 +42,8 @@ class NosaConfig(ctypes.Structure):
 
 class NosaStats(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in (
-        "hits", "misses", "new_blocks", "evictions", "steps", "bytes_up", "bytes_down", "candidates")]
+        "hits", "misses", "new_blocks", "evictions", "steps", "bytes_up", "bytes_down", "candidates",
+        "topk_required", "topk_misses")]
 
 
 class NosaStepIO(ctypes.Structure):

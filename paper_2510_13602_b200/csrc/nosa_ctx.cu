@@ -1715,6 +1715,8 @@ extern "C" int nosa_read_stats(NosaCtx* ctx, int l0, int l1, int s0, int s1, Nos
         out->evictions += p[nosa::ST_EVICT];
         out->steps += p[nosa::ST_STEPS];
         out->candidates += p[nosa::ST_CAND];
+        out->topk_required += p[nosa::ST_TOPK];
+        out->topk_misses += p[nosa::ST_TOPK_MISS];
       }
   out->bytes_up = out->misses * dv.bpb;
   out->bytes_down = out->evictions * dv.bpb;

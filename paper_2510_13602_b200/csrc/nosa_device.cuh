@@ -101,7 +101,9 @@ struct StageSeg {
   long long n16;
 };
 
-enum StatIdx { ST_HITS = 0, ST_MISSES, ST_NEW, ST_EVICT, ST_STEPS, ST_CAND, ST_N = 8 };  // ST_CAND: rows rescored in f64
+// ST_CAND: rows rescored in f64; ST_TOPK / ST_TOPK_MISS: required pool (top-k) blocks and the
+// fetches among them (offload_sim.py:291-293, hit_rate_topk)
+enum StatIdx { ST_HITS = 0, ST_MISSES, ST_NEW, ST_EVICT, ST_STEPS, ST_CAND, ST_TOPK, ST_TOPK_MISS, ST_N = 8 };
 
 // shared-pool mode: storage index of shared slot s of (layer, head) in the [lbh][C] arrays, and
 // the slot offset relative to sequence b's own pool row (pool + (lbh*C + rel)*bpb addresses it)

@@ -617,8 +617,17 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
       pf[f] = blk;
       n_new += (blk * dv.n_b >= t0);  // born during the run (offload_sim.py:286-289)
     }
+    // top-k accounting: required blocks of the selection pool and the fetches among them
+    const int rs_blk = max(0, t0 - dv.n_w + 1) / dv.n_b;
+    int n_tk = 0, n_tkm = 0;
+    for (int i = lane; i < n_req; i += 32) n_tk += sm.req[i] >= dv.n_sink && sm.req[i] < rs_blk;
+    for (int f = lane; f < nf; f += 32) n_tkm += sm.fetch[f] >= dv.n_sink && sm.fetch[f] < rs_blk;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) n_new += __shfl_xor_sync(0xffffffffu, n_new, o);
+    for (int o = 16; o; o >>= 1) {
+      n_new += __shfl_xor_sync(0xffffffffu, n_new, o);
+      n_tk += __shfl_xor_sync(0xffffffffu, n_tk, o);
+      n_tkm += __shfl_xor_sync(0xffffffffu, n_tkm, o);
+    }
     top -= nf;
     // enqueue the misses for the gather (K3)
     int base = 0;
@@ -657,6 +666,8 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
       st[ST_NEW] += n_new;
       st[ST_EVICT] += nev;
       st[ST_STEPS] += 1;
+      st[ST_TOPK] += n_tk;
+      st[ST_TOPK_MISS] += n_tkm;
       dv.plan_n[lbh * 3 + 0] = nf;
       dv.plan_n[lbh * 3 + 1] = nev;
       dv.plan_n[lbh * 3 + 2] = n_req - nf;
@@ -1021,7 +1032,13 @@ __global__ void __launch_bounds__(kSharedThreads)
       }
       top -= nf;
       misc[1] = top;
+      const int rs_blk = max(0, t0 - dv.n_w + 1) / dv.n_b;
+      int n_tk = 0, n_tkm = 0;
+      for (int i = 0; i < n; ++i) n_tk += req[i] >= dv.n_sink && req[i] < rs_blk;
+      for (int f = 0; f < nf; ++f) n_tkm += fetch[f] >= dv.n_sink && fetch[f] < rs_blk;
       long long* st = dv.stats + (size_t)lbh * ST_N;
+      st[ST_TOPK] += n_tk;
+      st[ST_TOPK_MISS] += n_tkm;
       st[ST_HITS] += n - nf;
       st[ST_MISSES] += nf;
       st[ST_NEW] += n_new;

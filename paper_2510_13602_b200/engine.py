@@ -39,11 +39,18 @@ class ResidencyStats:
     new_blocks: int = 0
     evictions: int = 0
     candidates: int = 0   # pool rows rescored in f64 by the screened selector
+    topk_required: int = 0  # required blocks picked from the selection pool (top-k)
+    topk_misses: int = 0    # fetches among them
 
     @property
     def hit_rate(self) -> float:
         total = self.hits + self.misses
         return 1.0 if total == 0 else self.hits / total
+
+    @property
+    def hit_rate_topk(self) -> float:
+        """Top-k blocks that were already fast-resident (offload_sim.py:291-293, 314)."""
+        return 1.0 if self.topk_required == 0 else 1.0 - self.topk_misses / self.topk_required
 
     def to_dict(self) -> dict:
         return {"hit_rate": self.hit_rate, "hits": self.hits, "misses": self.misses,
@@ -572,7 +579,8 @@ class NosaEngine:
         self._call(_lib.lib.nosa_read_stats, layers.start, layers.stop, seqs.start, seqs.stop, ctypes.byref(st))
         return ResidencyStats(hits=st.hits, misses=st.misses, bytes_up=st.bytes_up, bytes_down=st.bytes_down,
                               steps=st.steps, new_blocks=st.new_blocks, evictions=st.evictions,
-                              candidates=st.candidates)
+                              candidates=st.candidates, topk_required=st.topk_required,
+                              topk_misses=st.topk_misses)
 
     def reset_stats(self):
         with torch.cuda.device(self.device):

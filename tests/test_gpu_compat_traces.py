@@ -117,3 +117,18 @@ def test_gpu_trace_json_and_theorem_one(tmp_path):
         r.dump(tmp_path / "again.json")
         assert (tmp_path / "again.json").read_bytes() == path.read_bytes()
     eng.close()
+
+
+def test_recorded_gpu_traces_are_reproducible(tmp_path):
+    """tools/make_gpu_traces.py re-run on this box reproduces the committed fixtures byte for byte
+    (the CPU suite checks those against the oracle and the reference's serde / Theorem-1 checker)."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    subprocess.run([sys.executable, str(root / "tools" / "make_gpu_traces.py"), str(tmp_path)], check=True)
+    for name in ("gpu_trace_nosa.json", "gpu_trace_infllmv2.json"):
+        fixture = root / "tests" / "golden" / name
+        if not fixture.exists():
+            pytest.skip("fixtures not recorded yet")
+        assert (tmp_path / name).read_bytes() == fixture.read_bytes(), name

@@ -143,6 +143,7 @@ def _run_pair(cfg, *, batch, t0s, steps, fast_slots, seed, rho, selector="nosa",
     st = eng.residency_stats()
     ost = orc.stats()
     assert (st.hits, st.misses, st.evictions, st.steps) == (ost["hits"], ost["misses"], ost["evictions"], ost["steps"])
+    assert (st.topk_required, st.topk_misses) == (ost["topk_required"], ost["topk_misses"])  # hit_rate_topk
     assert st.bytes_up == st.misses * eng.bytes_per_block
     assert (eng.lengths() == np.array([[t + steps for t in t0s]] * layers)).all()
     eng.close()

@@ -98,6 +98,7 @@ def run_headline(*, t0, fast_slots, batch, layers, steps, rho, selector="nosa", 
                 assert got == orc.managers[l][b].slot_of[h], f"slot table layer {l} seq {b} head {h}"
     st, ost = eng.residency_stats(), orc.stats()
     assert (st.hits, st.misses, st.evictions, st.steps) == (ost["hits"], ost["misses"], ost["evictions"], ost["steps"])
+    assert (st.topk_required, st.topk_misses) == (ost["topk_required"], ost["topk_misses"])  # hit_rate_topk
     eng.close()
     return worst, ties, ost["evictions"]
 
