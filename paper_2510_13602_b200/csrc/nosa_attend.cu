@@ -435,6 +435,7 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
     for (int seq = 0;; ++seq) {
       const int s = seq % T::NS;
       mbar_wait(&full[s], (seq / T::NS) & 1);
+      __syncwarp();  // lanes leave the spin-wait independently: reconverge before ldmatrix / mma (.aligned)
       const ItemInfo it = info[s];
       if (it.flags & IF_END) break;
       if (it.flags & IF_FIRST) {

@@ -116,11 +116,13 @@ __global__ void __launch_bounds__(PTHREADS, 1)
     mbar_init(done, 1);
     fence_mbar_init();
   }
+  __syncwarp();     // reconverge warp 0 before its .sync.aligned allocation
   if (warp == 0) {  // accumulator: 128 lanes x 256 f32 columns of TMEM
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(PN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  __syncwarp();
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -163,6 +165,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   __syncwarp();
 
   mbar_wait(done, 0);
+  __syncwarp();  // lanes leave the spin-wait independently: reconverge before tcgen05.ld (.aligned)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const int trow = warp * 32 + lane;
   if (splits == 1) {

@@ -402,6 +402,36 @@ def test_capacity_exceeded_is_raised():
     eng.close()
 
 
+def test_full_head_cache_append_refused(monkeypatch):
+    """A step past the head capacity (HeadState, decode.py:65-71): the host entry points refuse it,
+    and with the host check bypassed the device append refuses it too (NOSA_FLAG_FULL) instead of
+    writing into the next row's block 0."""
+    cfg = ONE_B_SMALL
+    w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, 0)
+    t0 = 64 * 80 - 1                       # one step fills the last block exactly
+    eng = NosaEngine(cfg, batch=2, layers=1, max_tokens=t0 + 1, fast_slots=81, w1=w1, w2=w2)
+    K, V = workload.prefix_kv(0, 2, cfg.n_kv_head, t0, cfg.d_head)
+    eng.prefill(torch.from_numpy(K), torch.from_numpy(V), layer=0)
+    eng.start_run()
+    stream = workload.QueryStream(0, 1, 2, cfg.n_head, cfg.n_kv_head, cfg.d_head, 0.9)
+    eng.step(*stream.next())
+    rows = [(b, h) for b in range(2) for h in range(cfg.n_kv_head)]
+    before = [eng.read_kv(0, b, h, t=t0 + 1) for b, h in rows]
+    with pytest.raises(ValueError, match="capacity exhausted"):
+        eng.step(*stream.next())
+    with pytest.raises(ValueError, match="capacity exhausted"):
+        eng.replay()
+    monkeypatch.setattr(eng, "_check_step", lambda: None)
+    with pytest.raises(ValueError, match="capacity exhausted"):
+        eng.step(*stream.next())                               # device flag, raised by check_errors
+    assert list(eng.lengths()[0]) == [t0 + 1, t0 + 1]
+    for (b, h), (k0, v0) in zip(rows, before):                 # no row was overwritten
+        k1, v1 = eng.read_kv(0, b, h, t=t0 + 1)
+        np.testing.assert_array_equal(k1, k0)
+        np.testing.assert_array_equal(v1, v0)
+    eng.close()
+
+
 def test_empty_cache_rejected():
     w1, w2 = workload.eviction_head(SMALL.n_head, SMALL.d_head, 0)
     eng = NosaEngine(SMALL, batch=1, max_tokens=100, fast_slots=10, w1=w1, w2=w2)
