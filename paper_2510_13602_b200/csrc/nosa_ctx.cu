@@ -109,7 +109,9 @@ struct NosaCtx {
   size_t io_bytes = 0;
   int stage_grid = 32;              // CTAs of the input-staging kernel (host-buffer step)
   bool stage_with_copies = false;   // NOSA_STAGE_COPIES: stage host inputs with cudaMemcpyAsync
-  int attend_layers = 1;            // layers per attention launch (pipelined schedule)
+  int attend_layers = 1;            // most layers in one attention launch (pipelined schedule)
+  std::vector<int> att_plan;        // layers per attention launch, in order (sums to L)
+  std::vector<int> att_l0;          // (per step) first layer of the batch closed at layer l, else -1
   // QKV projection of nosa_decode_step_hidden: per-layer [W_q | W_k | W_v]^T, bf16 [n][d] (caller-owned)
   char* proj_wbuf = nullptr;         // [L][n][d] bf16, the layers' weights side by side
   std::vector<char> proj_set;        // per layer: weights loaded
@@ -368,14 +370,47 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   // persistent launch (measured on cfg 2: 1 / 4 / 6 / 7 / 8 / 10 / 14 layers per launch =
   // 37.0K / 44.7K / 45.7K / 45.4K / 46.3-46.5K / 46.5K / 45.7K tok/s); with offloaded blocks each
   // layer's attention waits only for its own miss transfer.  fp32 runs one layer per launch.
-  if (c.attend_layers > 0) {
-    ctx->attend_layers = c.attend_layers;
+  // With offloaded blocks the step is bound by the miss transfers, one layer after another; the
+  // attention of a batch of layers starts once the batch's last transfer lands, so the plan ramps
+  // 1, 4, 4, ..., 2, 1: the first and last layers' attention follow their own transfer at once
+  // (the step's head and tail), the middle layers share launches, which amortises the launch and
+  // dependency latency of each persistent launch (measured on cfg 3: 1 / 2 / 4 layers per launch
+  // = 0.74 / 0.89 / 0.97 of HBM bandwidth per launch by CUDA events; uniform 2 and 4 lengthen the
+  // step's tail by 1 and 3 attention layers).
+  std::vector<int>& plan = ctx->att_plan;
+  plan.clear();
+  const bool uniform_req = c.attend_layers > 0 || getenv("NOSA_ATTEND_LAYERS");
+  if (c.dtype != NOSA_DTYPE_BF16) {
+    plan.assign(dv.L, 1);
+  } else if (const char* e = getenv("NOSA_ATTEND_PLAN")) {  // experiments: "a,b,c,..." (summing to L)
+    int sum = 0;
+    for (const char* x = e; *x;) {
+      const int v = std::max(1, atoi(x));
+      plan.push_back(std::min(v, dv.L - sum));
+      sum += plan.back();
+      while (*x && *x != ',') ++x;
+      if (*x == ',') ++x;
+      if (sum >= dv.L) break;
+    }
+    if (sum < dv.L) plan.push_back(dv.L - sum);
+  } else if (uniform_req || dv.C >= dv.NB) {
+    int nl = c.attend_layers > 0 ? c.attend_layers : (dv.C >= dv.NB ? 8 : 1);
+    if (const char* e = getenv("NOSA_ATTEND_LAYERS")) nl = std::max(1, atoi(e));
+    nl = std::min(nl, dv.L);
+    for (int l = 0; l < dv.L; l += nl) plan.push_back(std::min(nl, dv.L - l));
   } else {
-    ctx->attend_layers = (dv.C >= dv.NB && c.dtype == NOSA_DTYPE_BF16) ? 8 : 1;
+    if (dv.L <= 3) {
+      plan.assign(dv.L, 1);
+    } else {
+      plan.push_back(1);
+      int mid = dv.L - 4;
+      for (; mid >= 4; mid -= 4) plan.push_back(4);
+      if (mid) plan.push_back(mid);
+      plan.push_back(2);
+      plan.push_back(1);
+    }
   }
-  if (const char* e = getenv("NOSA_ATTEND_LAYERS")) ctx->attend_layers = std::max(1, atoi(e));
-  if (c.dtype != NOSA_DTYPE_BF16) ctx->attend_layers = 1;
-  ctx->attend_layers = std::min(ctx->attend_layers, dv.L);
+  ctx->attend_layers = *std::max_element(plan.begin(), plan.end());
   dv.nbuf = 2 * ctx->attend_layers;
   const size_t LBH = (size_t)dv.L * dv.B * dv.H;
   const size_t BH = (size_t)dv.B * dv.H;
@@ -1019,7 +1054,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   groups.clear();
   if (grouped) {
     // sizes nl, nl, 2nl, 4nl, ... (nl = layers per attention batch): batch k's plans complete together
-    const int nlb = ctx->attend_layers;
+    const int nlb = ctx->att_plan[0];  // the first attention batch waits for the first group only
     for (int l0 = 0, n = nlb; l0 < dv.L; l0 += n, n = std::max(nlb, l0)) groups.push_back({l0, std::min(n, dv.L - l0)});
   } else {
     for (int l = 0; l < dv.L; ++l) groups.push_back({l, 1});
@@ -1171,9 +1206,15 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   // with the copy-engine mover, only the first two groups' inputs go ahead of the first miss
   // transfer; the rest follow it (the host submits that transfer once layer 0 is planned)
   if (int rc = issue_groups(groups.size())) return rc;
-  // attention batches: nl consecutive layers per persistent launch (layer-serial: one, since
-  // select(l+1) waits for layer l to finish)
-  const int nl = serial ? 1 : ctx->attend_layers;
+  // attention batches: att_plan's consecutive layer ranges, one persistent launch each
+  // (layer-serial: one layer per launch, since select(l+1) waits for layer l to finish)
+  std::vector<int>& att_l0 = ctx->att_l0;  // first layer of the batch that layer l closes, or -1
+  att_l0.assign(dv.L, -1);
+  if (serial) {
+    for (int l = 0; l < dv.L; ++l) att_l0[l] = l;
+  } else {
+    for (int l0 = 0, k = 0; l0 < dv.L; l0 += ctx->att_plan[k++]) att_l0[l0 + ctx->att_plan[k] - 1] = l0;
+  }
   int n_att = 0, n_gather_kernels = 0;
   ctx->memcpy_born_launches = 0;
   cudaEvent_t last_att[2] = {nullptr, nullptr};
@@ -1183,8 +1224,8 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
       if (int rc = project(l, 1)) return rc;
       if (int rc = select(l)) return rc;
     }
-    const bool batch_end = (l + 1) % nl == 0 || l == dv.L - 1;  // last layer of an attention batch
-    const int l0 = l - l % nl, n = l - l0 + 1;
+    const bool batch_end = att_l0[l] >= 0;  // last layer of an attention batch
+    const int l0 = batch_end ? att_l0[l] : l, n = l - l0 + 1;
     if (!dv.born_local) {  // (all resident: the planner placed the newborn blocks, nothing to move)
       CUDA_TRY(ctx, cudaStreamWaitEvent(cp, ctx->ev_plan[l], 0));
       if (io->gather_mode == NOSA_GATHER_MEMCPY) {

@@ -105,7 +105,7 @@ __device__ __forceinline__ bool vless(const VKey& a, const VKey& b) {
 //         fetch ids at base+3.., evict ids after them (victim order)
 __global__ void __launch_bounds__(kThreads) mgr_plan_kernel(Mgr m, int h, int batch) {
   __shared__ unsigned hist[256];
-  __shared__ int s_cnt, s_nf, s_hits, s_digit, s_below, s_nv;
+  __shared__ int s_cnt, s_nf, s_hits, s_digit, s_below, s_nv, s_unknown;
   __shared__ VKey s_thr;
   const int tid = threadIdx.x;
   const int n = m.io[0];
@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(kThreads) mgr_plan_kernel(Mgr m, int h, int ba
   if (tid == 0) {
     m.clock[0] = clock;  // the tick happens before any check (kv_manager.py:211-212)
     s_cnt = 0;
+    s_unknown = 0;
     s_nf = 0;
     s_hits = 0;
     out[0] = out[1] = out[2] = 0;
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(kThreads) mgr_plan_kernel(Mgr m, int h, int ba
       const int id = req[i];
       if (id < 0 || m.tier[(size_t)h * m.ids + id] < 0) {
         set_err(m, kErrUnknown);
-        s_cnt = -1;
+        s_unknown = 1;  // (its own flag: s_cnt is reset below while others may still test this)
         break;
       }
       const size_t k = (size_t)h * m.ids + id;
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(kThreads) mgr_plan_kernel(Mgr m, int h, int ba
     s_hits = hits;
   }
   __syncthreads();
-  if (s_cnt == -1) return;
+  if (s_unknown) return;
   const int nf = s_nf;
   const int shortfall = nf - m.tops[2 * h];
   int* ev = out + 3 + nf;
