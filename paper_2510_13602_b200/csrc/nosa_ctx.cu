@@ -1055,7 +1055,19 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   if (grouped) {
     // sizes nl, nl, 2nl, 4nl, ... (nl = layers per attention batch): batch k's plans complete together
     const int nlb = ctx->att_plan[0];  // the first attention batch waits for the first group only
-    for (int l0 = 0, n = nlb; l0 < dv.L; l0 += n, n = std::max(nlb, l0)) groups.push_back({l0, std::min(n, dv.L - l0)});
+    if (const char* e = getenv("NOSA_SELECT_PLAN")) {  // experiments: "a,b,..." layers per group
+      int l0 = 0;
+      for (const char* x = e; *x && l0 < dv.L;) {
+        const int n = std::min(std::max(1, atoi(x)), dv.L - l0);
+        groups.push_back({l0, n});
+        l0 += n;
+        while (*x && *x != ',') ++x;
+        if (*x == ',') ++x;
+      }
+      if (l0 < dv.L) groups.push_back({l0, dv.L - l0});
+    } else {
+      for (int l0 = 0, n = nlb; l0 < dv.L; l0 += n, n = std::max(nlb, l0)) groups.push_back({l0, std::min(n, dv.L - l0)});
+    }
   } else {
     for (int l = 0; l < dv.L; ++l) groups.push_back({l, 1});
   }

@@ -71,20 +71,12 @@ struct SelSmem {
   unsigned long long* ckey;
   unsigned* lo_key;  // [Pp] screened lower bound of each pool row (monotone u32 of the float)
   float* up;         // [Pp] screened upper bound
-  int* hist;         // [256] radix-select histogram, pass 1 (filled during the screen scan)
-  int* hist2;        // [256] pass 2
-  // planner state prefetched with cp.async while the selection runs (no global round trip in
-  // the hit test, victim choice or slot reuse): slot_of[0..NB), blk_of / lastreq / free stack [C]
-  int* pslot;
-  int* cblk;
-  int* clast;
-  int* cstack;
-  int* rk;           // [MQ+ME] prefix of the frozen s_e rank order (NOSA walk)
+  int* hist;         // [256] radix-select histogram
   int* misc;  // [16]
   long long* marks;  // diagnostics: clock64 at phase boundaries (NULL = off)
 };
 
-__device__ SelSmem carve_sel_smem(char* base, int D, int Pp, int C, int R) {
+__device__ SelSmem carve_sel_smem(char* base, int D, int Pp, int C) {
   SelSmem s;
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -106,31 +98,17 @@ __device__ SelSmem carve_sel_smem(char* base, int D, int Pp, int C, int R) {
   s.lo_key = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * Pp));
   s.up = reinterpret_cast<float*>(take(sizeof(float) * Pp));
   s.hist = reinterpret_cast<int*>(take(sizeof(int) * 256));
-  s.hist2 = reinterpret_cast<int*>(take(sizeof(int) * 256));
-  s.pslot = reinterpret_cast<int*>(take(sizeof(int) * Pp));
-  s.cblk = reinterpret_cast<int*>(take(sizeof(int) * C));
-  s.clast = reinterpret_cast<int*>(take(sizeof(int) * C));
-  s.cstack = reinterpret_cast<int*>(take(sizeof(int) * C));
-  s.rk = reinterpret_cast<int*>(take(sizeof(int) * R));
   s.misc = reinterpret_cast<int*>(take(sizeof(int) * 16));
   return s;
 }
 
-size_t sel_smem_bytes(int D, int Pp, int C, int R) {
+size_t sel_smem_bytes(int D, int Pp, int C) {
   auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
   return r(8 * D) + r(8 * (size_t)Pp) + r(4 * (size_t)Pp) + 2 * r(4 * (size_t)(Pp / 32)) +
-         5 * r(4 * (size_t)C) + r(8 * (size_t)C) + 2 * r(4 * (size_t)Pp) + 2 * r(4 * 256) +
-         r(4 * (size_t)Pp) + 3 * r(4 * (size_t)C) + r(4 * (size_t)R) + r(64);
+         5 * r(4 * (size_t)C) + r(8 * (size_t)C) + 2 * r(4 * (size_t)Pp) + r(4 * 256) + r(64);
 }
 
-// 4-byte asynchronous global -> shared copy (LDGSTS): issued early, waited with cp_async_wait_all
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-enum { M_NREQ = 0, M_NF, M_SHORT, M_NCAND, M_CLOCK, M_ERR, M_NQ, M_NE, M_QMAX, M_BIN, M_REM, M_NC, M_NPE };
+enum { M_NREQ = 0, M_NF, M_SHORT, M_NCAND, M_CLOCK, M_ERR, M_NQ, M_NE, M_QMAX, M_BIN, M_REM, M_NC };
 
 // diagnostics (Dev.sel_prof): phase boundary i of this CTA
 __device__ __forceinline__ void sel_mark(const SelSmem& sm, int i) {
@@ -234,19 +212,11 @@ __device__ void screened_topk(const Dev& dv, int lbh, int pool_lo, int P, int m,
     av[0] += __shfl_xor_sync(0xffffffffu, av[0], 1);
     const int u = (b3 ? 4 : 0) + (b2 ? 2 : 0) + (b1 ? 1 : 0);
     const int p = p0 + 2 * u + half;
-    const bool wr = !(hl & 1) && p < P;
-    const unsigned act = __ballot_sync(0xffffffffu, wr);
-    if (wr) {
+    if (!(hl & 1) && p < P) {
       const float s_ = sv[0], a_ = av[0];
       const float bound = (gam * a_ + __ldg(kerr + p) * qmax) * 1.001f + fabsf(s_) * 2.4e-7f + 1e-30f;
-      const unsigned key = f2key(__fsub_rd(s_, bound));
-      sm.lo_key[p] = key;
+      sm.lo_key[p] = f2key(__fsub_rd(s_, bound));
       sm.up[p] = __fadd_ru(s_, bound);
-      // radix pass 1 histogram (top 8 bits of the key): one atomic per distinct bin per warp
-      // (most rows share the sign/exponent byte, so per-lane atomics would serialise on it)
-      const unsigned bin = key >> 24;
-      const unsigned peers = __match_any_sync(act, bin);
-      if (__ffs(peers) - 1 == lane) atomicAdd(&sm.hist[bin], __popc(peers));
     }
   }
   __syncthreads();
@@ -259,19 +229,18 @@ __device__ void screened_topk(const Dev& dv, int lbh, int pool_lo, int P, int m,
   int remaining = m;
   for (int pass = 0; pass < 2; ++pass) {
     const int shift = 24 - 8 * pass;
-    int* hist = pass == 0 ? sm.hist : sm.hist2;  // (both cleared before the scan)
-    if (pass == 1) {
-      for (int p = tid; p < P; p += blockDim.x) {
-        const unsigned k = sm.lo_key[p];
-        if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1);
-      }
-      __syncthreads();
+    for (int i = tid; i < 256; i += blockDim.x) sm.hist[i] = 0;
+    __syncthreads();
+    for (int p = tid; p < P; p += blockDim.x) {
+      const unsigned k = sm.lo_key[p];
+      if ((k & pmask) == prefix) atomicAdd(&sm.hist[(k >> shift) & 255u], 1);
     }
+    __syncthreads();
     if (warp == 0) {
       int c[8], sum = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        c[j] = hist[255 - 8 * lane - j];
+        c[j] = sm.hist[255 - 8 * lane - j];
         sum += c[j];
       }
       int incl = sum;
@@ -367,30 +336,13 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
   const int a_end = min(dv.n_sink, nblk);                     // sink blocks < n_blocks(t)
   const int r_begin = max(recent_lo, a_end);
   const int Pp = next_pow2(P);
-  const int m_q_eff = min(selector == 0 ? dv.m_q : dv.m_topk, P);
-  const int m_e_eff = selector == 0 ? min(dv.m_e, P - m_q_eff) : 0;
-  // NOSA walk input: at most m_q_eff of the first m_q_eff + m_e_eff ranked blocks are query
-  // picks, so only that prefix of the frozen rank order is read (prefetched now)
-  const int need = min(P, m_q_eff + m_e_eff);
-  if (selector == 0)
-    for (int i = tid; i < need; i += blockDim.x) cp_async4(sm.rk + i, dv.rank_e + (size_t)lbh * dv.NB + i);
 
-  // (1) q_sum = sum of the group's query heads (decode.py:171-172), f64, heads added in order
+  // (1) q_sum = sum of the group's query heads (decode.py:171-172), f64
   if (tid == 0) sm.misc[M_QMAX] = 0;
-  for (int i = tid; i < 256; i += blockDim.x) {
-    sm.hist[i] = 0;
-    sm.hist2[i] = 0;
-  }
   __syncthreads();
   for (int i = tid; i < D; i += blockDim.x) {
-    const T* qi = q + ((size_t)b * dv.Hq + h * dv.G) * D + i;
-    float qv[16];  // every load in flight before the first add (G <= 16; bf16 / f32 -> f32 is exact)
-#pragma unroll
-    for (int g = 0; g < 16; ++g) qv[g] = g < dv.G ? (float)to_f64(qi[(size_t)g * D]) : 0.0f;
     double acc = 0.0;
-#pragma unroll
-    for (int g = 0; g < 16; ++g)
-      if (g < dv.G) acc += (double)qv[g];
+    for (int g = 0; g < dv.G; ++g) acc += to_f64(q[((size_t)b * dv.Hq + h * dv.G + g) * D + i]);
     sm.qsum[i] = acc;
     if (dv.screen) {
       dv.qsum_buf[(size_t)lbh * D + i] = acc;
@@ -399,6 +351,7 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
   }
   __syncthreads();
   sel_mark(sm, 1);
+  const int m_q_eff = min(selector == 0 ? dv.m_q : dv.m_topk, P);
   if (dv.screen) {
     for (int w = tid; w < Pp / 32; w += blockDim.x) {
       sm.bm_q[w] = 0u;
@@ -480,16 +433,19 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
 
   // (4) NOSA: query-agnostic picks = first m_e pool blocks of the frozen s_e rank order that
   //     were not picked by the query (selection.py:151-156)
-  cp_async_wait_all();  // this thread's prefetches (rank prefix, planner state) have landed
-  __syncthreads();      // ... and everyone's
   if (selector == 0 && warp == 0) {
+    const int m_e_eff = min(dv.m_e, P - m_q_eff);
+    const int* rank = dv.rank_e + (size_t)lbh * dv.NB;
+    // at most m_q_eff of the first m_q_eff + m_e_eff ranked blocks are query picks, so only
+    // that prefix is read; 4 x 32 entries are loaded before any is used
+    const int need = min(P, m_q_eff + m_e_eff);
     int cnt = 0;
     for (int g0 = 0; g0 < need && cnt < m_e_eff; g0 += 128) {
       int pr[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int i = g0 + 32 * k + lane;
-        pr[k] = i < need ? sm.rk[i] : -1;
+        pr[k] = i < need ? __ldg(rank + i) : -1;
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -501,16 +457,14 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
         cnt += __popc(bal);
       }
     }
-    if (lane == 0) sm.misc[M_NPE] = min(cnt, m_e_eff);
-  } else if (tid == 0 && selector != 0) {
-    sm.misc[M_NPE] = 0;
   }
   __syncthreads();
 
   sel_mark(sm, 6);
   // (5) sorted outputs: blocks_q, blocks_e, required = sink U picked U recent, one part per warp
   const int nw = Pp / 32;
-  const int n_picked = m_q_eff + sm.misc[M_NPE];  // exactly m_q_eff query picks, disjoint e-picks
+  int n_picked = 0;  // every thread counts the picks (broadcast reads of <= 32 words)
+  for (int w = 0; w < nw; ++w) n_picked += __popc(sm.bm_q[w] | sm.bm_e[w]);
   const int n_req = a_end + n_picked + (nblk - r_begin);
   if (warp == 0) {
     const int nq = warp_bits_to_sorted(sm.bm_q, nw, pool_lo, dv.sel_q + (size_t)lbh * dv.MQ);
@@ -577,7 +531,7 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
       for (int k = 0; k < 4; ++k) {
         const int i = g0 + 32 * k + lane;
         blk[k] = i < n_req ? sm.req[i] : 0;
-        sl[k] = i < n_req ? sm.pslot[blk[k]] : 0;
+        sl[k] = i < n_req ? slot_of[blk[k]] : 0;
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -585,7 +539,6 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
         const bool miss = i < n_req && sl[k] < 0;
         if (i < n_req && sl[k] >= 0) {
           lastreq[sl[k]] = clock;
-          sm.clast[sl[k]] = clock;
           sm.reqslot[i] = sl[k];
         }
         const unsigned bal = __ballot_sync(0xffffffffu, miss);
@@ -614,9 +567,9 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
   // (2) victims: least-recently-required resident blocks not required now (kv_manager.py:233-246)
   if (shortfall > 0) {
     for (int s = tid; s < C; s += blockDim.x) {
-      const int blk = sm.cblk[s];
-      const bool cand = blk >= 0 && sm.clast[s] != clock;
-      sm.ckey[s] = cand ? ((unsigned long long)(unsigned)sm.clast[s] << 32) | (unsigned)blk
+      const int blk = blk_of[s];
+      const bool cand = blk >= 0 && lastreq[s] != clock;
+      sm.ckey[s] = cand ? ((unsigned long long)(unsigned)lastreq[s] << 32) | (unsigned)blk
                         : ~0ull;
       if (cand) atomicAdd(&sm.misc[M_NCAND], 1);
     }
@@ -644,11 +597,10 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
     const int nev = shortfall > 0 ? shortfall : 0;
     for (int r = lane; r < nev; r += 32) {
       const int s = sm.victims[r];
-      const int blk = sm.cblk[s];
+      const int blk = blk_of[s];
       slot_of[blk] = -1;
       blk_of[s] = -1;
       fstack[top + r] = s;
-      sm.cstack[top + r] = s;
       pe[r] = blk;
     }
     __syncwarp();
@@ -656,7 +608,7 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
     const int t0 = dv.t0[lbh];
     int n_new = 0;
     for (int f = lane; f < nf; f += 32) {
-      const int s = sm.cstack[top - 1 - f];
+      const int s = fstack[top - 1 - f];
       const int blk = sm.fetch[f];
       slot_of[blk] = s;
       blk_of[s] = blk;
@@ -758,29 +710,18 @@ __global__ void __launch_bounds__(256, 4)  // 4 CTAs per SM: one CTA's scan over
   const int b = bh / dv.H, h = bh % dv.H;
   const int lbh = (layer * dv.B + b) * dv.H + h;
   const int Pp = next_pow2(dv.NB);
-  SelSmem sm = carve_sel_smem(smem_raw, dv.D, Pp, dv.C, dv.MQ + dv.ME);
+  SelSmem sm = carve_sel_smem(smem_raw, dv.D, Pp, dv.C);
   __shared__ long long marks[16];
   sm.marks = dv.sel_prof ? marks : nullptr;
   if (sm.marks && threadIdx.x == 0)
     for (int i = 0; i < 16; ++i) marks[i] = 0;
   sel_mark(sm, 0);
-  if (mode == 2 && ext_nreq[bh] < 0) return;  // this manager is not part of the call: no clock tick, no stats
-  if (mode != 0) {  // the planner's table rows, in flight while the selection runs
-    const int* so = dv.slot_of + (size_t)lbh * dv.NB;
-    for (int i = threadIdx.x; i < dv.NB; i += blockDim.x) cp_async4(sm.pslot + i, so + i);
-    const size_t r0 = (size_t)lbh * dv.C;
-    for (int i = threadIdx.x; i < dv.C; i += blockDim.x) {
-      cp_async4(sm.cblk + i, dv.blk_of + r0 + i);
-      cp_async4(sm.clast + i, dv.lastreq + r0 + i);
-      cp_async4(sm.cstack + i, dv.fstack + r0 + i);
-    }
-  }
 
   if (mode == 2) {
     const int n = ext_nreq[bh];
+    if (n < 0) return;  // this manager is not part of the call: no clock tick, no stats
     if (threadIdx.x == 0) sm.misc[M_NREQ] = n;
     for (int i = threadIdx.x; i < min(n, dv.C); i += blockDim.x) sm.req[i] = ext_req[(size_t)bh * dv.C + i];
-    cp_async_wait_all();
     __syncthreads();
   } else {
     select_phase<T>(dv, layer, b, h, q, selector, sm);
@@ -1136,7 +1077,7 @@ cudaError_t launch_select_plan(const Dev& dv, int layer, const void* q, int sele
                                const int* ext_req, const int* ext_nreq, cudaStream_t st, int layers) {
   int Pp = 32;
   while (Pp < dv.NB) Pp <<= 1;
-  const size_t smem = sel_smem_bytes(dv.D, Pp, dv.C, dv.MQ + dv.ME);
+  const size_t smem = sel_smem_bytes(dv.D, Pp, dv.C);
   const size_t qs = (size_t)dv.B * dv.Hq * dv.D;  // elements per layer of q
   const dim3 grid(dv.B * dv.H, layers);
   if (dv.dtype == 0) {
