@@ -260,6 +260,53 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "source": "NVML, 20 ms polling"}
 
 
+class PcieSampler:
+    """Hardware PCIe throughput during the timed region: NVML's per-device PCIe counters
+    (nvmlDeviceGetPcieThroughput, each call integrates a 20 ms window; RX = bytes the GPU
+    receives, i.e. host -> device; the same counters as `nvidia-smi dmon -s t`).  Independent of
+    the bench's own byte accounting, so it checks the H2D figure the step roofline is built on."""
+
+    def __init__(self, index):
+        self.index, self.rx, self.tx, self.stop = index, [], [], threading.Event()
+
+    def __enter__(self):
+        self.nvml = None
+        if os.environ.get("NOSA_BENCH_NO_CLOCKS"):
+            return self
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+        except Exception as exc:
+            self.nvml, self.err = None, str(exc)
+        return self
+
+    def _poll(self):
+        n = self.nvml
+        while not self.stop.is_set():
+            try:  # KB/s over the call's 20 ms window
+                self.rx.append(n.nvmlDeviceGetPcieThroughput(self.h, n.NVML_PCIE_UTIL_RX_BYTES) * 1e3 / 1e9)
+                self.tx.append(n.nvmlDeviceGetPcieThroughput(self.h, n.NVML_PCIE_UTIL_TX_BYTES) * 1e3 / 1e9)
+            except Exception:
+                return
+
+    def __exit__(self, *exc):
+        self.stop.set()
+        if self.nvml:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rx:
+            return None
+        return {"rx_h2d_gbs_median": round(statistics.median(self.rx), 2), "rx_h2d_gbs_max": round(max(self.rx), 2),
+                "tx_d2h_gbs_median": round(statistics.median(self.tx), 2), "samples": len(self.rx),
+                "source": "NVML nvmlDeviceGetPcieThroughput (device PCIe counters, 20 ms windows) during the "
+                          "timed region"}
+
+
 # ------------------------------------------------------------------------------ native arm
 def measure_link_gbs(torch, device, src_device=None):
     """Best of 10 1 GiB copies into `device`: from pinned host memory, or from `src_device`'s HBM
@@ -424,7 +471,7 @@ def run_native(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize(device)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clocks:
+    with ClockSampler(local_rank) as clocks, PcieSampler(local_rank) as pcie:
         ev0.record()
         run_steps(inputs[:args.steps], per_step=args.per_step)
         ev1.record()
@@ -672,6 +719,7 @@ def run_native(args, rank, world, local_rank):
             "instrumented_ms_per_step": round(instrumented_ms, 4),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(),
+            "pcie_counters": pcie.summary(),
             "setup_s": {"alloc_and_pin": round(t_alloc, 1), "prefill": round(t_prefill, 1)},
         }
         print(json.dumps(line), flush=True)
