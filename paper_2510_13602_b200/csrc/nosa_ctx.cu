@@ -451,6 +451,11 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
     ALLOC(dv.kc16, LBH * dv.NB * dv.D);
     ALLOC(dv.kc_err, LBH * dv.NB);
     ALLOC(dv.qsum_buf, LBH * dv.D);
+    dv.split_scan = getenv("NOSA_FUSED_SCAN") ? 0 : 1;
+    if (dv.split_scan) {
+      ALLOC(dv.scr_lo, LBH * dv.NB);
+      ALLOC(dv.scr_up, LBH * dv.NB);
+    }
   }
   ALLOC(dv.plan_fetch, LBH * dv.C);
   ALLOC(dv.plan_evict, LBH * dv.C);
@@ -703,6 +708,9 @@ extern "C" int nosa_start_run(NosaCtx* ctx, int seq_begin, int seq_count, void* 
   return NOSA_OK;
 }
 
+// kernels one selection launch issues: the screen scan (split, Dev::split_scan) + select_plan
+static int sel_kernels(const Dev& dv) { return dv.screen && dv.split_scan ? 2 : 1; }
+
 // K1+K2 for one layer: fused per-(sequence, head) select+plan, or select then the ordered
 // shared-pool planner (NOSA_RESIDENCY_SHARED)
 static cudaError_t plan_layer(NosaCtx* ctx, int layer, const void* q, int selector, cudaStream_t st,
@@ -725,7 +733,7 @@ extern "C" int nosa_select_plan(NosaCtx* ctx, int layer, const void* q, int sele
   cudaSetDevice(ctx->device);
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->dv.cnt + nosa::kCntStride * layer, 0, nosa::kCntStride * sizeof(int), S(stream)));
   CUDA_TRY(ctx, plan_layer(ctx, layer, q, selector, S(stream)));
-  ctx->launches += ctx->dv.shared ? 2 : 1;
+  ctx->launches += sel_kernels(ctx->dv) + (ctx->dv.shared ? 1 : 0);
   return NOSA_OK;
 }
 
@@ -735,7 +743,7 @@ extern "C" int nosa_select(NosaCtx* ctx, int layer, const void* q, int selector,
   if (selector != 0 && selector != 1) return fail(ctx, NOSA_ERR_VALUE, "selector must be nosa or infllmv2");
   cudaSetDevice(ctx->device);
   CUDA_TRY(ctx, nosa::launch_select_plan(ctx->dv, layer, q, selector, 0, nullptr, nullptr, S(stream)));
-  ctx->launches += 1;
+  ctx->launches += sel_kernels(ctx->dv);
   return NOSA_OK;
 }
 
@@ -1296,7 +1304,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->ev_fin[dv.L - 1], 0));
   // kernels of this step: selections (grouped, per layer, or per layer + shared planner),
   // gathers (device movers), attention batches, finalizes, input staging (counted inline)
-  const int n_sel = grouped ? (int)groups.size() : (dv.shared ? 2 : 1) * dv.L;
+  const int n_sel = grouped ? (int)groups.size() * sel_kernels(dv) : (sel_kernels(dv) + (dv.shared ? 1 : 0)) * dv.L;
   ctx->step_kernels = n_sel + n_gather_kernels + ctx->memcpy_born_launches + 2 * n_att + n_proj;  // one finalize per attention batch
   if (count) ctx->launches += ctx->step_kernels;
   return NOSA_OK;

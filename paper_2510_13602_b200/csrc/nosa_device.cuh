@@ -69,6 +69,10 @@ struct Dev {
   __nv_bfloat16* kc16;           // [lbh][NB][D] bf16(K_c) of the frozen pool (built at start_run)
   float* kc_err;                 // [lbh][NB] sum_i |K_c - bf16(K_c)| of each pool row (rounded up)
   double* qsum_buf;              // [lbh][D] the step's q_sum (parity readback recomputes s_q)
+  int split_scan;                // 1: the screen scan is its own bandwidth-bound kernel ahead of
+                                 // the selection/planning kernel (default), 0: fused in select_plan
+  unsigned* scr_lo;              // [lbh][NB] screened lower bound of each pool row (monotone key)
+  float* scr_up;                 // [lbh][NB] screened upper bound
   int* plan_fetch;               // [lbh][C]
   int* plan_evict;               // [lbh][C]
   int* plan_n;                   // [lbh][3] n_fetch, n_evict, n_hit

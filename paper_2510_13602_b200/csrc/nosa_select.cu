@@ -145,26 +145,28 @@ __device__ __forceinline__ double row_dot64(const double* __restrict__ row, cons
 // (radix select); a row with up < T has m rows strictly above it, so only rows with up >= T
 // are candidates, rescored in f64 and ranked by (score desc, index asc) = argtopk's order.
 // Sets the picked bits in sm.bm_q.  bf16 rows are 4x fewer bytes than the f64 scan.
-__device__ void screened_topk(const Dev& dv, int lbh, int pool_lo, int P, int m, SelSmem& sm) {
+// (a) screen of pool rows [pb, pe): a half-warp per row (16 lanes x D/16 dims: one 16-byte load
+//     per lane at D=128), 16 rows per warp iteration with every load issued first, then a
+//     reduce-scatter over the 16 lanes leaves row u's dot and abs-dot on lane 2*u' (u' =
+//     bit-reversed position).  Writes each row's interval [lo, up] (lo as a monotone key) to
+//     lo_out / up_out (shared memory when fused, the global scratch when split).
+__device__ __forceinline__ void screen_rows(const Dev& dv, int lbh, int pool_lo, int pb, int pe, const double* qsum,
+                                            float qmax, unsigned* lo_out, float* up_out) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int D = dv.D;
   const __nv_bfloat16* k16 = dv.kc16 + ((size_t)lbh * dv.NB + pool_lo) * D;
   const float* kerr = dv.kc_err + (size_t)lbh * dv.NB + pool_lo;
-  const float qmax = __int_as_float(sm.misc[M_QMAX]);
   const float gam = (float)(D + 8) * 5.9604645e-08f + 1.1920929e-07f;  // (D+8) 2^-24 + 2^-23 (+ f64 slack)
-  // (a) screen: a half-warp per row (16 lanes x D/16 dims: one 16-byte load per lane at D=128),
-  //     16 rows per warp iteration with every load issued first, then a reduce-scatter over the
-  //     16 lanes leaves row u's dot and abs-dot on lane 2*u' (u' = bit-reversed position)
   const int E = D / 16;  // dims per lane: 8 (D=128) or 4 (D=64)
   const int hl = lane & 15, half = lane >> 4;
   float qf[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) qf[j] = j < E ? (float)sm.qsum[hl * E + j] : 0.0f;
-  for (int p0 = warp * 16; p0 < P; p0 += nwarps * 16) {
+  for (int j = 0; j < 8; ++j) qf[j] = j < E ? (float)qsum[hl * E + j] : 0.0f;
+  for (int p0 = pb + warp * 16; p0 < pe; p0 += nwarps * 16) {
     uint4 raw[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const __nv_bfloat16* row = k16 + (size_t)min(p0 + 2 * u + half, P - 1) * D + hl * E;
+      const __nv_bfloat16* row = k16 + (size_t)min(p0 + 2 * u + half, pe - 1) * D + hl * E;
       if (E == 8) {
         raw[u] = __ldg(reinterpret_cast<const uint4*>(row));
       } else {
@@ -212,12 +214,27 @@ __device__ void screened_topk(const Dev& dv, int lbh, int pool_lo, int P, int m,
     av[0] += __shfl_xor_sync(0xffffffffu, av[0], 1);
     const int u = (b3 ? 4 : 0) + (b2 ? 2 : 0) + (b1 ? 1 : 0);
     const int p = p0 + 2 * u + half;
-    if (!(hl & 1) && p < P) {
+    if (!(hl & 1) && p < pe) {
       const float s_ = sv[0], a_ = av[0];
       const float bound = (gam * a_ + __ldg(kerr + p) * qmax) * 1.001f + fabsf(s_) * 2.4e-7f + 1e-30f;
-      sm.lo_key[p] = f2key(__fsub_rd(s_, bound));
-      sm.up[p] = __fadd_ru(s_, bound);
+      lo_out[p] = f2key(__fsub_rd(s_, bound));
+      up_out[p] = __fadd_ru(s_, bound);
     }
+  }
+}
+
+__device__ void screened_topk(const Dev& dv, int lbh, int pool_lo, int P, int m, SelSmem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int D = dv.D;
+  if (dv.split_scan) {  // the intervals come from screen_scan_kernel (same stream, earlier)
+    const unsigned* lo = dv.scr_lo + (size_t)lbh * dv.NB;
+    const float* up = dv.scr_up + (size_t)lbh * dv.NB;
+    for (int p = tid; p < P; p += blockDim.x) {
+      sm.lo_key[p] = __ldcg(lo + p);
+      sm.up[p] = __ldcg(up + p);
+    }
+  } else {
+    screen_rows(dv, lbh, pool_lo, 0, P, sm.qsum, __int_as_float(sm.misc[M_QMAX]), sm.lo_key, sm.up);
   }
   __syncthreads();
   sel_mark(sm, 2);
@@ -337,10 +354,13 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
   const int r_begin = max(recent_lo, a_end);
   const int Pp = next_pow2(P);
 
-  // (1) q_sum = sum of the group's query heads (decode.py:171-172), f64
+  // (1) q_sum = sum of the group's query heads (decode.py:171-172), f64 (split scan: the scan
+  //     kernel computed and stored it)
   if (tid == 0) sm.misc[M_QMAX] = 0;
   __syncthreads();
-  for (int i = tid; i < D; i += blockDim.x) {
+  if (dv.screen && dv.split_scan) {
+    for (int i = tid; i < D; i += blockDim.x) sm.qsum[i] = __ldcg(dv.qsum_buf + (size_t)lbh * D + i);
+  } else for (int i = tid; i < D; i += blockDim.x) {
     double acc = 0.0;
     for (int g = 0; g < dv.G; ++g) acc += to_f64(q[((size_t)b * dv.Hq + h * dv.G + g) * D + i]);
     sm.qsum[i] = acc;
@@ -695,6 +715,41 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
       }
     }
   }
+}
+
+// Screen scan as its own kernel (Dev::split_scan): grid = (row chunks of 128, B*H, layers), 256
+// threads.  Every CTA sums its unit's query group (the same f64 order as select_phase) and
+// screens 128 pool rows into the global interval scratch; chunk 0 also stores q_sum for the
+// f64 rescoring.  Purely bandwidth-bound (the bf16 K_c rows are the bytes), so it streams at
+// full occupancy instead of alternating with the selection's latency-bound phases.
+template <typename T>
+__global__ void __launch_bounds__(256) screen_scan_kernel(Dev dv, int layer0, const T* __restrict__ q0,
+                                                          size_t q_layer_stride) {
+  __shared__ double qs[128];
+  __shared__ int qmax_bits;
+  const int layer = layer0 + blockIdx.z;
+  const T* q = q0 + blockIdx.z * q_layer_stride;
+  const int bh = blockIdx.y, b = bh / dv.H, h = bh % dv.H;
+  const int lbh = (layer * dv.B + b) * dv.H + h;
+  const int D = dv.D, tid = threadIdx.x;
+  const int t0 = dv.t0[lbh];
+  const int recent_start = max(0, t0 - dv.n_w + 1);           // selection.py:49
+  const int pool_lo = dv.n_sink;                              // selection.py:59
+  const int P = max(pool_lo, recent_start / dv.n_b) - pool_lo;
+  const int pb = blockIdx.x * 128;
+  if (pb >= max(P, 1)) return;  // (chunk 0 always runs: it stores q_sum)
+  if (tid == 0) qmax_bits = 0;
+  __syncthreads();
+  for (int i = tid; i < D; i += blockDim.x) {
+    double acc = 0.0;
+    for (int g = 0; g < dv.G; ++g) acc += to_f64(q[((size_t)b * dv.Hq + h * dv.G + g) * D + i]);
+    qs[i] = acc;
+    atomicMax(&qmax_bits, __float_as_int(__double2float_ru(fabs(acc))));  // |q| bits order as ints
+    if (blockIdx.x == 0) dv.qsum_buf[(size_t)lbh * D + i] = acc;
+  }
+  __syncthreads();
+  screen_rows(dv, lbh, pool_lo, pb, min(pb + 128, P), qs, __int_as_float(qmax_bits),
+              dv.scr_lo + (size_t)lbh * dv.NB, dv.scr_up + (size_t)lbh * dv.NB);
 }
 
 // grid = (B*H, layers), block = 256: layer = layer0 + blockIdx.y with its queries at
@@ -1080,6 +1135,13 @@ cudaError_t launch_select_plan(const Dev& dv, int layer, const void* q, int sele
   const size_t smem = sel_smem_bytes(dv.D, Pp, dv.C);
   const size_t qs = (size_t)dv.B * dv.Hq * dv.D;  // elements per layer of q
   const dim3 grid(dv.B * dv.H, layers);
+  if (mode != 2 && dv.screen && dv.split_scan) {
+    const dim3 sgrid((dv.NB + 127) / 128, dv.B * dv.H, layers);
+    if (dv.dtype == 0)
+      screen_scan_kernel<__nv_bfloat16><<<sgrid, 256, 0, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(q), qs);
+    else
+      screen_scan_kernel<float><<<sgrid, 256, 0, st>>>(dv, layer, static_cast<const float*>(q), qs);
+  }
   if (dv.dtype == 0) {
     auto k = select_plan_kernel<__nv_bfloat16>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
