@@ -223,10 +223,11 @@ __device__ __forceinline__ void screen_rows(const Dev& dv, int lbh, int pool_lo,
   }
 }
 
+template <bool SPLIT>
 __device__ void screened_topk(const Dev& dv, int lbh, int pool_lo, int P, int m, SelSmem& sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int D = dv.D;
-  if (dv.split_scan) {  // the intervals come from screen_scan_kernel (same stream, earlier)
+  if (SPLIT) {  // the intervals come from screen_scan_kernel (same stream, earlier)
     const unsigned* lo = dv.scr_lo + (size_t)lbh * dv.NB;
     const float* up = dv.scr_up + (size_t)lbh * dv.NB;
     for (int p = tid; p < P; p += blockDim.x) {
@@ -337,7 +338,7 @@ __device__ void screened_topk(const Dev& dv, int lbh, int pool_lo, int P, int m,
 
 // ------------------------------------------------------------------------------------------
 // Selection phase: fills sm.req[0..n_req) (sorted) and the selection buffers.
-template <typename T>
+template <typename T, bool SPLIT>
 __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __restrict__ q,
                              int selector, SelSmem& sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
@@ -358,7 +359,7 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
   //     kernel computed and stored it)
   if (tid == 0) sm.misc[M_QMAX] = 0;
   __syncthreads();
-  if (dv.screen && dv.split_scan) {
+  if (SPLIT) {
     for (int i = tid; i < D; i += blockDim.x) sm.qsum[i] = __ldcg(dv.qsum_buf + (size_t)lbh * D + i);
   } else for (int i = tid; i < D; i += blockDim.x) {
     double acc = 0.0;
@@ -382,7 +383,7 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
       for (int p = tid; p < P; p += blockDim.x) atomicOr(&sm.bm_q[p >> 5], 1u << (p & 31));
       __syncthreads();
     } else if (m_q_eff > 0) {
-      screened_topk(dv, lbh, pool_lo, P, m_q_eff, sm);
+      screened_topk<SPLIT>(dv, lbh, pool_lo, P, m_q_eff, sm);
     }
   } else {
 
@@ -754,8 +755,13 @@ __global__ void __launch_bounds__(256) screen_scan_kernel(Dev dv, int layer0, co
 
 // grid = (B*H, layers), block = 256: layer = layer0 + blockIdx.y with its queries at
 // q + blockIdx.y * q_layer_stride.  mode: 0 = select only, 1 = select + plan, 2 = plan on ext_req.
-template <typename T>
-__global__ void __launch_bounds__(256, 4)  // 4 CTAs per SM: one CTA's scan overlaps another's sort/plan
+// SPLIT: the screen scan ran as screen_scan_kernel (no scan code here: fewer registers, more CTAs
+// per SM); otherwise 4 CTAs per SM so that one CTA's scan overlaps another's sort/plan.
+#ifndef SEL_SPLIT_CTAS
+#define SEL_SPLIT_CTAS 5
+#endif
+template <typename T, bool SPLIT>
+__global__ void __launch_bounds__(256, SPLIT ? SEL_SPLIT_CTAS : 4)
     select_plan_kernel(Dev dv, int layer0, const T* __restrict__ q0, size_t q_layer_stride, int selector,
                        int mode, const int* __restrict__ ext_req, const int* __restrict__ ext_nreq) {
   extern __shared__ __align__(16) char smem_raw[];
@@ -779,7 +785,7 @@ __global__ void __launch_bounds__(256, 4)  // 4 CTAs per SM: one CTA's scan over
     for (int i = threadIdx.x; i < min(n, dv.C); i += blockDim.x) sm.req[i] = ext_req[(size_t)bh * dv.C + i];
     __syncthreads();
   } else {
-    select_phase<T>(dv, layer, b, h, q, selector, sm);
+    select_phase<T, SPLIT>(dv, layer, b, h, q, selector, sm);
   }
   if (mode == 0) {
     if (threadIdx.x == 0) dv.n_req[lbh] = min(sm.misc[M_NREQ], dv.C);
@@ -1135,7 +1141,8 @@ cudaError_t launch_select_plan(const Dev& dv, int layer, const void* q, int sele
   const size_t smem = sel_smem_bytes(dv.D, Pp, dv.C);
   const size_t qs = (size_t)dv.B * dv.Hq * dv.D;  // elements per layer of q
   const dim3 grid(dv.B * dv.H, layers);
-  if (mode != 2 && dv.screen && dv.split_scan) {
+  const bool split = dv.screen && dv.split_scan;  // (mode 2 plans only: the selection code never runs)
+  if (mode != 2 && split) {
     const dim3 sgrid((dv.NB + 127) / 128, dv.B * dv.H, layers);
     if (dv.dtype == 0)
       screen_scan_kernel<__nv_bfloat16><<<sgrid, 256, 0, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(q), qs);
@@ -1143,13 +1150,13 @@ cudaError_t launch_select_plan(const Dev& dv, int layer, const void* q, int sele
       screen_scan_kernel<float><<<sgrid, 256, 0, st>>>(dv, layer, static_cast<const float*>(q), qs);
   }
   if (dv.dtype == 0) {
-    auto k = select_plan_kernel<__nv_bfloat16>;
+    auto k = split ? select_plan_kernel<__nv_bfloat16, true> : select_plan_kernel<__nv_bfloat16, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     max_shared_carveout(k);
     k<<<grid, 256, smem, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(q), qs, selector, mode, ext_req,
                                ext_nreq);
   } else {
-    auto k = select_plan_kernel<float>;
+    auto k = split ? select_plan_kernel<float, true> : select_plan_kernel<float, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     max_shared_carveout(k);
     k<<<grid, 256, smem, st>>>(dv, layer, static_cast<const float*>(q), qs, selector, mode, ext_req, ext_nreq);
