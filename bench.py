@@ -348,14 +348,9 @@ def run_native(args, rank, world, local_rank):
     torch.cuda.set_device(device)
     from paper_2510_13602_b200.dist import bind_to_gpu_numa_node
     numa_node = bind_to_gpu_numa_node(local_rank)  # before the pinned slow tier is allocated
-    try:  # the copy-engine mover keeps the host thread in step with the GPU: favour it over noise
-        os.nice(-10)
-    except OSError:
-        pass
     w = workload_dims(args, world)
-    if args.gather == "auto":  # measured: the copy engine moves offloaded misses fastest over PCIe;
-        # from a peer's HBM the SM gather is 30x faster than device-to-device copy-engine batches
-        args.gather = "uva" if (w["cache"] == "resident" or args.slow_tier == "peer") else "memcpy"
+    if args.gather == "auto":  # the device-driven SM gather: the whole step replays as one CUDA graph
+        args.gather = "uva"
     cfg = attention_config(w["shape"])
     L, B, ctx_len, seq0 = w["layers"], w["batch_local"], w["context"], w["seq0"]
     max_tokens, nblk, fast = token_budget(args, w)
@@ -644,7 +639,7 @@ def run_native(args, rank, world, local_rank):
     step_ms = ms_max / args.steps
     g = kern["gather"]
     gather_name = {"uva": "gather_kernel (K3, UVA zero-copy SM loads)", "tma": "gather_tma_kernel (K3, TMA bulk)",
-                   "memcpy": "cudaMemcpyBatchAsync (K3, copy engine)"}[args.gather]
+                   "memcpy": "cudaMemcpyAsync per block (K3, copy engine)"}[args.gather]
     link_roofline = {"bound": "pcie-h2d" if peer_dev is None else "peer-hbm", "kernel": gather_name,
                      "achieved": round(g["gbs"], 2) if g["gbs"] else 0.0, "peak": round(link_gbs, 2), "unit": "GB/s",
                      "frac": round(g["gbs"] / link_gbs, 4) if g["gbs"] else 0.0,

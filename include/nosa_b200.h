@@ -56,7 +56,7 @@ extern "C" {
 #define NOSA_DTYPE_FP32 1
 
 #define NOSA_GATHER_UVA 0     /* zero-copy SM gather kernel over mapped pinned memory     */
-#define NOSA_GATHER_MEMCPY 1  /* copy-engine path: host-planned cudaMemcpyBatchAsync        */
+#define NOSA_GATHER_MEMCPY 1  /* copy-engine path: host-planned, one cudaMemcpyAsync a block */
 #define NOSA_GATHER_TMA 2     /* TMA bulk copies pinned host -> shared -> HBM slot         */
 
 /* AttentionConfig (config.py:15-36) plus the engine extents of one GPU. */

@@ -90,13 +90,10 @@ struct NosaCtx {
   int* h_cnt = nullptr;
   int4* h_list = nullptr;
   std::vector<void*> b_dst, b_src;
-  std::vector<size_t> b_size;
-  long long batch_fallbacks = 0;
   // exported copy lists (Dev::x_*): mapped pinned host arrays the planner fills on the device
   void** h_xsrc = nullptr;
   void** h_xdst = nullptr;
   int* h_xcnt = nullptr;
-  std::vector<size_t> x_sizes;
   // host-buffer step (nosa_decode_step_host): device staging of the step's inputs and outputs,
   // per-layer input-arrival / output-ready events, and the device->host stream
   cudaStream_t d2h_stream = nullptr, in_stream = nullptr;
@@ -762,9 +759,9 @@ extern "C" int nosa_cache_plan(NosaCtx* ctx, int layer, const int32_t* req, cons
 }
 
 // Copy-engine mover: once the layer's plan (recorded as `plan_done`) has executed, the host
-// reads the miss list back through pinned memory and submits every 32 KiB block copy as one
-// cudaMemcpyBatchAsync on `copy_st`.  Costs one host wait per layer; frees the SMs and L2
-// request queues that the zero-copy gather kernel occupies.
+// reads the miss list back through pinned memory and submits one cudaMemcpyAsync per 32 KiB
+// block on `copy_st`.  Costs one host wait per layer and one API call per block (host-bound at
+// ~2 us a call: an experiment path, the device movers are the default).
 static int gather_memcpy(NosaCtx* ctx, int layer, cudaEvent_t plan_done, cudaStream_t copy_st, bool timed) {
   const Dev& dv = ctx->dv;
   if (!ctx->h_list) {
@@ -794,28 +791,14 @@ static int gather_memcpy(NosaCtx* ctx, int layer, cudaEvent_t plan_done, cudaStr
     ctx->b_dst[nc] = dv.pool + ((size_t)m.x * dv.C + m.z) * dv.bpb;
     ++nc;
   }
-  ctx->b_size.assign(nc, (size_t)dv.bpb);
   TimeScope ts(ctx, copy_st, 1, timed);
   if (n_born) {
     CUDA_TRY(ctx, nosa::launch_born(dv, layer, copy_st, std::min(n_born, ctx->num_sms)));
     ctx->memcpy_born_launches += 1;
   }
   if (nc == 0) return NOSA_OK;
-  cudaMemcpyAttributes attr{};
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.srcLocHint.type = ctx->mirror_device >= 0 ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
-  attr.srcLocHint.id = ctx->mirror_device >= 0 ? ctx->mirror_device : 0;
-  attr.dstLocHint.type = cudaMemLocationTypeDevice;
-  attr.dstLocHint.id = ctx->device;
-  size_t idx0 = 0, fail_idx = 0;
-  cudaError_t e = cudaMemcpyBatchAsync(ctx->b_dst.data(), ctx->b_src.data(), ctx->b_size.data(), nc, &attr, &idx0, 1,
-                                       &fail_idx, copy_st);
-  if (e != cudaSuccess) {  // driver without batched copies: one call per block
-    cudaGetLastError();
-    ctx->batch_fallbacks += 1;
-    for (int i = 0; i < nc; ++i)
-      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b_dst[i], ctx->b_src[i], ctx->b_size[i], cudaMemcpyDefault, copy_st));
-  }
+  for (int i = 0; i < nc; ++i)
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->b_dst[i], ctx->b_src[i], (size_t)dv.bpb, cudaMemcpyDefault, copy_st));
   return NOSA_OK;
 }
 
@@ -831,14 +814,13 @@ static int ensure_export(NosaCtx* ctx) {
   CUDA_TRY(ctx, cudaHostGetDevicePointer(reinterpret_cast<void**>(&dv.x_dst), ctx->h_xdst, 0));
   CUDA_TRY(ctx, cudaHostGetDevicePointer(reinterpret_cast<void**>(&dv.x_cnt), ctx->h_xcnt, 0));
   dv.x_src_base = ctx->host_mirror;  // the address the copy engine reads (host or peer HBM)
-  ctx->x_sizes.assign(cap, (size_t)dv.bpb);
   return NOSA_OK;
 }
 
 // Copy-engine mover inside a step: the layer's planner already wrote the copy list and its
 // counts into mapped host memory (select_plan_kernel with Dev::x_on), so once the plan has
-// executed (an event query: no device round trip, no copy) the host submits the whole list as
-// one cudaMemcpyBatchAsync.  Blocks born by the last append are rebuilt on the device.
+// executed (an event query: no device round trip, no copy) the host submits the list, one
+// cudaMemcpyAsync per block.  Blocks born by the last append are rebuilt on the device.
 static int gather_exported(NosaCtx* ctx, int layer, cudaStream_t copy_st, bool timed) {
   const Dev& dv = ctx->dv;
   cudaError_t e;
@@ -859,20 +841,8 @@ static int gather_exported(NosaCtx* ctx, int layer, cudaStream_t copy_st, bool t
   const size_t cap = (size_t)dv.B * dv.H * dv.C;
   void** dst = ctx->h_xdst + layer * cap;
   void** src = ctx->h_xsrc + layer * cap;
-  cudaMemcpyAttributes attr{};
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.srcLocHint.type = ctx->mirror_device >= 0 ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
-  attr.srcLocHint.id = ctx->mirror_device >= 0 ? ctx->mirror_device : 0;
-  attr.dstLocHint.type = cudaMemLocationTypeDevice;
-  attr.dstLocHint.id = ctx->device;
-  size_t idx0 = 0, fail_idx = 0;
-  e = cudaMemcpyBatchAsync(dst, src, ctx->x_sizes.data(), n, &attr, &idx0, 1, &fail_idx, copy_st);
-  if (e != cudaSuccess) {  // driver without batched copies: one call per block
-    cudaGetLastError();
-    ctx->batch_fallbacks += 1;
-    for (int i = 0; i < n; ++i)
-      CUDA_TRY(ctx, cudaMemcpyAsync(dst[i], src[i], (size_t)dv.bpb, cudaMemcpyDefault, copy_st));
-  }
+  for (int i = 0; i < n; ++i)
+    CUDA_TRY(ctx, cudaMemcpyAsync(dst[i], src[i], (size_t)dv.bpb, cudaMemcpyDefault, copy_st));
   return NOSA_OK;
 }
 

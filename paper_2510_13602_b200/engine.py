@@ -235,14 +235,10 @@ class NosaEngine:
             raise ValueError("head cache capacity exhausted")
 
     def _mover(self, gather: str, graph: bool = False) -> str:
-        """"auto": the copy engine (host-planned batches) when blocks live in pinned host memory
-        and some do not fit in HBM; the SM gather when every block is resident or the slow tier
-        is a GPU's HBM (measured: DESIGN.md §5), and for graph capture, which needs a
-        device-driven mover."""
-        if gather != "auto":
-            return gather
-        offloaded = self.fast_slots < self.max_blocks and self.slow_tier == "host"
-        return "memcpy" if offloaded and not graph else "uva"
+        """"auto": the SM zero-copy gather (`uva`), device-driven and graph-capturable, for every
+        tier.  `memcpy` (one host-submitted copy-engine copy per block, host-bound) and `tma`
+        stay selectable for experiments."""
+        return "uva" if gather == "auto" else gather
 
     def step(self, q, k_new, v_new, selector: str = "nosa", out: torch.Tensor | None = None,
              gather: str = "auto", check: bool = True, schedule: str = "pipelined") -> torch.Tensor:

@@ -1,7 +1,7 @@
 // link_probe.cu — PCIe H2D probe for the miss-gather design (not product code).
-// Measures, on pinned host memory: one large copy, batched scattered copies of several chunk
-// sizes on one and two copy streams, the SM zero-copy gather at several grid sizes, and the copy
-// engine + SM gather concurrently.  Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a
+// Measures, on pinned host memory: one large copy, scattered copies of several chunk sizes (one
+// cudaMemcpyAsync each, one and two copy streams), the SM zero-copy gather at several grid sizes,
+// and the copy engine + SM gather concurrently.  Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a
 // tools/link_probe.cu -o gpurun_out/link_probe
 #include <cuda_runtime.h>
 
@@ -75,76 +75,32 @@ int main() {
   timeit([&] { CK(cudaMemcpyAsync(d, h, 1ull << 30, cudaMemcpyHostToDevice, s1)); }, 1ull << 30, "single 1 GiB memcpy");
   // scattered chunk lists
   std::mt19937_64 rng(1);
-  cudaMemcpyAttributes attr{};
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.srcLocHint.type = cudaMemLocationTypeHost;
-  attr.dstLocHint.type = cudaMemLocationTypeDevice;
-  attr.dstLocHint.id = 0;
   const size_t total = 512ull << 20;
   for (size_t chunk : {32768ul, 65536ul, 131072ul, 262144ul}) {
     const int n = (int)(total / chunk);
     std::vector<void*> dst(n), src(n);
-    std::vector<size_t> sz(n, chunk);
     for (int i = 0; i < n; ++i) {
       src[i] = h + (rng() % (host_bytes / chunk)) * chunk;
       dst[i] = d + (rng() % (dev_bytes / chunk)) * chunk;
     }
-    for (int per : {256, 1024, n}) {
-      char name[128];
-      snprintf(name, sizeof name, "batch %zuK chunks, %d per batch, 1 stream", chunk >> 10, per);
-      timeit(
-          [&] {
-            for (int i0 = 0; i0 < n; i0 += per) {
-              size_t idx = 0, fi = 0;
-              CK(cudaMemcpyBatchAsync(dst.data() + i0, src.data() + i0, sz.data() + i0, std::min(per, n - i0), &attr,
-                                      &idx, 1, &fi, s1));
-            }
-          },
-          total, name);
-    }
-    {
-      char name[128];
-      snprintf(name, sizeof name, "batch %zuK chunks, 512 per batch, 2 streams", chunk >> 10);
-      timeit(
-          [&] {
-            CK(cudaEventRecord(a, s1));
-            CK(cudaStreamWaitEvent(s2, a, 0));
-            for (int i0 = 0, k = 0; i0 < n; i0 += 512, ++k) {
-              size_t idx = 0, fi = 0;
-              CK(cudaMemcpyBatchAsync(dst.data() + i0, src.data() + i0, sz.data() + i0, std::min(512, n - i0), &attr,
-                                      &idx, 1, &fi, (k & 1) ? s2 : s1));
-            }
-            cudaEvent_t j;
-            CK(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
-            CK(cudaEventRecord(j, s2));
-            CK(cudaStreamWaitEvent(s1, j, 0));
-            CK(cudaEventDestroy(j));
-          },
-          total, name);
-    }
+    char name[128];
+    snprintf(name, sizeof name, "%zuK chunks, one cudaMemcpyAsync each, 1 stream", chunk >> 10);
+    timeit([&] { for (int i = 0; i < n; ++i) CK(cudaMemcpyAsync(dst[i], src[i], chunk, cudaMemcpyHostToDevice, s1)); },
+           total, name);
+    snprintf(name, sizeof name, "%zuK chunks, one cudaMemcpyAsync each, 2 streams", chunk >> 10);
+    timeit(
+        [&] {
+          CK(cudaEventRecord(a, s1));
+          CK(cudaStreamWaitEvent(s2, a, 0));
+          for (int i = 0; i < n; ++i) CK(cudaMemcpyAsync(dst[i], src[i], chunk, cudaMemcpyHostToDevice, (i & 1) ? s2 : s1));
+          cudaEvent_t j;
+          CK(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
+          CK(cudaEventRecord(j, s2));
+          CK(cudaStreamWaitEvent(s1, j, 0));
+          CK(cudaEventDestroy(j));
+        },
+        total, name);
     if (chunk == 32768) {
-      // per-copy cudaMemcpyAsync
-      timeit(
-          [&] {
-            for (int i = 0; i < n; ++i) CK(cudaMemcpyAsync(dst[i], src[i], chunk, cudaMemcpyHostToDevice, s1));
-          },
-          total, "32K chunks, one cudaMemcpyAsync each");
-      // sorted by source address
-      std::vector<int> order(n);
-      for (int i = 0; i < n; ++i) order[i] = i;
-      std::sort(order.begin(), order.end(), [&](int x, int y) { return src[x] < src[y]; });
-      std::vector<void*> ds(n), ss(n);
-      for (int i = 0; i < n; ++i) ds[i] = dst[order[i]], ss[i] = src[order[i]];
-      timeit(
-          [&] {
-            for (int i0 = 0; i0 < n; i0 += 512) {
-              size_t idx = 0, fi = 0;
-              CK(cudaMemcpyBatchAsync(ds.data() + i0, ss.data() + i0, sz.data() + i0, std::min(512, n - i0), &attr, &idx,
-                                      1, &fi, s1));
-            }
-          },
-          total, "batch 32K chunks sorted by host address, 512 per batch");
-      // UVA gather
       std::vector<long long> so(n), doff(n);
       for (int i = 0; i < n; ++i) {
         so[i] = ((char*)src[i] - h) / 16;
@@ -156,24 +112,18 @@ int main() {
       CK(cudaMemcpy(dso, so.data(), n * 8, cudaMemcpyHostToDevice));
       CK(cudaMemcpy(ddo, doff.data(), n * 8, cudaMemcpyHostToDevice));
       for (int grid : {8, 16, 32, 64, 148, 296}) {
-        char name[128];
         snprintf(name, sizeof name, "UVA SM gather 32K chunks, grid %d", grid);
         timeit([&] { uva_gather<<<grid, 256, 0, s1>>>((const int4*)hdev, (int4*)d, dso, ddo, n, 32768 / 16); }, total,
                name);
       }
       for (int frac : {10, 20, 30}) {
         const int nk = n * frac / 100, nc = n - nk;
-        char name[128];
         snprintf(name, sizeof name, "copy engine %d%% + UVA grid 16 %d%% concurrently", 100 - frac, frac);
         timeit(
             [&] {
               CK(cudaEventRecord(a, s1));
               CK(cudaStreamWaitEvent(s2, a, 0));
-              for (int i0 = 0; i0 < nc; i0 += 512) {
-                size_t idx = 0, fi = 0;
-                CK(cudaMemcpyBatchAsync(dst.data() + i0, src.data() + i0, sz.data() + i0, std::min(512, nc - i0), &attr,
-                                        &idx, 1, &fi, s1));
-              }
+              for (int i = 0; i < nc; ++i) CK(cudaMemcpyAsync(dst[i], src[i], chunk, cudaMemcpyHostToDevice, s1));
               uva_gather<<<16, 256, 0, s2>>>((const int4*)hdev, (int4*)d, dso + nc, ddo + nc, nk, 32768 / 16);
               cudaEvent_t j;
               CK(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
@@ -183,6 +133,8 @@ int main() {
             },
             total, name);
       }
+      CK(cudaFree(dso));
+      CK(cudaFree(ddo));
     }
   }
   // D2H concurrently with H2D (full duplex check)
