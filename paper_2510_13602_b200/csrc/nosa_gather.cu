@@ -29,44 +29,49 @@ __device__ __forceinline__ int4 ld_host(const int4* p) {
 
 // Each CTA copies NBLK list entries per iteration: NBLK * bpb / (256 * 16) 16-byte loads per
 // thread are issued before any store, so NBLK * 32 KiB per CTA are in flight on the link.
+// One grid walks the layers [layer0, layer0 + nl) in order, so the SM loads in flight over PCIe
+// do not grow with the layers of an attention batch: zero-copy reads are served through L2, and
+// more than ~8 CTAs of them slow the attention's HBM stream and the link itself (measured,
+// tools/mover_probe.cu: an HBM stream keeps 0.91x of its rate next to 8 CTAs, 0.60x next to 32).
 template <int NBLK, bool L2HINT>
-__global__ void __launch_bounds__(256) gather_kernel(Dev dv, int layer0) {
+__global__ void __launch_bounds__(256) gather_kernel(Dev dv, int layer0, int nl) {
   constexpr int PER = 8;  // 16-byte vectors per thread per 32 KiB block at 256 threads
-  const int layer = layer0 + blockIdx.y;  // grid (CTAs, layers of an attention batch)
-  const int n = *reinterpret_cast<volatile int*>(dv.cnt + kCntStride * layer);
-  const int4* list = dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C;
   const int vecs = (int)(dv.bpb / 16);
-  for (int e0 = blockIdx.x * NBLK; e0 < n; e0 += gridDim.x * NBLK) {
-    int4 m[NBLK];
+  for (int layer = layer0; layer < layer0 + nl; ++layer) {
+    const int n = *reinterpret_cast<volatile int*>(dv.cnt + kCntStride * layer);
+    const int4* list = dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C;
+    for (int e0 = blockIdx.x * NBLK; e0 < n; e0 += gridDim.x * NBLK) {
+      int4 m[NBLK];
 #pragma unroll
-    for (int j = 0; j < NBLK; ++j) m[j] = e0 + j < n ? list[e0 + j] : make_int4(-1, 0, 0, 0);
-    for (int base = threadIdx.x; base < vecs; base += blockDim.x * PER) {
-      int4 v[NBLK][PER];
+      for (int j = 0; j < NBLK; ++j) m[j] = e0 + j < n ? list[e0 + j] : make_int4(-1, 0, 0, 0);
+      for (int base = threadIdx.x; base < vecs; base += blockDim.x * PER) {
+        int4 v[NBLK][PER];
 #pragma unroll
-      for (int j = 0; j < NBLK; ++j) {
-        if (m[j].x < 0 || m[j].w) continue;
-        const int4* src = reinterpret_cast<const int4*>(dv.host + ((size_t)m[j].x * dv.NB + m[j].y) * dv.bpb);
+        for (int j = 0; j < NBLK; ++j) {
+          if (m[j].x < 0 || m[j].w) continue;
+          const int4* src = reinterpret_cast<const int4*>(dv.host + ((size_t)m[j].x * dv.NB + m[j].y) * dv.bpb);
 #pragma unroll
-        for (int u = 0; u < PER; ++u) {
-          const int i = base + u * blockDim.x;
-          if (i < vecs) v[j][u] = ld_host<L2HINT>(src + i);
+          for (int u = 0; u < PER; ++u) {
+            const int i = base + u * blockDim.x;
+            if (i < vecs) v[j][u] = ld_host<L2HINT>(src + i);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < NBLK; ++j) {
+          if (m[j].x < 0 || m[j].w) continue;
+          int4* dst = reinterpret_cast<int4*>(dv.pool + ((size_t)m[j].x * dv.C + m[j].z) * dv.bpb);
+#pragma unroll
+          for (int u = 0; u < PER; ++u) {
+            const int i = base + u * blockDim.x;
+            if (i < vecs) dst[i] = v[j][u];
+          }
         }
       }
 #pragma unroll
-      for (int j = 0; j < NBLK; ++j) {
-        if (m[j].x < 0 || m[j].w) continue;
-        int4* dst = reinterpret_cast<int4*>(dv.pool + ((size_t)m[j].x * dv.C + m[j].z) * dv.bpb);
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-          const int i = base + u * blockDim.x;
-          if (i < vecs) dst[i] = v[j][u];
-        }
-      }
+      for (int j = 0; j < NBLK; ++j)
+        if (m[j].x >= 0 && m[j].w)
+          write_born_block(dv, m[j], reinterpret_cast<int4*>(dv.pool + ((size_t)m[j].x * dv.C + m[j].z) * dv.bpb), vecs);
     }
-#pragma unroll
-    for (int j = 0; j < NBLK; ++j)
-      if (m[j].x >= 0 && m[j].w)
-        write_born_block(dv, m[j], reinterpret_cast<int4*>(dv.pool + ((size_t)m[j].x * dv.C + m[j].z) * dv.bpb), vecs);
   }
 }
 
@@ -84,55 +89,59 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-__global__ void __launch_bounds__(32) gather_tma_kernel(Dev dv, int layer0) {
+__global__ void __launch_bounds__(32) gather_tma_kernel(Dev dv, int layer0, int nl) {
   extern __shared__ __align__(128) char smem_raw[];
-  const int layer = layer0 + blockIdx.y;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kTmaStages * dv.bpb);
-  const int n = *reinterpret_cast<volatile int*>(dv.cnt + kCntStride * layer);
-  const int4* list = dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C;
   const int lane = threadIdx.x;
-  const int m = n > (int)blockIdx.x ? (n - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;  // items of this CTA
   if (lane == 0) {
     for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
   __syncwarp();
-  auto item = [&](int k) { return list[blockIdx.x + (size_t)k * gridDim.x]; };
-  auto issue = [&](int k) {  // host -> stage (born blocks are written directly, see below)
-    const int4 e = item(k);
-    const int s = k % kTmaStages;
-    if (e.w) {
-      mbar_arrive_plain(&bars[s]);
-      return;
-    }
-    mbar_expect_tx(&bars[s], (unsigned)dv.bpb);
-    bulk_g2s(smem_raw + (size_t)s * dv.bpb, dv.host + ((size_t)e.x * dv.NB + e.y) * dv.bpb, (unsigned)dv.bpb, &bars[s]);
-  };
-  if (lane == 0)
-    for (int k = 0; k < min(kTmaStages, m); ++k) issue(k);
-  for (int k = 0; k < m; ++k) {
-    const int s = k % kTmaStages;
-    const int4 e = item(k);
-    char* dst = dv.pool + ((size_t)e.x * dv.C + e.z) * dv.bpb;
-    mbar_wait(&bars[s], (k / kTmaStages) & 1);
-    if (e.w) {  // born at the previous step: row 0 from the device stash, zeros elsewhere
-      const int vecs = (int)(dv.bpb / 16), row_vecs = dv.D * dv.elem / 16, plane_vecs = vecs / 2;
-      const int4* stash = reinterpret_cast<const int4*>(dv.newrow + (size_t)e.x * 2 * dv.D * dv.elem);
-      for (int i = lane; i < vecs; i += 32) {
-        const int which = i / plane_vecs, in_plane = i - which * plane_vecs;
-        reinterpret_cast<int4*>(dst)[i] = in_plane < row_vecs ? stash[which * row_vecs + in_plane] : make_int4(0, 0, 0, 0);
+  int k_base = 0;  // items issued by this CTA in earlier layers: the ring's stage and phase run on
+  for (int layer = layer0; layer < layer0 + nl; ++layer) {
+    const int n = *reinterpret_cast<volatile int*>(dv.cnt + kCntStride * layer);
+    const int4* list = dv.miss_list + (size_t)layer * dv.B * dv.H * dv.C;
+    const int m = n > (int)blockIdx.x ? (n - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;  // items of this CTA
+    auto item = [&](int k) { return list[blockIdx.x + (size_t)k * gridDim.x]; };
+    auto issue = [&](int k) {  // host -> stage (born blocks are written directly, see below)
+      const int4 e = item(k);
+      const int s = (k_base + k) % kTmaStages;
+      if (e.w) {
+        mbar_arrive_plain(&bars[s]);
+        return;
       }
-      __syncwarp();
-    } else if (lane == 0) {
-      bulk_s2g(dst, smem_raw + (size_t)s * dv.bpb, (unsigned)dv.bpb);
-      bulk_commit();
+      mbar_expect_tx(&bars[s], (unsigned)dv.bpb);
+      bulk_g2s(smem_raw + (size_t)s * dv.bpb, dv.host + ((size_t)e.x * dv.NB + e.y) * dv.bpb, (unsigned)dv.bpb, &bars[s]);
+    };
+    if (lane == 0)
+      for (int k = 0; k < min(kTmaStages, m); ++k) issue(k);
+    for (int k = 0; k < m; ++k) {
+      const int s = (k_base + k) % kTmaStages;
+      const int4 e = item(k);
+      char* dst = dv.pool + ((size_t)e.x * dv.C + e.z) * dv.bpb;
+      mbar_wait(&bars[s], ((k_base + k) / kTmaStages) & 1);
+      if (e.w) {  // born at the previous step: row 0 from the device stash, zeros elsewhere
+        const int vecs = (int)(dv.bpb / 16), row_vecs = dv.D * dv.elem / 16, plane_vecs = vecs / 2;
+        const int4* stash = reinterpret_cast<const int4*>(dv.newrow + (size_t)e.x * 2 * dv.D * dv.elem);
+        for (int i = lane; i < vecs; i += 32) {
+          const int which = i / plane_vecs, in_plane = i - which * plane_vecs;
+          reinterpret_cast<int4*>(dst)[i] = in_plane < row_vecs ? stash[which * row_vecs + in_plane] : make_int4(0, 0, 0, 0);
+        }
+        __syncwarp();
+      } else if (lane == 0) {
+        bulk_s2g(dst, smem_raw + (size_t)s * dv.bpb, (unsigned)dv.bpb);
+        bulk_commit();
+      }
+      if (lane == 0 && k + kTmaStages < m) {
+        bulk_wait_read_all();  // the store has finished reading stage s
+        issue(k + kTmaStages);
+      }
     }
-    if (lane == 0 && k + kTmaStages < m) {
-      bulk_wait_read_all();  // the store has finished reading stage s
-      issue(k + kTmaStages);
-    }
+    if (lane == 0) bulk_wait_all();  // the ring is reused by the next layer
+    __syncwarp();
+    k_base += m;
   }
-  if (lane == 0) bulk_wait_all();
 }
 
 // Blocks born by the previous step's append, for the copy-engine mover: the memcpy batch skips
@@ -154,12 +163,12 @@ cudaError_t launch_born(const Dev& dv, int layer, cudaStream_t st, int grid) {
 
 // layers [layer, layer + nl) in one launch
 cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, bool tma, int nl) {
-  const dim3 g(grid, nl);
+  const dim3 g(grid);
   if (tma) {
     const size_t smem = (size_t)kTmaStages * dv.bpb + kTmaStages * 8;
     cudaFuncSetAttribute(gather_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     max_shared_carveout(gather_tma_kernel);
-    gather_tma_kernel<<<g, 32, smem, st>>>(dv, layer);
+    gather_tma_kernel<<<g, 32, smem, st>>>(dv, layer, nl);
   } else {
     // NOSA_GATHER_VARIANT (experiments): bit 0 = two blocks per CTA iteration, bit 1 = L2::256B
     static const int variant = getenv("NOSA_GATHER_VARIANT") ? atoi(getenv("NOSA_GATHER_VARIANT")) : 0;
@@ -168,10 +177,10 @@ cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, b
     max_shared_carveout(gather_kernel<1, true>);
     max_shared_carveout(gather_kernel<2, true>);
     switch (variant & 3) {
-      case 0: gather_kernel<1, false><<<g, 256, 0, st>>>(dv, layer); break;
-      case 1: gather_kernel<2, false><<<g, 256, 0, st>>>(dv, layer); break;
-      case 2: gather_kernel<1, true><<<g, 256, 0, st>>>(dv, layer); break;
-      default: gather_kernel<2, true><<<g, 256, 0, st>>>(dv, layer); break;
+      case 0: gather_kernel<1, false><<<g, 256, 0, st>>>(dv, layer, nl); break;
+      case 1: gather_kernel<2, false><<<g, 256, 0, st>>>(dv, layer, nl); break;
+      case 2: gather_kernel<1, true><<<g, 256, 0, st>>>(dv, layer, nl); break;
+      default: gather_kernel<2, true><<<g, 256, 0, st>>>(dv, layer, nl); break;
     }
   }
   return cudaGetLastError();

@@ -150,76 +150,91 @@ __device__ __forceinline__ double row_dot64(const double* __restrict__ row, cons
 //     reduce-scatter over the 16 lanes leaves row u's dot and abs-dot on lane 2*u' (u' =
 //     bit-reversed position).  Writes each row's interval [lo, up] (lo as a monotone key) to
 //     lo_out / up_out (shared memory when fused, the global scratch when split).
+// loads of one warp iteration of (a): rows p0 + 2u + half, lane hl's 16-byte slice
+__device__ __forceinline__ void screen_load(const __nv_bfloat16* __restrict__ k16, int D, int p0, int pe,
+                                            uint4 (&raw)[8]) {
+  const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4, E = D / 16;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const __nv_bfloat16* row = k16 + (size_t)min(p0 + 2 * u + half, pe - 1) * D + hl * E;
+    if (E == 8) {
+      raw[u] = __ldg(reinterpret_cast<const uint4*>(row));
+    } else {
+      const uint2 r2 = __ldg(reinterpret_cast<const uint2*>(row));
+      raw[u] = make_uint4(r2.x, r2.y, 0u, 0u);
+    }
+  }
+}
+
+// the rest of (a) for one warp iteration: dots, the 16-lane reduce-scatter, the intervals
+__device__ __forceinline__ void screen_finish(const uint4 (&raw)[8], const float (&qf)[8], const float* __restrict__ kerr,
+                                             float gam, float qmax, int p0, int pe, unsigned* lo_out,
+                                             float* up_out) {
+  const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
+  float sv[8], av[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const unsigned w[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
+    float sacc = 0.0f, aacc = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(&w[j]);
+      const float k0 = __low2float(x), k1 = __high2float(x);
+      sacc = fmaf(k1, qf[2 * j + 1], fmaf(k0, qf[2 * j], sacc));
+      aacc = fmaf(fabsf(k1), fabsf(qf[2 * j + 1]), fmaf(fabsf(k0), fabsf(qf[2 * j]), aacc));
+    }
+    sv[u] = sacc;
+    av[u] = aacc;
+  }
+  const bool b3 = hl & 8, b2 = hl & 4, b1 = hl & 2;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float ss = b3 ? sv[i] : sv[i + 4], sk = b3 ? sv[i + 4] : sv[i];
+    const float as = b3 ? av[i] : av[i + 4], ak = b3 ? av[i + 4] : av[i];
+    sv[i] = sk + __shfl_xor_sync(0xffffffffu, ss, 8);
+    av[i] = ak + __shfl_xor_sync(0xffffffffu, as, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float ss = b2 ? sv[i] : sv[i + 2], sk = b2 ? sv[i + 2] : sv[i];
+    const float as = b2 ? av[i] : av[i + 2], ak = b2 ? av[i + 2] : av[i];
+    sv[i] = sk + __shfl_xor_sync(0xffffffffu, ss, 4);
+    av[i] = ak + __shfl_xor_sync(0xffffffffu, as, 4);
+  }
+  {
+    const float ss = b1 ? sv[0] : sv[1], sk = b1 ? sv[1] : sv[0];
+    const float as = b1 ? av[0] : av[1], ak = b1 ? av[1] : av[0];
+    sv[0] = sk + __shfl_xor_sync(0xffffffffu, ss, 2);
+    av[0] = ak + __shfl_xor_sync(0xffffffffu, as, 2);
+  }
+  sv[0] += __shfl_xor_sync(0xffffffffu, sv[0], 1);
+  av[0] += __shfl_xor_sync(0xffffffffu, av[0], 1);
+  const int u = (b3 ? 4 : 0) + (b2 ? 2 : 0) + (b1 ? 1 : 0);
+  const int p = p0 + 2 * u + half;
+  if (!(hl & 1) && p < pe) {
+    const float s_ = sv[0], a_ = av[0];
+    const float bound = (gam * a_ + __ldg(kerr + p) * qmax) * 1.001f + fabsf(s_) * 2.4e-7f + 1e-30f;
+    lo_out[p] = f2key(__fsub_rd(s_, bound));
+    up_out[p] = __fadd_ru(s_, bound);
+  }
+}
+
+// fp32 accumulation bound of the screen dot: (D+8) 2^-24 + 2^-23 (+ f64 slack)
+__device__ __forceinline__ float screen_gamma(int D) { return (float)(D + 8) * 5.9604645e-08f + 1.1920929e-07f; }
+
 __device__ __forceinline__ void screen_rows(const Dev& dv, int lbh, int pool_lo, int pb, int pe, const double* qsum,
                                             float qmax, unsigned* lo_out, float* up_out) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int D = dv.D;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int D = dv.D, E = D / 16, hl = lane & 15;
   const __nv_bfloat16* k16 = dv.kc16 + ((size_t)lbh * dv.NB + pool_lo) * D;
   const float* kerr = dv.kc_err + (size_t)lbh * dv.NB + pool_lo;
-  const float gam = (float)(D + 8) * 5.9604645e-08f + 1.1920929e-07f;  // (D+8) 2^-24 + 2^-23 (+ f64 slack)
-  const int E = D / 16;  // dims per lane: 8 (D=128) or 4 (D=64)
-  const int hl = lane & 15, half = lane >> 4;
   float qf[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) qf[j] = j < E ? (float)qsum[hl * E + j] : 0.0f;
   for (int p0 = pb + warp * 16; p0 < pe; p0 += nwarps * 16) {
     uint4 raw[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const __nv_bfloat16* row = k16 + (size_t)min(p0 + 2 * u + half, pe - 1) * D + hl * E;
-      if (E == 8) {
-        raw[u] = __ldg(reinterpret_cast<const uint4*>(row));
-      } else {
-        const uint2 r2 = __ldg(reinterpret_cast<const uint2*>(row));
-        raw[u] = make_uint4(r2.x, r2.y, 0u, 0u);
-      }
-    }
-    float sv[8], av[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const unsigned w[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
-      float sacc = 0.0f, aacc = 0.0f;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(&w[j]);
-        const float k0 = __low2float(x), k1 = __high2float(x);
-        sacc = fmaf(k1, qf[2 * j + 1], fmaf(k0, qf[2 * j], sacc));
-        aacc = fmaf(fabsf(k1), fabsf(qf[2 * j + 1]), fmaf(fabsf(k0), fabsf(qf[2 * j]), aacc));
-      }
-      sv[u] = sacc;
-      av[u] = aacc;
-    }
-    const bool b3 = hl & 8, b2 = hl & 4, b1 = hl & 2;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float ss = b3 ? sv[i] : sv[i + 4], sk = b3 ? sv[i + 4] : sv[i];
-      const float as = b3 ? av[i] : av[i + 4], ak = b3 ? av[i + 4] : av[i];
-      sv[i] = sk + __shfl_xor_sync(0xffffffffu, ss, 8);
-      av[i] = ak + __shfl_xor_sync(0xffffffffu, as, 8);
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const float ss = b2 ? sv[i] : sv[i + 2], sk = b2 ? sv[i + 2] : sv[i];
-      const float as = b2 ? av[i] : av[i + 2], ak = b2 ? av[i + 2] : av[i];
-      sv[i] = sk + __shfl_xor_sync(0xffffffffu, ss, 4);
-      av[i] = ak + __shfl_xor_sync(0xffffffffu, as, 4);
-    }
-    {
-      const float ss = b1 ? sv[0] : sv[1], sk = b1 ? sv[1] : sv[0];
-      const float as = b1 ? av[0] : av[1], ak = b1 ? av[1] : av[0];
-      sv[0] = sk + __shfl_xor_sync(0xffffffffu, ss, 2);
-      av[0] = ak + __shfl_xor_sync(0xffffffffu, as, 2);
-    }
-    sv[0] += __shfl_xor_sync(0xffffffffu, sv[0], 1);
-    av[0] += __shfl_xor_sync(0xffffffffu, av[0], 1);
-    const int u = (b3 ? 4 : 0) + (b2 ? 2 : 0) + (b1 ? 1 : 0);
-    const int p = p0 + 2 * u + half;
-    if (!(hl & 1) && p < pe) {
-      const float s_ = sv[0], a_ = av[0];
-      const float bound = (gam * a_ + __ldg(kerr + p) * qmax) * 1.001f + fabsf(s_) * 2.4e-7f + 1e-30f;
-      lo_out[p] = f2key(__fsub_rd(s_, bound));
-      up_out[p] = __fadd_ru(s_, bound);
-    }
+    screen_load(k16, D, p0, pe, raw);
+    screen_finish(raw, qf, kerr, screen_gamma(D), qmax, p0, pe, lo_out, up_out);
   }
 }
 
@@ -726,31 +741,56 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
 template <typename T>
 __global__ void __launch_bounds__(256) screen_scan_kernel(Dev dv, int layer0, const T* __restrict__ q0,
                                                           size_t q_layer_stride) {
-  __shared__ double qs[128];
+  __shared__ float qt[128];  // (float) q_sum, transposed [j][hl]: conflict-free qf loads
   __shared__ int qmax_bits;
   const int layer = layer0 + blockIdx.z;
   const T* q = q0 + blockIdx.z * q_layer_stride;
   const int bh = blockIdx.y, b = bh / dv.H, h = bh % dv.H;
   const int lbh = (layer * dv.B + b) * dv.H + h;
-  const int D = dv.D, tid = threadIdx.x;
+  const int D = dv.D, E = D / 16, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int t0 = dv.t0[lbh];
   const int recent_start = max(0, t0 - dv.n_w + 1);           // selection.py:49
   const int pool_lo = dv.n_sink;                              // selection.py:59
   const int P = max(pool_lo, recent_start / dv.n_b) - pool_lo;
-  const int pb = blockIdx.x * 128;
+  const int pb = blockIdx.x * 128, pe = min(pb + 128, P);
   if (pb >= max(P, 1)) return;  // (chunk 0 always runs: it stores q_sum)
+  // the pool rows do not depend on q: their loads are in flight while q_sum is formed
+  const __nv_bfloat16* k16 = dv.kc16 + ((size_t)lbh * dv.NB + pool_lo) * D;
+  const int p0 = pb + warp * 16;
+  uint4 raw[8];
+  if (p0 < pe) screen_load(k16, D, p0, pe, raw);
   if (tid == 0) qmax_bits = 0;
   __syncthreads();
   for (int i = tid; i < D; i += blockDim.x) {
+    const T* qg = q + ((size_t)b * dv.Hq + h * dv.G) * D + i;
+    T v[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) if (g < dv.G) v[g] = qg[(size_t)g * D];
     double acc = 0.0;
-    for (int g = 0; g < dv.G; ++g) acc += to_f64(q[((size_t)b * dv.Hq + h * dv.G + g) * D + i]);
-    qs[i] = acc;
-    atomicMax(&qmax_bits, __float_as_int(__double2float_ru(fabs(acc))));  // |q| bits order as ints
+#pragma unroll
+    for (int g = 0; g < 8; ++g) if (g < dv.G) acc += to_f64(v[g]);  // the order of select_phase
+    for (int g = 8; g < dv.G; ++g) acc += to_f64(qg[(size_t)g * D]);
+    qt[(i % E) * 16 + i / E] = (float)acc;
+    const int bits = __float_as_int(__double2float_ru(fabs(acc)));  // |q| bits order as ints
+    const int wmax = __reduce_max_sync(__activemask(), bits);
+    if ((tid & 31) == __ffs(__activemask()) - 1) atomicMax(&qmax_bits, wmax);
     if (blockIdx.x == 0) dv.qsum_buf[(size_t)lbh * D + i] = acc;
   }
   __syncthreads();
-  screen_rows(dv, lbh, pool_lo, pb, min(pb + 128, P), qs, __int_as_float(qmax_bits),
-              dv.scr_lo + (size_t)lbh * dv.NB, dv.scr_up + (size_t)lbh * dv.NB);
+  if (p0 >= pe) return;
+  const int hl = lane & 15;
+  float qf[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) qf[j] = j < E ? qt[j * 16 + hl] : 0.0f;
+  const float* kerr = dv.kc_err + (size_t)lbh * dv.NB + pool_lo;
+  unsigned* lo = dv.scr_lo + (size_t)lbh * dv.NB;
+  float* up = dv.scr_up + (size_t)lbh * dv.NB;
+  const float qmax = __int_as_float(qmax_bits), gam = screen_gamma(D);
+  screen_finish(raw, qf, kerr, gam, qmax, p0, pe, lo, up);
+  for (int p1 = p0 + nwarps * 16; p1 < pe; p1 += nwarps * 16) {  // (blockDim < 256 only)
+    screen_load(k16, D, p1, pe, raw);
+    screen_finish(raw, qf, kerr, gam, qmax, p1, pe, lo, up);
+  }
 }
 
 // grid = (B*H, layers), block = 256: layer = layer0 + blockIdx.y with its queries at
