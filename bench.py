@@ -84,7 +84,7 @@ def parse():
     ap.add_argument("--layers", type=int, default=None, help="override (for quick local checks only)")
     ap.add_argument("--batch", type=int, default=None, help="override (for quick local checks only)")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--gather", choices=["auto", "uva", "tma", "memcpy"], default="auto",
+    ap.add_argument("--gather", choices=["auto", "uva", "tma", "memcpy", "hostpack", "hybrid"], default="auto",
                     help="auto = copy-engine batches when blocks are offloaded, graph-replayed UVA otherwise")
     ap.add_argument("--schedule", choices=["pipelined", "serial"], default="pipelined")
     ap.add_argument("--burn-in", type=int, default=None,
@@ -437,7 +437,7 @@ def run_native(args, rank, world, local_rank):
     inputs = [stream.next() for _ in range(args.steps * 2 + (0 if args.no_e2e else args.steps + 1))]
     torch.cuda.synchronize(device)
     eng.reset_stats()
-    use_graph = args.gather != "memcpy" and not args.eager
+    use_graph = args.gather not in ("memcpy", "hostpack", "hybrid") and not args.eager
     if use_graph:  # the whole step as one CUDA graph on fixed buffers, fed by D2D copies
         gbufs = tuple(torch.empty_like(x) for x in inputs[0])
         if hidden:
@@ -639,7 +639,9 @@ def run_native(args, rank, world, local_rank):
     step_ms = ms_max / args.steps
     g = kern["gather"]
     gather_name = {"uva": "gather_kernel (K3, UVA zero-copy SM loads)", "tma": "gather_tma_kernel (K3, TMA bulk)",
-                   "memcpy": "cudaMemcpyAsync per block (K3, copy engine)"}[args.gather]
+                   "memcpy": "cudaMemcpyAsync per block (K3, copy engine)",
+                   "hostpack": "host-packed 2 MiB chunks, one DMA each + scatter_kernel (K3, copy engine)",
+                   "hybrid": "host-packed DMAs + gather_kernel (K3, copy engine and SM loads)"}[args.gather]
     link_roofline = {"bound": "pcie-h2d" if peer_dev is None else "peer-hbm", "kernel": gather_name,
                      "achieved": round(g["gbs"], 2) if g["gbs"] else 0.0, "peak": round(link_gbs, 2), "unit": "GB/s",
                      "frac": round(g["gbs"] / link_gbs, 4) if g["gbs"] else 0.0,

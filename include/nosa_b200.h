@@ -58,6 +58,8 @@ extern "C" {
 #define NOSA_GATHER_UVA 0     /* zero-copy SM gather kernel over mapped pinned memory     */
 #define NOSA_GATHER_MEMCPY 1  /* copy-engine path: host-planned, one cudaMemcpyAsync a block */
 #define NOSA_GATHER_TMA 2     /* TMA bulk copies pinned host -> shared -> HBM slot         */
+#define NOSA_GATHER_HOSTPACK 3 /* host threads pack the misses, one DMA per 2 MiB chunk      */
+#define NOSA_GATHER_HYBRID 4   /* units split: host-packed DMAs + the SM gather, concurrently */
 
 /* AttentionConfig (config.py:15-36) plus the engine extents of one GPU. */
 typedef struct NosaConfig {

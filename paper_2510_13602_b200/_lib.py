@@ -28,7 +28,7 @@ NOSA_ERR_STATE = 6
 SELECTOR = {"nosa": 0, "infllmv2": 1}
 VARIANT = {"ed-dma": 0, "s-dma": 1, "dma": 2}
 DTYPE = {"bf16": 0, "fp32": 1}
-GATHER = {"uva": 0, "memcpy": 1, "tma": 2}
+GATHER = {"uva": 0, "memcpy": 1, "tma": 2, "hostpack": 3, "hybrid": 4}
 SCHEDULE = {"pipelined": 0, "serial": 1}
 RESIDENCY = {"per-sequence": 0, "shared": 1}
 

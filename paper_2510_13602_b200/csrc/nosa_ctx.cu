@@ -9,7 +9,12 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <chrono>
+#include <thread>
 #include <vector>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 
 #include "../../include/nosa_b200.h"
 #include "nosa_device.cuh"
@@ -26,6 +31,7 @@ cudaError_t launch_select_scores(int n_prob, const double* s_q, const double* s_
                                  int* out_q, int* n_q, int* out_e, int* n_e, cudaStream_t st);
 cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, bool tma, int nl = 1);
 cudaError_t launch_born(const Dev& dv, int layer, cudaStream_t st, int grid);
+cudaError_t launch_scatter(const char* stage, void* const* dst, int count, int bpb, cudaStream_t st);
 cudaError_t launch_stage_inputs(const void* const* src, void* const* dst, const size_t* bytes, int grid,
                                 cudaStream_t st);
 const void* stage_inputs_kernel_fn();
@@ -45,6 +51,69 @@ bool attend_supported(int n_b, int d_head, int dtype);
 }  // namespace nosa
 
 using nosa::Dev;
+
+static inline void cpu_relax() {
+#if defined(__x86_64__)
+  _mm_pause();
+#endif
+}
+
+// Host threads of the host-pack mover (NOSA_GATHER_HOSTPACK): each job copies `count` blocks of
+// `bytes` from scattered host addresses into one contiguous pinned staging buffer.  The caller
+// takes part; workers claim blocks with an atomic counter and spin between jobs (sleeping once
+// idle for ~10 ms, e.g. between steps).
+struct PackPool {
+  std::vector<std::thread> th;
+  std::atomic<unsigned> gen{0};
+  std::atomic<int> next{0}, done{0};
+  std::atomic<bool> stop{false};
+  char* const* src = nullptr;
+  char* dst = nullptr;
+  int count = 0;
+  size_t bytes = 0;
+  void work() {
+    for (;;) {
+      const int i = next.fetch_add(1, std::memory_order_acq_rel);
+      if (i >= count) break;
+      memcpy(dst + (size_t)i * bytes, src[i], bytes);
+      done.fetch_add(1, std::memory_order_release);
+    }
+  }
+  void worker() {
+    unsigned seen = gen.load(std::memory_order_acquire);
+    long idle = 0;
+    while (!stop.load(std::memory_order_relaxed)) {
+      const unsigned g = gen.load(std::memory_order_acquire);
+      if (g != seen) {
+        seen = g;
+        work();
+        idle = 0;
+      } else if (++idle < 200000) {
+        cpu_relax();
+      } else {
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+      }
+    }
+  }
+  void start(int n) {
+    for (int i = 0; i < n; ++i) th.emplace_back([this] { worker(); });
+  }
+  void run(char* const* s, char* d, int n, size_t b) {
+    src = s;
+    dst = d;
+    count = n;
+    bytes = b;
+    done.store(0, std::memory_order_relaxed);
+    next.store(0, std::memory_order_release);
+    gen.fetch_add(1, std::memory_order_acq_rel);
+    work();
+    while (done.load(std::memory_order_acquire) < n) cpu_relax();
+  }
+  ~PackPool() {
+    stop = true;
+    for (auto& t : th) t.join();
+  }
+};
 
 struct NosaCtx {
   NosaConfig cfg{};
@@ -94,6 +163,21 @@ struct NosaCtx {
   void** h_xsrc = nullptr;
   void** h_xdst = nullptr;
   int* h_xcnt = nullptr;
+  // host-pack mover (NOSA_GATHER_HOSTPACK): pack threads, pinned host ring -> device ring (one DMA
+  // per chunk on the copy stream), scatter kernels on their own stream; dst list in device memory
+  PackPool* pack = nullptr;
+  int pack_chunk = 64;                 // blocks per chunk (2 MiB at 32 KiB blocks)
+  int pack_slots = 8;                  // ring depth
+  char* hp_host = nullptr;             // [slots][chunk][bpb] pinned
+  char* hp_dev = nullptr;              // [slots][chunk][bpb]
+  void** hp_xdst = nullptr;            // [L][B*H*C] device: slot address of every packed block
+  std::vector<cudaEvent_t> hp_ev_dma, hp_ev_sc;
+  std::vector<char> hp_used;
+  int hp_next = 0;
+  cudaStream_t scatter_stream = nullptr;
+  int hp_split = 1024;                 // this step's host-pack share of the units (of 1024)
+  cudaStream_t smg_stream = nullptr;   // hybrid mover: the SM gather's own stream
+  std::vector<cudaEvent_t> ev_smg;     // hybrid: SM gather of the attention batch ending at layer l
   // host-buffer step (nosa_decode_step_host): device staging of the step's inputs and outputs,
   // per-layer input-arrival / output-ready events, and the device->host stream
   cudaStream_t d2h_stream = nullptr, in_stream = nullptr;
@@ -260,6 +344,15 @@ static void release(NosaCtx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
+  delete ctx->pack;
+  for (auto* evs : {&ctx->hp_ev_dma, &ctx->hp_ev_sc})
+    for (auto e : *evs) cudaEventDestroy(e);
+  if (ctx->hp_host) cudaFreeHost(ctx->hp_host);
+  if (ctx->hp_dev) cudaFree(ctx->hp_dev);
+  if (ctx->hp_xdst) cudaFree(ctx->hp_xdst);
+  if (ctx->scatter_stream) cudaStreamDestroy(ctx->scatter_stream);
+  if (ctx->smg_stream) cudaStreamDestroy(ctx->smg_stream);
+  for (auto e : ctx->ev_smg) cudaEventDestroy(e);
   for (cudaGraphExec_t x : {ctx->graph_exec, ctx->graph_exec_timed, ctx->graph_exec_host})
     if (x) cudaGraphExecDestroy(x);
   for (cudaGraph_t x : {ctx->graph, ctx->graph_timed, ctx->graph_host})
@@ -711,11 +804,13 @@ static int sel_kernels(const Dev& dv) { return dv.screen && dv.split_scan ? 2 : 
 // K1+K2 for one layer: fused per-(sequence, head) select+plan, or select then the ordered
 // shared-pool planner (NOSA_RESIDENCY_SHARED)
 static cudaError_t plan_layer(NosaCtx* ctx, int layer, const void* q, int selector, cudaStream_t st,
-                              bool export_misses = false) {
+                              int export_mode = 0) {
   const Dev& dv = ctx->dv;
   if (!dv.shared) {
     Dev dx = dv;
-    dx.x_on = export_misses;
+    dx.x_on = export_mode != 0;
+    if (export_mode == 2) dx.x_dst = ctx->hp_xdst;  // host-pack: slot addresses stay on the device
+    dx.x_split = export_mode == 2 ? ctx->hp_split : 1024;
     return nosa::launch_select_plan(dx, layer, q, selector, 1, nullptr, nullptr, st);
   }
   cudaError_t e = nosa::launch_select_plan(dv, layer, q, selector, 0, nullptr, nullptr, st);
@@ -843,6 +938,86 @@ static int gather_exported(NosaCtx* ctx, int layer, cudaStream_t copy_st, bool t
   void** src = ctx->h_xsrc + layer * cap;
   for (int i = 0; i < n; ++i)
     CUDA_TRY(ctx, cudaMemcpyAsync(dst[i], src[i], (size_t)dv.bpb, cudaMemcpyDefault, copy_st));
+  return NOSA_OK;
+}
+
+// Host-pack mover: the planner exported the layer's copy list (host source addresses) and the
+// slot address of every entry (device memory, hp_xdst).  Host threads pack the scattered 32 KiB
+// blocks into pinned staging chunks; each chunk crosses PCIe as ONE large DMA on the copy engine
+// (the link's full rate, no SM loads in flight next to the attention), and a scatter kernel on
+// its own stream moves it from the device ring into the slots.  Packing chunk c+1 overlaps the
+// DMA of chunk c.  The layer's gather-done event is recorded after its last scatter.
+static int ensure_hostpack(NosaCtx* ctx) {
+  if (ctx->pack) return NOSA_OK;
+  Dev& dv = ctx->dv;
+  if (const char* e = getenv("NOSA_PACK_CHUNK")) ctx->pack_chunk = std::max(1, atoi(e));
+  if (const char* e = getenv("NOSA_PACK_SLOTS")) ctx->pack_slots = std::max(2, atoi(e));
+  int nthreads = 8;
+  if (const char* e = getenv("NOSA_PACK_THREADS")) nthreads = std::max(0, atoi(e));
+  const size_t ring = (size_t)ctx->pack_slots * ctx->pack_chunk * dv.bpb;
+  CUDA_TRY(ctx, cudaHostAlloc(reinterpret_cast<void**>(&ctx->hp_host), ring, cudaHostAllocDefault));
+  memset(ctx->hp_host, 0, ring);
+  CUDA_TRY(ctx, cudaMalloc(reinterpret_cast<void**>(&ctx->hp_dev), ring));
+  const size_t cap = (size_t)dv.B * dv.H * dv.C;
+  CUDA_TRY(ctx, cudaMalloc(reinterpret_cast<void**>(&ctx->hp_xdst), dv.L * cap * sizeof(void*)));
+  ctx->hp_ev_dma.resize(ctx->pack_slots);
+  ctx->hp_ev_sc.resize(ctx->pack_slots);
+  for (int i = 0; i < ctx->pack_slots; ++i) {
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->hp_ev_dma[i], cudaEventDisableTiming));
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->hp_ev_sc[i], cudaEventDisableTiming));
+  }
+  ctx->hp_used.assign(ctx->pack_slots, 0);
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  CUDA_TRY(ctx, cudaStreamCreateWithPriority(&ctx->scatter_stream, cudaStreamNonBlocking, hi));
+  CUDA_TRY(ctx, cudaStreamCreateWithPriority(&ctx->smg_stream, cudaStreamNonBlocking, hi));
+  ctx->ev_smg.resize(dv.L);
+  for (auto& e : ctx->ev_smg) CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  ctx->pack = new PackPool();
+  ctx->pack->start(nthreads);
+  return NOSA_OK;
+}
+
+static int gather_hostpack(NosaCtx* ctx, int layer, cudaStream_t copy_st, bool timed, bool hybrid) {
+  const Dev& dv = ctx->dv;
+  cudaError_t e;
+  while ((e = cudaEventQuery(ctx->ev_plan[layer])) == cudaErrorNotReady) cpu_relax();
+  CUDA_TRY(ctx, e);
+  const volatile int* xc = ctx->h_xcnt;
+  const int n = xc[2 * layer], n_born = xc[2 * layer + 1];
+  cudaStream_t sc = ctx->scatter_stream;
+  CUDA_TRY(ctx, cudaStreamWaitEvent(sc, ctx->ev_plan[layer], 0));
+  if (n_born && !hybrid) {  // (hybrid: the SM gather rebuilds the born blocks)
+    CUDA_TRY(ctx, nosa::launch_born(dv, layer, sc, std::min(n_born, ctx->num_sms)));
+    ctx->memcpy_born_launches += 1;
+  }
+  const size_t cap = (size_t)dv.B * dv.H * dv.C;
+  char* const* src = reinterpret_cast<char* const*>(ctx->h_xsrc + layer * cap);
+  void* const* dst = ctx->hp_xdst + layer * cap;
+  {
+    TimeScope ts(ctx, copy_st, 1, timed);
+    for (int c0 = 0; c0 < n; c0 += ctx->pack_chunk) {
+      const int cnt = std::min(ctx->pack_chunk, n - c0);
+      const int slot = ctx->hp_next;
+      ctx->hp_next = (ctx->hp_next + 1) % ctx->pack_slots;
+      char* hbuf = ctx->hp_host + (size_t)slot * ctx->pack_chunk * dv.bpb;
+      char* dbuf = ctx->hp_dev + (size_t)slot * ctx->pack_chunk * dv.bpb;
+      if (ctx->hp_used[slot]) {  // the host slot is free once its previous DMA has read it
+        while ((e = cudaEventQuery(ctx->hp_ev_dma[slot])) == cudaErrorNotReady) cpu_relax();
+        CUDA_TRY(ctx, e);
+        CUDA_TRY(ctx, cudaStreamWaitEvent(copy_st, ctx->hp_ev_sc[slot], 0));  // device slot: scattered
+      }
+      ctx->pack->run(src + c0, hbuf, cnt, (size_t)dv.bpb);
+      CUDA_TRY(ctx, cudaMemcpyAsync(dbuf, hbuf, (size_t)cnt * dv.bpb, cudaMemcpyHostToDevice, copy_st));
+      CUDA_TRY(ctx, cudaEventRecord(ctx->hp_ev_dma[slot], copy_st));
+      CUDA_TRY(ctx, cudaStreamWaitEvent(sc, ctx->hp_ev_dma[slot], 0));
+      CUDA_TRY(ctx, nosa::launch_scatter(dbuf, dst + c0, cnt, dv.bpb, sc));
+      CUDA_TRY(ctx, cudaEventRecord(ctx->hp_ev_sc[slot], sc));
+      ctx->hp_used[slot] = 1;
+      ctx->memcpy_born_launches += 1;  // (counted with the mover's kernels)
+    }
+  }
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[layer], sc));
   return NOSA_OK;
 }
 
@@ -1050,18 +1225,35 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
     for (int l = 0; l < dv.L; ++l) groups.push_back({l, 1});
   }
   // copy-engine mover: the planner exports each layer's copy list to mapped host memory
-  const bool export_misses = io->gather_mode == NOSA_GATHER_MEMCPY && !dv.shared && !dv.born_local &&
-                             !ctx->capturing && !getenv("NOSA_MEMCPY_READBACK");
+  const bool hybrid = io->gather_mode == NOSA_GATHER_HYBRID && !dv.born_local;
+  const bool hostpack = (io->gather_mode == NOSA_GATHER_HOSTPACK || io->gather_mode == NOSA_GATHER_HYBRID) &&
+                        !dv.born_local;
+  if (hostpack && (dv.shared || ctx->capturing || ctx->mirror_device >= 0))
+    return fail(ctx, NOSA_ERR_VALUE, "the host-pack mover needs per-sequence residency, a host slow tier and an eager step");
+  const bool export_misses = hostpack || (io->gather_mode == NOSA_GATHER_MEMCPY && !dv.shared && !dv.born_local &&
+                                          !ctx->capturing && !getenv("NOSA_MEMCPY_READBACK"));
   if (export_misses)
     if (int rc = ensure_export(ctx)) return rc;
+  if (hostpack)
+    if (int rc = ensure_hostpack(ctx)) return rc;
+  const int export_mode = hostpack ? 2 : (export_misses ? 1 : 0);
   Dev dx = dv;  // (ensure_export filled the x_* pointers of ctx->dv)
   dx.x_on = export_misses;
+  if (hostpack) {
+    ctx->hp_split = 1024;
+    if (hybrid) {  // NOSA_HOST_SHARE: the host-packed share of the units (default one half)
+      const char* e = getenv("NOSA_HOST_SHARE");
+      ctx->hp_split = std::min(1024, std::max(0, (int)lround((e ? atof(e) : 0.5) * 1024.0)));
+    }
+    dx.x_dst = ctx->hp_xdst;  // slot addresses stay on the device (plan_layer does the same)
+  }
+  dx.x_split = hostpack ? ctx->hp_split : 1024;
   auto select = [&](int l) -> int {
     if (hio) CUDA_TRY(ctx, cudaStreamWaitEvent(ss, ctx->ev_in[l], 0));
     CUDA_TRY(ctx, cudaMemsetAsync(dv.cnt + nosa::kCntStride * l, 0, nosa::kCntStride * sizeof(int), ss));
     {
       TimeScope ts(ctx, ss, 0, timed);
-      CUDA_TRY(ctx, plan_layer(ctx, l, q + l * qstride, io->selector, ss, export_misses));
+      CUDA_TRY(ctx, plan_layer(ctx, l, q + l * qstride, io->selector, ss, export_mode));
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_plan[l], ss));
     return NOSA_OK;
@@ -1208,6 +1400,20 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   int n_att = 0, n_gather_kernels = 0;
   ctx->memcpy_born_launches = 0;
   cudaEvent_t last_att[2] = {nullptr, nullptr};
+  // hybrid mover: the SM share of every attention batch, device-driven on its own stream, queued
+  // up front (each waits for its batch's last plan); the host packs the rest in the loop below
+  auto smg_launch = [&](int l) -> int {
+    const int l0 = ctx->att_l0[l];
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->smg_stream, ctx->ev_plan[l], 0));
+    CUDA_TRY(ctx, nosa::launch_gather(dv, l0, ctx->smg_stream, ctx->gather_grid, false, l - l0 + 1));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_smg[l], ctx->smg_stream));
+    ++n_gather_kernels;
+    return NOSA_OK;
+  };
+  if (hybrid && !serial)
+    for (int l = 0; l < dv.L; ++l)
+      if (ctx->att_l0[l] >= 0)
+        if (int rc = smg_launch(l)) return rc;
   for (int l = 0; l < dv.L; ++l) {
     if (serial) {
       if (l > 0) CUDA_TRY(ctx, cudaStreamWaitEvent(ss, ctx->ev_fin[l - 1], 0));
@@ -1218,7 +1424,14 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
     const int l0 = batch_end ? att_l0[l] : l, n = l - l0 + 1;
     if (!dv.born_local) {  // (all resident: the planner placed the newborn blocks, nothing to move)
       CUDA_TRY(ctx, cudaStreamWaitEvent(cp, ctx->ev_plan[l], 0));
-      if (io->gather_mode == NOSA_GATHER_MEMCPY) {
+      if (hostpack) {  // (records ev_gather[l] on the scatter stream itself)
+        if (hybrid && batch_end) {
+          if (serial)
+            if (int rc = smg_launch(l)) return rc;
+          CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->scatter_stream, ctx->ev_smg[l], 0));
+        }
+        if (int rc = gather_hostpack(ctx, l, cp, timed, hybrid)) return rc;
+      } else if (io->gather_mode == NOSA_GATHER_MEMCPY) {
         const int rc = export_misses ? gather_exported(ctx, l, cp, timed) : gather_memcpy(ctx, l, ctx->ev_plan[l], cp, timed);
         if (rc) return rc;
       } else if (batch_end) {  // device movers: one launch for the attention batch's layers
@@ -1227,7 +1440,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
         CUDA_TRY(ctx, nosa::launch_gather(dv, l0, cp, tma ? ctx->tma_gather_grid : ctx->gather_grid, tma, n));
         ++n_gather_kernels;
       }
-      CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[l], cp));
+      if (!hostpack) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[l], cp));
     }
     if (!batch_end) continue;
     cudaStream_t a = (n_att & 1) ? at2 : at;
@@ -1410,7 +1623,7 @@ static bool mapped_alias(const void* p, const char** out) {
 // re-pointed in the executable graph before the launch (launches already in flight keep theirs).
 extern "C" int nosa_step_graph_capture_host(NosaCtx* ctx, const NosaHostStepIO* hio) {
   if (!ctx) return NOSA_ERR_VALUE;
-  if (hio && hio->gather_mode == NOSA_GATHER_MEMCPY)
+  if (hio && (hio->gather_mode == NOSA_GATHER_MEMCPY || hio->gather_mode >= NOSA_GATHER_HOSTPACK))
     return fail(ctx, NOSA_ERR_VALUE, "graph capture needs a device-driven gather (uva or tma)");
   NosaStepIO io;
   if (int rc = host_staging(ctx, hio, &io)) return rc;
@@ -1508,7 +1721,7 @@ extern "C" int nosa_step_graph_capture_hidden(NosaCtx* ctx, const NosaHiddenStep
 }
 
 static int capture_step(NosaCtx* ctx, const NosaStepIO* io, const void* hidden) {
-  if (io->gather_mode == NOSA_GATHER_MEMCPY)
+  if (io->gather_mode == NOSA_GATHER_MEMCPY || io->gather_mode >= NOSA_GATHER_HOSTPACK)
     return fail(ctx, NOSA_ERR_VALUE, "graph capture needs a device-driven gather (uva or tma)");
   cudaSetDevice(ctx->device);
   for (cudaGraphExec_t* x : {&ctx->graph_exec, &ctx->graph_exec_timed})

@@ -82,6 +82,8 @@ struct Dev {
   // copy list straight into mapped pinned host memory, so the host submits the batch with no
   // device round trip (nosa_ctx.cu gather_exported)
   int x_on;                      // set per launch: export this launch's misses
+  int x_split;                   // host-pack share (hybrid mover): units with unit_hash < x_split
+                                 // go to the exported list, the rest stay with the SM gather; 1024 = all
   void** x_src;                  // [L][B*H*C] device alias of the host array of source addresses
   void** x_dst;                  // [L][B*H*C] destination slot addresses
   int* x_cnt;                    // [L][2] device alias of host ints: exported misses, born blocks

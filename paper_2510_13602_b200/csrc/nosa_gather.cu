@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) gather_kernel(Dev dv, int layer0, int nl)
       }
 #pragma unroll
       for (int j = 0; j < NBLK; ++j)
-        if (m[j].x >= 0 && m[j].w)
+        if (m[j].x >= 0 && m[j].w == 1)  // (w = 2: moved by the host-pack path)
           write_born_block(dv, m[j], reinterpret_cast<int4*>(dv.pool + ((size_t)m[j].x * dv.C + m[j].z) * dv.bpb), vecs);
     }
   }
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(32) gather_tma_kernel(Dev dv, int layer0, int 
     auto issue = [&](int k) {  // host -> stage (born blocks are written directly, see below)
       const int4 e = item(k);
       const int s = (k_base + k) % kTmaStages;
-      if (e.w) {
+      if (e.w) {  // born (rebuilt below) or moved by the host-pack path: nothing to load
         mbar_arrive_plain(&bars[s]);
         return;
       }
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(32) gather_tma_kernel(Dev dv, int layer0, int 
       const int4 e = item(k);
       char* dst = dv.pool + ((size_t)e.x * dv.C + e.z) * dv.bpb;
       mbar_wait(&bars[s], ((k_base + k) / kTmaStages) & 1);
-      if (e.w) {  // born at the previous step: row 0 from the device stash, zeros elsewhere
+      if (e.w == 1) {  // born at the previous step: row 0 from the device stash, zeros elsewhere
         const int vecs = (int)(dv.bpb / 16), row_vecs = dv.D * dv.elem / 16, plane_vecs = vecs / 2;
         const int4* stash = reinterpret_cast<const int4*>(dv.newrow + (size_t)e.x * 2 * dv.D * dv.elem);
         for (int i = lane; i < vecs; i += 32) {
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(32) gather_tma_kernel(Dev dv, int layer0, int 
           reinterpret_cast<int4*>(dst)[i] = in_plane < row_vecs ? stash[which * row_vecs + in_plane] : make_int4(0, 0, 0, 0);
         }
         __syncwarp();
-      } else if (lane == 0) {
+      } else if (e.w == 0 && lane == 0) {
         bulk_s2g(dst, smem_raw + (size_t)s * dv.bpb, (unsigned)dv.bpb);
         bulk_commit();
       }
@@ -152,8 +152,23 @@ __global__ void __launch_bounds__(256) born_kernel(Dev dv, int layer) {
   const int vecs = (int)(dv.bpb / 16);
   for (int e = blockIdx.x; e < n; e += gridDim.x) {
     const int4 m = list[e];
-    if (m.w) write_born_block(dv, m, reinterpret_cast<int4*>(dv.pool + ((size_t)m.x * dv.C + m.z) * dv.bpb), vecs);
+    if (m.w == 1) write_born_block(dv, m, reinterpret_cast<int4*>(dv.pool + ((size_t)m.x * dv.C + m.z) * dv.bpb), vecs);
   }
+}
+
+// Host-pack mover: one DMA'd chunk of packed blocks, device ring -> their slots (HBM -> HBM).
+__global__ void __launch_bounds__(256) scatter_kernel(const int4* __restrict__ stage, void* const* __restrict__ dst,
+                                                      int count, int vecs) {
+  for (int e = blockIdx.x; e < count; e += gridDim.x) {
+    const int4* s = stage + (size_t)e * vecs;
+    int4* d = reinterpret_cast<int4*>(dst[e]);
+    for (int i = threadIdx.x; i < vecs; i += blockDim.x) d[i] = __ldcs(s + i);
+  }
+}
+
+cudaError_t launch_scatter(const char* stage, void* const* dst, int count, int bpb, cudaStream_t st) {
+  scatter_kernel<<<count, 256, 0, st>>>(reinterpret_cast<const int4*>(stage), dst, count, bpb / 16);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_born(const Dev& dv, int layer, cudaStream_t st, int grid) {

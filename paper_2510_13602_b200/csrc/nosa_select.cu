@@ -673,12 +673,15 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
     // a block whose only token was appended at the previous step of this run is rebuilt from
     // the device-side stash of that row (the slow copy holds the same bytes)
     const int t_now = dv.t[lbh];
+    // hybrid mover: this unit's misses go to the host-packed list (w = 2: the SM gather skips
+    // them) or stay with the SM gather; a fixed hash of the unit splits the batch
+    const bool to_host = dv.x_on && ((((unsigned)lbh * 2654435761u) >> 22) < (unsigned)dv.x_split);
     for (int f = lane; f < nf; f += 32) {
       const int blk = sm.fetch[f];
       const int born = (blk * dv.n_b == t_now - 1) && (t_now - 1 >= t0);
-      ml[base + f] = make_int4(lbh, blk, sm.reqslot[sm.fpos[f]], born);
+      ml[base + f] = make_int4(lbh, blk, sm.reqslot[sm.fpos[f]], born ? 1 : (to_host ? 2 : 0));
     }
-    if (dv.x_on) {
+    if (to_host) {
       // copy list for the host: every miss but a block born by the last append (rebuilt on the
       // device; it is the newest block, so always the last fetch); the layer's last CTA then
       // publishes the counts (select_plan_kernel)

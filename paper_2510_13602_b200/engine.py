@@ -236,8 +236,9 @@ class NosaEngine:
 
     def _mover(self, gather: str, graph: bool = False) -> str:
         """"auto": the SM zero-copy gather (`uva`), device-driven and graph-capturable, for every
-        tier.  `memcpy` (one host-submitted copy-engine copy per block, host-bound) and `tma`
-        stay selectable for experiments."""
+        tier.  `hostpack` (host-packed chunks over the copy engine, eager steps only), `memcpy`
+        (one host-submitted copy-engine copy per block, host-bound) and `tma` stay selectable
+        (DESIGN.md §5)."""
         return "uva" if gather == "auto" else gather
 
     def step(self, q, k_new, v_new, selector: str = "nosa", out: torch.Tensor | None = None,
@@ -246,8 +247,9 @@ class NosaEngine:
 
         q: [layers][batch][n_head][d_head]; k_new, v_new: [layers][batch][n_kv_head][d_head].
         Returns out [layers][batch][n_head][d_head] float32 (attention over tokens [0, t)).
-        gather: "auto" (see _mover), "uva" (zero-copy SM kernel), "tma" (TMA bulk kernel) or
-        "memcpy" (copy engine).
+        gather: "auto" (see _mover), "uva" (zero-copy SM kernel), "tma" (TMA bulk kernel),
+        "hostpack" (host threads pack the misses into 2 MiB chunks, one DMA each) or "memcpy"
+        (one copy-engine copy per block).
         schedule: "pipelined" overlaps layer l's gather with the scoring of later layers;
         "serial" runs layer by layer (results are identical)."""
         if selector not in SELECTORS:

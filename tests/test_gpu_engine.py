@@ -327,7 +327,7 @@ def test_resident_multilayer_batched_attention():
     assert a <= TOL["bf16"]
 
 
-@pytest.mark.parametrize("gather", ["memcpy", "tma"])
+@pytest.mark.parametrize("gather", ["memcpy", "tma", "hostpack", "hybrid"])
 def test_other_gather_paths_vs_oracle(gather):
     a = _run_pair(SMALL, batch=2, t0s=[900, 800], steps=20, fast_slots=36, seed=12, rho=0.0, gather=gather)
     assert a <= TOL["bf16"]
@@ -342,7 +342,9 @@ def test_gather_paths_and_schedules_bitwise_identical():
     results = []
     runs = [("uva", "pipelined", False, 1), ("tma", "pipelined", False, 1), ("memcpy", "pipelined", False, 1),
             ("uva", "serial", False, 1), ("memcpy", "pipelined", True, 1), ("uva", "serial", True, 1),
-            ("uva", "pipelined", False, 2), ("memcpy", "pipelined", True, 3)]
+            ("uva", "pipelined", False, 2), ("memcpy", "pipelined", True, 3), ("hostpack", "pipelined", False, 1),
+            ("hostpack", "serial", False, 1), ("hostpack", "pipelined", True, 3), ("hybrid", "pipelined", False, 1),
+            ("hybrid", "serial", False, 2), ("hybrid", "pipelined", True, 3)]
     for gather, schedule, host, att_layers in runs:
         eng = NosaEngine(cfg, batch=2, layers=3, max_tokens=3100, fast_slots=70, w1=w1, w2=w2,
                          attend_layers=att_layers)
