@@ -736,14 +736,16 @@ __device__ void plan_phase(const Dev& dv, int layer, int b, int h, SelSmem& sm) 
   }
 }
 
-// Screen scan as its own kernel (Dev::split_scan): grid = (row chunks of 128, B*H, layers), 256
-// threads.  Every CTA sums its unit's query group (the same f64 order as select_phase) and
-// screens 128 pool rows into the global interval scratch; chunk 0 also stores q_sum for the
-// f64 rescoring.  Purely bandwidth-bound (the bf16 K_c rows are the bytes), so it streams at
-// full occupancy instead of alternating with the selection's latency-bound phases.
+// Screen scan as its own kernel (Dev::split_scan): grid = (row chunks, B*H, layers), 256 threads.
+// Every CTA sums its unit's query group (the same f64 order as select_phase) and screens its
+// chunk of pool rows (`rows`, a multiple of 128; by default the whole pool) into the global
+// interval scratch, 128 rows per iteration with the next iteration's rows already in flight;
+// chunk 0 also stores q_sum for the f64 rescoring.  Purely bandwidth-bound (the bf16 K_c rows
+// are the bytes), so it streams at full occupancy instead of alternating with the selection's
+// latency-bound phases.
 template <typename T>
 __global__ void __launch_bounds__(256) screen_scan_kernel(Dev dv, int layer0, const T* __restrict__ q0,
-                                                          size_t q_layer_stride) {
+                                                          size_t q_layer_stride, int rows) {
   __shared__ float qt[128];  // (float) q_sum, transposed [j][hl]: conflict-free qf loads
   __shared__ int qmax_bits;
   const int layer = layer0 + blockIdx.z;
@@ -755,11 +757,12 @@ __global__ void __launch_bounds__(256) screen_scan_kernel(Dev dv, int layer0, co
   const int recent_start = max(0, t0 - dv.n_w + 1);           // selection.py:49
   const int pool_lo = dv.n_sink;                              // selection.py:59
   const int P = max(pool_lo, recent_start / dv.n_b) - pool_lo;
-  const int pb = blockIdx.x * 128, pe = min(pb + 128, P);
+  const int pb = blockIdx.x * rows, pe = min(pb + rows, P);
   if (pb >= max(P, 1)) return;  // (chunk 0 always runs: it stores q_sum)
   // the pool rows do not depend on q: their loads are in flight while q_sum is formed
   const __nv_bfloat16* k16 = dv.kc16 + ((size_t)lbh * dv.NB + pool_lo) * D;
-  const int p0 = pb + warp * 16;
+  const int stride = nwarps * 16;
+  int p0 = pb + warp * 16;
   uint4 raw[8];
   if (p0 < pe) screen_load(k16, D, p0, pe, raw);
   if (tid == 0) qmax_bits = 0;
@@ -789,10 +792,15 @@ __global__ void __launch_bounds__(256) screen_scan_kernel(Dev dv, int layer0, co
   unsigned* lo = dv.scr_lo + (size_t)lbh * dv.NB;
   float* up = dv.scr_up + (size_t)lbh * dv.NB;
   const float qmax = __int_as_float(qmax_bits), gam = screen_gamma(D);
-  screen_finish(raw, qf, kerr, gam, qmax, p0, pe, lo, up);
-  for (int p1 = p0 + nwarps * 16; p1 < pe; p1 += nwarps * 16) {  // (blockDim < 256 only)
-    screen_load(k16, D, p1, pe, raw);
-    screen_finish(raw, qf, kerr, gam, qmax, p1, pe, lo, up);
+  for (;;) {
+    const int p1 = p0 + stride;
+    uint4 nxt[8];
+    if (p1 < pe) screen_load(k16, D, p1, pe, nxt);  // next iteration's rows in flight
+    screen_finish(raw, qf, kerr, gam, qmax, p0, pe, lo, up);
+    if (p1 >= pe) break;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) raw[u] = nxt[u];
+    p0 = p1;
   }
 }
 
@@ -1186,11 +1194,15 @@ cudaError_t launch_select_plan(const Dev& dv, int layer, const void* q, int sele
   const dim3 grid(dv.B * dv.H, layers);
   const bool split = dv.screen && dv.split_scan;  // (mode 2 plans only: the selection code never runs)
   if (mode != 2 && split) {
-    const dim3 sgrid((dv.NB + 127) / 128, dv.B * dv.H, layers);
+    // rows per CTA: the whole pool (one CTA per unit, the rows of the next 128-row iteration in
+    // flight); NOSA_SCAN_ROWS=128 gives one 128-row chunk per CTA (the first split kernel)
+    static const int env_rows = getenv("NOSA_SCAN_ROWS") ? std::max(1, atoi(getenv("NOSA_SCAN_ROWS"))) : 0;
+    const int rows = env_rows ? (env_rows + 127) / 128 * 128 : (dv.NB + 127) / 128 * 128;
+    const dim3 sgrid((dv.NB + rows - 1) / rows, dv.B * dv.H, layers);
     if (dv.dtype == 0)
-      screen_scan_kernel<__nv_bfloat16><<<sgrid, 256, 0, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(q), qs);
+      screen_scan_kernel<__nv_bfloat16><<<sgrid, 256, 0, st>>>(dv, layer, static_cast<const __nv_bfloat16*>(q), qs, rows);
     else
-      screen_scan_kernel<float><<<sgrid, 256, 0, st>>>(dv, layer, static_cast<const float*>(q), qs);
+      screen_scan_kernel<float><<<sgrid, 256, 0, st>>>(dv, layer, static_cast<const float*>(q), qs, rows);
   }
   if (dv.dtype == 0) {
     auto k = split ? select_plan_kernel<__nv_bfloat16, true> : select_plan_kernel<__nv_bfloat16, false>;
