@@ -176,8 +176,6 @@ struct NosaCtx {
   int hp_next = 0;
   cudaStream_t scatter_stream = nullptr;
   int hp_split = 1024;                 // this step's host-pack share of the units (of 1024)
-  bool hp_direct = false;              // NOSA_HYBRID_DIRECT: the host share as one copy per block
-  cudaEvent_t ev_direct = nullptr;
   cudaStream_t smg_stream = nullptr;   // hybrid mover: the SM gather's own stream
   std::vector<cudaEvent_t> ev_smg;     // hybrid: SM gather of the attention batch ending at layer l
   // host-buffer step (nosa_decode_step_host): device staging of the step's inputs and outputs,
@@ -354,7 +352,6 @@ static void release(NosaCtx* ctx) {
   if (ctx->hp_xdst) cudaFree(ctx->hp_xdst);
   if (ctx->scatter_stream) cudaStreamDestroy(ctx->scatter_stream);
   if (ctx->smg_stream) cudaStreamDestroy(ctx->smg_stream);
-  if (ctx->ev_direct) cudaEventDestroy(ctx->ev_direct);
   for (auto e : ctx->ev_smg) cudaEventDestroy(e);
   for (cudaGraphExec_t x : {ctx->graph_exec, ctx->graph_exec_timed, ctx->graph_exec_host})
     if (x) cudaGraphExecDestroy(x);
@@ -812,7 +809,7 @@ static cudaError_t plan_layer(NosaCtx* ctx, int layer, const void* q, int select
   if (!dv.shared) {
     Dev dx = dv;
     dx.x_on = export_mode != 0;
-    if (export_mode == 2 && !ctx->hp_direct) dx.x_dst = ctx->hp_xdst;  // host-pack: slot addresses on the device
+    if (export_mode == 2) dx.x_dst = ctx->hp_xdst;  // host-pack: slot addresses stay on the device
     dx.x_split = export_mode == 2 ? ctx->hp_split : 1024;
     return nosa::launch_select_plan(dx, layer, q, selector, 1, nullptr, nullptr, st);
   }
@@ -974,7 +971,6 @@ static int ensure_hostpack(NosaCtx* ctx) {
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   CUDA_TRY(ctx, cudaStreamCreateWithPriority(&ctx->scatter_stream, cudaStreamNonBlocking, hi));
   CUDA_TRY(ctx, cudaStreamCreateWithPriority(&ctx->smg_stream, cudaStreamNonBlocking, hi));
-  CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_direct, cudaEventDisableTiming));
   ctx->ev_smg.resize(dv.L);
   for (auto& e : ctx->ev_smg) CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   ctx->pack = new PackPool();
@@ -997,18 +993,6 @@ static int gather_hostpack(NosaCtx* ctx, int layer, cudaStream_t copy_st, bool t
   }
   const size_t cap = (size_t)dv.B * dv.H * dv.C;
   char* const* src = reinterpret_cast<char* const*>(ctx->h_xsrc + layer * cap);
-  if (ctx->hp_direct) {  // the host share straight into the slots, one copy-engine copy per block
-    void* const* hdst = ctx->h_xdst + layer * cap;
-    {
-      TimeScope ts(ctx, copy_st, 1, timed);
-      for (int i = 0; i < n; ++i)
-        CUDA_TRY(ctx, cudaMemcpyAsync(hdst[i], src[i], (size_t)dv.bpb, cudaMemcpyHostToDevice, copy_st));
-    }
-    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_direct, copy_st));
-    CUDA_TRY(ctx, cudaStreamWaitEvent(sc, ctx->ev_direct, 0));
-    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_gather[layer], sc));
-    return NOSA_OK;
-  }
   void* const* dst = ctx->hp_xdst + layer * cap;
   {
     TimeScope ts(ctx, copy_st, 1, timed);
@@ -1261,8 +1245,7 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
       const char* e = getenv("NOSA_HOST_SHARE");
       ctx->hp_split = std::min(1024, std::max(0, (int)lround((e ? atof(e) : 0.5) * 1024.0)));
     }
-    ctx->hp_direct = hybrid && getenv("NOSA_HYBRID_DIRECT");
-    if (!ctx->hp_direct) dx.x_dst = ctx->hp_xdst;  // slot addresses stay on the device (plan_layer too)
+    dx.x_dst = ctx->hp_xdst;  // slot addresses stay on the device (plan_layer does the same)
   }
   dx.x_split = hostpack ? ctx->hp_split : 1024;
   auto select = [&](int l) -> int {

@@ -185,8 +185,10 @@ cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, b
     max_shared_carveout(gather_tma_kernel);
     gather_tma_kernel<<<g, 32, smem, st>>>(dv, layer, nl);
   } else {
-    // NOSA_GATHER_VARIANT (experiments): bit 0 = two blocks per CTA iteration, bit 1 = L2::256B
-    static const int variant = getenv("NOSA_GATHER_VARIANT") ? atoi(getenv("NOSA_GATHER_VARIANT")) : 0;
+    // NOSA_GATHER_VARIANT: bit 0 = two blocks per CTA iteration, bit 1 = L2::256B.  Default 2:
+    // the 256-byte L2 fetch hint (cfg 3, two alternations: 14.13K vs 13.97K tok/s, attention next
+    // to the gather 0.83 vs 0.77 of HBM; tools/r2u.sh)
+    static const int variant = getenv("NOSA_GATHER_VARIANT") ? atoi(getenv("NOSA_GATHER_VARIANT")) : 2;
     max_shared_carveout(gather_kernel<1, false>);
     max_shared_carveout(gather_kernel<2, false>);
     max_shared_carveout(gather_kernel<1, true>);
