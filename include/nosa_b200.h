@@ -217,15 +217,17 @@ int nosa_gather(NosaCtx* ctx, int layer, int mode, void* stream);
 int nosa_attend(NosaCtx* ctx, int layer, const void* q, const void* k_new, const void* v_new,
                 float* out, void* stream);
 
-/* All layers of one decode step, pipelined: select+plan on `stream`, gathers on the
+/* All layers of one decode step, pipelined: select+plan on `stream`, the miss gathers on the
  * context's copy stream overlapped with scoring of the next layers, attention after each
- * layer's gather.  Equivalent to per-layer nosa_select_plan, nosa_gather, nosa_attend. */
+ * attention batch's gathers.  Equivalent to per-layer nosa_select_plan, nosa_gather, nosa_attend. */
 int nosa_decode_step(NosaCtx* ctx, const NosaStepIO* io, void* stream);
 
 /* nosa_decode_step on host buffers: the reference's own calling convention
- * (DecodeEngine.step takes and returns host arrays, decode.py:152-190), batched.  Layer l's
- * q/k/v go host->device on the copy stream ahead of the miss gathers, its output comes back on
- * a device->host stream as soon as layer l is done (overlapping later layers).  Asynchronous on
+ * (DecodeEngine.step takes and returns host arrays, decode.py:152-190), batched.  Each
+ * selection group's q/k/v are staged from pinned host memory by an SM zero-copy kernel on the
+ * context's input stream ahead of that group's selection (NOSA_STAGE_COPIES=1: copy-engine
+ * copies instead); layer l's output comes back on a device->host stream as soon as layer l is
+ * done (overlapping later layers).  Asynchronous on
  * `stream`: the host buffers must stay valid, and `out` is complete, once `stream` reaches this
  * point (cudaStreamSynchronize).  The context owns the device staging. */
 int nosa_decode_step_host(NosaCtx* ctx, const NosaHostStepIO* io, void* stream);

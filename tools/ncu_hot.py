@@ -17,7 +17,11 @@ for h, v in zip(hdr, vals):
 sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                       text=True).stdout
 srows = list(csv.reader(io.StringIO(sass)))
-shdr, data = srows[1], srows[2:]
+shdr, data = srows[1], []
+for r in srows[2:]:  # the first launch's rows (a report of several launches repeats the header)
+    if not r or not re.fullmatch(r"(0x)?[0-9a-fA-F]+", r[0]):
+        break
+    data.append(r)
 i_all = shdr.index("Warp Stall Sampling (All Samples)")
 keys = [k for k in shdr if k.startswith("stall_") and "Not Issued" not in k]
 # map SASS offsets to source lines with nvdisasm -g on the cubin inside the .so
@@ -69,4 +73,4 @@ def text(loc):
 print(f"stall samples: {tot:.0f}")
 for loc, v in by_line.most_common(24):
     tag = f"{loc[0]}:{loc[1]}" if loc else "?"
-    print(f"{100 * v / tot:5.1f}% {tag:22s} {text(loc):60s} {dict(reasons.get(loc, {}).most_common(3))}")
+    print(f"{100 * v / tot:5.1f}% {tag:22s} {text(loc):60s} {dict(reasons.get(loc, Counter()).most_common(3))}")
