@@ -274,6 +274,11 @@ int nosa_step_graph_launch(NosaCtx* ctx, void* stream);
 int nosa_project_qkv(const void* h, int m, int k, const void* w_t, int n, int nq, int nk, void* q,
                      void* k_out, void* v, int splits, void* stream);
 
+/* fp32 form of the projection for fp32 caches (project_qkv, attention.py:67-90, the parity
+ * mode): out [m][n] = h [m][k] . w [k][n], device float32, row-major, CUDA-core FMAs in k
+ * order.  No context; asynchronous on `stream`. */
+int nosa_project_f32(const float* h, int m, int k, const float* w, int n, float* out, void* stream);
+
 /* ---- standalone selector (drop-in for nosa_select / infllmv2_select on given scores) --- */
 
 /* n_prob independent selections.  s_q, s_e: device float64 [n_prob][stride] block scores.

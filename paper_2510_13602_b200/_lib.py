@@ -93,6 +93,7 @@ SIGNATURES = {
     "nosa_step_graph_capture": (_I, [_P, ctypes.POINTER(NosaStepIO)]),
     "nosa_step_graph_launch": (_I, [_P, _P]),
     "nosa_project_qkv": (_I, [_P, _I, _I, _P, _I, _I, _I, _P, _P, _P, _I, _P]),
+    "nosa_project_f32": (_I, [_P, _I, _I, _P, _I, _P, _P]),
     "nosa_select_scores": (_I, [_I, _P, _P, _I, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P]),
     "nosa_read_selection": (_I, [_P, _I, _I, _I32P, _I32P, _I32P, _I32P, _I32P, _I32P, _F64P]),
     "nosa_read_plan": (_I, [_P, _I, _I32P, _I32P, _I32P, _I32P, _I32P]),

@@ -6,8 +6,8 @@
 (n_head, d_head) outputs out, the new token appended after attention.  The QKV projection
 (project_qkv, attention.py:67-90) runs on the GPU: for bf16 caches on the tensor cores
 (`projection.QKVProjection`, the tcgen05 GEMM behind `nosa_project_qkv`) when the shapes
-tile (n % 128 == 0, d % 64 == 0), otherwise and for fp32 caches as an fp32 library GEMM
-(torch.matmul -> cuBLAS); selection, attention, the eviction score and the append run in the
+tile (n % 128 == 0, d % 64 == 0), otherwise and for fp32 caches as an fp32 CUDA-core GEMM
+(`nosa_project_f32`); selection, attention, the eviction score and the append run in the
 sm_100a kernels behind the C ABI.  Like the reference engine, all KV stays
 resident (every block is placed in an HBM slot at prefill).
 
@@ -22,6 +22,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import _lib
 from .config import AttentionConfig
 from .engine import NosaEngine
 from .projection import QKVProjection
@@ -103,8 +104,11 @@ class DecodeEngine:
     def _project(self, h: np.ndarray):
         if self._tc is not None:  # tcgen05 GEMM, bf16 operands, fp32 accumulation
             return self._tc(torch.as_tensor(np.asarray(h, dtype=np.float32)).to(self._tc.device))
-        x = torch.as_tensor(np.asarray(h, dtype=np.float32), device=self._w.device)
-        y = x @ self._w  # the projection GEMM (cuBLAS, fp32)
+        x = torch.as_tensor(np.asarray(h, dtype=np.float32), device=self._w.device).reshape(-1, self._w.shape[0])
+        y = torch.empty(x.shape[0], self._w.shape[1], dtype=torch.float32, device=x.device)
+        _lib.check(_lib.lib.nosa_project_f32(x.data_ptr(), x.shape[0], x.shape[1], self._w.data_ptr(),
+                                             self._w.shape[1], y.data_ptr(), _lib.stream_ptr()))
+        y = y.reshape(*np.shape(h)[:-1], self._w.shape[1])  # the projection GEMM (fp32, CUDA cores)
         q, k, v = torch.split(y, [self._split[0], self._split[1], self._split[1]], dim=-1)
         return q, k, v
 

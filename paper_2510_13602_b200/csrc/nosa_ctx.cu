@@ -37,6 +37,7 @@ cudaError_t launch_stage_inputs(const void* const* src, void* const* dst, const 
 const void* stage_inputs_kernel_fn();
 cudaError_t launch_project(const void* A, const void* Bt, int M, int N, int K, int splits, void* q, void* k, void* v,
                            int nq, int nk, cudaStream_t st, int layers = 1);
+cudaError_t launch_project_f32(const float* h, const float* w, int M, int K, int N, float* out, cudaStream_t st);
 
 cudaError_t launch_prefill(const Dev& dv, int layer, int seq_begin, int S, const void* k,
                            const void* v, int t, char* staging, cudaStream_t st);
@@ -1138,6 +1139,14 @@ extern "C" int nosa_project_qkv(const void* h, int m, int k, const void* w_t, in
     return fail(nullptr, NOSA_ERR_VALUE, "project_qkv: one split needs nq and nk multiples of 32 (nq=%d nk=%d)", nq, nk);
   cudaError_t e = nosa::launch_project(h, w_t, m, n, k, splits, q, k_out, v, nq, nk, S(stream));
   if (e != cudaSuccess) return fail(nullptr, NOSA_ERR_CUDA, "project_qkv: %s", cudaGetErrorString(e));
+  return NOSA_OK;
+}
+
+extern "C" int nosa_project_f32(const float* h, int m, int k, const float* w, int n, float* out, void* stream) {
+  if (!h || !w || !out) return fail(nullptr, NOSA_ERR_VALUE, "project_f32: NULL argument");
+  if (m <= 0 || k <= 0 || n <= 0) return fail(nullptr, NOSA_ERR_VALUE, "project_f32: bad shape");
+  cudaError_t e = nosa::launch_project_f32(h, w, m, k, n, out, S(stream));
+  if (e != cudaSuccess) return fail(nullptr, NOSA_ERR_CUDA, "project_f32: %s", cudaGetErrorString(e));
   return NOSA_OK;
 }
 

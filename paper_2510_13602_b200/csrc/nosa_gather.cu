@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(256) stage_inputs_kernel(StageSeg a, StageSeg 
 #pragma unroll
       for (int u = 0; u < PER; ++u) {
         const long long i = i0 + u * stride;
-        if (i < sg.n16) v[u] = __ldcs(sg.src + i);
+        if (i < sg.n16) v[u] = ld_host<true>(sg.src + i);  // 256-byte L2 fetches, like the gather
       }
 #pragma unroll
       for (int u = 0; u < PER; ++u) {

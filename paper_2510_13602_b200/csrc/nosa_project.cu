@@ -346,4 +346,57 @@ cudaError_t launch_project(const void* A, const void* Bt, int M, int N, int K, i
                      : launch_project_tiles<128, 6>(ma, mb, M, N, K, splits, q, k, v, nq, nk, layers, arows, st);
 }
 
+// fp32 projection for fp32 caches (compat.DecodeEngine with dtype="fp32", the parity mode):
+// out[m][n] = h[m][k] . w[k][n] on the CUDA cores, every output an fp32 FMA chain in k order.
+// 64 x 64 output tiles per CTA, 256 threads with 4 x 4 outputs each, 16-deep k tiles in shared
+// memory.  Decode-sized m (one token) is bound by reading w once; prefill m by the FMAs.
+__global__ void __launch_bounds__(256) project_f32_kernel(const float* __restrict__ h, const float* __restrict__ w,
+                                                          int M, int K, int N, float* __restrict__ out) {
+  __shared__ float sa[16][64 + 4];  // [k][m]
+  __shared__ float sb[16][64 + 4];  // [k][n]
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = tid; i < 64 * 16; i += 256) {
+      const int r = i >> 4, c = i & 15;            // h tile: row r, column c (coalesced along k)
+      const int gm = m0 + r, gk = k0 + c;
+      sa[c][r] = gm < M && gk < K ? h[(size_t)gm * K + gk] : 0.0f;
+      const int kr = i >> 6, nc = i & 63;          // w tile: row kr, column nc (coalesced along n)
+      const int wk = k0 + kr, wn = n0 + nc;
+      sb[kr][nc] = wk < K && wn < N ? w[(size_t)wk * N + wn] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = sa[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = sb[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + ty * 4 + i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gn = n0 + tx * 4 + j;
+      if (gn < N) out[(size_t)gm * N + gn] = acc[i][j];
+    }
+  }
+}
+
+cudaError_t launch_project_f32(const float* h, const float* w, int M, int K, int N, float* out, cudaStream_t st) {
+  const dim3 grid((N + 63) / 64, (M + 63) / 64);
+  project_f32_kernel<<<grid, 256, 0, st>>>(h, w, M, K, N, out);
+  return cudaGetLastError();
+}
+
 }  // namespace nosa

@@ -103,3 +103,21 @@ def test_hidden_state_step_matches_projected_step(schedule, graph, host):
     for a, b in zip(runs[0][2], runs[1][2]):
         for x, y in zip(a, b):
             np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("m,k,n", [(1, 512, 512), (1, 2048, 2560), (37, 300, 130), (513, 1024, 384)])
+def test_fp32_projection_matches_fp64_reference(m, k, n):
+    """nosa_project_f32 (the fp32-cache projection of compat.DecodeEngine) against an fp64 GEMM of
+    the same fp32 operands: fp32 FMA chains in k order, relative error ~ k * 2^-24."""
+    from paper_2510_13602_b200 import _lib
+    g = torch.Generator(device="cpu").manual_seed(m * 7 + n)
+    h = torch.randn(m, k, generator=g).cuda()
+    w = (torch.randn(k, n, generator=g) / k ** 0.5).cuda()
+    out = torch.empty(m, n, device="cuda")
+    _lib.check(_lib.lib.nosa_project_f32(h.data_ptr(), m, k, w.data_ptr(), n, out.data_ptr(), _lib.stream_ptr()))
+    ref = (h.double() @ w.double())
+    err = ((out.double() - ref).abs().max() / ref.abs().max()).item()
+    assert err < 1e-5, err
+    out2 = torch.empty_like(out)
+    _lib.check(_lib.lib.nosa_project_f32(h.data_ptr(), m, k, w.data_ptr(), n, out2.data_ptr(), _lib.stream_ptr()))
+    assert torch.equal(out, out2)
