@@ -61,22 +61,31 @@ static inline void cpu_relax() {
 
 // Host threads of the host-pack mover (NOSA_GATHER_HOSTPACK): each job copies `count` blocks of
 // `bytes` from scattered host addresses into one contiguous pinned staging buffer.  The caller
-// takes part; workers claim blocks with an atomic counter and spin between jobs (sleeping once
-// idle for ~10 ms, e.g. between steps).
+// takes part; workers claim blocks with tickets from one 64-bit counter (job generation in the
+// high half, block index in the low half), so a ticket always names the job it belongs to and a
+// late worker of an earlier job can neither take nor count a block of the next one.  Job
+// descriptors alternate between two slots (a job starts only after the previous one is done).
+// Workers spin between jobs, sleeping once idle for ~10 ms (e.g. between steps).
 struct PackPool {
+  struct Job {
+    char* const* src = nullptr;
+    char* dst = nullptr;
+    int count = 0;
+    size_t bytes = 0;
+  };
   std::vector<std::thread> th;
+  Job job[2];
+  std::atomic<unsigned long long> next{0};
   std::atomic<unsigned> gen{0};
-  std::atomic<int> next{0}, done{0};
+  std::atomic<int> done{0};
   std::atomic<bool> stop{false};
-  char* const* src = nullptr;
-  char* dst = nullptr;
-  int count = 0;
-  size_t bytes = 0;
   void work() {
     for (;;) {
-      const int i = next.fetch_add(1, std::memory_order_acq_rel);
-      if (i >= count) break;
-      memcpy(dst + (size_t)i * bytes, src[i], bytes);
+      const unsigned long long t = next.fetch_add(1, std::memory_order_acq_rel);
+      const Job& j = job[(t >> 32) & 1];
+      const int i = (int)(unsigned)t;
+      if (i >= j.count) break;
+      memcpy(j.dst + (size_t)i * j.bytes, j.src[i], j.bytes);
       done.fetch_add(1, std::memory_order_release);
     }
   }
@@ -100,13 +109,11 @@ struct PackPool {
     for (int i = 0; i < n; ++i) th.emplace_back([this] { worker(); });
   }
   void run(char* const* s, char* d, int n, size_t b) {
-    src = s;
-    dst = d;
-    count = n;
-    bytes = b;
+    const unsigned g = gen.load(std::memory_order_relaxed) + 1;
+    job[g & 1] = Job{s, d, n, b};
     done.store(0, std::memory_order_relaxed);
-    next.store(0, std::memory_order_release);
-    gen.fetch_add(1, std::memory_order_acq_rel);
+    next.store((unsigned long long)g << 32, std::memory_order_release);
+    gen.store(g, std::memory_order_release);
     work();
     while (done.load(std::memory_order_acquire) < n) cpu_relax();
   }
