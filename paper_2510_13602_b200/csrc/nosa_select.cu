@@ -151,9 +151,11 @@ __device__ __forceinline__ double row_dot64(const double* __restrict__ row, cons
 //     bit-reversed position).  Writes each row's interval [lo, up] (lo as a monotone key) to
 //     lo_out / up_out (shared memory when fused, the global scratch when split).
 // loads of one warp iteration of (a): rows p0 + 2u + half, lane hl's 16-byte slice
-__device__ __forceinline__ void screen_load(const __nv_bfloat16* __restrict__ k16, int D, int p0, int pe,
-                                            uint4 (&raw)[8]) {
+// (+ the K_c rounding bound of the row this lane will write, so it is in flight with the rows)
+__device__ __forceinline__ void screen_load(const __nv_bfloat16* __restrict__ k16, const float* __restrict__ kerr,
+                                            int D, int p0, int pe, uint4 (&raw)[8], float& kr) {
   const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4, E = D / 16;
+  kr = __ldg(kerr + min(p0 + 2 * (((hl & 8) ? 4 : 0) + ((hl & 4) ? 2 : 0) + ((hl & 2) ? 1 : 0)) + half, pe - 1));
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
     const __nv_bfloat16* row = k16 + (size_t)min(p0 + 2 * u + half, pe - 1) * D + hl * E;
@@ -167,7 +169,7 @@ __device__ __forceinline__ void screen_load(const __nv_bfloat16* __restrict__ k1
 }
 
 // the rest of (a) for one warp iteration: dots, the 16-lane reduce-scatter, the intervals
-__device__ __forceinline__ void screen_finish(const uint4 (&raw)[8], const float (&qf)[8], const float* __restrict__ kerr,
+__device__ __forceinline__ void screen_finish(const uint4 (&raw)[8], const float (&qf)[8], float kr,
                                              float gam, float qmax, int p0, int pe, unsigned* lo_out,
                                              float* up_out) {
   const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
@@ -213,7 +215,7 @@ __device__ __forceinline__ void screen_finish(const uint4 (&raw)[8], const float
   const int p = p0 + 2 * u + half;
   if (!(hl & 1) && p < pe) {
     const float s_ = sv[0], a_ = av[0];
-    const float bound = (gam * a_ + __ldg(kerr + p) * qmax) * 1.001f + fabsf(s_) * 2.4e-7f + 1e-30f;
+    const float bound = (gam * a_ + kr * qmax) * 1.001f + fabsf(s_) * 2.4e-7f + 1e-30f;
     lo_out[p] = f2key(__fsub_rd(s_, bound));
     up_out[p] = __fadd_ru(s_, bound);
   }
@@ -233,8 +235,9 @@ __device__ __forceinline__ void screen_rows(const Dev& dv, int lbh, int pool_lo,
   for (int j = 0; j < 8; ++j) qf[j] = j < E ? (float)qsum[hl * E + j] : 0.0f;
   for (int p0 = pb + warp * 16; p0 < pe; p0 += nwarps * 16) {
     uint4 raw[8];
-    screen_load(k16, D, p0, pe, raw);
-    screen_finish(raw, qf, kerr, screen_gamma(D), qmax, p0, pe, lo_out, up_out);
+    float kr;
+    screen_load(k16, kerr, D, p0, pe, raw, kr);
+    screen_finish(raw, qf, kr, screen_gamma(D), qmax, p0, pe, lo_out, up_out);
   }
 }
 
@@ -761,10 +764,12 @@ __global__ void __launch_bounds__(256) screen_scan_kernel(Dev dv, int layer0, co
   if (pb >= max(P, 1)) return;  // (chunk 0 always runs: it stores q_sum)
   // the pool rows do not depend on q: their loads are in flight while q_sum is formed
   const __nv_bfloat16* k16 = dv.kc16 + ((size_t)lbh * dv.NB + pool_lo) * D;
+  const float* kerr = dv.kc_err + (size_t)lbh * dv.NB + pool_lo;
   const int stride = nwarps * 16;
   int p0 = pb + warp * 16;
   uint4 raw[8];
-  if (p0 < pe) screen_load(k16, D, p0, pe, raw);
+  float kr = 0.0f;
+  if (p0 < pe) screen_load(k16, kerr, D, p0, pe, raw, kr);
   if (tid == 0) qmax_bits = 0;
   __syncthreads();
   for (int i = tid; i < D; i += blockDim.x) {
@@ -788,18 +793,19 @@ __global__ void __launch_bounds__(256) screen_scan_kernel(Dev dv, int layer0, co
   float qf[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) qf[j] = j < E ? qt[j * 16 + hl] : 0.0f;
-  const float* kerr = dv.kc_err + (size_t)lbh * dv.NB + pool_lo;
   unsigned* lo = dv.scr_lo + (size_t)lbh * dv.NB;
   float* up = dv.scr_up + (size_t)lbh * dv.NB;
   const float qmax = __int_as_float(qmax_bits), gam = screen_gamma(D);
   for (;;) {
     const int p1 = p0 + stride;
     uint4 nxt[8];
-    if (p1 < pe) screen_load(k16, D, p1, pe, nxt);  // next iteration's rows in flight
-    screen_finish(raw, qf, kerr, gam, qmax, p0, pe, lo, up);
+    float kn = 0.0f;
+    if (p1 < pe) screen_load(k16, kerr, D, p1, pe, nxt, kn);  // next iteration's rows in flight
+    screen_finish(raw, qf, kr, gam, qmax, p0, pe, lo, up);
     if (p1 >= pe) break;
 #pragma unroll
     for (int u = 0; u < 8; ++u) raw[u] = nxt[u];
+    kr = kn;
     p0 = p1;
   }
 }

@@ -32,12 +32,24 @@ subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath("paper_2510_13602_b
 cubin = [f for f in glob.glob(tmp + "/*.cubin") if os.path.basename(src).split(".")[0] in f][0]
 lines = subprocess.run(["nvdisasm", "-g", cubin], capture_output=True, text=True).stdout.split("\n")
 kernel_full = srows[0][1]
-mangled = None
+# the template instance the report profiled: demangle every kernel section and compare its
+# template arguments with the report's kernel name ("(bool)1" style in ncu, "true" in cu++filt)
+def _norm(x):
+    x = x.replace("(bool)1", "true").replace("(bool)0", "false").replace(" ", "")
+    return x.split("(")[0].replace("void", "", 1) if x.startswith("void") else x.split("(")[0]
+want = _norm(kernel_full)
+mangled, cands = None, []
 for l in lines:
-    m = re.match(r"\s*\.section\s+\.text\.(\S+),", l)
+    m = re.match(r"\s*\.section\s+\.text\.([^,\s]+),", l)
     if m and kname in m.group(1):
-        mangled = m.group(1)
+        cands.append(m.group(1))
+for c in cands:
+    dem = subprocess.run(["cu++filt", c], capture_output=True, text=True).stdout.strip()
+    if _norm(dem) == want:
+        mangled = c
         break
+if mangled is None:
+    mangled = cands[0]
 start = next(i for i, l in enumerate(lines) if l.strip().startswith(".section") and f".text.{mangled}," in l)
 cur, off2line = None, {}
 for l in lines[start + 1:]:
