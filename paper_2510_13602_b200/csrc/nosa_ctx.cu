@@ -549,7 +549,11 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
     ALLOC(dv.kc16, LBH * dv.NB * dv.D);
     ALLOC(dv.kc_err, LBH * dv.NB);
     ALLOC(dv.qsum_buf, LBH * dv.D);
-    dv.split_scan = getenv("NOSA_FUSED_SCAN") ? 0 : 1;
+    // the screen scan inside select_plan (fused, default) or as its own kernel ahead of it
+    // (NOSA_SPLIT_SCAN=1).  Measured (tools/r2y.sh, two alternations): cfg 2 46.3K vs 45.2K tok/s
+    // fused / split, 31 vs 38 us per 8-layer selection group; cfg 3 14.06K vs 14.15K (within
+    // run-to-run spread).  Fused, one CTA's scan overlaps another CTA's sort and plan on the SM.
+    dv.split_scan = getenv("NOSA_SPLIT_SCAN") ? 1 : 0;
     if (dv.split_scan) {
       ALLOC(dv.scr_lo, LBH * dv.NB);
       ALLOC(dv.scr_up, LBH * dv.NB);
