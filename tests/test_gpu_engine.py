@@ -231,16 +231,21 @@ def test_resident_prefill(dtype):
     ("nosa", "fp32", 3e4, 1e-4),   # large keys, tiny queries: the bound's relative terms dominate
     ("nosa", "fp32", 1.0, 0.0),    # zero queries: every pool score ties at 0, lowest blocks win
 ])
-def test_screened_selection_equals_full_f64_scan(selector, dtype, kscale, qscale):
+def test_screened_selection_equals_full_f64_scan(selector, dtype, kscale, qscale, monkeypatch):
     """The screened selector (bf16 pre-scan + f64 rescoring of the candidates) picks exactly the
-    blocks a full f64 scan of the pool picks, so every later quantity is bitwise identical."""
+    blocks a full f64 scan of the pool picks, so every later quantity is bitwise identical; the
+    pre-scan fused into select_plan (default) and as its own kernel (NOSA_SPLIT_SCAN) alike."""
     cfg = ONE_B_SMALL
     w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, 4)
     K, V = workload.prefix_kv(4, 6, cfg.n_kv_head, 6000, cfg.d_head)
     K = (K * kscale).astype(np.float32)
     K, V = K.reshape(2, 3, cfg.n_kv_head, 6000, cfg.d_head), V.reshape(2, 3, cfg.n_kv_head, 6000, cfg.d_head)
     runs = []
-    for exact in (True, False):
+    for exact, split in ((True, False), (False, False), (False, True)):
+        if split:
+            monkeypatch.setenv("NOSA_SPLIT_SCAN", "1")  # read when the context is created
+        else:
+            monkeypatch.delenv("NOSA_SPLIT_SCAN", raising=False)
         eng = NosaEngine(cfg, batch=3, layers=2, max_tokens=6100, fast_slots=75, w1=w1, w2=w2, dtype=dtype,
                          exact_scan=exact)
         eng.prefill(torch.from_numpy(K), torch.from_numpy(V))
@@ -254,12 +259,13 @@ def test_screened_selection_equals_full_f64_scan(selector, dtype, kscale, qscale
         st = eng.residency_stats()
         runs.append((np.stack(outs), sels, (st.hits, st.misses, st.evictions)))
         eng.close()
-    np.testing.assert_array_equal(runs[0][0], runs[1][0])
-    assert runs[0][2] == runs[1][2]
-    for a, b in zip(runs[0][1], runs[1][1]):
-        for la, lb in zip(a, b):
-            for x, y in zip(la, lb):
-                np.testing.assert_array_equal(x, y)
+    for other in runs[1:]:
+        np.testing.assert_array_equal(runs[0][0], other[0])
+        assert runs[0][2] == other[2]
+        for a, b in zip(runs[0][1], other[1]):
+            for la, lb in zip(a, b):
+                for x, y in zip(la, lb):
+                    np.testing.assert_array_equal(x, y)
 
 
 @pytest.mark.parametrize("gather", ["memcpy", "uva", "tma"])
