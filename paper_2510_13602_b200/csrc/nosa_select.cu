@@ -373,6 +373,14 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
   const int r_begin = max(recent_lo, a_end);
   const int Pp = next_pow2(P);
 
+  // (0) fused scan: pull the pool's bf16 rows and their bounds toward L2 while q_sum forms (they
+  //     do not depend on q), so the pre-scan's dependent loads hit L2
+  if (dv.screen && !SPLIT && P > 0) {
+    const char* rows = reinterpret_cast<const char*>(dv.kc16 + ((size_t)lbh * dv.NB + pool_lo) * D);
+    const int lines = (int)(((size_t)P * D * 2 + 127) / 128);
+    for (int i = tid; i < lines; i += blockDim.x) prefetch_l2(rows + (size_t)i * 128);
+    if (tid < (P * 4 + 127) / 128) prefetch_l2(reinterpret_cast<const char*>(dv.kc_err + (size_t)lbh * dv.NB + pool_lo) + tid * 128);
+  }
   // (1) q_sum = sum of the group's query heads (decode.py:171-172), f64 (split scan: the scan
   //     kernel computed and stored it)
   if (tid == 0) sm.misc[M_QMAX] = 0;
@@ -380,12 +388,20 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
   if (SPLIT) {
     for (int i = tid; i < D; i += blockDim.x) sm.qsum[i] = __ldcg(dv.qsum_buf + (size_t)lbh * D + i);
   } else for (int i = tid; i < D; i += blockDim.x) {
+    const T* qg = q + ((size_t)b * dv.Hq + h * dv.G) * D + i;
+    T v[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) if (g < dv.G) v[g] = qg[(size_t)g * D];  // every load in flight
     double acc = 0.0;
-    for (int g = 0; g < dv.G; ++g) acc += to_f64(q[((size_t)b * dv.Hq + h * dv.G + g) * D + i]);
+#pragma unroll
+    for (int g = 0; g < 8; ++g) if (g < dv.G) acc += to_f64(v[g]);        // in head order
+    for (int g = 8; g < dv.G; ++g) acc += to_f64(qg[(size_t)g * D]);
     sm.qsum[i] = acc;
     if (dv.screen) {
       dv.qsum_buf[(size_t)lbh * D + i] = acc;
-      atomicMax(&sm.misc[M_QMAX], __float_as_int(__double2float_ru(fabs(acc))));  // |q| bits order as ints
+      const int bits = __float_as_int(__double2float_ru(fabs(acc)));  // |q| bits order as ints
+      const int wmax = __reduce_max_sync(__activemask(), bits);
+      if (lane == __ffs(__activemask()) - 1) atomicMax(&sm.misc[M_QMAX], wmax);
     }
   }
   __syncthreads();
