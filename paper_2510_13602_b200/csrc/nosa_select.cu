@@ -373,14 +373,6 @@ __device__ void select_phase(const Dev& dv, int layer, int b, int h, const T* __
   const int r_begin = max(recent_lo, a_end);
   const int Pp = next_pow2(P);
 
-  // (0) fused scan: pull the pool's bf16 rows and their bounds toward L2 while q_sum forms (they
-  //     do not depend on q), so the pre-scan's dependent loads hit L2
-  if (dv.screen && !SPLIT && P > 0) {
-    const char* rows = reinterpret_cast<const char*>(dv.kc16 + ((size_t)lbh * dv.NB + pool_lo) * D);
-    const int lines = (int)(((size_t)P * D * 2 + 127) / 128);
-    for (int i = tid; i < lines; i += blockDim.x) prefetch_l2(rows + (size_t)i * 128);
-    if (tid < (P * 4 + 127) / 128) prefetch_l2(reinterpret_cast<const char*>(dv.kc_err + (size_t)lbh * dv.NB + pool_lo) + tid * 128);
-  }
   // (1) q_sum = sum of the group's query heads (decode.py:171-172), f64 (split scan: the scan
   //     kernel computed and stored it)
   if (tid == 0) sm.misc[M_QMAX] = 0;
