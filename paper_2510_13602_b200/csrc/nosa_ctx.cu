@@ -1226,7 +1226,8 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
   std::vector<std::pair<int, int>>& groups = ctx->groups;
   groups.clear();
   if (grouped) {
-    // sizes nl, nl, 2nl, 4nl, ... (nl = layers per attention batch): batch k's plans complete together
+    // group sizes (nl = layers of the first attention batch): 1, 1, 2, 4, ... when every layer has its
+    // own attention launch (offloaded), nl, 2nl, 4nl, ... when attention is batched
     const int nlb = ctx->att_plan[0];  // the first attention batch waits for the first group only
     if (const char* e = getenv("NOSA_SELECT_PLAN")) {  // experiments: "a,b,..." layers per group
       int l0 = 0;
@@ -1238,6 +1239,10 @@ static int enqueue_step(NosaCtx* ctx, const NosaStepIO* io, cudaStream_t st, boo
         if (*x == ',') ++x;
       }
       if (l0 < dv.L) groups.push_back({l0, dv.L - l0});
+    } else if (nlb > 1) {
+      // batched attention (all resident): the first batch's group, then doubling (8, 16, 4 at
+      // L = 28): measured 46.7K vs 46.4K tok/s for 8, 8, 12 at cfg 2 (tools/r2ac.sh)
+      for (int l0 = 0, n = nlb; l0 < dv.L; l0 += n, n *= 2) groups.push_back({l0, std::min(n, dv.L - l0)});
     } else {
       for (int l0 = 0, n = nlb; l0 < dv.L; l0 += n, n = std::max(nlb, l0)) groups.push_back({l0, std::min(n, dv.L - l0)});
     }
