@@ -105,7 +105,7 @@ constexpr int kFinThreads = 256;
 constexpr int kFinMaxRows = 16;  // eviction-head rows per thread (D / (kFinThreads / n_ev))
 
 template <typename T>
-__device__ void finalize_bh(const Dev& dv, int layer, int bh, int nc, const T* __restrict__ kn,
+__device__ void finalize_bh(const Dev& dv, int layer, int bh, const T* __restrict__ kn,
                             const T* __restrict__ vn, float* __restrict__ out, float* wsm, double* zsm) {
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int b = bh / dv.H, h = bh % dv.H;
@@ -114,8 +114,10 @@ __device__ void finalize_bh(const Dev& dv, int layer, int bh, int nc, const T* _
   const T* kr = kn + ((size_t)b * dv.H + h) * D;
   const T* vr = vn + ((size_t)b * dv.H + h) * D;
 
-  // ---- (0) independent loads: t, the new row's 16-byte chunks, eviction-head operands, tail sums
+  // ---- (0) independent loads: t, the record count, the new row's 16-byte chunks, eviction-head
+  //          operands, tail sums
   const int t = __ldcg(dv.t + lbh);
+  const int n_req = __ldcg(dv.n_req + (size_t)layer * dv.B * dv.H + bh);
   const int cpr = D * elem / 16;  // 16-byte chunks per row
   int4 rowv = make_int4(0, 0, 0, 0);
   if (tid < 2 * cpr) rowv = reinterpret_cast<const int4*>(tid < cpr ? (const void*)kr : (const void*)vr)[tid % cpr];
@@ -142,6 +144,9 @@ __device__ void finalize_bh(const Dev& dv, int layer, int bh, int nc, const T* _
     kv = to_f64(kr[tid]);
   }
   const double tse = __ldcg(dv.tail_se + lbh);
+
+  const int nc = (n_req + dv.chunk - 1) / dv.chunk;
+  if (nc == 0) return;  // the plan failed for this manager (CapacityExceeded): no step
 
   // ---- (1) merge the split-K records in record order (deterministic), thread -> (query, 4 dims)
   {
@@ -786,9 +791,7 @@ __global__ void __launch_bounds__(kFinThreads)
   float* wsm = reinterpret_cast<float*>(zsm + dv.n_ev);         // [kFinThreads] f64 reduction scratch
   const int bh = blockIdx.x, layer = layer0 + blockIdx.y;
   const size_t kst = (size_t)dv.B * dv.H * dv.D, ost = (size_t)dv.B * dv.Hq * dv.D;
-  const int nc = (dv.n_req[layer * dv.B * dv.H + bh] + dv.chunk - 1) / dv.chunk;
-  if (nc == 0) return;  // the plan failed for this manager (CapacityExceeded): no step
-  finalize_bh<T>(dv, layer, bh, nc, kn0 + blockIdx.y * kst, vn0 + blockIdx.y * kst, out0 + blockIdx.y * ost, wsm, zsm);
+  finalize_bh<T>(dv, layer, bh, kn0 + blockIdx.y * kst, vn0 + blockIdx.y * kst, out0 + blockIdx.y * ost, wsm, zsm);
 }
 
 // layers [layer, layer + nl): kn/vn/out point at layer `layer`'s rows
