@@ -379,6 +379,17 @@ int nosa_mgr_free(NosaMgr* mgr, int head, int id);
  * NOSA_ERR_UNKNOWN_KEY. */
 int nosa_mgr_plan(NosaMgr* mgr, int head, int batch, const int32_t* ids, int n, int32_t* fetch, int32_t* n_fetch,
                   int32_t* evict, int32_t* n_evict, int32_t* hits);
+/* plan_transfers with a caller-supplied eviction_policy (kv_manager.py:133-138, 236-250): the same
+ * clock tick, recency stamps, fetch ids and hits as nosa_mgr_plan, but no victim choice. When
+ * evictions are needed (*shortfall > 0), `candidates` receives the ids of the evictable FAST keys
+ * (every FAST key of the head but this call's required ones, in fast-slot order) for the caller's
+ * policy to order; the caller takes the first *shortfall of its order (CapacityExceeded when the
+ * policy returns fewer). `candidates` holds fast_blocks ids. */
+int nosa_mgr_plan_policy(NosaMgr* mgr, int head, int batch, const int32_t* ids, int n, int32_t* fetch,
+                         int32_t* n_fetch, int32_t* shortfall, int32_t* candidates, int32_t* n_cand, int32_t* hits);
+/* last_required clock of every id of a head ([fast_blocks + slow_blocks]; 0 = never required),
+ * the reference's `last_required` map handed to an eviction policy */
+int nosa_mgr_recency(NosaMgr* mgr, int head, uint32_t* last);
 /* apply_transfers' moves (kv_manager.py:276-298): evictions FAST -> SLOW then fetches SLOW -> FAST,
  * one _move at a time; copy_payload: the default mover's payload copies, on the device.
  * moves (optional): [n_evict + n_fetch][2] source and destination slot of each move (-1, -1 =

@@ -118,6 +118,8 @@ SIGNATURES = {
     "nosa_mgr_free": (_I, [_P, _I, _I]),
     "nosa_mgr_plan": (_I, [_P, _I, _I, _I32P, _I, _I32P, _I32P, _I32P, _I32P, _I32P]),
     "nosa_mgr_apply": (_I, [_P, _I, _I32P, _I, _I32P, _I, _I, _I32P]),
+    "nosa_mgr_plan_policy": (_I, [_P, _I, _I, _I32P, _I, _I32P, _I32P, _I32P, _I32P, _I32P, _I32P]),
+    "nosa_mgr_recency": (_I, [_P, _I, _P]),
     "nosa_mgr_lookup": (_I, [_P, _I, _I, _I32P, _I32P]),
     "nosa_mgr_tables": (_I, [_P, _I, _P, _I32P]),
     "nosa_mgr_audit": (_I, [_P, _I32P]),

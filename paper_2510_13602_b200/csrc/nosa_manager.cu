@@ -103,7 +103,10 @@ __device__ __forceinline__ bool vless(const VKey& a, const VKey& b) {
 // io in:  [0] n required, [1..n] ids in ascending block order (-1 = unmapped key)
 // io out: base = 1 + n: [base] n_fetch, [base+1] n_evict, [base+2] hits,
 //         fetch ids at base+3.., evict ids after them (victim order)
-__global__ void __launch_bounds__(kThreads) mgr_plan_kernel(Mgr m, int h, int batch) {
+// policy != 0 (a caller-supplied eviction_policy, kv_manager.py:133-138): no victim choice; when
+//         evictions are needed, the evictable candidates (kv_manager.py:236-243) follow the fetch
+//         ids as [count][ids in fast-slot order] for the caller to order
+__global__ void __launch_bounds__(kThreads) mgr_plan_kernel(Mgr m, int h, int batch, int policy) {
   __shared__ unsigned hist[256];
   __shared__ int s_cnt, s_nf, s_hits, s_digit, s_below, s_nv, s_unknown;
   __shared__ VKey s_thr;
@@ -149,7 +152,19 @@ __global__ void __launch_bounds__(kThreads) mgr_plan_kernel(Mgr m, int h, int ba
   const int nf = s_nf;
   const int shortfall = nf - m.tops[2 * h];
   int* ev = out + 3 + nf;
-  if (shortfall > 0) {
+  if (shortfall > 0 && policy) {
+    if (tid == 0) {
+      const int* fid = m.fast_id + (size_t)h * m.F;
+      int nc = 0;
+      for (int s = 0; s < m.F; ++s) {
+        const int id = fid[s];
+        if (id < 0) continue;
+        const size_t k = (size_t)h * m.ids + id;
+        if (!(m.last[k] == clock && m.kb[k].x == batch)) ev[1 + nc++] = id;
+      }
+      ev[0] = nc;
+    }
+  } else if (shortfall > 0) {
     // (2) candidates: FAST keys of the head not (batch == b and block in required): the
     //     required ids of this call carry last == clock and batch == b, so they are exactly the
     //     FAST keys with last == clock and kb.x == batch (a key of another batch keeps last <
@@ -496,7 +511,7 @@ extern "C" int nosa_mgr_plan(NosaMgr* g, int head, int batch, const int32_t* ids
   g->h_io[0] = n;
   std::copy(ids, ids + n, g->h_io + 1);
   MGR_TRY(g, cudaMemcpyAsync(g->m.io, g->h_io, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, g->st));
-  mgr_plan_kernel<<<1, kThreads, 0, g->st>>>(g->m, head, batch);
+  mgr_plan_kernel<<<1, kThreads, 0, g->st>>>(g->m, head, batch, 0);
   if (int rc = finish(g, "plan_transfers")) return rc;
   const size_t base = 1 + n;
   MGR_TRY(g, cudaMemcpyAsync(g->h_io + base, g->m.io + base, 3 * sizeof(int), cudaMemcpyDeviceToHost, g->st));
@@ -594,5 +609,43 @@ extern "C" int nosa_mgr_free_lists(NosaMgr* g, int head, int32_t* fast, int32_t*
   MGR_TRY(g, cudaMemcpy(slow, g->m.slow_free + (size_t)head * g->m.S, tops[1] * sizeof(int), cudaMemcpyDeviceToHost));
   *n_fast = tops[0];
   *n_slow = tops[1];
+  return NOSA_OK;
+}
+
+extern "C" int nosa_mgr_plan_policy(NosaMgr* g, int head, int batch, const int32_t* ids, int n, int32_t* fetch,
+                                    int32_t* n_fetch, int32_t* shortfall, int32_t* candidates, int32_t* n_cand,
+                                    int32_t* hits) {
+  if (!g || n < 0 || (n && !ids) || !fetch || !n_fetch || !shortfall || !candidates || !n_cand || !hits)
+    return NOSA_ERR_VALUE;
+  if (head < 0 || head >= g->m.H) return mfail(g, NOSA_ERR_VALUE, "head %d out of range", head);
+  cudaSetDevice(g->device);
+  if (n > g->m.F) n = g->m.F + 1;
+  g->h_io[0] = n;
+  std::copy(ids, ids + n, g->h_io + 1);
+  MGR_TRY(g, cudaMemcpyAsync(g->m.io, g->h_io, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, g->st));
+  mgr_plan_kernel<<<1, kThreads, 0, g->st>>>(g->m, head, batch, 1);
+  if (int rc = finish(g, "plan_transfers")) return rc;
+  const size_t base = 1 + n;
+  // fetch ids, then (when evictions are needed) the candidate count and ids: at most 3 + F + 1 + F
+  const size_t span = std::min<size_t>(4 + 2 * (size_t)g->m.F, g->io_ints - 1 - base);
+  MGR_TRY(g, cudaMemcpyAsync(g->h_io + base, g->m.io + base, span * sizeof(int), cudaMemcpyDeviceToHost, g->st));
+  MGR_TRY(g, cudaStreamSynchronize(g->st));
+  const int nf = g->h_io[base], sf = g->h_io[base + 1];
+  *n_fetch = nf;
+  *shortfall = sf;
+  *hits = g->h_io[base + 2];
+  std::copy(g->h_io + base + 3, g->h_io + base + 3 + nf, fetch);
+  const int nc = sf > 0 ? g->h_io[base + 3 + nf] : 0;
+  *n_cand = nc;
+  std::copy(g->h_io + base + 4 + nf, g->h_io + base + 4 + nf + nc, candidates);
+  return NOSA_OK;
+}
+
+extern "C" int nosa_mgr_recency(NosaMgr* g, int head, uint32_t* last) {
+  if (!g || head < 0 || head >= g->m.H || !last) return NOSA_ERR_VALUE;
+  cudaSetDevice(g->device);
+  MGR_TRY(g, cudaMemcpyAsync(last, g->m.last + (size_t)head * g->m.ids, g->m.ids * sizeof(unsigned),
+                             cudaMemcpyDeviceToHost, g->st));
+  MGR_TRY(g, cudaStreamSynchronize(g->st));
   return NOSA_OK;
 }

@@ -117,17 +117,18 @@ class TieredBlockManager:
     same fetch and victim lists, the same exceptions (LayoutMismatch, DuplicateKey, OutOfBlocks,
     UnknownKey, CapacityExceeded, StalePlan) and the same side effects of a failing call.  A custom
     `mover(key, src, dst)` is called once per move in the reference's order with the same
-    (tier, head, slot) locations, after the device has executed the plan.  Only the default
-    least-recently-required eviction order is available (it is the one the device computes);
-    passing another policy raises ValueError."""
+    (tier, head, slot) locations, after the device has executed the plan.  The default
+    least-recently-required victim order runs on the device (a radix select over the head's fast
+    keys).  A caller-supplied `eviction_policy(candidates, last_required)` (kv_manager.py:133-138)
+    is user code and runs on the host: the device plans the fetches and stamps recency, hands back
+    the evictable fast keys, and the policy's first `shortfall` keys become the victims
+    (kv_manager.py:236-250).  Its `last_required` map holds the planned head's keys with a nonzero
+    clock (the reference passes every head's)."""
 
     def __init__(self, fast: PhysicalLayout, slow: PhysicalLayout, store_payload: bool = False,
                  eviction_policy=least_recently_required, device: int = 0):
         if fast.tier != FAST or slow.tier != SLOW:
             raise LayoutMismatch("pass layouts as (fast, slow)")
-        if eviction_policy is not least_recently_required:
-            raise ValueError("only the least-recently-required eviction policy (kv_manager.py:125-127) runs on "
-                             "the device")
         self.eviction_policy = eviction_policy
         for attr in ("heads", "n_b", "d_head", "element_width"):
             if getattr(fast, attr) != getattr(slow, attr):
@@ -151,6 +152,7 @@ class TieredBlockManager:
         I32 = lambda n: (ctypes.c_int32 * max(n, 1))()
         self._buf = [I32(self._cap) for _ in range(3)]      # call scratch: ids in, fetch, evict
         self._moves = I32(4 * self._cap)
+        self._cand = I32(fast.num_blocks)
 
     def _call(self, fn, *args):
         _lib.check(fn(self._h, *args), mgr=self._h)
@@ -219,18 +221,41 @@ class TieredBlockManager:
         for i, b in enumerate(required):
             buf[i] = ids.get((batch, head, b), -1)
         nf, ne, hits = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        custom = self.eviction_policy is not least_recently_required
+        nc = ctypes.c_int32()
         try:
-            self._call(_lib.lib.nosa_mgr_plan, head, batch, buf, n, self._buf[1], ctypes.byref(nf), self._buf[2],
-                       ctypes.byref(ne), ctypes.byref(hits))
+            if custom:
+                self._call(_lib.lib.nosa_mgr_plan_policy, head, batch, buf, n, self._buf[1], ctypes.byref(nf),
+                           ctypes.byref(ne), self._cand, ctypes.byref(nc), ctypes.byref(hits))
+            else:
+                self._call(_lib.lib.nosa_mgr_plan, head, batch, buf, n, self._buf[1], ctypes.byref(nf),
+                           self._buf[2], ctypes.byref(ne), ctypes.byref(hits))
         except UnknownKey:
             bad = next((batch, head, b) for b in required if (batch, head, b) not in ids)
             raise UnknownKey(f"required block {bad} exists in no tier") from None
         keys = self._keys[head]
         fetch = [keys[self._buf[1][i]] for i in range(nf.value)]
-        evict = [keys[self._buf[2][i]] for i in range(ne.value)]
+        if custom:
+            evict = []
+            shortfall = ne.value
+            if shortfall > 0:  # kv_manager.py:234-250
+                evictable = self.eviction_policy([keys[self._cand[i]] for i in range(nc.value)],
+                                                 self._last_required(head))
+                if shortfall > len(evictable):
+                    raise CapacityExceeded(f"need {shortfall} evictions for head {head} but only "
+                                           f"{len(evictable)} blocks are evictable")
+                evict = list(evictable[:shortfall])
+        else:
+            evict = [keys[self._buf[2][i]] for i in range(ne.value)]
         bpb = self.bytes_per_block
         return TransferPlan(fetch=fetch, evict=evict, bytes_up=len(fetch) * bpb, bytes_down=len(evict) * bpb,
                             hits=hits.value, misses=len(fetch), version=self.version)
+
+    def _last_required(self, head: int) -> dict:
+        """The head's keys with a nonzero last-required clock (the reference's `last_required`)."""
+        last = np.empty(max(self._cap, 1), np.uint32)
+        self._call(_lib.lib.nosa_mgr_recency, head, last.ctypes.data)
+        return {key: int(last[kid]) for kid, key in self._keys[head].items() if last[kid]}
 
     def apply_transfers(self, plan: TransferPlan, mover=None):
         if plan.version != self.version:

@@ -190,7 +190,7 @@ def test_projection_rejects_untileable_shapes_without_a_gpu():
 
 def test_tiered_block_manager_constructor_contract():
     """The drop-in TieredBlockManager validates like the reference before touching the device
-    (kv_manager.py:59-81, 138-146): layout checks, tier order, the only supported policy."""
+    (kv_manager.py:59-81, 138-146): layout checks and tier order; the default policy."""
     from paper_2510_13602_b200 import FAST, SLOW, LayoutMismatch, PhysicalLayout, TieredBlockManager
     from paper_2510_13602_b200.kv_manager import least_recently_required
     with pytest.raises(ValueError):
@@ -203,7 +203,5 @@ def test_tiered_block_manager_constructor_contract():
         TieredBlockManager(slow, fast)
     with pytest.raises(LayoutMismatch, match="disagree"):
         TieredBlockManager(fast, PhysicalLayout(SLOW, 8, 3, 4, 8))
-    with pytest.raises(ValueError, match="policy"):
-        TieredBlockManager(fast, slow, eviction_policy=lambda c, last: c)
     keys = [(1, 0, 5), (0, 0, 9), (0, 0, 2)]
     assert least_recently_required(keys, {(0, 0, 9): 3}) == [(0, 0, 2), (1, 0, 5), (0, 0, 9)]
