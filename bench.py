@@ -81,6 +81,8 @@ def parse():
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
     ap.add_argument("--selector", choices=["nosa", "infllmv2"], default="nosa")
+    ap.add_argument("--dtype", choices=["bf16", "fp32"], default="bf16",
+                    help="KV / query storage: bf16 (tensor-core attention) or fp32 (the 1e-5 parity path)")
     ap.add_argument("--layers", type=int, default=None, help="override (for quick local checks only)")
     ap.add_argument("--batch", type=int, default=None, help="override (for quick local checks only)")
     ap.add_argument("--seed", type=int, default=0)
@@ -145,8 +147,13 @@ def bench_config(args, w, world) -> dict:
             "parallelism": f"dp{world} (batch-sharded, no data-path collective)",
             "inputs": f"counter-based synthetic q / k_new / v_new and prefix K/V (seed {args.seed}), identical bits "
                       f"on the GPU and in the CPU oracle",
+            "kv_storage": getattr(args, "dtype", "bf16"),
             "host_memory_limited_batch": w["host_limited"],
             "l2": "no flush needed: attended KV per layer-step exceeds the 126 MB L2"}
+
+
+def elem_bytes(args) -> int:
+    return 4 if getattr(args, "dtype", "bf16") == "fp32" else 2
 
 
 def workload_dims(args, world):
@@ -164,7 +171,7 @@ def workload_dims(args, world):
         import torch
         n_blocks = -(-(w["context"] + 256) // 64)
         frac = 1.0 if w["cache"] == "resident" else 1.0 + w["cache"]
-        per_seq = w["layers"] * 2 * n_blocks * (2 * 64 * 128 * 2 * frac + 128 * 10)
+        per_seq = w["layers"] * 2 * n_blocks * (2 * 64 * 128 * elem_bytes(args) * frac + 128 * 10)
         budget = int(0.55 * torch.cuda.get_device_properties(0).total_memory)
         if per_seq * w["batch_local"] > budget:
             w["batch_local"] = max(1, budget // int(per_seq))
@@ -174,7 +181,7 @@ def workload_dims(args, world):
         # (the reference arm sizes the same way, so both arms name the same batch)
         local = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
         n_blocks = -(-(w["context"] + 256) // 64)
-        per_seq = w["layers"] * 2 * n_blocks * 2 * 64 * 128 * 2  # [layers][kv heads][blocks] x 32 KiB
+        per_seq = w["layers"] * 2 * n_blocks * 2 * 64 * 128 * elem_bytes(args)  # [layers][kv heads][blocks] x 32 KiB
         avail = host_mem_available()
         budget = int(0.8 * avail / local) if avail else None
         if budget is not None and per_seq * w["batch_local"] > budget:
@@ -354,7 +361,9 @@ def run_native(args, rank, world, local_rank):
     cfg = attention_config(w["shape"])
     L, B, ctx_len, seq0 = w["layers"], w["batch_local"], w["context"], w["seq0"]
     max_tokens, nblk, fast = token_budget(args, w)
-    dtype = torch.bfloat16
+    dtype = torch.float32 if args.dtype == "fp32" else torch.bfloat16
+    if args.dtype == "fp32" and args.inputs == "hidden":
+        raise SystemExit("bench: --inputs hidden projects in bf16 on the tensor cores; use --dtype bf16")
     peer_dev = None
     if args.slow_tier == "peer":  # the slow tier in another GPU's HBM (alone on the box: loopback)
         ngpu = torch.cuda.device_count()
@@ -369,7 +378,7 @@ def run_native(args, rank, world, local_rank):
     # strong scaling splits a fixed global batch: pin the split-K chunk (the automatic one follows
     # the local batch) so every sequence's outputs are bit-identical at 1, 2, 4 and 8 GPUs
     chunk = 8 if w.get("strong") else 0
-    eng = NosaEngine(cfg, batch=B, layers=L, max_tokens=max_tokens, fast_slots=fast, w1=w1, w2=w2, dtype="bf16",
+    eng = NosaEngine(cfg, batch=B, layers=L, max_tokens=max_tokens, fast_slots=fast, w1=w1, w2=w2, dtype=args.dtype,
                      device=local_rank, slow_tier=slow_tier, attend_chunk=chunk)
     t_alloc = time.time() - t_setup
     # inputs: counter-based draws addressed by GLOBAL sequence id (a rank's shard draws the same
@@ -615,9 +624,10 @@ def run_native(args, rank, world, local_rank):
     traffic = None
     tpath = ROOT / "profiles" / "traffic.json"
     if tpath.exists():
-        traffic = json.loads(tpath.read_text()).get(f"{args.workload}:attend")
+        traffic = json.loads(tpath.read_text()).get(f"{args.workload}:attend" + ("" if args.dtype == "bf16" else ":fp32"))
     att = kern["attend"]
-    roofline = {"bound": "hbm", "kernel": "attend_bf16_kernel (K4+K5)", "achieved": round(att["gbs"], 1),
+    roofline = {"bound": "hbm", "kernel": "attend_f32_kernel (K4+K5, fp32 CUDA cores)" if args.dtype == "fp32" else
+                "attend_bf16_kernel (K4+K5)", "achieved": round(att["gbs"], 1),
                 "peak": hbm_peak, "unit": "GB/s", "frac": round(att["gbs"] / hbm_peak, 4), "traffic": traffic,
                 "peak_kind": peak_kind, "bytes_per_launch": int(per_launch["attend"]),
                 "avg_launch_ms": round(att["avg_ms"], 5),
@@ -682,10 +692,10 @@ def run_native(args, rank, world, local_rank):
             "metric": METRIC, "value": round(tokens / (ms_max * 1e-3), 2), "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
             "higher_is_better": True, "scaling": "strong" if w.get("strong") else "weak", "vs_baseline": None,
-            "dtype": "bf16",
+            "dtype": args.dtype,
             "data": (f"synthetic: K/V ~ N(0,1) bf16 (counter-based), AR(1) hidden states rho={w['rho']} through "
                      f"random per-layer projections (torch Philox / numpy PCG64, seed {args.seed})" if hidden else
-                     f"synthetic: K/V ~ N(0,1) bf16, AR(1) queries rho={w['rho']} (counter-based generator, seed "
+                     f"synthetic: K/V ~ N(0,1) {args.dtype}, AR(1) queries rho={w['rho']} (counter-based generator, seed "
                      f"{args.seed}: the same bits on the GPU and in the CPU oracle)"),
             "config": bench_config(args, w, world),
             "run": {"gather": args.gather, "schedule": args.schedule, "burn_in_steps": args.burn_in,
@@ -728,8 +738,10 @@ def cpu_baseline_sample(args, cfg, w, rec, device, fast, max_tokens):
     host core: the reference algorithm (attend_biased dense over every cached token, K re-pooled
     every step, TieredBlockManager with 32 KiB payload copies) on the identical inputs.  Times it
     (cpu_baseline) and compares every decision with the GPU's (parity): blocks_q, blocks_e,
-    required, fetch (plan order), evict (LRR order), hits exactly; outputs within 2e-2."""
+    required, fetch (plan order), evict (LRR order), hits exactly; outputs within 2e-2 (bf16 storage) or
+    1e-5 (fp32 storage)."""
     import numpy as np
+    import torch
 
     from oracle import nosa_oracle as O
     from paper_2510_13602_b200 import synth, workload
@@ -741,7 +753,8 @@ def cpu_baseline_sample(args, cfg, w, rec, device, fast, max_tokens):
     mism = {"blocks_q": 0, "blocks_e": 0, "required": 0, "fetch": 0, "evict": 0, "hits": 0}
     ties = evictions = fetches = 0
     for (l, b), steps in rec.items():
-        k, v = synth.prefix_kv(args.seed, l, w["seq0"] + b, 1, H, w["context"], cfg.d_head, device)
+        k, v = synth.prefix_kv(args.seed, l, w["seq0"] + b, 1, H, w["context"], cfg.d_head, device,
+                               torch.float32 if args.dtype == "fp32" else torch.bfloat16)
         k, v = k[0].float().cpu().numpy(), v[0].float().cpu().numpy()
         orc = O.OracleEngine(oc, 1, 1, max_tokens, fast, w1, w2, store_payload=True, dense=True)
         t0 = time.perf_counter()
@@ -781,7 +794,7 @@ def cpu_baseline_sample(args, cfg, w, rec, device, fast, max_tokens):
               "sel_mismatch": mism["blocks_q"] + mism["blocks_e"], "required_mismatch": mism["required"],
               "fetch_mismatch": mism["fetch"], "evict_mismatch": mism["evict"], "hit_mismatch": mism["hits"],
               "ties_reported": ties, "fetches_checked": fetches, "evictions_checked": evictions,
-              "max_rel_err": worst, "tolerance": 2e-2,
+              "max_rel_err": worst, "tolerance": 1e-5 if args.dtype == "fp32" else 2e-2,
               "what": "GPU vs oracle on identical inputs, every (step, head) of the sampled pairs: blocks_q, "
                       "blocks_e, required, fetch list, evict list, hits exactly; outputs max|o-o_ref|/max|o_ref|"}
     return cpu, parity

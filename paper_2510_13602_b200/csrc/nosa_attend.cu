@@ -778,6 +778,347 @@ __global__ void __launch_bounds__(32)
   }
 }
 
+// ---------------------------------------------------------------- fp32 CUDA-core kernel, warp group
+// fp32 storage (tolerance 1e-5): one persistent CTA per SM, the same chunk decomposition and
+// (m, l, O) records as the bf16 kernel, so the finalize merge is shared.
+//   copy warp      claims chunks, loads their metadata lane-parallel (required block, slot, bias,
+//                  live tokens), and streams each K|V block (2 n_b d_head fp32) HBM -> shared
+//                  memory with one 1-D bulk copy into a ring of NS stages; a chunk's query rows
+//                  ride on its first block's barrier.
+//   NW consumer    warps share every block.  QK: a key's dot products are split over LPK lanes
+//   warps          (DPL dims each, the group's queries in registers), then reduced with a
+//                  reduce-scatter butterfly (GP values over LPK lanes: one lane per query head
+//                  ends with its sum).  Online softmax: one warp per query head, accurate expf.
+//                  PV: each warp owns NBK/NW keys and DH/32 dims per lane for every query head;
+//                  per-warp partials are rescaled per block and summed over the warps in a fixed
+//                  tree at the chunk end (deterministic).  fp32 FMA throughout.
+template <int NBK, int DH, int GP>
+struct F32W {
+  static constexpr int NW = 8;                      // consumer warps
+  static constexpr int THREADS = (NW + 1) * 32;     // + the copy warp
+  static constexpr int BPB = 2 * NBK * DH * 4;      // one K|V block
+  static constexpr int PLANE = NBK * DH * 4;
+  static constexpr int DPL = GP >= 16 ? 4 : 8;      // QK dims per lane
+  static constexpr int LPK = DH / DPL;              // lanes per key
+  static constexpr int KPI = 32 / LPK;              // keys per warp iteration
+  static constexpr int PCH = DPL / 4;               // 16-byte pieces per lane
+  static constexpr int DPV = DH / 32;               // PV dims per lane
+  static constexpr int QSLOT = GP * DH * 4;
+  static constexpr int CB = 2;                      // partial buffers of the chunk-end tree
+  // everything but the stages, the query slots and the unit table (cbase)
+  static constexpr int FIXED = NBK * GP * 4 * 2 + CB * GP * DH * 4 + 3 * GP * 4 + 16 + 32 * 4 + 128;
+  static constexpr int PER_STAGE = BPB + QSLOT + 16 + 20;
+  // stages: as many as fit 227 KiB with 4 KiB left for the unit table, 2 to 4
+  static constexpr int NS_FIT = (232448 - 4096 - FIXED) / PER_STAGE;
+  static constexpr int NS = NS_FIT < 2 ? 2 : (NS_FIT > 4 ? 4 : NS_FIT);
+  static size_t smem(int units) { return (size_t)FIXED + (size_t)NS * PER_STAGE + (size_t)(units + 1) * 4; }
+  static_assert(GP <= LPK, "query heads per key group must not exceed its lanes");
+  static_assert(NBK % NW == 0 || NBK < NW, "keys split over the warps");
+};
+
+struct F32Info {
+  int bh, ci, count, flags;  // flags: 1 first block of its chunk, 2 last, 4 end of work
+  float beta;
+};
+
+// one level of the butterfly: with V > 1 values, exchange half of them (lanes with bit O set keep
+// the upper half); with one value left, a plain butterfly add
+template <int V, int O>
+struct RS {
+  template <int N>
+  static __device__ __forceinline__ void run(float (&v)[N], int lane, int& base) {
+    if constexpr (O >= 1) {
+      if constexpr (V > 1) {
+        const bool up = (lane & O) != 0;
+#pragma unroll
+        for (int j = 0; j < V / 2; ++j) {
+          const float send = up ? v[j] : v[j + V / 2];
+          const float keep = up ? v[j + V / 2] : v[j];
+          v[j] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+        }
+        base += up ? V / 2 : 0;
+        RS<V / 2, O / 2>::run(v, lane, base);
+      } else {
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], O);
+        RS<1, O / 2>::run(v, lane, base);
+      }
+    }
+  }
+};
+
+template <int NBK, int DH, int GP>
+__global__ void __launch_bounds__(F32W<NBK, DH, GP>::THREADS, 1)
+    attend_f32w_kernel(Dev dv, int layer, int nl, const float* __restrict__ q, size_t q_layer_stride) {
+  using T = F32W<NBK, DH, GP>;
+  constexpr int NW = T::NW, LPK = T::LPK, KPI = T::KPI, DPL = T::DPL, DPV = T::DPV, NS = T::NS;
+  extern __shared__ __align__(128) char smem_raw[];
+  const int BHL = dv.B * dv.H;
+  const int BH = nl * BHL;
+  const int G = dv.G;
+  char* p = smem_raw;
+  char* stages = p;                                  p += (size_t)NS * T::BPB;
+  char* qslots = p;                                  p += (size_t)NS * T::QSLOT;
+  float* S = reinterpret_cast<float*>(p);            p += NBK * GP * 4;   // [GP][NBK] logits
+  float* P = reinterpret_cast<float*>(p);            p += NBK * GP * 4;   // [NBK][GP] probabilities
+  float* comb = reinterpret_cast<float*>(p);         p += T::CB * GP * DH * 4;
+  float* run_m = reinterpret_cast<float*>(p);        p += GP * 4;
+  float* run_l = reinterpret_cast<float*>(p);        p += GP * 4;
+  float* scl = reinterpret_cast<float*>(p);          p += GP * 4;
+  p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+  uint64_t* full = reinterpret_cast<uint64_t*>(p);   p += NS * 8;
+  uint64_t* empty = reinterpret_cast<uint64_t*>(p);  p += NS * 8;
+  F32Info* info = reinterpret_cast<F32Info*>(p);     p += NS * sizeof(F32Info);
+  int* tmp = reinterpret_cast<int*>(p);              p += 32 * 4;
+  int* cbase = reinterpret_cast<int*>(p);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned long long t_start = dv.ktime ? globaltimer_ns() : 0ull;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    fence_mbar_init();
+  }
+  if (G < GP)  // query rows past the group stay zero (only G rows are copied in)
+    for (int x = tid; x < NS * T::QSLOT / 16; x += blockDim.x) reinterpret_cast<int4*>(qslots)[x] = make_int4(0, 0, 0, 0);
+  for (int g = tid; g < GP; g += blockDim.x) {
+    run_m[g] = -INFINITY;
+    run_l[g] = 0.0f;
+  }
+  chunk_scan(dv, layer, cbase, tmp, BH);  // also publishes the barrier inits (__syncthreads)
+  const int total = cbase[BH];
+
+  if (warp == NW) {
+    // ------------------------------------------------------------ copy warp
+    int seq = 0, cn = 0;
+    int c = 0;
+    if (lane == 0) c = atomicAdd(dv.cnt + kCntStride * layer + 1, 1);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    while (c < total) {
+      const int u = find_bh(cbase, BH, c);
+      const int ci = c - cbase[u];
+      const int lbh = layer * BHL + u;  // units of the launch's layers are contiguous in lbh
+      const int rl = layer + u / BHL, bh = u % BHL;
+      const int n = __ldcg(dv.n_req + lbh);
+      const int t = __ldcg(dv.t + lbh);
+      const int i0 = ci * dv.chunk, nb = min(dv.chunk, n - i0);
+      // the chunk's blocks, lane-parallel: block, slot, bias, live tokens
+      int blk = 0, slot = 0, cnt = 0;
+      float beta = 0.0f;
+      if (lane < nb) {
+        blk = __ldcg(dv.req + (size_t)lbh * dv.C + i0 + lane);
+        slot = __ldcg(dv.req_slot + (size_t)lbh * dv.C + i0 + lane);
+        cnt = min(NBK, t - blk * NBK);
+        beta = block_beta(dv, lbh, blk, t);
+      }
+      // the next chunk's claim is in flight while this one streams
+      int c_next = 0;
+      if (lane == 0) c_next = atomicAdd(dv.cnt + kCntStride * layer + 1, 1);
+      const int b = bh / dv.H, h = bh % dv.H;
+      const float* qrow = q + (size_t)(rl - layer) * q_layer_stride + ((size_t)b * dv.Hq + h * G) * DH;
+      for (int i = 0; i < nb; ++i, ++seq) {
+        const int st = seq % NS;
+        const int si = __shfl_sync(0xffffffffu, slot, i);
+        const int ki = __shfl_sync(0xffffffffu, cnt, i);
+        const float be = __shfl_sync(0xffffffffu, beta, i);
+        if (lane == 0) {
+          if (seq >= NS) mbar_wait(&empty[st], ((seq / NS) - 1) & 1);
+          info[st] = F32Info{u, ci, ki, (i == 0 ? 1 : 0) | (i == nb - 1 ? 2 : 0), be};
+          fence_proxy_async();
+          const unsigned qbytes = i == 0 ? (unsigned)(G * DH * 4) : 0u;
+          mbar_expect_tx(&full[st], T::BPB + qbytes);
+          bulk_g2s(stages + (size_t)st * T::BPB, dv.pool + ((size_t)lbh * dv.C + si) * (size_t)T::BPB, T::BPB, &full[st]);
+          if (qbytes) bulk_g2s(qslots + (size_t)(cn % NS) * T::QSLOT, qrow, qbytes, &full[st]);
+        }
+      }
+      ++cn;
+      c = __shfl_sync(0xffffffffu, c_next, 0);
+    }
+    if (lane == 0) {  // end of work
+      const int st = seq % NS;
+      if (seq >= NS) mbar_wait(&empty[st], ((seq / NS) - 1) & 1);
+      info[st] = F32Info{-1, 0, 0, 4, 0.0f};
+      mbar_arrive_plain(&full[st]);
+    }
+  } else {
+    // ------------------------------------------------------------ consumer warps
+    const int dl = lane % LPK, kq = lane / LPK;
+    float qr[GP][DPL];
+    float o[GP][DPV];
+#pragma unroll
+    for (int g = 0; g < GP; ++g)
+#pragma unroll
+      for (int x = 0; x < DPV; ++x) o[g][x] = 0.0f;
+    int seq = 0, cn = 0;
+    for (;; ++seq) {
+      const int st = seq % NS;
+      mbar_wait(&full[st], (seq / NS) & 1);
+      const F32Info it = info[st];
+      if (it.flags & 4) break;
+      const char* kb = stages + (size_t)st * T::BPB;
+      const char* vb = kb + T::PLANE;
+      if (it.flags & 1) {  // chunk start: the group's query slice into registers
+        const float* qs = reinterpret_cast<const float*>(qslots + (size_t)(cn % NS) * T::QSLOT);
+#pragma unroll
+        for (int g = 0; g < GP; ++g)
+#pragma unroll
+          for (int j = 0; j < DPL / 4; ++j) {
+            const float4 v4 = *reinterpret_cast<const float4*>(qs + g * DH + 4 * (dl + j * LPK));
+            qr[g][4 * j] = v4.x;
+            qr[g][4 * j + 1] = v4.y;
+            qr[g][4 * j + 2] = v4.z;
+            qr[g][4 * j + 3] = v4.w;
+          }
+      }
+      const int count = it.count;
+      // ---- QK: logits + bias into S[g][key] (keys past the live tokens: -inf)
+#pragma unroll
+      for (int it0 = 0; it0 < (NBK + NW * KPI - 1) / (NW * KPI); ++it0) {
+        const int key = (it0 * NW + warp) * KPI + kq;
+        if ((it0 * NW + warp) * KPI >= NBK) break;  // warp-uniform
+        float v[GP];
+#pragma unroll
+        for (int g = 0; g < GP; ++g) v[g] = 0.0f;
+        if (key < count) {
+#pragma unroll
+          for (int j = 0; j < DPL / 4; ++j) {
+            const int chunk = dl + j * LPK;
+            const float4 k4 = *reinterpret_cast<const float4*>(kb + key * DH * 4 + ((chunk ^ (key & 7)) << 4));
+#pragma unroll
+            for (int g = 0; g < GP; ++g) {
+              v[g] = fmaf(qr[g][4 * j], k4.x, v[g]);
+              v[g] = fmaf(qr[g][4 * j + 1], k4.y, v[g]);
+              v[g] = fmaf(qr[g][4 * j + 2], k4.z, v[g]);
+              v[g] = fmaf(qr[g][4 * j + 3], k4.w, v[g]);
+            }
+          }
+        }
+        int gb = 0;
+        RS<GP, LPK / 2>::run(v, lane, gb);
+        if (dl % (LPK / GP) == 0 && key < NBK && gb < G) S[gb * NBK + key] = key < count ? v[0] + it.beta : -INFINITY;
+      }
+      named_sync(kBarConsumers, NW * 32);
+      // ---- online softmax, one warp per query head
+      for (int g = warp; g < G; g += NW) {
+        float sv[(NBK + 31) / 32];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int r = 0; r < (NBK + 31) / 32; ++r) {
+          const int key = lane + 32 * r;
+          sv[r] = key < NBK ? S[g * NBK + key] : -INFINITY;
+          mx = fmaxf(mx, sv[r]);
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        const float m_old = run_m[g];
+        const float mn = fmaxf(m_old, mx);
+        float sum = 0.0f;
+#pragma unroll
+        for (int r = 0; r < (NBK + 31) / 32; ++r) {
+          const int key = lane + 32 * r;
+          const float pr = expf(sv[r] - mn);
+          if (key < NBK) P[key * GP + g] = pr;
+          sum += key < NBK ? pr : 0.0f;
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+        if (lane == 0) {
+          const float sc = expf(m_old - mn);
+          scl[g] = sc;
+          run_l[g] = run_l[g] * sc + sum;
+          run_m[g] = mn;
+        }
+      }
+      named_sync(kBarConsumers, NW * 32);
+      // ---- PV over this warp's keys, after rescaling its partial to the new running max
+#pragma unroll
+      for (int g = 0; g < GP; ++g) {
+        const float sc = g < G ? scl[g] : 0.0f;
+#pragma unroll
+        for (int x = 0; x < DPV; ++x) o[g][x] *= sc;
+      }
+      for (int key = warp; key < count; key += NW) {
+        float vv[DPV];
+        if constexpr (DPV == 4) {
+          const float4 v4 = *reinterpret_cast<const float4*>(vb + key * DH * 4 + ((lane ^ (key & 7)) << 4));
+          vv[0] = v4.x; vv[1] = v4.y; vv[2] = v4.z; vv[3] = v4.w;
+        } else {
+          const float2 v2 = *reinterpret_cast<const float2*>(vb + swz_off(key, DPV * lane, DH, 4));
+          vv[0] = v2.x; vv[1] = v2.y;
+        }
+        const float* pk = P + key * GP;
+#pragma unroll
+        for (int g4 = 0; g4 < GP; g4 += 4) {
+          const float4 p4 = *reinterpret_cast<const float4*>(pk + g4);
+          const float pp[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+#pragma unroll
+            for (int x = 0; x < DPV; ++x) o[g4 + e][x] = fmaf(pp[e], vv[x], o[g4 + e][x]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (it.flags & 2) {
+        // ---- chunk end: sum the warps' partials in a fixed tree (warp w += warp w + half, CB
+        //      pairs at a time through the partial buffers), warp 0 writes the record
+        for (int half = NW / 2; half >= 1; half >>= 1) {
+          for (int p0 = 0; p0 < half; p0 += T::CB) {
+            const int p1 = min(p0 + T::CB, half);
+            if (warp >= half + p0 && warp < half + p1) {
+              float* cw = comb + (size_t)(warp - half - p0) * GP * DH;
+#pragma unroll
+              for (int g = 0; g < GP; ++g)
+#pragma unroll
+                for (int x = 0; x < DPV; ++x) cw[g * DH + DPV * lane + x] = o[g][x];
+            }
+            named_sync(kBarConsumers, NW * 32);
+            if (warp >= p0 && warp < p1) {
+              const float* cw = comb + (size_t)(warp - p0) * GP * DH;
+#pragma unroll
+              for (int g = 0; g < GP; ++g)
+#pragma unroll
+                for (int x = 0; x < DPV; ++x) o[g][x] += cw[g * DH + DPV * lane + x];
+            }
+            named_sync(kBarConsumers, NW * 32);
+          }
+        }
+        if (warp == 0) {
+          const int u = it.bh, rl = layer + u / BHL;
+          const size_t pbase = (size_t)(u % BHL) * dv.max_chunks + it.ci;
+          float* po = part_o_of(dv, rl);
+#pragma unroll
+          for (int g = 0; g < GP; ++g) {
+            if (g >= G) break;
+            if constexpr (DPV == 4)
+              *reinterpret_cast<float4*>(po + (pbase * G + g) * DH + 4 * lane) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+            else
+              *reinterpret_cast<float2*>(po + (pbase * G + g) * DH + 2 * lane) = make_float2(o[g][0], o[g][1]);
+          }
+          if (lane < G) {
+            part_ml_of(dv, rl)[pbase * G + lane] = make_float2(run_m[lane], run_l[lane]);
+            run_m[lane] = -INFINITY;  // the next chunk's state (read after the next QK barrier)
+            run_l[lane] = 0.0f;
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < GP; ++g)
+#pragma unroll
+          for (int x = 0; x < DPV; ++x) o[g][x] = 0.0f;
+        ++cn;
+      }
+    }
+  }
+  if (dv.ktime) {  // diagnostics: device-clock span of the launch (first CTA start .. last CTA end)
+    __syncthreads();
+    if (tid == 0) {
+      atomicMin(dv.ktime + 2 * layer, t_start);
+      atomicMax(dv.ktime + 2 * layer + 1, globaltimer_ns());
+    }
+  }
+}
+
 // ---------------------------------------------------------------- finalize (merge + append)
 // One CTA per (b, h): log-sum-exp merge of the chunk records in chunk order, then the append.
 // Runs after the attention kernel of the layer, so every chunk record is complete and no
@@ -845,6 +1186,38 @@ static cudaError_t launch_f32(const Dev& dv, int layer, const void* q, const voi
   return cudaGetLastError();
 }
 
+template <int NBK, int DH, int GP>
+static cudaError_t launch_f32w(const Dev& dv, int layer, int nl, const void* q, cudaStream_t st, int num_sms) {
+  using T = F32W<NBK, DH, GP>;
+  const size_t smem = T::smem(nl * dv.B * dv.H);
+  if (smem > 232448) return cudaErrorInvalidConfiguration;  // unit table too large for one launch
+  auto k = attend_f32w_kernel<NBK, DH, GP>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  max_shared_carveout(k);
+  k<<<num_sms, T::THREADS, smem, st>>>(dv, layer, nl, static_cast<const float*>(q), (size_t)dv.B * dv.Hq * DH);
+  return cudaGetLastError();
+}
+
+static bool f32_single_warp() {  // the round-1 one-warp fp32 kernel, one layer per launch (A/B)
+  static const bool v = getenv("NOSA_F32_WARP") != nullptr;
+  return v;
+}
+
+template <int NBK, int DH>
+static cudaError_t dispatch_f32(const Dev& dv, int layer, int nl, const void* q, const void* kn, const void* vn,
+                                float* out, cudaStream_t st, int num_sms) {
+  if (f32_single_warp()) {
+    if (nl != 1) return cudaErrorInvalidValue;
+    return launch_f32<NBK, DH>(dv, layer, q, kn, vn, out, st, 2 * num_sms);
+  }
+  if (dv.G <= 4) return launch_f32w<NBK, DH, 4>(dv, layer, nl, q, st, num_sms);
+  if (dv.G <= 8) return launch_f32w<NBK, DH, 8>(dv, layer, nl, q, st, num_sms);
+  return launch_f32w<NBK, DH, 16>(dv, layer, nl, q, st, num_sms);
+}
+
+bool attend_f32_per_layer() { return f32_single_warp(); }
+
 bool attend_supported(int n_b, int d_head, int dtype) {
   const bool nb_ok = n_b == 16 || n_b == 32 || n_b == 64 || n_b == 128;
   const bool d_ok = d_head == 64 || d_head == 128;
@@ -858,14 +1231,14 @@ static cudaError_t dispatch_bf16(const Dev& dv, int layer, int nl, const void* q
                    : launch_bf16<NBK, DH, 2>(dv, layer, nl, q, st, num_sms);
 }
 
-// layers [layer, layer + nl) in one launch (bf16); the fp32 parity kernel runs one layer at a time
+// layers [layer, layer + nl) in one launch (bf16 and the fp32 warp-group kernel; the one-warp fp32
+// kernel of NOSA_F32_WARP=1 runs one layer at a time)
 cudaError_t launch_attend(const Dev& dv, int layer, int nl, const void* q, const void* kn, const void* vn, float* out,
                           cudaStream_t st, int num_sms) {
-  if (dv.dtype != 0 && nl != 1) return cudaErrorInvalidValue;
 #define NOSA_DISPATCH(NBK, DH)                                                                  \
   if (dv.n_b == NBK && dv.D == DH) {                                                            \
     return dv.dtype == 0 ? dispatch_bf16<NBK, DH>(dv, layer, nl, q, st, num_sms)                \
-                         : launch_f32<NBK, DH>(dv, layer, q, kn, vn, out, st, 2 * num_sms);     \
+                         : dispatch_f32<NBK, DH>(dv, layer, nl, q, kn, vn, out, st, num_sms);   \
   }
   NOSA_DISPATCH(64, 128)
   NOSA_DISPATCH(64, 64)

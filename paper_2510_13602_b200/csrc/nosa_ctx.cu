@@ -49,6 +49,7 @@ cudaError_t launch_attend(const Dev& dv, int layer, int nl, const void* q, const
 cudaError_t launch_finalize(const Dev& dv, int layer, const void* kn, const void* vn, float* out, cudaStream_t st,
                             int nl = 1);
 bool attend_supported(int n_b, int d_head, int dtype);
+bool attend_f32_per_layer();
 }  // namespace nosa
 
 using nosa::Dev;
@@ -478,7 +479,7 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   std::vector<int>& plan = ctx->att_plan;
   plan.clear();
   const bool uniform_req = c.attend_layers > 0 || getenv("NOSA_ATTEND_LAYERS");
-  if (c.dtype != NOSA_DTYPE_BF16) {
+  if (c.dtype != NOSA_DTYPE_BF16 && nosa::attend_f32_per_layer()) {
     plan.assign(dv.L, 1);
   } else if (const char* e = getenv("NOSA_ATTEND_PLAN")) {  // experiments: "a,b,c,..." (summing to L)
     int sum = 0;

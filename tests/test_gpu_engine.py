@@ -599,3 +599,38 @@ def test_all_resident_run_launches_no_gather(monkeypatch):
         for a, b in zip(r0, r1):
             for x, y in zip(a, b):
                 np.testing.assert_array_equal(np.asarray(x), np.asarray(y))
+
+
+def test_fp32_multilayer_batched_attention():
+    """fp32 storage, the warp-group CUDA-core kernel over several layers per persistent launch,
+    against the oracle at the fp32 tolerance (offloaded and resident)."""
+    a = _run_pair(ONE_B_SMALL, batch=2, t0s=[3000, 2900], steps=8, fast_slots=48, seed=17, rho=0.3, layers=6,
+                  resident=True, attend_layers=4, dtype="fp32")
+    assert a <= TOL["fp32"]
+    a = _run_pair(ONE_B_SMALL, batch=3, t0s=[2000, 2500, 1700], steps=10, fast_slots=40, seed=18, rho=0.0,
+                  layers=3, attend_layers=3, dtype="fp32")
+    assert a <= TOL["fp32"]
+
+
+def test_fp32_attention_bitwise_independent_of_launch_grouping():
+    """The fp32 kernel's result depends on the fixed chunking and its fixed reduction tree only:
+    layers per launch, mover and host-buffer staging leave every output bit unchanged."""
+    cfg = ONE_B_SMALL
+    w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, 4)
+    K, V = workload.prefix_kv(4, 6, cfg.n_kv_head, 2600, cfg.d_head, bf16=False)
+    K, V = K.reshape(3, 2, cfg.n_kv_head, 2600, cfg.d_head), V.reshape(3, 2, cfg.n_kv_head, 2600, cfg.d_head)
+    results = []
+    for gather, host, att_layers in [("uva", False, 1), ("uva", False, 3), ("memcpy", False, 2), ("uva", True, 3)]:
+        eng = NosaEngine(cfg, batch=2, layers=3, max_tokens=2700, fast_slots=60, w1=w1, w2=w2, dtype="fp32",
+                         attend_layers=att_layers)
+        eng.prefill(torch.from_numpy(K), torch.from_numpy(V))
+        eng.start_run()
+        stream = workload.QueryStream(4, 3, 2, cfg.n_head, cfg.n_kv_head, cfg.d_head, 0.0, bf16=False)
+        if host:
+            outs = [eng.step_host(*stream.next(), gather=gather).clone().numpy() for _ in range(30)]
+        else:
+            outs = [eng.step(*stream.next(), gather=gather).cpu().numpy() for _ in range(30)]
+        results.append(np.stack(outs))
+        eng.close()
+    for r in results[1:]:
+        np.testing.assert_array_equal(r, results[0])
