@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--rho", type=float, default=0.95)
     ap.add_argument("--selector", default="nosa")
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--gather", default="uva")
     ap.add_argument("--layer-by-layer", action="store_true", help="use the per-layer C-ABI calls")
     ap.add_argument("--trace", action="store_true", help="print the device timeline of the last step")
@@ -38,16 +39,17 @@ def main():
     fast = nblk if a.cache >= 1 else int(a.cache * nblk)
     w1, w2 = workload.eviction_head(cfg.n_head, cfg.d_head, 0)
     t0 = time.time()
-    eng = NosaEngine(cfg, batch=a.batch, layers=a.layers, max_tokens=max_tokens, fast_slots=fast, w1=w1, w2=w2)
+    tdt = torch.float32 if a.dtype == "fp32" else torch.bfloat16
+    eng = NosaEngine(cfg, batch=a.batch, layers=a.layers, max_tokens=max_tokens, fast_slots=fast, w1=w1, w2=w2,
+                     dtype=a.dtype)
     for l in range(a.layers):
         shape = (a.batch, cfg.n_kv_head, a.context, cfg.d_head)
-        eng.prefill(workload.torch_prefix_kv(2 * l, shape, dev, torch.bfloat16),
-                    workload.torch_prefix_kv(2 * l + 1, shape, dev, torch.bfloat16), layer=l, resident=a.cache >= 1)
+        eng.prefill(workload.torch_prefix_kv(2 * l, shape, dev, tdt),
+                    workload.torch_prefix_kv(2 * l + 1, shape, dev, tdt), layer=l, resident=a.cache >= 1)
     eng.start_run()
     torch.cuda.synchronize()
     print(f"setup {time.time() - t0:.1f}s", flush=True)
-    qs = workload.TorchQueryStream(7, a.layers, a.batch, cfg.n_head, cfg.n_kv_head, cfg.d_head, a.rho, dev,
-                                   torch.bfloat16)
+    qs = workload.TorchQueryStream(7, a.layers, a.batch, cfg.n_head, cfg.n_kv_head, cfg.d_head, a.rho, dev, tdt)
     out = torch.empty((a.layers, a.batch, cfg.n_head, cfg.d_head), dtype=torch.float32, device=dev)
     eng.timing_enable(4 * a.layers * a.steps + 8)
     for s in range(a.steps):
