@@ -806,7 +806,8 @@ struct F32W {
   static constexpr int QSLOT = GP * DH * 4;
   static constexpr int CB = 2;                      // partial buffers of the chunk-end tree
   // everything but the stages, the query slots and the unit table (cbase)
-  static constexpr int FIXED = NBK * GP * 4 * 2 + CB * GP * DH * 4 + 3 * GP * 4 + 16 + 32 * 4 + 128;
+  static constexpr int SLD = NBK + 1;               // logit row stride (conflict-free writes)
+  static constexpr int FIXED = NBK * GP * 4 * 2 + GP * 4 + CB * GP * DH * 4 + 3 * GP * 4 + 16 + 32 * 4 + 128;
   static constexpr int PER_STAGE = BPB + QSLOT + 16 + 20;
   // stages: as many as fit 227 KiB with 4 KiB left for the unit table, 2 to 4
   static constexpr int NS_FIT = (232448 - 4096 - FIXED) / PER_STAGE;
@@ -821,26 +822,24 @@ struct F32Info {
   float beta;
 };
 
-// one level of the butterfly: with V > 1 values, exchange half of them (lanes with bit O set keep
-// the upper half); with one value left, a plain butterfly add
+// Reduce-scatter butterfly of V values over the lanes of a key group.  Each lane holds its
+// values in a lane-dependent order: slot j is query head j ^ m with m = dl / (LPK / GP) (the
+// query rows are loaded permuted), so at every level the half a lane keeps is already its lower
+// half: it sends the upper half and adds the partner's upper half, with no selects.  After the
+// halving levels (offsets LPK/2 .. LPK/GP) slot 0 holds head m summed over the lanes that differ
+// in those bits; the remaining levels are plain butterfly adds.
 template <int V, int O>
 struct RS {
   template <int N>
-  static __device__ __forceinline__ void run(float (&v)[N], int lane, int& base) {
+  static __device__ __forceinline__ void run(float (&v)[N]) {
     if constexpr (O >= 1) {
       if constexpr (V > 1) {
-        const bool up = (lane & O) != 0;
 #pragma unroll
-        for (int j = 0; j < V / 2; ++j) {
-          const float send = up ? v[j] : v[j + V / 2];
-          const float keep = up ? v[j + V / 2] : v[j];
-          v[j] = keep + __shfl_xor_sync(0xffffffffu, send, O);
-        }
-        base += up ? V / 2 : 0;
-        RS<V / 2, O / 2>::run(v, lane, base);
+        for (int j = 0; j < V / 2; ++j) v[j] += __shfl_xor_sync(0xffffffffu, v[j + V / 2], O);
+        RS<V / 2, O / 2>::run(v);
       } else {
         v[0] += __shfl_xor_sync(0xffffffffu, v[0], O);
-        RS<1, O / 2>::run(v, lane, base);
+        RS<1, O / 2>::run(v);
       }
     }
   }
@@ -858,7 +857,7 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP>::THREADS, 1)
   char* p = smem_raw;
   char* stages = p;                                  p += (size_t)NS * T::BPB;
   char* qslots = p;                                  p += (size_t)NS * T::QSLOT;
-  float* S = reinterpret_cast<float*>(p);            p += NBK * GP * 4;   // [GP][NBK] logits
+  float* S = reinterpret_cast<float*>(p);            p += (NBK * GP + GP) * 4;  // [GP][NBK + 1] logits
   float* P = reinterpret_cast<float*>(p);            p += NBK * GP * 4;   // [NBK][GP] probabilities
   float* comb = reinterpret_cast<float*>(p);         p += T::CB * GP * DH * 4;
   float* run_m = reinterpret_cast<float*>(p);        p += GP * 4;
@@ -944,6 +943,7 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP>::THREADS, 1)
   } else {
     // ------------------------------------------------------------ consumer warps
     const int dl = lane % LPK, kq = lane / LPK;
+    const int qperm = dl / (LPK / GP);  // this lane's register slot j holds query head j ^ qperm
     float qr[GP][DPL];
     float o[GP][DPV];
 #pragma unroll
@@ -964,7 +964,7 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP>::THREADS, 1)
         for (int g = 0; g < GP; ++g)
 #pragma unroll
           for (int j = 0; j < DPL / 4; ++j) {
-            const float4 v4 = *reinterpret_cast<const float4*>(qs + g * DH + 4 * (dl + j * LPK));
+            const float4 v4 = *reinterpret_cast<const float4*>(qs + (g ^ qperm) * DH + 4 * (dl + j * LPK));
             qr[g][4 * j] = v4.x;
             qr[g][4 * j + 1] = v4.y;
             qr[g][4 * j + 2] = v4.z;
@@ -972,31 +972,45 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP>::THREADS, 1)
           }
       }
       const int count = it.count;
-      // ---- QK: logits + bias into S[g][key] (keys past the live tokens: -inf)
+      // ---- QK: logits + bias into S[g][key] (keys past the live tokens: -inf); every K load of
+      //      the warp's keys is issued before the first FMA
+      constexpr int NIT = (NBK + NW * KPI - 1) / (NW * KPI);
+      constexpr int PFI = GP >= 16 ? (NIT < 2 ? NIT : 2) : NIT;  // iterations whose K loads go out together
 #pragma unroll
-      for (int it0 = 0; it0 < (NBK + NW * KPI - 1) / (NW * KPI); ++it0) {
-        const int key = (it0 * NW + warp) * KPI + kq;
-        if ((it0 * NW + warp) * KPI >= NBK) break;  // warp-uniform
-        float v[GP];
+      for (int i0 = 0; i0 < NIT; i0 += PFI) {
+        if ((i0 * NW + warp) * KPI >= NBK) break;  // warp-uniform
+        float4 k4[PFI][DPL / 4];
 #pragma unroll
-        for (int g = 0; g < GP; ++g) v[g] = 0.0f;
-        if (key < count) {
+        for (int ii = 0; ii < PFI; ++ii) {
+          const int key = ((i0 + ii) * NW + warp) * KPI + kq;
 #pragma unroll
           for (int j = 0; j < DPL / 4; ++j) {
             const int chunk = dl + j * LPK;
-            const float4 k4 = *reinterpret_cast<const float4*>(kb + key * DH * 4 + ((chunk ^ (key & 7)) << 4));
-#pragma unroll
-            for (int g = 0; g < GP; ++g) {
-              v[g] = fmaf(qr[g][4 * j], k4.x, v[g]);
-              v[g] = fmaf(qr[g][4 * j + 1], k4.y, v[g]);
-              v[g] = fmaf(qr[g][4 * j + 2], k4.z, v[g]);
-              v[g] = fmaf(qr[g][4 * j + 3], k4.w, v[g]);
-            }
+            k4[ii][j] = key < count ? *reinterpret_cast<const float4*>(kb + key * DH * 4 + ((chunk ^ (key & 7)) << 4))
+                                    : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
           }
         }
-        int gb = 0;
-        RS<GP, LPK / 2>::run(v, lane, gb);
-        if (dl % (LPK / GP) == 0 && key < NBK && gb < G) S[gb * NBK + key] = key < count ? v[0] + it.beta : -INFINITY;
+#pragma unroll
+        for (int ii = 0; ii < PFI; ++ii) {
+          const int i = i0 + ii;
+          const int key = (i * NW + warp) * KPI + kq;
+          if (i >= NIT || (i * NW + warp) * KPI >= NBK) break;  // warp-uniform
+          float v[GP];
+#pragma unroll
+          for (int g = 0; g < GP; ++g) v[g] = 0.0f;
+#pragma unroll
+          for (int j = 0; j < DPL / 4; ++j)
+#pragma unroll
+            for (int g = 0; g < GP; ++g) {
+              v[g] = fmaf(qr[g][4 * j], k4[ii][j].x, v[g]);
+              v[g] = fmaf(qr[g][4 * j + 1], k4[ii][j].y, v[g]);
+              v[g] = fmaf(qr[g][4 * j + 2], k4[ii][j].z, v[g]);
+              v[g] = fmaf(qr[g][4 * j + 3], k4[ii][j].w, v[g]);
+            }
+          RS<GP, LPK / 2>::run(v);
+          if (dl % (LPK / GP) == 0 && key < NBK && qperm < G)
+            S[qperm * T::SLD + key] = key < count ? v[0] + it.beta : -INFINITY;
+        }
       }
       named_sync(kBarConsumers, NW * 32);
       // ---- online softmax, one warp per query head
@@ -1006,7 +1020,7 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP>::THREADS, 1)
 #pragma unroll
         for (int r = 0; r < (NBK + 31) / 32; ++r) {
           const int key = lane + 32 * r;
-          sv[r] = key < NBK ? S[g * NBK + key] : -INFINITY;
+          sv[r] = key < NBK ? S[g * T::SLD + key] : -INFINITY;
           mx = fmaxf(mx, sv[r]);
         }
 #pragma unroll
@@ -1069,17 +1083,26 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP>::THREADS, 1)
             if (warp >= half + p0 && warp < half + p1) {
               float* cw = comb + (size_t)(warp - half - p0) * GP * DH;
 #pragma unroll
-              for (int g = 0; g < GP; ++g)
-#pragma unroll
-                for (int x = 0; x < DPV; ++x) cw[g * DH + DPV * lane + x] = o[g][x];
+              for (int g = 0; g < GP; ++g) {
+                if constexpr (DPV == 4)
+                  *reinterpret_cast<float4*>(cw + g * DH + 4 * lane) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+                else
+                  *reinterpret_cast<float2*>(cw + g * DH + 2 * lane) = make_float2(o[g][0], o[g][1]);
+              }
             }
             named_sync(kBarConsumers, NW * 32);
             if (warp >= p0 && warp < p1) {
               const float* cw = comb + (size_t)(warp - p0) * GP * DH;
 #pragma unroll
-              for (int g = 0; g < GP; ++g)
-#pragma unroll
-                for (int x = 0; x < DPV; ++x) o[g][x] += cw[g * DH + DPV * lane + x];
+              for (int g = 0; g < GP; ++g) {
+                if constexpr (DPV == 4) {
+                  const float4 c4 = *reinterpret_cast<const float4*>(cw + g * DH + 4 * lane);
+                  o[g][0] += c4.x; o[g][1] += c4.y; o[g][2] += c4.z; o[g][3] += c4.w;
+                } else {
+                  const float2 c2 = *reinterpret_cast<const float2*>(cw + g * DH + 2 * lane);
+                  o[g][0] += c2.x; o[g][1] += c2.y;
+                }
+              }
             }
             named_sync(kBarConsumers, NW * 32);
           }
