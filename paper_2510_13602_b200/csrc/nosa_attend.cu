@@ -792,13 +792,13 @@ __global__ void __launch_bounds__(32)
 //                  PV: each warp owns NBK/NW keys and DH/32 dims per lane for every query head;
 //                  per-warp partials are rescaled per block and summed over the warps in a fixed
 //                  tree at the chunk end (deterministic).  fp32 FMA throughout.
-template <int NBK, int DH, int GP>
+template <int NBK, int DH, int GP, int NW_ = 8>
 struct F32W {
-  static constexpr int NW = 8;                      // consumer warps
+  static constexpr int NW = NW_;                    // consumer warps
   static constexpr int THREADS = (NW + 1) * 32;     // + the copy warp
   static constexpr int BPB = 2 * NBK * DH * 4;      // one K|V block
   static constexpr int PLANE = NBK * DH * 4;
-  static constexpr int DPL = GP >= 16 ? 4 : 8;      // QK dims per lane
+  static constexpr int DPL = (GP >= 16 || NW >= 16) ? 4 : 8;  // QK dims per lane
   static constexpr int LPK = DH / DPL;              // lanes per key
   static constexpr int KPI = 32 / LPK;              // keys per warp iteration
   static constexpr int PCH = DPL / 4;               // 16-byte pieces per lane
@@ -845,10 +845,10 @@ struct RS {
   }
 };
 
-template <int NBK, int DH, int GP>
-__global__ void __launch_bounds__(F32W<NBK, DH, GP>::THREADS, 1)
+template <int NBK, int DH, int GP, int NW_>
+__global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
     attend_f32w_kernel(Dev dv, int layer, int nl, const float* __restrict__ q, size_t q_layer_stride) {
-  using T = F32W<NBK, DH, GP>;
+  using T = F32W<NBK, DH, GP, NW_>;
   constexpr int NW = T::NW, LPK = T::LPK, KPI = T::KPI, DPL = T::DPL, DPV = T::DPV, NS = T::NS;
   extern __shared__ __align__(128) char smem_raw[];
   const int BHL = dv.B * dv.H;
@@ -1209,12 +1209,12 @@ static cudaError_t launch_f32(const Dev& dv, int layer, const void* q, const voi
   return cudaGetLastError();
 }
 
-template <int NBK, int DH, int GP>
+template <int NBK, int DH, int GP, int NW = 8>
 static cudaError_t launch_f32w(const Dev& dv, int layer, int nl, const void* q, cudaStream_t st, int num_sms) {
-  using T = F32W<NBK, DH, GP>;
+  using T = F32W<NBK, DH, GP, NW>;
   const size_t smem = T::smem(nl * dv.B * dv.H);
   if (smem > 232448) return cudaErrorInvalidConfiguration;  // unit table too large for one launch
-  auto k = attend_f32w_kernel<NBK, DH, GP>;
+  auto k = attend_f32w_kernel<NBK, DH, GP, NW>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   max_shared_carveout(k);
@@ -1234,6 +1234,8 @@ static cudaError_t dispatch_f32(const Dev& dv, int layer, int nl, const void* q,
     if (nl != 1) return cudaErrorInvalidValue;
     return launch_f32<NBK, DH>(dv, layer, q, kn, vn, out, st, 2 * num_sms);
   }
+  static const bool w16 = getenv("NOSA_F32_WARPS16") != nullptr;  // A/B: 16 consumer warps, 4 dims per lane
+  if (w16 && NBK == 64 && DH == 128 && dv.G > 4 && dv.G <= 8) return launch_f32w<NBK, DH, 8, 16>(dv, layer, nl, q, st, num_sms);
   if (dv.G <= 4) return launch_f32w<NBK, DH, 4>(dv, layer, nl, q, st, num_sms);
   if (dv.G <= 8) return launch_f32w<NBK, DH, 8>(dv, layer, nl, q, st, num_sms);
   return launch_f32w<NBK, DH, 16>(dv, layer, nl, q, st, num_sms);
