@@ -792,6 +792,20 @@ __global__ void __launch_bounds__(32)
 //                  PV: each warp owns NBK/NW keys and DH/32 dims per lane for every query head;
 //                  per-warp partials are rescaled per block and summed over the warps in a fixed
 //                  tree at the chunk end (deterministic).  fp32 FMA throughout.
+__device__ __forceinline__ unsigned f32_to_tf32(float x) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+// D = A(16x8 tf32, row) * B(8x8 tf32, col) + D, fp32 accumulate
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const unsigned (&a)[4], const unsigned (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
 template <int NBK, int DH, int GP, int NW_ = 8>
 struct F32W {
   static constexpr int NW = NW_;                    // consumer warps
@@ -807,7 +821,16 @@ struct F32W {
   static constexpr int CB = 2;                      // partial buffers of the chunk-end tree
   // everything but the stages, the query slots and the unit table (cbase)
   static constexpr int SLD = NBK + 1;               // logit row stride (conflict-free writes)
-  static constexpr int FIXED = NBK * GP * 4 * 2 + GP * 4 + CB * GP * DH * 4 + 3 * GP * 4 + 16 + 32 * 4 + 128;
+  // QK on the tensor cores (3xTF32, mma.m16n8k8) for a group of 5..8 query heads: keys on M in
+  // 16-row tiles, the heads on N = 8; with fewer tiles than warps the head dimension is split over
+  // KS warps, each writing its own partial logits (summed in a fixed order by the softmax)
+  static constexpr bool TC = GP == 8 && NW == 8;
+  static constexpr int MT = NBK / 16;
+  static constexpr int KS = TC ? (MT >= NW ? 1 : NW / MT) : 1;
+  static constexpr int KSTEPS = DH / 8 / KS;       // k-steps of 8 dims per warp
+  static constexpr int SPB = KS;                    // partial logit buffers
+  static constexpr int FIXED = NBK * GP * 4 + SPB * (NBK * GP + GP) * 4 + CB * GP * DH * 4 + 3 * GP * 4 + 16 +
+                               32 * 4 + 128;
   static constexpr int PER_STAGE = BPB + QSLOT + 16 + 20;
   // stages: as many as fit 227 KiB with 4 KiB left for the unit table, 2 to 4
   static constexpr int NS_FIT = (232448 - 4096 - FIXED) / PER_STAGE;
@@ -857,7 +880,7 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
   char* p = smem_raw;
   char* stages = p;                                  p += (size_t)NS * T::BPB;
   char* qslots = p;                                  p += (size_t)NS * T::QSLOT;
-  float* S = reinterpret_cast<float*>(p);            p += (NBK * GP + GP) * 4;  // [GP][NBK + 1] logits
+  float* S = reinterpret_cast<float*>(p);            p += T::SPB * (NBK * GP + GP) * 4;  // [SPB][GP][NBK + 1] logits
   float* P = reinterpret_cast<float*>(p);            p += NBK * GP * 4;   // [NBK][GP] probabilities
   float* comb = reinterpret_cast<float*>(p);         p += T::CB * GP * DH * 4;
   float* run_m = reinterpret_cast<float*>(p);        p += GP * 4;
@@ -944,7 +967,10 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
     // ------------------------------------------------------------ consumer warps
     const int dl = lane % LPK, kq = lane / LPK;
     const int qperm = dl / (LPK / GP);  // this lane's register slot j holds query head j ^ qperm
-    float qr[GP][DPL];
+    float qr[T::TC ? 1 : GP][T::TC ? 1 : DPL];
+    unsigned qhi[T::TC ? T::KSTEPS : 1][2], qlo[T::TC ? T::KSTEPS : 1][2];  // B fragments (TC)
+    const int gid = lane >> 2, tig = lane & 3;
+    const int tc_mt = warp % T::MT, tc_kp = warp / T::MT;  // TC: key tile, head-dimension part
     float o[GP][DPV];
 #pragma unroll
     for (int g = 0; g < GP; ++g)
@@ -960,18 +986,59 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
       const char* vb = kb + T::PLANE;
       if (it.flags & 1) {  // chunk start: the group's query slice into registers
         const float* qs = reinterpret_cast<const float*>(qslots + (size_t)(cn % NS) * T::QSLOT);
+        if constexpr (T::TC) {
 #pragma unroll
-        for (int g = 0; g < GP; ++g)
+          for (int k = 0; k < T::KSTEPS; ++k)
 #pragma unroll
-          for (int j = 0; j < DPL / 4; ++j) {
-            const float4 v4 = *reinterpret_cast<const float4*>(qs + (g ^ qperm) * DH + 4 * (dl + j * LPK));
-            qr[g][4 * j] = v4.x;
-            qr[g][4 * j + 1] = v4.y;
-            qr[g][4 * j + 2] = v4.z;
-            qr[g][4 * j + 3] = v4.w;
-          }
+            for (int e = 0; e < 2; ++e) {
+              const float x = qs[gid * DH + 8 * (tc_kp * T::KSTEPS + k) + tig + 4 * e];
+              qhi[k][e] = f32_to_tf32(x);
+              qlo[k][e] = f32_to_tf32(x - __uint_as_float(qhi[k][e]));
+            }
+        } else {
+#pragma unroll
+          for (int g = 0; g < GP; ++g)
+#pragma unroll
+            for (int j = 0; j < DPL / 4; ++j) {
+              const float4 v4 = *reinterpret_cast<const float4*>(qs + (g ^ qperm) * DH + 4 * (dl + j * LPK));
+              qr[g][4 * j] = v4.x;
+              qr[g][4 * j + 1] = v4.y;
+              qr[g][4 * j + 2] = v4.z;
+              qr[g][4 * j + 3] = v4.w;
+            }
+        }
       }
       const int count = it.count;
+      if constexpr (T::TC) {
+        // ---- QK on the tensor cores: this warp's 16-key tile x the group's 8 heads over its
+        //      k-steps; a = a_hi + a_lo in tf32 for K and q, D += a_lo b_hi + a_hi b_lo + a_hi b_hi
+        float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        const int mi = lane >> 3, r = lane & 7;
+        const int key_a = tc_mt * 16 + r + (mi & 1) * 8;
+        const unsigned rowb = smem_u32(kb) + key_a * DH * 4;
+#pragma unroll
+        for (int k = 0; k < T::KSTEPS; ++k) {
+          const int chunk = 2 * (tc_kp * T::KSTEPS + k) + (mi >> 1);
+          unsigned a[4];
+          ldsm_x4(rowb + ((chunk ^ (key_a & 7)) << 4), a[0], a[1], a[2], a[3]);
+          unsigned ahi[4], alo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float x = __uint_as_float(a[e]);
+            ahi[e] = f32_to_tf32(x);
+            alo[e] = f32_to_tf32(x - __uint_as_float(ahi[e]));
+          }
+          mma_tf32(c, alo, qhi[k]);
+          mma_tf32(c, ahi, qlo[k]);
+          mma_tf32(c, ahi, qhi[k]);
+        }
+        float* Sp = S + (size_t)tc_kp * (NBK * GP + GP);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int key = tc_mt * 16 + gid + (e >> 1) * 8, g = 2 * tig + (e & 1);
+          Sp[g * T::SLD + key] = c[e];
+        }
+      } else {
       // ---- QK: logits + bias into S[g][key] (keys past the live tokens: -inf); every K load of
       //      the warp's keys is issued before the first FMA
       constexpr int NIT = (NBK + NW * KPI - 1) / (NW * KPI);
@@ -1009,8 +1076,9 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
             }
           RS<GP, LPK / 2>::run(v);
           if (dl % (LPK / GP) == 0 && key < NBK && qperm < G)
-            S[qperm * T::SLD + key] = key < count ? v[0] + it.beta : -INFINITY;
+            S[qperm * T::SLD + key] = v[0];
         }
+      }
       }
       named_sync(kBarConsumers, NW * 32);
       // ---- online softmax, one warp per query head
@@ -1020,7 +1088,10 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
 #pragma unroll
         for (int r = 0; r < (NBK + 31) / 32; ++r) {
           const int key = lane + 32 * r;
-          sv[r] = key < NBK ? S[g * T::SLD + key] : -INFINITY;
+          float x = 0.0f;
+#pragma unroll
+          for (int pp = 0; pp < T::SPB; ++pp) x += key < NBK ? S[pp * (NBK * GP + GP) + g * T::SLD + key] : 0.0f;
+          sv[r] = key < count ? x + it.beta : -INFINITY;
           mx = fmaxf(mx, sv[r]);
         }
 #pragma unroll
