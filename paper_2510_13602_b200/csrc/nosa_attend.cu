@@ -1021,12 +1021,13 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
           const int chunk = 2 * (tc_kp * T::KSTEPS + k) + (mi >> 1);
           unsigned a[4];
           ldsm_x4(rowb + ((chunk ^ (key_a & 7)) << 4), a[0], a[1], a[2], a[3]);
+          // split in integer ops: hi = x rounded to the tf32 grid (round half away from zero on
+          // the magnitude), lo = x - hi exactly; the tensor core reads lo's top 19 bits
           unsigned ahi[4], alo[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float x = __uint_as_float(a[e]);
-            ahi[e] = f32_to_tf32(x);
-            alo[e] = f32_to_tf32(x - __uint_as_float(ahi[e]));
+            ahi[e] = (a[e] + 0x1000u) & 0xffffe000u;
+            alo[e] = __float_as_uint(__uint_as_float(a[e]) - __uint_as_float(ahi[e]));
           }
           mma_tf32(c, alo, qhi[k]);
           mma_tf32(c, ahi, qlo[k]);
@@ -1123,16 +1124,24 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
 #pragma unroll
         for (int x = 0; x < DPV; ++x) o[g][x] *= sc;
       }
-      for (int key = warp; key < count; key += NW) {
+      constexpr int KPW = (NBK + NW - 1) / NW;  // keys per warp: warp, warp + NW, ...
+      // with NW a multiple of 8 every key of this warp has the same swizzle phase (key & 7)
+      const char* vrow = vb + warp * DH * 4;
+      const float* prow = P + warp * GP;
+#pragma unroll
+      for (int j = 0; j < KPW; ++j) {
+        const int key = warp + NW * j;
+        if (key >= count) break;  // warp-uniform
         float vv[DPV];
         if constexpr (DPV == 4) {
-          const float4 v4 = *reinterpret_cast<const float4*>(vb + key * DH * 4 + ((lane ^ (key & 7)) << 4));
+          const int sw = (NW % 8 == 0) ? (warp & 7) : (key & 7);
+          const float4 v4 = *reinterpret_cast<const float4*>(vrow + j * NW * DH * 4 + ((lane ^ sw) << 4));
           vv[0] = v4.x; vv[1] = v4.y; vv[2] = v4.z; vv[3] = v4.w;
         } else {
           const float2 v2 = *reinterpret_cast<const float2*>(vb + swz_off(key, DPV * lane, DH, 4));
           vv[0] = v2.x; vv[1] = v2.y;
         }
-        const float* pk = P + key * GP;
+        const float* pk = prow + j * NW * GP;
 #pragma unroll
         for (int g4 = 0; g4 < GP; g4 += 4) {
           const float4 p4 = *reinterpret_cast<const float4*>(pk + g4);
