@@ -829,7 +829,13 @@ struct F32W {
   static constexpr int KS = TC ? (MT >= NW ? 1 : NW / MT) : 1;
   static constexpr int KSTEPS = DH / 8 / KS;       // k-steps of 8 dims per warp
   static constexpr int SPB = KS;                    // partial logit buffers
-  static constexpr int FIXED = NBK * GP * 4 + SPB * (NBK * GP + GP) * 4 + CB * GP * DH * 4 + 3 * GP * 4 + 16 +
+  // PV on the tensor cores too (3xTF32): O^T[dims x heads] = V^T[dims x keys] . P^T[keys x heads],
+  // dims on M (DH / 16 tiles), the 8 heads on N, 8 keys per k-step; warp w takes k-steps w, w + NW
+  static constexpr bool TCPV = TC;
+  static constexpr int MTD = DH / 16;
+  static constexpr int KT = NBK / 8;
+  static constexpr int CLD = DH + 4;                // partial-buffer row stride (conflict-free)
+  static constexpr int FIXED = NBK * GP * 4 + SPB * (NBK * GP + GP) * 4 + CB * GP * CLD * 4 + 3 * GP * 4 + 16 +
                                32 * 4 + 128;
   static constexpr int PER_STAGE = BPB + QSLOT + 16 + 20;
   // stages: as many as fit 227 KiB with 4 KiB left for the unit table, 2 to 4
@@ -882,7 +888,7 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
   char* qslots = p;                                  p += (size_t)NS * T::QSLOT;
   float* S = reinterpret_cast<float*>(p);            p += T::SPB * (NBK * GP + GP) * 4;  // [SPB][GP][NBK + 1] logits
   float* P = reinterpret_cast<float*>(p);            p += NBK * GP * 4;   // [NBK][GP] probabilities
-  float* comb = reinterpret_cast<float*>(p);         p += T::CB * GP * DH * 4;
+  float* comb = reinterpret_cast<float*>(p);         p += T::CB * GP * T::CLD * 4;
   float* run_m = reinterpret_cast<float*>(p);        p += GP * 4;
   float* run_l = reinterpret_cast<float*>(p);        p += GP * 4;
   float* scl = reinterpret_cast<float*>(p);          p += GP * 4;
@@ -971,11 +977,16 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
     unsigned qhi[T::TC ? T::KSTEPS : 1][2], qlo[T::TC ? T::KSTEPS : 1][2];  // B fragments (TC)
     const int gid = lane >> 2, tig = lane & 3;
     const int tc_mt = warp % T::MT, tc_kp = warp / T::MT;  // TC: key tile, head-dimension part
-    float o[GP][DPV];
+    // the lane's partial O: CUDA-core PV o[head][DPV dims at DPV*lane]; tensor-core PV
+    // o[m-tile][c fragment]: dim = 16 mt + gid (+8 for c2, c3), head = 2 tig (+1 for c1, c3)
+    constexpr int OA = T::TCPV ? T::MTD : GP, OB = T::TCPV ? 4 : DPV;
+    float o[OA][OB];
 #pragma unroll
-    for (int g = 0; g < GP; ++g)
+    for (int g = 0; g < OA; ++g)
 #pragma unroll
-      for (int x = 0; x < DPV; ++x) o[g][x] = 0.0f;
+      for (int x = 0; x < OB; ++x) o[g][x] = 0.0f;
+    auto o_dim = [&](int a, int b) { return T::TCPV ? 16 * a + gid + 8 * (b >> 1) : DPV * lane + b; };
+    auto o_head = [&](int a, int b) { return T::TCPV ? 2 * tig + (b & 1) : a; };
     int seq = 0, cn = 0;
     for (;; ++seq) {
       const int st = seq % NS;
@@ -1119,11 +1130,46 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
       named_sync(kBarConsumers, NW * 32);
       // ---- PV over this warp's keys, after rescaling its partial to the new running max
 #pragma unroll
-      for (int g = 0; g < GP; ++g) {
-        const float sc = g < G ? scl[g] : 0.0f;
+      for (int a = 0; a < OA; ++a)
 #pragma unroll
-        for (int x = 0; x < DPV; ++x) o[g][x] *= sc;
-      }
+        for (int b = 0; b < OB; ++b) {
+          const int g = o_head(a, b);
+          o[a][b] *= g < G ? scl[g] : 0.0f;
+        }
+      if constexpr (T::TCPV) {
+#pragma unroll
+        for (int kt = warp; kt < T::KT; kt += NW) {
+          const int k0 = 8 * kt;
+          if (k0 >= count) break;  // warp-uniform; keys past count carry p = 0
+          // B = P^T (keys x heads): b0 = P[head gid][key k0 + tig], b1 = key + 4
+          unsigned bhi[2], blo[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const unsigned x = __float_as_uint(P[(k0 + tig + 4 * e) * GP + gid]);
+            bhi[e] = (x + 0x1000u) & 0xffffe000u;
+            blo[e] = __float_as_uint(__uint_as_float(x) - __uint_as_float(bhi[e]));
+          }
+#pragma unroll
+          for (int mt = 0; mt < T::MTD; ++mt) {
+            // A = V^T (dims x keys): a0 = V[k0 + tig][16 mt + gid], a1 = dim + 8, a2 = key + 4, a3 = both
+            unsigned a[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int key = k0 + tig + 4 * (e >> 1), dim = 16 * mt + gid + 8 * (e & 1);
+              a[e] = *reinterpret_cast<const unsigned*>(vb + key * DH * 4 + ((((dim >> 2) ^ (key & 7)) << 4) | ((dim & 3) << 2)));
+            }
+            unsigned ahi[4], alo[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              ahi[e] = (a[e] + 0x1000u) & 0xffffe000u;
+              alo[e] = __float_as_uint(__uint_as_float(a[e]) - __uint_as_float(ahi[e]));
+            }
+            mma_tf32(o[mt], alo, bhi);
+            mma_tf32(o[mt], ahi, blo);
+            mma_tf32(o[mt], ahi, bhi);
+          }
+        }
+      } else {
       constexpr int KPW = (NBK + NW - 1) / NW;  // keys per warp: warp, warp + NW, ...
       // with NW a multiple of 8 every key of this warp has the same swizzle phase (key & 7)
       const char* vrow = vb + warp * DH * 4;
@@ -1152,6 +1198,7 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
             for (int x = 0; x < DPV; ++x) o[g4 + e][x] = fmaf(pp[e], vv[x], o[g4 + e][x]);
         }
       }
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
       if (it.flags & 2) {
@@ -1161,26 +1208,27 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
           for (int p0 = 0; p0 < half; p0 += T::CB) {
             const int p1 = min(p0 + T::CB, half);
             if (warp >= half + p0 && warp < half + p1) {
-              float* cw = comb + (size_t)(warp - half - p0) * GP * DH;
+              float* cw = comb + (size_t)(warp - half - p0) * GP * T::CLD;
 #pragma unroll
-              for (int g = 0; g < GP; ++g) {
-                if constexpr (DPV == 4)
-                  *reinterpret_cast<float4*>(cw + g * DH + 4 * lane) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+              for (int a = 0; a < OA; ++a) {
+                if constexpr (!T::TCPV && DPV == 4)
+                  *reinterpret_cast<float4*>(cw + a * T::CLD + 4 * lane) = make_float4(o[a][0], o[a][1], o[a][2], o[a][3]);
                 else
-                  *reinterpret_cast<float2*>(cw + g * DH + 2 * lane) = make_float2(o[g][0], o[g][1]);
+#pragma unroll
+                  for (int b = 0; b < OB; ++b) cw[o_head(a, b) * T::CLD + o_dim(a, b)] = o[a][b];
               }
             }
             named_sync(kBarConsumers, NW * 32);
             if (warp >= p0 && warp < p1) {
-              const float* cw = comb + (size_t)(warp - p0) * GP * DH;
+              const float* cw = comb + (size_t)(warp - p0) * GP * T::CLD;
 #pragma unroll
-              for (int g = 0; g < GP; ++g) {
-                if constexpr (DPV == 4) {
-                  const float4 c4 = *reinterpret_cast<const float4*>(cw + g * DH + 4 * lane);
-                  o[g][0] += c4.x; o[g][1] += c4.y; o[g][2] += c4.z; o[g][3] += c4.w;
+              for (int a = 0; a < OA; ++a) {
+                if constexpr (!T::TCPV && DPV == 4) {
+                  const float4 c4 = *reinterpret_cast<const float4*>(cw + a * T::CLD + 4 * lane);
+                  o[a][0] += c4.x; o[a][1] += c4.y; o[a][2] += c4.z; o[a][3] += c4.w;
                 } else {
-                  const float2 c2 = *reinterpret_cast<const float2*>(cw + g * DH + 2 * lane);
-                  o[g][0] += c2.x; o[g][1] += c2.y;
+#pragma unroll
+                  for (int b = 0; b < OB; ++b) o[a][b] += cw[o_head(a, b) * T::CLD + o_dim(a, b)];
                 }
               }
             }
@@ -1191,13 +1239,21 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
           const int u = it.bh, rl = layer + u / BHL;
           const size_t pbase = (size_t)(u % BHL) * dv.max_chunks + it.ci;
           float* po = part_o_of(dv, rl);
+          if constexpr (T::TCPV) {
 #pragma unroll
-          for (int g = 0; g < GP; ++g) {
-            if (g >= G) break;
-            if constexpr (DPV == 4)
-              *reinterpret_cast<float4*>(po + (pbase * G + g) * DH + 4 * lane) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
-            else
-              *reinterpret_cast<float2*>(po + (pbase * G + g) * DH + 2 * lane) = make_float2(o[g][0], o[g][1]);
+            for (int a = 0; a < OA; ++a)
+#pragma unroll
+              for (int b = 0; b < OB; ++b)
+                if (o_head(a, b) < G) po[(pbase * G + o_head(a, b)) * DH + o_dim(a, b)] = o[a][b];
+          } else {
+#pragma unroll
+            for (int g = 0; g < GP; ++g) {
+              if (g >= G) break;
+              if constexpr (DPV == 4)
+                *reinterpret_cast<float4*>(po + (pbase * G + g) * DH + 4 * lane) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+              else
+                *reinterpret_cast<float2*>(po + (pbase * G + g) * DH + 2 * lane) = make_float2(o[g][0], o[g][1]);
+            }
           }
           if (lane < G) {
             part_ml_of(dv, rl)[pbase * G + lane] = make_float2(run_m[lane], run_l[lane]);
@@ -1206,9 +1262,9 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
           }
         }
 #pragma unroll
-        for (int g = 0; g < GP; ++g)
+        for (int a = 0; a < OA; ++a)
 #pragma unroll
-          for (int x = 0; x < DPV; ++x) o[g][x] = 0.0f;
+          for (int b = 0; b < OB; ++b) o[a][b] = 0.0f;
         ++cn;
       }
     }
