@@ -830,8 +830,11 @@ struct F32W {
   static constexpr int KSTEPS = DH / 8 / KS;       // k-steps of 8 dims per warp
   static constexpr int SPB = KS;                    // partial logit buffers
   // PV on the tensor cores too (3xTF32): O^T[dims x heads] = V^T[dims x keys] . P^T[keys x heads],
-  // dims on M (DH / 16 tiles), the 8 heads on N, 8 keys per k-step; warp w takes k-steps w, w + NW
-  static constexpr bool TCPV = TC;
+  // dims on M (DH / 16 tiles), the 8 heads on N, 8 keys per k-step; warp w takes k-steps w, w + NW.
+  // Measured slower than the FMA PV (cfg 2 fp32 17.85K vs 18.47K tok/s, 139 vs 134 us per
+  // 2-layer launch): V^T fragments need scalar swizzled loads (5.6M vs 3.4M bank conflicts), so
+  // it is off; set true to rerun the comparison.
+  static constexpr bool TCPV = false;
   static constexpr int MTD = DH / 16;
   static constexpr int KT = NBK / 8;
   static constexpr int CLD = DH + 4;                // partial-buffer row stride (conflict-free)
