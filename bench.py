@@ -801,7 +801,7 @@ def cpu_baseline_sample(args, cfg, w, rec, device, fast, max_tokens):
 
 
 # ------------------------------------------------------------------------------ reference arm
-def _ref_worker(conn, pairs, cfg_d, context, max_tokens, fast, resident, rho, seed, selector):
+def _ref_worker(conn, pairs, cfg_d, context, max_tokens, fast, resident, rho, seed, selector, bf16=True):
     """One host process of the reference arm: the oracle (the reference algorithm) for its
     (layer, global sequence) pairs, on the exact inputs the GPU arm decodes for those pairs."""
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
@@ -812,14 +812,14 @@ def _ref_worker(conn, pairs, cfg_d, context, max_tokens, fast, resident, rho, se
     w1, w2 = wl.eviction_head(oc.n_head, oc.d_head, seed)
     units = []
     for (l, gb) in pairs:
-        K, V = wl.synth_prefix_kv(seed, l, [gb], oc.n_kv_head, context, oc.d_head)
+        K, V = wl.synth_prefix_kv(seed, l, [gb], oc.n_kv_head, context, oc.d_head, bf16=bf16)
         orc = O.OracleEngine(oc, 1, 1, max_tokens, fast, w1, w2, store_payload=True, dense=True)
         orc.prefill(0, 0, K[0], V[0])
         orc.start_run()
         if resident:
             for h in range(oc.n_kv_head):
                 orc.managers[0][0].make_resident(h, -(-context // oc.n_b))
-        stream = wl.SynthQueryStream(seed, [l], [gb], oc.n_head, oc.n_kv_head, oc.d_head, rho)
+        stream = wl.SynthQueryStream(seed, [l], [gb], oc.n_head, oc.n_kv_head, oc.d_head, rho, bf16=bf16)
         units.append((orc, stream))
         del K, V
     conn.send("ready")
@@ -861,7 +861,8 @@ def run_reference(args, rank, world):
     for i in range(nproc):
         a, b = ctx.Pipe()
         p = ctx.Process(target=_ref_worker, args=(b, pairs[i::nproc], cfg_d, w["context"], max_tokens, fast,
-                                                  w["cache"] == "resident", w["rho"], args.seed, args.selector),
+                                                  w["cache"] == "resident", w["rho"], args.seed, args.selector,
+                                                  args.dtype == "bf16"),
                         daemon=True)
         p.start()
         procs.append(p)
@@ -896,7 +897,7 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 2),
             "higher_is_better": True, "scaling": "strong" if w.get("strong") else "weak", "vs_baseline": None,
             "dtype": "f64",
-            "data": f"synthetic: K/V ~ N(0,1) bf16, AR(1) queries rho={w['rho']} (counter-based generator, seed "
+            "data": f"synthetic: K/V ~ N(0,1) {args.dtype}, AR(1) queries rho={w['rho']} (counter-based generator, seed "
                     f"{args.seed}: the same bits on the GPU and in the CPU oracle)",
             "config": bench_config(args, w, world),
             "sample_batch": S,

@@ -111,10 +111,12 @@ def synth_normal(seed: int, kind: int, layer: int, seqs, heads: int, pos0: int, 
     return (s - 131070).astype(np.float32) * scale
 
 
-def synth_prefix_kv(seed: int, layer: int, seqs, heads: int, t: int, d: int):
-    """Prefix K, V [len(seqs)][heads][t][d], bf16-representable float32."""
-    return (bf16_round(synth_normal(seed, KIND_K, layer, seqs, heads, 0, t, d)),
-            bf16_round(synth_normal(seed, KIND_V, layer, seqs, heads, 0, t, d)))
+def synth_prefix_kv(seed: int, layer: int, seqs, heads: int, t: int, d: int, bf16: bool = True):
+    """Prefix K, V [len(seqs)][heads][t][d] float32: bf16-representable (bf16 storage) or as drawn
+    (fp32 storage)."""
+    k = synth_normal(seed, KIND_K, layer, seqs, heads, 0, t, d)
+    v = synth_normal(seed, KIND_V, layer, seqs, heads, 0, t, d)
+    return (bf16_round(k), bf16_round(v)) if bf16 else (k, v)
 
 
 class SynthQueryStream:
