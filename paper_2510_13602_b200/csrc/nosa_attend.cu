@@ -922,37 +922,63 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
 
   if (warp == NW) {
     // ------------------------------------------------------------ copy warp
-    int seq = 0, cn = 0;
-    int c = 0;
-    if (lane == 0) c = atomicAdd(dv.cnt + kCntStride * layer + 1, 1);
-    c = __shfl_sync(0xffffffffu, c, 0);
-    while (c < total) {
-      const int u = find_bh(cbase, BH, c);
-      const int ci = c - cbase[u];
-      const int lbh = layer * BHL + u;  // units of the launch's layers are contiguous in lbh
-      const int rl = layer + u / BHL, bh = u % BHL;
-      const int n = __ldcg(dv.n_req + lbh);
-      const int t = __ldcg(dv.t + lbh);
-      const int i0 = ci * dv.chunk, nb = min(dv.chunk, n - i0);
-      // the chunk's blocks, lane-parallel: block, slot, bias, live tokens
-      int blk = 0, slot = 0, cnt = 0;
-      float beta = 0.0f;
-      if (lane < nb) {
-        blk = __ldcg(dv.req + (size_t)lbh * dv.C + i0 + lane);
-        slot = __ldcg(dv.req_slot + (size_t)lbh * dv.C + i0 + lane);
-        cnt = min(NBK, t - blk * NBK);
-        beta = block_beta(dv, lbh, blk, t);
+    // A chunk's metadata is a chain of dependent loads (claim -> unit -> required list -> bias);
+    // the next chunk's chain advances one link after each block this chunk issues, so the ring
+    // keeps filling across chunk boundaries.
+    struct Meta {
+      int c, u, ci, lbh, n, t, nb, blk, slot, cnt;
+      float beta;
+    };
+    auto claim = [&](Meta& m) {
+      m.c = 0;
+      if (lane == 0) m.c = atomicAdd(dv.cnt + kCntStride * layer + 1, 1);
+    };
+    auto advance = [&](Meta& m, int& stage) {  // warp-uniform
+      if (stage == 0) {
+        m.c = __shfl_sync(0xffffffffu, m.c, 0);
+        if (m.c >= total) { stage = 4; return; }
+        m.u = find_bh(cbase, BH, m.c);
+        m.ci = m.c - cbase[m.u];
+        m.lbh = layer * BHL + m.u;  // units of the launch's layers are contiguous in lbh
+        m.n = __ldcg(dv.n_req + m.lbh);
+        m.t = __ldcg(dv.t + m.lbh);
+        stage = 1;
+      } else if (stage == 1) {
+        const int i0 = m.ci * dv.chunk;
+        m.nb = min(dv.chunk, m.n - i0);
+        m.blk = m.slot = 0;
+        if (lane < m.nb) {
+          m.blk = __ldcg(dv.req + (size_t)m.lbh * dv.C + i0 + lane);
+          m.slot = __ldcg(dv.req_slot + (size_t)m.lbh * dv.C + i0 + lane);
+        }
+        stage = 2;
+      } else if (stage == 2) {
+        m.cnt = 0;
+        m.beta = 0.0f;
+        if (lane < m.nb) {
+          m.cnt = min(NBK, m.t - m.blk * NBK);
+          m.beta = block_beta(dv, m.lbh, m.blk, m.t);
+        }
+        stage = 3;
       }
-      // the next chunk's claim is in flight while this one streams
-      int c_next = 0;
-      if (lane == 0) c_next = atomicAdd(dv.cnt + kCntStride * layer + 1, 1);
+    };
+    int seq = 0, cn = 0;
+    Meta cur, nxt;
+    int cst = 0, nst = 0;
+    claim(cur);
+    while (cst < 3) advance(cur, cst);
+    while (cst == 3) {
+      claim(nxt);
+      nst = 0;
+      const int u = cur.u, ci = cur.ci, lbh = cur.lbh, nb = cur.nb;
+      const int rl = layer + u / BHL, bh = u % BHL;
       const int b = bh / dv.H, h = bh % dv.H;
       const float* qrow = q + (size_t)(rl - layer) * q_layer_stride + ((size_t)b * dv.Hq + h * G) * DH;
       for (int i = 0; i < nb; ++i, ++seq) {
         const int st = seq % NS;
-        const int si = __shfl_sync(0xffffffffu, slot, i);
-        const int ki = __shfl_sync(0xffffffffu, cnt, i);
-        const float be = __shfl_sync(0xffffffffu, beta, i);
+        const int si = __shfl_sync(0xffffffffu, cur.slot, i);
+        const int ki = __shfl_sync(0xffffffffu, cur.cnt, i);
+        const float be = __shfl_sync(0xffffffffu, cur.beta, i);
         if (lane == 0) {
           if (seq >= NS) mbar_wait(&empty[st], ((seq / NS) - 1) & 1);
           info[st] = F32Info{u, ci, ki, (i == 0 ? 1 : 0) | (i == nb - 1 ? 2 : 0), be};
@@ -962,9 +988,12 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
           bulk_g2s(stages + (size_t)st * T::BPB, dv.pool + ((size_t)lbh * dv.C + si) * (size_t)T::BPB, T::BPB, &full[st]);
           if (qbytes) bulk_g2s(qslots + (size_t)(cn % NS) * T::QSLOT, qrow, qbytes, &full[st]);
         }
+        if (nst < 3) advance(nxt, nst);
       }
+      while (nst < 3) advance(nxt, nst);
       ++cn;
-      c = __shfl_sync(0xffffffffu, c_next, 0);
+      cur = nxt;
+      cst = nst;
     }
     if (lane == 0) {  // end of work
       const int st = seq % NS;
