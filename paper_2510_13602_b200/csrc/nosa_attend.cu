@@ -829,16 +829,7 @@ struct F32W {
   static constexpr int KS = TC ? (MT >= NW ? 1 : NW / MT) : 1;
   static constexpr int KSTEPS = DH / 8 / KS;       // k-steps of 8 dims per warp
   static constexpr int SPB = KS;                    // partial logit buffers
-  // PV on the tensor cores too (3xTF32): O^T[dims x heads] = V^T[dims x keys] . P^T[keys x heads],
-  // dims on M (DH / 16 tiles), the 8 heads on N, 8 keys per k-step; warp w takes k-steps w, w + NW.
-  // Measured slower than the FMA PV (cfg 2 fp32 17.85K vs 18.47K tok/s, 139 vs 134 us per
-  // 2-layer launch): V^T fragments need scalar swizzled loads (5.6M vs 3.4M bank conflicts), so
-  // it is off; set true to rerun the comparison.
-  static constexpr bool TCPV = false;
-  static constexpr int MTD = DH / 16;
-  static constexpr int KT = NBK / 8;
-  static constexpr int CLD = DH + 4;                // partial-buffer row stride (conflict-free)
-  static constexpr int FIXED = NBK * GP * 4 + SPB * (NBK * GP + GP) * 4 + CB * GP * CLD * 4 + 3 * GP * 4 + 16 +
+  static constexpr int FIXED = NBK * GP * 4 + SPB * (NBK * GP + GP) * 4 + CB * GP * DH * 4 + 3 * GP * 4 + 16 +
                                32 * 4 + 128;
   static constexpr int PER_STAGE = BPB + QSLOT + 16 + 20;
   // stages: as many as fit 227 KiB with 4 KiB left for the unit table, 2 to 4
@@ -891,7 +882,7 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
   char* qslots = p;                                  p += (size_t)NS * T::QSLOT;
   float* S = reinterpret_cast<float*>(p);            p += T::SPB * (NBK * GP + GP) * 4;  // [SPB][GP][NBK + 1] logits
   float* P = reinterpret_cast<float*>(p);            p += NBK * GP * 4;   // [NBK][GP] probabilities
-  float* comb = reinterpret_cast<float*>(p);         p += T::CB * GP * T::CLD * 4;
+  float* comb = reinterpret_cast<float*>(p);         p += T::CB * GP * DH * 4;
   float* run_m = reinterpret_cast<float*>(p);        p += GP * 4;
   float* run_l = reinterpret_cast<float*>(p);        p += GP * 4;
   float* scl = reinterpret_cast<float*>(p);          p += GP * 4;
@@ -922,63 +913,37 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
 
   if (warp == NW) {
     // ------------------------------------------------------------ copy warp
-    // A chunk's metadata is a chain of dependent loads (claim -> unit -> required list -> bias);
-    // the next chunk's chain advances one link after each block this chunk issues, so the ring
-    // keeps filling across chunk boundaries.
-    struct Meta {
-      int c, u, ci, lbh, n, t, nb, blk, slot, cnt;
-      float beta;
-    };
-    auto claim = [&](Meta& m) {
-      m.c = 0;
-      if (lane == 0) m.c = atomicAdd(dv.cnt + kCntStride * layer + 1, 1);
-    };
-    auto advance = [&](Meta& m, int& stage) {  // warp-uniform
-      if (stage == 0) {
-        m.c = __shfl_sync(0xffffffffu, m.c, 0);
-        if (m.c >= total) { stage = 4; return; }
-        m.u = find_bh(cbase, BH, m.c);
-        m.ci = m.c - cbase[m.u];
-        m.lbh = layer * BHL + m.u;  // units of the launch's layers are contiguous in lbh
-        m.n = __ldcg(dv.n_req + m.lbh);
-        m.t = __ldcg(dv.t + m.lbh);
-        stage = 1;
-      } else if (stage == 1) {
-        const int i0 = m.ci * dv.chunk;
-        m.nb = min(dv.chunk, m.n - i0);
-        m.blk = m.slot = 0;
-        if (lane < m.nb) {
-          m.blk = __ldcg(dv.req + (size_t)m.lbh * dv.C + i0 + lane);
-          m.slot = __ldcg(dv.req_slot + (size_t)m.lbh * dv.C + i0 + lane);
-        }
-        stage = 2;
-      } else if (stage == 2) {
-        m.cnt = 0;
-        m.beta = 0.0f;
-        if (lane < m.nb) {
-          m.cnt = min(NBK, m.t - m.blk * NBK);
-          m.beta = block_beta(dv, m.lbh, m.blk, m.t);
-        }
-        stage = 3;
-      }
-    };
     int seq = 0, cn = 0;
-    Meta cur, nxt;
-    int cst = 0, nst = 0;
-    claim(cur);
-    while (cst < 3) advance(cur, cst);
-    while (cst == 3) {
-      claim(nxt);
-      nst = 0;
-      const int u = cur.u, ci = cur.ci, lbh = cur.lbh, nb = cur.nb;
+    int c = 0;
+    if (lane == 0) c = atomicAdd(dv.cnt + kCntStride * layer + 1, 1);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    while (c < total) {
+      const int u = find_bh(cbase, BH, c);
+      const int ci = c - cbase[u];
+      const int lbh = layer * BHL + u;  // units of the launch's layers are contiguous in lbh
       const int rl = layer + u / BHL, bh = u % BHL;
+      const int n = __ldcg(dv.n_req + lbh);
+      const int t = __ldcg(dv.t + lbh);
+      const int i0 = ci * dv.chunk, nb = min(dv.chunk, n - i0);
+      // the chunk's blocks, lane-parallel: block, slot, bias, live tokens
+      int blk = 0, slot = 0, cnt = 0;
+      float beta = 0.0f;
+      if (lane < nb) {
+        blk = __ldcg(dv.req + (size_t)lbh * dv.C + i0 + lane);
+        slot = __ldcg(dv.req_slot + (size_t)lbh * dv.C + i0 + lane);
+        cnt = min(NBK, t - blk * NBK);
+        beta = block_beta(dv, lbh, blk, t);
+      }
+      // the next chunk's claim is in flight while this one streams
+      int c_next = 0;
+      if (lane == 0) c_next = atomicAdd(dv.cnt + kCntStride * layer + 1, 1);
       const int b = bh / dv.H, h = bh % dv.H;
       const float* qrow = q + (size_t)(rl - layer) * q_layer_stride + ((size_t)b * dv.Hq + h * G) * DH;
       for (int i = 0; i < nb; ++i, ++seq) {
         const int st = seq % NS;
-        const int si = __shfl_sync(0xffffffffu, cur.slot, i);
-        const int ki = __shfl_sync(0xffffffffu, cur.cnt, i);
-        const float be = __shfl_sync(0xffffffffu, cur.beta, i);
+        const int si = __shfl_sync(0xffffffffu, slot, i);
+        const int ki = __shfl_sync(0xffffffffu, cnt, i);
+        const float be = __shfl_sync(0xffffffffu, beta, i);
         if (lane == 0) {
           if (seq >= NS) mbar_wait(&empty[st], ((seq / NS) - 1) & 1);
           info[st] = F32Info{u, ci, ki, (i == 0 ? 1 : 0) | (i == nb - 1 ? 2 : 0), be};
@@ -988,12 +953,9 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
           bulk_g2s(stages + (size_t)st * T::BPB, dv.pool + ((size_t)lbh * dv.C + si) * (size_t)T::BPB, T::BPB, &full[st]);
           if (qbytes) bulk_g2s(qslots + (size_t)(cn % NS) * T::QSLOT, qrow, qbytes, &full[st]);
         }
-        if (nst < 3) advance(nxt, nst);
       }
-      while (nst < 3) advance(nxt, nst);
       ++cn;
-      cur = nxt;
-      cst = nst;
+      c = __shfl_sync(0xffffffffu, c_next, 0);
     }
     if (lane == 0) {  // end of work
       const int st = seq % NS;
@@ -1009,16 +971,11 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
     unsigned qhi[T::TC ? T::KSTEPS : 1][2], qlo[T::TC ? T::KSTEPS : 1][2];  // B fragments (TC)
     const int gid = lane >> 2, tig = lane & 3;
     const int tc_mt = warp % T::MT, tc_kp = warp / T::MT;  // TC: key tile, head-dimension part
-    // the lane's partial O: CUDA-core PV o[head][DPV dims at DPV*lane]; tensor-core PV
-    // o[m-tile][c fragment]: dim = 16 mt + gid (+8 for c2, c3), head = 2 tig (+1 for c1, c3)
-    constexpr int OA = T::TCPV ? T::MTD : GP, OB = T::TCPV ? 4 : DPV;
-    float o[OA][OB];
+    float o[GP][DPV];
 #pragma unroll
-    for (int g = 0; g < OA; ++g)
+    for (int g = 0; g < GP; ++g)
 #pragma unroll
-      for (int x = 0; x < OB; ++x) o[g][x] = 0.0f;
-    auto o_dim = [&](int a, int b) { return T::TCPV ? 16 * a + gid + 8 * (b >> 1) : DPV * lane + b; };
-    auto o_head = [&](int a, int b) { return T::TCPV ? 2 * tig + (b & 1) : a; };
+      for (int x = 0; x < DPV; ++x) o[g][x] = 0.0f;
     int seq = 0, cn = 0;
     for (;; ++seq) {
       const int st = seq % NS;
@@ -1162,46 +1119,11 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
       named_sync(kBarConsumers, NW * 32);
       // ---- PV over this warp's keys, after rescaling its partial to the new running max
 #pragma unroll
-      for (int a = 0; a < OA; ++a)
+      for (int g = 0; g < GP; ++g) {
+        const float sc = g < G ? scl[g] : 0.0f;
 #pragma unroll
-        for (int b = 0; b < OB; ++b) {
-          const int g = o_head(a, b);
-          o[a][b] *= g < G ? scl[g] : 0.0f;
-        }
-      if constexpr (T::TCPV) {
-#pragma unroll
-        for (int kt = warp; kt < T::KT; kt += NW) {
-          const int k0 = 8 * kt;
-          if (k0 >= count) break;  // warp-uniform; keys past count carry p = 0
-          // B = P^T (keys x heads): b0 = P[head gid][key k0 + tig], b1 = key + 4
-          unsigned bhi[2], blo[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const unsigned x = __float_as_uint(P[(k0 + tig + 4 * e) * GP + gid]);
-            bhi[e] = (x + 0x1000u) & 0xffffe000u;
-            blo[e] = __float_as_uint(__uint_as_float(x) - __uint_as_float(bhi[e]));
-          }
-#pragma unroll
-          for (int mt = 0; mt < T::MTD; ++mt) {
-            // A = V^T (dims x keys): a0 = V[k0 + tig][16 mt + gid], a1 = dim + 8, a2 = key + 4, a3 = both
-            unsigned a[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int key = k0 + tig + 4 * (e >> 1), dim = 16 * mt + gid + 8 * (e & 1);
-              a[e] = *reinterpret_cast<const unsigned*>(vb + key * DH * 4 + ((((dim >> 2) ^ (key & 7)) << 4) | ((dim & 3) << 2)));
-            }
-            unsigned ahi[4], alo[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              ahi[e] = (a[e] + 0x1000u) & 0xffffe000u;
-              alo[e] = __float_as_uint(__uint_as_float(a[e]) - __uint_as_float(ahi[e]));
-            }
-            mma_tf32(o[mt], alo, bhi);
-            mma_tf32(o[mt], ahi, blo);
-            mma_tf32(o[mt], ahi, bhi);
-          }
-        }
-      } else {
+        for (int x = 0; x < DPV; ++x) o[g][x] *= sc;
+      }
       constexpr int KPW = (NBK + NW - 1) / NW;  // keys per warp: warp, warp + NW, ...
       // with NW a multiple of 8 every key of this warp has the same swizzle phase (key & 7)
       const char* vrow = vb + warp * DH * 4;
@@ -1230,7 +1152,6 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
             for (int x = 0; x < DPV; ++x) o[g4 + e][x] = fmaf(pp[e], vv[x], o[g4 + e][x]);
         }
       }
-      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
       if (it.flags & 2) {
@@ -1240,27 +1161,26 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
           for (int p0 = 0; p0 < half; p0 += T::CB) {
             const int p1 = min(p0 + T::CB, half);
             if (warp >= half + p0 && warp < half + p1) {
-              float* cw = comb + (size_t)(warp - half - p0) * GP * T::CLD;
+              float* cw = comb + (size_t)(warp - half - p0) * GP * DH;
 #pragma unroll
-              for (int a = 0; a < OA; ++a) {
-                if constexpr (!T::TCPV && DPV == 4)
-                  *reinterpret_cast<float4*>(cw + a * T::CLD + 4 * lane) = make_float4(o[a][0], o[a][1], o[a][2], o[a][3]);
+              for (int g = 0; g < GP; ++g) {
+                if constexpr (DPV == 4)
+                  *reinterpret_cast<float4*>(cw + g * DH + 4 * lane) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
                 else
-#pragma unroll
-                  for (int b = 0; b < OB; ++b) cw[o_head(a, b) * T::CLD + o_dim(a, b)] = o[a][b];
+                  *reinterpret_cast<float2*>(cw + g * DH + 2 * lane) = make_float2(o[g][0], o[g][1]);
               }
             }
             named_sync(kBarConsumers, NW * 32);
             if (warp >= p0 && warp < p1) {
-              const float* cw = comb + (size_t)(warp - p0) * GP * T::CLD;
+              const float* cw = comb + (size_t)(warp - p0) * GP * DH;
 #pragma unroll
-              for (int a = 0; a < OA; ++a) {
-                if constexpr (!T::TCPV && DPV == 4) {
-                  const float4 c4 = *reinterpret_cast<const float4*>(cw + a * T::CLD + 4 * lane);
-                  o[a][0] += c4.x; o[a][1] += c4.y; o[a][2] += c4.z; o[a][3] += c4.w;
+              for (int g = 0; g < GP; ++g) {
+                if constexpr (DPV == 4) {
+                  const float4 c4 = *reinterpret_cast<const float4*>(cw + g * DH + 4 * lane);
+                  o[g][0] += c4.x; o[g][1] += c4.y; o[g][2] += c4.z; o[g][3] += c4.w;
                 } else {
-#pragma unroll
-                  for (int b = 0; b < OB; ++b) o[a][b] += cw[o_head(a, b) * T::CLD + o_dim(a, b)];
+                  const float2 c2 = *reinterpret_cast<const float2*>(cw + g * DH + 2 * lane);
+                  o[g][0] += c2.x; o[g][1] += c2.y;
                 }
               }
             }
@@ -1271,21 +1191,13 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
           const int u = it.bh, rl = layer + u / BHL;
           const size_t pbase = (size_t)(u % BHL) * dv.max_chunks + it.ci;
           float* po = part_o_of(dv, rl);
-          if constexpr (T::TCPV) {
 #pragma unroll
-            for (int a = 0; a < OA; ++a)
-#pragma unroll
-              for (int b = 0; b < OB; ++b)
-                if (o_head(a, b) < G) po[(pbase * G + o_head(a, b)) * DH + o_dim(a, b)] = o[a][b];
-          } else {
-#pragma unroll
-            for (int g = 0; g < GP; ++g) {
-              if (g >= G) break;
-              if constexpr (DPV == 4)
-                *reinterpret_cast<float4*>(po + (pbase * G + g) * DH + 4 * lane) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
-              else
-                *reinterpret_cast<float2*>(po + (pbase * G + g) * DH + 2 * lane) = make_float2(o[g][0], o[g][1]);
-            }
+          for (int g = 0; g < GP; ++g) {
+            if (g >= G) break;
+            if constexpr (DPV == 4)
+              *reinterpret_cast<float4*>(po + (pbase * G + g) * DH + 4 * lane) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+            else
+              *reinterpret_cast<float2*>(po + (pbase * G + g) * DH + 2 * lane) = make_float2(o[g][0], o[g][1]);
           }
           if (lane < G) {
             part_ml_of(dv, rl)[pbase * G + lane] = make_float2(run_m[lane], run_l[lane]);
@@ -1294,9 +1206,9 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
           }
         }
 #pragma unroll
-        for (int a = 0; a < OA; ++a)
+        for (int g = 0; g < GP; ++g)
 #pragma unroll
-          for (int b = 0; b < OB; ++b) o[a][b] = 0.0f;
+          for (int x = 0; x < DPV; ++x) o[g][x] = 0.0f;
         ++cn;
       }
     }
