@@ -778,20 +778,22 @@ __global__ void __launch_bounds__(32)
   }
 }
 
-// ---------------------------------------------------------------- fp32 CUDA-core kernel, warp group
+// ---------------------------------------------------------------- fp32 kernel, warp group
 // fp32 storage (tolerance 1e-5): one persistent CTA per SM, the same chunk decomposition and
 // (m, l, O) records as the bf16 kernel, so the finalize merge is shared.
 //   copy warp      claims chunks, loads their metadata lane-parallel (required block, slot, bias,
 //                  live tokens), and streams each K|V block (2 n_b d_head fp32) HBM -> shared
 //                  memory with one 1-D bulk copy into a ring of NS stages; a chunk's query rows
 //                  ride on its first block's barrier.
-//   NW consumer    warps share every block.  QK: a key's dot products are split over LPK lanes
-//   warps          (DPL dims each, the group's queries in registers), then reduced with a
-//                  reduce-scatter butterfly (GP values over LPK lanes: one lane per query head
-//                  ends with its sum).  Online softmax: one warp per query head, accurate expf.
-//                  PV: each warp owns NBK/NW keys and DH/32 dims per lane for every query head;
-//                  per-warp partials are rescaled per block and summed over the warps in a fixed
-//                  tree at the chunk end (deterministic).  fp32 FMA throughout.
+//   NW consumer    warps share every block.  QK for a group of 5..8 heads (TC): on the tensor
+//   warps          cores in 3xTF32 (mma.m16n8k8: keys on M, heads on N; K tiles by ldmatrix from
+//                  the swizzled stage; a = a_hi + a_lo, D += a_lo b_hi + a_hi b_lo + a_hi b_hi).
+//                  Other group sizes: a key's dot products split over LPK lanes (DPL dims each,
+//                  the queries in registers), reduced by a reduce-scatter butterfly (one lane per
+//                  head ends with its sum).  Online softmax: one warp per head, accurate expf.
+//                  PV in fp32 FMA: each warp owns NBK/NW keys and DH/32 dims per lane for every
+//                  head; per-warp partials are rescaled per block and summed over the warps in a
+//                  fixed tree at the chunk end (deterministic).
 __device__ __forceinline__ unsigned f32_to_tf32(float x) {
   unsigned r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
