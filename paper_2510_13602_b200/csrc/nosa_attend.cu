@@ -1014,7 +1014,9 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
       if constexpr (T::TC) {
         // ---- QK on the tensor cores: this warp's 16-key tile x the group's 8 heads over its
         //      k-steps; a = a_hi + a_lo in tf32 for K and q, D += a_lo b_hi + a_hi b_lo + a_hi b_hi
-        float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        // four independent accumulators (k-step parity x {cross terms, hi.hi}) keep the MMA
+        // dependency chains short; summed in a fixed order after the k loop
+        float c4[4][4] = {};
         const int mi = lane >> 3, r = lane & 7;
         const int key_a = tc_mt * 16 + r + (mi & 1) * 8;
         const unsigned rowb = smem_u32(kb) + key_a * DH * 4;
@@ -1031,10 +1033,13 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
             ahi[e] = (a[e] + 0x1000u) & 0xffffe000u;
             alo[e] = __float_as_uint(__uint_as_float(a[e]) - __uint_as_float(ahi[e]));
           }
-          mma_tf32(c, alo, qhi[k]);
-          mma_tf32(c, ahi, qlo[k]);
-          mma_tf32(c, ahi, qhi[k]);
+          mma_tf32(c4[2 * (k & 1)], alo, qhi[k]);
+          mma_tf32(c4[2 * (k & 1)], ahi, qlo[k]);
+          mma_tf32(c4[2 * (k & 1) + 1], ahi, qhi[k]);
         }
+        float c[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c[e] = (c4[0][e] + c4[2][e]) + (c4[1][e] + c4[3][e]);
         float* Sp = S + (size_t)tc_kp * (NBK * GP + GP);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
