@@ -794,6 +794,11 @@ __global__ void __launch_bounds__(32)
 //                  PV in fp32 FMA: each warp owns NBK/NW keys and DH/32 dims per lane for every
 //                  head; per-warp partials are rescaled per block and summed over the warps in a
 //                  fixed tree at the chunk end (deterministic).
+__device__ __forceinline__ int float_to_ordered(float f) {  // signed-int order == float order
+  const int b = __float_as_int(f);
+  return b ^ ((b >> 31) & 0x7fffffff);
+}
+__device__ __forceinline__ float ordered_to_float(int k) { return __int_as_float(k ^ ((k >> 31) & 0x7fffffff)); }
 __device__ __forceinline__ unsigned f32_to_tf32(float x) {
   unsigned r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -1102,8 +1107,8 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
           sv[r] = key < count ? x + it.beta : -INFINITY;
           mx = fmaxf(mx, sv[r]);
         }
-#pragma unroll
-        for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        // warp max in one REDUX on the order-preserving integer image of the float
+        mx = ordered_to_float(__reduce_max_sync(0xffffffffu, float_to_ordered(mx)));
         const float m_old = run_m[g];
         const float mn = fmaxf(m_old, mx);
         float sum = 0.0f;
