@@ -983,6 +983,13 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
     for (int g = 0; g < GP; ++g)
 #pragma unroll
       for (int x = 0; x < DPV; ++x) o[g][x] = 0.0f;
+    constexpr int NHW = (GP + NW - 1) / NW;  // query heads per softmax warp
+    float mreg[NHW], lpart[NHW];
+#pragma unroll
+    for (int j = 0; j < NHW; ++j) {
+      mreg[j] = -INFINITY;
+      lpart[j] = 0.0f;
+    }
     int seq = 0, cn = 0;
     for (;; ++seq) {
       const int st = seq % NS;
@@ -1094,8 +1101,12 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
       }
       }
       named_sync(kBarConsumers, NW * 32);
-      // ---- online softmax, one warp per query head
-      for (int g = warp; g < G; g += NW) {
+      // ---- online softmax, one warp per query head: the running max in a register, the running
+      //      sum as per-lane partials (reduced across the lanes once, at the chunk end)
+#pragma unroll
+      for (int j = 0; j < NHW; ++j) {
+        const int g = warp + NW * j;
+        if (g >= G) break;
         float sv[(NBK + 31) / 32];
         float mx = -INFINITY;
 #pragma unroll
@@ -1109,8 +1120,9 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
         }
         // warp max in one REDUX on the order-preserving integer image of the float
         mx = ordered_to_float(__reduce_max_sync(0xffffffffu, float_to_ordered(mx)));
-        const float m_old = run_m[g];
+        const float m_old = mreg[j];
         const float mn = fmaxf(m_old, mx);
+        const float sc = expf(m_old - mn);
         float sum = 0.0f;
 #pragma unroll
         for (int r = 0; r < (NBK + 31) / 32; ++r) {
@@ -1119,14 +1131,9 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
           if (key < NBK) P[key * GP + g] = pr;
           sum += key < NBK ? pr : 0.0f;
         }
-#pragma unroll
-        for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-        if (lane == 0) {
-          const float sc = expf(m_old - mn);
-          scl[g] = sc;
-          run_l[g] = run_l[g] * sc + sum;
-          run_m[g] = mn;
-        }
+        lpart[j] = lpart[j] * sc + sum;
+        mreg[j] = mn;
+        if (lane == 0) scl[g] = sc;
       }
       named_sync(kBarConsumers, NW * 32);
       // ---- PV over this warp's keys, after rescaling its partial to the new running max
@@ -1167,8 +1174,24 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
       if (it.flags & 2) {
-        // ---- chunk end: sum the warps' partials in a fixed tree (warp w += warp w + half, CB
-        //      pairs at a time through the partial buffers), warp 0 writes the record
+        // ---- chunk end: each softmax warp publishes its heads' (m, l), l summed over the lanes
+        //      in a fixed butterfly; then the warps' partial O are summed in a fixed tree (warp w
+        //      += warp w + half, CB pairs at a time through the partial buffers), and warp 0 writes
+        //      the record (the tree's barriers order the (m, l) stores before its reads)
+#pragma unroll
+        for (int j = 0; j < NHW; ++j) {
+          const int g = warp + NW * j;
+          if (g >= G) break;
+          float l = lpart[j];
+#pragma unroll
+          for (int off = 16; off; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+          if (lane == 0) {
+            run_m[g] = mreg[j];
+            run_l[g] = l;
+          }
+          mreg[j] = -INFINITY;
+          lpart[j] = 0.0f;
+        }
         for (int half = NW / 2; half >= 1; half >>= 1) {
           for (int p0 = 0; p0 < half; p0 += T::CB) {
             const int p1 = min(p0 + T::CB, half);
@@ -1211,11 +1234,7 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
             else
               *reinterpret_cast<float2*>(po + (pbase * G + g) * DH + 2 * lane) = make_float2(o[g][0], o[g][1]);
           }
-          if (lane < G) {
-            part_ml_of(dv, rl)[pbase * G + lane] = make_float2(run_m[lane], run_l[lane]);
-            run_m[lane] = -INFINITY;  // the next chunk's state (read after the next QK barrier)
-            run_l[lane] = 0.0f;
-          }
+          if (lane < G) part_ml_of(dv, rl)[pbase * G + lane] = make_float2(run_m[lane], run_l[lane]);
         }
 #pragma unroll
         for (int g = 0; g < GP; ++g)
