@@ -836,9 +836,8 @@ struct F32W {
   static constexpr int KS = TC ? (MT >= NW ? 1 : NW / MT) : 1;
   static constexpr int KSTEPS = DH / 8 / KS;       // k-steps of 8 dims per warp
   static constexpr int SPB = KS;                    // partial logit buffers
-  static constexpr int SDB = TC ? 2 : 1;            // logit buffer sets (TC: double-buffered by block)
-  static constexpr int FIXED = NBK * GP * 4 + SDB * SPB * (NBK * GP + GP) * 4 + CB * GP * DH * 4 + 3 * GP * 4 +
-                               16 + 32 * 4 + 128;
+  static constexpr int FIXED = NBK * GP * 4 + SPB * (NBK * GP + GP) * 4 + CB * GP * DH * 4 + 3 * GP * 4 + 16 +
+                               32 * 4 + 128;
   static constexpr int PER_STAGE = BPB + QSLOT + 16 + 20;
   // stages: as many as fit 227 KiB with 4 KiB left for the unit table, 2 to 4
   static constexpr int NS_FIT = (232448 - 4096 - FIXED) / PER_STAGE;
@@ -888,7 +887,7 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
   char* p = smem_raw;
   char* stages = p;                                  p += (size_t)NS * T::BPB;
   char* qslots = p;                                  p += (size_t)NS * T::QSLOT;
-  float* S0 = reinterpret_cast<float*>(p);           p += T::SDB * T::SPB * (NBK * GP + GP) * 4;  // [SDB][SPB][GP][NBK + 1]
+  float* S = reinterpret_cast<float*>(p);            p += T::SPB * (NBK * GP + GP) * 4;  // [SPB][GP][NBK + 1] logits
   float* P = reinterpret_cast<float*>(p);            p += NBK * GP * 4;   // [NBK][GP] probabilities
   float* comb = reinterpret_cast<float*>(p);         p += T::CB * GP * DH * 4;
   float* run_m = reinterpret_cast<float*>(p);        p += GP * 4;
@@ -986,12 +985,6 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
       for (int x = 0; x < DPV; ++x) o[g][x] = 0.0f;
     constexpr int NHW = (GP + NW - 1) / NW;  // query heads per softmax warp
     float mreg[NHW], lpart[NHW];
-    // TC: every warp tracks the running max of every head (identical across warps) and a lane
-    // partial of the row sum over its own PV keys (head lane & 7)
-    float mall[T::TC ? GP : 1];
-    float lown = 0.0f;
-#pragma unroll
-    for (int g = 0; g < (T::TC ? GP : 1); ++g) mall[g] = -INFINITY;
 #pragma unroll
     for (int j = 0; j < NHW; ++j) {
       mreg[j] = -INFINITY;
@@ -1030,7 +1023,6 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
         }
       }
       const int count = it.count;
-      float* S = S0 + (size_t)(T::SDB == 2 ? (seq & 1) : 0) * T::SPB * (NBK * GP + GP);
       if constexpr (T::TC) {
         // ---- QK on the tensor cores: this warp's 16-key tile x the group's 8 heads over its
         //      k-steps; a = a_hi + a_lo in tf32 for K and q, D += a_lo b_hi + a_hi b_lo + a_hi b_hi
@@ -1109,59 +1101,6 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
       }
       }
       named_sync(kBarConsumers, NW * 32);
-      if constexpr (T::TC) {
-        // ---- online softmax without a second barrier: every warp forms the new running max of
-        //      every head (one REDUX each over the block's logits), then the probabilities of its
-        //      own PV keys only, which it alone reads (the logits are double-buffered by block)
-        float scv[GP];
-#pragma unroll
-        for (int g = 0; g < GP; ++g) {
-          scv[g] = 0.0f;
-          if (g >= G) continue;
-          float mx = -INFINITY;
-#pragma unroll
-          for (int r = 0; r < (NBK + 31) / 32; ++r) {
-            const int key = lane + 32 * r;
-            float x = 0.0f;
-#pragma unroll
-            for (int pp = 0; pp < T::SPB; ++pp) x += key < NBK ? S[pp * (NBK * GP + GP) + g * T::SLD + key] : 0.0f;
-            mx = fmaxf(mx, key < count ? x + it.beta : -INFINITY);
-          }
-          mx = ordered_to_float(__reduce_max_sync(0xffffffffu, float_to_ordered(mx)));
-          const float mn = fmaxf(mall[g], mx);
-          scv[g] = mn == mall[g] ? 1.0f : expf(mall[g] - mn);
-          mall[g] = mn;
-        }
-        const int hl = lane & 7, ks = lane >> 3;
-        float mh = -INFINITY, sch = 0.0f;
-#pragma unroll
-        for (int g = 0; g < GP; ++g)
-          if (hl == g) {
-            mh = mall[g];
-            sch = scv[g];
-          }
-        constexpr int KO = (NBK + NW - 1) / NW;  // own keys: warp + NW j
-        float psum = 0.0f;
-#pragma unroll
-        for (int i = 0; i < (KO + 3) / 4; ++i) {
-          const int jj = ks + 4 * i;
-          const int key = warp + NW * jj;
-          if (jj < KO && key < NBK) {
-            float x = 0.0f;
-#pragma unroll
-            for (int pp = 0; pp < T::SPB; ++pp) x += S[pp * (NBK * GP + GP) + hl * T::SLD + key];
-            const float pr = (hl < G && key < count) ? expf(x + it.beta - mh) : 0.0f;
-            P[key * GP + hl] = pr;
-            psum += pr;
-          }
-        }
-        lown = lown * sch + psum;
-        __syncwarp();
-#pragma unroll
-        for (int g = 0; g < GP; ++g)
-#pragma unroll
-          for (int x = 0; x < DPV; ++x) o[g][x] *= scv[g];
-      } else {
       // ---- online softmax, one warp per query head: the running max in a register, the running
       //      sum as per-lane partials (reduced across the lanes once, at the chunk end)
 #pragma unroll
@@ -1204,7 +1143,6 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
 #pragma unroll
         for (int x = 0; x < DPV; ++x) o[g][x] *= sc;
       }
-      }
       constexpr int KPW = (NBK + NW - 1) / NW;  // keys per warp: warp, warp + NW, ...
       // with NW a multiple of 8 every key of this warp has the same swizzle phase (key & 7)
       const char* vrow = vb + warp * DH * 4;
@@ -1240,17 +1178,8 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
         //      in a fixed butterfly; then the warps' partial O are summed in a fixed tree (warp w
         //      += warp w + half, CB pairs at a time through the partial buffers), and warp 0 writes
         //      the record (the tree's barriers order the (m, l) stores before its reads)
-        if constexpr (T::TC) {
-          // lane partials of each head summed within the warp (lanes hl, hl + 8, + 16, + 24),
-          // then one value per (warp, head) into the free probability buffer for warp 0
-          lown += __shfl_xor_sync(0xffffffffu, lown, 8);
-          lown += __shfl_xor_sync(0xffffffffu, lown, 16);
-          named_sync(kBarConsumers, NW * 32);  // every warp is past its PV reads of P
-          if (lane < 8) P[warp * GP + lane] = lown;
-          lown = 0.0f;
-        }
 #pragma unroll
-        for (int j = 0; j < (T::TC ? 0 : NHW); ++j) {
+        for (int j = 0; j < NHW; ++j) {
           const int g = warp + NW * j;
           if (g >= G) break;
           float l = lpart[j];
@@ -1305,24 +1234,12 @@ __global__ void __launch_bounds__(F32W<NBK, DH, GP, NW_>::THREADS, 1)
             else
               *reinterpret_cast<float2*>(po + (pbase * G + g) * DH + 2 * lane) = make_float2(o[g][0], o[g][1]);
           }
-          if constexpr (T::TC) {
-            float m = -INFINITY, l = 0.0f;
-#pragma unroll
-            for (int g = 0; g < GP; ++g)
-              if (lane == g) m = mall[g];
-#pragma unroll
-            for (int w = 0; w < NW; ++w) l += lane < GP ? P[w * GP + lane] : 0.0f;
-            if (lane < G) part_ml_of(dv, rl)[pbase * G + lane] = make_float2(m, l);
-          } else {
-            if (lane < G) part_ml_of(dv, rl)[pbase * G + lane] = make_float2(run_m[lane], run_l[lane]);
-          }
+          if (lane < G) part_ml_of(dv, rl)[pbase * G + lane] = make_float2(run_m[lane], run_l[lane]);
         }
 #pragma unroll
         for (int g = 0; g < GP; ++g)
 #pragma unroll
           for (int x = 0; x < DPV; ++x) o[g][x] = 0.0f;
-#pragma unroll
-        for (int g = 0; g < (T::TC ? GP : 1); ++g) mall[g] = -INFINITY;
         ++cn;
       }
     }
