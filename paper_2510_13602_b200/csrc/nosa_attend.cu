@@ -466,15 +466,12 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
       const unsigned kbase = smem_u32(stages + (size_t)s * T::BPB);
       const unsigned vbase = kbase + T::PLANE;
       const int key0 = w * T::KPW;
-      // ---- S^T = K Q^T : keys on M (16 per m-tile), queries on N; even and odd k-steps
-      //      accumulate separately (two short MMA dependency chains), summed once
-      float sc[T::MTK][NQT][4], sc2[T::MTK][NQT][4];
+      // ---- S^T = K Q^T : keys on M (16 per m-tile), queries on N
+      float sc[T::MTK][NQT][4];
 #pragma unroll
       for (int mk = 0; mk < T::MTK; ++mk)
 #pragma unroll
-        for (int nq = 0; nq < NQT; ++nq)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) sc[mk][nq][e] = sc2[mk][nq][e] = 0.0f;
+        for (int nq = 0; nq < NQT; ++nq) sc[mk][nq][0] = sc[mk][nq][1] = sc[mk][nq][2] = sc[mk][nq][3] = 0.0f;
 #pragma unroll
       for (int ks = 0; ks < T::KS; ++ks) {
 #pragma unroll
@@ -485,16 +482,9 @@ __global__ void __launch_bounds__(BF<NBK, DH, NQT>::THREADS, 1)
           unsigned a0, a1, a2, a3;
           ldsm_x4(kbase + key * (DH * 2) + ((chunk ^ (key & 7)) << 4), a0, a1, a2, a3);
 #pragma unroll
-          for (int nq = 0; nq < NQT; ++nq)
-            mma_bf16((ks & 1) ? sc2[mk][nq] : sc[mk][nq], a0, a1, a2, a3, qb[ks][nq][0], qb[ks][nq][1]);
+          for (int nq = 0; nq < NQT; ++nq) mma_bf16(sc[mk][nq], a0, a1, a2, a3, qb[ks][nq][0], qb[ks][nq][1]);
         }
       }
-#pragma unroll
-      for (int mk = 0; mk < T::MTK; ++mk)
-#pragma unroll
-        for (int nq = 0; nq < NQT; ++nq)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) sc[mk][nq][e] += sc2[mk][nq][e];
       // ---- online softmax over this warp's keys, per query column
       const float beta = it.beta;
       const int count = it.count;
