@@ -449,6 +449,9 @@ extern "C" int nosa_ctx_create(const NosaConfig* cfg, int device, NosaCtx** out)
   dv.screen = (c.exact_scan == 0 && (c.d_head == 128 || c.d_head == 64) && !getenv("NOSA_EXACT_SCAN")) ? 1 : 0;
   dv.elem = c.dtype == NOSA_DTYPE_BF16 ? 2 : 4;
   dv.bpb = 2LL * c.n_b * c.d_head * dv.elem;
+  // blocks over 32 KiB (fp32 storage): 12 gather CTAs with two blocks each in flight
+  // (cfg 3 fp32: 48.2 GB/s vs 39.8 with 8 CTAs of one block; tools/r2bb.sh)
+  if (dv.bpb > 32768 && !getenv("NOSA_GATHER_CTAS")) ctx->gather_grid = 12;
   // split-K chunk: the largest of 8, 4, 2, 1 blocks that still gives every SM two work
   // items per layer (measured: smaller chunks cost more in per-chunk overhead than they win in
   // balance once there are a few waves) (B*H*|R| blocks, |R| ~ fixed + top-k), so a small batch does not leave

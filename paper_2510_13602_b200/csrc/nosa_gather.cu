@@ -185,10 +185,13 @@ cudaError_t launch_gather(const Dev& dv, int layer, cudaStream_t st, int grid, b
     max_shared_carveout(gather_tma_kernel);
     gather_tma_kernel<<<g, 32, smem, st>>>(dv, layer, nl);
   } else {
-    // NOSA_GATHER_VARIANT: bit 0 = two blocks per CTA iteration, bit 1 = L2::256B.  Default 2:
-    // the 256-byte L2 fetch hint (cfg 3, two alternations: 14.13K vs 13.97K tok/s, attention next
-    // to the gather 0.83 vs 0.77 of HBM; tools/r2u.sh)
-    static const int variant = getenv("NOSA_GATHER_VARIANT") ? atoi(getenv("NOSA_GATHER_VARIANT")) : 2;
+    // NOSA_GATHER_VARIANT: bit 0 = two blocks per CTA iteration, bit 1 = L2::256B.  Default 2
+    // for 32 KiB blocks: the 256-byte L2 fetch hint (cfg 3, two alternations: 14.13K vs 13.97K
+    // tok/s, attention next to the gather 0.83 vs 0.77 of HBM; tools/r2u.sh).  Default 3 for
+    // larger (fp32) blocks, which take two 32 KiB passes each: two blocks per iteration keep
+    // 64 KiB per CTA in flight (cfg 3 fp32 with 12 CTAs: 6.36K vs 5.13K tok/s; tools/r2bb.sh)
+    static const int env_variant = getenv("NOSA_GATHER_VARIANT") ? atoi(getenv("NOSA_GATHER_VARIANT")) : -1;
+    const int variant = env_variant >= 0 ? env_variant : (dv.bpb > 32768 ? 3 : 2);
     max_shared_carveout(gather_kernel<1, false>);
     max_shared_carveout(gather_kernel<2, false>);
     max_shared_carveout(gather_kernel<1, true>);
