@@ -634,3 +634,16 @@ def test_fp32_attention_bitwise_independent_of_launch_grouping():
         eng.close()
     for r in results[1:]:
         np.testing.assert_array_equal(r, results[0])
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("n_head,d_head", [(12, 128), (10, 64), (32, 64)])
+def test_padded_and_wide_query_groups(dtype, n_head, d_head):
+    """Query groups the kernels pad (G = 6 and 5 of 8 columns: the fp32 tensor-core QK with zero
+    query rows) or split (G = 16: the fp32 CUDA-core reduce-scatter, two bf16 N tiles) against
+    the oracle at each dtype's tolerance."""
+    cfg = AttentionConfig(n=8192, d=n_head * d_head, n_head=n_head, n_kv_head=2, d_head=d_head, n_b=64, n_s=64,
+                          n_w=1024, k=4096, k_q=1024, k_e=3072)
+    a = _run_pair(cfg, batch=2, t0s=[2600, 2400], steps=6, fast_slots=40, seed=23, rho=0.2, layers=2,
+                  dtype=dtype)
+    assert a <= TOL[dtype]
