@@ -644,6 +644,6 @@ def test_padded_and_wide_query_groups(dtype, n_head, d_head):
     the oracle at each dtype's tolerance."""
     cfg = AttentionConfig(n=8192, d=n_head * d_head, n_head=n_head, n_kv_head=2, d_head=d_head, n_b=64, n_s=64,
                           n_w=1024, k=4096, k_q=1024, k_e=3072)
-    a = _run_pair(cfg, batch=2, t0s=[2600, 2400], steps=6, fast_slots=40, seed=23, rho=0.2, layers=2,
+    a = _run_pair(cfg, batch=2, t0s=[2600, 2400], steps=6, fast_slots=48, seed=23, rho=0.2, layers=2,
                   dtype=dtype)
     assert a <= TOL[dtype]
